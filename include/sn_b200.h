@@ -1,0 +1,154 @@
+/*
+ * sn_b200.h -- C ABI of the B200-native stereonorm hot path.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types in signatures); a
+ * stream is passed as `void*` (a cudaStream_t / CUstream handle, NULL =
+ * legacy default stream).  Device entry points are asynchronous on that
+ * stream and never synchronise the host; *_host entry points take host
+ * buffers and return when the result is in host memory.
+ *
+ * Every entry point returns one of the SN_* codes below; on failure
+ * sn_last_error() (thread-local) describes it.  Python maps the codes to
+ * ValueError / DegenerateSupportError / RuntimeError exactly as the
+ * reference raises them.
+ *
+ * Reference interfaces replaced (paths relative to pkg/src/stereonorm):
+ *   sn_oriented_points[_f64]  estimate_normals_fixed   kernels.py:237-261
+ *                             + triangulate_grid        geometry.py:85-89
+ *                             dense record of the CLI's PLY path cli.py:118-123
+ *   sn_affine[_f64]           convolve_affine           kernels.py:182-203
+ *   sn_passable               depth_field + depth_laplacian + ST test
+ *                             geometry.py:169-172, adaptive.py:80-97,130-132
+ *   sn_ccl_labels             (new) 8-connected labels of
+ *                             the ST-passable set, canonical min raster index
+ *   sn_kernel_moments         build_kernels             kernels.py:78-103
+ *
+ * Layouts: disparity [B][H][W] row-major (fp32 or fp64, NaN/+-inf = invalid),
+ * out6 [B][H][W][6] fp32 = (x, y, z, nx, ny, nz) -- the PLY vertex record
+ * (formats.py:167-183) -- with NaN normals where the normal is invalid and
+ * NaN points where the disparity is not finite and > 0; mask [B][H][W]
+ * uint8 (1 = valid normal), optional (NULL).  Offsets are (vx, vy) int32
+ * pairs, exactly KernelSpec.offsets (kernels.py:31-55).
+ */
+#ifndef SN_B200_H
+#define SN_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SN_API __attribute__((visibility("default")))
+#else
+#define SN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SN_OK 0
+#define SN_EINVAL 1      /* invalid argument            -> ValueError             */
+#define SN_EDEGENERATE 2 /* collinear offset pattern    -> DegenerateSupportError */
+#define SN_ECUDA 3       /* CUDA / driver failure       -> RuntimeError           */
+
+#define SN_ABI_VERSION 1
+
+typedef struct sn_rig {
+  double fx, fy, u0, v0, baseline; /* geometry.py:22-36 (StereoRig) */
+} sn_rig_t;
+
+/* Integer moments of an offset pattern (kernels.py:87-103). */
+typedef struct sn_moments {
+  int64_t alpha, beta, gamma, det, sx, sy;
+  int32_t hx, hy;       /* half extents of the support box               */
+  int32_t square_r;     /* R if the pattern is the centred (2R+1)^2 square, else -1 */
+} sn_moments_t;
+
+typedef struct sn_plan sn_plan_t;
+
+SN_API int sn_abi_version(void);
+SN_API const char* sn_last_error(void);
+
+/* A plan binds a device and owns the host-path workspace (pinned staging,
+ * device buffers, copy/compute streams).  Device entry points only use it
+ * for the device id and cached properties and are safe to call concurrently
+ * on distinct streams. */
+SN_API int sn_plan_create(int device, sn_plan_t** plan);
+SN_API int sn_plan_destroy(sn_plan_t* plan);
+
+/* kernels.py:78-103: validates the pattern (N>0, distinct) and returns its
+ * integer moments; SN_EDEGENERATE when det <= 0.5. */
+SN_API int sn_kernel_moments(const int32_t* offsets_xy, int32_t n_off, sn_moments_t* out);
+
+/* Fused fixed-kernel pass: LSQ affine fit + closed-form normal + triangulated
+ * point, dense AoS-6 output.  Device pointers. */
+SN_API int sn_oriented_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                       const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
+                       float* out6, uint8_t* mask, void* stream);
+SN_API int sn_oriented_points_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                           int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
+                           int32_t n_off, float* out6, uint8_t* mask, void* stream);
+
+/* Same pass, host buffers: pinned staging + overlapped H2D / compute / D2H,
+ * returns when out6 (and mask, if non-NULL) hold the result. */
+SN_API int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
+                            int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
+                            int32_t n_off, float* out6_host, uint8_t* mask_host);
+
+/* convolve_affine (gradient convention a1 - 1 = dd/du, a2 = dd/dv); a1/a2 are
+ * NaN where mask is 0.  Device pointers, fp64 outputs. */
+SN_API int sn_affine(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+              const int32_t* offsets_xy, int32_t n_off, double* a1, double* a2,
+              uint8_t* mask, void* stream);
+SN_API int sn_affine_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                  const int32_t* offsets_xy, int32_t n_off, double* a1, double* a2,
+                  uint8_t* mask, void* stream);
+
+/* ST-passable set: edge value valid and <= t (bit-exact fp64 predicate).
+ * edges (optional, NULL to skip) receives the depth-Laplacian values, NaN
+ * where invalid. */
+SN_API int sn_passable(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                const sn_rig_t* rig, double t, uint8_t* passable, double* edges,
+                void* stream);
+
+/* 8-connected component labels of the passable set; label = smallest raster
+ * index v*W + u + index_base in the component (per frame), -1 elsewhere.
+ * row_base lets a strip of a larger frame use global raster indices
+ * (index_base = row_base * W).  Device pointers. */
+SN_API int sn_ccl_labels(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                  const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                  void* stream);
+
+/* Label an already-computed passable grid (uint8) -- used by strip mode and
+ * by tests of the labeller alone. */
+SN_API int sn_ccl_from_passable(sn_plan_t* plan, const uint8_t* passable, int64_t B, int64_t H,
+                         int64_t W, int64_t row_base, int32_t* labels, void* stream);
+
+/* Strip-seam merge.  HOST memory: `seams` holds, for each
+ * of the n_strips strips in row order, its first and last owned label rows
+ * ([n_strips][2][W] int32, global raster indices, -1 = not passable), as
+ * gathered from all ranks.  8-adjacent passable pixels across each seam are
+ * united with min-root links; writes the (label -> root) pairs of every label
+ * that changes, sorted by label, to map_keys/map_vals (capacity
+ * 2*n_strips*W) and their count to *n_map.  Deterministic and identical on
+ * every rank. */
+SN_API int sn_seam_merge_host(const int32_t* seams, int32_t n_strips, int64_t W, int32_t* map_keys,
+                       int32_t* map_vals, int32_t* n_map);
+
+/* Apply a (label -> root) map to a strip's label grid in place (device).
+ * Labels of the strip are global raster indices in [index_base,
+ * index_base + n); scratch is an int32 device buffer of n elements. */
+SN_API int sn_relabel(sn_plan_t* plan, int32_t* labels, int64_t n, int64_t index_base,
+               const int32_t* map_keys, const int32_t* map_vals, const int32_t* n_map,
+               int32_t map_capacity, int32_t* scratch, void* stream);
+
+/* Test hook: the fixed pass forced onto the generic (non-TMA) kernel, used to
+ * cross-check the TMA fast path on identical inputs. */
+SN_API int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
+                               int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
+                               int32_t n_off, float* out6, uint8_t* mask, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SN_B200_H */

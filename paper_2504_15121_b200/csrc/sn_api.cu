@@ -1,0 +1,536 @@
+// C ABI (include/sn_b200.h): argument validation, kernel-pattern moments,
+// rig pre-combination, dispatch, the host-buffer pipeline and the strip
+// seam merge.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <numeric>
+#include <unordered_map>
+#include <vector>
+
+#include "sn_b200.h"
+#include "sn_internal.h"
+
+namespace sn {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int set_cuda_error(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  return set_error(SN_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SN_ECUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return SN_OK;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+int encode_tiled(CUtensorMap* map, CUtensorMapDataType dt, int rank, void* gaddr,
+                 const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                 const cuuint32_t* elem_strides, CUtensorMapSwizzle swizzle,
+                 CUtensorMapFloatOOBfill oob) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return set_error(SN_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const CUresult r = fn(map, dt, (cuuint32_t)rank, gaddr, dims, strides, box, elem_strides,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        oob);
+  if (r != CUDA_SUCCESS) return set_error(SN_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SN_OK;
+}
+
+}  // namespace sn
+
+using namespace sn;
+
+// ---------------------------------------------------------------------------
+// plan
+
+struct sn_plan {
+  int device;
+  int num_sms;
+  // host-path workspace
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr},
+              ev_out[2] = {nullptr, nullptr};
+  float* d_in[2] = {nullptr, nullptr};
+  float* d_out[2] = {nullptr, nullptr};
+  uint8_t* d_mask[2] = {nullptr, nullptr};
+  size_t cap_px = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int check_shape(int64_t B, int64_t H, int64_t W) {
+  if (B < 0 || H < 0 || W < 0) return set_error(SN_EINVAL, "negative shape (%lld, %lld, %lld)",
+                                               (long long)B, (long long)H, (long long)W);
+  if (H > 0x7fffffffLL || W > 0x7fffffffLL || B > 0x7fffffffLL)
+    return set_error(SN_EINVAL, "dimension exceeds int32 range");
+  return SN_OK;
+}
+
+int check_rig(const sn_rig_t* rig) {
+  if (!rig) return set_error(SN_EINVAL, "rig is NULL");
+  // geometry.py:32-36
+  if (!(rig->fx > 0.0 && rig->fy > 0.0)) return set_error(SN_EINVAL, "focal lengths must be positive");
+  if (!(rig->baseline > 0.0)) return set_error(SN_EINVAL, "baseline must be positive");
+  if (!isfinite(rig->u0) || !isfinite(rig->v0) || !isfinite(rig->fx) || !isfinite(rig->fy) ||
+      !isfinite(rig->baseline))
+    return set_error(SN_EINVAL, "rig parameters must be finite");
+  return SN_OK;
+}
+
+void fill_rig(FixedParams& p, const sn_rig_t* rig) {
+  p.fx = rig->fx;
+  p.fy = rig->fy;
+  p.u0 = rig->u0;
+  p.v0 = rig->v0;
+  p.fxb = rig->fx * rig->baseline;  // geometry.py:43 evaluates fx * b first
+  p.fxb_f = (float)p.fxb;
+  p.inv_fx_f = (float)(1.0 / rig->fx);
+  p.inv_fy_f = (float)(1.0 / rig->fy);
+  p.u0_hi = (float)rig->u0;
+  p.u0_lo = (float)(rig->u0 - (double)p.u0_hi);
+  p.v0_hi = (float)rig->v0;
+  p.v0_lo = (float)(rig->v0 - (double)p.v0_hi);
+}
+
+int prepare(const int32_t* offsets_xy, int32_t n_off, sn_moments_t& m, OffsetTable& tab) {
+  int rc = sn_kernel_moments(offsets_xy, n_off, &m);
+  if (rc) return rc;
+  if (n_off > kMaxOffsets)
+    return set_error(SN_EINVAL, "at most %d offsets are supported (got %d)", kMaxOffsets, n_off);
+  tab.n = n_off;
+  for (int i = 0; i < n_off; ++i) tab.v[i] = make_int2(offsets_xy[2 * i], offsets_xy[2 * i + 1]);
+  return SN_OK;
+}
+
+void fill_moments(FixedParams& p, const sn_moments_t& m) {
+  p.alpha = (double)m.alpha;
+  p.beta = (double)m.beta;
+  p.gamma = (double)m.gamma;
+  p.det = (double)m.det;
+  p.sx = (double)m.sx;
+  p.sy = (double)m.sy;
+  p.R = m.square_r;
+}
+
+LaunchCtx make_ctx(sn_plan_t* plan, void* stream) {
+  LaunchCtx c;
+  c.stream = reinterpret_cast<cudaStream_t>(stream);
+  c.device = plan->device;
+  c.num_sms = plan->num_sms;
+  return c;
+}
+
+template <typename T>
+int oriented_points_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                         const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
+                         float* out6, uint8_t* mask, void* stream, int force_generic) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  sn_moments_t m;
+  static thread_local OffsetTable tab;
+  if ((rc = prepare(offsets_xy, n_off, m, tab))) return rc;
+  if (B * H * W > 0 && (!disp || !out6)) return set_error(SN_EINVAL, "NULL buffer");
+  FixedParams p{};
+  p.B = B;
+  p.H = H;
+  p.W = W;
+  fill_rig(p, rig);
+  fill_moments(p, m);
+  DeviceGuard g(plan->device);
+  return run_fixed<T>(make_ctx(plan, stream), disp, p, m, tab, out6, mask, nullptr, nullptr, false,
+                      force_generic);
+}
+
+template <typename T>
+int affine_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                const int32_t* offsets_xy, int32_t n_off, double* a1, double* a2, uint8_t* mask,
+                void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  sn_moments_t m;
+  static thread_local OffsetTable tab;
+  if ((rc = prepare(offsets_xy, n_off, m, tab))) return rc;
+  if (B * H * W > 0 && (!disp || !a1 || !a2)) return set_error(SN_EINVAL, "NULL buffer");
+  FixedParams p{};
+  p.B = B;
+  p.H = H;
+  p.W = W;
+  fill_moments(p, m);
+  DeviceGuard g(plan->device);
+  return run_fixed<T>(make_ctx(plan, stream), disp, p, m, tab, nullptr, mask, a1, a2, true, 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_abi_version(void) { return SN_ABI_VERSION; }
+
+const char* sn_last_error(void) { return g_err; }
+
+int sn_plan_create(int device, sn_plan_t** plan) {
+  if (!plan) return set_error(SN_EINVAL, "plan out-pointer is NULL");
+  *plan = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return set_error(SN_ECUDA, "no CUDA device available");
+  if (device < 0 || device >= n) return set_error(SN_EINVAL, "device %d out of range [0, %d)", device, n);
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (major != 10)
+    return set_error(SN_ECUDA, "device %d has compute capability %d.x; this build targets sm_100a",
+                     device, major);
+  sn_plan* p = new sn_plan();
+  p->device = device;
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+  *plan = p;
+  return SN_OK;
+}
+
+int sn_plan_destroy(sn_plan_t* plan) {
+  if (!plan) return SN_OK;
+  {
+    DeviceGuard g(plan->device);
+    for (int i = 0; i < 2; ++i) {
+      if (plan->d_in[i]) cudaFree(plan->d_in[i]);
+      if (plan->d_out[i]) cudaFree(plan->d_out[i]);
+      if (plan->d_mask[i]) cudaFree(plan->d_mask[i]);
+      if (plan->ev_in[i]) cudaEventDestroy(plan->ev_in[i]);
+      if (plan->ev_done[i]) cudaEventDestroy(plan->ev_done[i]);
+      if (plan->ev_out[i]) cudaEventDestroy(plan->ev_out[i]);
+    }
+    if (plan->s_h2d) cudaStreamDestroy(plan->s_h2d);
+    if (plan->s_comp) cudaStreamDestroy(plan->s_comp);
+    if (plan->s_d2h) cudaStreamDestroy(plan->s_d2h);
+  }
+  delete plan;
+  return SN_OK;
+}
+
+int sn_kernel_moments(const int32_t* offsets_xy, int32_t n_off, sn_moments_t* out) {
+  if (!out) return set_error(SN_EINVAL, "moments out-pointer is NULL");
+  // kernels.py:38-43
+  if (!offsets_xy || n_off <= 0) return set_error(SN_EINVAL, "offsets must have shape (N, 2)");
+  std::vector<int64_t> keys(n_off);
+  for (int i = 0; i < n_off; ++i)
+    keys[i] = ((int64_t)offsets_xy[2 * i] << 32) ^ (uint32_t)offsets_xy[2 * i + 1];
+  std::sort(keys.begin(), keys.end());
+  if (std::adjacent_find(keys.begin(), keys.end()) != keys.end())
+    return set_error(SN_EINVAL, "offsets must be distinct");
+  sn_moments_t m{};
+  int32_t minx = 0, maxx = 0, miny = 0, maxy = 0;
+  for (int i = 0; i < n_off; ++i) {
+    const int64_t vx = offsets_xy[2 * i], vy = offsets_xy[2 * i + 1];
+    m.alpha += vx * vx;
+    m.beta += vx * vy;
+    m.gamma += vy * vy;
+    m.sx += vx;
+    m.sy += vy;
+    minx = std::min<int32_t>(minx, (int32_t)vx);
+    maxx = std::max<int32_t>(maxx, (int32_t)vx);
+    miny = std::min<int32_t>(miny, (int32_t)vy);
+    maxy = std::max<int32_t>(maxy, (int32_t)vy);
+  }
+  m.det = m.alpha * m.gamma - m.beta * m.beta;
+  m.hx = std::max(maxx, -minx);
+  m.hy = std::max(maxy, -miny);
+  // centred (2R+1)^2 square?
+  m.square_r = -1;
+  if (minx == -maxx && miny == -maxy && maxx == maxy) {
+    const int64_t side = 2 * (int64_t)maxx + 1;
+    if (side * side == n_off) m.square_r = maxx;  // distinct + inside the box => full square
+  }
+  *out = m;
+  // kernels.py:91-93: det is an exact integer, so det <= 0.5 <=> det <= 0
+  if (m.det <= 0) return set_error(SN_EDEGENERATE, "offset pattern is rank deficient (det=%lld)",
+                                   (long long)m.det);
+  return SN_OK;
+}
+
+int sn_oriented_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                       const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, float* out6,
+                       uint8_t* mask, void* stream) {
+  return oriented_points_impl<float>(plan, disp, B, H, W, rig, offsets_xy, n_off, out6, mask,
+                                     stream, 0);
+}
+
+int sn_oriented_points_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                           const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
+                           float* out6, uint8_t* mask, void* stream) {
+  return oriented_points_impl<double>(plan, disp, B, H, W, rig, offsets_xy, n_off, out6, mask,
+                                      stream, 0);
+}
+
+/* test hook: force the generic (non-TMA) kernel, to cross-check the fast path */
+int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                               const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
+                               float* out6, uint8_t* mask, void* stream) {
+  return oriented_points_impl<float>(plan, disp, B, H, W, rig, offsets_xy, n_off, out6, mask,
+                                     stream, 1);
+}
+
+int sn_affine(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+              const int32_t* offsets_xy, int32_t n_off, double* a1, double* a2, uint8_t* mask,
+              void* stream) {
+  return affine_impl<float>(plan, disp, B, H, W, offsets_xy, n_off, a1, a2, mask, stream);
+}
+
+int sn_affine_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                  const int32_t* offsets_xy, int32_t n_off, double* a1, double* a2, uint8_t* mask,
+                  void* stream) {
+  return affine_impl<double>(plan, disp, B, H, W, offsets_xy, n_off, a1, a2, mask, stream);
+}
+
+int sn_passable(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                const sn_rig_t* rig, double t, uint8_t* passable, double* edges, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");  // adaptive.py:56-57
+  if (B * H * W > 0 && !disp) return set_error(SN_EINVAL, "NULL buffer");
+  CclParams p{B, H, W, rig->fx * rig->baseline, t};
+  DeviceGuard g(plan->device);
+  return run_passable(make_ctx(plan, stream), disp, p, passable, edges);
+}
+
+int sn_ccl_labels(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                  const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
+  if (B * H * W > 0 && (!disp || !labels)) return set_error(SN_EINVAL, "NULL buffer");
+  if (row_base < 0 || (row_base + H) * W > 0x7fffffffLL)
+    return set_error(SN_EINVAL, "label index range exceeds int32");
+  CclParams p{B, H, W, rig->fx * rig->baseline, t};
+  DeviceGuard g(plan->device);
+  return run_ccl(make_ctx(plan, stream), disp, nullptr, p, row_base * W, labels);
+}
+
+int sn_ccl_from_passable(sn_plan_t* plan, const uint8_t* passable, int64_t B, int64_t H, int64_t W,
+                         int64_t row_base, int32_t* labels, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (B * H * W > 0 && (!passable || !labels)) return set_error(SN_EINVAL, "NULL buffer");
+  if (row_base < 0 || (row_base + H) * W > 0x7fffffffLL)
+    return set_error(SN_EINVAL, "label index range exceeds int32");
+  CclParams p{B, H, W, 0.0, 0.0};
+  DeviceGuard g(plan->device);
+  return run_ccl(make_ctx(plan, stream), nullptr, passable, p, row_base * W, labels);
+}
+
+int sn_relabel(sn_plan_t* plan, int32_t* labels, int64_t n, int64_t index_base,
+               const int32_t* map_keys, const int32_t* map_vals, const int32_t* n_map,
+               int32_t map_capacity, int32_t* scratch, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  if (n < 0 || map_capacity < 0) return set_error(SN_EINVAL, "negative size");
+  if (n > 0 && (!labels || !scratch || !map_keys || !map_vals || !n_map))
+    return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_relabel(make_ctx(plan, stream), labels, n, index_base, map_keys, map_vals, n_map,
+                     map_capacity, scratch);
+}
+
+// Strip-seam merge on gathered boundary rows (host memory; tiny: 2 rows per
+// strip).  Union-find over label values with min-root links, so the map is
+// independent of gather order and identical on every rank.
+int sn_seam_merge_host(const int32_t* seams, int32_t n_strips, int64_t W, int32_t* map_keys,
+                       int32_t* map_vals, int32_t* n_map) {
+  if (!seams || !map_keys || !map_vals || !n_map || n_strips < 0 || W < 0)
+    return set_error(SN_EINVAL, "bad seam-merge arguments");
+  std::unordered_map<int32_t, int32_t> parent;
+  parent.reserve((size_t)n_strips * 2 * (size_t)W);
+  auto find = [&](int32_t x) {
+    int32_t r = x;
+    while (true) {
+      const int32_t p = parent[r];
+      if (p == r) break;
+      r = p;
+    }
+    while (parent[x] != r) {  // path compression
+      const int32_t nx = parent[x];
+      parent[x] = r;
+      x = nx;
+    }
+    return r;
+  };
+  for (int64_t i = 0; i < (int64_t)n_strips * 2 * W; ++i)
+    if (seams[i] >= 0) parent.emplace(seams[i], seams[i]);
+  for (int32_t s = 0; s + 1 < n_strips; ++s) {
+    const int32_t* a = seams + ((int64_t)s * 2 + 1) * W;   // last owned row of strip s
+    const int32_t* b = seams + ((int64_t)(s + 1) * 2) * W;  // first owned row of strip s+1
+    for (int64_t u = 0; u < W; ++u) {
+      if (b[u] < 0) continue;
+      for (int64_t du = -1; du <= 1; ++du) {
+        const int64_t uu = u + du;
+        if (uu < 0 || uu >= W || a[uu] < 0) continue;
+        int32_t ra = find(a[uu]), rb = find(b[u]);
+        if (ra == rb) continue;
+        if (ra < rb) parent[rb] = ra;
+        else parent[ra] = rb;
+      }
+    }
+  }
+  std::vector<int32_t> keys;
+  keys.reserve(parent.size());
+  for (auto& kv : parent) keys.push_back(kv.first);
+  std::sort(keys.begin(), keys.end());
+  int32_t n = 0;
+  for (int32_t k : keys) {
+    const int32_t r = find(k);
+    if (r != k) {
+      map_keys[n] = k;
+      map_vals[n] = r;
+      ++n;
+    }
+  }
+  *n_map = n;
+  return SN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer path: frames in chunks, H2D / compute / D2H overlapped on three
+// streams with double-buffered device staging.
+
+int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
+                            int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
+                            int32_t n_off, float* out6_host, uint8_t* mask_host) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  sn_moments_t m;
+  if ((rc = sn_kernel_moments(offsets_xy, n_off, &m))) return rc;
+  const int64_t frame_px = H * W;
+  if (B * frame_px == 0) return SN_OK;
+  if (!disp_host || !out6_host) return set_error(SN_EINVAL, "NULL buffer");
+  std::lock_guard<std::mutex> lock(plan->mu);
+  DeviceGuard g(plan->device);
+  // chunk: ~16 Mpx per step (64 MB in, 384 MB out), whole frames
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(16 << 20) / std::max<int64_t>(frame_px, 1));
+  chunk = std::min<int64_t>(chunk, B);
+  const size_t need = (size_t)(chunk * frame_px);
+  if (plan->cap_px < need) {
+    for (int i = 0; i < 2; ++i) {
+      if (plan->d_in[i]) cudaFree(plan->d_in[i]);
+      if (plan->d_out[i]) cudaFree(plan->d_out[i]);
+      if (plan->d_mask[i]) cudaFree(plan->d_mask[i]);
+      plan->d_in[i] = nullptr;
+      plan->d_out[i] = nullptr;
+      plan->d_mask[i] = nullptr;
+    }
+    plan->cap_px = 0;
+    for (int i = 0; i < 2; ++i) {
+      if (cudaMalloc(&plan->d_in[i], need * sizeof(float)) != cudaSuccess ||
+          cudaMalloc(&plan->d_out[i], need * 24) != cudaSuccess ||
+          cudaMalloc(&plan->d_mask[i], need) != cudaSuccess)
+        return set_cuda_error("cudaMalloc(host-path staging)");
+    }
+    plan->cap_px = need;
+  }
+  if (!plan->s_h2d) {
+    if (cudaStreamCreateWithFlags(&plan->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&plan->s_comp, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&plan->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+      return set_cuda_error("cudaStreamCreate");
+    for (int i = 0; i < 2; ++i) {
+      if (cudaEventCreateWithFlags(&plan->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&plan->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&plan->ev_out[i], cudaEventDisableTiming) != cudaSuccess)
+        return set_cuda_error("cudaEventCreate");
+    }
+  }
+  const int64_t n_chunks = (B + chunk - 1) / chunk;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int s = (int)(c & 1);
+    const int64_t f0 = c * chunk;
+    const int64_t nf = std::min<int64_t>(chunk, B - f0);
+    const size_t px = (size_t)(nf * frame_px);
+    // buffers of slot s are free once chunk c-2's compute (inputs) and D2H (outputs) are done
+    if (c >= 2) {
+      cudaStreamWaitEvent(plan->s_h2d, plan->ev_done[s], 0);
+      cudaStreamWaitEvent(plan->s_comp, plan->ev_out[s], 0);
+    }
+    if (cudaMemcpyAsync(plan->d_in[s], disp_host + f0 * frame_px, px * sizeof(float),
+                        cudaMemcpyHostToDevice, plan->s_h2d) != cudaSuccess)
+      return set_cuda_error("H2D copy");
+    cudaEventRecord(plan->ev_in[s], plan->s_h2d);
+    cudaStreamWaitEvent(plan->s_comp, plan->ev_in[s], 0);
+    rc = sn_oriented_points(plan, plan->d_in[s], nf, H, W, rig, offsets_xy, n_off, plan->d_out[s],
+                            mask_host ? plan->d_mask[s] : nullptr, plan->s_comp);
+    if (rc) return rc;
+    cudaEventRecord(plan->ev_done[s], plan->s_comp);
+    cudaStreamWaitEvent(plan->s_d2h, plan->ev_done[s], 0);
+    if (cudaMemcpyAsync(out6_host + f0 * frame_px * 6, plan->d_out[s], px * 24,
+                        cudaMemcpyDeviceToHost, plan->s_d2h) != cudaSuccess)
+      return set_cuda_error("D2H copy");
+    if (mask_host &&
+        cudaMemcpyAsync(mask_host + f0 * frame_px, plan->d_mask[s], px, cudaMemcpyDeviceToHost,
+                        plan->s_d2h) != cudaSuccess)
+      return set_cuda_error("D2H mask copy");
+    cudaEventRecord(plan->ev_out[s], plan->s_d2h);
+  }
+  if (cudaStreamSynchronize(plan->s_d2h) != cudaSuccess) return set_cuda_error("host-path sync");
+  if (cudaStreamSynchronize(plan->s_comp) != cudaSuccess) return set_cuda_error("host-path sync");
+  return SN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,155 @@
+// Shared device helpers for the sm_100a kernels: TMA / mbarrier / bulk-copy
+// PTX wrappers and the closed-form normal epilogue.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sn_b200.h"
+
+namespace sn {
+
+// ---------------------------------------------------------------------------
+// kernel parameters shared by the fixed-pass kernels
+
+struct FixedParams {
+  int64_t B, H, W;
+  // rig, pre-combined on the host in Python's double order
+  double fx, fy, u0, v0;
+  double fxb;      // fx * b (Python double product, geometry.py:43)
+  float fxb_f;     // fp32(fx * b)       point path
+  float inv_fx_f;  // fp32(1 / fx)
+  float inv_fy_f;  // fp32(1 / fy)
+  float u0_hi, u0_lo, v0_hi, v0_lo;  // two-float split of u0, v0
+  // integer moments of the offset pattern (exact in double)
+  double alpha, beta, gamma, det, sx, sy;
+  int R;  // square radius (fast path)
+};
+
+// ---------------------------------------------------------------------------
+// PTX wrappers (sm_90+ async proxy; all used on sm_100a)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y,
+                                             int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::
+                   "l"(reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// closed-form normal (geometry.py:175-216, rescaled)
+//
+// The reference computes, for d > 0 and w = b/d, g = -dd/du:
+//   n ~ (g w fx^2, -a2 w fx fy, ((a2 dv - g du) w - b) fx)
+// Dividing by w*fx > 0 and multiplying by det > 0 (neither changes the
+// direction) gives, with P1 = det*dd/du, P2 = det*dd/dv:
+//   n ~ (-P1 fx, -P2 fy, P2 dv + P1 du - det d)
+// which needs no division before the normalisation and cannot overflow for
+// fp32-representable inputs.  The camera-facing flip never fires
+// (n . X = -b fx z < 0, geometry.py:181-184), so none is applied.
+
+__device__ __forceinline__ void normal_from_moments(double P1, double P2, double det, double d,
+                                                    double du, double dv, double fx, double fy,
+                                                    float& nx, float& ny, float& nz) {
+  const double ax = -P1 * fx;
+  const double ay = -P2 * fy;
+  const double az = fma(P2, dv, fma(P1, du, -det * d));
+  const double s = fma(ax, ax, fma(ay, ay, az * az));
+  const double inv = rsqrt(s);
+  nx = static_cast<float>(ax * inv);
+  ny = static_cast<float>(ay * inv);
+  nz = static_cast<float>(az * inv);
+}
+
+// z = (fx b)/d; x = (u - u0) z / fx; y = (v - v0) z / fy  (geometry.py:39-64),
+// fp32 with <= ~4 ulp relative error; NaN unless d is finite and > 0.
+__device__ __forceinline__ void point_from_disparity(float d, float du, float dv, float fxb,
+                                                     float inv_fx, float inv_fy, float& x,
+                                                     float& y, float& z) {
+  const bool ok = (d > 0.0f) && (d <= 3.402823466e38f);
+  const float zz = ok ? fxb * __frcp_rn(d) : __int_as_float(0x7fc00000);
+  z = zz;
+  x = du * zz * inv_fx;
+  y = dv * zz * inv_fy;
+}
+
+// fp64-input variant (geometry.py:39-64 in double, then rounded to fp32).
+__device__ __forceinline__ void point_from_disparity_f64(double d, double du, double dv,
+                                                         const FixedParams& p, float& x, float& y,
+                                                         float& z) {
+  const bool ok = (d > 0.0) && (d <= 1.7976931348623157e308);
+  if (ok) {
+    const double zz = p.fxb / d;
+    z = static_cast<float>(zz);
+    x = static_cast<float>(du * zz / p.fx);
+    y = static_cast<float>(dv * zz / p.fy);
+  } else {
+    x = y = z = __int_as_float(0x7fc00000);
+  }
+}
+
+__device__ __forceinline__ bool finite_f(float v) { return fabsf(v) <= 3.402823466e38f; }
+__device__ __forceinline__ bool finite_d(double v) { return fabs(v) <= 1.7976931348623157e308; }
+
+}  // namespace sn

@@ -1,0 +1,522 @@
+// Fused fixed-kernel oriented-point pass for sm_100a.
+//
+// Reference path (pkg/src/stereonorm): kernels.py:135-179 (_affine_pass:
+// masked correlation with the precomputed LSQ weights, centre correction,
+// support/border invalidation), kernels.py:237-261 (estimate_normals_fixed),
+// geometry.py:175-216 (fused normal epilogue) and geometry.py:39-64,85-89
+// (triangulation).  The reference never materialises the denoised map; nor
+// does this pass: one launch reads the fp32 disparity once and writes the
+// 24-byte (x, y, z, nx, ny, nz) record per pixel.
+//
+// Arithmetic: the weights s1 = vx/alpha, s2 = vy/alpha of a
+// square pattern are integer offsets over an integer moment, so the device
+// accumulates U = sum vx*d and V = sum vy*d EXACTLY in fp64 (fp32 inputs
+// times small integers need < 53 bits) and divides by the moments once, in
+// the rescaled normal formula of sn_common.cuh.  The square pattern is
+// separable, so the sums are two sliding-window passes:
+//   pass V (lane <-> column): C = sum_dy d,   Rr = sum_dy dy*d
+//   pass H (lane <-> row):    U = sum_dx dx*C, V = sum_dx Rr
+// each O(1) per pixel.  Every intermediate is an exact sum of the current
+// window whenever the window's dynamic range fits 53 bits; columns/runs that
+// hold |d| > 2^40 take a direct (non-sliding) path so no rounding can leak
+// past the window.  Validity is tracked exactly with bit masks: a pixel is
+// valid iff every support sample is inside the image and finite and the
+// centre disparity is > 0; samples outside the image are
+// masked by coordinate, which reproduces kernels.py:166-176.
+//
+// Data movement (B200): the input tile + halo is one 3D TMA load
+// (cp.async.bulk.tensor) per item, prefetched while the previous item's
+// pass H runs; the AoS-6 output tile is
+// staged in 128B-swizzled shared memory (conflict-free float4 writes from
+// lanes that own different rows) and leaves as 24 TMA stores per item, so
+// HBM sees full-line writes only.  Persistent grid, two CTAs per SM.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "sn_common.cuh"
+#include "sn_internal.h"
+
+namespace sn {
+
+constexpr int kTW = 128;           // output columns per item
+constexpr int kG = 16;             // output rows per item
+constexpr int kCP = kG + 1;        // pitch of the column-major C/Rr/Dc arrays (odd)
+constexpr int kBoxF = 32;          // floats per TMA store box row (128 B)
+constexpr int kBoxes = kTW * 6 / kBoxF;  // 24
+constexpr int kFastThreads = 160;  // 5 warps: pass V uses up to 128+2R lanes, pass H 128
+constexpr double kBig = 1099511627776.0;  // 2^40
+
+__host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+template <int R, typename T>
+struct FastCfg {
+  static constexpr int NC = kTW + 2 * R;
+  static constexpr int NR = kG + 2 * R;
+  static constexpr int AE = 16 / (int)sizeof(T);
+  // the box starts at (x0 - R) rounded down to 16 B, so it spans up to AE-1 extra columns
+  static constexpr int BW = (NC + AE - 1 + AE - 1) / AE * AE;
+  static constexpr size_t STAGE = 0;
+  static constexpr size_t STAGE_BYTES = (size_t)kBoxes * kG * 128;
+  static constexpr size_t IN = STAGE + STAGE_BYTES;
+  static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
+  static constexpr size_t CS = align_up(IN + IN_BYTES, 128);
+  static constexpr size_t CS_BYTES = (size_t)NC * kCP * 8;
+  static constexpr size_t RS = CS + CS_BYTES;
+  static constexpr size_t DC = RS + CS_BYTES;
+  static constexpr size_t DC_BYTES = (size_t)kTW * kCP * sizeof(T);
+  static constexpr size_t FL = align_up(DC + DC_BYTES, 16);
+  static constexpr size_t BAR = align_up(FL + NC * 4, 16);
+  static constexpr size_t TOTAL = BAR + 16 + 1024;  // + slack for 1024-B alignment
+  static_assert(NC <= kFastThreads, "pass V needs one lane per column");
+  static_assert(NR <= 32, "row validity bits must fit 32 bits");
+};
+
+template <typename T>
+__device__ __forceinline__ bool finite_t(T v) {
+  return fabs((double)v) <= 1.7976931348623157e308;
+}
+template <>
+__device__ __forceinline__ bool finite_t<float>(float v) {
+  return fabsf(v) <= 3.402823466e38f;
+}
+
+// ---------------------------------------------------------------------------
+// fast path: centred square pattern, radius R
+
+template <int R, typename T>
+__global__ void __launch_bounds__(kFastThreads, 2)
+    fixed_square_kernel(const __grid_constant__ CUtensorMap in_map,
+                        const __grid_constant__ CUtensorMap out_map, const FixedParams p,
+                        uint8_t* __restrict__ mask_out, const int64_t n_items, const int tiles_x,
+                        const int tiles_y) {
+  using Cfg = FastCfg<R, T>;
+  constexpr int NC = Cfg::NC, NR = Cfg::NR, BW = Cfg::BW;
+  constexpr int NWIN = 2 * R + 1;
+  constexpr int NH = kG + 2 * R;  // columns read per pass-H run (run = 16 outputs)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  T* in = reinterpret_cast<T*>(smem + Cfg::IN);
+  double* Cs = reinterpret_cast<double*>(smem + Cfg::CS);
+  double* Rs = reinterpret_cast<double*>(smem + Cfg::RS);
+  T* Dc = reinterpret_cast<T*>(smem + Cfg::DC);
+  uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
+  const uint32_t stage_base = smem_u32(smem + Cfg::STAGE);
+  const int tid = threadIdx.x;
+
+  int64_t item = blockIdx.x;
+  if (item >= n_items) return;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&in_map);
+    tma_prefetch_desc(&out_map);
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto decode = [&](int64_t it, int& x0, int& y0, int& bz) {
+    const int tx = (int)(it % tiles_x);
+    const int64_t r = it / tiles_x;
+    x0 = tx * kTW;
+    y0 = (int)(r % tiles_y) * kG;
+    bz = (int)(r / tiles_y);
+  };
+
+  // TMA tile origin: the halo origin with its innermost coordinate rounded
+  // down to a 16-byte multiple (an unaligned innermost TMA coordinate raises
+  // an illegal-instruction fault on this part -- measured, tools/ubench/
+  // tma_probe.cu).  Negative (aligned) coordinates are fine.  Pass V masks
+  // out-of-image samples by coordinate, which reproduces the no-padding
+  // border rule kernels.py:166-176.
+  constexpr int AE = Cfg::AE;
+  auto tile_x = [](int x0) { return (int)floorf((float)(x0 - R) / (float)AE) * AE; };
+  auto load_tile = [&](int x0, int y0, int bz) {
+    mbar_arrive_expect_tx(bar, (uint32_t)Cfg::IN_BYTES);
+    tma_load_3d(in, &in_map, bar, tile_x(x0), y0 - R, bz);
+  };
+  if (tid == 0) {
+    int x0, y0, bz;
+    decode(item, x0, y0, bz);
+    load_tile(x0, y0, bz);
+  }
+
+  uint32_t phase = 0;
+  for (; item < n_items; item += gridDim.x) {
+    int x0, y0, bz;
+    decode(item, x0, y0, bz);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const int ox = tile_x(x0) - (x0 - R);  // logical column c <-> smem column c - ox (ox <= 0)
+    constexpr int oy = 0;
+
+    // ------------------------------------------------------------ pass V
+    if (tid < NC) {
+      const int c = tid;
+      const int gxc = x0 - R + c;
+      const bool col_ok = gxc >= 0 && gxc < p.W;
+      const T* col = in + (c - ox);
+      const int gy0 = y0 - R;
+      double v[NR];
+      uint32_t invb = 0;
+      bool big = false;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const bool in_img = col_ok && (gy0 + i) >= 0 && (gy0 + i) < p.H;
+        const T raw = in_img ? col[(i - oy) * BW] : (T)0;
+        const bool f = in_img && finite_t(raw);
+        invb |= (f ? 0u : 1u) << i;
+        const double dv = f ? (double)raw : 0.0;
+        big |= fabs(dv) > kBig;
+        v[i] = dv;
+      }
+      double* cs = Cs + c * kCP;
+      double* rs = Rs + c * kCP;
+      if (!big) {
+        double C = 0.0, Rr = 0.0;
+#pragma unroll
+        for (int j = 0; j < NWIN; ++j) {
+          C += v[j];
+          Rr = fma((double)(j - R), v[j], Rr);
+        }
+        cs[0] = C;
+        rs[0] = Rr;
+#pragma unroll
+        for (int g = 1; g < kG; ++g) {
+          const double vin = v[g + 2 * R], vout = v[g - 1];
+          C += vin - vout;
+          Rr = fma((double)R, vout, fma((double)(R + 1), vin, Rr - C));
+          cs[g] = C;
+          rs[g] = Rr;
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          double C = 0.0, Rr = 0.0;
+#pragma unroll
+          for (int j = 0; j < NWIN; ++j) {
+            C += v[g + j];
+            Rr = fma((double)(j - R), v[g + j], Rr);
+          }
+          cs[g] = C;
+          rs[g] = Rr;
+        }
+      }
+      uint32_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
+      fl[c] = (acc & 0xFFFFu) | (big ? 0x80000000u : 0u);
+      if (c >= R && c < R + kTW) {
+        T* dc = Dc + (c - R) * kCP;
+#pragma unroll
+        for (int g = 0; g < kG; ++g) dc[g] = col[(g + R - oy) * BW];
+      }
+    }
+    if (tid == 0) bulk_wait_read0();  // staging of the previous item consumed by TMA
+    __syncthreads();
+
+    // input tile consumed: prefetch the next item while pass H runs
+    if (tid == 0) {
+      const int64_t nxt = item + gridDim.x;
+      if (nxt < n_items) {
+        int nx0, ny0, nbz;
+        decode(nxt, nx0, ny0, nbz);
+        load_tile(nx0, ny0, nbz);
+      }
+    }
+
+    // ------------------------------------------------------------ pass H + epilogue
+    if (tid < kTW) {
+      const int g = tid & 15;
+      const int q = tid >> 4;  // run of 16 output columns
+      const int colbase = q * 16;
+      double cc[NH], rr[NH];
+      uint32_t colinv = 0;
+      bool big = false;
+#pragma unroll
+      for (int i = 0; i < NH; ++i) {
+        cc[i] = Cs[(colbase + i) * kCP + g];
+        rr[i] = Rs[(colbase + i) * kCP + g];
+        const uint32_t f = fl[colbase + i];
+        colinv |= ((f >> g) & 1u) << i;
+        big |= (f >> 31) != 0u;
+      }
+      uint32_t win = 0;
+#pragma unroll
+      for (int j = 0; j < NWIN; ++j) win |= colinv >> j;
+
+      const int yg = y0 + g;
+      const int xb = x0 + colbase;
+      const double dv = (double)yg - p.v0;
+      const float dv_f = ((float)yg - p.v0_hi) - p.v0_lo;
+      const double du0 = (double)xb - p.u0;
+      const T* dcp = Dc + colbase * kCP + g;
+      const double alpha = p.alpha;
+      const uint32_t gsw = (uint32_t)(g & 7);
+      const uint32_t rowaddr = stage_base + (uint32_t)g * 128u;
+
+      double Box = 0.0, U = 0.0, V = 0.0;
+      if (!big) {
+#pragma unroll
+        for (int j = 0; j < NWIN; ++j) {
+          Box += cc[j];
+          U = fma((double)(j - R), cc[j], U);
+          V += rr[j];
+        }
+      }
+      float o[12];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (!big) {
+          if (j > 0) {
+            const double cin = cc[j + 2 * R], cout = cc[j - 1];
+            Box += cin - cout;
+            U = fma((double)R, cout, fma((double)(R + 1), cin, U - Box));
+            V += rr[j + 2 * R] - rr[j - 1];
+          }
+        } else {
+          U = 0.0;
+          V = 0.0;
+#pragma unroll
+          for (int i = 0; i < NWIN; ++i) {
+            U = fma((double)(i - R), cc[j + i], U);
+            V += rr[j + i];
+          }
+        }
+        const T dcv = dcp[j * kCP];
+        const bool valid = (((win >> j) & 1u) == 0u) && (dcv > (T)0);
+        float px, py, pz, nx, ny, nz;
+        const int xg = xb + j;
+        const float du_f = ((float)xg - p.u0_hi) - p.u0_lo;
+        if constexpr (sizeof(T) == 4) {
+          point_from_disparity((float)dcv, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
+        } else {
+          point_from_disparity_f64((double)dcv, (double)xg - p.u0, dv, p, px, py, pz);
+        }
+        if (valid) {
+          normal_from_moments(U, V, alpha, (double)dcv, du0 + (double)j, dv, p.fx, p.fy, nx, ny, nz);
+        } else {
+          nx = ny = nz = __int_as_float(0x7fc00000);
+        }
+        const int s = (j & 1) * 6;
+        o[s + 0] = px;
+        o[s + 1] = py;
+        o[s + 2] = pz;
+        o[s + 3] = nx;
+        o[s + 4] = ny;
+        o[s + 5] = nz;
+        if (j & 1) {
+          // pixels (j-1, j) = 12 floats = 3 chunks of the 128B-swizzled staging row
+          const int K = q * 24 + (j >> 1) * 3;  // chunk index within the 768-float tile row
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int kk = K + t;
+            const uint32_t box = (uint32_t)(kk >> 3);
+            const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
+            st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[4 * t], o[4 * t + 1],
+                         o[4 * t + 2], o[4 * t + 3]);
+          }
+        }
+        if (mask_out != nullptr && yg < p.H && xg < p.W) {
+          mask_out[((int64_t)bz * p.H + yg) * p.W + xg] = valid ? 1 : 0;
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll 1
+      for (int b = 0; b < kBoxes; ++b) {
+        tma_store_3d(&out_map, smem + Cfg::STAGE + (size_t)b * kG * 128, x0 * 6 + b * kBoxF, y0, bz);
+      }
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------
+// generic path: any offset pattern, any shape (thread per pixel, direct sums)
+
+template <typename T, bool AFFINE>
+__global__ void __launch_bounds__(256)
+    fixed_generic_kernel(const T* __restrict__ disp, const FixedParams p,
+                         const __grid_constant__ OffsetTable tab, float* __restrict__ out6,
+                         uint8_t* __restrict__ mask, double* __restrict__ a1,
+                         double* __restrict__ a2) {
+  const int n_off = tab.n;
+  const int2* soff = tab.v;
+  const int64_t total = p.B * p.H * p.W;
+  const int64_t W = p.W, H = p.H;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = idx % W;
+    const int64_t r = idx / W;
+    const int64_t y = r % H;
+    const T* frame = disp + (r / H) * H * W;
+    const T dc = frame[y * W + x];
+    bool ok = finite_t(dc);
+    double U = 0.0, V = 0.0;
+    for (int i = 0; i < n_off && ok; ++i) {
+      const int2 o = soff[i];
+      const int64_t xx = x + o.x, yy = y + o.y;
+      if (xx < 0 || xx >= W || yy < 0 || yy >= H) {
+        ok = false;
+        break;
+      }
+      const T v = frame[yy * W + xx];
+      if (!finite_t(v)) {
+        ok = false;
+        break;
+      }
+      U = fma((double)o.x, (double)v, U);
+      V = fma((double)o.y, (double)v, V);
+    }
+    const double dcd = (double)dc;
+    const double Up = U - p.sx * dcd;
+    const double Vp = V - p.sy * dcd;
+    const double P1 = p.gamma * Up - p.beta * Vp;  // det * dd/du
+    const double P2 = p.alpha * Vp - p.beta * Up;  // det * dd/dv
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    if (AFFINE) {
+      a1[idx] = ok ? 1.0 + P1 / p.det : qnan;
+      a2[idx] = ok ? P2 / p.det : qnan;
+      if (mask) mask[idx] = ok ? 1 : 0;
+    } else {
+      const bool valid = ok && (dc > (T)0);
+      float px, py, pz, nx, ny, nz;
+      if constexpr (sizeof(T) == 4) {
+        const float du_f = ((float)x - p.u0_hi) - p.u0_lo;
+        const float dv_f = ((float)y - p.v0_hi) - p.v0_lo;
+        point_from_disparity((float)dc, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
+      } else {
+        point_from_disparity_f64(dcd, (double)x - p.u0, (double)y - p.v0, p, px, py, pz);
+      }
+      if (valid) {
+        normal_from_moments(P1, P2, p.det, dcd, (double)x - p.u0, (double)y - p.v0, p.fx, p.fy, nx,
+                            ny, nz);
+      } else {
+        nx = ny = nz = __int_as_float(0x7fc00000);
+      }
+      float* o6 = out6 + idx * 6;
+      reinterpret_cast<float2*>(o6)[0] = make_float2(px, py);
+      reinterpret_cast<float2*>(o6)[1] = make_float2(pz, nx);
+      reinterpret_cast<float2*>(o6)[2] = make_float2(ny, nz);
+      if (mask) mask[idx] = valid ? 1 : 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launchers
+
+template <int R, typename T>
+static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams& p, float* out6,
+                         uint8_t* mask) {
+  using Cfg = FastCfg<R, T>;
+  CUtensorMap in_map, out_map;
+  const CUtensorMapDataType dt =
+      sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.B};
+    cuuint64_t strides[2] = {(cuuint64_t)(p.W * sizeof(T)), (cuuint64_t)(p.W * p.H * sizeof(T))};
+    cuuint32_t box[3] = {(cuuint32_t)Cfg::BW, (cuuint32_t)Cfg::NR, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (encode_tiled(&in_map, dt, 3, (void*)disp, dims, strides, box, es,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != 0)
+      return SN_ECUDA;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)(p.W * 6), (cuuint64_t)p.H, (cuuint64_t)p.B};
+    cuuint64_t strides[2] = {(cuuint64_t)(p.W * 24), (cuuint64_t)(p.W * p.H * 24)};
+    cuuint32_t box[3] = {(cuuint32_t)kBoxF, (cuuint32_t)kG, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (encode_tiled(&out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)out6, dims, strides, box,
+                     es, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != 0)
+      return SN_ECUDA;
+  }
+  auto kern = fixed_square_kernel<R, T>;
+  static bool attr_set = false;  // per template instance
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::TOTAL) !=
+        cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(fixed_square_kernel)");
+    attr_set = true;
+  }
+  const int tiles_x = (int)((p.W + kTW - 1) / kTW);
+  const int tiles_y = (int)((p.H + kG - 1) / kG);
+  const int64_t n_items = (int64_t)tiles_x * tiles_y * p.B;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFastThreads, Cfg::TOTAL) !=
+      cudaSuccess)
+    return set_cuda_error("occupancy query");
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)per_sm * ctx.num_sms;
+  if (grid > n_items) grid = n_items;
+  kern<<<(unsigned)grid, kFastThreads, Cfg::TOTAL, ctx.stream>>>(in_map, out_map, p, mask, n_items,
+                                                                 tiles_x, tiles_y);
+  return check_launch("fixed_square_kernel");
+}
+
+template <typename T>
+static int dispatch_square(int R, const LaunchCtx& ctx, const T* disp, const FixedParams& p,
+                           float* out6, uint8_t* mask) {
+  switch (R) {
+    case 1: return launch_square<1, T>(ctx, disp, p, out6, mask);
+    case 2: return launch_square<2, T>(ctx, disp, p, out6, mask);
+    case 3: return launch_square<3, T>(ctx, disp, p, out6, mask);
+    case 4: return launch_square<4, T>(ctx, disp, p, out6, mask);
+    case 5: return launch_square<5, T>(ctx, disp, p, out6, mask);
+    case 6: return launch_square<6, T>(ctx, disp, p, out6, mask);
+    case 7: return launch_square<7, T>(ctx, disp, p, out6, mask);
+    case 8: return launch_square<8, T>(ctx, disp, p, out6, mask);
+    default: return -1;
+  }
+}
+
+template <typename T>
+static int launch_generic(const LaunchCtx& ctx, const T* disp, const FixedParams& p,
+                          const OffsetTable& tab, float* out6, uint8_t* mask, double* a1,
+                          double* a2, bool affine) {
+  const int64_t total = p.B * p.H * p.W;
+  if (total == 0) return SN_OK;
+  int64_t grid = (total + 255) / 256;
+  const int64_t cap = (int64_t)ctx.num_sms * 8;
+  if (grid > cap) grid = cap;
+  if (affine)
+    fixed_generic_kernel<T, true><<<(unsigned)grid, 256, 0, ctx.stream>>>(disp, p, tab, out6, mask,
+                                                                        a1, a2);
+  else
+    fixed_generic_kernel<T, false><<<(unsigned)grid, 256, 0, ctx.stream>>>(disp, p, tab, out6, mask,
+                                                                         a1, a2);
+  return check_launch("fixed_generic_kernel");
+}
+
+template <typename T>
+int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const sn_moments_t& m,
+              const OffsetTable& tab, float* out6, uint8_t* mask, double* a1, double* a2,
+              bool affine, int force_generic) {
+  if (p.B * p.H * p.W == 0) return SN_OK;
+  const bool aligned = (reinterpret_cast<uintptr_t>(disp) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(out6) % 16 == 0) &&
+                       (p.W % (16 / (int64_t)sizeof(T)) == 0) && (p.W % 2 == 0) &&
+                       p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
+  if (!affine && !force_generic && m.square_r >= 1 && m.square_r <= 8 && aligned) {
+    const int rc = dispatch_square<T>(m.square_r, ctx, disp, p, out6, mask);
+    if (rc >= 0) return rc;
+  }
+  return launch_generic<T>(ctx, disp, p, tab, out6, mask, a1, a2, affine);
+}
+
+template int run_fixed<float>(const LaunchCtx&, const float*, const FixedParams&,
+                              const sn_moments_t&, const OffsetTable&, float*, uint8_t*, double*,
+                              double*, bool, int);
+template int run_fixed<double>(const LaunchCtx&, const double*, const FixedParams&,
+                               const sn_moments_t&, const OffsetTable&, float*, uint8_t*, double*,
+                               double*, bool, int);
+
+}  // namespace sn

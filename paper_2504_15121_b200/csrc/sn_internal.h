@@ -1,0 +1,55 @@
+// Host-side internals shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sn_b200.h"
+#include "sn_common.cuh"
+
+namespace sn {
+
+struct LaunchCtx {
+  cudaStream_t stream;
+  int device;
+  int num_sms;
+};
+
+// error plumbing (thread-local message, see sn_api.cu)
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(const char* what);
+int check_launch(const char* what);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+int encode_tiled(CUtensorMap* map, CUtensorMapDataType dt, int rank, void* gaddr,
+                 const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                 const cuuint32_t* elem_strides, CUtensorMapSwizzle swizzle,
+                 CUtensorMapFloatOOBfill oob);
+
+constexpr int kMaxOffsets = 1024;
+struct OffsetTable {
+  int n;
+  int2 v[kMaxOffsets];
+};
+
+template <typename T>
+int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const sn_moments_t& m,
+              const OffsetTable& tab, float* out6, uint8_t* mask, double* a1, double* a2,
+              bool affine, int force_generic);
+
+struct CclParams {
+  int64_t B, H, W;
+  double fxb;  // fx * b in Python's double order (geometry.py:43)
+  double t;    // ST threshold
+};
+
+int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, uint8_t* passable,
+                 double* edges);
+int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* passable, const CclParams& p,
+            int64_t index_base, int32_t* labels);
+int run_relabel(const LaunchCtx& ctx, int32_t* labels, int64_t n, int64_t base,
+                const int32_t* keys, const int32_t* vals, const int32_t* n_map, int32_t cap,
+                int32_t* scratch);
+
+}  // namespace sn

@@ -1,0 +1,201 @@
+"""Device entry points on CUDA tensors (torch is plumbing: memory + streams).
+
+Each function validates its tensors, takes the caller's current CUDA stream
+and calls the C ABI (include/sn_b200.h) asynchronously -- no host
+synchronisation, CUDA-graph capturable.  Shapes: disparity ``[B, H, W]`` (or
+``[H, W]``), fp32 (headline path) or fp64; outputs are allocated when not
+supplied.
+
+Reference functions these replace (pkg/src/stereonorm):
+  oriented_points   estimate_normals_fixed kernels.py:237-261 +
+                    triangulate_grid geometry.py:85-89 (dense PLY record, cli.py:118-123)
+  affine            convolve_affine kernels.py:182-203
+  passable          depth_laplacian adaptive.py:80-97 + ST test adaptive.py:130-132
+  component_labels  new
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from ._native import check
+
+
+def _offsets_of(kernels) -> np.ndarray:
+    from .kernels import PrecomputedKernels, KernelSpec  # local: avoid import cycle
+    if isinstance(kernels, PrecomputedKernels):
+        return _native.offsets_array(kernels.spec.offsets)
+    if isinstance(kernels, KernelSpec):
+        return _native.offsets_array(kernels.offsets)
+    return _native.offsets_array(KernelSpec.square(int(kernels)).offsets)
+
+
+def _batched(disp: torch.Tensor, name: str = "disparity") -> torch.Tensor:
+    if not isinstance(disp, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor on a CUDA device")
+    if not disp.is_cuda:
+        raise ValueError(f"{name} must live on a CUDA device (no CPU path exists)")
+    if disp.dim() == 2:
+        disp = disp.unsqueeze(0)
+    if disp.dim() != 3:
+        raise ValueError(f"{name} must have shape [B, H, W] or [H, W], got {tuple(disp.shape)}")
+    return disp.contiguous()
+
+
+def _stream(dev: torch.device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _check_out(t: torch.Tensor | None, shape, dtype, dev, name):
+    if t is None:
+        return torch.empty(shape, dtype=dtype, device=dev)
+    if shape[0] == 1 and tuple(t.shape) == tuple(shape[1:]):
+        t = t.unsqueeze(0)  # unbatched [H, W, ...] buffer for an unbatched input
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != dev or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)} on {dev}")
+    return t
+
+
+def oriented_points(disparity: torch.Tensor, rig, kernels=9, *, out: torch.Tensor | None = None,
+                    mask: torch.Tensor | None = None, generic: bool = False) -> torch.Tensor:
+    """Fused fit + normal + triangulation: returns ``[B, H, W, 6]`` fp32 (always
+    batched; a 2D input gives B = 1)
+    ``(x, y, z, nx, ny, nz)``; NaN normals where invalid, NaN points where
+    the disparity is not finite and positive.  ``mask`` (uint8 ``[B, H, W]``)
+    optionally receives the normal validity."""
+    d = _batched(disparity)
+    B, H, W = d.shape
+    dev = d.device
+    out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
+    if mask is not None:
+        mask = _check_out(mask, (B, H, W), torch.uint8, dev, "mask")
+    off = _offsets_of(kernels)
+    lib = _native.load()
+    if d.dtype == torch.float32:
+        fn = lib.sn_oriented_points_generic if generic else lib.sn_oriented_points
+    elif d.dtype == torch.float64:
+        if generic:
+            raise ValueError("generic=True is an fp32 test hook")
+        fn = lib.sn_oriented_points_f64
+    else:
+        raise ValueError(f"disparity dtype must be float32 or float64, got {d.dtype}")
+    rs = _native.rig_struct(rig)
+    rc = fn(_native.plan(dev.index), d.data_ptr(), B, H, W, ctypes.byref(rs), off.ctypes.data,
+            len(off), out.data_ptr(), mask.data_ptr() if mask is not None else None, _stream(dev))
+    check(rc, "oriented_points")
+    return out
+
+
+def affine(disparity: torch.Tensor, kernels, *, a1=None, a2=None, mask=None):
+    """convolve_affine on the device: (a1, a2, mask) fp64/fp64/uint8 ``[B, H, W]``."""
+    d = _batched(disparity)
+    B, H, W = d.shape
+    dev = d.device
+    a1 = _check_out(a1, (B, H, W), torch.float64, dev, "a1")
+    a2 = _check_out(a2, (B, H, W), torch.float64, dev, "a2")
+    mask = _check_out(mask, (B, H, W), torch.uint8, dev, "mask")
+    off = _offsets_of(kernels)
+    lib = _native.load()
+    if d.dtype == torch.float32:
+        fn = lib.sn_affine
+    elif d.dtype == torch.float64:
+        fn = lib.sn_affine_f64
+    else:
+        raise ValueError(f"disparity dtype must be float32 or float64, got {d.dtype}")
+    rc = fn(_native.plan(dev.index), d.data_ptr(), B, H, W, off.ctypes.data, len(off),
+            a1.data_ptr(), a2.data_ptr(), mask.data_ptr(), _stream(dev))
+    check(rc, "affine")
+    return a1, a2, mask
+
+
+def _fp32(d: torch.Tensor) -> torch.Tensor:
+    if d.dtype != torch.float32:
+        raise ValueError(f"this entry point takes float32 disparities, got {d.dtype}")
+    return d
+
+
+def passable(disparity: torch.Tensor, rig, threshold: float, *, out=None, edges=None):
+    """ST-passable set (uint8) and optionally the depth-Laplacian values."""
+    d = _fp32(_batched(disparity))
+    B, H, W = d.shape
+    dev = d.device
+    out = _check_out(out, (B, H, W), torch.uint8, dev, "out")
+    want_edges = edges is not None
+    if want_edges:
+        edges = _check_out(edges, (B, H, W), torch.float64, dev, "edges")
+    rs = _native.rig_struct(rig)
+    rc = _native.load().sn_passable(_native.plan(dev.index), d.data_ptr(), B, H, W,
+                                    ctypes.byref(rs), float(threshold), out.data_ptr(),
+                                    edges.data_ptr() if want_edges else None, _stream(dev))
+    check(rc, "passable")
+    return (out, edges) if want_edges else out
+
+
+def component_labels(disparity: torch.Tensor, rig, threshold: float, *, out=None,
+                     row_base: int = 0) -> torch.Tensor:
+    """8-connected labels of the ST-passable set: int32 ``[B, H, W]`` holding
+    the smallest raster index ``v*W + u`` (+ ``row_base*W``) of each pixel's
+    component, -1 where not passable."""
+    d = _fp32(_batched(disparity))
+    B, H, W = d.shape
+    dev = d.device
+    out = _check_out(out, (B, H, W), torch.int32, dev, "out")
+    rs = _native.rig_struct(rig)
+    rc = _native.load().sn_ccl_labels(_native.plan(dev.index), d.data_ptr(), B, H, W,
+                                      ctypes.byref(rs), float(threshold), int(row_base),
+                                      out.data_ptr(), _stream(dev))
+    check(rc, "component_labels")
+    return out
+
+
+def labels_from_passable(p: torch.Tensor, *, out=None, row_base: int = 0) -> torch.Tensor:
+    """Label an existing uint8/bool passable grid ``[B, H, W]``."""
+    p = _batched(p, "passable")
+    if p.dtype == torch.bool:
+        p = p.to(torch.uint8)
+    if p.dtype != torch.uint8:
+        raise ValueError("passable must be uint8 or bool")
+    B, H, W = p.shape
+    dev = p.device
+    out = _check_out(out, (B, H, W), torch.int32, dev, "out")
+    rc = _native.load().sn_ccl_from_passable(_native.plan(dev.index), p.data_ptr(), B, H, W,
+                                             int(row_base), out.data_ptr(), _stream(dev))
+    check(rc, "labels_from_passable")
+    return out
+
+
+def relabel(labels: torch.Tensor, keys: torch.Tensor, vals: torch.Tensor, n_map: torch.Tensor,
+            index_base: int, scratch: torch.Tensor | None = None) -> torch.Tensor:
+    """In-place (label -> root) remap of one strip's labels (device)."""
+    if not labels.is_cuda or labels.dtype != torch.int32 or not labels.is_contiguous():
+        raise ValueError("labels must be a contiguous int32 CUDA tensor")
+    dev = labels.device
+    n = labels.numel()
+    if scratch is None:
+        scratch = torch.empty(n, dtype=torch.int32, device=dev)
+    rc = _native.load().sn_relabel(_native.plan(dev.index), labels.data_ptr(), n, int(index_base),
+                                   keys.data_ptr(), vals.data_ptr(), n_map.data_ptr(),
+                                   int(keys.numel()), scratch.data_ptr(), _stream(dev))
+    check(rc, "relabel")
+    return labels
+
+
+def seam_merge(seams: np.ndarray):
+    """Deterministic union-find over gathered seam rows (host, tiny).
+    ``seams``: int32 ``[n_strips, 2, W]``.  Returns (keys, vals) int32."""
+    s = np.ascontiguousarray(np.asarray(seams, dtype=np.int32))
+    if s.ndim != 3 or s.shape[1] != 2:
+        raise ValueError("seams must have shape [n_strips, 2, W]")
+    n_strips, _, W = s.shape
+    cap = max(1, 2 * n_strips * W)
+    keys = np.empty(cap, dtype=np.int32)
+    vals = np.empty(cap, dtype=np.int32)
+    n = ctypes.c_int32(0)
+    rc = _native.load().sn_seam_merge_host(s.ctypes.data, n_strips, W, keys.ctypes.data,
+                                           vals.ctypes.data, ctypes.byref(n))
+    check(rc, "seam_merge")
+    return keys[:n.value].copy(), vals[:n.value].copy()

@@ -1,0 +1,41 @@
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu on the GPU box)")
+
+
+def _load(name):
+    z = np.load(GOLDEN / name, allow_pickle=False)
+    names = [str(n) for n in z["names"]]
+    cases = {}
+    for n in names:
+        pre = f"{n}__"
+        cases[n] = {k[len(pre):]: z[k] for k in z.files if k.startswith(pre)}
+    return cases
+
+
+@pytest.fixture(scope="session")
+def fixed_golden():
+    return _load("fixed_cases.npz")
+
+
+@pytest.fixture(scope="session")
+def ccl_golden():
+    return _load("ccl_cases.npz")
+
+
+@pytest.fixture(scope="session")
+def cuda_dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda", 0)

@@ -1,0 +1,202 @@
+"""Device parity: the CUDA path vs the reference golden vectors and the oracle.
+
+Bars (north star): normal masks and component labels bit-exact; normals
+within 0.01 deg (we assert 1e-4 deg, the fp32-storage floor is ~1e-5 deg);
+points within 1e-5 relative (|p - p_ref| / |p_ref|); affine parameters
+within 1e-9 relative (the reference's own criterion 2,
+test_acceptance.py:115-181).
+"""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import max_angle_deg, max_point_rel, max_rel, orig_of, rig_of
+
+pytestmark = pytest.mark.gpu
+
+ANGLE_TOL_DEG = 1e-4
+POINT_TOL = 1e-5
+
+FIXED = ["const", "hramp", "vramp", "border5", "hole", "asym", "tiny", "rand0", "rand1", "rand2",
+         "rand3", "rand4", "rand5", "rand6", "quirks", "quirks9", "plane", "street_k3",
+         "street_k9", "street_k15", "street_holes_k9", "sphere_k9", "odd_k5", "rand_f64"]
+CCL = ["street_s11_t0.05", "street_s11_t0.2", "street_s11_t1.0", "street_s12_t0.05",
+       "street_s12_t0.2", "street_s12_t1.0", "step_depth", "random"]
+
+
+def _check_record(o6, mask, c, tol=ANGLE_TOL_DEG):
+    nm = c["nmask"]
+    assert np.array_equal(mask.astype(bool), nm), "normal mask differs"
+    assert np.array_equal(np.isfinite(o6[..., 3:]).all(-1), nm)
+    ang = max_angle_deg(o6[nm][:, 3:], c["normals"][nm])
+    assert ang < tol, f"max normal angle {ang:.3e} deg"
+    unit = np.linalg.norm(o6[nm][:, 3:].astype(np.float64), axis=-1)
+    assert np.all(np.abs(unit - 1.0) < 1e-6)
+    pref = c["points"]
+    fin = np.isfinite(pref).all(-1)
+    assert np.array_equal(np.isfinite(o6[..., :3]).all(-1), fin), "point NaN pattern differs"
+    rel = max_point_rel(o6[fin][:, :3], pref[fin])
+    assert rel < POINT_TOL, f"point rel error {rel:.3e}"
+    return ang, rel
+
+
+@pytest.mark.parametrize("path", ["fp32", "fp32_generic", "fp64"])
+@pytest.mark.parametrize("name", FIXED)
+def test_oriented_points_golden(fixed_golden, cuda_dev, name, path):
+    from paper_2504_15121_b200 import device
+    c = fixed_golden[name]
+    if name.endswith("_f64") and path != "fp64":
+        pytest.skip("input is not fp32-representable")
+    dt = torch.float64 if path == "fp64" else torch.float32
+    d = torch.from_numpy(c["d"]).to(cuda_dev, dt)
+    mask = torch.empty((1,) + tuple(d.shape), dtype=torch.uint8, device=cuda_dev)
+    out = device.oriented_points(d, rig_of(c["rig"]), _spec(c), mask=mask,
+                                 generic=(path == "fp32_generic"))
+    torch.cuda.synchronize()
+    _check_record(out[0].cpu().numpy(), mask[0].cpu().numpy(), c)
+
+
+def _spec(c):
+    from paper_2504_15121_b200 import KernelSpec
+    return KernelSpec(c["offsets"])
+
+
+@pytest.mark.parametrize("name", FIXED)
+def test_affine_golden(fixed_golden, cuda_dev, name):
+    from paper_2504_15121_b200 import device
+    c = fixed_golden[name]
+    dt = torch.float64 if name.endswith("_f64") else torch.float32
+    d = torch.from_numpy(c["d"]).to(cuda_dev, dt)
+    a1, a2, m = device.affine(d, _spec(c))
+    m = m[0].cpu().numpy().astype(bool)
+    assert np.array_equal(m, c["amask"])
+    assert max_rel(a1[0].cpu().numpy()[m], c["a1"][m], 1.0) <= 1e-9
+    assert max_rel(a2[0].cpu().numpy()[m], c["a2"][m], 1.0) <= 1e-9
+    assert np.isnan(a1[0].cpu().numpy()[~m]).all()
+
+
+@pytest.mark.parametrize("name", CCL)
+def test_passable_and_labels_golden(ccl_golden, cuda_dev, name):
+    from paper_2504_15121_b200 import device
+    c = ccl_golden[name]
+    rig = rig_of(c["rig"])
+    d = torch.from_numpy(c["d"]).to(cuda_dev, torch.float32)
+    e = torch.empty(d.shape, dtype=torch.float64, device=cuda_dev)
+    p, e = device.passable(d, rig, float(c["t"]), edges=e)
+    p = p[0].cpu().numpy().astype(bool)
+    e = e[0].cpu().numpy()
+    em = c["emask"]
+    assert np.array_equal(~np.isnan(e), em)
+    np.testing.assert_array_equal(e[em], c["edges"][em])  # bit-exact fp64
+    assert np.array_equal(p, c["passable"])
+    lab = device.component_labels(d, rig, float(c["t"]))[0].cpu().numpy()
+    assert np.array_equal(lab.astype(np.int64), c["labels"])
+    lab2 = device.labels_from_passable(torch.from_numpy(c["passable"]).to(cuda_dev))
+    assert np.array_equal(lab2[0].cpu().numpy().astype(np.int64), c["labels"])
+
+
+def test_reference_api_matches_golden(fixed_golden, cuda_dev):
+    import paper_2504_15121_b200 as sn
+    c = fixed_golden["street_holes_k9"]
+    rig = rig_of(c["rig"])
+    field = sn.ScalarField.from_array(c["d"])
+    nf = sn.estimate_normals_fixed(field, rig, 9)
+    assert np.array_equal(nf.mask, c["nmask"])
+    assert max_angle_deg(nf.vectors[nf.mask], c["normals"][nf.mask]) < ANGLE_TOL_DEG
+    aff = sn.convolve_affine(field, 9)
+    assert np.array_equal(aff.mask, c["amask"])
+    pts = sn.triangulate_grid(field, rig)
+    fin = np.isfinite(c["points"]).all(-1)
+    assert max_point_rel(pts[fin], c["points"][fin]) < POINT_TOL
+    est = sn.AffineNormalEstimator(rig, kernel_size=9)
+    out = est.fit_transform(c["d"])
+    assert np.array_equal(np.isfinite(out).all(-1), c["nmask"])
+
+
+def test_accuracy_anchor_sphere(cuda_dev):
+    """End to end vs the reference's own accuracy on pkg/scenes/sphere.scn
+    (acceptance criterion 4 inputs; golden from tests/golden/accuracy.json)."""
+    from pathlib import Path
+    from paper_2504_15121_b200 import device, scenes
+    gold = json.loads((Path(__file__).parent / "golden" / "accuracy.json").read_text())
+    sc = scenes.sphere_scene(1024, 1024, fx=1024.0)
+    disp, _, gtn = scenes.raycast(sc)
+    gtm = np.isfinite(gtn).all(-1)
+    for row in gold["rows"]:
+        d = scenes.add_gaussian_noise(disp, row["sigma"], 7).astype(np.float32)
+        out = device.oriented_points(torch.from_numpy(d).to(cuda_dev), sc.rig, row["k"])
+        n = out[0, ..., 3:].cpu().numpy().astype(np.float64)
+        ok = np.isfinite(n).all(-1) & gtm
+        assert int(ok.sum()) == row["valid_count"]
+        dot = np.abs(np.sum(n[ok] / np.linalg.norm(n[ok], axis=-1, keepdims=True) * gtn[ok], -1))
+        avg = float(np.degrees(np.arccos(np.clip(dot, 0, 1))).mean())
+        assert abs(avg - row["avg_deg"]) < 2e-4, (row, avg)
+
+
+def _oracle_record(d, sc_rig, k):
+    from oracle import stereonorm_oracle as orc
+    rig = orc.Rig(sc_rig.fx, sc_rig.fy, sc_rig.u0, sc_rig.v0, sc_rig.baseline)
+    rec, ok = orc.oriented_points(d.astype(np.float64), rig, k, threads=8)
+    return {"nmask": ok, "normals": rec[..., 3:], "points": rec[..., :3]}
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C1_noisy", "C3"])
+def test_configs_vs_oracle(cuda_dev, cfg):
+    from paper_2504_15121_b200 import device, scenes
+    from paper_2504_15121_b200.geometry import StereoRig
+    if cfg.startswith("C1"):
+        rig = StereoRig(640.0, 640.0, 319.5, 239.5, 0.3)
+        n = np.array([0.25, -0.4, -1.0])
+        disp, _ = scenes.plane_disparity(n, -5.0, rig, 640, 480)
+        if cfg == "C1_noisy":
+            disp = scenes.add_gaussian_noise(disp, 0.2, 7)
+    else:
+        sc = scenes.street_scene(2048, 1024)
+        rig = sc.rig
+        disp = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.2, 0)
+    d = disp.astype(np.float32)
+    mask = torch.empty((1,) + d.shape, dtype=torch.uint8, device=cuda_dev)
+    out = device.oriented_points(torch.from_numpy(d).to(cuda_dev), rig, 9, mask=mask)
+    _check_record(out[0].cpu().numpy(), mask[0].cpu().numpy(), _oracle_record(d, rig, 9))
+
+
+def test_batch_and_generic_agree(cuda_dev):
+    """Frame-batch invariance and fast-path == generic-path on a street batch."""
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(512, 256)
+    clean = scenes.raycast(sc)[0]
+    frames = np.stack([scenes.add_gaussian_noise(clean, 0.5, i) for i in range(4)])
+    frames[1, 100:110, 200:230] = np.nan
+    d = torch.from_numpy(frames.astype(np.float32)).to(cuda_dev)
+    batch = device.oriented_points(d, sc.rig, 9)
+    gen = device.oriented_points(d, sc.rig, 9, generic=True)
+    for i in range(4):
+        one = device.oriented_points(d[i], sc.rig, 9)
+        assert torch.equal(torch.nan_to_num(one[0], 7.0), torch.nan_to_num(batch[i], 7.0))
+    b = batch.cpu().numpy()
+    g = gen.cpu().numpy()
+    ok = np.isfinite(b[..., 3:]).all(-1)
+    assert np.array_equal(ok, np.isfinite(g[..., 3:]).all(-1))
+    assert max_angle_deg(b[ok][:, 3:], g[ok][:, 3:]) < 1e-5
+
+
+def test_labels_large_vs_oracle(cuda_dev):
+    """C4-style CCL stress frame (sigma 1 + dilated holes) vs the oracle."""
+    from scipy import ndimage
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(2048, 1024)
+    d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 1.0, 3)
+    holes = ndimage.binary_dilation(np.random.default_rng(1003).random(d.shape) < 0.002,
+                                    iterations=3)
+    d[holes] = np.nan
+    d = d.astype(np.float32)
+    rig = orc.Rig(sc.rig.fx, sc.rig.fy, sc.rig.u0, sc.rig.v0, sc.rig.baseline)
+    dt = torch.from_numpy(d).to(cuda_dev)
+    for t in (0.05, 0.2, 1.0):
+        lab = device.component_labels(dt, sc.rig, t)[0].cpu().numpy().astype(np.int64)
+        ref = orc.ccl_labels(d.astype(np.float64), rig, t)
+        assert np.array_equal(lab, ref), t
