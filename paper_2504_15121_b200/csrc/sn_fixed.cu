@@ -53,21 +53,20 @@ __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + 
 
 template <int R, typename T>
 struct FastCfg {
-  static constexpr int NC = kTW + 2 * R;
-  static constexpr int NR = kG + 2 * R;
+  static constexpr int NC = kTW + 2 * R;  // C/Rr columns (output columns + halo)
+  static constexpr int NR = kG + 2 * R;   // input rows per item
   static constexpr int AE = 16 / (int)sizeof(T);
   // the box starts at (x0 - R) rounded down to 16 B, so it spans up to AE-1 extra columns
   static constexpr int BW = (NC + AE - 1 + AE - 1) / AE * AE;
   static constexpr size_t STAGE = 0;
   static constexpr size_t STAGE_BYTES = (size_t)kBoxes * kG * 128;
-  static constexpr size_t IN = STAGE + STAGE_BYTES;
   static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
-  static constexpr size_t CS = align_up(IN + IN_BYTES, 128);
+  static constexpr size_t IN0 = STAGE + STAGE_BYTES;
+  static constexpr size_t IN1 = align_up(IN0 + IN_BYTES, 128);
+  static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);
   static constexpr size_t CS_BYTES = (size_t)NC * kCP * 8;
   static constexpr size_t RS = CS + CS_BYTES;
-  static constexpr size_t DC = RS + CS_BYTES;
-  static constexpr size_t DC_BYTES = (size_t)kTW * kCP * sizeof(T);
-  static constexpr size_t FL = align_up(DC + DC_BYTES, 16);
+  static constexpr size_t FL = align_up(RS + CS_BYTES, 16);
   static constexpr size_t BAR = align_up(FL + NC * 4, 16);
   static constexpr size_t TOTAL = BAR + 16 + 1024;  // + slack for 1024-B alignment
   static_assert(NC <= kFastThreads, "pass V needs one lane per column");
@@ -85,113 +84,135 @@ __device__ __forceinline__ bool finite_t<float>(float v) {
 
 // ---------------------------------------------------------------------------
 // fast path: centred square pattern, radius R
+//
+// Per item (128 columns x 16 rows of one frame):
+//   pass V  lane <-> input column (128 + 2R lanes): C, Rr for the 16 output
+//           rows as two independent 8-row sliding chains -> smem, column-major
+//           (pitch 17 doubles: conflict-free for both passes)
+//   pass H  lane <-> (output row, run of 16 columns): U, V as two independent
+//           8-column sliding chains, closed-form normal + point, 6 floats per
+//           pixel into the 128B-swizzled staging tile
+// The input tile is double-buffered: the TMA load of item i+1 is in flight
+// during all of item i.
 
 template <int R, typename T>
 __global__ void __launch_bounds__(kFastThreads, 2)
     fixed_square_kernel(const __grid_constant__ CUtensorMap in_map,
                         const __grid_constant__ CUtensorMap out_map, const FixedParams p,
-                        uint8_t* __restrict__ mask_out, const int64_t n_items, const int tiles_x,
+                        uint8_t* __restrict__ mask_out, const int n_items, const int tiles_x,
                         const int tiles_y) {
   using Cfg = FastCfg<R, T>;
-  constexpr int NC = Cfg::NC, NR = Cfg::NR, BW = Cfg::BW;
+  constexpr int NC = Cfg::NC, NR = Cfg::NR, BW = Cfg::BW, AE = Cfg::AE;
   constexpr int NWIN = 2 * R + 1;
-  constexpr int NH = kG + 2 * R;  // columns read per pass-H run (run = 16 outputs)
+  constexpr int NH = 16 + 2 * R;  // C/Rr columns read per pass-H run (16 outputs)
+  constexpr int HG = kG / 2;      // rows per pass-V chain
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  T* in = reinterpret_cast<T*>(smem + Cfg::IN);
   double* Cs = reinterpret_cast<double*>(smem + Cfg::CS);
   double* Rs = reinterpret_cast<double*>(smem + Cfg::RS);
-  T* Dc = reinterpret_cast<T*>(smem + Cfg::DC);
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
   const uint32_t stage_base = smem_u32(smem + Cfg::STAGE);
   const int tid = threadIdx.x;
+  const int W = (int)p.W, H = (int)p.H;
 
-  int64_t item = blockIdx.x;
+  int item = blockIdx.x;
   if (item >= n_items) return;
+
+  // TMA tile origin: the halo origin with its innermost coordinate rounded
+  // down to a 16-byte multiple (an unaligned innermost TMA coordinate raises
+  // an illegal-instruction fault on this part -- measured with
+  // tools/ubench/tma_probe.cu).  Negative aligned coordinates are fine; the
+  // samples outside the image are masked by coordinate in pass V, which
+  // reproduces the no-padding border rule kernels.py:166-176.
+  auto tile_x = [](int x0) { return ((x0 - R) & ~(AE - 1)); };  // floor to AE (two's complement)
+  auto decode = [&](int it, int& x0, int& y0, int& bz) {
+    const unsigned u = (unsigned)it;
+    const unsigned r = u / (unsigned)tiles_x;
+    x0 = (int)(u - r * (unsigned)tiles_x) * kTW;
+    const unsigned f = r / (unsigned)tiles_y;
+    y0 = (int)(r - f * (unsigned)tiles_y) * kG;
+    bz = (int)f;
+  };
+  auto load_tile = [&](int it, int buf) {
+    int x0, y0, bz;
+    decode(it, x0, y0, bz);
+    T* dst = reinterpret_cast<T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
+    mbar_arrive_expect_tx(bar + buf, (uint32_t)Cfg::IN_BYTES);
+    tma_load_3d(dst, &in_map, bar + buf, tile_x(x0), y0 - R, bz);
+  };
 
   if (tid == 0) {
     tma_prefetch_desc(&in_map);
     tma_prefetch_desc(&out_map);
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_mbar_init();
+    load_tile(item, 0);
   }
   __syncthreads();
 
-  auto decode = [&](int64_t it, int& x0, int& y0, int& bz) {
-    const int tx = (int)(it % tiles_x);
-    const int64_t r = it / tiles_x;
-    x0 = tx * kTW;
-    y0 = (int)(r % tiles_y) * kG;
-    bz = (int)(r / tiles_y);
-  };
-
-  // TMA tile origin: the halo origin with its innermost coordinate rounded
-  // down to a 16-byte multiple (an unaligned innermost TMA coordinate raises
-  // an illegal-instruction fault on this part -- measured, tools/ubench/
-  // tma_probe.cu).  Negative (aligned) coordinates are fine.  Pass V masks
-  // out-of-image samples by coordinate, which reproduces the no-padding
-  // border rule kernels.py:166-176.
-  constexpr int AE = Cfg::AE;
-  auto tile_x = [](int x0) { return (int)floorf((float)(x0 - R) / (float)AE) * AE; };
-  auto load_tile = [&](int x0, int y0, int bz) {
-    mbar_arrive_expect_tx(bar, (uint32_t)Cfg::IN_BYTES);
-    tma_load_3d(in, &in_map, bar, tile_x(x0), y0 - R, bz);
-  };
-  if (tid == 0) {
+  for (int it = 0; item < n_items; ++it, item += gridDim.x) {
+    const int buf = it & 1;
+    if (tid == 0 && item + (int)gridDim.x < n_items) load_tile(item + gridDim.x, buf ^ 1);
     int x0, y0, bz;
     decode(item, x0, y0, bz);
-    load_tile(x0, y0, bz);
-  }
-
-  uint32_t phase = 0;
-  for (; item < n_items; item += gridDim.x) {
-    int x0, y0, bz;
-    decode(item, x0, y0, bz);
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-    const int ox = tile_x(x0) - (x0 - R);  // logical column c <-> smem column c - ox (ox <= 0)
-    constexpr int oy = 0;
+    const int sh = (x0 - R) - tile_x(x0);  // logical column c <-> smem column c + sh
+    const T* in = reinterpret_cast<const T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
+    mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
     // ------------------------------------------------------------ pass V
     if (tid < NC) {
       const int c = tid;
-      const int gxc = x0 - R + c;
-      const bool col_ok = gxc >= 0 && gxc < p.W;
-      const T* col = in + (c - ox);
-      const int gy0 = y0 - R;
+      const int gx = x0 - R + c;
+      // rows of the item inside the image
+      const int lo = max(0, R - y0), hi = min(NR, H - y0 + R);
+      uint32_t inside = 0;
+      if ((unsigned)gx < (unsigned)W && hi > lo)
+        inside = (uint32_t)(((1ull << (hi - lo)) - 1ull) << lo);
+      const T* col = in + c + sh;
       double v[NR];
-      uint32_t invb = 0;
+      uint32_t fin = 0;
       bool big = false;
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
-        const bool in_img = col_ok && (gy0 + i) >= 0 && (gy0 + i) < p.H;
-        const T raw = in_img ? col[(i - oy) * BW] : (T)0;
-        const bool f = in_img && finite_t(raw);
-        invb |= (f ? 0u : 1u) << i;
+        const T raw = col[i * BW];
+        const bool f = finite_t(raw);
+        fin |= (f ? 1u : 0u) << i;
         const double dv = f ? (double)raw : 0.0;
         big |= fabs(dv) > kBig;
         v[i] = dv;
       }
+      const uint32_t invb = ~(fin & inside);
       double* cs = Cs + c * kCP;
       double* rs = Rs + c * kCP;
       if (!big) {
-        double C = 0.0, Rr = 0.0;
+        // two independent sliding chains (rows 0..7, 8..15) for ILP
+        double C0 = 0.0, R0 = 0.0, C1 = 0.0, R1 = 0.0;
 #pragma unroll
         for (int j = 0; j < NWIN; ++j) {
-          C += v[j];
-          Rr = fma((double)(j - R), v[j], Rr);
+          C0 += v[j];
+          R0 = fma((double)(j - R), v[j], R0);
+          C1 += v[HG + j];
+          R1 = fma((double)(j - R), v[HG + j], R1);
         }
-        cs[0] = C;
-        rs[0] = Rr;
+        cs[0] = C0;
+        rs[0] = R0;
+        cs[HG] = C1;
+        rs[HG] = R1;
 #pragma unroll
-        for (int g = 1; g < kG; ++g) {
-          const double vin = v[g + 2 * R], vout = v[g - 1];
-          C += vin - vout;
-          Rr = fma((double)R, vout, fma((double)(R + 1), vin, Rr - C));
-          cs[g] = C;
-          rs[g] = Rr;
+        for (int g = 1; g < HG; ++g) {
+          const double i0 = v[g + 2 * R], o0 = v[g - 1];
+          const double i1 = v[HG + g + 2 * R], o1 = v[HG + g - 1];
+          C0 += i0 - o0;
+          C1 += i1 - o1;
+          R0 = fma((double)R, o0, fma((double)(R + 1), i0, R0 - C0));
+          R1 = fma((double)R, o1, fma((double)(R + 1), i1, R1 - C1));
+          cs[g] = C0;
+          rs[g] = R0;
+          cs[HG + g] = C1;
+          rs[HG + g] = R1;
         }
       } else {
 #pragma unroll
@@ -210,24 +231,9 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 #pragma unroll
       for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
       fl[c] = (acc & 0xFFFFu) | (big ? 0x80000000u : 0u);
-      if (c >= R && c < R + kTW) {
-        T* dc = Dc + (c - R) * kCP;
-#pragma unroll
-        for (int g = 0; g < kG; ++g) dc[g] = col[(g + R - oy) * BW];
-      }
     }
     if (tid == 0) bulk_wait_read0();  // staging of the previous item consumed by TMA
     __syncthreads();
-
-    // input tile consumed: prefetch the next item while pass H runs
-    if (tid == 0) {
-      const int64_t nxt = item + gridDim.x;
-      if (nxt < n_items) {
-        int nx0, ny0, nbz;
-        decode(nxt, nx0, ny0, nbz);
-        load_tile(nx0, ny0, nbz);
-      }
-    }
 
     // ------------------------------------------------------------ pass H + epilogue
     if (tid < kTW) {
@@ -254,76 +260,106 @@ __global__ void __launch_bounds__(kFastThreads, 2)
       const double dv = (double)yg - p.v0;
       const float dv_f = ((float)yg - p.v0_hi) - p.v0_lo;
       const double du0 = (double)xb - p.u0;
-      const T* dcp = Dc + colbase * kCP + g;
-      const double alpha = p.alpha;
+      const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
       const uint32_t gsw = (uint32_t)(g & 7);
       const uint32_t rowaddr = stage_base + (uint32_t)g * 128u;
+      uint32_t validbits = 0;
 
-      double Box = 0.0, U = 0.0, V = 0.0;
+      // two sliding chains: outputs 0..7 (A) and 8..15 (B)
+      double BA = 0.0, UA = 0.0, VA = 0.0, BB = 0.0, UB = 0.0, VB = 0.0;
       if (!big) {
 #pragma unroll
         for (int j = 0; j < NWIN; ++j) {
-          Box += cc[j];
-          U = fma((double)(j - R), cc[j], U);
-          V += rr[j];
+          BA += cc[j];
+          UA = fma((double)(j - R), cc[j], UA);
+          VA += rr[j];
+          BB += cc[8 + j];
+          UB = fma((double)(j - R), cc[8 + j], UB);
+          VB += rr[8 + j];
         }
       }
-      float o[12];
+      float o[2][12];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < 8; ++j) {
+        double U2[2], V2[2];
         if (!big) {
           if (j > 0) {
-            const double cin = cc[j + 2 * R], cout = cc[j - 1];
-            Box += cin - cout;
-            U = fma((double)R, cout, fma((double)(R + 1), cin, U - Box));
-            V += rr[j + 2 * R] - rr[j - 1];
+            {
+              const double cin = cc[j + 2 * R], cout = cc[j - 1];
+              BA += cin - cout;
+              UA = fma((double)R, cout, fma((double)(R + 1), cin, UA - BA));
+              VA += rr[j + 2 * R] - rr[j - 1];
+            }
+            {
+              const double cin = cc[8 + j + 2 * R], cout = cc[8 + j - 1];
+              BB += cin - cout;
+              UB = fma((double)R, cout, fma((double)(R + 1), cin, UB - BB));
+              VB += rr[8 + j + 2 * R] - rr[8 + j - 1];
+            }
           }
+          U2[0] = UA;
+          V2[0] = VA;
+          U2[1] = UB;
+          V2[1] = VB;
         } else {
-          U = 0.0;
-          V = 0.0;
 #pragma unroll
-          for (int i = 0; i < NWIN; ++i) {
-            U = fma((double)(i - R), cc[j + i], U);
-            V += rr[j + i];
-          }
-        }
-        const T dcv = dcp[j * kCP];
-        const bool valid = (((win >> j) & 1u) == 0u) && (dcv > (T)0);
-        float px, py, pz, nx, ny, nz;
-        const int xg = xb + j;
-        const float du_f = ((float)xg - p.u0_hi) - p.u0_lo;
-        if constexpr (sizeof(T) == 4) {
-          point_from_disparity((float)dcv, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
-        } else {
-          point_from_disparity_f64((double)dcv, (double)xg - p.u0, dv, p, px, py, pz);
-        }
-        if (valid) {
-          normal_from_moments(U, V, alpha, (double)dcv, du0 + (double)j, dv, p.fx, p.fy, nx, ny, nz);
-        } else {
-          nx = ny = nz = __int_as_float(0x7fc00000);
-        }
-        const int s = (j & 1) * 6;
-        o[s + 0] = px;
-        o[s + 1] = py;
-        o[s + 2] = pz;
-        o[s + 3] = nx;
-        o[s + 4] = ny;
-        o[s + 5] = nz;
-        if (j & 1) {
-          // pixels (j-1, j) = 12 floats = 3 chunks of the 128B-swizzled staging row
-          const int K = q * 24 + (j >> 1) * 3;  // chunk index within the 768-float tile row
+          for (int h = 0; h < 2; ++h) {
+            double U = 0.0, V = 0.0;
 #pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            const int kk = K + t;
-            const uint32_t box = (uint32_t)(kk >> 3);
-            const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
-            st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[4 * t], o[4 * t + 1],
-                         o[4 * t + 2], o[4 * t + 3]);
+            for (int i = 0; i < NWIN; ++i) {
+              U = fma((double)(i - R), cc[8 * h + j + i], U);
+              V += rr[8 * h + j + i];
+            }
+            U2[h] = U;
+            V2[h] = V;
           }
         }
-        if (mask_out != nullptr && yg < p.H && xg < p.W) {
-          mask_out[((int64_t)bz * p.H + yg) * p.W + xg] = valid ? 1 : 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int jj = 8 * h + j;
+          const T dcv = drow[jj];
+          const bool valid = (((win >> jj) & 1u) == 0u) && (dcv > (T)0);
+          validbits |= (valid ? 1u : 0u) << jj;
+          float px, py, pz, nx, ny, nz;
+          const int xg = xb + jj;
+          if constexpr (sizeof(T) == 4) {
+            const float du_f = ((float)xg - p.u0_hi) - p.u0_lo;
+            point_from_disparity((float)dcv, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py,
+                                 pz);
+          } else {
+            point_from_disparity_f64((double)dcv, (double)xg - p.u0, dv, p, px, py, pz);
+          }
+          if (valid) {
+            normal_from_moments(U2[h], V2[h], p.alpha, (double)dcv, du0 + (double)jj, dv, p.fx,
+                                p.fy, nx, ny, nz);
+          } else {
+            nx = ny = nz = __int_as_float(0x7fc00000);
+          }
+          const int s6 = (jj & 1) * 6;
+          o[h][s6 + 0] = px;
+          o[h][s6 + 1] = py;
+          o[h][s6 + 2] = pz;
+          o[h][s6 + 3] = nx;
+          o[h][s6 + 4] = ny;
+          o[h][s6 + 5] = nz;
+          if (jj & 1) {
+            // pixels (jj-1, jj) = 12 floats = 3 chunks of the 128B-swizzled staging row
+            const int K = q * 24 + (jj >> 1) * 3;  // chunk index within the 768-float tile row
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              const int kk = K + t;
+              const uint32_t box = (uint32_t)(kk >> 3);
+              const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
+              st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[h][4 * t],
+                           o[h][4 * t + 1], o[h][4 * t + 2], o[h][4 * t + 3]);
+            }
+          }
         }
+      }
+      if (mask_out != nullptr && yg < H) {
+        uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
+#pragma unroll 1
+        for (int j = 0; j < 16 && xb + j < W; ++j) mrow[j] = (uint8_t)((validbits >> j) & 1u);
       }
     }
     fence_proxy_async_smem();
@@ -449,7 +485,9 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
   }
   const int tiles_x = (int)((p.W + kTW - 1) / kTW);
   const int tiles_y = (int)((p.H + kG - 1) / kG);
-  const int64_t n_items = (int64_t)tiles_x * tiles_y * p.B;
+  const int64_t n_items64 = (int64_t)tiles_x * tiles_y * p.B;
+  if (n_items64 >= 0x7fffffffLL) return -1;  // generic path handles absurd batches
+  const int n_items = (int)n_items64;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFastThreads, Cfg::TOTAL) !=
       cudaSuccess)
