@@ -13,7 +13,7 @@
 // the component.  Union-find where every link goes from the larger index to
 // the smaller (atomicMin), so a tree's root is always its minimum element and
 // the result is independent of scheduling:
-//   1. ccl_local: 32x32 tile in shared memory -- each warp owns a tile row,
+//   1. ccl_local: 32x64 tile in shared memory -- each warp owns a tile row,
 //      __ballot_sync gives the passable bits of the row and every pixel links
 //      to the first pixel of its horizontal run (no atomics), then rows are
 //      merged with the pixels above (3 candidates, redundant unions pruned);
@@ -80,28 +80,35 @@ __global__ void passable_kernel(const float* __restrict__ disp, const CclParams 
 // ---------------------------------------------------------------------------
 // union-find helpers (indices only ever point to smaller indices)
 
-__device__ __forceinline__ int uf_find(const int32_t* L, int x) {
-  int px = L[x];
-  while (px != x) {
-    x = px;
-    px = L[x];
+// find with path halving: every write replaces a parent by an ancestor, so it
+// commutes with concurrent unions (which only atomicMin roots)
+__device__ __forceinline__ int uf_find(volatile int32_t* L, int x) {
+  while (true) {
+    const int p = L[x];
+    if (p == x) return x;
+    const int gp = L[p];
+    if (gp == p) return p;
+    L[x] = gp;
+    x = gp;
   }
-  return x;
 }
 
-__device__ __forceinline__ int uf_find_vol(volatile int32_t* L, int x) {
-  int px = L[x];
-  while (px != x) {
-    x = px;
-    px = L[x];
+// read-only find: used where concurrent writers store final roots (flatten),
+// so a late path-halving store can never overwrite a root with an ancestor
+__device__ __forceinline__ int uf_root(const volatile int32_t* L, int x) {
+  int p = L[x];
+  while (p != x) {
+    x = p;
+    p = L[x];
   }
   return x;
 }
 
 __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
+  volatile int32_t* V = L;
   while (true) {
-    a = uf_find_vol(L, a);
-    b = uf_find_vol(L, b);
+    a = uf_find(V, a);
+    b = uf_find(V, b);
     if (a == b) return;
     if (a > b) {
       const int t = a;
@@ -116,63 +123,74 @@ __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
 
 // ---------------------------------------------------------------------------
 // 1. tile-local labelling (+ fused predicate when disp != nullptr)
+//
+// Tile = 32 columns x 64 rows; warp w owns rows w, w+8, ..., lane = column.
+
+constexpr int kTY = 64;                 // CCL tile rows (kCT = 32 columns)
+constexpr int kZW = kCT + 2, kZH = kTY + 2;
+constexpr int kRowsPerWarp = kTY / (kCclThreads / 32);
 
 __global__ void __launch_bounds__(kCclThreads)
     ccl_local_kernel(const float* __restrict__ disp, const uint8_t* __restrict__ pas_in,
                      const CclParams p, int32_t* __restrict__ labels) {
-  __shared__ double zs[(kCT + 2) * (kCT + 2)];
-  __shared__ int32_t L[kCT * kCT];
-  __shared__ uint32_t rowbits[kCT];
+  __shared__ double zs[kZH * kZW];
+  __shared__ int32_t L[kTY * kCT];
+  __shared__ uint32_t rowbits[kTY];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int64_t x0 = (int64_t)blockIdx.x * kCT, y0 = (int64_t)blockIdx.y * kCT;
+  const int W = (int)p.W, H = (int)p.H;
+  const int x0 = blockIdx.x * kCT, y0 = blockIdx.y * kTY;
   const int64_t fbase = (int64_t)blockIdx.z * p.H * p.W;
   if (disp) {
     const float* f = disp + fbase;
-    for (int i = tid; i < (kCT + 2) * (kCT + 2); i += kCclThreads) {
-      const int64_t gx = x0 - 1 + i % (kCT + 2), gy = y0 - 1 + i / (kCT + 2);
+    for (int i = tid; i < kZH * kZW; i += kCclThreads) {
+      const int iy = i / kZW, ix = i - iy * kZW;
+      const int gx = x0 - 1 + ix, gy = y0 - 1 + iy;
       double z = __longlong_as_double(0x7ff8000000000000ll);
-      if (gx >= 0 && gx < p.W && gy >= 0 && gy < p.H) z = depth_of(f[gy * p.W + gx], p.fxb);
+      if ((unsigned)gx < (unsigned)W && (unsigned)gy < (unsigned)H)
+        z = depth_of(f[(int64_t)gy * W + gx], p.fxb);
       zs[i] = z;
     }
     __syncthreads();
   }
-  bool P[4];
+  uint32_t Pbits = 0;  // bit k: pixel (warp + 8k, lane) passable
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int ly = warp + 8 * k, lx = lane;
-    const int64_t gx = x0 + lx, gy = y0 + ly;
+  for (int k = 0; k < kRowsPerWarp; ++k) {
+    const int ly = warp + 8 * k;
+    const int gx = x0 + lane, gy = y0 + ly;
     bool pk = false;
     if (disp) {
-      if (gx >= 1 && gx + 1 < p.W && gy >= 1 && gy + 1 < p.H) {
-        const int zi = (ly + 1) * (kCT + 2) + lx + 1;
-        const double c = zs[zi], l = zs[zi - 1], r = zs[zi + 1], u = zs[zi - (kCT + 2)],
-                     dn = zs[zi + (kCT + 2)];
+      if (gx >= 1 && gx + 1 < W && gy >= 1 && gy + 1 < H) {
+        const int zi = (ly + 1) * kZW + lane + 1;
+        const double c = zs[zi], l = zs[zi - 1], r = zs[zi + 1], u = zs[zi - kZW],
+                     dn = zs[zi + kZW];
         if (valid_z(c) && valid_z(l) && valid_z(r) && valid_z(u) && valid_z(dn))
           pk = edge_value(c, l, r, u, dn) <= p.t;
       }
-    } else if (gx < p.W && gy < p.H) {
-      pk = pas_in[fbase + gy * p.W + gx] != 0;
+    } else if (gx < W && gy < H) {
+      pk = pas_in[fbase + (int64_t)gy * W + gx] != 0;
     }
-    P[k] = pk;
+    Pbits |= (pk ? 1u : 0u) << k;
     const uint32_t b = __ballot_sync(0xffffffffu, pk);
     const uint32_t starts = b & ~(b << 1);
-    const uint32_t upto = starts & (0xffffffffu >> (31 - lx));
-    L[ly * kCT + lx] = pk ? ly * kCT + (31 - __clz(upto)) : -1;
+    const uint32_t upto = starts & (0xffffffffu >> (31 - lane));
+    L[ly * kCT + lane] = pk ? ly * kCT + (31 - __clz(upto)) : -1;
     if (lane == 0) rowbits[ly] = b;
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int ly = warp + 8 * k, lx = lane;
-    if (!P[k] || ly == 0) continue;
+  for (int k = 0; k < kRowsPerWarp; ++k) {
+    const int ly = warp + 8 * k;
+    if (!((Pbits >> k) & 1u) || ly == 0) continue;
     const uint32_t b = rowbits[ly], up = rowbits[ly - 1];
-    const bool left = lx > 0 && ((b >> (lx - 1)) & 1u);
-    const bool right = lx < 31 && ((b >> (lx + 1)) & 1u);
-    const bool u = (up >> lx) & 1u;
-    const bool ul = lx > 0 && ((up >> (lx - 1)) & 1u);
-    const bool ur = lx < 31 && ((up >> (lx + 1)) & 1u);
-    const int i = ly * kCT + lx;
+    const bool left = lane > 0 && ((b >> (lane - 1)) & 1u);
+    const bool right = lane < 31 && ((b >> (lane + 1)) & 1u);
+    const bool u = (up >> lane) & 1u;
+    const bool ul = lane > 0 && ((up >> (lane - 1)) & 1u);
+    const bool ur = lane < 31 && ((up >> (lane + 1)) & 1u);
+    const int i = ly * kCT + lane;
+    // a run shares its connections: only the pixels whose upper neighbours are
+    // not already reached through the horizontal neighbour do the union
     if (u) {
       if (!(left && ul)) uf_unite(L, i, i - kCT);
     } else {
@@ -182,59 +200,71 @@ __global__ void __launch_bounds__(kCclThreads)
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int ly = warp + 8 * k, lx = lane;
-    const int64_t gx = x0 + lx, gy = y0 + ly;
-    if (gx >= p.W || gy >= p.H) continue;
+  for (int k = 0; k < kRowsPerWarp; ++k) {
+    const int ly = warp + 8 * k;
+    const int gx = x0 + lane, gy = y0 + ly;
+    if (gx >= W || gy >= H) continue;
     int32_t out = -1;
-    if (P[k]) {
-      const int root = uf_find(L, ly * kCT + lx);
-      out = (int32_t)((y0 + root / kCT) * p.W + x0 + root % kCT);
+    if ((Pbits >> k) & 1u) {
+      const int root = uf_find(L, ly * kCT + lane);
+      out = (y0 + (root >> 5)) * W + x0 + (root & 31);
     }
-    labels[fbase + gy * p.W + gx] = out;
+    labels[fbase + (int64_t)gy * W + gx] = out;
   }
 }
 
 // ---------------------------------------------------------------------------
-// 2. merge across tile edges
+// 2. merge across tile edges (global union-find on the label array)
+//
+// One thread per pixel on the first column / first row of a tile (except the
+// image's own first column / row).  Same pruning as the in-tile rule: the
+// pixel unites with its straight neighbour across the edge if passable, else
+// with the diagonal ones not already reached through its along-edge neighbour.
 
-__global__ void ccl_merge_kernel(const CclParams p, int32_t* __restrict__ labels, int64_t n_col,
-                                 int64_t n_row) {
-  const int64_t per_frame = n_col + n_row;
-  const int64_t total = per_frame * p.B;
-  const int64_t tiles_x = (p.W + kCT - 1) / kCT;
+__global__ void ccl_merge_kernel(const CclParams p, int32_t* __restrict__ labels, int n_col,
+                                 int n_row) {
+  const int W = (int)p.W, H = (int)p.H;
+  const int per_frame = n_col + n_row;
+  const int64_t total = (int64_t)per_frame * p.B;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = idx / per_frame;
-    int64_t r = idx % per_frame;
-    int32_t* L = labels + f * p.H * p.W;
-    int64_t x, y;
+    const int f = (int)(idx / per_frame);
+    int r = (int)(idx - (int64_t)f * per_frame);
+    int32_t* L = labels + (int64_t)f * p.H * p.W;
+    volatile int32_t* V = L;
     if (r < n_col) {
-      // vertical tile edges: x = k*32, k >= 1; neighbours at x-1, rows y-1..y+1
-      y = r % p.H;
-      x = (r / p.H + 1) * kCT;
-      const int64_t i = y * p.W + x;
-      if (L[i] < 0) continue;
-      for (int dy = -1; dy <= 1; ++dy) {
-        const int64_t yy = y + dy;
-        if (yy < 0 || yy >= p.H) continue;
-        const int64_t j = yy * p.W + x - 1;
-        if (L[j] >= 0) uf_unite(L, (int)i, (int)j);
+      // vertical tile edge at x = (r / H + 1) * 32; across-edge neighbours at x - 1
+      const int y = r % H;
+      const int x = (r / H + 1) * kCT;
+      const int i = y * W + x;
+      if (V[i] < 0) continue;
+      // pruning may only lean on an along-edge neighbour of the SAME tile
+      // (already connected by ccl_local); across a tile corner both links stay
+      const bool up_same = (y % kTY) != 0, down_same = ((y + 1) % kTY) != 0;
+      if (V[i - 1] >= 0) {
+        if (!(up_same && V[i - W] >= 0 && V[i - W - 1] >= 0)) uf_unite(L, i, i - 1);
+      } else {
+        if (y > 0 && V[i - W - 1] >= 0 && !(up_same && V[i - W] >= 0)) uf_unite(L, i, i - W - 1);
+        if (y + 1 < H && V[i + W - 1] >= 0 && !(down_same && V[i + W] >= 0))
+          uf_unite(L, i, i + W - 1);
       }
     } else {
+      // horizontal tile edge at y = (r / W + 1) * kTY; neighbours in row y - 1
       r -= n_col;
-      x = r % p.W;
-      y = (r / p.W + 1) * kCT;
-      const int64_t i = y * p.W + x;
-      if (L[i] < 0) continue;
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int64_t xx = x + dx;
-        if (xx < 0 || xx >= p.W) continue;
-        const int64_t j = (y - 1) * p.W + xx;
-        if (L[j] >= 0) uf_unite(L, (int)i, (int)j);
+      const int x = r % W;
+      const int y = (r / W + 1) * kTY;
+      const int i = y * W + x;
+      if (V[i] < 0) continue;
+      const bool left_same = (x % kCT) != 0, right_same = ((x + 1) % kCT) != 0;
+      const bool left = x > 0 && V[i - 1] >= 0;
+      const bool right = x + 1 < W && V[i + 1] >= 0;
+      if (V[i - W] >= 0) {
+        if (!(left_same && left && V[i - W - 1] >= 0)) uf_unite(L, i, i - W);
+      } else {
+        if (x > 0 && V[i - W - 1] >= 0 && !(left_same && left)) uf_unite(L, i, i - W - 1);
+        if (x + 1 < W && V[i - W + 1] >= 0 && !(right_same && right)) uf_unite(L, i, i - W + 1);
       }
     }
-    (void)tiles_x;
   }
 }
 
@@ -249,7 +279,7 @@ __global__ void ccl_flatten_kernel(const CclParams p, int32_t* __restrict__ labe
     int32_t* L = labels + (idx / HW) * HW;
     const int i = (int)(idx % HW);
     const int v = L[i];
-    if (v >= 0 && v != i) L[i] = uf_find(L, v);
+    if (v >= 0 && v != i) L[i] = uf_root(L, v);
   }
 }
 
@@ -313,14 +343,14 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
   const int64_t n = p.B * p.H * p.W;
   if (n == 0) return SN_OK;
   if (p.H * p.W > 0x7fffffffLL || p.B > 65535) return set_error(SN_EINVAL, "frame too large for int32 labels");
-  dim3 grid((unsigned)((p.W + kCT - 1) / kCT), (unsigned)((p.H + kCT - 1) / kCT), (unsigned)p.B);
+  dim3 grid((unsigned)((p.W + kCT - 1) / kCT), (unsigned)((p.H + kTY - 1) / kTY), (unsigned)p.B);
   ccl_local_kernel<<<grid, kCclThreads, 0, ctx.stream>>>(disp, pas, p, labels);
   int rc = check_launch("ccl_local_kernel");
   if (rc) return rc;
-  const int64_t n_col = ((p.W - 1) / kCT) * p.H;
-  const int64_t n_row = ((p.H - 1) / kCT) * p.W;
+  const int n_col = (int)(((p.W - 1) / kCT) * p.H);
+  const int n_row = (int)(((p.H - 1) / kTY) * p.W);
   if (n_col + n_row > 0) {
-    ccl_merge_kernel<<<grid_for(ctx, (n_col + n_row) * p.B, 256), 256, 0, ctx.stream>>>(
+    ccl_merge_kernel<<<grid_for(ctx, (int64_t)(n_col + n_row) * p.B, 256), 256, 0, ctx.stream>>>(
         p, labels, n_col, n_row);
     rc = check_launch("ccl_merge_kernel");
     if (rc) return rc;

@@ -200,3 +200,18 @@ def test_labels_large_vs_oracle(cuda_dev):
         lab = device.component_labels(dt, sc.rig, t)[0].cpu().numpy().astype(np.int64)
         ref = orc.ccl_labels(d.astype(np.float64), rig, t)
         assert np.array_equal(lab, ref), t
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (5, 7), (64, 32), (65, 33), (130, 97), (300, 517),
+                                   (1024, 2048)])
+@pytest.mark.parametrize("density", [0.3, 0.55, 0.62, 0.9])
+def test_labeller_random_grids(cuda_dev, shape, density):
+    """Labeller alone on random passable grids (percolation-critical
+    densities produce long, tile-crossing components)."""
+    from oracle.stereonorm_oracle import label_components
+    from paper_2504_15121_b200 import device
+    rng = np.random.default_rng(hash((shape, density)) % 2**32)
+    p = rng.random((3,) + shape) < density
+    lab = device.labels_from_passable(torch.from_numpy(p).to(cuda_dev)).cpu().numpy()
+    for i in range(3):
+        assert np.array_equal(lab[i].astype(np.int64), label_components(p[i]))
