@@ -114,16 +114,27 @@ __device__ __forceinline__ void normal_from_moments(double P1, double P2, double
                                                     float& nx, float& ny, float& nz) {
   const double ax = -P1 * fx;
   const double ay = -P2 * fy;
-  const double az = fma(P2, dv, fma(P1, du, -det * d));
-  const double s = fma(ax, ax, fma(ay, ay, az * az));
-  // MUFU rsqrt approximation + one Newton step (~1e-14 relative); the
-  // direction does not depend on it, only the unit length does
-  double inv;
-  asm("rsqrt.approx.f64 %0, %1;" : "=d"(inv) : "d"(s));
-  inv = inv * fma(-0.5 * s * inv, inv, 1.5);
-  nx = static_cast<float>(ax * inv);
-  ny = static_cast<float>(ay * inv);
-  nz = static_cast<float>(az * inv);
+  const double az = fma(P2, dv, fma(P1, du, -det * d));  // the cancelling component, in fp64
+  // fp32 normalisation of the fp64-rounded components: the direction keeps
+  // ~1e-7 relative accuracy (~6e-6 deg); out-of-range magnitudes take the
+  // fp64 path so no input can overflow or underflow the fp32 squares
+  const float fxv = (float)ax, fyv = (float)ay, fzv = (float)az;
+  const float s = fmaf(fxv, fxv, fmaf(fyv, fyv, fzv * fzv));
+  if (s > 1e-30f && s < 1e30f) {
+    float r = rsqrtf(s);
+    r = r * fmaf(-0.5f * s * r, r, 1.5f);  // one Newton step: ~1 ulp
+    nx = fxv * r;
+    ny = fyv * r;
+    nz = fzv * r;
+  } else {
+    const double s64 = fma(ax, ax, fma(ay, ay, az * az));
+    double inv;
+    asm("rsqrt.approx.f64 %0, %1;" : "=d"(inv) : "d"(s64));
+    inv = inv * fma(-0.5 * s64 * inv, inv, 1.5);
+    nx = static_cast<float>(ax * inv);
+    ny = static_cast<float>(ay * inv);
+    nz = static_cast<float>(az * inv);
+  }
 }
 
 // z = (fx b)/d; x = (u - u0) z / fx; y = (v - v0) z / fy  (geometry.py:39-64),

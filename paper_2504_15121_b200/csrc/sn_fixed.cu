@@ -46,7 +46,8 @@ constexpr int kG = 16;             // output rows per item
 constexpr int kCP = kG + 1;        // pitch of the column-major C/Rr/Dc arrays (odd)
 constexpr int kBoxF = 32;          // floats per TMA store box row (128 B)
 constexpr int kBoxes = kTW * 6 / kBoxF;  // 24
-constexpr int kFastThreads = 160;  // 5 warps: pass V uses up to 128+2R lanes, pass H 128
+constexpr int kFastThreads = 288;  // 9 warps: pass V 2*(128+2R) units, pass H 256 lanes
+constexpr int kRun = 8;            // output columns per pass-H lane
 constexpr double kBig = 1099511627776.0;  // 2^40
 
 __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -63,13 +64,12 @@ struct FastCfg {
   static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
   static constexpr size_t IN0 = STAGE + STAGE_BYTES;
   static constexpr size_t IN1 = align_up(IN0 + IN_BYTES, 128);
-  static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);
-  static constexpr size_t CS_BYTES = (size_t)NC * kCP * 8;
-  static constexpr size_t RS = CS + CS_BYTES;
-  static constexpr size_t FL = align_up(RS + CS_BYTES, 16);
-  static constexpr size_t BAR = align_up(FL + NC * 4, 16);
+  static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);  // double2 (C, Rr) [NC][kCP]
+  static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;
+  static constexpr size_t FL = align_up(CS + CS_BYTES, 16);
+  static constexpr size_t BAR = align_up(FL + (NC + 2) * 4, 16);
   static constexpr size_t TOTAL = BAR + 16 + 1024;  // + slack for 1024-B alignment
-  static_assert(NC <= kFastThreads, "pass V needs one lane per column");
+  static_assert(2 * NC <= kFastThreads + 32, "pass V: at most two units per lane");
   static_assert(NR <= 32, "row validity bits must fit 32 bits");
 };
 
@@ -104,13 +104,15 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   using Cfg = FastCfg<R, T>;
   constexpr int NC = Cfg::NC, NR = Cfg::NR, BW = Cfg::BW, AE = Cfg::AE;
   constexpr int NWIN = 2 * R + 1;
-  constexpr int NH = 16 + 2 * R;  // C/Rr columns read per pass-H run (16 outputs)
-  constexpr int HG = kG / 2;      // rows per pass-V chain
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  double* Cs = reinterpret_cast<double*>(smem + Cfg::CS);
-  double* Rs = reinterpret_cast<double*>(smem + Cfg::RS);
+  constexpr int HG = kG / 2;           // rows per pass-V unit
+  constexpr int NV = HG + 2 * R;       // input rows read per pass-V unit
+  constexpr int NH = kRun + 2 * R;     // C/Rr columns read per pass-H lane
+  constexpr int kLanesH = kTW / kRun * kG;  // 256
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B aligned base for the swizzled staging tile; offset arithmetic on the
+  // __shared__ array keeps the shared address space (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  double2* CR = reinterpret_cast<double2*>(smem + Cfg::CS);
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
   const uint32_t stage_base = smem_u32(smem + Cfg::STAGE);
@@ -149,6 +151,8 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
     fence_mbar_init();
+    fl[NC] = 0u;
+    fl[NC + 1] = 0u;
     load_tile(item, 0);
   }
   __syncthreads();
@@ -163,208 +167,192 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
     // ------------------------------------------------------------ pass V
-    if (tid < NC) {
-      const int c = tid;
+    // unit = (column c, half h): rows 8h .. 8h+7 of the item
+#pragma unroll 1
+    for (int u = tid; u < 2 * NC; u += kFastThreads) {
+      const int h = u >= NC ? 1 : 0;
+      const int c = u - h * NC;
       const int gx = x0 - R + c;
-      // rows of the item inside the image
-      const int lo = max(0, R - y0), hi = min(NR, H - y0 + R);
+      const int r0 = h * HG;  // first input row of the unit (item-relative, incl. halo)
+      // rows of the unit inside the image
+      const int lo = max(0, R - y0 - r0), hi = min(NV, H - y0 + R - r0);
       uint32_t inside = 0;
       if ((unsigned)gx < (unsigned)W && hi > lo)
         inside = (uint32_t)(((1ull << (hi - lo)) - 1ull) << lo);
-      const T* col = in + c + sh;
-      double v[NR];
-      uint32_t fin = 0;
-      bool big = false;
+      const T* col = in + r0 * BW + c + sh;
+      double v[NV];
+      uint32_t small = 0;  // bit i: |sample| <= 2^40 (finite and not "big")
 #pragma unroll
-      for (int i = 0; i < NR; ++i) {
+      for (int i = 0; i < NV; ++i) {
         const T raw = col[i * BW];
-        const bool f = finite_t(raw);
-        fin |= (f ? 1u : 0u) << i;
-        const double dv = f ? (double)raw : 0.0;
-        big |= fabs(dv) > kBig;
-        v[i] = dv;
+        small |= (fabs((double)raw) <= kBig ? 1u : 0u) << i;
+        v[i] = (double)raw;
+      }
+      constexpr uint32_t kAll = (NV >= 32) ? 0xffffffffu : ((1u << NV) - 1u);
+      uint32_t fin = small;
+      bool big = false;
+      if (small != kAll) {
+        // rare: non-finite (zeroed so the sliding sums stay finite) or huge samples
+        fin = 0;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const bool f = finite_t(col[i * BW]);
+          fin |= (f ? 1u : 0u) << i;
+          if (!f) v[i] = 0.0;
+          big |= f && !((small >> i) & 1u);
+        }
       }
       const uint32_t invb = ~(fin & inside);
-      double* cs = Cs + c * kCP;
-      double* rs = Rs + c * kCP;
+      double2* cr = CR + c * kCP + r0;
       if (!big) {
-        // two independent sliding chains (rows 0..7, 8..15) for ILP
-        double C0 = 0.0, R0 = 0.0, C1 = 0.0, R1 = 0.0;
+        double C = 0.0, Rr = 0.0;
 #pragma unroll
         for (int j = 0; j < NWIN; ++j) {
-          C0 += v[j];
-          R0 = fma((double)(j - R), v[j], R0);
-          C1 += v[HG + j];
-          R1 = fma((double)(j - R), v[HG + j], R1);
+          C += v[j];
+          Rr = fma((double)(j - R), v[j], Rr);
         }
-        cs[0] = C0;
-        rs[0] = R0;
-        cs[HG] = C1;
-        rs[HG] = R1;
+        cr[0] = make_double2(C, Rr);
 #pragma unroll
         for (int g = 1; g < HG; ++g) {
-          const double i0 = v[g + 2 * R], o0 = v[g - 1];
-          const double i1 = v[HG + g + 2 * R], o1 = v[HG + g - 1];
-          C0 += i0 - o0;
-          C1 += i1 - o1;
-          R0 = fma((double)R, o0, fma((double)(R + 1), i0, R0 - C0));
-          R1 = fma((double)R, o1, fma((double)(R + 1), i1, R1 - C1));
-          cs[g] = C0;
-          rs[g] = R0;
-          cs[HG + g] = C1;
-          rs[HG + g] = R1;
+          const double vin = v[g + 2 * R], vout = v[g - 1];
+          C += vin - vout;
+          Rr = fma((double)R, vout, fma((double)(R + 1), vin, Rr - C));
+          cr[g] = make_double2(C, Rr);
         }
       } else {
 #pragma unroll
-        for (int g = 0; g < kG; ++g) {
+        for (int g = 0; g < HG; ++g) {
           double C = 0.0, Rr = 0.0;
 #pragma unroll
           for (int j = 0; j < NWIN; ++j) {
             C += v[g + j];
             Rr = fma((double)(j - R), v[g + j], Rr);
           }
-          cs[g] = C;
-          rs[g] = Rr;
+          cr[g] = make_double2(C, Rr);
         }
       }
       uint32_t acc = 0;
 #pragma unroll
       for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
-      fl[c] = (acc & 0xFFFFu) | (big ? 0x80000000u : 0u);
+      // flag bits: 0..15 = support of output row has an invalid sample,
+      // 16 / 17 = big values in half 0 / 1 (two writers per column: halves)
+      // flag word of column c: half h's low byte holds its 8 output rows
+      reinterpret_cast<uint16_t*>(fl + c)[h] = (uint16_t)(acc & 0xFFu);
+      if (big) atomicOr(fl + NC + buf, 1u);  // per-parity "big value" flag of the item
     }
     if (tid == 0) bulk_wait_read0();  // staging of the previous item consumed by TMA
     __syncthreads();
 
     // ------------------------------------------------------------ pass H + epilogue
-    if (tid < kTW) {
+    if (tid < kLanesH) {
       const int g = tid & 15;
-      const int q = tid >> 4;  // run of 16 output columns
-      const int colbase = q * 16;
+      const int q = tid >> 4;  // run of kRun output columns
+      const int colbase = q * kRun;
       double cc[NH], rr[NH];
-      uint32_t colinv = 0;
-      bool big = false;
+      uint32_t any = 0;
 #pragma unroll
       for (int i = 0; i < NH; ++i) {
-        cc[i] = Cs[(colbase + i) * kCP + g];
-        rr[i] = Rs[(colbase + i) * kCP + g];
-        const uint32_t f = fl[colbase + i];
-        colinv |= ((f >> g) & 1u) << i;
-        big |= (f >> 31) != 0u;
+        const double2 v = CR[(colbase + i) * kCP + g];
+        cc[i] = v.x;
+        rr[i] = v.y;
+        any |= fl[colbase + i];
       }
-      uint32_t win = 0;
+      const bool big = fl[NC + buf] != 0u;
+      uint32_t win = 0;  // bit j: support of output j holds an invalid sample
+      if (any != 0u) {
+        uint32_t colinv = 0;
 #pragma unroll
-      for (int j = 0; j < NWIN; ++j) win |= colinv >> j;
+        for (int i = 0; i < NH; ++i) colinv |= ((fl[colbase + i] >> (g + (g & 8))) & 1u) << i;
+#pragma unroll
+        for (int j = 0; j < NWIN; ++j) win |= colinv >> j;
+      }
 
       const int yg = y0 + g;
       const int xb = x0 + colbase;
       const double dv = (double)yg - p.v0;
       const float dv_f = ((float)yg - p.v0_hi) - p.v0_lo;
       const double du0 = (double)xb - p.u0;
+      const float du_hi = (float)xb - p.u0_hi;  // exact; + j stays exact
       const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
       const uint32_t gsw = (uint32_t)(g & 7);
       const uint32_t rowaddr = stage_base + (uint32_t)g * 128u;
       uint32_t validbits = 0;
 
-      // two sliding chains: outputs 0..7 (A) and 8..15 (B)
-      double BA = 0.0, UA = 0.0, VA = 0.0, BB = 0.0, UB = 0.0, VB = 0.0;
+      double Bx = 0.0, U = 0.0, V = 0.0;
       if (!big) {
 #pragma unroll
         for (int j = 0; j < NWIN; ++j) {
-          BA += cc[j];
-          UA = fma((double)(j - R), cc[j], UA);
-          VA += rr[j];
-          BB += cc[8 + j];
-          UB = fma((double)(j - R), cc[8 + j], UB);
-          VB += rr[8 + j];
+          Bx += cc[j];
+          U = fma((double)(j - R), cc[j], U);
+          V += rr[j];
         }
       }
-      float o[2][12];
+      float o[12];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        double U2[2], V2[2];
+      for (int j = 0; j < kRun; ++j) {
         if (!big) {
           if (j > 0) {
-            {
-              const double cin = cc[j + 2 * R], cout = cc[j - 1];
-              BA += cin - cout;
-              UA = fma((double)R, cout, fma((double)(R + 1), cin, UA - BA));
-              VA += rr[j + 2 * R] - rr[j - 1];
-            }
-            {
-              const double cin = cc[8 + j + 2 * R], cout = cc[8 + j - 1];
-              BB += cin - cout;
-              UB = fma((double)R, cout, fma((double)(R + 1), cin, UB - BB));
-              VB += rr[8 + j + 2 * R] - rr[8 + j - 1];
-            }
+            const double cin = cc[j + 2 * R], cout = cc[j - 1];
+            Bx += cin - cout;
+            U = fma((double)R, cout, fma((double)(R + 1), cin, U - Bx));
+            V += rr[j + 2 * R] - rr[j - 1];
           }
-          U2[0] = UA;
-          V2[0] = VA;
-          U2[1] = UB;
-          V2[1] = VB;
         } else {
+          U = 0.0;
+          V = 0.0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            double U = 0.0, V = 0.0;
-#pragma unroll
-            for (int i = 0; i < NWIN; ++i) {
-              U = fma((double)(i - R), cc[8 * h + j + i], U);
-              V += rr[8 * h + j + i];
-            }
-            U2[h] = U;
-            V2[h] = V;
+          for (int i = 0; i < NWIN; ++i) {
+            U = fma((double)(i - R), cc[j + i], U);
+            V += rr[j + i];
           }
         }
+        const T dcv = drow[j];
+        const bool valid = (((win >> j) & 1u) == 0u) && (dcv > (T)0);
+        validbits |= (valid ? 1u : 0u) << j;
+        float px, py, pz, nx, ny, nz;
+        const int xg = xb + j;
+        if constexpr (sizeof(T) == 4) {
+          const float du_f = (du_hi + (float)j) - p.u0_lo;
+          point_from_disparity((float)dcv, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
+        } else {
+          point_from_disparity_f64((double)dcv, (double)xg - p.u0, dv, p, px, py, pz);
+        }
+        if (valid) {
+          normal_from_moments(U, V, p.alpha, (double)dcv, du0 + (double)j, dv, p.fx, p.fy, nx, ny,
+                              nz);
+        } else {
+          nx = ny = nz = __int_as_float(0x7fc00000);
+        }
+        const int s6 = (j & 1) * 6;
+        o[s6 + 0] = px;
+        o[s6 + 1] = py;
+        o[s6 + 2] = pz;
+        o[s6 + 3] = nx;
+        o[s6 + 4] = ny;
+        o[s6 + 5] = nz;
+        if (j & 1) {
+          // pixels (j-1, j) = 12 floats = 3 chunks of the 128B-swizzled staging row
+          const int K = q * (kRun * 6 / 4) + (j >> 1) * 3;  // chunk index in the 768-float row
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int jj = 8 * h + j;
-          const T dcv = drow[jj];
-          const bool valid = (((win >> jj) & 1u) == 0u) && (dcv > (T)0);
-          validbits |= (valid ? 1u : 0u) << jj;
-          float px, py, pz, nx, ny, nz;
-          const int xg = xb + jj;
-          if constexpr (sizeof(T) == 4) {
-            const float du_f = ((float)xg - p.u0_hi) - p.u0_lo;
-            point_from_disparity((float)dcv, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py,
-                                 pz);
-          } else {
-            point_from_disparity_f64((double)dcv, (double)xg - p.u0, dv, p, px, py, pz);
-          }
-          if (valid) {
-            normal_from_moments(U2[h], V2[h], p.alpha, (double)dcv, du0 + (double)jj, dv, p.fx,
-                                p.fy, nx, ny, nz);
-          } else {
-            nx = ny = nz = __int_as_float(0x7fc00000);
-          }
-          const int s6 = (jj & 1) * 6;
-          o[h][s6 + 0] = px;
-          o[h][s6 + 1] = py;
-          o[h][s6 + 2] = pz;
-          o[h][s6 + 3] = nx;
-          o[h][s6 + 4] = ny;
-          o[h][s6 + 5] = nz;
-          if (jj & 1) {
-            // pixels (jj-1, jj) = 12 floats = 3 chunks of the 128B-swizzled staging row
-            const int K = q * 24 + (jj >> 1) * 3;  // chunk index within the 768-float tile row
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-              const int kk = K + t;
-              const uint32_t box = (uint32_t)(kk >> 3);
-              const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
-              st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[h][4 * t],
-                           o[h][4 * t + 1], o[h][4 * t + 2], o[h][4 * t + 3]);
-            }
+          for (int t = 0; t < 3; ++t) {
+            const int kk = K + t;
+            const uint32_t box = (uint32_t)(kk >> 3);
+            const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
+            st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[4 * t], o[4 * t + 1],
+                         o[4 * t + 2], o[4 * t + 3]);
           }
         }
       }
       if (mask_out != nullptr && yg < H) {
         uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
 #pragma unroll 1
-        for (int j = 0; j < 16 && xb + j < W; ++j) mrow[j] = (uint8_t)((validbits >> j) & 1u);
+        for (int j = 0; j < kRun && xb + j < W; ++j) mrow[j] = (uint8_t)((validbits >> j) & 1u);
       }
     }
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
+      fl[NC + buf] = 0u;  // reset this parity's big flag (next used two items later)
 #pragma unroll 1
       for (int b = 0; b < kBoxes; ++b) {
         tma_store_3d(&out_map, smem + Cfg::STAGE + (size_t)b * kG * 128, x0 * 6 + b * kBoxF, y0, bz);
