@@ -215,8 +215,9 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 #pragma unroll
         for (int g = 1; g < HG; ++g) {
           const double vin = v[g + 2 * R], vout = v[g - 1];
+          const double tin = fma((double)R, vout, (double)(R + 1) * vin);  // off the chain
           C += vin - vout;
-          Rr = fma((double)R, vout, fma((double)(R + 1), vin, Rr - C));
+          Rr = (Rr - C) + tin;
           cr[g] = make_double2(C, Rr);
         }
       } else {
@@ -278,34 +279,45 @@ __global__ void __launch_bounds__(kFastThreads, 2)
       const uint32_t rowaddr = stage_base + (uint32_t)g * 128u;
       uint32_t validbits = 0;
 
-      double Bx = 0.0, U = 0.0, V = 0.0;
+      // sliding sums first (short dependent chain), then 8 independent epilogues
+      double Us[kRun], Vs[kRun];
       if (!big) {
+        double Bx = 0.0, U = 0.0, V = 0.0;
 #pragma unroll
         for (int j = 0; j < NWIN; ++j) {
           Bx += cc[j];
           U = fma((double)(j - R), cc[j], U);
           V += rr[j];
         }
-      }
-      float o[12];
+        Us[0] = U;
+        Vs[0] = V;
 #pragma unroll
-      for (int j = 0; j < kRun; ++j) {
-        if (!big) {
-          if (j > 0) {
-            const double cin = cc[j + 2 * R], cout = cc[j - 1];
-            Bx += cin - cout;
-            U = fma((double)R, cout, fma((double)(R + 1), cin, U - Bx));
-            V += rr[j + 2 * R] - rr[j - 1];
-          }
-        } else {
-          U = 0.0;
-          V = 0.0;
+        for (int j = 1; j < kRun; ++j) {
+          const double cin = cc[j + 2 * R], cout = cc[j - 1];
+          const double tin = fma((double)R, cout, (double)(R + 1) * cin);  // independent of the chain
+          Bx += cin - cout;
+          U = (U - Bx) + tin;
+          V += rr[j + 2 * R] - rr[j - 1];
+          Us[j] = U;
+          Vs[j] = V;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kRun; ++j) {
+          double U = 0.0, V = 0.0;
 #pragma unroll
           for (int i = 0; i < NWIN; ++i) {
             U = fma((double)(i - R), cc[j + i], U);
             V += rr[j + i];
           }
+          Us[j] = U;
+          Vs[j] = V;
         }
+      }
+      float o[12];
+#pragma unroll
+      for (int j = 0; j < kRun; ++j) {
+        const double U = Us[j], V = Vs[j];
         const T dcv = drow[j];
         const bool valid = (((win >> j) & 1u) == 0u) && (dcv > (T)0);
         validbits |= (valid ? 1u : 0u) << j;
