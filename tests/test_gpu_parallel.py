@@ -1,0 +1,51 @@
+"""Partition invariance on the device (reference test_parallel.py:48-75,
+restated for strips and frame shards): strip-partitioned points and labels
+are bit-identical to the whole-frame result, for any strip count; frame
+shards reproduce the whole batch."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _nan_eq(a, b):
+    return torch.equal(torch.nan_to_num(a, 7.0), torch.nan_to_num(b, 7.0))
+
+
+@pytest.mark.parametrize("n_strips,k", [(2, 9), (3, 9), (8, 9), (5, 15), (4, 3)])
+def test_strip_frame_matches_whole_frame(cuda_dev, n_strips, k):
+    from scipy import ndimage
+    from paper_2504_15121_b200 import device, scenes
+    from paper_2504_15121_b200.parallel import StripPlan, local_strip_frame
+    sc = scenes.street_scene(768, 432)
+    d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 1.0, 5)
+    holes = ndimage.binary_dilation(np.random.default_rng(3).random(d.shape) < 0.002, iterations=2)
+    d[holes] = np.nan
+    dt = torch.from_numpy(d.astype(np.float32)).to(cuda_dev)
+    plan = StripPlan.for_kernel(432, 768, n_strips, k)
+    for t in (0.05, 1.0):
+        pts, lab = local_strip_frame(dt, plan, sc.rig, k, t)
+        whole_pts = device.oriented_points(dt, sc.rig, k)[0]
+        whole_lab = device.component_labels(dt, sc.rig, t)[0]
+        assert _nan_eq(pts, whole_pts)
+        assert torch.equal(lab, whole_lab)
+
+
+def test_frame_shards_match_batch(cuda_dev):
+    from paper_2504_15121_b200 import device, scenes
+    from paper_2504_15121_b200.parallel import shard_range
+    sc = scenes.street_scene(512, 256)
+    clean = scenes.raycast(sc)[0]
+    frames = np.stack([scenes.add_gaussian_noise(clean, 0.2, i) for i in range(7)])
+    d = torch.from_numpy(frames.astype(np.float32)).to(cuda_dev)
+    whole = device.oriented_points(d, sc.rig, 9)
+    whole_lab = device.component_labels(d, sc.rig, 0.2)
+    for world in (2, 3, 4):
+        for r in range(world):
+            a, b = shard_range(7, r, world)
+            if a == b:
+                continue
+            assert _nan_eq(device.oriented_points(d[a:b], sc.rig, 9), whole[a:b])
+            assert torch.equal(device.component_labels(d[a:b], sc.rig, 0.2), whole_lab[a:b])
