@@ -225,6 +225,7 @@ def main():
         disp[i] = base + 0.2 * torch.randn((H, W), generator=g, device=dev)
     out = torch.empty((B, H, W, 6), dtype=torch.float32, device=dev)
     labels = torch.empty((B, H, W), dtype=torch.int32, device=dev)
+    ccl_ws = device.ccl_workspace(B, H, W, dev)
     stream = torch.cuda.current_stream(dev)
 
     def step(ev=None):
@@ -234,7 +235,7 @@ def main():
         if ev is not None:
             ev[1].record(stream)
         if args.pipeline == "full":
-            device.component_labels(disp, rig, T_ST, out=labels)
+            device.component_labels(disp, rig, T_ST, out=labels, workspace=ccl_ws)
         if ev is not None:
             ev[2].record(stream)
 

@@ -33,6 +33,7 @@
 #ifndef SN_B200_H
 #define SN_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -88,6 +89,16 @@ SN_API int sn_oriented_points_f64(sn_plan_t* plan, const double* disp, int64_t B
                            int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
                            int32_t n_off, float* out6, uint8_t* mask, void* stream);
 
+/* Same pass over a block of rows of a taller image (strip partitioning,
+ * SURVEY.md §8(e)): block row i is image row row0 + i, which only changes the
+ * pixel coordinate v of the normal and point; the block's first and last
+ * rows are treated as image borders, so a strip passes its owned rows plus
+ * a halo of R rows on each interior side and keeps the owned rows. */
+SN_API int sn_oriented_points_rows(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
+                            int64_t W, int64_t row0, const sn_rig_t* rig,
+                            const int32_t* offsets_xy, int32_t n_off, float* out6,
+                            uint8_t* mask, void* stream);
+
 /* Same pass, host buffers: pinned staging + overlapped H2D / compute / D2H,
  * returns when out6 (and mask, if non-NULL) hold the result. */
 SN_API int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
@@ -122,6 +133,19 @@ SN_API int sn_ccl_labels(sn_plan_t* plan, const float* disp, int64_t B, int64_t 
  * by tests of the labeller alone. */
 SN_API int sn_ccl_from_passable(sn_plan_t* plan, const uint8_t* passable, int64_t B, int64_t H,
                          int64_t W, int64_t row_base, int32_t* labels, void* stream);
+
+/* The labeller needs a device workspace (passable bit mask + tile seam rows,
+ * ~H*W/8 + 8*(H*W/64 + H*W/128) bytes per frame).  The two entry points above
+ * use one owned by the plan (grown on demand, so calls sharing a plan must
+ * be stream-ordered); the *_ws variants take the caller's, so concurrent
+ * streams each pass their own. */
+SN_API int sn_ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes);
+SN_API int sn_ccl_labels_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                     const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                     void* workspace, size_t ws_bytes, void* stream);
+SN_API int sn_ccl_from_passable_ws(sn_plan_t* plan, const uint8_t* passable, int64_t B,
+                            int64_t H, int64_t W, int64_t row_base, int32_t* labels,
+                            void* workspace, size_t ws_bytes, void* stream);
 
 /* Strip-seam merge.  HOST memory: `seams` holds, for each
  * of the n_strips strips in row order, its first and last owned label rows

@@ -58,12 +58,16 @@ SIGNATURES = {
     "sn_oriented_points": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
     "sn_oriented_points_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
     "sn_oriented_points_generic": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
+    "sn_oriented_points_rows": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
     "sn_oriented_points_host": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P],
     "sn_affine": [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P, _P],
     "sn_affine_f64": [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P, _P],
     "sn_passable": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P, _P],
     "sn_ccl_labels": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _I64, _P, _P],
     "sn_ccl_from_passable": [_P, _P, _I64, _I64, _I64, _I64, _P, _P],
+    "sn_ccl_workspace_bytes": [_I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
+    "sn_ccl_labels_ws": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _I64, _P, _P, ctypes.c_size_t, _P],
+    "sn_ccl_from_passable_ws": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_seam_merge_host": [_P, _I32, _I64, _P, _P, _P],
     "sn_relabel": [_P, _P, _I64, _I64, _P, _P, _P, _I32, _P, _P],
 }
@@ -130,6 +134,13 @@ def plan(device: int):
             _plans[device] = h
             p = h
     return p
+
+
+def ccl_workspace_bytes(B: int, H: int, W: int) -> int:
+    n = ctypes.c_size_t(0)
+    check(load().sn_ccl_workspace_bytes(int(B), int(H), int(W), ctypes.byref(n)),
+          "sn_ccl_workspace_bytes")
+    return int(n.value)
 
 
 def rig_struct(rig) -> SnRig:

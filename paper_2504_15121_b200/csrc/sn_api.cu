@@ -92,6 +92,9 @@ struct sn_plan {
   float* d_out[2] = {nullptr, nullptr};
   uint8_t* d_mask[2] = {nullptr, nullptr};
   size_t cap_px = 0;
+  // labeller workspace for the entry points without an explicit one
+  void* ccl_ws = nullptr;
+  size_t ccl_ws_bytes = 0;
   std::mutex mu;
 };
 
@@ -175,8 +178,10 @@ LaunchCtx make_ctx(sn_plan_t* plan, void* stream) {
 template <typename T>
 int oriented_points_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
                          const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
-                         float* out6, uint8_t* mask, void* stream, int force_generic) {
+                         float* out6, uint8_t* mask, void* stream, int force_generic,
+                         int64_t row0 = 0) {
   if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  if (row0 < 0 || row0 + H > 0x7fffffffLL) return set_error(SN_EINVAL, "row offset out of range");
   int rc = check_shape(B, H, W);
   if (rc) return rc;
   if ((rc = check_rig(rig))) return rc;
@@ -190,6 +195,7 @@ int oriented_points_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, i
   p.W = W;
   fill_rig(p, rig);
   fill_moments(p, m);
+  p.row0 = (int)row0;
   DeviceGuard g(plan->device);
   return run_fixed<T>(make_ctx(plan, stream), disp, p, m, tab, out6, mask, nullptr, nullptr, false,
                       force_generic);
@@ -254,6 +260,7 @@ int sn_plan_destroy(sn_plan_t* plan) {
       if (plan->ev_done[i]) cudaEventDestroy(plan->ev_done[i]);
       if (plan->ev_out[i]) cudaEventDestroy(plan->ev_out[i]);
     }
+    if (plan->ccl_ws) cudaFree(plan->ccl_ws);
     if (plan->s_h2d) cudaStreamDestroy(plan->s_h2d);
     if (plan->s_comp) cudaStreamDestroy(plan->s_comp);
     if (plan->s_d2h) cudaStreamDestroy(plan->s_d2h);
@@ -316,6 +323,13 @@ int sn_oriented_points_f64(sn_plan_t* plan, const double* disp, int64_t B, int64
                                       stream, 0);
 }
 
+int sn_oriented_points_rows(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                            int64_t row0, const sn_rig_t* rig, const int32_t* offsets_xy,
+                            int32_t n_off, float* out6, uint8_t* mask, void* stream) {
+  return oriented_points_impl<float>(plan, disp, B, H, W, rig, offsets_xy, n_off, out6, mask,
+                                     stream, 0, row0);
+}
+
 /* test hook: force the generic (non-TMA) kernel, to cross-check the fast path */
 int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                                const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
@@ -344,37 +358,96 @@ int sn_passable(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_
   if ((rc = check_rig(rig))) return rc;
   if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");  // adaptive.py:56-57
   if (B * H * W > 0 && !disp) return set_error(SN_EINVAL, "NULL buffer");
-  CclParams p{B, H, W, rig->fx * rig->baseline, t};
+  const CclParams p = make_ccl_params(B, H, W, rig->fx * rig->baseline, t);
   DeviceGuard g(plan->device);
   return run_passable(make_ctx(plan, stream), disp, p, passable, edges);
 }
 
-int sn_ccl_labels(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
-                  const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels, void* stream) {
+int sn_ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
+  if (!bytes) return set_error(SN_EINVAL, "bytes out-pointer is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  *bytes = ccl_workspace_bytes(B, H, W);
+  return SN_OK;
+}
+
+namespace {
+
+int ccl_args(sn_plan_t* plan, int64_t B, int64_t H, int64_t W, int64_t row_base,
+             const void* input, const int32_t* labels) {
   if (!plan) return set_error(SN_EINVAL, "plan is NULL");
   int rc = check_shape(B, H, W);
   if (rc) return rc;
-  if ((rc = check_rig(rig))) return rc;
-  if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
-  if (B * H * W > 0 && (!disp || !labels)) return set_error(SN_EINVAL, "NULL buffer");
+  if (B * H * W > 0 && (!input || !labels)) return set_error(SN_EINVAL, "NULL buffer");
   if (row_base < 0 || (row_base + H) * W > 0x7fffffffLL)
     return set_error(SN_EINVAL, "label index range exceeds int32");
-  CclParams p{B, H, W, rig->fx * rig->baseline, t};
+  return SN_OK;
+}
+
+// plan-owned workspace (grown on demand; stream-ordered use only)
+int plan_workspace(sn_plan_t* plan, int64_t B, int64_t H, int64_t W, void** ws, size_t* bytes) {
+  const size_t need = ccl_workspace_bytes(B, H, W);
+  if (plan->ccl_ws_bytes < need) {
+    if (plan->ccl_ws) cudaFree(plan->ccl_ws);  // synchronises the device: growth only
+    plan->ccl_ws = nullptr;
+    plan->ccl_ws_bytes = 0;
+    if (cudaMalloc(&plan->ccl_ws, need) != cudaSuccess)
+      return set_cuda_error("cudaMalloc(labeller workspace)");
+    plan->ccl_ws_bytes = need;
+  }
+  *ws = plan->ccl_ws;
+  *bytes = plan->ccl_ws_bytes;
+  return SN_OK;
+}
+
+}  // namespace
+
+int sn_ccl_labels_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                     const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                     void* workspace, size_t ws_bytes, void* stream) {
+  int rc = ccl_args(plan, B, H, W, row_base, disp, labels);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
+  const CclParams p = make_ccl_params(B, H, W, rig->fx * rig->baseline, t);
   DeviceGuard g(plan->device);
-  return run_ccl(make_ctx(plan, stream), disp, nullptr, p, row_base * W, labels);
+  return run_ccl(make_ctx(plan, stream), disp, nullptr, p, row_base * W, labels, workspace,
+                 ws_bytes);
+}
+
+int sn_ccl_labels(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                  const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels, void* stream) {
+  int rc = ccl_args(plan, B, H, W, row_base, disp, labels);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(plan->mu);
+  DeviceGuard g(plan->device);
+  void* ws = nullptr;
+  size_t bytes = 0;
+  if ((rc = plan_workspace(plan, B, H, W, &ws, &bytes))) return rc;
+  return sn_ccl_labels_ws(plan, disp, B, H, W, rig, t, row_base, labels, ws, bytes, stream);
+}
+
+int sn_ccl_from_passable_ws(sn_plan_t* plan, const uint8_t* passable, int64_t B, int64_t H,
+                            int64_t W, int64_t row_base, int32_t* labels, void* workspace,
+                            size_t ws_bytes, void* stream) {
+  int rc = ccl_args(plan, B, H, W, row_base, passable, labels);
+  if (rc) return rc;
+  const CclParams p = make_ccl_params(B, H, W, 0.0, 1.0);
+  DeviceGuard g(plan->device);
+  return run_ccl(make_ctx(plan, stream), nullptr, passable, p, row_base * W, labels, workspace,
+                 ws_bytes);
 }
 
 int sn_ccl_from_passable(sn_plan_t* plan, const uint8_t* passable, int64_t B, int64_t H, int64_t W,
                          int64_t row_base, int32_t* labels, void* stream) {
-  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
-  int rc = check_shape(B, H, W);
+  int rc = ccl_args(plan, B, H, W, row_base, passable, labels);
   if (rc) return rc;
-  if (B * H * W > 0 && (!passable || !labels)) return set_error(SN_EINVAL, "NULL buffer");
-  if (row_base < 0 || (row_base + H) * W > 0x7fffffffLL)
-    return set_error(SN_EINVAL, "label index range exceeds int32");
-  CclParams p{B, H, W, 0.0, 0.0};
+  std::lock_guard<std::mutex> lock(plan->mu);
   DeviceGuard g(plan->device);
-  return run_ccl(make_ctx(plan, stream), nullptr, passable, p, row_base * W, labels);
+  void* ws = nullptr;
+  size_t bytes = 0;
+  if ((rc = plan_workspace(plan, B, H, W, &ws, &bytes))) return rc;
+  return sn_ccl_from_passable_ws(plan, passable, B, H, W, row_base, labels, ws, bytes, stream);
 }
 
 int sn_relabel(sn_plan_t* plan, int32_t* labels, int64_t n, int64_t index_base,

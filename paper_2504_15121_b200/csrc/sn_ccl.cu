@@ -6,20 +6,32 @@
 // numpy's left-to-right order with correctly rounded fp64 operations
 // (adaptive.py:80-97), valid only at interior pixels with all five depths
 // valid; passable = edge valid and e <= t (the ST ray test,
-// adaptive.py:130-132, 218-221).
+// adaptive.py:130-132, 218-221).  The labeller evaluates it as an fp32
+// filter with a rigorous error bound and falls back to the exact fp64
+// evaluation only when |e32 - t| is inside the bound, so every decision is
+// the fp64 decision (see fast_passable below).
 //
 // Labelling (no reference function): 8-connected
 // components of the passable set, canonical label = smallest raster index in
-// the component.  Union-find where every link goes from the larger index to
-// the smaller (atomicMin), so a tree's root is always its minimum element and
-// the result is independent of scheduling:
-//   1. ccl_local: 32x64 tile in shared memory -- each warp owns a tile row,
-//      __ballot_sync gives the passable bits of the row and every pixel links
-//      to the first pixel of its horizontal run (no atomics), then rows are
-//      merged with the pixels above (3 candidates, redundant unions pruned);
-//      tile roots are written as frame raster indices.
-//   2. ccl_merge: unions across tile edges in global memory.
-//   3. ccl_flatten: global path compression, label = root index.
+// the component.  The passable set is a BIT mask (one uint32 word per 32
+// pixels of a row) and the union-find runs over word-runs (maximal runs of
+// set bits inside one word), not pixels: ~4x fewer nodes and unions than a
+// pixel union-find on street scenes.  Every link goes from the larger node
+// to the smaller (atomicMin), so a root is always its component's minimum
+// and the result is independent of scheduling.  Three launches per batch:
+//
+//   1. ccl_tile_kernel   128x64 tile per CTA, 256 threads = (row, word).
+//      predicate -> bits (ballot), bits -> global (for pass 3), run
+//      union-find in shared memory, tile-border labels -> compact seam rows /
+//      columns, global node init G[root] = root for border-touching roots.
+//   2. ccl_seam_kernel   unions across tile seams in global memory (G is the
+//      label array itself; only border-touching roots are ever nodes).
+//   3. ccl_resolve_kernel  re-runs the (deterministic) tile union-find from
+//      the bits, resolves border-touching roots through G, writes every
+//      label once with coalesced stores.
+//
+// HBM traffic per pixel: 4 B disparity in, 4 B labels out, 2 x 1/8 B bits,
+// plus the sparse seam/root traffic -- against the 8 B/px floor of §8(d).
 
 #include <cuda_runtime.h>
 #include <float.h>
@@ -29,8 +41,11 @@
 
 namespace sn {
 
-constexpr int kCT = 32;  // CCL tile edge
-constexpr int kCclThreads = 256;
+constexpr int kLTW = 128;             // label tile columns
+constexpr int kLTH = 64;              // label tile rows
+constexpr int kLWords = kLTW / 32;    // words per tile row
+constexpr int kLThreads = kLTH * kLWords;  // 256: one thread per (row, word)
+constexpr int kZW = kLTW + 2, kZH = kLTH + 2;  // fp32 depth tile with a 1-pixel halo
 
 __device__ __forceinline__ double depth_of(float d, double fxb) {
   // NaN marks an invalid depth sample
@@ -48,8 +63,20 @@ __device__ __forceinline__ double edge_value(double c, double l, double r, doubl
 
 __device__ __forceinline__ bool valid_z(double z) { return z == z; }
 
+// exact fp64 predicate at interior pixel (x, y) of frame f (row pitch W)
+__device__ __noinline__ bool exact_passable(const float* __restrict__ f, int64_t W, int64_t x,
+                                            int64_t y, double fxb, double t) {
+  const double c = depth_of(f[y * W + x], fxb);
+  const double l = depth_of(f[y * W + x - 1], fxb);
+  const double r = depth_of(f[y * W + x + 1], fxb);
+  const double u = depth_of(f[(y - 1) * W + x], fxb);
+  const double dn = depth_of(f[(y + 1) * W + x], fxb);
+  if (!(valid_z(c) && valid_z(l) && valid_z(r) && valid_z(u) && valid_z(dn))) return false;
+  return edge_value(c, l, r, u, dn) <= t;
+}
+
 // ---------------------------------------------------------------------------
-// standalone predicate (API sn_passable; the CCL kernel evaluates it inline)
+// standalone predicate (API sn_passable; exact fp64 per pixel, optional edges)
 
 __global__ void passable_kernel(const float* __restrict__ disp, const CclParams p,
                                 uint8_t* __restrict__ pas, double* __restrict__ edges) {
@@ -78,6 +105,44 @@ __global__ void passable_kernel(const float* __restrict__ disp, const CclParams 
 }
 
 // ---------------------------------------------------------------------------
+// fp32 filter for the predicate
+//
+// zf = fl(fxb_f * rcp.approx(d)) has relative error <= 2^-24 (fxb_f) + 2^-23
+// (rcp.approx, 1 ulp) + 2^-24 (product) = 2^-22 while zf stays a normal
+// float.  With S = 4c + l + r + u + dn (all depths > 0), the fp32 edge value
+// differs from the exact one by <= 2^-22 S (inputs) + 4 * 2^-24 S (four
+// roundings of partial sums bounded by S) = 2^-21 S, and the fp64 edge value
+// from the exact one by < 2^-50 S; t_f = fl(t) is within 2^-24 t.  So when
+// |e32 - t_f| > 2^-19 S_f + 2^-20 t_f (a 4x safety factor) both sides agree
+// on e <= t; otherwise the pixel takes the exact fp64 path.  Samples that
+// are invalid (non-finite or <= 0) are NaN; samples whose zf would leave
+// [1e-30, 1e30] are +inf and force the exact path.
+
+__device__ __forceinline__ float zfast(float d, float fxb_f) {
+  if (!(d > 0.0f && d <= FLT_MAX)) return __int_as_float(0x7fc00000);
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(d));
+  const float z = __fmul_rn(fxb_f, r);
+  return (z >= 1e-30f && z <= 1e30f) ? z : __int_as_float(0x7f800000);
+}
+
+// 0 = not passable, 1 = passable, 2 = undecided (exact path)
+__device__ __forceinline__ int fast_passable(float c, float l, float r, float u, float dn,
+                                             float t_f) {
+  if (!(c == c && l == l && r == r && u == u && dn == dn)) return 0;
+  const float S = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(4.0f, c), l), r), u), dn);
+  if (!(S <= 1e30f)) return 2;  // an out-of-range sample
+  const float e =
+      fabsf(__fsub_rn(__fsub_rn(__fsub_rn(__fsub_rn(__fmul_rn(4.0f, c), l), r), u), dn));
+  const float margin = __fadd_rn(__fmul_rn(S, 1.9073486328125e-06f /* 2^-19 */),
+                                 __fmul_rn(t_f, 9.5367431640625e-07f /* 2^-20 */));
+  const float gap = __fsub_rn(e, t_f);
+  if (gap > margin) return 0;
+  if (-gap > margin) return 1;
+  return 2;
+}
+
+// ---------------------------------------------------------------------------
 // union-find helpers (indices only ever point to smaller indices)
 
 // find with path halving: every write replaces a parent by an ancestor, so it
@@ -93,8 +158,7 @@ __device__ __forceinline__ int uf_find(volatile int32_t* L, int x) {
   }
 }
 
-// read-only find: used where concurrent writers store final roots (flatten),
-// so a late path-halving store can never overwrite a root with an ancestor
+// read-only find
 __device__ __forceinline__ int uf_root(const volatile int32_t* L, int x) {
   int p = L[x];
   while (p != x) {
@@ -121,165 +185,327 @@ __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
   }
 }
 
+__device__ __forceinline__ uint32_t run_starts(uint32_t A) { return A & ~(A << 1); }
+
+// start bit of the run (inside word A, starts st) that contains bit p
+__device__ __forceinline__ int start_of(uint32_t st, int p) {
+  const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
+  return 31 - __clz(st & upto);
+}
+
 // ---------------------------------------------------------------------------
-// 1. tile-local labelling (+ fused predicate when disp != nullptr)
+// tile union-find over word-runs
 //
-// Tile = 32 columns x 64 rows; warp w owns rows w, w+8, ..., lane = column.
+// Node id = local pixel index r * 128 + c of a run's first pixel; L (shared)
+// holds parents at node ids only.  On return every node points at its root
+// (the smallest node of its tile component) and `flag` has bit `root` set for
+// every root whose component touches the tile border.
 
-constexpr int kTY = 64;                 // CCL tile rows (kCT = 32 columns)
-constexpr int kZW = kCT + 2, kZH = kTY + 2;
-constexpr int kRowsPerWarp = kTY / (kCclThreads / 32);
+__device__ __forceinline__ void tile_union_find(int32_t* L, const uint32_t* bits, uint32_t* flag,
+                                                int tid) {
+  const int r = tid >> 2, w = tid & 3;
+  const int base = r * kLTW + w * 32;
+  const uint32_t A = bits[tid];
+  const uint32_t st = run_starts(A);
+  for (uint32_t m = st; m; m &= m - 1u) {
+    const int n = base + __ffs(m) - 1;
+    L[n] = n;
+  }
+  flag[tid] = 0u;
+  __syncthreads();
 
-__global__ void __launch_bounds__(kCclThreads)
-    ccl_local_kernel(const float* __restrict__ disp, const uint8_t* __restrict__ pas_in,
-                     const CclParams p, int32_t* __restrict__ labels) {
-  __shared__ double zs[kZH * kZW];
-  __shared__ int32_t L[kTY * kCT];
-  __shared__ uint32_t rowbits[kTY];
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  // a run crossing into this word from the left neighbour word
+  if ((A & 1u) && w > 0) {
+    const uint32_t Al = bits[tid - 1];
+    if (Al >> 31) uf_unite(L, base, base - 32 + (31 - __clz(run_starts(Al))));
+  }
+  // runs of the row above (8-connected: the run dilated by one pixel)
+  if (r > 0) {
+    const uint32_t B = bits[tid - kLWords];
+    const uint32_t BL = w > 0 ? bits[tid - kLWords - 1] : 0u;
+    const uint32_t BR = w + 1 < kLWords ? bits[tid - kLWords + 1] : 0u;
+    const uint32_t stB = run_starts(B);
+    const int bbase = base - kLTW;
+    for (uint32_t m = st; m; m &= m - 1u) {
+      const int s = __ffs(m) - 1;
+      const uint32_t hi = 0xffffffffu << s;
+      const uint32_t zer = ~A & hi;  // zeros of A at or above s (bit s itself is set)
+      const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+      const int n = base + s;
+      uint32_t o = (run | (run << 1) | (run >> 1)) & B;
+      while (o) {
+        const int p = __ffs(o) - 1;
+        uf_unite(L, n, bbase + start_of(stB, p));
+        const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
+        const uint32_t zb = ~B & ~upto;  // zeros of B above p: end of that run
+        if (!zb) break;
+        o &= ~((zb & (0u - zb)) - 1u);
+      }
+      if ((run & 1u) && (BL >> 31)) uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(BL))));
+      if ((run >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
+    }
+  }
+  __syncthreads();
+  // every node -> its root (only root values are written in this phase)
+  for (uint32_t m = st; m; m &= m - 1u) {
+    const int n = base + __ffs(m) - 1;
+    L[n] = uf_root(L, n);
+  }
+  __syncthreads();
+  // roots of components that touch the tile border
+  auto mark = [&](int n) {
+    const int root = L[n];
+    atomicOr(&flag[root >> 5], 1u << (root & 31));
+  };
+  if (r == 0 || r == kLTH - 1)
+    for (uint32_t m = st; m; m &= m - 1u) mark(base + __ffs(m) - 1);
+  else {
+    if (w == 0 && (A & 1u)) mark(base);
+    if (w == kLWords - 1 && (A >> 31)) mark(base + (31 - __clz(st)));
+  }
+  __syncthreads();
+}
+
+struct CclWorkspace {
+  uint32_t* bits;  // [B][H][WW]
+  int32_t* top;    // [B][n_ty][W]  first row of each tile row
+  int32_t* bot;    // [B][n_ty][W]  last row of each tile row
+  int32_t* left;   // [B][n_tx][H]  first column of each tile column
+  int32_t* right;  // [B][n_tx][H]  last column of each tile column
+  int WW, n_tx, n_ty;
+};
+
+__device__ __forceinline__ int frame_index(int node, int x0, int y0, int W) {
+  return (y0 + (node >> 7)) * W + x0 + (node & (kLTW - 1));
+}
+
+// ---------------------------------------------------------------------------
+// 1. tile pass.  MODE 0: predicate from fp32 disparity; MODE 1: uint8 passable
+
+template <int MODE>
+__global__ void __launch_bounds__(kLThreads)
+    ccl_tile_kernel(const float* __restrict__ disp, const uint8_t* __restrict__ pas_in,
+                    const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
+  __shared__ __align__(16) int32_t smem[kZH * kZW];  // fp32 depth tile, then the parent array
+  __shared__ uint32_t bits[kLThreads];
+  __shared__ uint32_t flag[kLThreads];
+  static_assert(kZH * kZW >= kLTH * kLTW, "parent array must fit the depth tile");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
-  const int x0 = blockIdx.x * kCT, y0 = blockIdx.y * kTY;
+  const int tx = blockIdx.x, ty = blockIdx.y;
+  const int x0 = tx * kLTW, y0 = ty * kLTH;
   const int64_t fbase = (int64_t)blockIdx.z * p.H * p.W;
-  if (disp) {
+
+  if (MODE == 0) {
     const float* f = disp + fbase;
-    for (int i = tid; i < kZH * kZW; i += kCclThreads) {
+    float* zs = reinterpret_cast<float*>(smem);
+    for (int i = tid; i < kZH * kZW; i += kLThreads) {
       const int iy = i / kZW, ix = i - iy * kZW;
       const int gx = x0 - 1 + ix, gy = y0 - 1 + iy;
-      double z = __longlong_as_double(0x7ff8000000000000ll);
+      float z = __int_as_float(0x7fc00000);  // outside the frame: invalid sample
       if ((unsigned)gx < (unsigned)W && (unsigned)gy < (unsigned)H)
-        z = depth_of(f[(int64_t)gy * W + gx], p.fxb);
+        z = p.exact_only ? __int_as_float(0x7f800000) : zfast(f[(int64_t)gy * W + gx], p.fxb_f);
       zs[i] = z;
     }
     __syncthreads();
-  }
-  uint32_t Pbits = 0;  // bit k: pixel (warp + 8k, lane) passable
-#pragma unroll
-  for (int k = 0; k < kRowsPerWarp; ++k) {
-    const int ly = warp + 8 * k;
-    const int gx = x0 + lane, gy = y0 + ly;
-    bool pk = false;
-    if (disp) {
-      if (gx >= 1 && gx + 1 < W && gy >= 1 && gy + 1 < H) {
-        const int zi = (ly + 1) * kZW + lane + 1;
-        const double c = zs[zi], l = zs[zi - 1], r = zs[zi + 1], u = zs[zi - kZW],
-                     dn = zs[zi + kZW];
-        if (valid_z(c) && valid_z(l) && valid_z(r) && valid_z(u) && valid_z(dn))
-          pk = edge_value(c, l, r, u, dn) <= p.t;
+    for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
+      const int r = rw >> 2, c = (rw & 3) * 32 + lane;
+      const int gx = x0 + c, gy = y0 + r;
+      bool pk = false;
+      if (gx < W && gy < H) {
+        const int zi = (r + 1) * kZW + c + 1;
+        const int dec = fast_passable(zs[zi], zs[zi - 1], zs[zi + 1], zs[zi - kZW], zs[zi + kZW],
+                                      p.t_f);
+        if (dec == 2) pk = exact_passable(f, W, gx, gy, p.fxb, p.t);
+        else pk = dec == 1;
       }
-    } else if (gx < W && gy < H) {
-      pk = pas_in[fbase + (int64_t)gy * W + gx] != 0;
+      const uint32_t b = __ballot_sync(0xffffffffu, pk);
+      if (lane == 0) bits[rw] = b;
     }
-    Pbits |= (pk ? 1u : 0u) << k;
-    const uint32_t b = __ballot_sync(0xffffffffu, pk);
-    const uint32_t starts = b & ~(b << 1);
-    const uint32_t upto = starts & (0xffffffffu >> (31 - lane));
-    L[ly * kCT + lane] = pk ? ly * kCT + (31 - __clz(upto)) : -1;
-    if (lane == 0) rowbits[ly] = b;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < kRowsPerWarp; ++k) {
-    const int ly = warp + 8 * k;
-    if (!((Pbits >> k) & 1u) || ly == 0) continue;
-    const uint32_t b = rowbits[ly], up = rowbits[ly - 1];
-    const bool left = lane > 0 && ((b >> (lane - 1)) & 1u);
-    const bool right = lane < 31 && ((b >> (lane + 1)) & 1u);
-    const bool u = (up >> lane) & 1u;
-    const bool ul = lane > 0 && ((up >> (lane - 1)) & 1u);
-    const bool ur = lane < 31 && ((up >> (lane + 1)) & 1u);
-    const int i = ly * kCT + lane;
-    // a run shares its connections: only the pixels whose upper neighbours are
-    // not already reached through the horizontal neighbour do the union
-    if (u) {
-      if (!(left && ul)) uf_unite(L, i, i - kCT);
-    } else {
-      if (ul && !left) uf_unite(L, i, i - kCT - 1);
-      if (ur && !right) uf_unite(L, i, i - kCT + 1);
+  } else {
+    for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
+      const int r = rw >> 2, c = (rw & 3) * 32 + lane;
+      const int gx = x0 + c, gy = y0 + r;
+      const bool pk = gx < W && gy < H && pas_in[fbase + (int64_t)gy * W + gx] != 0;
+      const uint32_t b = __ballot_sync(0xffffffffu, pk);
+      if (lane == 0) bits[rw] = b;
     }
   }
   __syncthreads();
+  {
+    const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
+    if (y0 + r < H && wc < ws.WW)
+      ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc] = bits[tid];
+  }
+
+  int32_t* L = smem;
+  tile_union_find(L, bits, flag, tid);
+
+  // seam rows / columns: frame index of each border pixel's root, -1 if not passable
+  const int64_t seam_row = ((int64_t)blockIdx.z * ws.n_ty + ty) * W;
+  const int64_t seam_col = ((int64_t)blockIdx.z * ws.n_tx + tx) * H;
+  if (warp < 2) {
+    const int r = warp == 0 ? 0 : kLTH - 1;
+    int32_t* dst = (warp == 0 ? ws.top : ws.bot) + seam_row;
+    if (y0 + r < H) {
 #pragma unroll
-  for (int k = 0; k < kRowsPerWarp; ++k) {
-    const int ly = warp + 8 * k;
-    const int gx = x0 + lane, gy = y0 + ly;
-    if (gx >= W || gy >= H) continue;
-    int32_t out = -1;
-    if ((Pbits >> k) & 1u) {
-      const int root = uf_find(L, ly * kCT + lane);
-      out = (y0 + (root >> 5)) * W + x0 + (root & 31);
+      for (int w = 0; w < kLWords; ++w) {
+        const uint32_t A = bits[r * kLWords + w];
+        const int gx = x0 + w * 32 + lane;
+        if (gx < W) {
+          int32_t v = -1;
+          if ((A >> lane) & 1u)
+            v = frame_index(L[r * kLTW + w * 32 + start_of(run_starts(A), lane)], x0, y0, W);
+          dst[gx] = v;
+        }
+      }
     }
-    labels[fbase + (int64_t)gy * W + gx] = out;
+  } else if (warp < 4) {
+    // warp 2: first column, warp 3: last column; lanes <-> rows
+    for (int r = lane; r < kLTH; r += 32) {
+      if (y0 + r >= H) break;
+      int32_t v = -1;
+      if (warp == 2) {
+        const uint32_t A = bits[r * kLWords];
+        if (A & 1u) v = frame_index(L[r * kLTW], x0, y0, W);
+        ws.left[seam_col + y0 + r] = v;
+      } else {
+        const uint32_t A = bits[r * kLWords + kLWords - 1];
+        if (A >> 31)
+          v = frame_index(L[r * kLTW + (kLWords - 1) * 32 + (31 - __clz(run_starts(A)))], x0, y0,
+                          W);
+        ws.right[seam_col + y0 + r] = v;
+      }
+    }
+  }
+  // global union-find nodes: border-touching roots only
+  {
+    const int r = tid >> 2, w = tid & 3;
+    const int base = r * kLTW + w * 32;
+    int32_t* G = labels + fbase;
+    for (uint32_t m = run_starts(bits[tid]); m; m &= m - 1u) {
+      const int n = base + __ffs(m) - 1;
+      if (L[n] == n && ((flag[n >> 5] >> (n & 31)) & 1u)) {
+        const int g = frame_index(n, x0, y0, W);
+        G[g] = g;
+      }
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// 2. merge across tile edges (global union-find on the label array)
+// 2. seams between tiles (global union-find on G = labels)
 //
-// One thread per pixel on the first column / first row of a tile (except the
-// image's own first column / row).  Same pruning as the in-tile rule: the
-// pixel unites with its straight neighbour across the edge if passable, else
-// with the diagonal ones not already reached through its along-edge neighbour.
+// Horizontal seams: pixel (x, y) in the last row of tile row ty against
+// (x-1 .. x+1, y+1) in the first row of tile row ty+1 -- diagonals across tile
+// columns included, so tile corners need no extra case.  Vertical seams:
+// (x, y) in the last column of tile column tx against (x+1, y-1 .. y+1).
+// A straight neighbour makes the diagonal links redundant (the diagonal
+// pixels are 8-adjacent to it along the seam row/column).
 
-__global__ void ccl_merge_kernel(const CclParams p, int32_t* __restrict__ labels, int n_col,
-                                 int n_row) {
+__global__ void ccl_seam_kernel(const CclParams p, const CclWorkspace ws,
+                                int32_t* __restrict__ labels) {
   const int W = (int)p.W, H = (int)p.H;
-  const int per_frame = n_col + n_row;
-  const int64_t total = (int64_t)per_frame * p.B;
+  const int64_t n_h = (int64_t)(ws.n_ty - 1) * W;  // horizontal seam positions per frame
+  const int64_t n_v = (int64_t)(ws.n_tx - 1) * H;
+  const int64_t per_frame = n_h + n_v;
+  const int64_t total = per_frame * p.B;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int f = (int)(idx / per_frame);
-    int r = (int)(idx - (int64_t)f * per_frame);
-    int32_t* L = labels + (int64_t)f * p.H * p.W;
-    volatile int32_t* V = L;
-    if (r < n_col) {
-      // vertical tile edge at x = (r / H + 1) * 32; across-edge neighbours at x - 1
-      const int y = r % H;
-      const int x = (r / H + 1) * kCT;
-      const int i = y * W + x;
-      if (V[i] < 0) continue;
-      // pruning may only lean on an along-edge neighbour of the SAME tile
-      // (already connected by ccl_local); across a tile corner both links stay
-      const bool up_same = (y % kTY) != 0, down_same = ((y + 1) % kTY) != 0;
-      if (V[i - 1] >= 0) {
-        if (!(up_same && V[i - W] >= 0 && V[i - W - 1] >= 0)) uf_unite(L, i, i - 1);
-      } else {
-        if (y > 0 && V[i - W - 1] >= 0 && !(up_same && V[i - W] >= 0)) uf_unite(L, i, i - W - 1);
-        if (y + 1 < H && V[i + W - 1] >= 0 && !(down_same && V[i + W] >= 0))
-          uf_unite(L, i, i + W - 1);
-      }
+    const int64_t f = idx / per_frame;
+    int64_t k = idx - f * per_frame;
+    int32_t* G = labels + f * p.H * p.W;
+    const int32_t* a_row;
+    const int32_t* b_row;
+    int i, n;
+    if (k < n_h) {
+      const int s = (int)(k / W);
+      i = (int)(k - (int64_t)s * W);
+      n = W;
+      a_row = ws.bot + (f * ws.n_ty + s) * W;
+      b_row = ws.top + (f * ws.n_ty + s + 1) * W;
     } else {
-      // horizontal tile edge at y = (r / W + 1) * kTY; neighbours in row y - 1
-      r -= n_col;
-      const int x = r % W;
-      const int y = (r / W + 1) * kTY;
-      const int i = y * W + x;
-      if (V[i] < 0) continue;
-      const bool left_same = (x % kCT) != 0, right_same = ((x + 1) % kCT) != 0;
-      const bool left = x > 0 && V[i - 1] >= 0;
-      const bool right = x + 1 < W && V[i + 1] >= 0;
-      if (V[i - W] >= 0) {
-        if (!(left_same && left && V[i - W - 1] >= 0)) uf_unite(L, i, i - W);
-      } else {
-        if (x > 0 && V[i - W - 1] >= 0 && !(left_same && left)) uf_unite(L, i, i - W - 1);
-        if (x + 1 < W && V[i - W + 1] >= 0 && !(right_same && right)) uf_unite(L, i, i - W + 1);
+      k -= n_h;
+      const int s = (int)(k / H);
+      i = (int)(k - (int64_t)s * H);
+      n = H;
+      a_row = ws.right + (f * ws.n_tx + s) * H;
+      b_row = ws.left + (f * ws.n_tx + s + 1) * H;
+    }
+    const int32_t a = a_row[i];
+    if (a < 0) continue;
+    const int32_t b = b_row[i];
+    if (b >= 0) {
+      if (a != b) uf_unite(G, a, b);
+    } else {
+      if (i > 0) {
+        const int32_t bl = b_row[i - 1];
+        if (bl >= 0 && bl != a) uf_unite(G, a, bl);
+      }
+      if (i + 1 < n) {
+        const int32_t br = b_row[i + 1];
+        if (br >= 0 && br != a) uf_unite(G, a, br);
       }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// 3. flatten (+ optional raster-index offset for strips, second pass)
+// 3. resolve: tile union-find again from the bits, border roots through G,
+// one coalesced label store per pixel
 
-__global__ void ccl_flatten_kernel(const CclParams p, int32_t* __restrict__ labels) {
-  const int64_t total = p.B * p.H * p.W;
-  const int64_t HW = p.H * p.W;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int32_t* L = labels + (idx / HW) * HW;
-    const int i = (int)(idx % HW);
-    const int v = L[i];
-    if (v >= 0 && v != i) L[i] = uf_root(L, v);
+__global__ void __launch_bounds__(kLThreads)
+    ccl_resolve_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
+  __shared__ __align__(16) int32_t L[kLTH * kLTW];
+  __shared__ uint32_t bits[kLThreads];
+  __shared__ uint32_t flag[kLThreads];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int W = (int)p.W, H = (int)p.H;
+  const int tx = blockIdx.x, ty = blockIdx.y;
+  const int x0 = tx * kLTW, y0 = ty * kLTH;
+  const int64_t fbase = (int64_t)blockIdx.z * p.H * p.W;
+  {
+    const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
+    bits[tid] = (y0 + r < H && wc < ws.WW)
+                    ? ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc]
+                    : 0u;
+  }
+  __syncthreads();
+  tile_union_find(L, bits, flag, tid);
+
+  // border-touching roots: final root through the global forest.  Nodes are
+  // only ever roots of tile components, and a concurrent resolve of another
+  // tile overwrites such a node with its final label -- an ancestor -- so the
+  // read-only walk stays valid.
+  {
+    const int r = tid >> 2, w = tid & 3;
+    const int base = r * kLTW + w * 32;
+    const volatile int32_t* G = labels + fbase;
+    for (uint32_t m = run_starts(bits[tid]); m; m &= m - 1u) {
+      const int n = base + __ffs(m) - 1;
+      if (L[n] == n && ((flag[n >> 5] >> (n & 31)) & 1u))
+        L[n] = -2 - uf_root(G, frame_index(n, x0, y0, W));
+    }
+  }
+  __syncthreads();
+  int32_t* out = labels + fbase;
+  for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
+    const int r = rw >> 2, w = rw & 3;
+    const int gx = x0 + w * 32 + lane, gy = y0 + r;
+    if (gx >= W || gy >= H) continue;
+    const uint32_t A = bits[rw];
+    int32_t lab = -1;
+    if ((A >> lane) & 1u) {
+      const int n = r * kLTW + w * 32 + start_of(run_starts(A), lane);
+      const int v = L[n];
+      if (v < 0) {
+        lab = -2 - v;
+      } else {
+        const int v2 = L[v];
+        lab = v2 < 0 ? -2 - v2 : frame_index(v, x0, y0, W);
+      }
+    }
+    out[(int64_t)gy * W + gx] = lab;
   }
 }
 
@@ -330,6 +556,29 @@ static unsigned grid_for(const LaunchCtx& ctx, int64_t n, int threads) {
   return (unsigned)g;
 }
 
+CclParams make_ccl_params(int64_t B, int64_t H, int64_t W, double fxb, double t) {
+  CclParams p{};
+  p.B = B;
+  p.H = H;
+  p.W = W;
+  p.fxb = fxb;
+  p.t = t;
+  p.fxb_f = (float)fxb;
+  p.t_f = (float)t;
+  // the filter's error bound assumes normal fp32 operands (fxb_f, t_f, zf)
+  p.exact_only = !(fxb >= 1e-20 && fxb <= 1e20 && t >= 1e-30 && t <= 1e30);
+  return p;
+}
+
+static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W) {
+  const int64_t WW = (W + 31) / 32;
+  const int64_t n_tx = (W + kLTW - 1) / kLTW, n_ty = (H + kLTH - 1) / kLTH;
+  return align256((size_t)(B * H * WW) * 4) + 2 * align256((size_t)(B * n_ty * W) * 4) +
+         2 * align256((size_t)(B * n_tx * H) * 4);
+}
+
 int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, uint8_t* pas,
                  double* edges) {
   const int64_t n = p.B * p.H * p.W;
@@ -339,25 +588,43 @@ int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, ui
 }
 
 int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const CclParams& p,
-            int64_t index_base, int32_t* labels) {
+            int64_t index_base, int32_t* labels, void* workspace, size_t ws_bytes) {
   const int64_t n = p.B * p.H * p.W;
   if (n == 0) return SN_OK;
-  if (p.H * p.W > 0x7fffffffLL || p.B > 65535) return set_error(SN_EINVAL, "frame too large for int32 labels");
-  dim3 grid((unsigned)((p.W + kCT - 1) / kCT), (unsigned)((p.H + kTY - 1) / kTY), (unsigned)p.B);
-  ccl_local_kernel<<<grid, kCclThreads, 0, ctx.stream>>>(disp, pas, p, labels);
-  int rc = check_launch("ccl_local_kernel");
+  if (p.H * p.W > 0x7fffffffLL || p.B > 65535)
+    return set_error(SN_EINVAL, "frame too large for int32 labels");
+  if (!workspace || ws_bytes < ccl_workspace_bytes(p.B, p.H, p.W))
+    return set_error(SN_EINVAL, "labeller workspace too small (%zu < %zu bytes)", ws_bytes,
+                     ccl_workspace_bytes(p.B, p.H, p.W));
+  CclWorkspace ws;
+  ws.WW = (int)((p.W + 31) / 32);
+  ws.n_tx = (int)((p.W + kLTW - 1) / kLTW);
+  ws.n_ty = (int)((p.H + kLTH - 1) / kLTH);
+  uint8_t* q = static_cast<uint8_t*>(workspace);
+  ws.bits = reinterpret_cast<uint32_t*>(q);
+  q += align256((size_t)(p.B * p.H * ws.WW) * 4);
+  ws.top = reinterpret_cast<int32_t*>(q);
+  q += align256((size_t)(p.B * ws.n_ty * p.W) * 4);
+  ws.bot = reinterpret_cast<int32_t*>(q);
+  q += align256((size_t)(p.B * ws.n_ty * p.W) * 4);
+  ws.left = reinterpret_cast<int32_t*>(q);
+  q += align256((size_t)(p.B * ws.n_tx * p.H) * 4);
+  ws.right = reinterpret_cast<int32_t*>(q);
+
+  dim3 grid((unsigned)ws.n_tx, (unsigned)ws.n_ty, (unsigned)p.B);
+  if (disp)
+    ccl_tile_kernel<0><<<grid, kLThreads, 0, ctx.stream>>>(disp, nullptr, p, ws, labels);
+  else
+    ccl_tile_kernel<1><<<grid, kLThreads, 0, ctx.stream>>>(nullptr, pas, p, ws, labels);
+  int rc = check_launch("ccl_tile_kernel");
   if (rc) return rc;
-  const int n_col = (int)(((p.W - 1) / kCT) * p.H);
-  const int n_row = (int)(((p.H - 1) / kTY) * p.W);
-  if (n_col + n_row > 0) {
-    ccl_merge_kernel<<<grid_for(ctx, (int64_t)(n_col + n_row) * p.B, 256), 256, 0, ctx.stream>>>(
-        p, labels, n_col, n_row);
-    rc = check_launch("ccl_merge_kernel");
-    if (rc) return rc;
-    ccl_flatten_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(p, labels);
-    rc = check_launch("ccl_flatten_kernel");
-    if (rc) return rc;
+  const int64_t n_seam = ((int64_t)(ws.n_ty - 1) * p.W + (int64_t)(ws.n_tx - 1) * p.H) * p.B;
+  if (n_seam > 0) {
+    ccl_seam_kernel<<<grid_for(ctx, n_seam, 256), 256, 0, ctx.stream>>>(p, ws, labels);
+    if ((rc = check_launch("ccl_seam_kernel"))) return rc;
   }
+  ccl_resolve_kernel<<<grid, kLThreads, 0, ctx.stream>>>(p, ws, labels);
+  if ((rc = check_launch("ccl_resolve_kernel"))) return rc;
   if (index_base != 0) {
     add_offset_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(labels, n, index_base);
     rc = check_launch("add_offset_kernel");

@@ -24,7 +24,8 @@ struct FixedParams {
   float u0_hi, u0_lo, v0_hi, v0_lo;  // two-float split of u0, v0
   // integer moments of the offset pattern (exact in double)
   double alpha, beta, gamma, det, sx, sy;
-  int R;  // square radius (fast path)
+  int R;     // square radius (fast path)
+  int row0;  // image row of the block's first row (strips of a larger frame)
 };
 
 // ---------------------------------------------------------------------------

@@ -270,8 +270,9 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 
       const int yg = y0 + g;
       const int xb = x0 + colbase;
-      const double dv = (double)yg - p.v0;
-      const float dv_f = ((float)yg - p.v0_hi) - p.v0_lo;
+      const int yv = p.row0 + yg;  // image row (strips: block row + offset)
+      const double dv = (double)yv - p.v0;
+      const float dv_f = ((float)yv - p.v0_hi) - p.v0_lo;
       const double du0 = (double)xb - p.u0;
       const float du_hi = (float)xb - p.u0_hi;  // exact; + j stays exact
       const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
@@ -427,13 +428,14 @@ __global__ void __launch_bounds__(256)
       float px, py, pz, nx, ny, nz;
       if constexpr (sizeof(T) == 4) {
         const float du_f = ((float)x - p.u0_hi) - p.u0_lo;
-        const float dv_f = ((float)y - p.v0_hi) - p.v0_lo;
+        const float dv_f = ((float)(y + p.row0) - p.v0_hi) - p.v0_lo;
         point_from_disparity((float)dc, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
       } else {
-        point_from_disparity_f64(dcd, (double)x - p.u0, (double)y - p.v0, p, px, py, pz);
+        point_from_disparity_f64(dcd, (double)x - p.u0, (double)(y + p.row0) - p.v0, p, px, py,
+                                 pz);
       }
       if (valid) {
-        normal_from_moments(P1, P2, p.det, dcd, (double)x - p.u0, (double)y - p.v0, p.fx, p.fy, nx,
+        normal_from_moments(P1, P2, p.det, dcd, (double)x - p.u0, (double)(y + p.row0) - p.v0, p.fx, p.fy, nx,
                             ny, nz);
       } else {
         nx = ny = nz = __int_as_float(0x7fc00000);

@@ -40,14 +40,20 @@ int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const s
 
 struct CclParams {
   int64_t B, H, W;
-  double fxb;  // fx * b in Python's double order (geometry.py:43)
-  double t;    // ST threshold
+  double fxb;       // fx * b in Python's double order (geometry.py:43)
+  double t;         // ST threshold
+  float fxb_f;      // fp32(fxb) for the filtered predicate
+  float t_f;        // fp32(t)
+  int exact_only;   // fxb outside the filter's range: every pixel takes the fp64 path
 };
+
+CclParams make_ccl_params(int64_t B, int64_t H, int64_t W, double fxb, double t);
+size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W);
 
 int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, uint8_t* passable,
                  double* edges);
 int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* passable, const CclParams& p,
-            int64_t index_base, int32_t* labels);
+            int64_t index_base, int32_t* labels, void* workspace, size_t ws_bytes);
 int run_relabel(const LaunchCtx& ctx, int32_t* labels, int64_t n, int64_t base,
                 const int32_t* keys, const int32_t* vals, const int32_t* n_map, int32_t cap,
                 int32_t* scratch);

@@ -61,12 +61,14 @@ def _check_out(t: torch.Tensor | None, shape, dtype, dev, name):
 
 
 def oriented_points(disparity: torch.Tensor, rig, kernels=9, *, out: torch.Tensor | None = None,
-                    mask: torch.Tensor | None = None, generic: bool = False) -> torch.Tensor:
+                    mask: torch.Tensor | None = None, generic: bool = False,
+                    row0: int = 0) -> torch.Tensor:
     """Fused fit + normal + triangulation: returns ``[B, H, W, 6]`` fp32 (always
     batched; a 2D input gives B = 1)
     ``(x, y, z, nx, ny, nz)``; NaN normals where invalid, NaN points where
     the disparity is not finite and positive.  ``mask`` (uint8 ``[B, H, W]``)
-    optionally receives the normal validity."""
+    optionally receives the normal validity.  ``row0`` is the image row of
+    the first input row when the input is a strip of a taller image (fp32)."""
     d = _batched(disparity)
     B, H, W = d.shape
     dev = d.device
@@ -84,8 +86,17 @@ def oriented_points(disparity: torch.Tensor, rig, kernels=9, *, out: torch.Tenso
     else:
         raise ValueError(f"disparity dtype must be float32 or float64, got {d.dtype}")
     rs = _native.rig_struct(rig)
+    mptr = mask.data_ptr() if mask is not None else None
+    if row0:
+        if d.dtype != torch.float32 or generic:
+            raise ValueError("row0 is supported on the fp32 fast path only")
+        rc = lib.sn_oriented_points_rows(_native.plan(dev.index), d.data_ptr(), B, H, W, int(row0),
+                                         ctypes.byref(rs), off.ctypes.data, len(off),
+                                         out.data_ptr(), mptr, _stream(dev))
+        check(rc, "oriented_points")
+        return out
     rc = fn(_native.plan(dev.index), d.data_ptr(), B, H, W, ctypes.byref(rs), off.ctypes.data,
-            len(off), out.data_ptr(), mask.data_ptr() if mask is not None else None, _stream(dev))
+            len(off), out.data_ptr(), mptr, _stream(dev))
     check(rc, "oriented_points")
     return out
 
@@ -135,8 +146,23 @@ def passable(disparity: torch.Tensor, rig, threshold: float, *, out=None, edges=
     return (out, edges) if want_edges else out
 
 
+def ccl_workspace(B: int, H: int, W: int, dev: torch.device) -> torch.Tensor:
+    """Device scratch for the labeller (bit mask + tile seams), from torch's
+    caching allocator so concurrent streams never share one."""
+    return torch.empty(_native.ccl_workspace_bytes(B, H, W), dtype=torch.uint8, device=dev)
+
+
+def _workspace(ws, B, H, W, dev):
+    need = _native.ccl_workspace_bytes(B, H, W)
+    if ws is None:
+        return torch.empty(need, dtype=torch.uint8, device=dev)
+    if ws.device != dev or not ws.is_contiguous() or ws.numel() * ws.element_size() < need:
+        raise ValueError(f"workspace must be a contiguous buffer of >= {need} bytes on {dev}")
+    return ws
+
+
 def component_labels(disparity: torch.Tensor, rig, threshold: float, *, out=None,
-                     row_base: int = 0) -> torch.Tensor:
+                     row_base: int = 0, workspace: torch.Tensor | None = None) -> torch.Tensor:
     """8-connected labels of the ST-passable set: int32 ``[B, H, W]`` holding
     the smallest raster index ``v*W + u`` (+ ``row_base*W``) of each pixel's
     component, -1 where not passable."""
@@ -144,15 +170,18 @@ def component_labels(disparity: torch.Tensor, rig, threshold: float, *, out=None
     B, H, W = d.shape
     dev = d.device
     out = _check_out(out, (B, H, W), torch.int32, dev, "out")
+    ws = _workspace(workspace, B, H, W, dev)
     rs = _native.rig_struct(rig)
-    rc = _native.load().sn_ccl_labels(_native.plan(dev.index), d.data_ptr(), B, H, W,
-                                      ctypes.byref(rs), float(threshold), int(row_base),
-                                      out.data_ptr(), _stream(dev))
+    rc = _native.load().sn_ccl_labels_ws(_native.plan(dev.index), d.data_ptr(), B, H, W,
+                                         ctypes.byref(rs), float(threshold), int(row_base),
+                                         out.data_ptr(), ws.data_ptr(),
+                                         ws.numel() * ws.element_size(), _stream(dev))
     check(rc, "component_labels")
     return out
 
 
-def labels_from_passable(p: torch.Tensor, *, out=None, row_base: int = 0) -> torch.Tensor:
+def labels_from_passable(p: torch.Tensor, *, out=None, row_base: int = 0,
+                         workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Label an existing uint8/bool passable grid ``[B, H, W]``."""
     p = _batched(p, "passable")
     if p.dtype == torch.bool:
@@ -162,8 +191,10 @@ def labels_from_passable(p: torch.Tensor, *, out=None, row_base: int = 0) -> tor
     B, H, W = p.shape
     dev = p.device
     out = _check_out(out, (B, H, W), torch.int32, dev, "out")
-    rc = _native.load().sn_ccl_from_passable(_native.plan(dev.index), p.data_ptr(), B, H, W,
-                                             int(row_base), out.data_ptr(), _stream(dev))
+    ws = _workspace(workspace, B, H, W, dev)
+    rc = _native.load().sn_ccl_from_passable_ws(_native.plan(dev.index), p.data_ptr(), B, H, W,
+                                                int(row_base), out.data_ptr(), ws.data_ptr(),
+                                                ws.numel() * ws.element_size(), _stream(dev))
     check(rc, "labels_from_passable")
     return out
 

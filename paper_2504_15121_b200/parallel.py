@@ -141,7 +141,8 @@ def strip_points(block, plan: StripPlan, s: int, rig, kernels=9, *, out=None):
     from . import device
 
     o0, o1 = plan.owned_in_block(s)
-    res = device.oriented_points(block, rig, kernels, out=out)
+    b0, _ = plan.block(s)
+    res = device.oriented_points(block, rig, kernels, out=out, row0=b0)
     return res[0, o0:o1]
 
 

@@ -215,3 +215,38 @@ def test_labeller_random_grids(cuda_dev, shape, density):
     lab = device.labels_from_passable(torch.from_numpy(p).to(cuda_dev)).cpu().numpy()
     for i in range(3):
         assert np.array_equal(lab[i].astype(np.int64), label_components(p[i]))
+
+
+@pytest.mark.parametrize("pick", ["exact_tie", "exact_only_rig", "tiny_and_huge"])
+def test_labels_filter_edge_cases(cuda_dev, pick):
+    """The fp32 predicate filter must defer to the exact fp64 decision:
+    thresholds equal to an edge value (e <= t ties), a rig whose fx*b leaves
+    the filter's range, and disparities that leave fp32's comfortable range."""
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import device, scenes
+    from paper_2504_15121_b200.geometry import StereoRig
+    sc = scenes.street_scene(384, 200)
+    d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.5, 9).astype(np.float32)
+    rig = sc.rig
+    if pick == "exact_only_rig":
+        rig = StereoRig(rig.fx * 1e12, rig.fy, rig.u0, rig.v0, rig.baseline * 1e10)
+    if pick == "tiny_and_huge":
+        rng = np.random.default_rng(4)
+        sel = rng.random(d.shape)
+        d[sel < 0.02] = 1e-38
+        d[(sel >= 0.02) & (sel < 0.04)] = 3e38
+        d[(sel >= 0.04) & (sel < 0.05)] = 1e-44  # subnormal
+        d[(sel >= 0.05) & (sel < 0.06)] = -3.0
+    o = orc.Rig(rig.fx, rig.fy, rig.u0, rig.v0, rig.baseline)
+    d64 = d.astype(np.float64)
+    z, zm = orc.depth_field(d64, o)
+    e, em = orc.depth_laplacian(z, zm)
+    ts = [0.2, 1.0]
+    if pick == "exact_tie":
+        vals = np.sort(e[em])
+        ts = [float(vals[len(vals) // 4]), float(vals[len(vals) // 2]), float(vals[-1])]
+    dt = torch.from_numpy(d).to(cuda_dev)
+    for t in ts:
+        lab = device.component_labels(dt, rig, t)[0].cpu().numpy().astype(np.int64)
+        ref = orc.ccl_labels(d64, o, t)
+        assert np.array_equal(lab, ref), t
