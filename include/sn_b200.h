@@ -99,6 +99,27 @@ SN_API int sn_oriented_points_rows(sn_plan_t* plan, const float* disp, int64_t B
                             const int32_t* offsets_xy, int32_t n_off, float* out6,
                             uint8_t* mask, void* stream);
 
+/* Same pass + the ST-passable bit mask in the same read of the disparity
+ * (adaptive.py:80-97,130-132; threshold t > 0): bits is [B][H][ceil(W/32)]
+ * uint32, bit (u % 32) of word u / 32 set iff pixel u of the row is passable.
+ * row0 as for sn_oriented_points_rows. */
+SN_API int sn_oriented_points_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
+                            int64_t W, int64_t row0, const sn_rig_t* rig,
+                            const int32_t* offsets_xy, int32_t n_off, double t, float* out6,
+                            uint8_t* mask, uint32_t* bits, void* stream);
+
+/* The whole north-star pipeline in one call: fused fit + normal + point +
+ * passable bits, then component labels from the bits (label semantics as
+ * sn_ccl_labels with row_base 0).  Device pointers.  The _ws variant takes a
+ * caller workspace of sn_ccl_workspace_bytes(B, H, W) bytes. */
+SN_API int sn_pipeline(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                float* out6, uint8_t* mask, int32_t* labels, void* stream);
+SN_API int sn_pipeline_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                   const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                   float* out6, uint8_t* mask, int32_t* labels, void* workspace,
+                   size_t ws_bytes, void* stream);
+
 /* Same pass, host buffers: pinned staging + overlapped H2D / compute / D2H,
  * returns when out6 (and mask, if non-NULL) hold the result. */
 SN_API int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
@@ -143,6 +164,11 @@ SN_API int sn_ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes
 SN_API int sn_ccl_labels_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                      const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
                      void* workspace, size_t ws_bytes, void* stream);
+/* Label from a passable bit mask (layout of sn_oriented_points_bits); the
+ * workspace's own bit-mask region is unused. */
+SN_API int sn_ccl_from_bits_ws(sn_plan_t* plan, const uint32_t* bits, int64_t B, int64_t H,
+                        int64_t W, int64_t row_base, int32_t* labels, void* workspace,
+                        size_t ws_bytes, void* stream);
 SN_API int sn_ccl_from_passable_ws(sn_plan_t* plan, const uint8_t* passable, int64_t B,
                             int64_t H, int64_t W, int64_t row_base, int32_t* labels,
                             void* workspace, size_t ws_bytes, void* stream);

@@ -147,6 +147,21 @@ void fill_rig(FixedParams& p, const sn_rig_t* rig) {
   p.v0_lo = (float)(rig->v0 - (double)p.v0_hi);
 }
 
+}  // namespace
+
+void sn::fill_predicate(FixedParams& p, double fxb, double t, uint32_t* bits) {
+  p.bits = bits;
+  p.bits_ww = (int)((p.W + 31) / 32);
+  p.t = t;
+  p.t_f = (float)t;
+  p.fxb_pf = (float)fxb;
+  // the filter's ranges (sn_common.cuh pred_bit): K and t in [2^-40, 2^40]
+  const double lo = 9.094947017729282e-13, hi = 1099511627776.0;
+  p.pred_exact = !(fxb >= lo && fxb <= hi && t >= lo && t <= hi);
+}
+
+namespace {
+
 int prepare(const int32_t* offsets_xy, int32_t n_off, sn_moments_t& m, OffsetTable& tab) {
   int rc = sn_kernel_moments(offsets_xy, n_off, &m);
   if (rc) return rc;
@@ -179,7 +194,7 @@ template <typename T>
 int oriented_points_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
                          const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
                          float* out6, uint8_t* mask, void* stream, int force_generic,
-                         int64_t row0 = 0) {
+                         int64_t row0 = 0, uint32_t* bits = nullptr, double t = 0.0) {
   if (!plan) return set_error(SN_EINVAL, "plan is NULL");
   if (row0 < 0 || row0 + H > 0x7fffffffLL) return set_error(SN_EINVAL, "row offset out of range");
   int rc = check_shape(B, H, W);
@@ -196,6 +211,10 @@ int oriented_points_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, i
   fill_rig(p, rig);
   fill_moments(p, m);
   p.row0 = (int)row0;
+  if (bits) {
+    if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
+    fill_predicate(p, p.fxb, t, bits);
+  }
   DeviceGuard g(plan->device);
   return run_fixed<T>(make_ctx(plan, stream), disp, p, m, tab, out6, mask, nullptr, nullptr, false,
                       force_generic);
@@ -330,6 +349,15 @@ int sn_oriented_points_rows(sn_plan_t* plan, const float* disp, int64_t B, int64
                                      stream, 0, row0);
 }
 
+int sn_oriented_points_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                            int64_t row0, const sn_rig_t* rig, const int32_t* offsets_xy,
+                            int32_t n_off, double t, float* out6, uint8_t* mask, uint32_t* bits,
+                            void* stream) {
+  if (B * H * W > 0 && !bits) return set_error(SN_EINVAL, "NULL bit-mask buffer");
+  return oriented_points_impl<float>(plan, disp, B, H, W, rig, offsets_xy, n_off, out6, mask,
+                                     stream, 0, row0, bits, t);
+}
+
 /* test hook: force the generic (non-TMA) kernel, to cross-check the fast path */
 int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                                const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
@@ -448,6 +476,48 @@ int sn_ccl_from_passable(sn_plan_t* plan, const uint8_t* passable, int64_t B, in
   size_t bytes = 0;
   if ((rc = plan_workspace(plan, B, H, W, &ws, &bytes))) return rc;
   return sn_ccl_from_passable_ws(plan, passable, B, H, W, row_base, labels, ws, bytes, stream);
+}
+
+int sn_ccl_from_bits_ws(sn_plan_t* plan, const uint32_t* bits, int64_t B, int64_t H, int64_t W,
+                        int64_t row_base, int32_t* labels, void* workspace, size_t ws_bytes,
+                        void* stream) {
+  int rc = ccl_args(plan, B, H, W, row_base, bits, labels);
+  if (rc) return rc;
+  const CclParams p = make_ccl_params(B, H, W, 0.0, 1.0);
+  DeviceGuard g(plan->device);
+  return run_ccl(make_ctx(plan, stream), nullptr, nullptr, p, row_base * W, labels, workspace,
+                 ws_bytes, bits);
+}
+
+int sn_pipeline_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                   const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                   float* out6, uint8_t* mask, int32_t* labels, void* workspace, size_t ws_bytes,
+                   void* stream) {
+  int rc = ccl_args(plan, B, H, W, 0, disp, labels);
+  if (rc) return rc;
+  if (B * H * W == 0) return SN_OK;
+  if (!workspace || ws_bytes < ccl_workspace_bytes(B, H, W))
+    return set_error(SN_EINVAL, "pipeline workspace too small");
+  // the bit mask lives at the head of the labeller workspace
+  uint32_t* bits = static_cast<uint32_t*>(workspace);
+  if ((rc = sn_oriented_points_bits(plan, disp, B, H, W, 0, rig, offsets_xy, n_off, t, out6, mask,
+                                    bits, stream)))
+    return rc;
+  return sn_ccl_from_bits_ws(plan, bits, B, H, W, 0, labels, workspace, ws_bytes, stream);
+}
+
+int sn_pipeline(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                float* out6, uint8_t* mask, int32_t* labels, void* stream) {
+  int rc = ccl_args(plan, B, H, W, 0, disp, labels);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(plan->mu);
+  DeviceGuard g(plan->device);
+  void* ws = nullptr;
+  size_t bytes = 0;
+  if ((rc = plan_workspace(plan, B, H, W, &ws, &bytes))) return rc;
+  return sn_pipeline_ws(plan, disp, B, H, W, rig, offsets_xy, n_off, t, out6, mask, labels, ws,
+                        bytes, stream);
 }
 
 int sn_relabel(sn_plan_t* plan, int32_t* labels, int64_t n, int64_t index_base,

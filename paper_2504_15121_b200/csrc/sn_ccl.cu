@@ -214,38 +214,47 @@ __device__ __forceinline__ void tile_union_find(int32_t* L, const uint32_t* bits
   flag[tid] = 0u;
   __syncthreads();
 
-  // a run crossing into this word from the left neighbour word
+  // a run crossing into this word from the left neighbour word (chains <= 4)
   if ((A & 1u) && w > 0) {
     const uint32_t Al = bits[tid - 1];
     if (Al >> 31) uf_unite(L, base, base - 32 + (31 - __clz(run_starts(Al))));
   }
-  // runs of the row above (8-connected: the run dilated by one pixel)
-  if (r > 0) {
-    const uint32_t B = bits[tid - kLWords];
-    const uint32_t BL = w > 0 ? bits[tid - kLWords - 1] : 0u;
-    const uint32_t BR = w + 1 < kLWords ? bits[tid - kLWords + 1] : 0u;
-    const uint32_t stB = run_starts(B);
-    const int bbase = base - kLTW;
-    for (uint32_t m = st; m; m &= m - 1u) {
-      const int s = __ffs(m) - 1;
-      const uint32_t hi = 0xffffffffu << s;
-      const uint32_t zer = ~A & hi;  // zeros of A at or above s (bit s itself is set)
-      const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
-      const int n = base + s;
-      uint32_t o = (run | (run << 1) | (run >> 1)) & B;
-      while (o) {
-        const int p = __ffs(o) - 1;
-        uf_unite(L, n, bbase + start_of(stB, p));
-        const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
-        const uint32_t zb = ~B & ~upto;  // zeros of B above p: end of that run
-        if (!zb) break;
-        o &= ~((zb & (0u - zb)) - 1u);
-      }
-      if ((run & 1u) && (BL >> 31)) uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(BL))));
-      if ((run >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
-    }
-  }
   __syncthreads();
+  // rows merge in log2(64) rounds, like a reduction tree: round k joins the
+  // blocks of 2^k rows that meet at rows r = 2^k (mod 2^(k+1)).  Joining all
+  // rows at once would link every run to the run above it concurrently and
+  // build chains as long as the tile is high; in rounds a node's depth grows
+  // by at most one per round.
+  const uint32_t B = r > 0 ? bits[tid - kLWords] : 0u;
+  const uint32_t BL = (r > 0 && w > 0) ? bits[tid - kLWords - 1] : 0u;
+  const uint32_t BR = (r > 0 && w + 1 < kLWords) ? bits[tid - kLWords + 1] : 0u;
+  const int my_round = r > 0 ? __ffs(r) - 1 : -1;  // round in which row r joins row r - 1
+#pragma unroll 1
+  for (int k = 0; (1 << k) < kLTH; ++k) {
+    if (my_round == k && (A & (B | (B << 1) | (B >> 1) | (BL >> 31) | (BR << 31)))) {
+      const uint32_t stB = run_starts(B);
+      const int bbase = base - kLTW;
+      for (uint32_t m = st; m; m &= m - 1u) {
+        const int s = __ffs(m) - 1;
+        const uint32_t hi = 0xffffffffu << s;
+        const uint32_t zer = ~A & hi;  // zeros of A at or above s (bit s itself is set)
+        const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+        const int n = base + s;
+        uint32_t o = (run | (run << 1) | (run >> 1)) & B;
+        while (o) {
+          const int p = __ffs(o) - 1;
+          uf_unite(L, n, bbase + start_of(stB, p));
+          const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
+          const uint32_t zb = ~B & ~upto;  // zeros of B above p: end of that run
+          if (!zb) break;
+          o &= ~((zb & (0u - zb)) - 1u);
+        }
+        if ((run & 1u) && (BL >> 31)) uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(BL))));
+        if ((run >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
+      }
+    }
+    __syncthreads();
+  }
   // every node -> its root (only root values are written in this phase)
   for (uint32_t m = st; m; m &= m - 1u) {
     const int n = base + __ffs(m) - 1;
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(kLThreads)
       const uint32_t b = __ballot_sync(0xffffffffu, pk);
       if (lane == 0) bits[rw] = b;
     }
-  } else {
+  } else if (MODE == 1) {
     for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
       const int r = rw >> 2, c = (rw & 3) * 32 + lane;
       const int gx = x0 + c, gy = y0 + r;
@@ -330,9 +339,15 @@ __global__ void __launch_bounds__(kLThreads)
       const uint32_t b = __ballot_sync(0xffffffffu, pk);
       if (lane == 0) bits[rw] = b;
     }
+  } else {
+    // MODE 2: the bit mask is the input (emitted by the fused pass)
+    const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
+    bits[tid] = (y0 + r < H && wc < ws.WW)
+                    ? ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc]
+                    : 0u;
   }
   __syncthreads();
-  {
+  if (MODE != 2) {
     const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
     if (y0 + r < H && wc < ws.WW)
       ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc] = bits[tid];
@@ -587,8 +602,40 @@ int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, ui
   return check_launch("passable_kernel");
 }
 
+// standalone passable bit mask (fallback for the fused emission): one warp
+// per 32-pixel word, the same fp32 filter + fp64 fallback as the fused pass
+__global__ void passable_bits_kernel(const float* __restrict__ disp, const FixedParams p,
+                                     uint32_t* __restrict__ bits) {
+  const int W = (int)p.W, H = (int)p.H;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_words = p.B * p.H * p.bits_ww;
+  for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < n_words;
+       wi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t row = wi / p.bits_ww;
+    const int x = (int)(wi - row * p.bits_ww) * 32 + lane;
+    const int y = (int)(row % p.H);
+    const float* f = disp + (row - y) * p.W;
+    uint32_t pk = 0;
+    if (x >= 1 && x + 1 < W && y >= 1 && y + 1 < H) {
+      const float* c = f + (int64_t)y * W + x;
+      pk = pred_bit(c[0], c[-1], c[1], c[-W], c[W], p);
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, pk != 0u);
+    if (lane == 0) bits[wi] = b;
+  }
+}
+
+int run_passable_bits(const LaunchCtx& ctx, const float* disp, const FixedParams& p,
+                      uint32_t* bits) {
+  const int64_t n = p.B * p.H * p.bits_ww * 32;
+  if (n == 0) return SN_OK;
+  passable_bits_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(disp, p, bits);
+  return check_launch("passable_bits_kernel");
+}
+
 int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const CclParams& p,
-            int64_t index_base, int32_t* labels, void* workspace, size_t ws_bytes) {
+            int64_t index_base, int32_t* labels, void* workspace, size_t ws_bytes,
+            const uint32_t* bits_in) {
   const int64_t n = p.B * p.H * p.W;
   if (n == 0) return SN_OK;
   if (p.H * p.W > 0x7fffffffLL || p.B > 65535)
@@ -611,8 +658,11 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
   q += align256((size_t)(p.B * ws.n_tx * p.H) * 4);
   ws.right = reinterpret_cast<int32_t*>(q);
 
+  if (bits_in) ws.bits = const_cast<uint32_t*>(bits_in);  // read-only in MODE 2
   dim3 grid((unsigned)ws.n_tx, (unsigned)ws.n_ty, (unsigned)p.B);
-  if (disp)
+  if (bits_in)
+    ccl_tile_kernel<2><<<grid, kLThreads, 0, ctx.stream>>>(nullptr, nullptr, p, ws, labels);
+  else if (disp)
     ccl_tile_kernel<0><<<grid, kLThreads, 0, ctx.stream>>>(disp, nullptr, p, ws, labels);
   else
     ccl_tile_kernel<1><<<grid, kLThreads, 0, ctx.stream>>>(nullptr, pas, p, ws, labels);

@@ -26,7 +26,72 @@ struct FixedParams {
   double alpha, beta, gamma, det, sx, sy;
   int R;     // square radius (fast path)
   int row0;  // image row of the block's first row (strips of a larger frame)
+  // optional ST-passable bit mask emitted by the fused pass ([B][H][bits_ww]
+  // uint32, bit u%32 of word u/32 = pixel u of the row); NULL = not wanted
+  uint32_t* bits;
+  int bits_ww;
+  int pred_exact;  // every predicate decision on the fp64 path (filter out of range)
+  double t;        // ST threshold
+  float t_f, fxb_pf;  // fp32 threshold / fx*b for the predicate filter
 };
+
+// ---------------------------------------------------------------------------
+// ST-passable predicate (adaptive.py:80-97,130-132) from raw disparities
+//
+// exact: z_i = fl64(fxb / d_i) (geometry.py:39-45), e = |((((4 z_c - z_l) -
+// z_r) - z_u) - z_d)| with correctly rounded fp64 operations in numpy's
+// order, passable iff all five d finite and > 0 and e <= t.
+
+__device__ __forceinline__ double pred_depth(float d, double fxb) {
+  double z = __longlong_as_double(0x7ff8000000000000ll);
+  if (d > 0.0f && d <= 3.402823466e38f) {
+    const double q = __ddiv_rn(fxb, (double)d);
+    if (fabs(q) <= 1.7976931348623157e308) z = q;
+  }
+  return z;
+}
+
+static __device__ __noinline__ uint32_t pred_exact_d(float a, float b, float c, float e, float f,
+                                             double fxb, double t) {
+  const double zc = pred_depth(a, fxb), zl = pred_depth(b, fxb), zr = pred_depth(c, fxb),
+               zu = pred_depth(e, fxb), zd = pred_depth(f, fxb);
+  if (!(zc == zc && zl == zl && zr == zr && zu == zu && zd == zd)) return 0u;
+  const double ev =
+      fabs(__dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(__dmul_rn(4.0, zc), zl), zr), zu), zd));
+  return ev <= t ? 1u : 0u;
+}
+
+// fp32 filter without divisions.  With every d in [2^-8, 2^16] and K = fx*b:
+//   e = K |4/a - 1/b - 1/c - 1/e - 1/f| = K |N| / D,
+//   N = 4 bcef - a Q,  Q = ef (b + c) + bc (e + f),  D = a bcef > 0,
+// so e <= t  <=>  K |N| <= t D.  In fp32 (u = 2^-24) |N32 - N| <= 6u M with
+// M = 4 bcef + a Q, D32 and the two products carry <= 8u relative error, and
+// the fp64 evaluation of e is within 2^-50 K M / D of the real value; so when
+// |K32 |N32| - t32 D32| > 2^-19 (K32 M32 + t32 D32) -- a 4x margin -- the fp32
+// comparison equals the fp64 one.  The ranges keep every product a normal
+// float (|K| and t in [2^-40, 2^40], host-checked).  Anything else -- an
+// out-of-range sample or a decision inside the margin -- takes pred_exact_d.
+__device__ __forceinline__ uint32_t pred_bit(float a, float b, float c, float e, float f,
+                                             const FixedParams& p) {
+  const uint32_t lo = 0x3b800000u, span = 0x47800000u - 0x3b800000u;  // [2^-8, 2^16)
+  const bool fast = ((__float_as_uint(a) - lo) < span) & ((__float_as_uint(b) - lo) < span) &
+                    ((__float_as_uint(c) - lo) < span) & ((__float_as_uint(e) - lo) < span) &
+                    ((__float_as_uint(f) - lo) < span) & !p.pred_exact;
+  if (fast) {
+    const float bc = __fmul_rn(b, c), ef = __fmul_rn(e, f);
+    const float bcef = __fmul_rn(bc, ef);
+    const float Q = __fadd_rn(__fmul_rn(ef, __fadd_rn(b, c)), __fmul_rn(bc, __fadd_rn(e, f)));
+    const float m4 = __fmul_rn(4.0f, bcef), aQ = __fmul_rn(a, Q);
+    const float X = __fmul_rn(p.fxb_pf, fabsf(__fsub_rn(m4, aQ)));
+    const float Y = __fmul_rn(p.t_f, __fmul_rn(a, bcef));
+    const float margin =
+        __fmul_rn(__fadd_rn(__fmul_rn(p.fxb_pf, __fadd_rn(m4, aQ)), Y), 1.9073486328125e-06f);
+    const float gap = __fsub_rn(X, Y);
+    if (gap > margin) return 0u;
+    if (-gap > margin) return 1u;
+  }
+  return pred_exact_d(a, b, c, e, f, p.fxb, p.t);
+}
 
 // ---------------------------------------------------------------------------
 // PTX wrappers (sm_90+ async proxy; all used on sm_100a)

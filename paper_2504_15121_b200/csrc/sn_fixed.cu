@@ -67,7 +67,8 @@ struct FastCfg {
   static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);  // double2 (C, Rr) [NC][kCP]
   static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;
   static constexpr size_t FL = align_up(CS + CS_BYTES, 16);
-  static constexpr size_t BAR = align_up(FL + (NC + 2) * 4, 16);
+  static constexpr size_t PB = align_up(FL + (NC + 2) * 4, 16);  // passable bytes [kG][16]
+  static constexpr size_t BAR = PB + kG * (kTW / 8);
   static constexpr size_t TOTAL = BAR + 16 + 1024;  // + slack for 1024-B alignment
   static_assert(2 * NC <= kFastThreads + 32, "pass V: at most two units per lane");
   static_assert(NR <= 32, "row validity bits must fit 32 bits");
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double2* CR = reinterpret_cast<double2*>(smem + Cfg::CS);
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
+  uint8_t* pbytes = smem + Cfg::PB;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
   const uint32_t stage_base = smem_u32(smem + Cfg::STAGE);
   const int tid = threadIdx.x;
@@ -356,6 +358,22 @@ __global__ void __launch_bounds__(kFastThreads, 2)
           }
         }
       }
+      if constexpr (sizeof(T) == 4) {
+        if (p.bits != nullptr) {
+          // ST-passable bits of the run (fused: the tile already holds the
+          // 4-neighbourhood; zero-filled samples outside the image are invalid)
+          uint32_t pb = 0;
+          float dl = drow[-1], dc = drow[0];
+#pragma unroll
+          for (int j = 0; j < kRun; ++j) {
+            const float dr = drow[j + 1];
+            pb |= pred_bit(dc, dl, dr, drow[j - BW], drow[j + BW], p) << j;
+            dl = dc;
+            dc = dr;
+          }
+          pbytes[g * (kTW / 8) + q] = (uint8_t)pb;
+        }
+      }
       if (mask_out != nullptr && yg < H) {
         uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
 #pragma unroll 1
@@ -364,6 +382,13 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     }
     fence_proxy_async_smem();
     __syncthreads();
+    if (sizeof(T) == 4 && p.bits != nullptr && tid >= 32 && tid < 32 + kG * (kTW / 32)) {
+      const int gg = (tid - 32) >> 2, wi = (tid - 32) & 3;
+      const int wc = x0 / 32 + wi;
+      if (y0 + gg < H && wc < p.bits_ww)
+        p.bits[((int64_t)bz * H + y0 + gg) * p.bits_ww + wc] =
+            reinterpret_cast<const uint32_t*>(pbytes)[gg * (kTW / 32) + wi];
+    }
     if (tid == 0) {
       fl[NC + buf] = 0u;  // reset this parity's big flag (next used two items later)
 #pragma unroll 1
@@ -547,9 +572,13 @@ int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const s
                        p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
   if (!affine && !force_generic && m.square_r >= 1 && m.square_r <= 8 && aligned) {
     const int rc = dispatch_square<T>(m.square_r, ctx, disp, p, out6, mask);
-    if (rc >= 0) return rc;
+    if (rc >= 0) return rc;  // the fused kernel also emitted p.bits
   }
-  return launch_generic<T>(ctx, disp, p, tab, out6, mask, a1, a2, affine);
+  int rc = launch_generic<T>(ctx, disp, p, tab, out6, mask, a1, a2, affine);
+  if (rc == SN_OK && !affine && p.bits != nullptr) {
+    if constexpr (sizeof(T) == 4) rc = run_passable_bits(ctx, disp, p, p.bits);
+  }
+  return rc;
 }
 
 template int run_fixed<float>(const LaunchCtx&, const float*, const FixedParams&,

@@ -53,7 +53,12 @@ size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W);
 int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, uint8_t* passable,
                  double* edges);
 int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* passable, const CclParams& p,
-            int64_t index_base, int32_t* labels, void* workspace, size_t ws_bytes);
+            int64_t index_base, int32_t* labels, void* workspace, size_t ws_bytes,
+            const uint32_t* bits_in = nullptr);
+int run_passable_bits(const LaunchCtx& ctx, const float* disp, const FixedParams& p,
+                      uint32_t* bits);
+// host-side fill of the predicate fields of FixedParams
+void fill_predicate(FixedParams& p, double fxb, double t, uint32_t* bits);
 int run_relabel(const LaunchCtx& ctx, int32_t* labels, int64_t n, int64_t base,
                 const int32_t* keys, const int32_t* vals, const int32_t* n_map, int32_t cap,
                 int32_t* scratch);

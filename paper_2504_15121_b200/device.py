@@ -101,6 +101,74 @@ def oriented_points(disparity: torch.Tensor, rig, kernels=9, *, out: torch.Tenso
     return out
 
 
+def bit_words(W: int) -> int:
+    """uint32 words per row of a passable bit mask."""
+    return (int(W) + 31) // 32
+
+
+def oriented_points_bits(disparity: torch.Tensor, rig, kernels, threshold: float, *,
+                         out=None, mask=None, bits=None, row0: int = 0):
+    """Fused pass that also emits the ST-passable bit mask (same read of the
+    disparity): returns (``[B, H, W, 6]`` fp32, ``[B, H, ceil(W/32)]`` int32
+    bit words; bit ``u % 32`` of word ``u // 32`` = pixel ``u``)."""
+    d = _fp32(_batched(disparity))
+    B, H, W = d.shape
+    dev = d.device
+    out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
+    if mask is not None:
+        mask = _check_out(mask, (B, H, W), torch.uint8, dev, "mask")
+    bits = _check_out(bits, (B, H, bit_words(W)), torch.int32, dev, "bits")
+    off = _offsets_of(kernels)
+    rs = _native.rig_struct(rig)
+    rc = _native.load().sn_oriented_points_bits(
+        _native.plan(dev.index), d.data_ptr(), B, H, W, int(row0), ctypes.byref(rs),
+        off.ctypes.data, len(off), float(threshold), out.data_ptr(),
+        mask.data_ptr() if mask is not None else None, bits.data_ptr(), _stream(dev))
+    check(rc, "oriented_points_bits")
+    return out, bits
+
+
+def labels_from_bits(bits: torch.Tensor, width: int, *, out=None, row_base: int = 0,
+                     workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Component labels from a passable bit mask ``[B, H, ceil(W/32)]``."""
+    bits = _batched(bits, "bits")
+    if bits.dtype != torch.int32 or bits.shape[-1] != bit_words(width):
+        raise ValueError("bits must be int32 [B, H, ceil(width/32)]")
+    B, H, _ = bits.shape
+    W = int(width)
+    dev = bits.device
+    out = _check_out(out, (B, H, W), torch.int32, dev, "out")
+    ws = _workspace(workspace, B, H, W, dev)
+    rc = _native.load().sn_ccl_from_bits_ws(_native.plan(dev.index), bits.data_ptr(), B, H, W,
+                                            int(row_base), out.data_ptr(), ws.data_ptr(),
+                                            ws.numel() * ws.element_size(), _stream(dev))
+    check(rc, "labels_from_bits")
+    return out
+
+
+def pipeline(disparity: torch.Tensor, rig, kernels, threshold: float, *, out=None, labels=None,
+             mask=None, workspace: torch.Tensor | None = None):
+    """The whole hot path in one call: fused fit + normal + point + passable
+    bits, then component labels.  Returns (``[B, H, W, 6]`` fp32, ``[B, H, W]``
+    int32 labels)."""
+    d = _fp32(_batched(disparity))
+    B, H, W = d.shape
+    dev = d.device
+    out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
+    labels = _check_out(labels, (B, H, W), torch.int32, dev, "labels")
+    if mask is not None:
+        mask = _check_out(mask, (B, H, W), torch.uint8, dev, "mask")
+    ws = _workspace(workspace, B, H, W, dev)
+    off = _offsets_of(kernels)
+    rs = _native.rig_struct(rig)
+    rc = _native.load().sn_pipeline_ws(
+        _native.plan(dev.index), d.data_ptr(), B, H, W, ctypes.byref(rs), off.ctypes.data,
+        len(off), float(threshold), out.data_ptr(), mask.data_ptr() if mask is not None else None,
+        labels.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(), _stream(dev))
+    check(rc, "pipeline")
+    return out, labels
+
+
 def affine(disparity: torch.Tensor, kernels, *, a1=None, a2=None, mask=None):
     """convolve_affine on the device: (a1, a2, mask) fp64/fp64/uint8 ``[B, H, W]``."""
     d = _batched(disparity)

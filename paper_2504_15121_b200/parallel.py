@@ -133,29 +133,21 @@ def seam_map(labels_owned, world: int, group=None) -> tuple[np.ndarray, np.ndarr
 # per-rank device work
 
 
-def strip_points(block, plan: StripPlan, s: int, rig, kernels=9, *, out=None):
-    """Fused fit + normal + point over the extended block; returns the view of
-    the strip's owned rows ``[rows, W, 6]`` (identical to the same rows of the
-    whole-frame result: the owned rows are >= halo from any block edge that is
-    not an image edge)."""
+def strip_pass(block, plan: StripPlan, s: int, rig, kernels=9, threshold: float = 0.2):
+    """Fused pass over the strip's extended block (fit + normal + point + the
+    passable bits in one read), then labels of the owned rows from the bits
+    with global raster indices (before the seam merge).  Returns views of the
+    owned rows: (points ``[rows, W, 6]``, labels ``[rows, W]``) -- identical to
+    the same rows of the whole-frame result, because the owned rows are at
+    least ``halo`` rows from any block edge that is not an image edge."""
     from . import device
 
     o0, o1 = plan.owned_in_block(s)
     b0, _ = plan.block(s)
-    res = device.oriented_points(block, rig, kernels, out=out, row0=b0)
-    return res[0, o0:o1]
-
-
-def strip_labels(block, plan: StripPlan, s: int, rig, threshold: float, *, out=None):
-    """Labels of the strip's owned rows (global raster indices) before the
-    seam merge: the predicate reads the block's halo, labelling sees only the
-    owned rows."""
-    from . import device
-
-    o0, o1 = plan.owned_in_block(s)
     r0, _ = plan.owned(s)
-    pas = device.passable(block, rig, threshold)
-    return device.labels_from_passable(pas[0, o0:o1].contiguous(), out=out, row_base=r0)[0]
+    pts, bits = device.oriented_points_bits(block, rig, kernels, threshold, row0=b0)
+    lab = device.labels_from_bits(bits[:, o0:o1].contiguous(), plan.width, row_base=r0)
+    return pts[0, o0:o1], lab[0]
 
 
 def apply_seam_map(labels, plan: StripPlan, s: int, keys: np.ndarray, vals: np.ndarray):
@@ -186,8 +178,7 @@ def distributed_strip_frame(owned, plan: StripPlan, rig, kernels=9, threshold: f
     if world != plan.n_strips:
         raise ValueError("one strip per rank")
     block = exchange_halo(owned, plan, rank, group)
-    pts = strip_points(block, plan, rank, rig, kernels)
-    lab = strip_labels(block, plan, rank, rig, threshold)
+    pts, lab = strip_pass(block, plan, rank, rig, kernels, threshold)
     keys, vals = seam_map(lab, world, group)
     apply_seam_map(lab, plan, rank, keys, vals)
     return pts, lab
@@ -205,9 +196,9 @@ def local_strip_frame(disp, plan: StripPlan, rig, kernels=9, threshold: float = 
     pts, labs = [], []
     for s in range(plan.n_strips):
         b0, b1 = plan.block(s)
-        block = disp[b0:b1].contiguous()
-        pts.append(strip_points(block, plan, s, rig, kernels))
-        labs.append(strip_labels(block, plan, s, rig, threshold))
+        p_s, l_s = strip_pass(disp[b0:b1].contiguous(), plan, s, rig, kernels, threshold)
+        pts.append(p_s)
+        labs.append(l_s)
     seams = np.stack([torch.stack([l[0], l[-1]]).cpu().numpy() for l in labs]).astype(np.int32)
     keys, vals = seam_merge(seams)
     for s, l in enumerate(labs):

@@ -250,3 +250,67 @@ def test_labels_filter_edge_cases(cuda_dev, pick):
         lab = device.component_labels(dt, rig, t)[0].cpu().numpy().astype(np.int64)
         ref = orc.ccl_labels(d64, o, t)
         assert np.array_equal(lab, ref), t
+
+
+def _bits_to_bool(bits, W):
+    b = bits.cpu().numpy().astype(np.uint32)
+    out = np.zeros(b.shape[:-1] + (b.shape[-1] * 32,), dtype=bool)
+    for k in range(32):
+        out[..., k::32] = (b >> np.uint32(k)) & 1
+    return out[..., :W]
+
+
+@pytest.mark.parametrize("kernel", [9, 3, 15, "cross"])
+@pytest.mark.parametrize("shape", [(256, 512), (77, 130), (200, 384)])
+def test_fused_bits_and_pipeline(cuda_dev, kernel, shape):
+    """The passable bits the fused pass emits (or the standalone bit kernel
+    for non-square / unaligned shapes) equal the oracle's passable set bit for
+    bit, and the one-call pipeline equals the separate entry points."""
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import KernelSpec, device, scenes
+    from scipy import ndimage
+    H, W = shape
+    sc = scenes.street_scene(W, H)
+    d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 1.0, 2)
+    holes = ndimage.binary_dilation(np.random.default_rng(8).random(d.shape) < 0.003, iterations=2)
+    d[holes] = np.nan
+    d[5, 7] = -2.0
+    d = d.astype(np.float32)
+    kern = KernelSpec(np.array([[0, 0], [1, 0], [-1, 0], [0, 1], [0, -1]])) if kernel == "cross" \
+        else kernel
+    o = orc.Rig(sc.rig.fx, sc.rig.fy, sc.rig.u0, sc.rig.v0, sc.rig.baseline)
+    dt = torch.from_numpy(np.stack([d, d[::-1].copy()])).to(cuda_dev)
+    for t in (0.05, 0.2, 1.0):
+        pts, bits = device.oriented_points_bits(dt, sc.rig, kern, t)
+        ref_pts = device.oriented_points(dt, sc.rig, kern)
+        assert torch.equal(torch.nan_to_num(pts, 7.0), torch.nan_to_num(ref_pts, 7.0))
+        got = _bits_to_bool(bits, W)
+        for i in range(2):
+            assert np.array_equal(got[i], orc.passable(dt[i].cpu().numpy().astype(np.float64),
+                                                        o, t)), (i, t)
+        p2, lab = device.pipeline(dt, sc.rig, kern, t)
+        assert torch.equal(torch.nan_to_num(p2, 7.0), torch.nan_to_num(ref_pts, 7.0))
+        assert torch.equal(lab, device.component_labels(dt, sc.rig, t))
+        assert torch.equal(lab, device.labels_from_bits(bits, W))
+
+
+def test_bits_filter_ties_and_ranges(cuda_dev):
+    """Fused predicate filter at exact ties (t = an edge value) and with
+    disparities outside the filter's range."""
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(512, 256)
+    d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.5, 4).astype(np.float32)
+    rng = np.random.default_rng(6)
+    sel = rng.random(d.shape)
+    d[sel < 0.01] = 1e-3
+    d[(sel >= 0.01) & (sel < 0.02)] = 1e6
+    d[(sel >= 0.02) & (sel < 0.025)] = 1e-40
+    o = orc.Rig(sc.rig.fx, sc.rig.fy, sc.rig.u0, sc.rig.v0, sc.rig.baseline)
+    d64 = d.astype(np.float64)
+    e, em = orc.depth_laplacian(*orc.depth_field(d64, o))
+    vals = np.sort(e[em])
+    dt = torch.from_numpy(d).to(cuda_dev)
+    for t in (float(vals[len(vals) // 3]), float(vals[len(vals) // 2]), float(vals[-2]), 0.2):
+        _, bits = device.oriented_points_bits(dt, sc.rig, 9, t)
+        assert np.array_equal(_bits_to_bool(bits, 512)[0], orc.passable(d64, o, t)), t
