@@ -21,17 +21,19 @@
 // and the result is independent of scheduling.  Three launches per batch:
 //
 //   1. ccl_tile_kernel   128x64 tile per CTA, 256 threads = (row, word).
-//      predicate -> bits (ballot), bits -> global (for pass 3), run
-//      union-find in shared memory, tile-border labels -> compact seam rows /
-//      columns, global node init G[root] = root for border-touching roots.
+//      (predicate -> bits by ballot, unless the fused pass already emitted
+//      them), run union-find in shared memory, tile-border labels -> compact
+//      seam rows / columns, global node init G[root] = root for
+//      border-touching roots, and every pixel's local root as a 2-byte tile
+//      index + the tile's border-root flags for pass 3.
 //   2. ccl_seam_kernel   unions across tile seams in global memory (G is the
 //      label array itself; only border-touching roots are ever nodes).
-//   3. ccl_resolve_kernel  re-runs the (deterministic) tile union-find from
-//      the bits, resolves border-touching roots through G, writes every
-//      label once with coalesced stores.
+//   3. ccl_resolve_kernel  walks G once per border-touching root, then maps
+//      each pixel's 2-byte local root to its label with coalesced stores.
 //
-// HBM traffic per pixel: 4 B disparity in, 4 B labels out, 2 x 1/8 B bits,
-// plus the sparse seam/root traffic -- against the 8 B/px floor of §8(d).
+// HBM traffic per pixel from the fused pass's bit mask: 1/8 B bits in, 2 B
+// local roots out and back, 4 B labels out (+ the sparse seam/root traffic),
+// against the 4 B/px floor of writing the labels.
 
 #include <cuda_runtime.h>
 #include <float.h>
@@ -214,47 +216,41 @@ __device__ __forceinline__ void tile_union_find(int32_t* L, const uint32_t* bits
   flag[tid] = 0u;
   __syncthreads();
 
-  // a run crossing into this word from the left neighbour word (chains <= 4)
+  // a run crossing into this word from the left neighbour word
   if ((A & 1u) && w > 0) {
     const uint32_t Al = bits[tid - 1];
     if (Al >> 31) uf_unite(L, base, base - 32 + (31 - __clz(run_starts(Al))));
   }
-  __syncthreads();
-  // rows merge in log2(64) rounds, like a reduction tree: round k joins the
-  // blocks of 2^k rows that meet at rows r = 2^k (mod 2^(k+1)).  Joining all
-  // rows at once would link every run to the run above it concurrently and
-  // build chains as long as the tile is high; in rounds a node's depth grows
-  // by at most one per round.
-  const uint32_t B = r > 0 ? bits[tid - kLWords] : 0u;
-  const uint32_t BL = (r > 0 && w > 0) ? bits[tid - kLWords - 1] : 0u;
-  const uint32_t BR = (r > 0 && w + 1 < kLWords) ? bits[tid - kLWords + 1] : 0u;
-  const int my_round = r > 0 ? __ffs(r) - 1 : -1;  // round in which row r joins row r - 1
-#pragma unroll 1
-  for (int k = 0; (1 << k) < kLTH; ++k) {
-    if (my_round == k && (A & (B | (B << 1) | (B >> 1) | (BL >> 31) | (BR << 31)))) {
-      const uint32_t stB = run_starts(B);
-      const int bbase = base - kLTW;
-      for (uint32_t m = st; m; m &= m - 1u) {
-        const int s = __ffs(m) - 1;
-        const uint32_t hi = 0xffffffffu << s;
-        const uint32_t zer = ~A & hi;  // zeros of A at or above s (bit s itself is set)
-        const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
-        const int n = base + s;
-        uint32_t o = (run | (run << 1) | (run >> 1)) & B;
-        while (o) {
-          const int p = __ffs(o) - 1;
-          uf_unite(L, n, bbase + start_of(stB, p));
-          const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
-          const uint32_t zb = ~B & ~upto;  // zeros of B above p: end of that run
-          if (!zb) break;
-          o &= ~((zb & (0u - zb)) - 1u);
-        }
-        if ((run & 1u) && (BL >> 31)) uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(BL))));
-        if ((run >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
+  // runs of the row above (8-connected: the run dilated by one pixel).  All
+  // rows at once: measured (tools/ccl_bench.cu) 2.3x faster than merging rows
+  // in log-depth rounds -- finds average 1.3 steps here, so the tile is
+  // latency-bound on its barriers, not on chain length.
+  if (r > 0) {
+    const uint32_t B = bits[tid - kLWords];
+    const uint32_t BL = w > 0 ? bits[tid - kLWords - 1] : 0u;
+    const uint32_t BR = w + 1 < kLWords ? bits[tid - kLWords + 1] : 0u;
+    const uint32_t stB = run_starts(B);
+    const int bbase = base - kLTW;
+    for (uint32_t m = st; m; m &= m - 1u) {
+      const int s = __ffs(m) - 1;
+      const uint32_t hi = 0xffffffffu << s;
+      const uint32_t zer = ~A & hi;  // zeros of A at or above s (bit s itself is set)
+      const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+      const int n = base + s;
+      uint32_t o = (run | (run << 1) | (run >> 1)) & B;
+      while (o) {
+        const int p = __ffs(o) - 1;
+        uf_unite(L, n, bbase + start_of(stB, p));
+        const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
+        const uint32_t zb = ~B & ~upto;  // zeros of B above p: end of that run
+        if (!zb) break;
+        o &= ~((zb & (0u - zb)) - 1u);
       }
+      if ((run & 1u) && (BL >> 31)) uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(BL))));
+      if ((run >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
     }
-    __syncthreads();
   }
+  __syncthreads();
   // every node -> its root (only root values are written in this phase)
   for (uint32_t m = st; m; m &= m - 1u) {
     const int n = base + __ffs(m) - 1;
@@ -275,8 +271,12 @@ __device__ __forceinline__ void tile_union_find(int32_t* L, const uint32_t* bits
   __syncthreads();
 }
 
+constexpr int kTilePx = kLTW * kLTH;  // 8192: tile pixel index fits 13 bits
+
 struct CclWorkspace {
   uint32_t* bits;  // [B][H][WW]
+  uint16_t* roots;  // [tile][kTilePx] local root (tile pixel index) per pixel, tile-major
+  uint32_t* flags;  // [tile][kTilePx / 32] border-touching roots
   int32_t* top;    // [B][n_ty][W]  first row of each tile row
   int32_t* bot;    // [B][n_ty][W]  last row of each tile row
   int32_t* left;   // [B][n_tx][H]  first column of each tile column
@@ -393,7 +393,9 @@ __global__ void __launch_bounds__(kLThreads)
       }
     }
   }
-  // global union-find nodes: border-touching roots only
+  // global union-find nodes (border-touching roots only), border flags and
+  // every pixel's local root for the resolve pass
+  const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
   {
     const int r = tid >> 2, w = tid & 3;
     const int base = r * kLTW + w * 32;
@@ -405,6 +407,15 @@ __global__ void __launch_bounds__(kLThreads)
         G[g] = g;
       }
     }
+    ws.flags[tile * (kTilePx / 32) + tid] = flag[tid];
+  }
+  uint16_t* roots = ws.roots + tile * kTilePx;
+  for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
+    const uint32_t A = bits[rw];
+    const int n0 = (rw >> 2) * kLTW + (rw & 3) * 32;
+    uint16_t v = 0xffffu;
+    if ((A >> lane) & 1u) v = (uint16_t)L[n0 + start_of(run_starts(A), lane)];
+    roots[n0 + lane] = v;
   }
 }
 
@@ -466,59 +477,62 @@ __global__ void ccl_seam_kernel(const CclParams p, const CclWorkspace ws,
 }
 
 // ---------------------------------------------------------------------------
-// 3. resolve: tile union-find again from the bits, border roots through G,
-// one coalesced label store per pixel
+// 3. resolve: border-touching roots through G (one walk per root), then one
+// 2-byte read and one coalesced 4-byte label store per pixel
 
 __global__ void __launch_bounds__(kLThreads)
     ccl_resolve_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
-  __shared__ __align__(16) int32_t L[kLTH * kLTW];
-  __shared__ uint32_t bits[kLThreads];
   __shared__ uint32_t flag[kLThreads];
+  __shared__ int32_t rank0[kLThreads];  // flagged roots before word i
+  __shared__ int32_t fin[kLThreads * 2];  // final label per flagged root (<= border pixels)
+  __shared__ int32_t warp_sum[kLThreads / 32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
   const int tx = blockIdx.x, ty = blockIdx.y;
   const int x0 = tx * kLTW, y0 = ty * kLTH;
   const int64_t fbase = (int64_t)blockIdx.z * p.H * p.W;
-  {
-    const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
-    bits[tid] = (y0 + r < H && wc < ws.WW)
-                    ? ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc]
-                    : 0u;
+  const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
+  const uint32_t fw = ws.flags[tile * (kTilePx / 32) + tid];
+  flag[tid] = fw;
+  // exclusive prefix of popcounts over the 256 flag words
+  const int c = __popc(fw);
+  int inc = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += v;
   }
+  if (lane == 31) warp_sum[warp] = inc;
   __syncthreads();
-  tile_union_find(L, bits, flag, tid);
-
-  // border-touching roots: final root through the global forest.  Nodes are
-  // only ever roots of tile components, and a concurrent resolve of another
-  // tile overwrites such a node with its final label -- an ancestor -- so the
-  // read-only walk stays valid.
+  int off = 0;
+  for (int i = 0; i < warp; ++i) off += warp_sum[i];
+  const int excl = off + inc - c;
+  rank0[tid] = excl;
+  // walk G once per flagged root.  Nodes are only ever roots of tile
+  // components, and a concurrent resolve of another tile overwrites such a
+  // node with its final label -- an ancestor -- so the read-only walk is valid.
   {
-    const int r = tid >> 2, w = tid & 3;
-    const int base = r * kLTW + w * 32;
     const volatile int32_t* G = labels + fbase;
-    for (uint32_t m = run_starts(bits[tid]); m; m &= m - 1u) {
-      const int n = base + __ffs(m) - 1;
-      if (L[n] == n && ((flag[n >> 5] >> (n & 31)) & 1u))
-        L[n] = -2 - uf_root(G, frame_index(n, x0, y0, W));
+    int k = excl;
+    for (uint32_t m = fw; m; m &= m - 1u) {
+      const int n = tid * 32 + __ffs(m) - 1;
+      if (k < kLThreads * 2) fin[k] = uf_root(G, frame_index(n, x0, y0, W));
+      ++k;
     }
   }
   __syncthreads();
+  const uint16_t* roots = ws.roots + tile * kTilePx;
   int32_t* out = labels + fbase;
   for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
     const int r = rw >> 2, w = rw & 3;
     const int gx = x0 + w * 32 + lane, gy = y0 + r;
+    const int v = roots[r * kLTW + w * 32 + lane];
     if (gx >= W || gy >= H) continue;
-    const uint32_t A = bits[rw];
     int32_t lab = -1;
-    if ((A >> lane) & 1u) {
-      const int n = r * kLTW + w * 32 + start_of(run_starts(A), lane);
-      const int v = L[n];
-      if (v < 0) {
-        lab = -2 - v;
-      } else {
-        const int v2 = L[v];
-        lab = v2 < 0 ? -2 - v2 : frame_index(v, x0, y0, W);
-      }
+    if (v != 0xffff) {
+      const uint32_t fwv = flag[v >> 5];
+      const uint32_t bit = 1u << (v & 31);
+      lab = (fwv & bit) ? fin[rank0[v >> 5] + __popc(fwv & (bit - 1u))] : frame_index(v, x0, y0, W);
     }
     out[(int64_t)gy * W + gx] = lab;
   }
@@ -590,8 +604,10 @@ static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W) {
   const int64_t WW = (W + 31) / 32;
   const int64_t n_tx = (W + kLTW - 1) / kLTW, n_ty = (H + kLTH - 1) / kLTH;
+  const int64_t tiles = B * n_tx * n_ty;
   return align256((size_t)(B * H * WW) * 4) + 2 * align256((size_t)(B * n_ty * W) * 4) +
-         2 * align256((size_t)(B * n_tx * H) * 4);
+         2 * align256((size_t)(B * n_tx * H) * 4) + align256((size_t)(tiles * kTilePx) * 2) +
+         align256((size_t)(tiles * kTilePx / 32) * 4);
 }
 
 int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, uint8_t* pas,
@@ -657,6 +673,11 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
   ws.left = reinterpret_cast<int32_t*>(q);
   q += align256((size_t)(p.B * ws.n_tx * p.H) * 4);
   ws.right = reinterpret_cast<int32_t*>(q);
+  q += align256((size_t)(p.B * ws.n_tx * p.H) * 4);
+  const int64_t tiles = p.B * ws.n_tx * ws.n_ty;
+  ws.roots = reinterpret_cast<uint16_t*>(q);
+  q += align256((size_t)(tiles * kTilePx) * 2);
+  ws.flags = reinterpret_cast<uint32_t*>(q);
 
   if (bits_in) ws.bits = const_cast<uint32_t*>(bits_in);  // read-only in MODE 2
   dim3 grid((unsigned)ws.n_tx, (unsigned)ws.n_ty, (unsigned)p.B);

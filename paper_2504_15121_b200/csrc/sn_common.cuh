@@ -65,32 +65,36 @@ static __device__ __noinline__ uint32_t pred_exact_d(float a, float b, float c, 
 //   e = K |4/a - 1/b - 1/c - 1/e - 1/f| = K |N| / D,
 //   N = 4 bcef - a Q,  Q = ef (b + c) + bc (e + f),  D = a bcef > 0,
 // so e <= t  <=>  K |N| <= t D.  In fp32 (u = 2^-24) |N32 - N| <= 6u M with
-// M = 4 bcef + a Q, D32 and the two products carry <= 8u relative error, and
-// the fp64 evaluation of e is within 2^-50 K M / D of the real value; so when
-// |K32 |N32| - t32 D32| > 2^-19 (K32 M32 + t32 D32) -- a 4x margin -- the fp32
-// comparison equals the fp64 one.  The ranges keep every product a normal
-// float (|K| and t in [2^-40, 2^40], host-checked).  Anything else -- an
-// out-of-range sample or a decision inside the margin -- takes pred_exact_d.
-__device__ __forceinline__ uint32_t pred_bit(float a, float b, float c, float e, float f,
-                                             const FixedParams& p) {
+// M = 4 bcef + a Q, so |K32 |N32| - K |N|| <= 8u K M and |t32 D32 - t D| <=
+// 6u t D, while the fp64 evaluation of e is within 2^-50 K M / D of the real
+// value; so when |K32 |N32| - t32 D32| > 2^-20 (K32 M32 + t32 D32) -- twice the
+// bound -- the fp32 comparison equals the fp64 one.  The ranges keep every
+// product a normal float (K and t in [2^-40, 2^40], host-checked).
+// Returns 0 / 1 (decided) or 2 (out-of-range sample or inside the margin:
+// the caller evaluates pred_exact_d).
+__device__ __forceinline__ uint32_t pred_fast(float a, float b, float c, float e, float f,
+                                              const FixedParams& p) {
   const uint32_t lo = 0x3b800000u, span = 0x47800000u - 0x3b800000u;  // [2^-8, 2^16)
   const bool fast = ((__float_as_uint(a) - lo) < span) & ((__float_as_uint(b) - lo) < span) &
                     ((__float_as_uint(c) - lo) < span) & ((__float_as_uint(e) - lo) < span) &
-                    ((__float_as_uint(f) - lo) < span) & !p.pred_exact;
-  if (fast) {
-    const float bc = __fmul_rn(b, c), ef = __fmul_rn(e, f);
-    const float bcef = __fmul_rn(bc, ef);
-    const float Q = __fadd_rn(__fmul_rn(ef, __fadd_rn(b, c)), __fmul_rn(bc, __fadd_rn(e, f)));
-    const float m4 = __fmul_rn(4.0f, bcef), aQ = __fmul_rn(a, Q);
-    const float X = __fmul_rn(p.fxb_pf, fabsf(__fsub_rn(m4, aQ)));
-    const float Y = __fmul_rn(p.t_f, __fmul_rn(a, bcef));
-    const float margin =
-        __fmul_rn(__fadd_rn(__fmul_rn(p.fxb_pf, __fadd_rn(m4, aQ)), Y), 1.9073486328125e-06f);
-    const float gap = __fsub_rn(X, Y);
-    if (gap > margin) return 0u;
-    if (-gap > margin) return 1u;
-  }
-  return pred_exact_d(a, b, c, e, f, p.fxb, p.t);
+                    ((__float_as_uint(f) - lo) < span);
+  if (!fast) return 2u;
+  const float bc = __fmul_rn(b, c), ef = __fmul_rn(e, f);
+  const float bcef = __fmul_rn(bc, ef);
+  const float Q = __fadd_rn(__fmul_rn(ef, __fadd_rn(b, c)), __fmul_rn(bc, __fadd_rn(e, f)));
+  const float m4 = __fmul_rn(4.0f, bcef), aQ = __fmul_rn(a, Q);
+  const float X = __fmul_rn(p.fxb_pf, fabsf(__fsub_rn(m4, aQ)));
+  const float Y = __fmul_rn(p.t_f, __fmul_rn(a, bcef));
+  const float margin =
+      __fmul_rn(__fadd_rn(__fmul_rn(p.fxb_pf, __fadd_rn(m4, aQ)), Y), 9.5367431640625e-07f);
+  const float gap = __fsub_rn(X, Y);
+  return gap > margin ? 0u : (-gap > margin ? 1u : 2u);
+}
+
+__device__ __forceinline__ uint32_t pred_bit(float a, float b, float c, float e, float f,
+                                             const FixedParams& p) {
+  const uint32_t r = p.pred_exact ? 2u : pred_fast(a, b, c, e, f, p);
+  return r != 2u ? r : pred_exact_d(a, b, c, e, f, p.fxb, p.t);
 }
 
 // ---------------------------------------------------------------------------

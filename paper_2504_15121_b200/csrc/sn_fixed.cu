@@ -362,14 +362,27 @@ __global__ void __launch_bounds__(kFastThreads, 2)
         if (p.bits != nullptr) {
           // ST-passable bits of the run (fused: the tile already holds the
           // 4-neighbourhood; zero-filled samples outside the image are invalid)
-          uint32_t pb = 0;
-          float dl = drow[-1], dc = drow[0];
+          uint32_t pb = 0, undecided = 0;
+          if (!p.pred_exact) {
+            float dl = drow[-1], dc = drow[0];
 #pragma unroll
-          for (int j = 0; j < kRun; ++j) {
-            const float dr = drow[j + 1];
-            pb |= pred_bit(dc, dl, dr, drow[j - BW], drow[j + BW], p) << j;
-            dl = dc;
-            dc = dr;
+            for (int j = 0; j < kRun; ++j) {
+              const float dr = drow[j + 1];
+              const uint32_t r = pred_fast(dc, dl, dr, drow[j - BW], drow[j + BW], p);
+              pb |= (r & 1u) << j;
+              undecided |= (r >> 1) << j;
+              dl = dc;
+              dc = dr;
+            }
+          } else {
+            undecided = (1u << kRun) - 1u;
+          }
+          // rare exact decisions, batched so a warp diverges once per item
+          while (undecided) {
+            const int j = __ffs(undecided) - 1;
+            undecided &= undecided - 1u;
+            pb |= pred_exact_d(drow[j], drow[j - 1], drow[j + 1], drow[j - BW], drow[j + BW],
+                               p.fxb, p.t) << j;
           }
           pbytes[g * (kTW / 8) + q] = (uint8_t)pb;
         }
