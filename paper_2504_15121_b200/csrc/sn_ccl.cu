@@ -107,44 +107,6 @@ __global__ void passable_kernel(const float* __restrict__ disp, const CclParams 
 }
 
 // ---------------------------------------------------------------------------
-// fp32 filter for the predicate
-//
-// zf = fl(fxb_f * rcp.approx(d)) has relative error <= 2^-24 (fxb_f) + 2^-23
-// (rcp.approx, 1 ulp) + 2^-24 (product) = 2^-22 while zf stays a normal
-// float.  With S = 4c + l + r + u + dn (all depths > 0), the fp32 edge value
-// differs from the exact one by <= 2^-22 S (inputs) + 4 * 2^-24 S (four
-// roundings of partial sums bounded by S) = 2^-21 S, and the fp64 edge value
-// from the exact one by < 2^-50 S; t_f = fl(t) is within 2^-24 t.  So when
-// |e32 - t_f| > 2^-19 S_f + 2^-20 t_f (a 4x safety factor) both sides agree
-// on e <= t; otherwise the pixel takes the exact fp64 path.  Samples that
-// are invalid (non-finite or <= 0) are NaN; samples whose zf would leave
-// [1e-30, 1e30] are +inf and force the exact path.
-
-__device__ __forceinline__ float zfast(float d, float fxb_f) {
-  if (!(d > 0.0f && d <= FLT_MAX)) return __int_as_float(0x7fc00000);
-  float r;
-  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(d));
-  const float z = __fmul_rn(fxb_f, r);
-  return (z >= 1e-30f && z <= 1e30f) ? z : __int_as_float(0x7f800000);
-}
-
-// 0 = not passable, 1 = passable, 2 = undecided (exact path)
-__device__ __forceinline__ int fast_passable(float c, float l, float r, float u, float dn,
-                                             float t_f) {
-  if (!(c == c && l == l && r == r && u == u && dn == dn)) return 0;
-  const float S = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(4.0f, c), l), r), u), dn);
-  if (!(S <= 1e30f)) return 2;  // an out-of-range sample
-  const float e =
-      fabsf(__fsub_rn(__fsub_rn(__fsub_rn(__fsub_rn(__fmul_rn(4.0f, c), l), r), u), dn));
-  const float margin = __fadd_rn(__fmul_rn(S, 1.9073486328125e-06f /* 2^-19 */),
-                                 __fmul_rn(t_f, 9.5367431640625e-07f /* 2^-20 */));
-  const float gap = __fsub_rn(e, t_f);
-  if (gap > margin) return 0;
-  if (-gap > margin) return 1;
-  return 2;
-}
-
-// ---------------------------------------------------------------------------
 // union-find helpers (indices only ever point to smaller indices)
 
 // find with path halving: every write replaces a parent by an ancestor, so it
@@ -323,8 +285,8 @@ __global__ void __launch_bounds__(kLThreads)
       bool pk = false;
       if (gx < W && gy < H) {
         const int zi = (r + 1) * kZW + c + 1;
-        const int dec = fast_passable(zs[zi], zs[zi - 1], zs[zi + 1], zs[zi - kZW], zs[zi + kZW],
-                                      p.t_f);
+        const int dec = (int)zpred(zs[zi], zs[zi - 1], zs[zi + 1], zs[zi - kZW], zs[zi + kZW],
+                                   p.t_f);
         if (dec == 2) pk = exact_passable(f, W, gx, gy, p.fxb, p.t);
         else pk = dec == 1;
       }

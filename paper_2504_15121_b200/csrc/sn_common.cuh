@@ -53,6 +53,12 @@ __device__ __forceinline__ double pred_depth(float d, double fxb) {
 
 static __device__ __noinline__ uint32_t pred_exact_d(float a, float b, float c, float e, float f,
                                              double fxb, double t) {
+  // invalid neighbourhoods (a sample not finite and > 0) first, without dividing
+  const uint32_t lim = 0x7f7fffffu;
+  if (!(((__float_as_uint(a) - 1u) < lim) & ((__float_as_uint(b) - 1u) < lim) &
+        ((__float_as_uint(c) - 1u) < lim) & ((__float_as_uint(e) - 1u) < lim) &
+        ((__float_as_uint(f) - 1u) < lim)))
+    return 0u;
   const double zc = pred_depth(a, fxb), zl = pred_depth(b, fxb), zr = pred_depth(c, fxb),
                zu = pred_depth(e, fxb), zd = pred_depth(f, fxb);
   if (!(zc == zc && zl == zl && zr == zr && zu == zu && zd == zd)) return 0u;
@@ -61,7 +67,39 @@ static __device__ __noinline__ uint32_t pred_exact_d(float a, float b, float c, 
   return ev <= t ? 1u : 0u;
 }
 
-// fp32 filter without divisions.  With every d in [2^-8, 2^16] and K = fx*b:
+// fp32 filter on depths (z-form).  zf = fl(fxb_f * rcp.approx(d)) has
+// relative error <= 2^-24 (fxb_f) + 2^-23 (rcp.approx, 1 ulp) + 2^-24
+// (product) = 2^-22 while zf stays a normal float.  With S = 4c + l + r + u + dn
+// (all depths > 0) the fp32 edge value is within 2^-22 S (inputs) + 4 * 2^-24 S
+// (four roundings of partial sums bounded by S) = 2^-21 S of the exact one, the
+// fp64 edge value within 2^-50 S, and t_f = fl(t) within 2^-24 t.  So when
+// |e32 - t_f| > 2^-20 S_f + 2^-21 t_f (twice the bound) both agree on e <= t;
+// otherwise the pixel takes pred_exact_d.  Invalid samples (non-finite or
+// <= 0) are NaN; samples whose zf would leave [1e-30, 1e30] are +inf and force
+// the exact path.  Valid for fx*b and t in [2^-40, 2^40] (host-checked).
+__device__ __forceinline__ float zfast(float d, float fxb_f) {
+  if (!(d > 0.0f && d <= 3.402823466e38f)) return __int_as_float(0x7fc00000);
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(d));
+  const float z = __fmul_rn(fxb_f, r);
+  return (z >= 1e-30f && z <= 1e30f) ? z : __int_as_float(0x7f800000);
+}
+
+// 0 = not passable, 1 = passable, 2 = undecided (exact path)
+__device__ __forceinline__ uint32_t zpred(float c, float l, float r, float u, float dn, float t_f) {
+  if (!(c == c && l == l && r == r && u == u && dn == dn)) return 0u;
+  const float c4 = __fmul_rn(4.0f, c);
+  const float S = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(c4, l), r), u), dn);
+  if (!(S <= 1e30f)) return 2u;  // an out-of-range sample
+  const float e = fabsf(__fsub_rn(__fsub_rn(__fsub_rn(__fsub_rn(c4, l), r), u), dn));
+  const float margin = __fadd_rn(__fmul_rn(S, 9.5367431640625e-07f /* 2^-20 */),
+                                 __fmul_rn(t_f, 4.76837158203125e-07f /* 2^-21 */));
+  const float gap = __fsub_rn(e, t_f);
+  return gap > margin ? 0u : (-gap > margin ? 1u : 2u);
+}
+
+// fp32 filter without divisions (used where depths are not at hand).  With
+// every d in [2^-8, 2^16] and K = fx*b:
 //   e = K |4/a - 1/b - 1/c - 1/e - 1/f| = K |N| / D,
 //   N = 4 bcef - a Q,  Q = ef (b + c) + bc (e + f),  D = a bcef > 0,
 // so e <= t  <=>  K |N| <= t D.  In fp32 (u = 2^-24) |N32 - N| <= 6u M with

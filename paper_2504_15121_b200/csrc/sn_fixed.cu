@@ -46,9 +46,10 @@ constexpr int kG = 16;             // output rows per item
 constexpr int kCP = kG + 1;        // pitch of the column-major C/Rr/Dc arrays (odd)
 constexpr int kBoxF = 32;          // floats per TMA store box row (128 B)
 constexpr int kBoxes = kTW * 6 / kBoxF;  // 24
-constexpr int kFastThreads = 288;  // 9 warps: pass V 2*(128+2R) units, pass H 256 lanes
+constexpr int kHalfUnits = 160;    // pass-V units per half: 5 warps, 32-column aligned
+constexpr int kFastThreads = 2 * kHalfUnits;  // 10 warps; pass H uses the first 8
 constexpr int kRun = 8;            // output columns per pass-H lane
-constexpr double kBig = 1099511627776.0;  // 2^40
+constexpr uint32_t kBigBits = 0x53800000u;  // fp32 bit pattern of 2^40
 
 __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -67,10 +68,11 @@ struct FastCfg {
   static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);  // double2 (C, Rr) [NC][kCP]
   static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;
   static constexpr size_t FL = align_up(CS + CS_BYTES, 16);
-  static constexpr size_t PB = align_up(FL + (NC + 2) * 4, 16);  // passable bytes [kG][16]
-  static constexpr size_t BAR = PB + kG * (kTW / 8);
+  // passable ballots [half][column block of 32][row of the half]
+  static constexpr size_t PW = align_up(FL + (NC + 2) * 4, 16);
+  static constexpr size_t BAR = PW + 2 * (kHalfUnits / 32) * (kG / 2) * 4;
   static constexpr size_t TOTAL = BAR + 16 + 1024;  // + slack for 1024-B alignment
-  static_assert(2 * NC <= kFastThreads + 32, "pass V: at most two units per lane");
+  static_assert(NC <= kHalfUnits, "pass V: one unit per thread");
   static_assert(NR <= 32, "row validity bits must fit 32 bits");
 };
 
@@ -83,16 +85,54 @@ __device__ __forceinline__ bool finite_t<float>(float v) {
   return fabsf(v) <= 3.402823466e38f;
 }
 
+// |v| <= 2^40 (and finite): the sliding sums stay exact
+template <typename T>
+__device__ __forceinline__ bool small_t(T v) {
+  return fabs((double)v) <= 1099511627776.0;
+}
+template <>
+__device__ __forceinline__ bool small_t<float>(float v) {
+  return (__float_as_uint(v) & 0x7fffffffu) <= kBigBits;
+}
+
+// normal from the exact sums, fp32 after one rounding of U and V: the
+// components are U fx, V fy and V dv + U du - alpha d, each bounded by ~|n|
+// (n . (du, dv, fx) = -alpha d fx for a camera-facing normal), so fp32 adds
+// only a few ulp of angle (~1e-5 deg); out-of-range magnitudes take the fp64
+// path of normal_from_moments
+__device__ __forceinline__ void normal_square(double U, double V, float alpha_f, float d,
+                                              float du, float dv, float fx_f, float fy_f,
+                                              const FixedParams& p, float& nx, float& ny,
+                                              float& nz) {
+  const float Uf = (float)U, Vf = (float)V;
+  const float ax = -Uf * fx_f, ay = -Vf * fy_f;
+  const float az = fmaf(Vf, dv, fmaf(Uf, du, -alpha_f * d));
+  const float s = fmaf(ax, ax, fmaf(ay, ay, az * az));
+  if (s > 1e-30f && s < 1e30f) {
+    float r = rsqrtf(s);
+    r = r * fmaf(-0.5f * s * r, r, 1.5f);  // one Newton step: ~1 ulp
+    nx = ax * r;
+    ny = ay * r;
+    nz = az * r;
+  } else {
+    normal_from_moments(U, V, p.alpha, (double)d, (double)du, (double)dv, p.fx, p.fy, nx, ny, nz);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // fast path: centred square pattern, radius R
 //
-// Per item (128 columns x 16 rows of one frame):
-//   pass V  lane <-> input column (128 + 2R lanes): C, Rr for the 16 output
-//           rows as two independent 8-row sliding chains -> smem, column-major
-//           (pitch 17 doubles: conflict-free for both passes)
-//   pass H  lane <-> (output row, run of 16 columns): U, V as two independent
-//           8-column sliding chains, closed-form normal + point, 6 floats per
-//           pixel into the 128B-swizzled staging tile
+// Per item (128 columns x 16 rows of one frame), 10 warps:
+//   pass V  unit = (half h, column c): warps 5h .. 5h+4, lane <-> column, so
+//           each warp covers 32 aligned columns.  C, Rr for the 8 output rows
+//           of the half as a sliding chain -> smem, column-major (pitch 17
+//           doubles: conflict-free for both passes).  With a threshold, the
+//           same registers give the ST-passable bits: depths of the unit's
+//           rows, left/right depths by shuffle, one ballot per row.
+//   pass H  warps 0-7, lane <-> (output row, run of 8 columns): U, V as a
+//           sliding chain, closed-form normal + point, 6 floats per pixel
+//           into the 128B-swizzled staging tile.  Warps 8-9 meanwhile turn
+//           the ballots into bit-mask words and store them.
 // The input tile is double-buffered: the TMA load of item i+1 is in flight
 // during all of item i.
 
@@ -109,17 +149,19 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   constexpr int NV = HG + 2 * R;       // input rows read per pass-V unit
   constexpr int NH = kRun + 2 * R;     // C/Rr columns read per pass-H lane
   constexpr int kLanesH = kTW / kRun * kG;  // 256
+  constexpr int kBlocks = kHalfUnits / 32;  // column blocks per half
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned base for the swizzled staging tile; offset arithmetic on the
   // __shared__ array keeps the shared address space (LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double2* CR = reinterpret_cast<double2*>(smem + Cfg::CS);
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
-  uint8_t* pbytes = smem + Cfg::PB;
+  uint32_t* pw = reinterpret_cast<uint32_t*>(smem + Cfg::PW);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
   const uint32_t stage_base = smem_u32(smem + Cfg::STAGE);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
+  const bool want_bits = (sizeof(T) == 4) && p.bits != nullptr;
 
   int item = blockIdx.x;
   if (item >= n_items) return;
@@ -129,13 +171,21 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   // an illegal-instruction fault on this part -- measured with
   // tools/ubench/tma_probe.cu).  Negative aligned coordinates are fine; the
   // samples outside the image are masked by coordinate in pass V, which
-  // reproduces the no-padding border rule kernels.py:166-176.
+  // reproduces the no-padding border rule kernels.py:166-176 (and arrive as
+  // zeros, i.e. invalid depths, for the passable predicate).
   auto tile_x = [](int x0) { return ((x0 - R) & ~(AE - 1)); };  // floor to AE (two's complement)
+  const double inv_tx = 1.0 / (double)tiles_x, inv_ty = 1.0 / (double)tiles_y;
+  auto udiv = [](unsigned u, unsigned d, double inv) {  // exact u / d for u < 2^31
+    unsigned q = (unsigned)((double)u * inv);
+    if (q * d > u) --q;
+    else if ((q + 1) * d <= u) ++q;
+    return q;
+  };
   auto decode = [&](int it, int& x0, int& y0, int& bz) {
     const unsigned u = (unsigned)it;
-    const unsigned r = u / (unsigned)tiles_x;
+    const unsigned r = udiv(u, (unsigned)tiles_x, inv_tx);
     x0 = (int)(u - r * (unsigned)tiles_x) * kTW;
-    const unsigned f = r / (unsigned)tiles_y;
+    const unsigned f = udiv(r, (unsigned)tiles_y, inv_ty);
     y0 = (int)(r - f * (unsigned)tiles_y) * kG;
     bz = (int)f;
   };
@@ -159,6 +209,10 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   }
   __syncthreads();
 
+  const int h = tid >= kHalfUnits ? 1 : 0;  // pass-V unit of this thread
+  const int c = tid - h * kHalfUnits;
+  const bool unit = c < NC;
+
   for (int it = 0; item < n_items; ++it, item += gridDim.x) {
     const int buf = it & 1;
     if (tid == 0 && item + (int)gridDim.x < n_items) load_tile(item + gridDim.x, buf ^ 1);
@@ -170,78 +224,157 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 
     // ------------------------------------------------------------ pass V
     // unit = (column c, half h): rows 8h .. 8h+7 of the item
-#pragma unroll 1
-    for (int u = tid; u < 2 * NC; u += kFastThreads) {
-      const int h = u >= NC ? 1 : 0;
-      const int c = u - h * NC;
+    {
       const int gx = x0 - R + c;
       const int r0 = h * HG;  // first input row of the unit (item-relative, incl. halo)
-      // rows of the unit inside the image
-      const int lo = max(0, R - y0 - r0), hi = min(NV, H - y0 + R - r0);
-      uint32_t inside = 0;
-      if ((unsigned)gx < (unsigned)W && hi > lo)
-        inside = (uint32_t)(((1ull << (hi - lo)) - 1ull) << lo);
       const T* col = in + r0 * BW + c + sh;
-      double v[NV];
+      T raw[NV];
       uint32_t small = 0;  // bit i: |sample| <= 2^40 (finite and not "big")
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const T raw = col[i * BW];
-        small |= (fabs((double)raw) <= kBig ? 1u : 0u) << i;
-        v[i] = (double)raw;
-      }
-      constexpr uint32_t kAll = (NV >= 32) ? 0xffffffffu : ((1u << NV) - 1u);
-      uint32_t fin = small;
-      bool big = false;
-      if (small != kAll) {
-        // rare: non-finite (zeroed so the sliding sums stay finite) or huge samples
-        fin = 0;
+      if (unit) {
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
-          const bool f = finite_t(col[i * BW]);
-          fin |= (f ? 1u : 0u) << i;
-          if (!f) v[i] = 0.0;
-          big |= f && !((small >> i) & 1u);
-        }
-      }
-      const uint32_t invb = ~(fin & inside);
-      double2* cr = CR + c * kCP + r0;
-      if (!big) {
-        double C = 0.0, Rr = 0.0;
-#pragma unroll
-        for (int j = 0; j < NWIN; ++j) {
-          C += v[j];
-          Rr = fma((double)(j - R), v[j], Rr);
-        }
-        cr[0] = make_double2(C, Rr);
-#pragma unroll
-        for (int g = 1; g < HG; ++g) {
-          const double vin = v[g + 2 * R], vout = v[g - 1];
-          const double tin = fma((double)R, vout, (double)(R + 1) * vin);  // off the chain
-          C += vin - vout;
-          Rr = (Rr - C) + tin;
-          cr[g] = make_double2(C, Rr);
+          raw[i] = col[i * BW];
+          small |= (small_t(raw[i]) ? 1u : 0u) << i;
         }
       } else {
 #pragma unroll
-        for (int g = 0; g < HG; ++g) {
+        for (int i = 0; i < NV; ++i) raw[i] = (T)0;
+      }
+      if (unit) {
+        // rows of the unit inside the image
+        const int lo = max(0, R - y0 - r0), hi = min(NV, H - y0 + R - r0);
+        uint32_t inside = 0;
+        if ((unsigned)gx < (unsigned)W && hi > lo)
+          inside = (uint32_t)(((1ull << (hi - lo)) - 1ull) << lo);
+        double v[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = (double)raw[i];
+        constexpr uint32_t kAll = (NV >= 32) ? 0xffffffffu : ((1u << NV) - 1u);
+        uint32_t fin = small;
+        bool big = false;
+        if (small != kAll) {
+          // rare: non-finite (zeroed so the sliding sums stay finite) or huge samples
+          fin = 0;
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            const bool f = finite_t(raw[i]);
+            fin |= (f ? 1u : 0u) << i;
+            if (!f) v[i] = 0.0;
+            big |= f && !((small >> i) & 1u);
+          }
+        }
+        const uint32_t invb = ~(fin & inside);
+        double2* cr = CR + c * kCP + r0;
+        if (!big) {
           double C = 0.0, Rr = 0.0;
 #pragma unroll
           for (int j = 0; j < NWIN; ++j) {
-            C += v[g + j];
-            Rr = fma((double)(j - R), v[g + j], Rr);
+            C += v[j];
+            Rr = fma((double)(j - R), v[j], Rr);
           }
-          cr[g] = make_double2(C, Rr);
+          cr[0] = make_double2(C, Rr);
+#pragma unroll
+          for (int g = 1; g < HG; ++g) {
+            const double vin = v[g + 2 * R], vout = v[g - 1];
+            const double tin = fma((double)R, vout, (double)(R + 1) * vin);  // off the chain
+            C += vin - vout;
+            Rr = (Rr - C) + tin;
+            cr[g] = make_double2(C, Rr);
+          }
+        } else {
+#pragma unroll
+          for (int g = 0; g < HG; ++g) {
+            double C = 0.0, Rr = 0.0;
+#pragma unroll
+            for (int j = 0; j < NWIN; ++j) {
+              C += v[g + j];
+              Rr = fma((double)(j - R), v[g + j], Rr);
+            }
+            cr[g] = make_double2(C, Rr);
+          }
+        }
+        uint32_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
+        // flag word of column c: half h's low byte holds its 8 output rows
+        reinterpret_cast<uint16_t*>(fl + c)[h] = (uint16_t)(acc & 0xFFu);
+        if (big) atomicOr(fl + NC + buf, 1u);  // per-parity "big value" flag of the item
+      }
+      if constexpr (sizeof(T) == 4) {
+        if (want_bits) {
+          // ST-passable bits of output rows 8h .. 8h+7 at output column c - R
+          // (adaptive.py:80-97,130-132).  Depths zf of the unit's rows
+          // R-1 .. R+8 (sn_common.cuh zfast, without its checks), left/right
+          // neighbours by shuffle (the warp-edge lanes load theirs).  The
+          // filter needs all five depths in [2^-100, 2^103] (positive normal
+          // floats whose sums stay normal, given fx*b and t in [2^-40, 2^40]);
+          // that also implies five valid disparities.  Anything else --
+          // invalid samples included -- is "undecided" and takes the exact
+          // path, which rejects invalid neighbourhoods before dividing.  The
+          // edge value is evaluated as (4c - u - d) - (l + r): four roundings
+          // of partial sums bounded by S, the same 2^-21 S bound as zpred.
+          constexpr int NZ = HG + 2;
+          float z[NZ];
+#pragma unroll
+          for (int k = 0; k < NZ; ++k) {
+            float r;
+            asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"((float)raw[R - 1 + k]));
+            z[k] = __fmul_rn(p.fxb_pf, r);
+          }
+          float ze[HG];
+          const int ce = lane == 0 ? c - 1 : c + 1;
+          if ((lane == 0 || lane == 31) && ce >= 0 && ce < NC) {
+#pragma unroll
+            for (int k = 0; k < HG; ++k) {
+              float r;
+              asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"((float)in[(r0 + R + k) * BW + ce + sh]));
+              ze[k] = __fmul_rn(p.fxb_pf, r);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < HG; ++k) ze[k] = __int_as_float(0x7fc00000);
+          }
+          const float tm = __fmul_rn(p.t_f, 4.76837158203125e-07f /* 2^-21 */);
+          uint32_t pass = 0, sure = 0;  // bit k: decided passable / decided (either way)
+#pragma unroll
+          for (int k = 0; k < HG; ++k) {
+            float zl = __shfl_up_sync(0xffffffffu, z[k + 1], 1);
+            float zr = __shfl_down_sync(0xffffffffu, z[k + 1], 1);
+            if (lane == 0) zl = ze[k];
+            if (lane == 31) zr = ze[k];
+            const float c4 = __fmul_rn(4.0f, z[k + 1]);
+            const float vp = __fsub_rn(__fsub_rn(c4, z[k]), z[k + 2]);
+            const float sp = __fadd_rn(__fadd_rn(c4, z[k]), z[k + 2]);
+            const float hs = __fadd_rn(zl, zr);
+            const float S = __fadd_rn(sp, hs);
+            const float a = __fsub_rn(fabsf(__fsub_rn(vp, hs)), p.t_f);  // e - t
+            const float margin = __fmaf_rn(S, 9.5367431640625e-07f /* 2^-20 */, tm);
+            const float mn = fminf(fminf(fminf(z[k], z[k + 2]), fminf(zl, zr)), z[k + 1]);
+            const bool ok = (S <= 1.0141204801825835e31f /* 2^103 */) &&
+                            (mn >= 7.888609052210118e-31f /* 2^-100 */);
+            pass |= (ok && a < -margin ? 1u : 0u) << k;
+            sure |= (ok && (a < -margin || a > margin) ? 1u : 0u) << k;
+          }
+          const bool out_col = unit && c >= R && c < R + kTW;
+          uint32_t pb = p.pred_exact ? 0u : pass;
+          uint32_t undecided = p.pred_exact ? 0xFFu : (~sure & 0xFFu);
+          if (!out_col) pb = undecided = 0;
+          // rare exact decisions (fp64, reference op order), batched per unit
+          while (undecided) {
+            const int k = __ffs(undecided) - 1;
+            undecided &= undecided - 1u;
+            const T* ck = col + (R + k) * BW;
+            pb |= pred_exact_d((float)ck[0], (float)ck[-1], (float)ck[1], (float)ck[-BW],
+                               (float)ck[BW], p.fxb, p.t)
+                  << k;
+          }
+#pragma unroll
+          for (int k = 0; k < HG; ++k) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (pb >> k) & 1u);
+            if (lane == k) pw[(h * kBlocks + (c >> 5)) * HG + k] = b;
+          }
         }
       }
-      uint32_t acc = 0;
-#pragma unroll
-      for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
-      // flag bits: 0..15 = support of output row has an invalid sample,
-      // 16 / 17 = big values in half 0 / 1 (two writers per column: halves)
-      // flag word of column c: half h's low byte holds its 8 output rows
-      reinterpret_cast<uint16_t*>(fl + c)[h] = (uint16_t)(acc & 0xFFu);
-      if (big) atomicOr(fl + NC + buf, 1u);  // per-parity "big value" flag of the item
     }
     if (tid == 0) bulk_wait_read0();  // staging of the previous item consumed by TMA
     __syncthreads();
@@ -275,7 +408,6 @@ __global__ void __launch_bounds__(kFastThreads, 2)
       const int yv = p.row0 + yg;  // image row (strips: block row + offset)
       const double dv = (double)yv - p.v0;
       const float dv_f = ((float)yv - p.v0_hi) - p.v0_lo;
-      const double du0 = (double)xb - p.u0;
       const float du_hi = (float)xb - p.u0_hi;  // exact; + j stays exact
       const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
       const uint32_t gsw = (uint32_t)(g & 7);
@@ -317,26 +449,31 @@ __global__ void __launch_bounds__(kFastThreads, 2)
           Vs[j] = V;
         }
       }
+      const float alpha_f = (float)p.alpha, fx_f = (float)p.fx, fy_f = (float)p.fy;
       float o[12];
 #pragma unroll
       for (int j = 0; j < kRun; ++j) {
-        const double U = Us[j], V = Vs[j];
         const T dcv = drow[j];
         const bool valid = (((win >> j) & 1u) == 0u) && (dcv > (T)0);
         validbits |= (valid ? 1u : 0u) << j;
         float px, py, pz, nx, ny, nz;
         const int xg = xb + j;
+        const float du_f = (du_hi + (float)j) - p.u0_lo;
         if constexpr (sizeof(T) == 4) {
-          const float du_f = (du_hi + (float)j) - p.u0_lo;
           point_from_disparity((float)dcv, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
+          if (valid) {
+            normal_square(Us[j], Vs[j], alpha_f, (float)dcv, du_f, dv_f, fx_f, fy_f, p, nx, ny, nz);
+          } else {
+            nx = ny = nz = __int_as_float(0x7fc00000);
+          }
         } else {
           point_from_disparity_f64((double)dcv, (double)xg - p.u0, dv, p, px, py, pz);
-        }
-        if (valid) {
-          normal_from_moments(U, V, p.alpha, (double)dcv, du0 + (double)j, dv, p.fx, p.fy, nx, ny,
-                              nz);
-        } else {
-          nx = ny = nz = __int_as_float(0x7fc00000);
+          if (valid) {
+            normal_from_moments(Us[j], Vs[j], p.alpha, (double)dcv, (double)xg - p.u0, dv, p.fx,
+                                p.fy, nx, ny, nz);
+          } else {
+            nx = ny = nz = __int_as_float(0x7fc00000);
+          }
         }
         const int s6 = (j & 1) * 6;
         o[s6 + 0] = px;
@@ -358,50 +495,26 @@ __global__ void __launch_bounds__(kFastThreads, 2)
           }
         }
       }
-      if constexpr (sizeof(T) == 4) {
-        if (p.bits != nullptr) {
-          // ST-passable bits of the run (fused: the tile already holds the
-          // 4-neighbourhood; zero-filled samples outside the image are invalid)
-          uint32_t pb = 0, undecided = 0;
-          if (!p.pred_exact) {
-            float dl = drow[-1], dc = drow[0];
-#pragma unroll
-            for (int j = 0; j < kRun; ++j) {
-              const float dr = drow[j + 1];
-              const uint32_t r = pred_fast(dc, dl, dr, drow[j - BW], drow[j + BW], p);
-              pb |= (r & 1u) << j;
-              undecided |= (r >> 1) << j;
-              dl = dc;
-              dc = dr;
-            }
-          } else {
-            undecided = (1u << kRun) - 1u;
-          }
-          // rare exact decisions, batched so a warp diverges once per item
-          while (undecided) {
-            const int j = __ffs(undecided) - 1;
-            undecided &= undecided - 1u;
-            pb |= pred_exact_d(drow[j], drow[j - 1], drow[j + 1], drow[j - BW], drow[j + BW],
-                               p.fxb, p.t) << j;
-          }
-          pbytes[g * (kTW / 8) + q] = (uint8_t)pb;
-        }
-      }
       if (mask_out != nullptr && yg < H) {
         uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
 #pragma unroll 1
         for (int j = 0; j < kRun && xb + j < W; ++j) mrow[j] = (uint8_t)((validbits >> j) & 1u);
       }
+    } else if (want_bits && tid < kLanesH + kG * (kTW / 32)) {
+      // warps 8-9: bit-mask words of the item.  Word m of output row g covers
+      // output columns 32m .. 32m+31 = logical columns 32m+R .. 32m+R+31,
+      // split over the ballots of column blocks m and m+1.
+      const int k = tid - kLanesH;
+      const int g = k >> 2, m = k & 3;
+      const int hh = g / HG, kr = g % HG;
+      const uint32_t lo = pw[(hh * kBlocks + m) * HG + kr];
+      const uint32_t hi = pw[(hh * kBlocks + m + 1) * HG + kr];
+      const int wc = x0 / 32 + m;
+      if (y0 + g < H && wc < p.bits_ww)
+        p.bits[((int64_t)bz * H + y0 + g) * p.bits_ww + wc] = __funnelshift_r(lo, hi, R);
     }
     fence_proxy_async_smem();
     __syncthreads();
-    if (sizeof(T) == 4 && p.bits != nullptr && tid >= 32 && tid < 32 + kG * (kTW / 32)) {
-      const int gg = (tid - 32) >> 2, wi = (tid - 32) & 3;
-      const int wc = x0 / 32 + wi;
-      if (y0 + gg < H && wc < p.bits_ww)
-        p.bits[((int64_t)bz * H + y0 + gg) * p.bits_ww + wc] =
-            reinterpret_cast<const uint32_t*>(pbytes)[gg * (kTW / 32) + wi];
-    }
     if (tid == 0) {
       fl[NC + buf] = 0u;  // reset this parity's big flag (next used two items later)
 #pragma unroll 1
