@@ -119,6 +119,74 @@ __device__ __forceinline__ void normal_square(double U, double V, float alpha_f,
   }
 }
 
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Oriented-point records of two neighbouring pixels (same row) with packed
+// f32x2 arithmetic (FFMA2/FMUL2 on sm_100a).  Point: z = fxb/d (rcp.approx,
+// <= ~3 ulp), x = du z / fx, y = dv z / fy, NaN unless d is finite and > 0;
+// subnormal d takes an fp64 division (flush-to-zero would turn a finite z
+// into inf).  Normal: normal_square's formula for both pixels; a pixel whose
+// |n|^2 leaves fp32's comfortable range takes the fp64 path.
+__device__ __forceinline__ void records_pair(double U0, double V0, double U1, double V1, float d0,
+                                             float d1, bool ok0, bool ok1, float duh, float dv,
+                                             const FixedParams& p, float* o) {
+  // points; duh = (x - u0_hi) exactly, du = duh - u0_lo (two-float u0)
+  const float2 dd = make_float2(d0, d1);
+  const float2 du = make_float2(duh - p.u0_lo, (duh + 1.0f) - p.u0_lo);
+  float2 zz = __fmul2_rn(make_float2(p.fxb_f, p.fxb_f), make_float2(rcp_ftz(d0), rcp_ftz(d1)));
+  const bool pv0 = (d0 > 0.0f) && (d0 <= 3.402823466e38f);
+  const bool pv1 = (d1 > 0.0f) && (d1 <= 3.402823466e38f);
+  if (pv0 && d0 < 1.175494351e-38f) zz.x = (float)(p.fxb / (double)d0);
+  if (pv1 && d1 < 1.175494351e-38f) zz.y = (float)(p.fxb / (double)d1);
+  if (!pv0) zz.x = __int_as_float(0x7fc00000);
+  if (!pv1) zz.y = __int_as_float(0x7fc00000);
+  const float2 px = __fmul2_rn(__fmul2_rn(du, zz), make_float2(p.inv_fx_f, p.inv_fx_f));
+  const float2 py = __fmul2_rn(__fmul2_rn(make_float2(dv, dv), zz), make_float2(p.inv_fy_f, p.inv_fy_f));
+  o[0] = px.x;
+  o[1] = py.x;
+  o[2] = zz.x;
+  o[6] = px.y;
+  o[7] = py.y;
+  o[8] = zz.y;
+  // normals
+  const float2 Uf = make_float2((float)U0, (float)U1), Vf = make_float2((float)V0, (float)V1);
+  const float nfx = -(float)p.fx, nfy = -(float)p.fy, nal = -(float)p.alpha;
+  const float2 ax = __fmul2_rn(Uf, make_float2(nfx, nfx));
+  const float2 ay = __fmul2_rn(Vf, make_float2(nfy, nfy));
+  const float2 az = __ffma2_rn(Vf, make_float2(dv, dv),
+                               __ffma2_rn(Uf, du, __fmul2_rn(make_float2(nal, nal), dd)));
+  const float2 s = __ffma2_rn(ax, ax, __ffma2_rn(ay, ay, __fmul2_rn(az, az)));
+  float2 r = make_float2(rsqrt_ftz(s.x), rsqrt_ftz(s.y));
+  // one Newton step: r *= 1.5 - 0.5 s r^2
+  const float2 hs = __fmul2_rn(make_float2(-0.5f, -0.5f), __fmul2_rn(s, r));
+  r = __fmul2_rn(r, __ffma2_rn(hs, r, make_float2(1.5f, 1.5f)));
+  const float2 nx = __fmul2_rn(ax, r), ny = __fmul2_rn(ay, r), nz = __fmul2_rn(az, r);
+  o[3] = nx.x;
+  o[4] = ny.x;
+  o[5] = nz.x;
+  o[9] = nx.y;
+  o[10] = ny.y;
+  o[11] = nz.y;
+  const bool in0 = s.x > 1e-30f && s.x < 1e30f, in1 = s.y > 1e-30f && s.y < 1e30f;
+  if (ok0 && !in0)
+    normal_from_moments(U0, V0, p.alpha, (double)d0, (double)du.x, (double)dv, p.fx, p.fy, o[3],
+                        o[4], o[5]);
+  if (ok1 && !in1)
+    normal_from_moments(U1, V1, p.alpha, (double)d1, (double)du.y, (double)dv, p.fx, p.fy, o[9],
+                        o[10], o[11]);
+  if (!ok0) o[3] = o[4] = o[5] = __int_as_float(0x7fc00000);
+  if (!ok1) o[9] = o[10] = o[11] = __int_as_float(0x7fc00000);
+}
+
 // ---------------------------------------------------------------------------
 // fast path: centred square pattern, radius R
 //
@@ -229,12 +297,22 @@ __global__ void __launch_bounds__(kFastThreads, 2)
       const int r0 = h * HG;  // first input row of the unit (item-relative, incl. halo)
       const T* col = in + r0 * BW + c + sh;
       T raw[NV];
-      uint32_t small = 0;  // bit i: |sample| <= 2^40 (finite and not "big")
+      bool all_small = true;  // every sample finite with |v| <= 2^40 (sliding sums exact)
       if (unit) {
+        if constexpr (sizeof(T) == 4) {
+          uint32_t mx = 0;
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          raw[i] = col[i * BW];
-          small |= (small_t(raw[i]) ? 1u : 0u) << i;
+          for (int i = 0; i < NV; ++i) {
+            raw[i] = col[i * BW];
+            mx = max(mx, __float_as_uint(raw[i]) & 0x7fffffffu);
+          }
+          all_small = mx <= kBigBits;
+        } else {
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            raw[i] = col[i * BW];
+            all_small &= small_t(raw[i]);
+          }
         }
       } else {
 #pragma unroll
@@ -250,9 +328,9 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 #pragma unroll
         for (int i = 0; i < NV; ++i) v[i] = (double)raw[i];
         constexpr uint32_t kAll = (NV >= 32) ? 0xffffffffu : ((1u << NV) - 1u);
-        uint32_t fin = small;
+        uint32_t fin = kAll;
         bool big = false;
-        if (small != kAll) {
+        if (!all_small) {
           // rare: non-finite (zeroed so the sliding sums stay finite) or huge samples
           fin = 0;
 #pragma unroll
@@ -260,7 +338,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
             const bool f = finite_t(raw[i]);
             fin |= (f ? 1u : 0u) << i;
             if (!f) v[i] = 0.0;
-            big |= f && !((small >> i) & 1u);
+            big |= f && !small_t(raw[i]);
           }
         }
         const uint32_t invb = ~(fin & inside);
@@ -317,18 +395,14 @@ __global__ void __launch_bounds__(kFastThreads, 2)
           float z[NZ];
 #pragma unroll
           for (int k = 0; k < NZ; ++k) {
-            float r;
-            asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"((float)raw[R - 1 + k]));
-            z[k] = __fmul_rn(p.fxb_pf, r);
+            z[k] = __fmul_rn(p.fxb_pf, rcp_ftz((float)raw[R - 1 + k]));
           }
           float ze[HG];
           const int ce = lane == 0 ? c - 1 : c + 1;
           if ((lane == 0 || lane == 31) && ce >= 0 && ce < NC) {
 #pragma unroll
             for (int k = 0; k < HG; ++k) {
-              float r;
-              asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"((float)in[(r0 + R + k) * BW + ce + sh]));
-              ze[k] = __fmul_rn(p.fxb_pf, r);
+              ze[k] = __fmul_rn(p.fxb_pf, rcp_ftz((float)in[(r0 + R + k) * BW + ce + sh]));
             }
           } else {
 #pragma unroll
@@ -368,10 +442,13 @@ __global__ void __launch_bounds__(kFastThreads, 2)
                                (float)ck[BW], p.fxb, p.t)
                   << k;
           }
+          uint32_t bw[HG];
 #pragma unroll
-          for (int k = 0; k < HG; ++k) {
-            const uint32_t b = __ballot_sync(0xffffffffu, (pb >> k) & 1u);
-            if (lane == k) pw[(h * kBlocks + (c >> 5)) * HG + k] = b;
+          for (int k = 0; k < HG; ++k) bw[k] = __ballot_sync(0xffffffffu, (pb >> k) & 1u);
+          if (lane == 0) {
+            uint4* dst = reinterpret_cast<uint4*>(pw + (h * kBlocks + (c >> 5)) * HG);
+            dst[0] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+            dst[1] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
           }
         }
       }
@@ -449,50 +526,39 @@ __global__ void __launch_bounds__(kFastThreads, 2)
           Vs[j] = V;
         }
       }
-      const float alpha_f = (float)p.alpha, fx_f = (float)p.fx, fy_f = (float)p.fy;
       float o[12];
 #pragma unroll
-      for (int j = 0; j < kRun; ++j) {
-        const T dcv = drow[j];
-        const bool valid = (((win >> j) & 1u) == 0u) && (dcv > (T)0);
-        validbits |= (valid ? 1u : 0u) << j;
-        float px, py, pz, nx, ny, nz;
-        const int xg = xb + j;
-        const float du_f = (du_hi + (float)j) - p.u0_lo;
+      for (int j = 0; j < kRun; j += 2) {
+        const T d0 = drow[j], d1 = drow[j + 1];
+        const bool ok0 = (((win >> j) & 1u) == 0u) && (d0 > (T)0);
+        const bool ok1 = (((win >> (j + 1)) & 1u) == 0u) && (d1 > (T)0);
+        validbits |= ((ok0 ? 1u : 0u) | (ok1 ? 2u : 0u)) << j;
         if constexpr (sizeof(T) == 4) {
-          point_from_disparity((float)dcv, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
-          if (valid) {
-            normal_square(Us[j], Vs[j], alpha_f, (float)dcv, du_f, dv_f, fx_f, fy_f, p, nx, ny, nz);
-          } else {
-            nx = ny = nz = __int_as_float(0x7fc00000);
-          }
+          records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], (float)d0, (float)d1, ok0, ok1,
+                       du_hi + (float)j, dv_f, p, o);
         } else {
-          point_from_disparity_f64((double)dcv, (double)xg - p.u0, dv, p, px, py, pz);
-          if (valid) {
-            normal_from_moments(Us[j], Vs[j], p.alpha, (double)dcv, (double)xg - p.u0, dv, p.fx,
-                                p.fy, nx, ny, nz);
-          } else {
-            nx = ny = nz = __int_as_float(0x7fc00000);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double dcv = (double)(e ? d1 : d0);
+            const double du = (double)(xb + j + e) - p.u0;
+            float* r = o + 6 * e;
+            point_from_disparity_f64(dcv, du, dv, p, r[0], r[1], r[2]);
+            if (e ? ok1 : ok0)
+              normal_from_moments(Us[j + e], Vs[j + e], p.alpha, dcv, du, dv, p.fx, p.fy, r[3],
+                                  r[4], r[5]);
+            else
+              r[3] = r[4] = r[5] = __int_as_float(0x7fc00000);
           }
         }
-        const int s6 = (j & 1) * 6;
-        o[s6 + 0] = px;
-        o[s6 + 1] = py;
-        o[s6 + 2] = pz;
-        o[s6 + 3] = nx;
-        o[s6 + 4] = ny;
-        o[s6 + 5] = nz;
-        if (j & 1) {
-          // pixels (j-1, j) = 12 floats = 3 chunks of the 128B-swizzled staging row
-          const int K = q * (kRun * 6 / 4) + (j >> 1) * 3;  // chunk index in the 768-float row
+        // pixels (j, j+1) = 12 floats = 3 chunks of the 128B-swizzled staging row
+        const int K = q * (kRun * 6 / 4) + (j >> 1) * 3;  // chunk index in the 768-float row
 #pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            const int kk = K + t;
-            const uint32_t box = (uint32_t)(kk >> 3);
-            const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
-            st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[4 * t], o[4 * t + 1],
-                         o[4 * t + 2], o[4 * t + 3]);
-          }
+        for (int t = 0; t < 3; ++t) {
+          const int kk = K + t;
+          const uint32_t box = (uint32_t)(kk >> 3);
+          const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
+          st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[4 * t], o[4 * t + 1],
+                       o[4 * t + 2], o[4 * t + 3]);
         }
       }
       if (mask_out != nullptr && yg < H) {

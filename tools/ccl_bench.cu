@@ -56,6 +56,43 @@ __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
     b = old;
   }
 }
+// padded shared-memory layout: one pad word per 32 nodes, so the lanes of a
+// warp (8 rows x 4 words) touching the same bit position hit distinct banks
+__device__ __forceinline__ int px_(int x) { return x + (x >> 5); }
+__device__ __forceinline__ int pfind(volatile int32_t* L, int x) {
+  while (true) {
+    const int p = L[px_(x)];
+    if (p == x) return x;
+    const int gp = L[px_(p)];
+    if (gp == p) return p;
+    L[px_(x)] = gp;
+    x = gp;
+  }
+}
+__device__ __forceinline__ int proot(const volatile int32_t* L, int x) {
+  int p = L[px_(x)];
+  while (p != x) {
+    x = p;
+    p = L[px_(x)];
+  }
+  return x;
+}
+__device__ __forceinline__ void punite(int32_t* L, int a, int b) {
+  volatile int32_t* V = L;
+  while (true) {
+    a = pfind(V, a);
+    b = pfind(V, b);
+    if (a == b) return;
+    if (a > b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicMin(&L[px_(b)], a);
+    if (old == b) return;
+    b = old;
+  }
+}
 __device__ __forceinline__ uint32_t run_starts(uint32_t A) { return A & ~(A << 1); }
 __device__ __forceinline__ int start_of(uint32_t st, int p) {
   const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
@@ -63,8 +100,10 @@ __device__ __forceinline__ int start_of(uint32_t st, int p) {
 }
 
 // unions of the run starting at bit s of word (r, w) with the row above
+template <bool PAD = false>
 __device__ __forceinline__ void vertical_unions(int32_t* L, const uint32_t* bits, int r, int w,
                                                 int s) {
+  auto unite = [&](int a, int b) { if (PAD) punite(L, a, b); else uf_unite(L, a, b); };
   const int rw = r * WPR + w;
   const uint32_t A = bits[rw];
   const uint32_t B = bits[rw - WPR];
@@ -79,21 +118,23 @@ __device__ __forceinline__ void vertical_unions(int32_t* L, const uint32_t* bits
   uint32_t o = (run | (run << 1) | (run >> 1)) & B;
   while (o) {
     const int p = __ffs(o) - 1;
-    uf_unite(L, n, bbase + start_of(stB, p));
+    unite(n, bbase + start_of(stB, p));
     const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
     const uint32_t zb = ~B & ~upto;
     if (!zb) break;
     o &= ~((zb & (0u - zb)) - 1u);
   }
-  if ((run & 1u) && (BL >> 31)) uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(BL))));
-  if ((run >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
+  if ((run & 1u) && (BL >> 31)) unite(n, bbase - 32 + (31 - __clz(run_starts(BL))));
+  if ((run >> 31) && (BR & 1u)) unite(n, bbase + 32);
 }
 
+template <bool PAD = false>
 __device__ __forceinline__ void horizontal_union(int32_t* L, const uint32_t* bits, int r, int w) {
   const int rw = r * WPR + w;
   if ((bits[rw] & 1u) && w > 0) {
     const uint32_t Al = bits[rw - 1];
-    if (Al >> 31) uf_unite(L, r * TW + w * 32, r * TW + w * 32 - 32 + (31 - __clz(run_starts(Al))));
+    const int a = r * TW + w * 32, b = r * TW + w * 32 - 32 + (31 - __clz(run_starts(Al)));
+    if (Al >> 31) { if (PAD) punite(L, a, b); else uf_unite(L, a, b); }
   }
 }
 
@@ -109,6 +150,7 @@ __device__ __forceinline__ int slot_row(int slot) {
 }
 
 // write per-pixel local root (tile pixel index) or -1
+template <bool PAD = false>
 __device__ void emit(const int32_t* L, const uint32_t* bits, int32_t* out, int frame, int H, int W,
                      int x0, int y0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -116,7 +158,10 @@ __device__ void emit(const int32_t* L, const uint32_t* bits, int32_t* out, int f
     const int r = rw / WPR, w = rw % WPR;
     const uint32_t A = bits[rw];
     int v = -1;
-    if ((A >> lane) & 1u) v = L[r * TW + w * 32 + start_of(run_starts(A), lane)];
+    if ((A >> lane) & 1u) {
+      const int n = r * TW + w * 32 + start_of(run_starts(A), lane);
+      v = L[PAD ? px_(n) : n];
+    }
     const int gy = y0 + r, gx = x0 + w * 32 + lane;
     if (gy < H && gx < W) out[((int64_t)frame * H + gy) * W + gx] = v;
   }
@@ -126,7 +171,7 @@ template <int V>
 __global__ void __launch_bounds__(NT) tile_kernel(const uint32_t* __restrict__ gbits, int nsrc,
                                                   int H, int W, int WW, int32_t* out,
                                                   long long* clk) {
-  __shared__ int32_t L[TH * TW];
+  __shared__ int32_t L[TH * TW + TH * TW / 32];
   __shared__ uint32_t bits[NT];
   __shared__ uint16_t lst[NT / 32][32 * 16];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -180,6 +225,22 @@ __global__ void __launch_bounds__(NT) tile_kernel(const uint32_t* __restrict__ g
       atomicAdd(&g_phase[1], (unsigned long long)(tb - ta));
       atomicAdd(&g_phase[2], (unsigned long long)(tc - tb));
     }
+  } else if (V == 4) {
+    const int r = tid / WPR, w = tid % WPR;
+    const uint32_t st = run_starts(bits[tid]);
+    for (uint32_t m = st; m; m &= m - 1u) {
+      const int n = r * TW + w * 32 + __ffs(m) - 1;
+      L[px_(n)] = n;
+    }
+    __syncthreads();
+    horizontal_union<true>(L, bits, r, w);
+    if (r > 0)
+      for (uint32_t m = st; m; m &= m - 1u) vertical_unions<true>(L, bits, r, w, __ffs(m) - 1);
+    __syncthreads();
+    for (uint32_t m = st; m; m &= m - 1u) {
+      const int n = r * TW + w * 32 + __ffs(m) - 1;
+      L[px_(n)] = proot(L, n);
+    }
   } else if (V == 1) {
     const int r = slot_row(tid / WPR), w = tid % WPR;
     const uint32_t st = run_starts(bits[r * WPR + w]);
@@ -220,7 +281,8 @@ __global__ void __launch_bounds__(NT) tile_kernel(const uint32_t* __restrict__ g
   }
   __syncthreads();
   long long t1 = clock64();
-  emit(L, bits, out, f, H, W, x0, y0);
+  if (V == 4) emit<true>(L, bits, out, f, H, W, x0, y0);
+  else emit(L, bits, out, f, H, W, x0, y0);
   if (tid == 0 && clk) clk[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t1 - t0;
 }
 
@@ -295,13 +357,14 @@ int main(int argc, char** argv) {
       case 1: tile_kernel<1><<<grid, NT>>>(dbits, nsrc, H, W, WW, dout, clk); break;
       case 2: tile_kernel<2><<<grid, NT>>>(dbits, nsrc, H, W, WW, dout, clk); break;
       case 3: tile_kernel<3><<<grid, NT>>>(dbits, nsrc, H, W, WW, dout, clk); break;
+      case 4: tile_kernel<4><<<grid, NT>>>(dbits, nsrc, H, W, WW, dout, clk); break;
     }
   };
   const char* names[] = {"V0 concurrent (row,word)", "V1 rounds+remap", "V2 warp-balanced list",
-                         "V3 pixel lanes (run starts)"};
+                         "V3 pixel lanes (run starts)", "V4 = V0 + padded smem"};
   std::vector<int32_t> got((size_t)nsrc * H * W);
   std::vector<long long> clk(ntiles);
-  for (int v = 0; v < 4; ++v) {
+  for (int v = 0; v < 5; ++v) {
     run(v, dclk);
     cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(clk.data(), dclk, ntiles * 8, cudaMemcpyDeviceToHost);

@@ -80,7 +80,8 @@ def num(d, key):
     v, u = d.get(key, ("nan", ""))
     v = float(v.replace(",", "")) if v not in ("", "n/a") else float("nan")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-             "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(u, 1.0)
+             "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6,
+             "ms": 1e-3, "s": 1.0}.get(u, 1.0)
     return v * scale
 
 
