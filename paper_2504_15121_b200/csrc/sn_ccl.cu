@@ -24,12 +24,13 @@
 //      (predicate -> bits by ballot, unless the fused pass already emitted
 //      them), run union-find in shared memory, tile-border labels -> compact
 //      seam rows / columns, global node init G[root] = root for
-//      border-touching roots, and every pixel's local root as a 2-byte tile
-//      index + the tile's border-root flags for pass 3.
+//      border-touching roots, and the tile's parent array (2-byte node ids,
+//      roots at run starts) + border-root flags for pass 3.
 //   2. ccl_seam_kernel   unions across tile seams in global memory (G is the
 //      label array itself; only border-touching roots are ever nodes).
 //   3. ccl_resolve_kernel  walks G once per border-touching root, then maps
-//      each pixel's 2-byte local root to its label with coalesced stores.
+//      each pixel to its run start (bit ops), the run to its root (the tile's
+//      parent array) and the root to its label, with coalesced stores.
 //
 // HBM traffic per pixel from the fused pass's bit mask: 1/8 B bits in, 2 B
 // local roots out and back, 4 B labels out (+ the sparse seam/root traffic),
@@ -237,7 +238,7 @@ constexpr int kTilePx = kLTW * kLTH;  // 8192: tile pixel index fits 13 bits
 
 struct CclWorkspace {
   uint32_t* bits;  // [B][H][WW]
-  uint16_t* roots;  // [tile][kTilePx] local root (tile pixel index) per pixel, tile-major
+  uint16_t* roots;  // [tile][kTilePx] tile parent array (roots at run starts), tile-major
   uint32_t* flags;  // [tile][kTilePx / 32] border-touching roots
   int32_t* top;    // [B][n_ty][W]  first row of each tile row
   int32_t* bot;    // [B][n_ty][W]  last row of each tile row
@@ -371,13 +372,14 @@ __global__ void __launch_bounds__(kLThreads)
     }
     ws.flags[tile * (kTilePx / 32) + tid] = flag[tid];
   }
-  uint16_t* roots = ws.roots + tile * kTilePx;
-  for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
-    const uint32_t A = bits[rw];
-    const int n0 = (rw >> 2) * kLTW + (rw & 3) * 32;
-    uint16_t v = 0xffffu;
-    if ((A >> lane) & 1u) v = (uint16_t)L[n0 + start_of(run_starts(A), lane)];
-    roots[n0 + lane] = v;
+  // the tile's parent array (run-start entries = roots) as 2-byte node ids;
+  // the resolve pass maps pixels to their run start itself
+  uint2* dst = reinterpret_cast<uint2*>(ws.roots + tile * kTilePx);
+  const int4* src = reinterpret_cast<const int4*>(L);
+#pragma unroll
+  for (int i = 0; i < kTilePx / 4 / kLThreads; ++i) {
+    const int4 v = src[i * kLThreads + tid];
+    dst[i * kLThreads + tid] = make_uint2(__byte_perm(v.x, v.y, 0x5410), __byte_perm(v.z, v.w, 0x5410));
   }
 }
 
@@ -444,6 +446,8 @@ __global__ void ccl_seam_kernel(const CclParams p, const CclWorkspace ws,
 
 __global__ void __launch_bounds__(kLThreads)
     ccl_resolve_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
+  __shared__ __align__(16) uint16_t Ls[kTilePx];  // tile parents (roots at run starts)
+  __shared__ uint32_t bits[kLThreads];
   __shared__ uint32_t flag[kLThreads];
   __shared__ int32_t rank0[kLThreads];  // flagged roots before word i
   __shared__ int32_t fin[kLThreads * 2];  // final label per flagged root (<= border pixels)
@@ -454,6 +458,16 @@ __global__ void __launch_bounds__(kLThreads)
   const int x0 = tx * kLTW, y0 = ty * kLTH;
   const int64_t fbase = (int64_t)blockIdx.z * p.H * p.W;
   const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(ws.roots + tile * kTilePx);
+    uint4* dst = reinterpret_cast<uint4*>(Ls);
+#pragma unroll
+    for (int i = 0; i < kTilePx / 8 / kLThreads; ++i) dst[i * kLThreads + tid] = src[i * kLThreads + tid];
+    const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
+    bits[tid] = (y0 + r < H && wc < ws.WW)
+                    ? ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc]
+                    : 0u;
+  }
   const uint32_t fw = ws.flags[tile * (kTilePx / 32) + tid];
   flag[tid] = fw;
   // exclusive prefix of popcounts over the 256 flag words
@@ -483,15 +497,16 @@ __global__ void __launch_bounds__(kLThreads)
     }
   }
   __syncthreads();
-  const uint16_t* roots = ws.roots + tile * kTilePx;
   int32_t* out = labels + fbase;
+  const bool full = x0 + kLTW <= W && y0 + kLTH <= H;
   for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
     const int r = rw >> 2, w = rw & 3;
     const int gx = x0 + w * 32 + lane, gy = y0 + r;
-    const int v = roots[r * kLTW + w * 32 + lane];
-    if (gx >= W || gy >= H) continue;
+    if (!full && (gx >= W || gy >= H)) continue;
+    const uint32_t A = bits[rw];
     int32_t lab = -1;
-    if (v != 0xffff) {
+    if ((A >> lane) & 1u) {
+      const int v = Ls[r * kLTW + w * 32 + start_of(run_starts(A), lane)];
       const uint32_t fwv = flag[v >> 5];
       const uint32_t bit = 1u << (v & 31);
       lab = (fwv & bit) ? fin[rank0[v >> 5] + __popc(fwv & (bit - 1u))] : frame_index(v, x0, y0, W);
