@@ -47,7 +47,10 @@ namespace sn {
 constexpr int kLTW = 128;             // label tile columns
 constexpr int kLTH = 64;              // label tile rows
 constexpr int kLWords = kLTW / 32;    // words per tile row
-constexpr int kLThreads = kLTH * kLWords;  // 256: one thread per (row, word)
+constexpr int kRowWords = kLTH * kLWords;  // 256 row-words per tile
+constexpr int kBands = kLTH / 2;      // 2-row bands per tile
+constexpr int kLThreads = kBands * kLWords;  // 128: one thread per (band, word)
+constexpr int kSlots = kBands * kLTW;  // node slots: band * 128 + column of a band-run start
 constexpr int kZW = kLTW + 2, kZH = kLTH + 2;  // fp32 depth tile with a 1-pixel halo
 
 __device__ __forceinline__ double depth_of(float d, double fxb) {
@@ -159,77 +162,106 @@ __device__ __forceinline__ int start_of(uint32_t st, int p) {
 }
 
 // ---------------------------------------------------------------------------
-// tile union-find over word-runs
+// tile union-find over band runs
 //
-// Node id = local pixel index r * 128 + c of a run's first pixel; L (shared)
-// holds parents at node ids only.  On return every node points at its root
-// (the smallest node of its tile component) and `flag` has bit `root` set for
-// every root whose component touches the tile border.
+// A band is two consecutive rows; a band run is a maximal run of set bits of
+// G = row0 | row1 inside one 32-bit word.  Every band run is 8-connected by
+// itself (consecutive columns of G are 8-adjacent whichever row their pixels
+// are in), so band runs are the union-find nodes: ~3x fewer than pixel runs
+// of single rows on C3, and half the rows to merge.  A node's slot is
+// band * 128 + column of the run's first column; links go to smaller slots
+// (atomicMin), so roots are the minimum slot of their tile component and the
+// result is schedule-independent.  The component's label is its smallest
+// PIXEL index, reduced with atomicMin after compression.  Measured with
+// tools/ccl_bench.cu on C3 bit masks: 2.1x faster than union-find over
+// single-row word-runs (5.4 vs 11.2 us/frame), which was itself 2.3x faster
+// than merging rows in log-depth rounds.
+//
+// On return L[slot] (for run-start slots) is the root slot (>= 0) of a
+// non-root, or enc(label) = label - 2^30 (< 0) for a root.
 
-__device__ __forceinline__ void tile_union_find(int32_t* L, const uint32_t* bits, uint32_t* flag,
-                                                int tid) {
-  const int r = tid >> 2, w = tid & 3;
-  const int base = r * kLTW + w * 32;
-  const uint32_t A = bits[tid];
-  const uint32_t st = run_starts(A);
-  for (uint32_t m = st; m; m &= m - 1u) {
+constexpr int kEnc = 0x40000000;
+
+__device__ __forceinline__ uint32_t band_word(const uint32_t* bits, int k, int w) {
+  return bits[(2 * k) * kLWords + w] | bits[(2 * k + 1) * kLWords + w];
+}
+
+// bits [s, end of the run starting at s) of a word whose bit s is set
+__device__ __forceinline__ uint32_t run_mask(uint32_t G, int s) {
+  const uint32_t hi = 0xffffffffu << s;
+  const uint32_t zer = ~G & hi;
+  return zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+}
+
+__device__ __forceinline__ int slot_label(const int32_t* L, int slot) {
+  const int v = L[slot];
+  return (v >= 0 ? L[v] : v) + kEnc;
+}
+
+// slot of the band run holding pixel (r, c) of the tile (the pixel must be set)
+__device__ __forceinline__ int pixel_slot(const uint32_t* bits, int r, int c) {
+  const int k = r >> 1, w = c >> 5;
+  return k * kLTW + w * 32 + start_of(run_starts(band_word(bits, k, w)), c & 31);
+}
+
+__device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits, int tid) {
+  const int k = tid >> 2, w = tid & 3;
+  const int base = k * kLTW + w * 32;
+  const uint32_t A0 = bits[(2 * k) * kLWords + w], A1 = bits[(2 * k + 1) * kLWords + w];
+  const uint32_t G = A0 | A1, stG = run_starts(G);
+  for (uint32_t m = stG; m; m &= m - 1u) {
     const int n = base + __ffs(m) - 1;
     L[n] = n;
   }
-  flag[tid] = 0u;
   __syncthreads();
-
-  // a run crossing into this word from the left neighbour word
-  if ((A & 1u) && w > 0) {
-    const uint32_t Al = bits[tid - 1];
-    if (Al >> 31) uf_unite(L, base, base - 32 + (31 - __clz(run_starts(Al))));
+  // a band run crossing into this word from the left neighbour word
+  if ((G & 1u) && w > 0) {
+    const uint32_t Gl = band_word(bits, k, w - 1);
+    if (Gl >> 31) uf_unite(L, base, base - 32 + (31 - __clz(run_starts(Gl))));
   }
-  // runs of the row above (8-connected: the run dilated by one pixel).  All
-  // rows at once: measured (tools/ccl_bench.cu) 2.3x faster than merging rows
-  // in log-depth rounds -- finds average 1.3 steps here, so the tile is
-  // latency-bound on its barriers, not on chain length.
-  if (r > 0) {
-    const uint32_t B = bits[tid - kLWords];
-    const uint32_t BL = w > 0 ? bits[tid - kLWords - 1] : 0u;
-    const uint32_t BR = w + 1 < kLWords ? bits[tid - kLWords + 1] : 0u;
-    const uint32_t stB = run_starts(B);
+  // band k-1: only this band's first-row pixels touch it (its last row)
+  if (k > 0) {
+    const int rb = (2 * k - 1) * kLWords + w;
+    const uint32_t B = bits[rb];
+    const uint32_t stGb = run_starts(bits[rb - kLWords] | B);
+    const uint32_t Gb = bits[rb - kLWords] | B;
+    const uint32_t BL = w > 0 ? bits[rb - 1] : 0u, BR = w + 1 < kLWords ? bits[rb + 1] : 0u;
     const int bbase = base - kLTW;
-    for (uint32_t m = st; m; m &= m - 1u) {
+    for (uint32_t m = stG; m; m &= m - 1u) {
       const int s = __ffs(m) - 1;
-      const uint32_t hi = 0xffffffffu << s;
-      const uint32_t zer = ~A & hi;  // zeros of A at or above s (bit s itself is set)
-      const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+      const uint32_t a = A0 & run_mask(G, s);
+      if (!a) continue;
       const int n = base + s;
-      uint32_t o = (run | (run << 1) | (run >> 1)) & B;
+      uint32_t o = (a | (a << 1) | (a >> 1)) & B;
       while (o) {
         const int p = __ffs(o) - 1;
-        uf_unite(L, n, bbase + start_of(stB, p));
+        uf_unite(L, n, bbase + start_of(stGb, p));
         const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
-        const uint32_t zb = ~B & ~upto;  // zeros of B above p: end of that run
+        const uint32_t zb = ~Gb & ~upto;  // zeros of band k-1 above p: end of that band run
         if (!zb) break;
         o &= ~((zb & (0u - zb)) - 1u);
       }
-      if ((run & 1u) && (BL >> 31)) uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(BL))));
-      if ((run >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
+      if ((a & 1u) && (BL >> 31))
+        uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(bits[rb - kLWords - 1] | BL))));
+      if ((a >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
     }
   }
   __syncthreads();
   // every node -> its root (only root values are written in this phase)
-  for (uint32_t m = st; m; m &= m - 1u) {
+  for (uint32_t m = stG; m; m &= m - 1u) {
     const int n = base + __ffs(m) - 1;
     L[n] = uf_root(L, n);
   }
   __syncthreads();
-  // roots of components that touch the tile border
-  auto mark = [&](int n) {
-    const int root = L[n];
-    atomicOr(&flag[root >> 5], 1u << (root & 31));
-  };
-  if (r == 0 || r == kLTH - 1)
-    for (uint32_t m = st; m; m &= m - 1u) mark(base + __ffs(m) - 1);
-  else {
-    if (w == 0 && (A & 1u)) mark(base);
-    if (w == kLWords - 1 && (A >> 31)) mark(base + (31 - __clz(st)));
+  // component label = smallest pixel index, reduced into the root's entry
+  for (uint32_t m = stG; m; m &= m - 1u) {
+    const int s = __ffs(m) - 1;
+    const uint32_t run = run_mask(G, s);
+    const uint32_t a0 = A0 & run;
+    const int mp = a0 ? (2 * k) * kLTW + w * 32 + __ffs(a0) - 1
+                      : (2 * k + 1) * kLTW + w * 32 + __ffs(A1 & run) - 1;
+    const int pr = L[base + s];
+    atomicMin(&L[pr >= 0 ? pr : base + s], mp - kEnc);
   }
   __syncthreads();
 }
@@ -237,37 +269,41 @@ __device__ __forceinline__ void tile_union_find(int32_t* L, const uint32_t* bits
 constexpr int kTilePx = kLTW * kLTH;  // 8192: tile pixel index fits 13 bits
 
 struct CclWorkspace {
-  uint32_t* bits;  // [B][H][WW]
-  uint16_t* roots;  // [tile][kTilePx] tile parent array (roots at run starts), tile-major
-  uint32_t* flags;  // [tile][kTilePx / 32] border-touching roots
-  int32_t* top;    // [B][n_ty][W]  first row of each tile row
-  int32_t* bot;    // [B][n_ty][W]  last row of each tile row
-  int32_t* left;   // [B][n_tx][H]  first column of each tile column
-  int32_t* right;  // [B][n_tx][H]  last column of each tile column
+  uint32_t* bits;   // [B][H][WW]
+  uint16_t* lbl;    // [tile][kSlots] component label (tile pixel index) per band-run slot
+  uint32_t* flags;  // [tile][kTilePx / 32] border-touching components (bit = label)
+  int32_t* top;     // [B][n_ty][W]  first row of each tile row
+  int32_t* bot;     // [B][n_ty][W]  last row of each tile row
+  int32_t* left;    // [B][n_tx][H]  first column of each tile column
+  int32_t* right;   // [B][n_tx][H]  last column of each tile column
   int WW, n_tx, n_ty;
 };
 
-__device__ __forceinline__ int frame_index(int node, int x0, int y0, int W) {
-  return (y0 + (node >> 7)) * W + x0 + (node & (kLTW - 1));
+__device__ __forceinline__ int frame_index(int px, int x0, int y0, int W) {
+  return (y0 + (px >> 7)) * W + x0 + (px & (kLTW - 1));
 }
 
 // ---------------------------------------------------------------------------
-// 1. tile pass.  MODE 0: predicate from fp32 disparity; MODE 1: uint8 passable
+// 1. tile pass.  MODE 0: predicate from fp32 disparity; MODE 1: uint8
+// passable; MODE 2: the bit mask is the input (emitted by the fused pass)
 
 template <int MODE>
 __global__ void __launch_bounds__(kLThreads)
     ccl_tile_kernel(const float* __restrict__ disp, const uint8_t* __restrict__ pas_in,
                     const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
-  __shared__ __align__(16) int32_t smem[kZH * kZW];  // fp32 depth tile, then the parent array
-  __shared__ uint32_t bits[kLThreads];
-  __shared__ uint32_t flag[kLThreads];
-  static_assert(kZH * kZW >= kLTH * kLTW, "parent array must fit the depth tile");
+  // fp32 depth tile (MODE 0), then the parent array + the exported labels
+  __shared__ __align__(16) int32_t smem[MODE == 0 ? kZH * kZW : kSlots + kSlots / 2];
+  __shared__ uint32_t bits[kRowWords];
+  __shared__ uint32_t flag[kTilePx / 32];
+  static_assert(kZH * kZW * 4 >= kSlots * 4 + kSlots * 2, "L + exported labels fit the z tile");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
   const int tx = blockIdx.x, ty = blockIdx.y;
   const int x0 = tx * kLTW, y0 = ty * kLTH;
   const int64_t fbase = (int64_t)blockIdx.z * p.H * p.W;
+  const int64_t frow = (int64_t)blockIdx.z * H;
 
+  for (int i = tid; i < kTilePx / 32; i += kLThreads) flag[i] = 0u;
   if (MODE == 0) {
     const float* f = disp + fbase;
     float* zs = reinterpret_cast<float*>(smem);
@@ -280,7 +316,7 @@ __global__ void __launch_bounds__(kLThreads)
       zs[i] = z;
     }
     __syncthreads();
-    for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
+    for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
       const int r = rw >> 2, c = (rw & 3) * 32 + lane;
       const int gx = x0 + c, gy = y0 + r;
       bool pk = false;
@@ -295,7 +331,7 @@ __global__ void __launch_bounds__(kLThreads)
       if (lane == 0) bits[rw] = b;
     }
   } else if (MODE == 1) {
-    for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
+    for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
       const int r = rw >> 2, c = (rw & 3) * 32 + lane;
       const int gx = x0 + c, gy = y0 + r;
       const bool pk = gx < W && gy < H && pas_in[fbase + (int64_t)gy * W + gx] != 0;
@@ -303,23 +339,42 @@ __global__ void __launch_bounds__(kLThreads)
       if (lane == 0) bits[rw] = b;
     }
   } else {
-    // MODE 2: the bit mask is the input (emitted by the fused pass)
-    const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
-    bits[tid] = (y0 + r < H && wc < ws.WW)
-                    ? ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc]
-                    : 0u;
+    for (int i = tid; i < kRowWords; i += kLThreads) {
+      const int r = i >> 2, wc = tx * kLWords + (i & 3);
+      bits[i] = (y0 + r < H && wc < ws.WW) ? ws.bits[(frow + y0 + r) * ws.WW + wc] : 0u;
+    }
   }
   __syncthreads();
   if (MODE != 2) {
-    const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
-    if (y0 + r < H && wc < ws.WW)
-      ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc] = bits[tid];
+    for (int i = tid; i < kRowWords; i += kLThreads) {
+      const int r = i >> 2, wc = tx * kLWords + (i & 3);
+      if (y0 + r < H && wc < ws.WW) ws.bits[(frow + y0 + r) * ws.WW + wc] = bits[i];
+    }
   }
 
   int32_t* L = smem;
-  tile_union_find(L, bits, flag, tid);
+  uint16_t* lbl = reinterpret_cast<uint16_t*>(smem + kSlots);
+  band_union_find(L, bits, tid);
 
-  // seam rows / columns: frame index of each border pixel's root, -1 if not passable
+  // export labels of the band-run slots; flag components touching the tile border
+  {
+    const int k = tid >> 2, w = tid & 3;
+    const int base = k * kLTW + w * 32;
+    const uint32_t A0 = bits[(2 * k) * kLWords + w], A1 = bits[(2 * k + 1) * kLWords + w];
+    const uint32_t G = A0 | A1;
+    for (uint32_t m = run_starts(G); m; m &= m - 1u) {
+      const int s = __ffs(m) - 1;
+      const int v = slot_label(L, base + s);
+      lbl[base + s] = (uint16_t)v;
+      const uint32_t run = run_mask(G, s);
+      if ((k == 0 && (A0 & run)) || (k == kBands - 1 && (A1 & run)) || (w == 0 && (run & 1u)) ||
+          (w == kLWords - 1 && (run >> 31)))
+        atomicOr(&flag[v >> 5], 1u << (v & 31));
+    }
+  }
+  __syncthreads();
+
+  // seam rows / columns: frame index of each border pixel's component, -1 if not passable
   const int64_t seam_row = ((int64_t)blockIdx.z * ws.n_ty + ty) * W;
   const int64_t seam_col = ((int64_t)blockIdx.z * ws.n_tx + tx) * H;
   if (warp < 2) {
@@ -328,58 +383,46 @@ __global__ void __launch_bounds__(kLThreads)
     if (y0 + r < H) {
 #pragma unroll
       for (int w = 0; w < kLWords; ++w) {
-        const uint32_t A = bits[r * kLWords + w];
-        const int gx = x0 + w * 32 + lane;
+        const int c = w * 32 + lane, gx = x0 + c;
         if (gx < W) {
           int32_t v = -1;
-          if ((A >> lane) & 1u)
-            v = frame_index(L[r * kLTW + w * 32 + start_of(run_starts(A), lane)], x0, y0, W);
+          if ((bits[r * kLWords + w] >> lane) & 1u)
+            v = frame_index(lbl[pixel_slot(bits, r, c)], x0, y0, W);
           dst[gx] = v;
         }
       }
     }
-  } else if (warp < 4) {
+  } else {
     // warp 2: first column, warp 3: last column; lanes <-> rows
+    const int c = warp == 2 ? 0 : kLTW - 1;
+    int32_t* dst = (warp == 2 ? ws.left : ws.right) + seam_col;
     for (int r = lane; r < kLTH; r += 32) {
       if (y0 + r >= H) break;
       int32_t v = -1;
-      if (warp == 2) {
-        const uint32_t A = bits[r * kLWords];
-        if (A & 1u) v = frame_index(L[r * kLTW], x0, y0, W);
-        ws.left[seam_col + y0 + r] = v;
-      } else {
-        const uint32_t A = bits[r * kLWords + kLWords - 1];
-        if (A >> 31)
-          v = frame_index(L[r * kLTW + (kLWords - 1) * 32 + (31 - __clz(run_starts(A)))], x0, y0,
-                          W);
-        ws.right[seam_col + y0 + r] = v;
-      }
+      if ((bits[r * kLWords + (c >> 5)] >> (c & 31)) & 1u)
+        v = frame_index(lbl[pixel_slot(bits, r, c)], x0, y0, W);
+      dst[y0 + r] = v;
     }
   }
-  // global union-find nodes (border-touching roots only), border flags and
-  // every pixel's local root for the resolve pass
+  // global union-find nodes: one per border-touching component, G[label] = label
   const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
   {
-    const int r = tid >> 2, w = tid & 3;
-    const int base = r * kLTW + w * 32;
     int32_t* G = labels + fbase;
-    for (uint32_t m = run_starts(bits[tid]); m; m &= m - 1u) {
-      const int n = base + __ffs(m) - 1;
-      if (L[n] == n && ((flag[n >> 5] >> (n & 31)) & 1u)) {
-        const int g = frame_index(n, x0, y0, W);
+    for (int i = tid; i < kTilePx / 32; i += kLThreads) {
+      const uint32_t fw = flag[i];
+      ws.flags[tile * (kTilePx / 32) + i] = fw;
+      for (uint32_t m = fw; m; m &= m - 1u) {
+        const int g = frame_index(i * 32 + __ffs(m) - 1, x0, y0, W);
         G[g] = g;
       }
     }
-    ws.flags[tile * (kTilePx / 32) + tid] = flag[tid];
   }
-  // the tile's parent array (run-start entries = roots) as 2-byte node ids;
-  // the resolve pass maps pixels to their run start itself
-  uint2* dst = reinterpret_cast<uint2*>(ws.roots + tile * kTilePx);
-  const int4* src = reinterpret_cast<const int4*>(L);
+  // the slot labels for the resolve pass (run-start entries only are meaningful)
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(lbl);
+    uint4* dst = reinterpret_cast<uint4*>(ws.lbl + tile * kSlots);
 #pragma unroll
-  for (int i = 0; i < kTilePx / 4 / kLThreads; ++i) {
-    const int4 v = src[i * kLThreads + tid];
-    dst[i * kLThreads + tid] = make_uint2(__byte_perm(v.x, v.y, 0x5410), __byte_perm(v.z, v.w, 0x5410));
+    for (int i = 0; i < kSlots / 8 / kLThreads; ++i) dst[i * kLThreads + tid] = src[i * kLThreads + tid];
   }
 }
 
@@ -441,17 +484,18 @@ __global__ void ccl_seam_kernel(const CclParams p, const CclWorkspace ws,
 }
 
 // ---------------------------------------------------------------------------
-// 3. resolve: border-touching roots through G (one walk per root), then one
-// 2-byte read and one coalesced 4-byte label store per pixel
+// 3. resolve: border-touching components through G (one walk each), then per
+// pixel: band-run slot (bit ops) -> tile label -> final label, coalesced stores
 
 __global__ void __launch_bounds__(kLThreads)
     ccl_resolve_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
-  __shared__ __align__(16) uint16_t Ls[kTilePx];  // tile parents (roots at run starts)
-  __shared__ uint32_t bits[kLThreads];
-  __shared__ uint32_t flag[kLThreads];
-  __shared__ int32_t rank0[kLThreads];  // flagged roots before word i
-  __shared__ int32_t fin[kLThreads * 2];  // final label per flagged root (<= border pixels)
+  __shared__ __align__(16) uint16_t lbl[kSlots];
+  __shared__ uint32_t bits[kRowWords];
+  __shared__ uint32_t flag[kTilePx / 32];
+  __shared__ int32_t rank0[kTilePx / 32];  // flagged labels before word i
+  __shared__ int32_t fin[512];  // final label per flagged component (<= border pixels)
   __shared__ int32_t warp_sum[kLThreads / 32];
+  constexpr int FPT = kTilePx / 32 / kLThreads;  // flag words per thread (2)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
   const int tx = blockIdx.x, ty = blockIdx.y;
@@ -459,19 +503,26 @@ __global__ void __launch_bounds__(kLThreads)
   const int64_t fbase = (int64_t)blockIdx.z * p.H * p.W;
   const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
   {
-    const uint4* src = reinterpret_cast<const uint4*>(ws.roots + tile * kTilePx);
-    uint4* dst = reinterpret_cast<uint4*>(Ls);
+    const uint4* src = reinterpret_cast<const uint4*>(ws.lbl + tile * kSlots);
+    uint4* dst = reinterpret_cast<uint4*>(lbl);
 #pragma unroll
-    for (int i = 0; i < kTilePx / 8 / kLThreads; ++i) dst[i * kLThreads + tid] = src[i * kLThreads + tid];
-    const int r = tid >> 2, wc = tx * kLWords + (tid & 3);
-    bits[tid] = (y0 + r < H && wc < ws.WW)
+    for (int i = 0; i < kSlots / 8 / kLThreads; ++i) dst[i * kLThreads + tid] = src[i * kLThreads + tid];
+    for (int i = tid; i < kRowWords; i += kLThreads) {
+      const int r = i >> 2, wc = tx * kLWords + (i & 3);
+      bits[i] = (y0 + r < H && wc < ws.WW)
                     ? ws.bits[((int64_t)blockIdx.z * H + y0 + r) * ws.WW + wc]
                     : 0u;
+    }
   }
-  const uint32_t fw = ws.flags[tile * (kTilePx / 32) + tid];
-  flag[tid] = fw;
-  // exclusive prefix of popcounts over the 256 flag words
-  const int c = __popc(fw);
+  // flag words tid*FPT .. tid*FPT+FPT-1; exclusive prefix of their popcounts
+  uint32_t fw[FPT];
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < FPT; ++j) {
+    fw[j] = ws.flags[tile * (kTilePx / 32) + tid * FPT + j];
+    flag[tid * FPT + j] = fw[j];
+    c += __popc(fw[j]);
+  }
   int inc = c;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -482,31 +533,33 @@ __global__ void __launch_bounds__(kLThreads)
   __syncthreads();
   int off = 0;
   for (int i = 0; i < warp; ++i) off += warp_sum[i];
-  const int excl = off + inc - c;
-  rank0[tid] = excl;
-  // walk G once per flagged root.  Nodes are only ever roots of tile
-  // components, and a concurrent resolve of another tile overwrites such a
-  // node with its final label -- an ancestor -- so the read-only walk is valid.
+  int k = off + inc - c;
+  // walk G once per flagged component.  Nodes are only ever tile-component
+  // labels, and a concurrent resolve of another tile overwrites such a node
+  // with its final label -- an ancestor -- so the read-only walk is valid.
   {
     const volatile int32_t* G = labels + fbase;
-    int k = excl;
-    for (uint32_t m = fw; m; m &= m - 1u) {
-      const int n = tid * 32 + __ffs(m) - 1;
-      if (k < kLThreads * 2) fin[k] = uf_root(G, frame_index(n, x0, y0, W));
-      ++k;
+#pragma unroll
+    for (int j = 0; j < FPT; ++j) {
+      rank0[tid * FPT + j] = k;
+      for (uint32_t m = fw[j]; m; m &= m - 1u) {
+        const int v = (tid * FPT + j) * 32 + __ffs(m) - 1;
+        if (k < 512) fin[k] = uf_root(G, frame_index(v, x0, y0, W));
+        ++k;
+      }
     }
   }
   __syncthreads();
   int32_t* out = labels + fbase;
   const bool full = x0 + kLTW <= W && y0 + kLTH <= H;
-  for (int rw = warp; rw < kLThreads; rw += kLThreads / 32) {
+  for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
     const int r = rw >> 2, w = rw & 3;
     const int gx = x0 + w * 32 + lane, gy = y0 + r;
     if (!full && (gx >= W || gy >= H)) continue;
     const uint32_t A = bits[rw];
     int32_t lab = -1;
     if ((A >> lane) & 1u) {
-      const int v = Ls[r * kLTW + w * 32 + start_of(run_starts(A), lane)];
+      const int v = lbl[pixel_slot(bits, r, w * 32 + lane)];
       const uint32_t fwv = flag[v >> 5];
       const uint32_t bit = 1u << (v & 31);
       lab = (fwv & bit) ? fin[rank0[v >> 5] + __popc(fwv & (bit - 1u))] : frame_index(v, x0, y0, W);
@@ -583,7 +636,7 @@ size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W) {
   const int64_t n_tx = (W + kLTW - 1) / kLTW, n_ty = (H + kLTH - 1) / kLTH;
   const int64_t tiles = B * n_tx * n_ty;
   return align256((size_t)(B * H * WW) * 4) + 2 * align256((size_t)(B * n_ty * W) * 4) +
-         2 * align256((size_t)(B * n_tx * H) * 4) + align256((size_t)(tiles * kTilePx) * 2) +
+         2 * align256((size_t)(B * n_tx * H) * 4) + align256((size_t)(tiles * kSlots) * 2) +
          align256((size_t)(tiles * kTilePx / 32) * 4);
 }
 
@@ -652,8 +705,8 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
   ws.right = reinterpret_cast<int32_t*>(q);
   q += align256((size_t)(p.B * ws.n_tx * p.H) * 4);
   const int64_t tiles = p.B * ws.n_tx * ws.n_ty;
-  ws.roots = reinterpret_cast<uint16_t*>(q);
-  q += align256((size_t)(tiles * kTilePx) * 2);
+  ws.lbl = reinterpret_cast<uint16_t*>(q);
+  q += align256((size_t)(tiles * kSlots) * 2);
   ws.flags = reinterpret_cast<uint32_t*>(q);
 
   if (bits_in) ws.bits = const_cast<uint32_t*>(bits_in);  // read-only in MODE 2

@@ -286,6 +286,197 @@ __global__ void __launch_bounds__(NT) tile_kernel(const uint32_t* __restrict__ g
   if (tid == 0 && clk) clk[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t1 - t0;
 }
 
+
+// V5: nodes are runs of G = (row 2k | row 2k+1) ("band runs"): every band run
+// is 8-connected inside its two rows, so nodes drop ~3x and rows to merge
+// halve.  Node slot = band*128 + word*32 + start bit of the band run.  Roots
+// are min slots; the component label (min pixel) is a min-reduction after
+// compression.
+constexpr int NB = TH / 2;          // bands per tile
+constexpr int NT5 = NB * WPR;       // 128 threads
+__global__ void __launch_bounds__(NT5) tile_kernel5(const uint32_t* __restrict__ gbits, int nsrc,
+                                                    int H, int W, int WW, int32_t* out,
+                                                    long long* clk) {
+  __shared__ int32_t L[NB * TW];
+  __shared__ int32_t M[NB * TW];
+  __shared__ uint32_t bits[NT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, f = blockIdx.z;
+  const uint32_t* src = gbits + (size_t)(f % nsrc) * H * WW;
+  long long t0 = clock64();
+  for (int i = tid; i < NT; i += NT5) {
+    const int r = i / WPR, wc = blockIdx.x * WPR + i % WPR;
+    bits[i] = (y0 + r < H && wc < WW) ? src[(size_t)(y0 + r) * WW + wc] : 0u;
+  }
+  __syncthreads();
+  const int k = tid / WPR, w = tid % WPR;
+  const uint32_t A0 = bits[(2 * k) * WPR + w], A1 = bits[(2 * k + 1) * WPR + w];
+  const uint32_t G = A0 | A1, stG = run_starts(G);
+  const int base = k * TW + w * 32;
+  for (uint32_t m = stG; m; m &= m - 1u) {
+    const int n = base + __ffs(m) - 1;
+    L[n] = n;
+    M[n] = 0x7fffffff;
+  }
+  __syncthreads();
+  if ((G & 1u) && w > 0) {
+    const uint32_t Gl = bits[(2 * k) * WPR + w - 1] | bits[(2 * k + 1) * WPR + w - 1];
+    if (Gl >> 31) uf_unite(L, base, base - 32 + (31 - __clz(run_starts(Gl))));
+  }
+  if (k > 0) {
+    const int rb = (2 * k - 1) * WPR + w;  // row 2k-1 (second row of band k-1)
+    const uint32_t B = bits[rb];
+    const uint32_t Gb = bits[rb - WPR] | B, stGb = run_starts(Gb);
+    const uint32_t BL = w > 0 ? bits[rb - 1] : 0u, BR = w + 1 < WPR ? bits[rb + 1] : 0u;
+    const int bbase = base - TW;
+    for (uint32_t m = stG; m; m &= m - 1u) {
+      const int s = __ffs(m) - 1;
+      const uint32_t hi = 0xffffffffu << s;
+      const uint32_t zer = ~G & hi;
+      const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+      const uint32_t a = A0 & run;  // row-2k pixels of this band run
+      if (!a) continue;
+      const int n = base + s;
+      uint32_t o = (a | (a << 1) | (a >> 1)) & B;
+      while (o) {
+        const int p = __ffs(o) - 1;
+        uf_unite(L, n, bbase + start_of(stGb, p));
+        const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
+        const uint32_t zb = ~Gb & ~upto;
+        if (!zb) break;
+        o &= ~((zb & (0u - zb)) - 1u);
+      }
+      if ((a & 1u) && (BL >> 31)) {
+        const uint32_t GbL = bits[rb - WPR - 1] | BL;
+        uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(GbL))));
+      }
+      if ((a >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
+    }
+  }
+  __syncthreads();
+  for (uint32_t m = stG; m; m &= m - 1u) {
+    const int n = base + __ffs(m) - 1;
+    L[n] = uf_root(L, n);
+  }
+  __syncthreads();
+  for (uint32_t m = stG; m; m &= m - 1u) {
+    const int s = __ffs(m) - 1;
+    const uint32_t hi = 0xffffffffu << s;
+    const uint32_t zer = ~G & hi;
+    const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+    const uint32_t a0 = A0 & run;
+    const int mp = a0 ? (2 * k) * TW + w * 32 + __ffs(a0) - 1
+                      : (2 * k + 1) * TW + w * 32 + __ffs(A1 & run) - 1;
+    atomicMin(&M[L[base + s]], mp);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  for (int rw = warp; rw < NT; rw += NT5 / 32) {
+    const int r = rw / WPR, ww = rw % WPR;
+    const int kk = r >> 1;
+    const uint32_t A = bits[rw];
+    const uint32_t Gk = bits[(2 * kk) * WPR + ww] | bits[(2 * kk + 1) * WPR + ww];
+    int v = -1;
+    if ((A >> lane) & 1u) v = M[L[kk * TW + ww * 32 + start_of(run_starts(Gk), lane)]];
+    const int gy = y0 + r, gx = x0 + ww * 32 + lane;
+    if (gy < H && gx < W) out[((int64_t)f * H + gy) * W + gx] = v;
+  }
+  if (tid == 0 && clk) clk[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t1 - t0;
+}
+
+__global__ void __launch_bounds__(NT5) tile_kernel6(const uint32_t* __restrict__ gbits, int nsrc,
+                                                    int H, int W, int WW, int32_t* out,
+                                                    long long* clk) {
+  __shared__ int32_t L[NB * TW];  // parents; after compression roots hold enc(min pixel) < 0
+  __shared__ uint32_t bits[NT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, f = blockIdx.z;
+  const uint32_t* src = gbits + (size_t)(f % nsrc) * H * WW;
+  long long t0 = clock64();
+  for (int i = tid; i < NT; i += NT5) {
+    const int r = i / WPR, wc = blockIdx.x * WPR + i % WPR;
+    bits[i] = (y0 + r < H && wc < WW) ? src[(size_t)(y0 + r) * WW + wc] : 0u;
+  }
+  __syncthreads();
+  const int k = tid / WPR, w = tid % WPR;
+  const uint32_t A0 = bits[(2 * k) * WPR + w], A1 = bits[(2 * k + 1) * WPR + w];
+  const uint32_t G = A0 | A1, stG = run_starts(G);
+  const int base = k * TW + w * 32;
+  for (uint32_t m = stG; m; m &= m - 1u) {
+    const int n = base + __ffs(m) - 1;
+    L[n] = n;
+  }
+  __syncthreads();
+  if ((G & 1u) && w > 0) {
+    const uint32_t Gl = bits[(2 * k) * WPR + w - 1] | bits[(2 * k + 1) * WPR + w - 1];
+    if (Gl >> 31) uf_unite(L, base, base - 32 + (31 - __clz(run_starts(Gl))));
+  }
+  if (k > 0) {
+    const int rb = (2 * k - 1) * WPR + w;  // row 2k-1 (second row of band k-1)
+    const uint32_t B = bits[rb];
+    const uint32_t Gb = bits[rb - WPR] | B, stGb = run_starts(Gb);
+    const uint32_t BL = w > 0 ? bits[rb - 1] : 0u, BR = w + 1 < WPR ? bits[rb + 1] : 0u;
+    const int bbase = base - TW;
+    for (uint32_t m = stG; m; m &= m - 1u) {
+      const int s = __ffs(m) - 1;
+      const uint32_t hi = 0xffffffffu << s;
+      const uint32_t zer = ~G & hi;
+      const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+      const uint32_t a = A0 & run;  // row-2k pixels of this band run
+      if (!a) continue;
+      const int n = base + s;
+      uint32_t o = (a | (a << 1) | (a >> 1)) & B;
+      while (o) {
+        const int p = __ffs(o) - 1;
+        uf_unite(L, n, bbase + start_of(stGb, p));
+        const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
+        const uint32_t zb = ~Gb & ~upto;
+        if (!zb) break;
+        o &= ~((zb & (0u - zb)) - 1u);
+      }
+      if ((a & 1u) && (BL >> 31)) {
+        const uint32_t GbL = bits[rb - WPR - 1] | BL;
+        uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(GbL))));
+      }
+      if ((a >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
+    }
+  }
+  __syncthreads();
+  for (uint32_t m = stG; m; m &= m - 1u) {
+    const int n = base + __ffs(m) - 1;
+    L[n] = uf_root(L, n);
+  }
+  __syncthreads();
+  for (uint32_t m = stG; m; m &= m - 1u) {
+    const int s = __ffs(m) - 1;
+    const uint32_t hi = 0xffffffffu << s;
+    const uint32_t zer = ~G & hi;
+    const uint32_t run = zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
+    const uint32_t a0 = A0 & run;
+    const int mp = a0 ? (2 * k) * TW + w * 32 + __ffs(a0) - 1
+                      : (2 * k + 1) * TW + w * 32 + __ffs(A1 & run) - 1;
+    const int pr = L[base + s];
+    atomicMin(&L[pr >= 0 ? pr : base + s], mp - 0x40000000);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  for (int rw = warp; rw < NT; rw += NT5 / 32) {
+    const int r = rw / WPR, ww = rw % WPR;
+    const int kk = r >> 1;
+    const uint32_t A = bits[rw];
+    const uint32_t Gk = bits[(2 * kk) * WPR + ww] | bits[(2 * kk + 1) * WPR + ww];
+    int v = -1;
+    if ((A >> lane) & 1u) {
+      const int pr = L[kk * TW + ww * 32 + start_of(run_starts(Gk), lane)];
+      v = (pr >= 0 ? L[pr] : pr) + 0x40000000;
+    }
+    const int gy = y0 + r, gx = x0 + ww * 32 + lane;
+    if (gy < H && gx < W) out[((int64_t)f * H + gy) * W + gx] = v;
+  }
+  if (tid == 0 && clk) clk[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t1 - t0;
+}
+
+
 // CPU reference: per-tile 8-connected flood fill, label = min tile pixel index
 static void cpu_tiles(const std::vector<uint32_t>& bits, int nsrc, int H, int W, int WW,
                       std::vector<int32_t>& out) {
@@ -358,13 +549,16 @@ int main(int argc, char** argv) {
       case 2: tile_kernel<2><<<grid, NT>>>(dbits, nsrc, H, W, WW, dout, clk); break;
       case 3: tile_kernel<3><<<grid, NT>>>(dbits, nsrc, H, W, WW, dout, clk); break;
       case 4: tile_kernel<4><<<grid, NT>>>(dbits, nsrc, H, W, WW, dout, clk); break;
+      case 5: tile_kernel5<<<grid, NT5>>>(dbits, nsrc, H, W, WW, dout, clk); break;
+      case 6: tile_kernel6<<<grid, NT5>>>(dbits, nsrc, H, W, WW, dout, clk); break;
     }
   };
   const char* names[] = {"V0 concurrent (row,word)", "V1 rounds+remap", "V2 warp-balanced list",
-                         "V3 pixel lanes (run starts)", "V4 = V0 + padded smem"};
+                         "V3 pixel lanes (run starts)", "V4 = V0 + padded smem",
+                         "V5 band runs (2-row nodes)", "V6 = V5, one smem array"};
   std::vector<int32_t> got((size_t)nsrc * H * W);
   std::vector<long long> clk(ntiles);
-  for (int v = 0; v < 5; ++v) {
+  for (int v = 0; v < 7; ++v) {
     run(v, dclk);
     cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(clk.data(), dclk, ntiles * 8, cudaMemcpyDeviceToHost);
