@@ -49,6 +49,7 @@ constexpr int kBoxes = kTW * 6 / kBoxF;  // 24
 constexpr int kHalfUnits = 160;    // pass-V units per half: 5 warps, 32-column aligned
 constexpr int kFastThreads = 2 * kHalfUnits;  // 10 warps; pass H uses the first 8
 constexpr int kRun = 8;            // output columns per pass-H lane
+constexpr int kStoreTid = 8 * 32;  // warp 8 issues the output TMA stores
 constexpr uint32_t kBigBits = 0x53800000u;  // fp32 bit pattern of 2^40
 
 __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -453,7 +454,8 @@ __global__ void __launch_bounds__(kFastThreads, 2)
         }
       }
     }
-    if (tid == 0) bulk_wait_read0();  // staging of the previous item consumed by TMA
+    // staging of the previous item consumed by its TMA stores (issued by warp 8)
+    if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait_read0();
     __syncthreads();
 
     // ------------------------------------------------------------ pass H + epilogue
@@ -581,16 +583,16 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     }
     fence_proxy_async_smem();
     __syncthreads();
-    if (tid == 0) {
-      fl[NC + buf] = 0u;  // reset this parity's big flag (next used two items later)
-#pragma unroll 1
-      for (int b = 0; b < kBoxes; ++b) {
-        tma_store_3d(&out_map, smem + Cfg::STAGE + (size_t)b * kG * 128, x0 * 6 + b * kBoxF, y0, bz);
-      }
+    if (tid == 0) fl[NC + buf] = 0u;  // reset this parity's big flag (next used two items later)
+    // one TMA store per 128-B box column, one lane each, from a warp that is
+    // idle in pass H -- warp 0 goes straight on to the next item
+    if (tid >= kStoreTid && tid < kStoreTid + kBoxes) {
+      const int b = tid - kStoreTid;
+      tma_store_3d(&out_map, smem + Cfg::STAGE + (size_t)b * kG * 128, x0 * 6 + b * kBoxF, y0, bz);
       bulk_commit();
     }
   }
-  if (tid == 0) bulk_wait0();
+  if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait0();
 }
 
 // ---------------------------------------------------------------------------
