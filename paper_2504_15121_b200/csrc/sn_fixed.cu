@@ -61,20 +61,42 @@ struct FastCfg {
   static constexpr int AE = 16 / (int)sizeof(T);
   // the box starts at (x0 - R) rounded down to 16 B, so it spans up to AE-1 extra columns
   static constexpr int BW = (NC + AE - 1 + AE - 1) / AE * AE;
-  static constexpr size_t STAGE = 0;
   static constexpr size_t STAGE_BYTES = (size_t)kBoxes * kG * 128;
   static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
+  static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;  // double2 (C, Rr) [NC][kCP]
+  static constexpr size_t FL_BYTES = align_up((size_t)NC * 4, 16);
+  // passable ballots [half][column block of 32][row of the half]
+  static constexpr size_t PW_BYTES = 2 * (kHalfUnits / 32) * (kG / 2) * 4;
+  // single-CTA-pipeline layout (classic kernel: 1 stage, 2 inputs, 1 CR)
+  static constexpr size_t STAGE = 0;
   static constexpr size_t IN0 = STAGE + STAGE_BYTES;
   static constexpr size_t IN1 = align_up(IN0 + IN_BYTES, 128);
-  static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);  // double2 (C, Rr) [NC][kCP]
-  static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;
+  static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);
   static constexpr size_t FL = align_up(CS + CS_BYTES, 16);
-  // passable ballots [half][column block of 32][row of the half]
-  static constexpr size_t PW = align_up(FL + (NC + 2) * 4, 16);
-  static constexpr size_t BAR = PW + 2 * (kHalfUnits / 32) * (kG / 2) * 4;
+  static constexpr size_t PW = align_up(FL + FL_BYTES, 16);
+  static constexpr size_t BAR = PW + PW_BYTES;
   static constexpr size_t TOTAL = BAR + 16 + 1024;  // + slack for 1024-B alignment
   static_assert(NC <= kHalfUnits, "pass V: one unit per thread");
   static_assert(NR <= 32, "row validity bits must fit 32 bits");
+};
+
+// warp-specialised pipeline layout: 2 staging tiles, 3 input tiles, 2 x (CR,
+// flags, ballots), 10 mbarriers
+template <int R>
+struct PipeCfg {
+  using C = FastCfg<R, float>;
+  static constexpr int kIn = 3, kCr = 2, kSt = 2;
+  static constexpr size_t STAGE = 0;
+  static constexpr size_t IN = STAGE + kSt * C::STAGE_BYTES;
+  static constexpr size_t IN_STRIDE = align_up(C::IN_BYTES, 128);
+  static constexpr size_t CS = IN + kIn * IN_STRIDE;
+  static constexpr size_t CS_STRIDE = align_up(C::CS_BYTES, 128);
+  static constexpr size_t FL = CS + kCr * CS_STRIDE;
+  static constexpr size_t PW = FL + kCr * C::FL_BYTES;
+  static constexpr size_t BAR = align_up(PW + kCr * C::PW_BYTES, 16);
+  static constexpr int kBars = kIn * 2 + kCr * 2 + kSt * 2;
+  static constexpr size_t TOTAL = BAR + kBars * 8 + 1024;
+  static constexpr bool fits = TOTAL <= 227 * 1024;
 };
 
 template <typename T>
@@ -191,19 +213,368 @@ __device__ __forceinline__ void records_pair(double U0, double V0, double U1, do
 // ---------------------------------------------------------------------------
 // fast path: centred square pattern, radius R
 //
-// Per item (128 columns x 16 rows of one frame), 10 warps:
-//   pass V  unit = (half h, column c): warps 5h .. 5h+4, lane <-> column, so
+// Per item (128 columns x 16 rows of one frame):
+//   pass V  unit = (half h, column c), 5 warps per half, lane <-> column, so
 //           each warp covers 32 aligned columns.  C, Rr for the 8 output rows
 //           of the half as a sliding chain -> smem, column-major (pitch 17
-//           doubles: conflict-free for both passes).  With a threshold, the
-//           same registers give the ST-passable bits: depths of the unit's
-//           rows, left/right depths by shuffle, one ballot per row.
-//   pass H  warps 0-7, lane <-> (output row, run of 8 columns): U, V as a
-//           sliding chain, closed-form normal + point, 6 floats per pixel
-//           into the 128B-swizzled staging tile.  Warps 8-9 meanwhile turn
-//           the ballots into bit-mask words and store them.
-// The input tile is double-buffered: the TMA load of item i+1 is in flight
-// during all of item i.
+//           doubles: conflict-free for both passes), validity bits per column
+//           (bit 8 of a half's flags: a sample too large for exact sliding).
+//           With a threshold, the same registers give the ST-passable bits:
+//           depths of the unit's rows, left/right depths by shuffle, one
+//           ballot per row.
+//   pass H  8 warps, lane <-> (output row, run of 8 columns): U, V as a
+//           sliding chain, closed-form normal + point (packed f32x2), 6 floats
+//           per pixel into the 128B-swizzled staging tile, TMA stores.
+// Two kernels share the passes: fixed_square_kernel (2 CTAs/SM, passes
+// separated by CTA barriers, any R <= 8, fp32/fp64) and
+// fixed_square_pipe_kernel (1 CTA/SM, warp-specialised: pass V of item i+1,
+// pass H of item i and the TMA traffic of other items run concurrently,
+// synchronised by mbarriers; fp32, R <= 4).
+
+struct ItemDecoder {
+  int tiles_x, tiles_y;
+  double inv_tx, inv_ty;
+  __device__ ItemDecoder(int tx, int ty)
+      : tiles_x(tx), tiles_y(ty), inv_tx(1.0 / (double)tx), inv_ty(1.0 / (double)ty) {}
+  __device__ static unsigned udiv(unsigned u, unsigned d, double inv) {  // exact for u < 2^31
+    unsigned q = (unsigned)((double)u * inv);
+    if (q * d > u) --q;
+    else if ((q + 1) * d <= u) ++q;
+    return q;
+  }
+  __device__ void operator()(int it, int& x0, int& y0, int& bz) const {
+    const unsigned u = (unsigned)it;
+    const unsigned r = udiv(u, (unsigned)tiles_x, inv_tx);
+    x0 = (int)(u - r * (unsigned)tiles_x) * kTW;
+    const unsigned f = udiv(r, (unsigned)tiles_y, inv_ty);
+    y0 = (int)(r - f * (unsigned)tiles_y) * kG;
+    bz = (int)f;
+  }
+};
+
+// TMA tile origin: the halo origin with its innermost coordinate rounded
+// down to a 16-byte multiple (an unaligned innermost TMA coordinate raises
+// an illegal-instruction fault on this part -- measured with
+// tools/ubench/tma_probe.cu).  Negative aligned coordinates are fine; the
+// samples outside the image are masked by coordinate in pass V, which
+// reproduces the no-padding border rule kernels.py:166-176 (and arrive as
+// zeros, i.e. invalid depths, for the passable predicate).
+template <int R, int AE>
+__device__ __forceinline__ int tile_x0(int x0) {
+  return (x0 - R) & ~(AE - 1);
+}
+
+// pass V for unit (h, c) of one item.  Every thread of the 10 pass-V warps
+// calls it (the shuffles/ballots need full warps); `unit` is false for the
+// idle lanes beyond NC.
+template <int R, typename T>
+__device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int H, int W, int h,
+                                       int c, bool unit, int lane, double2* CR, uint32_t* fl,
+                                       uint32_t* pw, const FixedParams& p, bool want_bits) {
+  using Cfg = FastCfg<R, T>;
+  constexpr int NC = Cfg::NC, BW = Cfg::BW;
+  constexpr int NWIN = 2 * R + 1;
+  constexpr int HG = kG / 2;      // rows per pass-V unit
+  constexpr int NV = HG + 2 * R;  // input rows read per pass-V unit
+  constexpr int kBlocks = kHalfUnits / 32;
+  const int gx = x0 - R + c;
+  const int r0 = h * HG;  // first input row of the unit (item-relative, incl. halo)
+  const T* col = in + r0 * BW + c + sh;
+  T raw[NV];
+  bool all_small = true;  // every sample finite with |v| <= 2^40 (sliding sums exact)
+  if (unit) {
+    if constexpr (sizeof(T) == 4) {
+      uint32_t mx = 0;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        raw[i] = col[i * BW];
+        mx = max(mx, __float_as_uint(raw[i]) & 0x7fffffffu);
+      }
+      all_small = mx <= kBigBits;
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        raw[i] = col[i * BW];
+        all_small &= small_t(raw[i]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) raw[i] = (T)0;
+  }
+  if (unit) {
+    // rows of the unit inside the image
+    const int lo = max(0, R - y0 - r0), hi = min(NV, H - y0 + R - r0);
+    uint32_t inside = 0;
+    if ((unsigned)gx < (unsigned)W && hi > lo) inside = (uint32_t)(((1ull << (hi - lo)) - 1ull) << lo);
+    double v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = (double)raw[i];
+    constexpr uint32_t kAll = (NV >= 32) ? 0xffffffffu : ((1u << NV) - 1u);
+    uint32_t fin = kAll;
+    bool big = false;
+    if (!all_small) {
+      // rare: non-finite (zeroed so the sliding sums stay finite) or huge samples
+      fin = 0;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const bool f = finite_t(raw[i]);
+        fin |= (f ? 1u : 0u) << i;
+        if (!f) v[i] = 0.0;
+        big |= f && !small_t(raw[i]);
+      }
+    }
+    const uint32_t invb = ~(fin & inside);
+    double2* cr = CR + c * kCP + r0;
+    if (!big) {
+      double C = 0.0, Rr = 0.0;
+#pragma unroll
+      for (int j = 0; j < NWIN; ++j) {
+        C += v[j];
+        Rr = fma((double)(j - R), v[j], Rr);
+      }
+      cr[0] = make_double2(C, Rr);
+#pragma unroll
+      for (int g = 1; g < HG; ++g) {
+        const double vin = v[g + 2 * R], vout = v[g - 1];
+        const double tin = fma((double)R, vout, (double)(R + 1) * vin);  // off the chain
+        C += vin - vout;
+        Rr = (Rr - C) + tin;
+        cr[g] = make_double2(C, Rr);
+      }
+    } else {
+#pragma unroll
+      for (int g = 0; g < HG; ++g) {
+        double C = 0.0, Rr = 0.0;
+#pragma unroll
+        for (int j = 0; j < NWIN; ++j) {
+          C += v[g + j];
+          Rr = fma((double)(j - R), v[g + j], Rr);
+        }
+        cr[g] = make_double2(C, Rr);
+      }
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
+    // flags of column c, half h: bits 0-7 = support of output row 8h+i holds
+    // an invalid sample, bit 8 = the half's sums were computed directly
+    reinterpret_cast<uint16_t*>(fl + c)[h] = (uint16_t)((acc & 0xFFu) | (big ? 0x100u : 0u));
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (want_bits) {
+      // ST-passable bits of output rows 8h .. 8h+7 at output column c - R
+      // (adaptive.py:80-97,130-132).  Depths zf of the unit's rows
+      // R-1 .. R+8 (sn_common.cuh zfast, without its checks), left/right
+      // neighbours by shuffle (the warp-edge lanes load theirs).  The
+      // filter needs all five depths in [2^-100, 2^103] (positive normal
+      // floats whose sums stay normal, given fx*b and t in [2^-40, 2^40]);
+      // that also implies five valid disparities.  Anything else --
+      // invalid samples included -- is "undecided" and takes the exact
+      // path, which rejects invalid neighbourhoods before dividing.  The
+      // edge value is evaluated as (4c - u - d) - (l + r): four roundings
+      // of partial sums bounded by S, the same 2^-21 S bound as zpred.
+      constexpr int NZ = HG + 2;
+      float z[NZ];
+#pragma unroll
+      for (int k = 0; k < NZ; ++k) z[k] = __fmul_rn(p.fxb_pf, rcp_ftz((float)raw[R - 1 + k]));
+      float ze[HG];
+      const int ce = lane == 0 ? c - 1 : c + 1;
+      if ((lane == 0 || lane == 31) && ce >= 0 && ce < NC) {
+#pragma unroll
+        for (int k = 0; k < HG; ++k)
+          ze[k] = __fmul_rn(p.fxb_pf, rcp_ftz((float)in[(r0 + R + k) * BW + ce + sh]));
+      } else {
+#pragma unroll
+        for (int k = 0; k < HG; ++k) ze[k] = __int_as_float(0x7fc00000);
+      }
+      const float tm = __fmul_rn(p.t_f, 4.76837158203125e-07f /* 2^-21 */);
+      uint32_t pass = 0, sure = 0;  // bit k: decided passable / decided (either way)
+#pragma unroll
+      for (int k = 0; k < HG; ++k) {
+        float zl = __shfl_up_sync(0xffffffffu, z[k + 1], 1);
+        float zr = __shfl_down_sync(0xffffffffu, z[k + 1], 1);
+        if (lane == 0) zl = ze[k];
+        if (lane == 31) zr = ze[k];
+        const float c4 = __fmul_rn(4.0f, z[k + 1]);
+        const float vp = __fsub_rn(__fsub_rn(c4, z[k]), z[k + 2]);
+        const float sp = __fadd_rn(__fadd_rn(c4, z[k]), z[k + 2]);
+        const float hs = __fadd_rn(zl, zr);
+        const float S = __fadd_rn(sp, hs);
+        const float a = __fsub_rn(fabsf(__fsub_rn(vp, hs)), p.t_f);  // e - t
+        const float margin = __fmaf_rn(S, 9.5367431640625e-07f /* 2^-20 */, tm);
+        const float mn = fminf(fminf(fminf(z[k], z[k + 2]), fminf(zl, zr)), z[k + 1]);
+        const bool ok = (S <= 1.0141204801825835e31f /* 2^103 */) &&
+                        (mn >= 7.888609052210118e-31f /* 2^-100 */);
+        pass |= (ok && a < -margin ? 1u : 0u) << k;
+        sure |= (ok && (a < -margin || a > margin) ? 1u : 0u) << k;
+      }
+      const bool out_col = unit && c >= R && c < R + kTW;
+      uint32_t pb = p.pred_exact ? 0u : pass;
+      uint32_t undecided = p.pred_exact ? 0xFFu : (~sure & 0xFFu);
+      if (!out_col) pb = undecided = 0;
+      // rare exact decisions (fp64, reference op order), batched per unit
+      while (undecided) {
+        const int k = __ffs(undecided) - 1;
+        undecided &= undecided - 1u;
+        const T* ck = col + (R + k) * BW;
+        pb |= pred_exact_d((float)ck[0], (float)ck[-1], (float)ck[1], (float)ck[-BW],
+                           (float)ck[BW], p.fxb, p.t)
+              << k;
+      }
+      uint32_t bw[HG];
+#pragma unroll
+      for (int k = 0; k < HG; ++k) bw[k] = __ballot_sync(0xffffffffu, (pb >> k) & 1u);
+      if (lane == 0) {
+        uint4* dst = reinterpret_cast<uint4*>(pw + (h * kBlocks + (c >> 5)) * HG);
+        dst[0] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+        dst[1] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
+      }
+    }
+  }
+}
+
+// bit-mask word m of output row g of an item (k = g * 4 + m, k < 64): output
+// columns 32m .. 32m+31 = logical columns 32m+R .. 32m+R+31, split over the
+// ballots of column blocks m and m+1
+template <int R>
+__device__ __forceinline__ void bits_word(int k, const uint32_t* pw, int x0, int y0, int bz, int H,
+                                          const FixedParams& p) {
+  constexpr int HG = kG / 2;
+  constexpr int kBlocks = kHalfUnits / 32;
+  const int g = k >> 2, m = k & 3;
+  const int hh = g / HG, kr = g % HG;
+  const uint32_t lo = pw[(hh * kBlocks + m) * HG + kr];
+  const uint32_t hi = pw[(hh * kBlocks + m + 1) * HG + kr];
+  const int wc = x0 / 32 + m;
+  if (y0 + g < H && wc < p.bits_ww)
+    p.bits[((int64_t)bz * H + y0 + g) * p.bits_ww + wc] = __funnelshift_r(lo, hi, R);
+}
+
+// pass H + epilogue for lane hl (< 256) of one item
+template <int R, typename T>
+__device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int y0, int bz, int H,
+                                       int W, const double2* CR, const uint32_t* fl,
+                                       uint32_t stage_base, const FixedParams& p,
+                                       uint8_t* mask_out) {
+  using Cfg = FastCfg<R, T>;
+  constexpr int BW = Cfg::BW;
+  constexpr int NWIN = 2 * R + 1;
+  constexpr int NH = kRun + 2 * R;  // C/Rr columns read per pass-H lane
+  const int g = hl & 15;
+  const int q = hl >> 4;  // run of kRun output columns
+  const int colbase = q * kRun;
+  double cc[NH], rr[NH];
+  uint32_t any = 0;
+#pragma unroll
+  for (int i = 0; i < NH; ++i) {
+    const double2 v = CR[(colbase + i) * kCP + g];
+    cc[i] = v.x;
+    rr[i] = v.y;
+    any |= fl[colbase + i];
+  }
+  const uint32_t hshift = (uint32_t)(g & 8) * 2;  // 0 or 16: the half of row g
+  const bool big = ((any >> (hshift + 8)) & 1u) != 0u;
+  uint32_t win = 0;  // bit j: support of output j holds an invalid sample
+  if (((any >> hshift) & 0xFFu) != 0u) {
+    uint32_t colinv = 0;
+#pragma unroll
+    for (int i = 0; i < NH; ++i) colinv |= ((fl[colbase + i] >> (hshift + (g & 7))) & 1u) << i;
+#pragma unroll
+    for (int j = 0; j < NWIN; ++j) win |= colinv >> j;
+  }
+
+  const int yg = y0 + g;
+  const int xb = x0 + colbase;
+  const int yv = p.row0 + yg;  // image row (strips: block row + offset)
+  const double dv = (double)yv - p.v0;
+  const float dv_f = ((float)yv - p.v0_hi) - p.v0_lo;
+  const float du_hi = (float)xb - p.u0_hi;  // exact; + j stays exact
+  const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
+  const uint32_t gsw = (uint32_t)(g & 7);
+  const uint32_t rowaddr = stage_base + (uint32_t)g * 128u;
+  uint32_t validbits = 0;
+
+  // sliding sums first (short dependent chain), then independent epilogues
+  double Us[kRun], Vs[kRun];
+  if (!big) {
+    double Bx = 0.0, U = 0.0, V = 0.0;
+#pragma unroll
+    for (int j = 0; j < NWIN; ++j) {
+      Bx += cc[j];
+      U = fma((double)(j - R), cc[j], U);
+      V += rr[j];
+    }
+    Us[0] = U;
+    Vs[0] = V;
+#pragma unroll
+    for (int j = 1; j < kRun; ++j) {
+      const double cin = cc[j + 2 * R], cout = cc[j - 1];
+      const double tin = fma((double)R, cout, (double)(R + 1) * cin);  // independent of the chain
+      Bx += cin - cout;
+      U = (U - Bx) + tin;
+      V += rr[j + 2 * R] - rr[j - 1];
+      Us[j] = U;
+      Vs[j] = V;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) {
+      double U = 0.0, V = 0.0;
+#pragma unroll
+      for (int i = 0; i < NWIN; ++i) {
+        U = fma((double)(i - R), cc[j + i], U);
+        V += rr[j + i];
+      }
+      Us[j] = U;
+      Vs[j] = V;
+    }
+  }
+  float o[12];
+#pragma unroll
+  for (int j = 0; j < kRun; j += 2) {
+    const T d0 = drow[j], d1 = drow[j + 1];
+    const bool ok0 = (((win >> j) & 1u) == 0u) && (d0 > (T)0);
+    const bool ok1 = (((win >> (j + 1)) & 1u) == 0u) && (d1 > (T)0);
+    validbits |= ((ok0 ? 1u : 0u) | (ok1 ? 2u : 0u)) << j;
+    if constexpr (sizeof(T) == 4) {
+      records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], (float)d0, (float)d1, ok0, ok1,
+                   du_hi + (float)j, dv_f, p, o);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double dcv = (double)(e ? d1 : d0);
+        const double du = (double)(xb + j + e) - p.u0;
+        float* r = o + 6 * e;
+        point_from_disparity_f64(dcv, du, dv, p, r[0], r[1], r[2]);
+        if (e ? ok1 : ok0)
+          normal_from_moments(Us[j + e], Vs[j + e], p.alpha, dcv, du, dv, p.fx, p.fy, r[3], r[4],
+                              r[5]);
+        else
+          r[3] = r[4] = r[5] = __int_as_float(0x7fc00000);
+      }
+    }
+    // pixels (j, j+1) = 12 floats = 3 chunks of the 128B-swizzled staging row
+    const int K = q * (kRun * 6 / 4) + (j >> 1) * 3;  // chunk index in the 768-float row
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int kk = K + t;
+      const uint32_t box = (uint32_t)(kk >> 3);
+      const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
+      st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[4 * t], o[4 * t + 1],
+                   o[4 * t + 2], o[4 * t + 3]);
+    }
+  }
+  if (mask_out != nullptr && yg < H) {
+    uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
+#pragma unroll 1
+    for (int j = 0; j < kRun && xb + j < W; ++j) mrow[j] = (uint8_t)((validbits >> j) & 1u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// classic kernel: persistent, 2 CTAs/SM, the passes of one item separated by
+// CTA barriers; the next item's input is prefetched during the current item
 
 template <int R, typename T>
 __global__ void __launch_bounds__(kFastThreads, 2)
@@ -212,13 +583,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
                         uint8_t* __restrict__ mask_out, const int n_items, const int tiles_x,
                         const int tiles_y) {
   using Cfg = FastCfg<R, T>;
-  constexpr int NC = Cfg::NC, NR = Cfg::NR, BW = Cfg::BW, AE = Cfg::AE;
-  constexpr int NWIN = 2 * R + 1;
-  constexpr int HG = kG / 2;           // rows per pass-V unit
-  constexpr int NV = HG + 2 * R;       // input rows read per pass-V unit
-  constexpr int NH = kRun + 2 * R;     // C/Rr columns read per pass-H lane
-  constexpr int kLanesH = kTW / kRun * kG;  // 256
-  constexpr int kBlocks = kHalfUnits / 32;  // column blocks per half
+  constexpr int NC = Cfg::NC, AE = Cfg::AE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned base for the swizzled staging tile; offset arithmetic on the
   // __shared__ array keeps the shared address space (LDS/STS, not generic LD/ST)
@@ -234,36 +599,13 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 
   int item = blockIdx.x;
   if (item >= n_items) return;
-
-  // TMA tile origin: the halo origin with its innermost coordinate rounded
-  // down to a 16-byte multiple (an unaligned innermost TMA coordinate raises
-  // an illegal-instruction fault on this part -- measured with
-  // tools/ubench/tma_probe.cu).  Negative aligned coordinates are fine; the
-  // samples outside the image are masked by coordinate in pass V, which
-  // reproduces the no-padding border rule kernels.py:166-176 (and arrive as
-  // zeros, i.e. invalid depths, for the passable predicate).
-  auto tile_x = [](int x0) { return ((x0 - R) & ~(AE - 1)); };  // floor to AE (two's complement)
-  const double inv_tx = 1.0 / (double)tiles_x, inv_ty = 1.0 / (double)tiles_y;
-  auto udiv = [](unsigned u, unsigned d, double inv) {  // exact u / d for u < 2^31
-    unsigned q = (unsigned)((double)u * inv);
-    if (q * d > u) --q;
-    else if ((q + 1) * d <= u) ++q;
-    return q;
-  };
-  auto decode = [&](int it, int& x0, int& y0, int& bz) {
-    const unsigned u = (unsigned)it;
-    const unsigned r = udiv(u, (unsigned)tiles_x, inv_tx);
-    x0 = (int)(u - r * (unsigned)tiles_x) * kTW;
-    const unsigned f = udiv(r, (unsigned)tiles_y, inv_ty);
-    y0 = (int)(r - f * (unsigned)tiles_y) * kG;
-    bz = (int)f;
-  };
+  const ItemDecoder decode(tiles_x, tiles_y);
   auto load_tile = [&](int it, int buf) {
     int x0, y0, bz;
     decode(it, x0, y0, bz);
     T* dst = reinterpret_cast<T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
     mbar_arrive_expect_tx(bar + buf, (uint32_t)Cfg::IN_BYTES);
-    tma_load_3d(dst, &in_map, bar + buf, tile_x(x0), y0 - R, bz);
+    tma_load_3d(dst, &in_map, bar + buf, tile_x0<R, AE>(x0), y0 - R, bz);
   };
 
   if (tid == 0) {
@@ -272,8 +614,6 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
     fence_mbar_init();
-    fl[NC] = 0u;
-    fl[NC + 1] = 0u;
     load_tile(item, 0);
   }
   __syncthreads();
@@ -287,303 +627,22 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     if (tid == 0 && item + (int)gridDim.x < n_items) load_tile(item + gridDim.x, buf ^ 1);
     int x0, y0, bz;
     decode(item, x0, y0, bz);
-    const int sh = (x0 - R) - tile_x(x0);  // logical column c <-> smem column c + sh
+    const int sh = (x0 - R) - tile_x0<R, AE>(x0);  // logical column c <-> smem column c + sh
     const T* in = reinterpret_cast<const T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
     mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
-    // ------------------------------------------------------------ pass V
-    // unit = (column c, half h): rows 8h .. 8h+7 of the item
-    {
-      const int gx = x0 - R + c;
-      const int r0 = h * HG;  // first input row of the unit (item-relative, incl. halo)
-      const T* col = in + r0 * BW + c + sh;
-      T raw[NV];
-      bool all_small = true;  // every sample finite with |v| <= 2^40 (sliding sums exact)
-      if (unit) {
-        if constexpr (sizeof(T) == 4) {
-          uint32_t mx = 0;
-#pragma unroll
-          for (int i = 0; i < NV; ++i) {
-            raw[i] = col[i * BW];
-            mx = max(mx, __float_as_uint(raw[i]) & 0x7fffffffu);
-          }
-          all_small = mx <= kBigBits;
-        } else {
-#pragma unroll
-          for (int i = 0; i < NV; ++i) {
-            raw[i] = col[i * BW];
-            all_small &= small_t(raw[i]);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < NV; ++i) raw[i] = (T)0;
-      }
-      if (unit) {
-        // rows of the unit inside the image
-        const int lo = max(0, R - y0 - r0), hi = min(NV, H - y0 + R - r0);
-        uint32_t inside = 0;
-        if ((unsigned)gx < (unsigned)W && hi > lo)
-          inside = (uint32_t)(((1ull << (hi - lo)) - 1ull) << lo);
-        double v[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) v[i] = (double)raw[i];
-        constexpr uint32_t kAll = (NV >= 32) ? 0xffffffffu : ((1u << NV) - 1u);
-        uint32_t fin = kAll;
-        bool big = false;
-        if (!all_small) {
-          // rare: non-finite (zeroed so the sliding sums stay finite) or huge samples
-          fin = 0;
-#pragma unroll
-          for (int i = 0; i < NV; ++i) {
-            const bool f = finite_t(raw[i]);
-            fin |= (f ? 1u : 0u) << i;
-            if (!f) v[i] = 0.0;
-            big |= f && !small_t(raw[i]);
-          }
-        }
-        const uint32_t invb = ~(fin & inside);
-        double2* cr = CR + c * kCP + r0;
-        if (!big) {
-          double C = 0.0, Rr = 0.0;
-#pragma unroll
-          for (int j = 0; j < NWIN; ++j) {
-            C += v[j];
-            Rr = fma((double)(j - R), v[j], Rr);
-          }
-          cr[0] = make_double2(C, Rr);
-#pragma unroll
-          for (int g = 1; g < HG; ++g) {
-            const double vin = v[g + 2 * R], vout = v[g - 1];
-            const double tin = fma((double)R, vout, (double)(R + 1) * vin);  // off the chain
-            C += vin - vout;
-            Rr = (Rr - C) + tin;
-            cr[g] = make_double2(C, Rr);
-          }
-        } else {
-#pragma unroll
-          for (int g = 0; g < HG; ++g) {
-            double C = 0.0, Rr = 0.0;
-#pragma unroll
-            for (int j = 0; j < NWIN; ++j) {
-              C += v[g + j];
-              Rr = fma((double)(j - R), v[g + j], Rr);
-            }
-            cr[g] = make_double2(C, Rr);
-          }
-        }
-        uint32_t acc = 0;
-#pragma unroll
-        for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
-        // flag word of column c: half h's low byte holds its 8 output rows
-        reinterpret_cast<uint16_t*>(fl + c)[h] = (uint16_t)(acc & 0xFFu);
-        if (big) atomicOr(fl + NC + buf, 1u);  // per-parity "big value" flag of the item
-      }
-      if constexpr (sizeof(T) == 4) {
-        if (want_bits) {
-          // ST-passable bits of output rows 8h .. 8h+7 at output column c - R
-          // (adaptive.py:80-97,130-132).  Depths zf of the unit's rows
-          // R-1 .. R+8 (sn_common.cuh zfast, without its checks), left/right
-          // neighbours by shuffle (the warp-edge lanes load theirs).  The
-          // filter needs all five depths in [2^-100, 2^103] (positive normal
-          // floats whose sums stay normal, given fx*b and t in [2^-40, 2^40]);
-          // that also implies five valid disparities.  Anything else --
-          // invalid samples included -- is "undecided" and takes the exact
-          // path, which rejects invalid neighbourhoods before dividing.  The
-          // edge value is evaluated as (4c - u - d) - (l + r): four roundings
-          // of partial sums bounded by S, the same 2^-21 S bound as zpred.
-          constexpr int NZ = HG + 2;
-          float z[NZ];
-#pragma unroll
-          for (int k = 0; k < NZ; ++k) {
-            z[k] = __fmul_rn(p.fxb_pf, rcp_ftz((float)raw[R - 1 + k]));
-          }
-          float ze[HG];
-          const int ce = lane == 0 ? c - 1 : c + 1;
-          if ((lane == 0 || lane == 31) && ce >= 0 && ce < NC) {
-#pragma unroll
-            for (int k = 0; k < HG; ++k) {
-              ze[k] = __fmul_rn(p.fxb_pf, rcp_ftz((float)in[(r0 + R + k) * BW + ce + sh]));
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < HG; ++k) ze[k] = __int_as_float(0x7fc00000);
-          }
-          const float tm = __fmul_rn(p.t_f, 4.76837158203125e-07f /* 2^-21 */);
-          uint32_t pass = 0, sure = 0;  // bit k: decided passable / decided (either way)
-#pragma unroll
-          for (int k = 0; k < HG; ++k) {
-            float zl = __shfl_up_sync(0xffffffffu, z[k + 1], 1);
-            float zr = __shfl_down_sync(0xffffffffu, z[k + 1], 1);
-            if (lane == 0) zl = ze[k];
-            if (lane == 31) zr = ze[k];
-            const float c4 = __fmul_rn(4.0f, z[k + 1]);
-            const float vp = __fsub_rn(__fsub_rn(c4, z[k]), z[k + 2]);
-            const float sp = __fadd_rn(__fadd_rn(c4, z[k]), z[k + 2]);
-            const float hs = __fadd_rn(zl, zr);
-            const float S = __fadd_rn(sp, hs);
-            const float a = __fsub_rn(fabsf(__fsub_rn(vp, hs)), p.t_f);  // e - t
-            const float margin = __fmaf_rn(S, 9.5367431640625e-07f /* 2^-20 */, tm);
-            const float mn = fminf(fminf(fminf(z[k], z[k + 2]), fminf(zl, zr)), z[k + 1]);
-            const bool ok = (S <= 1.0141204801825835e31f /* 2^103 */) &&
-                            (mn >= 7.888609052210118e-31f /* 2^-100 */);
-            pass |= (ok && a < -margin ? 1u : 0u) << k;
-            sure |= (ok && (a < -margin || a > margin) ? 1u : 0u) << k;
-          }
-          const bool out_col = unit && c >= R && c < R + kTW;
-          uint32_t pb = p.pred_exact ? 0u : pass;
-          uint32_t undecided = p.pred_exact ? 0xFFu : (~sure & 0xFFu);
-          if (!out_col) pb = undecided = 0;
-          // rare exact decisions (fp64, reference op order), batched per unit
-          while (undecided) {
-            const int k = __ffs(undecided) - 1;
-            undecided &= undecided - 1u;
-            const T* ck = col + (R + k) * BW;
-            pb |= pred_exact_d((float)ck[0], (float)ck[-1], (float)ck[1], (float)ck[-BW],
-                               (float)ck[BW], p.fxb, p.t)
-                  << k;
-          }
-          uint32_t bw[HG];
-#pragma unroll
-          for (int k = 0; k < HG; ++k) bw[k] = __ballot_sync(0xffffffffu, (pb >> k) & 1u);
-          if (lane == 0) {
-            uint4* dst = reinterpret_cast<uint4*>(pw + (h * kBlocks + (c >> 5)) * HG);
-            dst[0] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
-            dst[1] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
-          }
-        }
-      }
-    }
+    pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, lane, CR, fl, pw, p, want_bits);
     // staging of the previous item consumed by its TMA stores (issued by warp 8)
     if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait_read0();
     __syncthreads();
 
-    // ------------------------------------------------------------ pass H + epilogue
-    if (tid < kLanesH) {
-      const int g = tid & 15;
-      const int q = tid >> 4;  // run of kRun output columns
-      const int colbase = q * kRun;
-      double cc[NH], rr[NH];
-      uint32_t any = 0;
-#pragma unroll
-      for (int i = 0; i < NH; ++i) {
-        const double2 v = CR[(colbase + i) * kCP + g];
-        cc[i] = v.x;
-        rr[i] = v.y;
-        any |= fl[colbase + i];
-      }
-      const bool big = fl[NC + buf] != 0u;
-      uint32_t win = 0;  // bit j: support of output j holds an invalid sample
-      if (any != 0u) {
-        uint32_t colinv = 0;
-#pragma unroll
-        for (int i = 0; i < NH; ++i) colinv |= ((fl[colbase + i] >> (g + (g & 8))) & 1u) << i;
-#pragma unroll
-        for (int j = 0; j < NWIN; ++j) win |= colinv >> j;
-      }
-
-      const int yg = y0 + g;
-      const int xb = x0 + colbase;
-      const int yv = p.row0 + yg;  // image row (strips: block row + offset)
-      const double dv = (double)yv - p.v0;
-      const float dv_f = ((float)yv - p.v0_hi) - p.v0_lo;
-      const float du_hi = (float)xb - p.u0_hi;  // exact; + j stays exact
-      const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
-      const uint32_t gsw = (uint32_t)(g & 7);
-      const uint32_t rowaddr = stage_base + (uint32_t)g * 128u;
-      uint32_t validbits = 0;
-
-      // sliding sums first (short dependent chain), then 8 independent epilogues
-      double Us[kRun], Vs[kRun];
-      if (!big) {
-        double Bx = 0.0, U = 0.0, V = 0.0;
-#pragma unroll
-        for (int j = 0; j < NWIN; ++j) {
-          Bx += cc[j];
-          U = fma((double)(j - R), cc[j], U);
-          V += rr[j];
-        }
-        Us[0] = U;
-        Vs[0] = V;
-#pragma unroll
-        for (int j = 1; j < kRun; ++j) {
-          const double cin = cc[j + 2 * R], cout = cc[j - 1];
-          const double tin = fma((double)R, cout, (double)(R + 1) * cin);  // independent of the chain
-          Bx += cin - cout;
-          U = (U - Bx) + tin;
-          V += rr[j + 2 * R] - rr[j - 1];
-          Us[j] = U;
-          Vs[j] = V;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < kRun; ++j) {
-          double U = 0.0, V = 0.0;
-#pragma unroll
-          for (int i = 0; i < NWIN; ++i) {
-            U = fma((double)(i - R), cc[j + i], U);
-            V += rr[j + i];
-          }
-          Us[j] = U;
-          Vs[j] = V;
-        }
-      }
-      float o[12];
-#pragma unroll
-      for (int j = 0; j < kRun; j += 2) {
-        const T d0 = drow[j], d1 = drow[j + 1];
-        const bool ok0 = (((win >> j) & 1u) == 0u) && (d0 > (T)0);
-        const bool ok1 = (((win >> (j + 1)) & 1u) == 0u) && (d1 > (T)0);
-        validbits |= ((ok0 ? 1u : 0u) | (ok1 ? 2u : 0u)) << j;
-        if constexpr (sizeof(T) == 4) {
-          records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], (float)d0, (float)d1, ok0, ok1,
-                       du_hi + (float)j, dv_f, p, o);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const double dcv = (double)(e ? d1 : d0);
-            const double du = (double)(xb + j + e) - p.u0;
-            float* r = o + 6 * e;
-            point_from_disparity_f64(dcv, du, dv, p, r[0], r[1], r[2]);
-            if (e ? ok1 : ok0)
-              normal_from_moments(Us[j + e], Vs[j + e], p.alpha, dcv, du, dv, p.fx, p.fy, r[3],
-                                  r[4], r[5]);
-            else
-              r[3] = r[4] = r[5] = __int_as_float(0x7fc00000);
-          }
-        }
-        // pixels (j, j+1) = 12 floats = 3 chunks of the 128B-swizzled staging row
-        const int K = q * (kRun * 6 / 4) + (j >> 1) * 3;  // chunk index in the 768-float row
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          const int kk = K + t;
-          const uint32_t box = (uint32_t)(kk >> 3);
-          const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
-          st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[4 * t], o[4 * t + 1],
-                       o[4 * t + 2], o[4 * t + 3]);
-        }
-      }
-      if (mask_out != nullptr && yg < H) {
-        uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
-#pragma unroll 1
-        for (int j = 0; j < kRun && xb + j < W; ++j) mrow[j] = (uint8_t)((validbits >> j) & 1u);
-      }
-    } else if (want_bits && tid < kLanesH + kG * (kTW / 32)) {
-      // warps 8-9: bit-mask words of the item.  Word m of output row g covers
-      // output columns 32m .. 32m+31 = logical columns 32m+R .. 32m+R+31,
-      // split over the ballots of column blocks m and m+1.
-      const int k = tid - kLanesH;
-      const int g = k >> 2, m = k & 3;
-      const int hh = g / HG, kr = g % HG;
-      const uint32_t lo = pw[(hh * kBlocks + m) * HG + kr];
-      const uint32_t hi = pw[(hh * kBlocks + m + 1) * HG + kr];
-      const int wc = x0 / 32 + m;
-      if (y0 + g < H && wc < p.bits_ww)
-        p.bits[((int64_t)bz * H + y0 + g) * p.bits_ww + wc] = __funnelshift_r(lo, hi, R);
+    if (tid < 256) {
+      pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
+    } else if (want_bits && tid < 256 + kG * (kTW / 32)) {
+      bits_word<R>(tid - 256, pw, x0, y0, bz, H, p);  // warps 8-9 meanwhile
     }
     fence_proxy_async_smem();
     __syncthreads();
-    if (tid == 0) fl[NC + buf] = 0u;  // reset this parity's big flag (next used two items later)
     // one TMA store per 128-B box column, one lane each, from a warp that is
     // idle in pass H -- warp 0 goes straight on to the next item
     if (tid >= kStoreTid && tid < kStoreTid + kBoxes) {
@@ -593,6 +652,131 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     }
   }
   if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------
+// warp-specialised pipeline: 1 CTA/SM, 19 warps
+//   warps 0-9    pass V of item i (writes CR/flags/ballots slot i % 2)
+//   warps 10-17  pass H of item i-1 (reads them, writes staging slot (i-1) % 2)
+//   warp 18      TMA: input loads two items ahead, output stores of item i-2
+// mbarriers (use n of a slot has parity n & 1; a producer's first wait on an
+// "empty" barrier passes at once):
+//   in_full[3]  tx-count of the input load      in_empty[3]  256 pass-H threads
+//   cr_full[2]  320 pass-V threads              cr_empty[2]  256 pass-H threads
+//   st_full[2]  256 pass-H threads              st_empty[2]  1 (warp 18 after read-out)
+
+constexpr int kPipeV = 10 * 32, kPipeH = 8 * 32, kPipeThreads = kPipeV + kPipeH + 32;
+
+template <int R>
+__global__ void __launch_bounds__(kPipeThreads, 1)
+    fixed_square_pipe_kernel(const __grid_constant__ CUtensorMap in_map,
+                             const __grid_constant__ CUtensorMap out_map, const FixedParams p,
+                             uint8_t* __restrict__ mask_out, const int n_items, const int tiles_x,
+                             const int tiles_y) {
+  using Cfg = FastCfg<R, float>;
+  using PC = PipeCfg<R>;
+  constexpr int NC = Cfg::NC, AE = Cfg::AE;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + PC::BAR);
+  uint64_t* in_full = bar;
+  uint64_t* in_empty = bar + PC::kIn;
+  uint64_t* cr_full = bar + 2 * PC::kIn;
+  uint64_t* cr_empty = cr_full + PC::kCr;
+  uint64_t* st_full = cr_empty + PC::kCr;
+  uint64_t* st_empty = st_full + PC::kSt;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int W = (int)p.W, H = (int)p.H;
+  const bool want_bits = p.bits != nullptr;
+  const ItemDecoder decode(tiles_x, tiles_y);
+  auto in_tile = [&](int s) { return reinterpret_cast<float*>(smem + PC::IN + s * PC::IN_STRIDE); };
+  auto cr_slot = [&](int s) { return reinterpret_cast<double2*>(smem + PC::CS + s * PC::CS_STRIDE); };
+  auto fl_slot = [&](int s) { return reinterpret_cast<uint32_t*>(smem + PC::FL + s * Cfg::FL_BYTES); };
+  auto pw_slot = [&](int s) { return reinterpret_cast<uint32_t*>(smem + PC::PW + s * Cfg::PW_BYTES); };
+  auto st_slot = [&](int s) { return smem + PC::STAGE + s * Cfg::STAGE_BYTES; };
+
+  if (tid == 0) {
+    tma_prefetch_desc(&in_map);
+    tma_prefetch_desc(&out_map);
+    for (int i = 0; i < PC::kIn; ++i) {
+      mbar_init(in_full + i, 1);
+      mbar_init(in_empty + i, kPipeH);
+    }
+    for (int i = 0; i < PC::kCr; ++i) {
+      mbar_init(cr_full + i, kPipeV);
+      mbar_init(cr_empty + i, kPipeH);
+    }
+    for (int i = 0; i < PC::kSt; ++i) {
+      mbar_init(st_full + i, kPipeH);
+      mbar_init(st_empty + i, 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // this CTA's items: blockIdx.x + n * gridDim.x, n = 0 .. n_mine - 1
+  const int n_mine = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto item_of = [&](int n) { return (int)blockIdx.x + n * (int)gridDim.x; };
+
+  if (tid < kPipeV) {
+    // ---------------------------------------------------------- pass V
+    const int h = tid >= kHalfUnits ? 1 : 0;
+    const int c = tid - h * kHalfUnits;
+    const bool unit = c < NC;
+    for (int n = 0; n < n_mine; ++n) {
+      int x0, y0, bz;
+      decode(item_of(n), x0, y0, bz);
+      const int si = n % PC::kIn, ci = n % PC::kCr;
+      mbar_wait(in_full + si, (uint32_t)(n / PC::kIn) & 1u);
+      mbar_wait(cr_empty + ci, ((uint32_t)(n / PC::kCr) & 1u) ^ 1u);
+      pass_v<R, float>(in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, H, W, h, c, unit, lane,
+                       cr_slot(ci), fl_slot(ci), pw_slot(ci), p, want_bits);
+      mbar_arrive(cr_full + ci);
+    }
+  } else if (tid < kPipeV + kPipeH) {
+    // ---------------------------------------------------------- pass H
+    const int hl = tid - kPipeV;
+    for (int n = 0; n < n_mine; ++n) {
+      int x0, y0, bz;
+      decode(item_of(n), x0, y0, bz);
+      const int si = n % PC::kIn, ci = n % PC::kCr, ss = n % PC::kSt;
+      mbar_wait(cr_full + ci, (uint32_t)(n / PC::kCr) & 1u);
+      if (want_bits && hl < kG * (kTW / 32)) bits_word<R>(hl, pw_slot(ci), x0, y0, bz, H, p);
+      mbar_wait(st_empty + ss, ((uint32_t)(n / PC::kSt) & 1u) ^ 1u);
+      pass_h<R, float>(hl, in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, bz, H, W,
+                       cr_slot(ci), fl_slot(ci), smem_u32(st_slot(ss)), p, mask_out);
+      fence_proxy_async_smem();
+      mbar_arrive(st_full + ss);
+      mbar_arrive(cr_empty + ci);
+      mbar_arrive(in_empty + si);
+    }
+  } else {
+    // ---------------------------------------------------------- TMA warp
+    auto load = [&](int n) {
+      int x0, y0, bz;
+      decode(item_of(n), x0, y0, bz);
+      const int si = n % PC::kIn;
+      mbar_wait(in_empty + si, ((uint32_t)(n / PC::kIn) & 1u) ^ 1u);
+      mbar_arrive_expect_tx(in_full + si, (uint32_t)Cfg::IN_BYTES);
+      tma_load_3d(in_tile(si), &in_map, in_full + si, tile_x0<R, AE>(x0), y0 - R, bz);
+    };
+    if (lane == 0)
+      for (int n = 0; n < PC::kIn - 1 && n < n_mine; ++n) load(n);
+    for (int n = 0; n < n_mine; ++n) {
+      if (lane == 0 && n + PC::kIn - 1 < n_mine) load(n + PC::kIn - 1);
+      int x0, y0, bz;
+      decode(item_of(n), x0, y0, bz);
+      const int ss = n % PC::kSt;
+      mbar_wait(st_full + ss, (uint32_t)(n / PC::kSt) & 1u);
+      if (lane < kBoxes) {
+        tma_store_3d(&out_map, st_slot(ss) + (size_t)lane * kG * 128, x0 * 6 + lane * kBoxF, y0, bz);
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(st_empty + ss);
+    }
+    if (lane < kBoxes) bulk_wait0();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -696,6 +880,30 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
                      es, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != 0)
       return SN_ECUDA;
   }
+  const int tiles_x = (int)((p.W + kTW - 1) / kTW);
+  const int tiles_y = (int)((p.H + kG - 1) / kG);
+  const int64_t n_items64 = (int64_t)tiles_x * tiles_y * p.B;
+  if (n_items64 >= 0x7fffffffLL) return -1;  // generic path handles absurd batches
+  const int n_items = (int)n_items64;
+  if constexpr (sizeof(T) == 4 && R <= 4) {
+    // warp-specialised pipeline (SN_FUSED_CLASSIC=1 selects the classic kernel)
+    static const bool classic = getenv("SN_FUSED_CLASSIC") != nullptr;
+    if (!classic && PipeCfg<R>::fits) {
+      auto kern = fixed_square_pipe_kernel<R>;
+      static bool attr_set = false;
+      if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)PipeCfg<R>::TOTAL) != cudaSuccess)
+          return set_cuda_error("cudaFuncSetAttribute(fixed_square_pipe_kernel)");
+        attr_set = true;
+      }
+      int64_t grid = ctx.num_sms;
+      if (grid > n_items) grid = n_items;
+      kern<<<(unsigned)grid, kPipeThreads, PipeCfg<R>::TOTAL, ctx.stream>>>(
+          in_map, out_map, p, mask, n_items, tiles_x, tiles_y);
+      return check_launch("fixed_square_pipe_kernel");
+    }
+  }
   auto kern = fixed_square_kernel<R, T>;
   static bool attr_set = false;  // per template instance
   if (!attr_set) {
@@ -704,11 +912,6 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
       return set_cuda_error("cudaFuncSetAttribute(fixed_square_kernel)");
     attr_set = true;
   }
-  const int tiles_x = (int)((p.W + kTW - 1) / kTW);
-  const int tiles_y = (int)((p.H + kG - 1) / kG);
-  const int64_t n_items64 = (int64_t)tiles_x * tiles_y * p.B;
-  if (n_items64 >= 0x7fffffffLL) return -1;  // generic path handles absurd batches
-  const int n_items = (int)n_items64;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFastThreads, Cfg::TOTAL) !=
       cudaSuccess)
