@@ -166,10 +166,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)  // suspend up to 1 ms per try: waiting warps stop issuing
       : "memory");
 }
 
