@@ -160,12 +160,12 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 // into inf).  Normal: normal_square's formula for both pixels; a pixel whose
 // |n|^2 leaves fp32's comfortable range takes the fp64 path.
 __device__ __forceinline__ void records_pair(double U0, double V0, double U1, double V1, float d0,
-                                             float d1, bool ok0, bool ok1, float duh, float dv,
-                                             const FixedParams& p, float* o) {
-  // points; duh = (x - u0_hi) exactly, du = duh - u0_lo (two-float u0)
+                                             float d1, float2 zz, bool ok0, bool ok1, float duh,
+                                             float dv, const FixedParams& p, float* o) {
+  // points; zz = fxb_f * rcp(d) as computed by the caller (shared with the
+  // passable predicate); duh = (x - u0_hi) exactly, du = duh - u0_lo
   const float2 dd = make_float2(d0, d1);
   const float2 du = make_float2(duh - p.u0_lo, (duh + 1.0f) - p.u0_lo);
-  float2 zz = __fmul2_rn(make_float2(p.fxb_f, p.fxb_f), make_float2(rcp_ftz(d0), rcp_ftz(d1)));
   const bool pv0 = (d0 > 0.0f) && (d0 <= 3.402823466e38f);
   const bool pv1 = (d1 > 0.0f) && (d1 <= 3.402823466e38f);
   if (pv0 && d0 < 1.175494351e-38f) zz.x = (float)(p.fxb / (double)d0);
@@ -269,10 +269,13 @@ __device__ __forceinline__ int tile_x0(int x0) {
 // idle lanes beyond NC.
 template <int R, typename T>
 __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int H, int W, int h,
-                                       int c, bool unit, int lane, double2* CR, uint32_t* fl,
-                                       uint32_t* pw, const FixedParams& p, bool want_bits) {
+                                       int c, bool unit, double2* CR, uint32_t* fl) {
   using Cfg = FastCfg<R, T>;
-  constexpr int NC = Cfg::NC, BW = Cfg::BW;
+  constexpr int BW = Cfg::BW;
+  // all operands live in shared memory: let the compiler emit LDS/STS
+  __builtin_assume(__isShared(in));
+  __builtin_assume(__isShared(CR));
+  __builtin_assume(__isShared(fl));
   constexpr int NWIN = 2 * R + 1;
   constexpr int HG = kG / 2;      // rows per pass-V unit
   constexpr int NV = HG + 2 * R;  // input rows read per pass-V unit
@@ -361,94 +364,93 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
     // an invalid sample, bit 8 = the half's sums were computed directly
     reinterpret_cast<uint16_t*>(fl + c)[h] = (uint16_t)((acc & 0xFFu) | (big ? 0x100u : 0u));
   }
-  if constexpr (sizeof(T) == 4) {
-    if (want_bits) {
-      // ST-passable bits of output rows 8h .. 8h+7 at output column c - R
-      // (adaptive.py:80-97,130-132).  Depths zf of the unit's rows
-      // R-1 .. R+8 (sn_common.cuh zfast, without its checks), left/right
-      // neighbours by shuffle (the warp-edge lanes load theirs).  The
-      // filter needs all five depths in [2^-100, 2^103] (positive normal
-      // floats whose sums stay normal, given fx*b and t in [2^-40, 2^40]);
-      // that also implies five valid disparities.  Anything else --
-      // invalid samples included -- is "undecided" and takes the exact
-      // path, which rejects invalid neighbourhoods before dividing.  The
-      // edge value is evaluated as (4c - u - d) - (l + r): four roundings
-      // of partial sums bounded by S, the same 2^-21 S bound as zpred.
-      constexpr int NZ = HG + 2;
-      float z[NZ];
-#pragma unroll
-      for (int k = 0; k < NZ; ++k) z[k] = __fmul_rn(p.fxb_pf, rcp_ftz((float)raw[R - 1 + k]));
-      float ze[HG];
-      const int ce = lane == 0 ? c - 1 : c + 1;
-      if ((lane == 0 || lane == 31) && ce >= 0 && ce < NC) {
-#pragma unroll
-        for (int k = 0; k < HG; ++k)
-          ze[k] = __fmul_rn(p.fxb_pf, rcp_ftz((float)in[(r0 + R + k) * BW + ce + sh]));
-      } else {
-#pragma unroll
-        for (int k = 0; k < HG; ++k) ze[k] = __int_as_float(0x7fc00000);
-      }
-      const float tm = __fmul_rn(p.t_f, 4.76837158203125e-07f /* 2^-21 */);
-      uint32_t pass = 0, sure = 0;  // bit k: decided passable / decided (either way)
-#pragma unroll
-      for (int k = 0; k < HG; ++k) {
-        float zl = __shfl_up_sync(0xffffffffu, z[k + 1], 1);
-        float zr = __shfl_down_sync(0xffffffffu, z[k + 1], 1);
-        if (lane == 0) zl = ze[k];
-        if (lane == 31) zr = ze[k];
-        const float c4 = __fmul_rn(4.0f, z[k + 1]);
-        const float vp = __fsub_rn(__fsub_rn(c4, z[k]), z[k + 2]);
-        const float sp = __fadd_rn(__fadd_rn(c4, z[k]), z[k + 2]);
-        const float hs = __fadd_rn(zl, zr);
-        const float S = __fadd_rn(sp, hs);
-        const float a = __fsub_rn(fabsf(__fsub_rn(vp, hs)), p.t_f);  // e - t
-        const float margin = __fmaf_rn(S, 9.5367431640625e-07f /* 2^-20 */, tm);
-        const float mn = fminf(fminf(fminf(z[k], z[k + 2]), fminf(zl, zr)), z[k + 1]);
-        const bool ok = (S <= 1.0141204801825835e31f /* 2^103 */) &&
-                        (mn >= 7.888609052210118e-31f /* 2^-100 */);
-        pass |= (ok && a < -margin ? 1u : 0u) << k;
-        sure |= (ok && (a < -margin || a > margin) ? 1u : 0u) << k;
-      }
-      const bool out_col = unit && c >= R && c < R + kTW;
-      uint32_t pb = p.pred_exact ? 0u : pass;
-      uint32_t undecided = p.pred_exact ? 0xFFu : (~sure & 0xFFu);
-      if (!out_col) pb = undecided = 0;
-      // rare exact decisions (fp64, reference op order), batched per unit
-      while (undecided) {
-        const int k = __ffs(undecided) - 1;
-        undecided &= undecided - 1u;
-        const T* ck = col + (R + k) * BW;
-        pb |= pred_exact_d((float)ck[0], (float)ck[-1], (float)ck[1], (float)ck[-BW],
-                           (float)ck[BW], p.fxb, p.t)
-              << k;
-      }
-      uint32_t bw[HG];
-#pragma unroll
-      for (int k = 0; k < HG; ++k) bw[k] = __ballot_sync(0xffffffffu, (pb >> k) & 1u);
-      if (lane == 0) {
-        uint4* dst = reinterpret_cast<uint4*>(pw + (h * kBlocks + (c >> 5)) * HG);
-        dst[0] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
-        dst[1] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
-      }
-    }
-  }
 }
 
-// bit-mask word m of output row g of an item (k = g * 4 + m, k < 64): output
-// columns 32m .. 32m+31 = logical columns 32m+R .. 32m+R+31, split over the
-// ballots of column blocks m and m+1
-template <int R>
-__device__ __forceinline__ void bits_word(int k, const uint32_t* pw, int x0, int y0, int bz, int H,
+// bit-mask word m of output row g of an item (k = g * 4 + m, k < 64): the
+// four pass-H lanes of row g wrote its bytes (pb[g][q], q = 4m .. 4m+3)
+__device__ __forceinline__ void bits_word(int k, const uint32_t* pb, int x0, int y0, int bz, int H,
                                           const FixedParams& p) {
-  constexpr int HG = kG / 2;
-  constexpr int kBlocks = kHalfUnits / 32;
+  __builtin_assume(__isShared(pb));
   const int g = k >> 2, m = k & 3;
-  const int hh = g / HG, kr = g % HG;
-  const uint32_t lo = pw[(hh * kBlocks + m) * HG + kr];
-  const uint32_t hi = pw[(hh * kBlocks + m + 1) * HG + kr];
   const int wc = x0 / 32 + m;
-  if (y0 + g < H && wc < p.bits_ww)
-    p.bits[((int64_t)bz * H + y0 + g) * p.bits_ww + wc] = __funnelshift_r(lo, hi, R);
+  if (y0 + g < H && wc < p.bits_ww) p.bits[((int64_t)bz * H + y0 + g) * p.bits_ww + wc] = pb[k];
+}
+
+// ST-passable bits (adaptive.py:80-97,130-132) of the 8 pixels of a pass-H
+// run: zc = depths of the run's columns -1 .. 8 in its row (row g), the rows
+// above/below by shuffle from lanes g-1 / g+1 (rows -1 and 16 of the item
+// are loaded by the lanes of rows 0 and 15).  Filter (sn_common.cuh zfast
+// bound): all five depths in [2^-100, 2^100] (positive normal floats whose
+// sums stay normal, given fx*b and t in [2^-40, 2^40] -- that also implies
+// five valid disparities) and |e32 - t| > 2^-20 S + 2^-21 t, with the edge
+// value evaluated as (4c - u - d) - (l + r) (four roundings of partial sums
+// bounded by S: the 2^-21 S bound).  Anything else -- invalid samples
+// included -- takes the exact fp64 path (reference op order), which rejects
+// invalid neighbourhoods before dividing.  Packed f32x2 over pixel pairs.
+template <int R>
+__device__ __forceinline__ uint32_t passable_run(int hl, const float* drow, const float* zc,
+                                                 const FixedParams& p) {
+  constexpr int BW = FastCfg<R, float>::BW;
+  __builtin_assume(__isShared(drow));
+  const int g = hl & 15;
+  float zu[kRun], zd[kRun];
+#pragma unroll
+  for (int j = 0; j < kRun; ++j) {
+    zu[j] = __shfl_up_sync(0xffffffffu, zc[j + 1], 1);
+    zd[j] = __shfl_down_sync(0xffffffffu, zc[j + 1], 1);
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) zu[j] = __fmul_rn(p.fxb_f, rcp_ftz(drow[j - BW]));
+  } else if (g == 15) {
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) zd[j] = __fmul_rn(p.fxb_f, rcp_ftz(drow[j + BW]));
+  }
+  // range of the run's own depths (columns -1 .. 8) and its rows above/below
+  float mn = zc[0], mx = zc[0];
+#pragma unroll
+  for (int j = 1; j < kRun + 2; ++j) {
+    mn = fminf(mn, zc[j]);
+    mx = fmaxf(mx, zc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < kRun; ++j) {
+    mn = fminf(mn, fminf(zu[j], zd[j]));
+    mx = fmaxf(mx, fmaxf(zu[j], zd[j]));
+  }
+  const bool ok = !p.pred_exact && mn >= 7.888609052210118e-31f /* 2^-100 */ &&
+                  mx <= 1.2676506002282294e30f /* 2^100 */;
+  const float2 tm2 = make_float2(__fmul_rn(p.t_f, 4.76837158203125e-07f /* 2^-21 */),
+                                 __fmul_rn(p.t_f, 4.76837158203125e-07f));
+  const float2 k20 = make_float2(9.5367431640625e-07f, 9.5367431640625e-07f);  // 2^-20
+  const float2 four = make_float2(4.0f, 4.0f);
+  uint32_t pass = 0, sure = 0;
+#pragma unroll
+  for (int j = 0; j < kRun; j += 2) {
+    const float2 cc = make_float2(zc[j + 1], zc[j + 2]);
+    const float2 up = make_float2(zu[j], zu[j + 1]), dn = make_float2(zd[j], zd[j + 1]);
+    const float2 c4 = __fmul2_rn(four, cc);
+    const float2 vp = __fadd2_rn(__fadd2_rn(c4, make_float2(-up.x, -up.y)),
+                                 make_float2(-dn.x, -dn.y));
+    const float2 sp = __fadd2_rn(__fadd2_rn(c4, up), dn);
+    const float2 hs = __fadd2_rn(make_float2(zc[j], zc[j + 1]), make_float2(zc[j + 2], zc[j + 3]));
+    const float2 S = __fadd2_rn(sp, hs);
+    const float2 e = __fadd2_rn(vp, make_float2(-hs.x, -hs.y));
+    const float a0 = __fsub_rn(fabsf(e.x), p.t_f), a1 = __fsub_rn(fabsf(e.y), p.t_f);  // e - t
+    const float2 m = __ffma2_rn(S, k20, tm2);
+    pass |= ((a0 < -m.x ? 1u : 0u) | (a1 < -m.y ? 2u : 0u)) << j;
+    sure |= (((a0 < -m.x || a0 > m.x) ? 1u : 0u) | ((a1 < -m.y || a1 > m.y) ? 2u : 0u)) << j;
+  }
+  uint32_t pb = ok ? pass : 0u;
+  uint32_t undecided = ok ? (~sure & 0xFFu) : 0xFFu;
+  // rare exact decisions (fp64, reference op order), batched per lane
+  while (undecided) {
+    const int j = __ffs(undecided) - 1;
+    undecided &= undecided - 1u;
+    pb |= pred_exact_d(drow[j], drow[j - 1], drow[j + 1], drow[j - BW], drow[j + BW], p.fxb, p.t)
+          << j;
+  }
+  return pb;
 }
 
 // pass H + epilogue for lane hl (< 256) of one item
@@ -456,8 +458,12 @@ template <int R, typename T>
 __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int y0, int bz, int H,
                                        int W, const double2* CR, const uint32_t* fl,
                                        uint32_t stage_base, const FixedParams& p,
-                                       uint8_t* mask_out) {
+                                       uint8_t* mask_out, uint8_t* pbytes) {
   using Cfg = FastCfg<R, T>;
+  __builtin_assume(__isShared(in));
+  __builtin_assume(__isShared(CR));
+  __builtin_assume(__isShared(fl));
+  __builtin_assume(pbytes == nullptr || __isShared(pbytes));
   constexpr int BW = Cfg::BW;
   constexpr int NWIN = 2 * R + 1;
   constexpr int NH = kRun + 2 * R;  // C/Rr columns read per pass-H lane
@@ -530,6 +536,18 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
       Vs[j] = V;
     }
   }
+  // depths zf = fxb * rcp(d) of the run's columns -1 .. 8 (shared by the
+  // points and the passable predicate)
+  float zc[kRun + 2];
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int j = 0; j < kRun + 2; ++j)
+      zc[j] = (pbytes != nullptr || (j >= 1 && j <= kRun))
+                  ? __fmul_rn(p.fxb_f, rcp_ftz((float)drow[j - 1]))
+                  : 0.0f;
+    if (pbytes != nullptr)
+      pbytes[g * (kTW / 8) + q] = (uint8_t)passable_run<R>(hl, drow, zc, p);
+  }
   float o[12];
 #pragma unroll
   for (int j = 0; j < kRun; j += 2) {
@@ -538,8 +556,8 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
     const bool ok1 = (((win >> (j + 1)) & 1u) == 0u) && (d1 > (T)0);
     validbits |= ((ok0 ? 1u : 0u) | (ok1 ? 2u : 0u)) << j;
     if constexpr (sizeof(T) == 4) {
-      records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], (float)d0, (float)d1, ok0, ok1,
-                   du_hi + (float)j, dv_f, p, o);
+      records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], (float)d0, (float)d1,
+                   make_float2(zc[j + 1], zc[j + 2]), ok0, ok1, du_hi + (float)j, dv_f, p, o);
     } else {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -631,18 +649,18 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     const T* in = reinterpret_cast<const T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
     mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
-    pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, lane, CR, fl, pw, p, want_bits);
+    pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl);
     // staging of the previous item consumed by its TMA stores (issued by warp 8)
     if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait_read0();
     __syncthreads();
 
-    if (tid < 256) {
-      pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
-    } else if (want_bits && tid < 256 + kG * (kTW / 32)) {
-      bits_word<R>(tid - 256, pw, x0, y0, bz, H, p);  // warps 8-9 meanwhile
-    }
+    if (tid < 256)
+      pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out,
+                   want_bits ? reinterpret_cast<uint8_t*>(pw) : nullptr);
     fence_proxy_async_smem();
     __syncthreads();
+    // warps 8-9: the item's bit-mask words (pass-H bytes), before the next pass H
+    if (want_bits && tid >= 256 && tid < 256 + kG * (kTW / 32)) bits_word(tid - 256, pw, x0, y0, bz, H, p);
     // one TMA store per 128-B box column, one lane each, from a warp that is
     // idle in pass H -- warp 0 goes straight on to the next item
     if (tid >= kStoreTid && tid < kStoreTid + kBoxes) {
@@ -728,8 +746,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       const int si = n % PC::kIn, ci = n % PC::kCr;
       mbar_wait(in_full + si, (uint32_t)(n / PC::kIn) & 1u);
       mbar_wait(cr_empty + ci, ((uint32_t)(n / PC::kCr) & 1u) ^ 1u);
-      pass_v<R, float>(in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, H, W, h, c, unit, lane,
-                       cr_slot(ci), fl_slot(ci), pw_slot(ci), p, want_bits);
+      pass_v<R, float>(in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, H, W, h, c, unit,
+                       cr_slot(ci), fl_slot(ci));
       mbar_arrive(cr_full + ci);
     }
   } else if (tid < kPipeV + kPipeH) {
@@ -740,10 +758,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       decode(item_of(n), x0, y0, bz);
       const int si = n % PC::kIn, ci = n % PC::kCr, ss = n % PC::kSt;
       mbar_wait(cr_full + ci, (uint32_t)(n / PC::kCr) & 1u);
-      if (want_bits && hl < kG * (kTW / 32)) bits_word<R>(hl, pw_slot(ci), x0, y0, bz, H, p);
       mbar_wait(st_empty + ss, ((uint32_t)(n / PC::kSt) & 1u) ^ 1u);
       pass_h<R, float>(hl, in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, bz, H, W,
-                       cr_slot(ci), fl_slot(ci), smem_u32(st_slot(ss)), p, mask_out);
+                       cr_slot(ci), fl_slot(ci), smem_u32(st_slot(ss)), p, mask_out,
+                       want_bits ? reinterpret_cast<uint8_t*>(pw_slot(ss)) : nullptr);
       fence_proxy_async_smem();
       mbar_arrive(st_full + ss);
       mbar_arrive(cr_empty + ci);
@@ -767,6 +785,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       decode(item_of(n), x0, y0, bz);
       const int ss = n % PC::kSt;
       mbar_wait(st_full + ss, (uint32_t)(n / PC::kSt) & 1u);
+      if (want_bits) {
+        bits_word(lane, pw_slot(ss), x0, y0, bz, H, p);
+        bits_word(lane + 32, pw_slot(ss), x0, y0, bz, H, p);
+      }
       if (lane < kBoxes) {
         tma_store_3d(&out_map, st_slot(ss) + (size_t)lane * kG * 128, x0 * 6 + lane * kBoxF, y0, bz);
         bulk_commit();
