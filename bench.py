@@ -6,8 +6,8 @@ Workload (default, N=1 and per rank for N>1): configuration C3 -- synthetic
 rank owns its own 256-frame shard, no data-path collective).  One step =
 the full north-star pipeline over the batch: fused fixed-kernel pass
 (k = 9 LSQ fit + closed-form normal + triangulation -> dense [B,H,W,6] fp32
-oriented points) followed by the 8-connected ST-passable component labels
-(t = 0.2).  Inputs are resident in HBM; they are 2.1 GB in / 12.9 GB out per
+oriented points), the ST-passable bit mask (t = 0.2) and the 8-connected
+component labels from it.  Inputs are resident in HBM; they are 2.1 GB in / 12.9 GB out per
 step, far larger than the 126 MB L2, so no explicit flush is needed.
 
 Reported: value = whole-job Mpx/s (all ranks) from CUDA events on the launch
@@ -41,7 +41,6 @@ sys.path.insert(0, str(ROOT))
 METRIC = "megapixels/sec (oriented points) at 2048×1024, 1/2/4/8 B200; % HBM roofline"
 H, W, FRAMES, KSIZE, T_ST = 1024, 2048, 256, 9, 0.2
 BYTES_PER_PX = 28  # algorithmic: 4 B fp32 disparity in + 24 B (x,y,z,nx,ny,nz) out
-BITS_PER_PX = 1 / 8  # + the passable bit mask the fused pass emits
 
 
 def parse():
@@ -232,20 +231,21 @@ def main():
     bits = torch.empty((B, H, device.bit_words(W)), dtype=torch.int32, device=dev)
 
     def step(ev=None):
-        # = device.pipeline(...), split in its two launches so the fused
-        # kernel's own time can be bracketed by events
+        # = device.pipeline(...): fused pass, passable bits, labels -- split so
+        # each kernel's own time is bracketed by events on the launch stream
         if ev is not None:
             ev[0].record(stream)
-        if args.pipeline == "full":
-            device.oriented_points_bits(disp, rig, KSIZE, T_ST, out=out, bits=bits)
-        else:
-            device.oriented_points(disp, rig, KSIZE, out=out)
+        device.oriented_points(disp, rig, KSIZE, out=out)
         if ev is not None:
             ev[1].record(stream)
         if args.pipeline == "full":
-            device.labels_from_bits(bits, W, out=labels, workspace=ccl_ws)
+            device.passable_bits(disp, rig, T_ST, bits=bits)
         if ev is not None:
             ev[2].record(stream)
+        if args.pipeline == "full":
+            device.labels_from_bits(bits, W, out=labels, workspace=ccl_ws)
+        if ev is not None:
+            ev[3].record(stream)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -257,7 +257,7 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.2)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -275,12 +275,13 @@ def main():
 
     total_ms = t_start.elapsed_time(t_end)
     fused_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    ccl_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    stats = torch.tensor([total_ms, statistics.mean(fused_ms), statistics.mean(ccl_ms)],
-                         dtype=torch.float64, device=dev)
+    bits_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    ccl_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    stats = torch.tensor([total_ms, statistics.mean(fused_ms), statistics.mean(bits_ms),
+                          statistics.mean(ccl_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    total_ms, fused_avg, ccl_avg = stats.tolist()
+    total_ms, fused_avg, bits_avg, ccl_avg = stats.tolist()
     ms_per_step = total_ms / args.steps
     px_step = B * H * W
     value = world * px_step / 1e6 / (ms_per_step / 1e3)
@@ -291,7 +292,7 @@ def main():
     if pk.exists():
         peaks = json.loads(pk.read_text())
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    fused_bytes = BYTES_PER_PX + (BITS_PER_PX if args.pipeline == 'full' else 0.0)
+    fused_bytes = BYTES_PER_PX
     achieved = fused_bytes * px_step / (fused_avg / 1e3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
@@ -354,7 +355,8 @@ def main():
                        "parallelism": f"frame-batch dp{world}",
                        "l2": "inputs+outputs (15 GB/step) >> 126 MB L2, no flush needed"},
             "frames_per_sec_per_gpu": B / (ms_per_step / 1e3),
-            "stages_ms_per_frame": {"fused_pass": fused_avg / B, "ccl": ccl_avg / B},
+            "stages_ms_per_frame": {"fused_pass": fused_avg / B, "passable_bits": bits_avg / B,
+                                    "ccl": ccl_avg / B},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "fixed_square_kernel<4,float>",
@@ -362,7 +364,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback"},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": args.steps * (1 + (3 if args.pipeline == "full" else 0)),
+            "gpu_launches": args.steps * (1 + (4 if args.pipeline == "full" else 0)),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

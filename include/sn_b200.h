@@ -99,14 +99,20 @@ SN_API int sn_oriented_points_rows(sn_plan_t* plan, const float* disp, int64_t B
                             const int32_t* offsets_xy, int32_t n_off, float* out6,
                             uint8_t* mask, void* stream);
 
-/* Same pass + the ST-passable bit mask in the same read of the disparity
- * (adaptive.py:80-97,130-132; threshold t > 0): bits is [B][H][ceil(W/32)]
+/* Same pass + the ST-passable bit mask (adaptive.py:80-97,130-132;
+ * threshold t > 0; the fused pass and sn_passable_bits back to back on the
+ * stream): bits is [B][H][ceil(W/32)]
  * uint32, bit (u % 32) of word u / 32 set iff pixel u of the row is passable.
  * row0 as for sn_oriented_points_rows. */
 SN_API int sn_oriented_points_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
                             int64_t W, int64_t row0, const sn_rig_t* rig,
                             const int32_t* offsets_xy, int32_t n_off, double t, float* out6,
                             uint8_t* mask, uint32_t* bits, void* stream);
+
+/* The ST-passable bit mask alone (layout of sn_oriented_points_bits), as one
+ * streaming kernel over the disparity. */
+SN_API int sn_passable_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                     const sn_rig_t* rig, double t, uint32_t* bits, void* stream);
 
 /* The whole north-star pipeline in one call: fused fit + normal + point +
  * passable bits, then component labels from the bits (label semantics as

@@ -61,6 +61,7 @@ SIGNATURES = {
     "sn_oriented_points_rows": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
     "sn_oriented_points_bits": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P,
                                 _P],
+    "sn_passable_bits": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P],
     "sn_pipeline": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P],
     "sn_pipeline_ws": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P,
                        ctypes.c_size_t, _P],

@@ -358,6 +358,25 @@ int sn_oriented_points_bits(sn_plan_t* plan, const float* disp, int64_t B, int64
                                      stream, 0, row0, bits, t);
 }
 
+int sn_passable_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                     const sn_rig_t* rig, double t, uint32_t* bits, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
+  if (B * H * W == 0) return SN_OK;
+  if (!disp || !bits) return set_error(SN_EINVAL, "NULL buffer");
+  FixedParams p{};
+  p.B = B;
+  p.H = H;
+  p.W = W;
+  fill_rig(p, rig);
+  fill_predicate(p, p.fxb, t, bits);
+  DeviceGuard g(plan->device);
+  return run_passable_bits(make_ctx(plan, stream), disp, p, bits);
+}
+
 /* test hook: force the generic (non-TMA) kernel, to cross-check the fast path */
 int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                                const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,

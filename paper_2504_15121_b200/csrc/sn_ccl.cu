@@ -648,34 +648,132 @@ int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, ui
   return check_launch("passable_kernel");
 }
 
-// standalone passable bit mask (fallback for the fused emission): one warp
-// per 32-pixel word, the same fp32 filter + fp64 fallback as the fused pass
-__global__ void passable_bits_kernel(const float* __restrict__ disp, const FixedParams p,
-                                     uint32_t* __restrict__ bits) {
-  const int W = (int)p.W, H = (int)p.H;
+// ST-passable bit mask (adaptive.py:80-97,130-132) as a streaming kernel.
+// A warp owns 32 aligned columns x kPbRows rows of a frame, lane <-> column:
+// depths zf = fxb * rcp(d) of rows -1 .. kPbRows in registers, left/right
+// neighbours by shuffle (the warp's edge columns come from two more strided
+// loads), one ballot per row = one bit-mask word.  The fp32 filter is the
+// z-form of sn_common.cuh (margin 2^-20 S + 2^-21 t, all five depths in
+// [2^-100, 2^100]); undecided pixels -- ties, out-of-range or invalid
+// samples -- take the exact fp64 path with the reference's op order.  Reads
+// 4 B/px (+ halo through L2), writes 1/8 B/px; full occupancy, no shared
+// memory.
+constexpr int kPbRows = 16;
+
+__global__ void __launch_bounds__(256)
+    passable_bits_kernel(const float* __restrict__ disp, const FixedParams p,
+                         uint32_t* __restrict__ bits) {
+  const int W = (int)p.W, H = (int)p.H, WW = p.bits_ww;
   const int lane = threadIdx.x & 31;
-  const int64_t n_words = p.B * p.H * p.bits_ww;
-  for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < n_words;
-       wi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t row = wi / p.bits_ww;
-    const int x = (int)(wi - row * p.bits_ww) * 32 + lane;
-    const int y = (int)(row % p.H);
-    const float* f = disp + (row - y) * p.W;
-    uint32_t pk = 0;
-    if (x >= 1 && x + 1 < W && y >= 1 && y + 1 < H) {
-      const float* c = f + (int64_t)y * W + x;
-      pk = pred_bit(c[0], c[-1], c[1], c[-W], c[W], p);
+  const unsigned strips_y = (unsigned)((H + kPbRows - 1) / kPbRows);
+  const unsigned n_tasks = (unsigned)p.B * strips_y * (unsigned)WW;  // < 2^31 (host-checked)
+  const float nanf_ = __int_as_float(0x7fc00000);
+  const float tm = __fmul_rn(p.t_f, 4.76837158203125e-07f /* 2^-21 */);
+  for (unsigned task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < n_tasks;
+       task += (gridDim.x * blockDim.x) >> 5) {
+    const unsigned rest = task / (unsigned)WW;
+    const int wc = (int)(task - rest * (unsigned)WW);
+    const unsigned f = rest / strips_y;
+    const int y0 = (int)(rest - f * strips_y) * kPbRows;
+    const int x = wc * 32 + lane;
+    const float* fr = disp + (int64_t)f * p.H * p.W;
+    // depths of this column, rows y0-1 .. y0+kPbRows (NaN outside the frame)
+    float z[kPbRows + 2];
+    if (y0 >= 1 && y0 + kPbRows < H && wc * 32 + 32 <= W) {
+      const float* src = fr + (y0 - 1) * W + x;  // frame offsets fit int32 (host-checked)
+#pragma unroll
+      for (int k = 0; k < kPbRows + 2; ++k) z[k] = __fmul_rn(p.fxb_f, rcp_ftz(__ldg(src + k * W)));
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPbRows + 2; ++k) {
+        const int y = y0 - 1 + k;
+        const float d = (x < W && y >= 0 && y < H) ? __ldg(fr + y * W + x) : nanf_;
+        z[k] = __fmul_rn(p.fxb_f, rcp_ftz(d));
+      }
     }
-    const uint32_t b = __ballot_sync(0xffffffffu, pk != 0u);
-    if (lane == 0) bits[wi] = b;
+    // the warp's edge columns: lane k < kPbRows holds row y0+k of column
+    // wc*32-1 (el) and of column wc*32+32 (er)
+    float el = nanf_, er = nanf_;
+    {
+      const int y = y0 + lane;
+      if (lane < kPbRows && y < H) {
+        const int xl = wc * 32 - 1, xr = wc * 32 + 32;
+        if (xl >= 0) el = __fmul_rn(p.fxb_f, rcp_ftz(__ldg(fr + y * W + xl)));
+        if (xr < W) er = __fmul_rn(p.fxb_f, rcp_ftz(__ldg(fr + y * W + xr)));
+      }
+    }
+    uint32_t pb = 0, ub = 0;  // bit k: row y0 + k passable / undecided by the filter
+    const float2 tm2 = make_float2(tm, tm);
+    const float2 k20 = make_float2(9.5367431640625e-07f, 9.5367431640625e-07f);  // 2^-20
+    const float2 four = make_float2(4.0f, 4.0f);
+    // rows in pairs, packed f32x2 (FADD2/FMUL2/FFMA2)
+#pragma unroll
+    for (int k = 0; k < kPbRows; k += 2) {
+      float2 L, R;
+      L.x = __shfl_up_sync(0xffffffffu, z[k + 1], 1);
+      L.y = __shfl_up_sync(0xffffffffu, z[k + 2], 1);
+      R.x = __shfl_down_sync(0xffffffffu, z[k + 1], 1);
+      R.y = __shfl_down_sync(0xffffffffu, z[k + 2], 1);
+      const float el0 = __shfl_sync(0xffffffffu, el, k), el1 = __shfl_sync(0xffffffffu, el, k + 1);
+      const float er0 = __shfl_sync(0xffffffffu, er, k), er1 = __shfl_sync(0xffffffffu, er, k + 1);
+      if (lane == 0) L = make_float2(el0, el1);
+      if (lane == 31) R = make_float2(er0, er1);
+      const float2 C = make_float2(z[k + 1], z[k + 2]);
+      const float2 U = make_float2(z[k], z[k + 1]), D = make_float2(z[k + 2], z[k + 3]);
+      const float2 c4 = __fmul2_rn(four, C);
+      const float2 vp = __fadd2_rn(__fadd2_rn(c4, make_float2(-U.x, -U.y)), make_float2(-D.x, -D.y));
+      const float2 sp = __fadd2_rn(__fadd2_rn(c4, U), D);
+      const float2 hs = __fadd2_rn(L, R);
+      const float2 S = __fadd2_rn(sp, hs);
+      const float2 e = __fadd2_rn(vp, make_float2(-hs.x, -hs.y));
+      const float2 m = __ffma2_rn(S, k20, tm2);
+      const float a0 = __fsub_rn(fabsf(e.x), p.t_f), a1 = __fsub_rn(fabsf(e.y), p.t_f);  // e - t
+      const float mn0 = fminf(fminf(fminf(U.x, D.x), fminf(L.x, R.x)), C.x);
+      const float mn1 = fminf(fminf(fminf(U.y, D.y), fminf(L.y, R.y)), C.y);
+      const bool ok0 = (S.x <= 1.0141204801825835e31f) && (mn0 >= 7.888609052210118e-31f);
+      const bool ok1 = (S.y <= 1.0141204801825835e31f) && (mn1 >= 7.888609052210118e-31f);
+      pb |= ((ok0 && a0 < -m.x ? 1u : 0u) | (ok1 && a1 < -m.y ? 2u : 0u)) << k;
+      ub |= ((ok0 && (a0 < -m.x || a0 > m.x) ? 0u : 1u) | (ok1 && (a1 < -m.y || a1 > m.y) ? 0u : 2u))
+            << k;
+    }
+    // interior pixels only (the reference has no padding)
+    uint32_t rows_in = (kPbRows == 32) ? 0xffffffffu : ((1u << kPbRows) - 1u);
+    if (y0 == 0) rows_in &= ~1u;
+    if (H - 1 - y0 < kPbRows) rows_in &= (H - 1 - y0 > 0) ? ((1u << (H - 1 - y0)) - 1u) : 0u;
+    if (!(x >= 1 && x + 1 < W)) rows_in = 0;
+    if (p.pred_exact) {
+      pb = 0;
+      ub = rows_in;
+    }
+    pb &= rows_in;
+    ub &= rows_in;
+    // rare exact decisions (fp64, reference op order), after the row loop so
+    // a warp diverges at most once per task
+    while (ub) {
+      const int k = __ffs(ub) - 1;
+      ub &= ub - 1u;
+      const float* c = fr + (y0 + k) * W + x;
+      pb |= pred_exact_d(c[0], c[-1], c[1], c[-W], c[W], p.fxb, p.t) << k;
+    }
+    uint32_t mine = 0;  // lane k < kPbRows: the bit-mask word of row y0 + k
+#pragma unroll
+    for (int k = 0; k < kPbRows; ++k) {
+      const uint32_t b = __ballot_sync(0xffffffffu, (pb >> k) & 1u);
+      if (lane == k) mine = b;
+    }
+    if (lane < kPbRows && y0 + lane < H) bits[((int64_t)f * p.H + y0 + lane) * WW + wc] = mine;
   }
 }
 
 int run_passable_bits(const LaunchCtx& ctx, const float* disp, const FixedParams& p,
                       uint32_t* bits) {
-  const int64_t n = p.B * p.H * p.bits_ww * 32;
+  const int64_t n = p.B * ((p.H + kPbRows - 1) / kPbRows) * p.bits_ww * 32;
   if (n == 0) return SN_OK;
-  passable_bits_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(disp, p, bits);
+  if (p.H * p.W > 0x7fffffffLL || n / 32 > 0x7fffffffLL)
+    return set_error(SN_EINVAL, "frame or batch too large for the passable-bit kernel");
+  int64_t g = (n + 255) / 256;
+  if (g > (int64_t)ctx.num_sms * 64) g = (int64_t)ctx.num_sms * 64;
+  passable_bits_kernel<<<(unsigned)g, 256, 0, ctx.stream>>>(disp, p, bits);
   return check_launch("passable_bits_kernel");
 }
 

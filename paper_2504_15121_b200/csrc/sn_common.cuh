@@ -35,6 +35,17 @@ struct FixedParams {
   float t_f, fxb_pf;  // fp32 threshold / fx*b for the predicate filter
 };
 
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // ST-passable predicate (adaptive.py:80-97,130-132) from raw disparities
 //

@@ -65,23 +65,20 @@ struct FastCfg {
   static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
   static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;  // double2 (C, Rr) [NC][kCP]
   static constexpr size_t FL_BYTES = align_up((size_t)NC * 4, 16);
-  // passable ballots [half][column block of 32][row of the half]
-  static constexpr size_t PW_BYTES = 2 * (kHalfUnits / 32) * (kG / 2) * 4;
   // single-CTA-pipeline layout (classic kernel: 1 stage, 2 inputs, 1 CR)
   static constexpr size_t STAGE = 0;
   static constexpr size_t IN0 = STAGE + STAGE_BYTES;
   static constexpr size_t IN1 = align_up(IN0 + IN_BYTES, 128);
   static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);
   static constexpr size_t FL = align_up(CS + CS_BYTES, 16);
-  static constexpr size_t PW = align_up(FL + FL_BYTES, 16);
-  static constexpr size_t BAR = PW + PW_BYTES;
+  static constexpr size_t BAR = align_up(FL + FL_BYTES, 16);
   static constexpr size_t TOTAL = BAR + 16 + 1024;  // + slack for 1024-B alignment
   static_assert(NC <= kHalfUnits, "pass V: one unit per thread");
   static_assert(NR <= 32, "row validity bits must fit 32 bits");
 };
 
 // warp-specialised pipeline layout: 2 staging tiles, 3 input tiles, 2 x (CR,
-// flags, ballots), 10 mbarriers
+// flags), 14 mbarriers
 template <int R>
 struct PipeCfg {
   using C = FastCfg<R, float>;
@@ -92,8 +89,7 @@ struct PipeCfg {
   static constexpr size_t CS = IN + kIn * IN_STRIDE;
   static constexpr size_t CS_STRIDE = align_up(C::CS_BYTES, 128);
   static constexpr size_t FL = CS + kCr * CS_STRIDE;
-  static constexpr size_t PW = FL + kCr * C::FL_BYTES;
-  static constexpr size_t BAR = align_up(PW + kCr * C::PW_BYTES, 16);
+  static constexpr size_t BAR = align_up(FL + kCr * C::FL_BYTES, 16);
   static constexpr int kBars = kIn * 2 + kCr * 2 + kSt * 2;
   static constexpr size_t TOTAL = BAR + kBars * 8 + 1024;
   static constexpr bool fits = TOTAL <= 227 * 1024;
@@ -140,17 +136,6 @@ __device__ __forceinline__ void normal_square(double U, double V, float alpha_f,
   } else {
     normal_from_moments(U, V, p.alpha, (double)d, (double)du, (double)dv, p.fx, p.fy, nx, ny, nz);
   }
-}
-
-__device__ __forceinline__ float rcp_ftz(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ float rsqrt_ftz(float x) {
-  float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
 }
 
 // Oriented-point records of two neighbouring pixels (same row) with packed
@@ -366,104 +351,16 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   }
 }
 
-// bit-mask word m of output row g of an item (k = g * 4 + m, k < 64): the
-// four pass-H lanes of row g wrote its bytes (pb[g][q], q = 4m .. 4m+3)
-__device__ __forceinline__ void bits_word(int k, const uint32_t* pb, int x0, int y0, int bz, int H,
-                                          const FixedParams& p) {
-  __builtin_assume(__isShared(pb));
-  const int g = k >> 2, m = k & 3;
-  const int wc = x0 / 32 + m;
-  if (y0 + g < H && wc < p.bits_ww) p.bits[((int64_t)bz * H + y0 + g) * p.bits_ww + wc] = pb[k];
-}
-
-// ST-passable bits (adaptive.py:80-97,130-132) of the 8 pixels of a pass-H
-// run: zc = depths of the run's columns -1 .. 8 in its row (row g), the rows
-// above/below by shuffle from lanes g-1 / g+1 (rows -1 and 16 of the item
-// are loaded by the lanes of rows 0 and 15).  Filter (sn_common.cuh zfast
-// bound): all five depths in [2^-100, 2^100] (positive normal floats whose
-// sums stay normal, given fx*b and t in [2^-40, 2^40] -- that also implies
-// five valid disparities) and |e32 - t| > 2^-20 S + 2^-21 t, with the edge
-// value evaluated as (4c - u - d) - (l + r) (four roundings of partial sums
-// bounded by S: the 2^-21 S bound).  Anything else -- invalid samples
-// included -- takes the exact fp64 path (reference op order), which rejects
-// invalid neighbourhoods before dividing.  Packed f32x2 over pixel pairs.
-template <int R>
-__device__ __forceinline__ uint32_t passable_run(int hl, const float* drow, const float* zc,
-                                                 const FixedParams& p) {
-  constexpr int BW = FastCfg<R, float>::BW;
-  __builtin_assume(__isShared(drow));
-  const int g = hl & 15;
-  float zu[kRun], zd[kRun];
-#pragma unroll
-  for (int j = 0; j < kRun; ++j) {
-    zu[j] = __shfl_up_sync(0xffffffffu, zc[j + 1], 1);
-    zd[j] = __shfl_down_sync(0xffffffffu, zc[j + 1], 1);
-  }
-  if (g == 0) {
-#pragma unroll
-    for (int j = 0; j < kRun; ++j) zu[j] = __fmul_rn(p.fxb_f, rcp_ftz(drow[j - BW]));
-  } else if (g == 15) {
-#pragma unroll
-    for (int j = 0; j < kRun; ++j) zd[j] = __fmul_rn(p.fxb_f, rcp_ftz(drow[j + BW]));
-  }
-  // range of the run's own depths (columns -1 .. 8) and its rows above/below
-  float mn = zc[0], mx = zc[0];
-#pragma unroll
-  for (int j = 1; j < kRun + 2; ++j) {
-    mn = fminf(mn, zc[j]);
-    mx = fmaxf(mx, zc[j]);
-  }
-#pragma unroll
-  for (int j = 0; j < kRun; ++j) {
-    mn = fminf(mn, fminf(zu[j], zd[j]));
-    mx = fmaxf(mx, fmaxf(zu[j], zd[j]));
-  }
-  const bool ok = !p.pred_exact && mn >= 7.888609052210118e-31f /* 2^-100 */ &&
-                  mx <= 1.2676506002282294e30f /* 2^100 */;
-  const float2 tm2 = make_float2(__fmul_rn(p.t_f, 4.76837158203125e-07f /* 2^-21 */),
-                                 __fmul_rn(p.t_f, 4.76837158203125e-07f));
-  const float2 k20 = make_float2(9.5367431640625e-07f, 9.5367431640625e-07f);  // 2^-20
-  const float2 four = make_float2(4.0f, 4.0f);
-  uint32_t pass = 0, sure = 0;
-#pragma unroll
-  for (int j = 0; j < kRun; j += 2) {
-    const float2 cc = make_float2(zc[j + 1], zc[j + 2]);
-    const float2 up = make_float2(zu[j], zu[j + 1]), dn = make_float2(zd[j], zd[j + 1]);
-    const float2 c4 = __fmul2_rn(four, cc);
-    const float2 vp = __fadd2_rn(__fadd2_rn(c4, make_float2(-up.x, -up.y)),
-                                 make_float2(-dn.x, -dn.y));
-    const float2 sp = __fadd2_rn(__fadd2_rn(c4, up), dn);
-    const float2 hs = __fadd2_rn(make_float2(zc[j], zc[j + 1]), make_float2(zc[j + 2], zc[j + 3]));
-    const float2 S = __fadd2_rn(sp, hs);
-    const float2 e = __fadd2_rn(vp, make_float2(-hs.x, -hs.y));
-    const float a0 = __fsub_rn(fabsf(e.x), p.t_f), a1 = __fsub_rn(fabsf(e.y), p.t_f);  // e - t
-    const float2 m = __ffma2_rn(S, k20, tm2);
-    pass |= ((a0 < -m.x ? 1u : 0u) | (a1 < -m.y ? 2u : 0u)) << j;
-    sure |= (((a0 < -m.x || a0 > m.x) ? 1u : 0u) | ((a1 < -m.y || a1 > m.y) ? 2u : 0u)) << j;
-  }
-  uint32_t pb = ok ? pass : 0u;
-  uint32_t undecided = ok ? (~sure & 0xFFu) : 0xFFu;
-  // rare exact decisions (fp64, reference op order), batched per lane
-  while (undecided) {
-    const int j = __ffs(undecided) - 1;
-    undecided &= undecided - 1u;
-    pb |= pred_exact_d(drow[j], drow[j - 1], drow[j + 1], drow[j - BW], drow[j + BW], p.fxb, p.t)
-          << j;
-  }
-  return pb;
-}
-
 // pass H + epilogue for lane hl (< 256) of one item
 template <int R, typename T>
 __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int y0, int bz, int H,
                                        int W, const double2* CR, const uint32_t* fl,
                                        uint32_t stage_base, const FixedParams& p,
-                                       uint8_t* mask_out, uint8_t* pbytes) {
+                                       uint8_t* mask_out) {
   using Cfg = FastCfg<R, T>;
   __builtin_assume(__isShared(in));
   __builtin_assume(__isShared(CR));
   __builtin_assume(__isShared(fl));
-  __builtin_assume(pbytes == nullptr || __isShared(pbytes));
   constexpr int BW = Cfg::BW;
   constexpr int NWIN = 2 * R + 1;
   constexpr int NH = kRun + 2 * R;  // C/Rr columns read per pass-H lane
@@ -536,17 +433,11 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
       Vs[j] = V;
     }
   }
-  // depths zf = fxb * rcp(d) of the run's columns -1 .. 8 (shared by the
-  // points and the passable predicate)
+  // depths zf = fxb * rcp(d) of the run's pixels (zc[1 .. kRun])
   float zc[kRun + 2];
   if constexpr (sizeof(T) == 4) {
 #pragma unroll
-    for (int j = 0; j < kRun + 2; ++j)
-      zc[j] = (pbytes != nullptr || (j >= 1 && j <= kRun))
-                  ? __fmul_rn(p.fxb_f, rcp_ftz((float)drow[j - 1]))
-                  : 0.0f;
-    if (pbytes != nullptr)
-      pbytes[g * (kTW / 8) + q] = (uint8_t)passable_run<R>(hl, drow, zc, p);
+    for (int j = 1; j <= kRun; ++j) zc[j] = __fmul_rn(p.fxb_f, rcp_ftz((float)drow[j - 1]));
   }
   float o[12];
 #pragma unroll
@@ -608,12 +499,10 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double2* CR = reinterpret_cast<double2*>(smem + Cfg::CS);
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
-  uint32_t* pw = reinterpret_cast<uint32_t*>(smem + Cfg::PW);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
   const uint32_t stage_base = smem_u32(smem + Cfg::STAGE);
   const int tid = threadIdx.x, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
-  const bool want_bits = (sizeof(T) == 4) && p.bits != nullptr;
 
   int item = blockIdx.x;
   if (item >= n_items) return;
@@ -654,13 +543,9 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait_read0();
     __syncthreads();
 
-    if (tid < 256)
-      pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out,
-                   want_bits ? reinterpret_cast<uint8_t*>(pw) : nullptr);
+    if (tid < 256) pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
     fence_proxy_async_smem();
     __syncthreads();
-    // warps 8-9: the item's bit-mask words (pass-H bytes), before the next pass H
-    if (want_bits && tid >= 256 && tid < 256 + kG * (kTW / 32)) bits_word(tid - 256, pw, x0, y0, bz, H, p);
     // one TMA store per 128-B box column, one lane each, from a warp that is
     // idle in pass H -- warp 0 goes straight on to the next item
     if (tid >= kStoreTid && tid < kStoreTid + kBoxes) {
@@ -705,12 +590,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
   uint64_t* st_empty = st_full + PC::kSt;
   const int tid = threadIdx.x, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
-  const bool want_bits = p.bits != nullptr;
   const ItemDecoder decode(tiles_x, tiles_y);
   auto in_tile = [&](int s) { return reinterpret_cast<float*>(smem + PC::IN + s * PC::IN_STRIDE); };
   auto cr_slot = [&](int s) { return reinterpret_cast<double2*>(smem + PC::CS + s * PC::CS_STRIDE); };
   auto fl_slot = [&](int s) { return reinterpret_cast<uint32_t*>(smem + PC::FL + s * Cfg::FL_BYTES); };
-  auto pw_slot = [&](int s) { return reinterpret_cast<uint32_t*>(smem + PC::PW + s * Cfg::PW_BYTES); };
   auto st_slot = [&](int s) { return smem + PC::STAGE + s * Cfg::STAGE_BYTES; };
 
   if (tid == 0) {
@@ -760,8 +643,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       mbar_wait(cr_full + ci, (uint32_t)(n / PC::kCr) & 1u);
       mbar_wait(st_empty + ss, ((uint32_t)(n / PC::kSt) & 1u) ^ 1u);
       pass_h<R, float>(hl, in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, bz, H, W,
-                       cr_slot(ci), fl_slot(ci), smem_u32(st_slot(ss)), p, mask_out,
-                       want_bits ? reinterpret_cast<uint8_t*>(pw_slot(ss)) : nullptr);
+                       cr_slot(ci), fl_slot(ci), smem_u32(st_slot(ss)), p, mask_out);
       fence_proxy_async_smem();
       mbar_arrive(st_full + ss);
       mbar_arrive(cr_empty + ci);
@@ -785,10 +667,6 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       decode(item_of(n), x0, y0, bz);
       const int ss = n % PC::kSt;
       mbar_wait(st_full + ss, (uint32_t)(n / PC::kSt) & 1u);
-      if (want_bits) {
-        bits_word(lane, pw_slot(ss), x0, y0, bz, H, p);
-        bits_word(lane + 32, pw_slot(ss), x0, y0, bz, H, p);
-      }
       if (lane < kBoxes) {
         tma_store_3d(&out_map, st_slot(ss) + (size_t)lane * kG * 128, x0 * 6 + lane * kBoxF, y0, bz);
         bulk_commit();
@@ -908,9 +786,11 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
   if (n_items64 >= 0x7fffffffLL) return -1;  // generic path handles absurd batches
   const int n_items = (int)n_items64;
   if constexpr (sizeof(T) == 4 && R <= 4) {
-    // warp-specialised pipeline (SN_FUSED_CLASSIC=1 selects the classic kernel)
-    static const bool classic = getenv("SN_FUSED_CLASSIC") != nullptr;
-    if (!classic && PipeCfg<R>::fits) {
+    // warp-specialised pipeline, opt-in (SN_FUSED_PIPE=1): measured 14.6 vs
+    // 13.8 us/frame for the classic kernel at C3 -- the passes are not
+    // barrier-bound but latency-bound at ~20 resident warps either way
+    static const bool pipe = getenv("SN_FUSED_PIPE") != nullptr;
+    if (pipe && PipeCfg<R>::fits) {
       auto kern = fixed_square_pipe_kernel<R>;
       static bool attr_set = false;
       if (!attr_set) {
@@ -990,8 +870,11 @@ int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const s
                        (p.W % (16 / (int64_t)sizeof(T)) == 0) && (p.W % 2 == 0) &&
                        p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
   if (!affine && !force_generic && m.square_r >= 1 && m.square_r <= 8 && aligned) {
-    const int rc = dispatch_square<T>(m.square_r, ctx, disp, p, out6, mask);
-    if (rc >= 0) return rc;  // the fused kernel also emitted p.bits
+    int rc = dispatch_square<T>(m.square_r, ctx, disp, p, out6, mask);
+    if (rc == SN_OK && p.bits != nullptr) {
+      if constexpr (sizeof(T) == 4) rc = run_passable_bits(ctx, disp, p, p.bits);
+    }
+    if (rc >= 0) return rc;
   }
   int rc = launch_generic<T>(ctx, disp, p, tab, out6, mask, a1, a2, affine);
   if (rc == SN_OK && !affine && p.bits != nullptr) {

@@ -128,6 +128,20 @@ def oriented_points_bits(disparity: torch.Tensor, rig, kernels, threshold: float
     return out, bits
 
 
+def passable_bits(disparity: torch.Tensor, rig, threshold: float, *, bits=None) -> torch.Tensor:
+    """ST-passable bit mask ``[B, H, ceil(W/32)]`` int32 (streaming kernel)."""
+    d = _fp32(_batched(disparity))
+    B, H, W = d.shape
+    dev = d.device
+    bits = _check_out(bits, (B, H, bit_words(W)), torch.int32, dev, "bits")
+    rs = _native.rig_struct(rig)
+    rc = _native.load().sn_passable_bits(_native.plan(dev.index), d.data_ptr(), B, H, W,
+                                         ctypes.byref(rs), float(threshold), bits.data_ptr(),
+                                         _stream(dev))
+    check(rc, "passable_bits")
+    return bits
+
+
 def labels_from_bits(bits: torch.Tensor, width: int, *, out=None, row_base: int = 0,
                      workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Component labels from a passable bit mask ``[B, H, ceil(W/32)]``."""

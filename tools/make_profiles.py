@@ -113,11 +113,11 @@ def main():
             "dram_bytes_read": rd, "dram_bytes_write": wr,
             "dram_bytes_per_launch_at_c3": (rd + wr) * 256 / frames,
             "dram_bytes_per_px": (rd + wr) / px,
-            "algorithmic_bytes_per_px": 28.125,
+            "algorithmic_bytes_per_px": 28.0,
             "ncu_time_ms": t * 1e3,
             "dram_gbs_under_ncu": (rd + wr) / t / 1e9,
         }
-    ccl = full_summary(tag, "ccl", "ccl_")
+    ccl = full_summary(tag, "ccl", "ccl_|passable_bits")
     if ccl:
         summ["ccl"] = {}
         for d in ccl:
