@@ -702,11 +702,19 @@ __global__ void __launch_bounds__(256)
         if (xr < W) er = __fmul_rn(p.fxb_f, rcp_ftz(__ldg(fr + y * W + xr)));
       }
     }
-    uint32_t pb = 0, ub = 0;  // bit k: row y0 + k passable / undecided by the filter
+    // interior pixels only (the reference has no padding): rows 1 .. H-2, cols 1 .. W-2
+    uint32_t rows_in = (kPbRows == 32) ? 0xffffffffu : ((1u << kPbRows) - 1u);
+    if (y0 == 0) rows_in &= ~1u;
+    if (H - 1 - y0 < kPbRows) rows_in &= (H - 1 - y0 > 0) ? ((1u << (H - 1 - y0)) - 1u) : 0u;
+    if (!(x >= 1 && x + 1 < W)) rows_in = 0;
     const float2 tm2 = make_float2(tm, tm);
     const float2 k20 = make_float2(9.5367431640625e-07f, 9.5367431640625e-07f);  // 2^-20
     const float2 four = make_float2(4.0f, 4.0f);
-    // rows in pairs, packed f32x2 (FADD2/FMUL2/FFMA2)
+    const bool pe = p.pred_exact != 0;
+    // lane k < kPbRows ends up with the words of row y0 + k: passable (mine)
+    // and undecided by the filter (mund)
+    uint32_t mine = 0, mund = 0;
+    // rows in pairs, packed f32x2 (FADD2/FMUL2/FFMA2); one ballot per row
 #pragma unroll
     for (int k = 0; k < kPbRows; k += 2) {
       float2 L, R;
@@ -721,45 +729,46 @@ __global__ void __launch_bounds__(256)
       const float2 C = make_float2(z[k + 1], z[k + 2]);
       const float2 U = make_float2(z[k], z[k + 1]), D = make_float2(z[k + 2], z[k + 3]);
       const float2 c4 = __fmul2_rn(four, C);
-      const float2 vp = __fadd2_rn(__fadd2_rn(c4, make_float2(-U.x, -U.y)), make_float2(-D.x, -D.y));
-      const float2 sp = __fadd2_rn(__fadd2_rn(c4, U), D);
+      const float2 ud = __fadd2_rn(U, D);
       const float2 hs = __fadd2_rn(L, R);
-      const float2 S = __fadd2_rn(sp, hs);
-      const float2 e = __fadd2_rn(vp, make_float2(-hs.x, -hs.y));
+      const float2 S = __fadd2_rn(__fadd2_rn(c4, ud), hs);
+      // e = (4c - (u + d)) - (l + r): three roundings of partial sums <= S
+      const float2 e = __ffma2_rn(make_float2(-1.0f, -1.0f), hs,
+                                  __ffma2_rn(make_float2(-1.0f, -1.0f), ud, c4));
       const float2 m = __ffma2_rn(S, k20, tm2);
       const float a0 = __fsub_rn(fabsf(e.x), p.t_f), a1 = __fsub_rn(fabsf(e.y), p.t_f);  // e - t
       const float mn0 = fminf(fminf(fminf(U.x, D.x), fminf(L.x, R.x)), C.x);
       const float mn1 = fminf(fminf(fminf(U.y, D.y), fminf(L.y, R.y)), C.y);
-      const bool ok0 = (S.x <= 1.0141204801825835e31f) && (mn0 >= 7.888609052210118e-31f);
-      const bool ok1 = (S.y <= 1.0141204801825835e31f) && (mn1 >= 7.888609052210118e-31f);
-      pb |= ((ok0 && a0 < -m.x ? 1u : 0u) | (ok1 && a1 < -m.y ? 2u : 0u)) << k;
-      ub |= ((ok0 && (a0 < -m.x || a0 > m.x) ? 0u : 1u) | (ok1 && (a1 < -m.y || a1 > m.y) ? 0u : 2u))
-            << k;
+      const bool ok0 = !pe && (S.x <= 1.0141204801825835e31f) && (mn0 >= 7.888609052210118e-31f);
+      const bool ok1 = !pe && (S.y <= 1.0141204801825835e31f) && (mn1 >= 7.888609052210118e-31f);
+      const bool in0 = (rows_in >> k) & 1u, in1 = (rows_in >> (k + 1)) & 1u;
+      const uint32_t wp0 = __ballot_sync(0xffffffffu, in0 && ok0 && a0 < -m.x);
+      const uint32_t wp1 = __ballot_sync(0xffffffffu, in1 && ok1 && a1 < -m.y);
+      const uint32_t wu0 = __ballot_sync(0xffffffffu, in0 && !(ok0 && fabsf(a0) > m.x));
+      const uint32_t wu1 = __ballot_sync(0xffffffffu, in1 && !(ok1 && fabsf(a1) > m.y));
+      if (lane == k) {
+        mine = wp0;
+        mund = wu0;
+      }
+      if (lane == k + 1) {
+        mine = wp1;
+        mund = wu1;
+      }
     }
-    // interior pixels only (the reference has no padding)
-    uint32_t rows_in = (kPbRows == 32) ? 0xffffffffu : ((1u << kPbRows) - 1u);
-    if (y0 == 0) rows_in &= ~1u;
-    if (H - 1 - y0 < kPbRows) rows_in &= (H - 1 - y0 > 0) ? ((1u << (H - 1 - y0)) - 1u) : 0u;
-    if (!(x >= 1 && x + 1 < W)) rows_in = 0;
-    if (p.pred_exact) {
-      pb = 0;
-      ub = rows_in;
-    }
-    pb &= rows_in;
-    ub &= rows_in;
     // rare exact decisions (fp64, reference op order), after the row loop so
-    // a warp diverges at most once per task
-    while (ub) {
-      const int k = __ffs(ub) - 1;
-      ub &= ub - 1u;
-      const float* c = fr + (y0 + k) * W + x;
-      pb |= pred_exact_d(c[0], c[-1], c[1], c[-W], c[W], p.fxb, p.t) << k;
-    }
-    uint32_t mine = 0;  // lane k < kPbRows: the bit-mask word of row y0 + k
-#pragma unroll
-    for (int k = 0; k < kPbRows; ++k) {
-      const uint32_t b = __ballot_sync(0xffffffffu, (pb >> k) & 1u);
-      if (lane == k) mine = b;
+    // a warp diverges only for the rows that need it
+    if (__any_sync(0xffffffffu, mund != 0u)) {
+      for (int k = 0; k < kPbRows; ++k) {
+        const uint32_t wu = __shfl_sync(0xffffffffu, mund, k);
+        if (wu == 0u) continue;
+        bool pk = false;
+        if ((wu >> lane) & 1u) {
+          const float* c = fr + (y0 + k) * W + x;
+          pk = pred_exact_d(c[0], c[-1], c[1], c[-W], c[W], p.fxb, p.t) != 0u;
+        }
+        const uint32_t fix = __ballot_sync(0xffffffffu, pk);
+        if (lane == k) mine |= fix;
+      }
     }
     if (lane < kPbRows && y0 + lane < H) bits[((int64_t)f * p.H + y0 + lane) * WW + wc] = mine;
   }
