@@ -299,22 +299,32 @@ def main():
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("fused_pass", {}).get("dram_bytes_per_launch_at_c3")
 
-    # e2e through the C-ABI host-buffer entry (pinned host buffers)
+    # e2e through the C-ABI host-buffer entry (pinned host buffers): the same
+    # pipeline (points + passable bits + labels) with H2D of the disparities
+    # and D2H of the points and labels inside the timed region
     e2e = None
     if not args.no_e2e:
         host_in = disp.cpu().pin_memory()
         host_out = torch.empty((B, H, W, 6), dtype=torch.float32).pin_memory()
+        host_lab = torch.empty((B, H, W), dtype=torch.int32).pin_memory()
         lib = _native.load()
         plan = _native.plan(local)
         rs = _native.rig_struct(rig)
         off = _native.offsets_array(__import__("paper_2504_15121_b200").KernelSpec.square(KSIZE).offsets)
+        full = args.pipeline == "full"
 
         def host_step():
-            rc = lib.sn_oriented_points_host(plan, host_in.data_ptr(), B, H, W, ctypes.byref(rs),
-                                             off.ctypes.data, len(off), host_out.data_ptr(), None)
-            _native.check(rc, "sn_oriented_points_host")
-            # read back one result value from the host buffer (the step's result is in host memory)
-            return float(host_out[0, H // 2, W // 2, 5])
+            if full:
+                rc = lib.sn_pipeline_host(plan, host_in.data_ptr(), B, H, W, ctypes.byref(rs),
+                                          off.ctypes.data, len(off), T_ST, host_out.data_ptr(),
+                                          None, host_lab.data_ptr())
+            else:
+                rc = lib.sn_oriented_points_host(plan, host_in.data_ptr(), B, H, W, ctypes.byref(rs),
+                                                 off.ctypes.data, len(off), host_out.data_ptr(),
+                                                 None)
+            _native.check(rc, "host pipeline")
+            # the step's result is in host memory: read one value of each output
+            return float(host_out[0, H // 2, W // 2, 5]) + (int(host_lab[0, H // 2, W // 2]) if full else 0)
 
         host_step()
         if world > 1:
@@ -328,9 +338,11 @@ def main():
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         sec = float(e2e_s.item())
         e2e = {"value": world * px_step / 1e6 / sec, "unit": "Mpx/s",
-               "h2d_bytes_per_step": int(px_step * 4), "d2h_bytes_per_step": int(px_step * 24),
+               "h2d_bytes_per_step": int(px_step * 4),
+               "d2h_bytes_per_step": int(px_step * (24 + (4 if full else 0))),
                "ms_per_step": sec * 1e3,
-               "path": "sn_oriented_points_host (pinned host in/out, 3-stream H2D/compute/D2H overlap)"}
+               "path": ("sn_pipeline_host" if full else "sn_oriented_points_host") +
+                       " (pinned host in/out, 3-stream H2D/compute/D2H overlap)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -132,6 +132,13 @@ SN_API int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int6
                             int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
                             int32_t n_off, float* out6_host, uint8_t* mask_host);
 
+/* The whole pipeline on host buffers (pinned for full overlap): points,
+ * optional mask, and component labels, chunked with H2D / compute / D2H
+ * overlapped; returns when every output is in host memory. */
+SN_API int sn_pipeline_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
+                     int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
+                     double t, float* out6_host, uint8_t* mask_host, int32_t* labels_host);
+
 /* convolve_affine (gradient convention a1 - 1 = dd/du, a2 = dd/dv); a1/a2 are
  * NaN where mask is 0.  Device pointers, fp64 outputs. */
 SN_API int sn_affine(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,

@@ -15,7 +15,7 @@ tensors, [B, H, W] in, [B, H, W, 6] fp32 out); multi-GPU sharding lives in
 """
 
 from ._native import DegenerateSupportError, NativeLibraryError
-from .components import edge_map, label_components, passable_set
+from .components import edge_map, label_components, oriented_point_cloud, passable_set
 from .estimators import AffineNormalEstimator, BaseNormalEstimator, as_rig, as_scalar_field
 from .fields import AffineField, NormalField, ScalarField
 from .geometry import StereoRig, pixel_grid, triangulate_grid
@@ -29,5 +29,5 @@ __all__ = [
     "KernelSpec", "NativeLibraryError", "NormalField", "PrecomputedKernels", "ScalarField",
     "StereoRig", "as_rig", "as_scalar_field", "build_kernels", "convolve_affine", "edge_map",
     "estimate_affine_direct", "estimate_normals_fixed", "format_kernel_dump",
-    "label_components", "passable_set", "pixel_grid", "triangulate_grid",
+    "label_components", "oriented_point_cloud", "passable_set", "pixel_grid", "triangulate_grid",
 ]

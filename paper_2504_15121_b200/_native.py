@@ -67,6 +67,7 @@ SIGNATURES = {
                        ctypes.c_size_t, _P],
     "sn_ccl_from_bits_ws": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_oriented_points_host": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P],
+    "sn_pipeline_host": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P],
     "sn_affine": [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P, _P],
     "sn_affine_f64": [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P, _P],
     "sn_passable": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P, _P],

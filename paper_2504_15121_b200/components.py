@@ -56,3 +56,32 @@ def label_components(disparity: ScalarField, rig: StereoRig, threshold: float) -
 
     d = to_device(disparity.values, dtype=torch.float32)
     return to_host(device.component_labels(d, rig, _threshold(threshold))[0])
+
+
+def oriented_point_cloud(disparities, rig: StereoRig, kernel_size: int = 9,
+                         threshold: float = 0.2):
+    """The whole hot path on host arrays: ``disparities`` ``[B, H, W]`` (or
+    ``[H, W]``) -> (``[B, H, W, 6]`` float32 oriented points ``(x, y, z, nx, ny,
+    nz)`` -- the dense PLY vertex record, cli.py:118-123 -- and ``[B, H, W]``
+    int32 component labels).  One C-ABI call (sn_pipeline_host): chunked
+    H2D / compute / D2H overlap on the device of the current torch context."""
+    import ctypes
+    from . import _native
+    from ._host import current_device
+    from .kernels import KernelSpec
+
+    d = np.ascontiguousarray(np.asarray(disparities, dtype=np.float32))
+    if d.ndim == 2:
+        d = d[None]
+    if d.ndim != 3:
+        raise ValueError(f"disparities must have shape [B, H, W] or [H, W], got {d.shape}")
+    B, H, W = d.shape
+    pts = np.empty((B, H, W, 6), dtype=np.float32)
+    lab = np.empty((B, H, W), dtype=np.int32)
+    off = _native.offsets_array(KernelSpec.square(int(kernel_size)).offsets)
+    rs = _native.rig_struct(rig)
+    rc = _native.load().sn_pipeline_host(
+        _native.plan(current_device().index), d.ctypes.data, B, H, W, ctypes.byref(rs),
+        off.ctypes.data, len(off), _threshold(threshold), pts.ctypes.data, None, lab.ctypes.data)
+    _native.check(rc, "oriented_point_cloud")
+    return pts, lab

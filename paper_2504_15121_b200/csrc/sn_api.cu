@@ -91,7 +91,9 @@ struct sn_plan {
   float* d_in[2] = {nullptr, nullptr};
   float* d_out[2] = {nullptr, nullptr};
   uint8_t* d_mask[2] = {nullptr, nullptr};
-  size_t cap_px = 0;
+  int32_t* d_lab[2] = {nullptr, nullptr};
+  void* d_ws[2] = {nullptr, nullptr};
+  size_t cap_px = 0, ws_cap = 0;
   // labeller workspace for the entry points without an explicit one
   void* ccl_ws = nullptr;
   size_t ccl_ws_bytes = 0;
@@ -275,6 +277,8 @@ int sn_plan_destroy(sn_plan_t* plan) {
       if (plan->d_in[i]) cudaFree(plan->d_in[i]);
       if (plan->d_out[i]) cudaFree(plan->d_out[i]);
       if (plan->d_mask[i]) cudaFree(plan->d_mask[i]);
+      if (plan->d_lab[i]) cudaFree(plan->d_lab[i]);
+      if (plan->d_ws[i]) cudaFree(plan->d_ws[i]);
       if (plan->ev_in[i]) cudaEventDestroy(plan->ev_in[i]);
       if (plan->ev_done[i]) cudaEventDestroy(plan->ev_done[i]);
       if (plan->ev_out[i]) cudaEventDestroy(plan->ev_out[i]);
@@ -612,15 +616,23 @@ int sn_seam_merge_host(const int32_t* seams, int32_t n_strips, int64_t W, int32_
 // host-buffer path: frames in chunks, H2D / compute / D2H overlapped on three
 // streams with double-buffered device staging.
 
-int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
-                            int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
-                            int32_t n_off, float* out6_host, uint8_t* mask_host) {
+}  // extern "C"
+
+namespace {
+
+// host-buffer pipeline: frames in chunks, H2D / compute / D2H overlapped on
+// three streams with double-buffered device staging; labels (and the
+// passable bits they need) only when labels_host is non-NULL
+int host_pipeline(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H, int64_t W,
+                  const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                  float* out6_host, uint8_t* mask_host, int32_t* labels_host) {
   if (!plan) return set_error(SN_EINVAL, "plan is NULL");
   int rc = check_shape(B, H, W);
   if (rc) return rc;
   if ((rc = check_rig(rig))) return rc;
   sn_moments_t m;
   if ((rc = sn_kernel_moments(offsets_xy, n_off, &m))) return rc;
+  if (labels_host && !(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
   const int64_t frame_px = H * W;
   if (B * frame_px == 0) return SN_OK;
   if (!disp_host || !out6_host) return set_error(SN_EINVAL, "NULL buffer");
@@ -630,23 +642,34 @@ int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, 
   int64_t chunk = std::max<int64_t>(1, (int64_t)(16 << 20) / std::max<int64_t>(frame_px, 1));
   chunk = std::min<int64_t>(chunk, B);
   const size_t need = (size_t)(chunk * frame_px);
-  if (plan->cap_px < need) {
+  const size_t ws_need = labels_host ? ccl_workspace_bytes(chunk, H, W) : 0;
+  if (plan->cap_px < need || (labels_host && (!plan->d_lab[0] || plan->ws_cap < ws_need))) {
     for (int i = 0; i < 2; ++i) {
-      if (plan->d_in[i]) cudaFree(plan->d_in[i]);
-      if (plan->d_out[i]) cudaFree(plan->d_out[i]);
-      if (plan->d_mask[i]) cudaFree(plan->d_mask[i]);
+      cudaFree(plan->d_in[i]);
+      cudaFree(plan->d_out[i]);
+      cudaFree(plan->d_mask[i]);
+      cudaFree(plan->d_lab[i]);
+      cudaFree(plan->d_ws[i]);
       plan->d_in[i] = nullptr;
       plan->d_out[i] = nullptr;
       plan->d_mask[i] = nullptr;
+      plan->d_lab[i] = nullptr;
+      plan->d_ws[i] = nullptr;
     }
     plan->cap_px = 0;
+    plan->ws_cap = 0;
+    const size_t cap = std::max(need, plan->cap_px);
     for (int i = 0; i < 2; ++i) {
-      if (cudaMalloc(&plan->d_in[i], need * sizeof(float)) != cudaSuccess ||
-          cudaMalloc(&plan->d_out[i], need * 24) != cudaSuccess ||
-          cudaMalloc(&plan->d_mask[i], need) != cudaSuccess)
+      if (cudaMalloc(&plan->d_in[i], cap * sizeof(float)) != cudaSuccess ||
+          cudaMalloc(&plan->d_out[i], cap * 24) != cudaSuccess ||
+          cudaMalloc(&plan->d_mask[i], cap) != cudaSuccess)
         return set_cuda_error("cudaMalloc(host-path staging)");
+      if (labels_host && (cudaMalloc(&plan->d_lab[i], cap * 4) != cudaSuccess ||
+                          cudaMalloc(&plan->d_ws[i], ws_need) != cudaSuccess))
+        return set_cuda_error("cudaMalloc(host-path labeller staging)");
     }
-    plan->cap_px = need;
+    plan->cap_px = cap;
+    if (labels_host) plan->ws_cap = ws_need;
   }
   if (!plan->s_h2d) {
     if (cudaStreamCreateWithFlags(&plan->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
@@ -676,8 +699,13 @@ int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, 
       return set_cuda_error("H2D copy");
     cudaEventRecord(plan->ev_in[s], plan->s_h2d);
     cudaStreamWaitEvent(plan->s_comp, plan->ev_in[s], 0);
-    rc = sn_oriented_points(plan, plan->d_in[s], nf, H, W, rig, offsets_xy, n_off, plan->d_out[s],
-                            mask_host ? plan->d_mask[s] : nullptr, plan->s_comp);
+    uint8_t* dmask = mask_host ? plan->d_mask[s] : nullptr;
+    if (labels_host)
+      rc = sn_pipeline_ws(plan, plan->d_in[s], nf, H, W, rig, offsets_xy, n_off, t, plan->d_out[s],
+                          dmask, plan->d_lab[s], plan->d_ws[s], plan->ws_cap, plan->s_comp);
+    else
+      rc = sn_oriented_points(plan, plan->d_in[s], nf, H, W, rig, offsets_xy, n_off,
+                              plan->d_out[s], dmask, plan->s_comp);
     if (rc) return rc;
     cudaEventRecord(plan->ev_done[s], plan->s_comp);
     cudaStreamWaitEvent(plan->s_d2h, plan->ev_done[s], 0);
@@ -688,11 +716,34 @@ int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, 
         cudaMemcpyAsync(mask_host + f0 * frame_px, plan->d_mask[s], px, cudaMemcpyDeviceToHost,
                         plan->s_d2h) != cudaSuccess)
       return set_cuda_error("D2H mask copy");
+    if (labels_host &&
+        cudaMemcpyAsync(labels_host + f0 * frame_px, plan->d_lab[s], px * 4,
+                        cudaMemcpyDeviceToHost, plan->s_d2h) != cudaSuccess)
+      return set_cuda_error("D2H label copy");
     cudaEventRecord(plan->ev_out[s], plan->s_d2h);
   }
   if (cudaStreamSynchronize(plan->s_d2h) != cudaSuccess) return set_cuda_error("host-path sync");
   if (cudaStreamSynchronize(plan->s_comp) != cudaSuccess) return set_cuda_error("host-path sync");
   return SN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
+                            int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
+                            int32_t n_off, float* out6_host, uint8_t* mask_host) {
+  return host_pipeline(plan, disp_host, B, H, W, rig, offsets_xy, n_off, 0.0, out6_host,
+                       mask_host, nullptr);
+}
+
+int sn_pipeline_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H, int64_t W,
+                     const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                     float* out6_host, uint8_t* mask_host, int32_t* labels_host) {
+  if (B * H * W > 0 && !labels_host) return set_error(SN_EINVAL, "NULL label buffer");
+  return host_pipeline(plan, disp_host, B, H, W, rig, offsets_xy, n_off, t, out6_host, mask_host,
+                       labels_host);
 }
 
 }  // extern "C"

@@ -49,3 +49,18 @@ def test_frame_shards_match_batch(cuda_dev):
                 continue
             assert _nan_eq(device.oriented_points(d[a:b], sc.rig, 9), whole[a:b])
             assert torch.equal(device.component_labels(d[a:b], sc.rig, 0.2), whole_lab[a:b])
+
+
+def test_host_pipeline_matches_device(cuda_dev):
+    """sn_pipeline_host (chunked H2D / compute / D2H) == the device pipeline,
+    with a batch that spans several chunks and an odd last chunk."""
+    import paper_2504_15121_b200 as sn
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(2048, 1024)
+    clean = scenes.raycast(sc)[0]
+    frames = np.stack([scenes.add_gaussian_noise(clean, 0.3, i) for i in range(11)]).astype(np.float32)
+    frames[3, 100:140, 500:560] = np.nan
+    pts, lab = sn.oriented_point_cloud(frames, sc.rig, 9, 0.2)
+    dp, dl = device.pipeline(torch.from_numpy(frames).to(cuda_dev), sc.rig, 9, 0.2)
+    assert np.array_equal(np.nan_to_num(pts, nan=7.0), np.nan_to_num(dp.cpu().numpy(), nan=7.0))
+    assert np.array_equal(lab, dl.cpu().numpy())
