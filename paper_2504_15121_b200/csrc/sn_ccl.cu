@@ -20,9 +20,9 @@
 // to the smaller (atomicMin), so a root is always its component's minimum
 // and the result is independent of scheduling.  Three launches per batch:
 //
-//   1. ccl_tile_kernel   128x64 tile per CTA, 256 threads = (row, word).
-//      (predicate -> bits by ballot, unless the fused pass already emitted
-//      them), run union-find in shared memory, tile-border labels -> compact
+//   1. ccl_tile_kernel   128x128 tile per CTA, 256 threads = (2-row band,
+//      word); bits from passable_bits_kernel (or a uint8 grid), band-run
+//      union-find in shared memory, tile-border labels -> compact
 //      seam rows / columns, global node init G[root] = root for
 //      border-touching roots, and the tile's parent array (2-byte node ids,
 //      roots at run starts) + border-root flags for pass 3.
@@ -45,13 +45,12 @@
 namespace sn {
 
 constexpr int kLTW = 128;             // label tile columns
-constexpr int kLTH = 64;              // label tile rows
+constexpr int kLTH = 128;             // label tile rows
 constexpr int kLWords = kLTW / 32;    // words per tile row
-constexpr int kRowWords = kLTH * kLWords;  // 256 row-words per tile
+constexpr int kRowWords = kLTH * kLWords;  // 512 row-words per tile
 constexpr int kBands = kLTH / 2;      // 2-row bands per tile
-constexpr int kLThreads = kBands * kLWords;  // 128: one thread per (band, word)
+constexpr int kLThreads = kBands * kLWords;  // 256: one thread per (band, word)
 constexpr int kSlots = kBands * kLTW;  // node slots: band * 128 + column of a band-run start
-constexpr int kZW = kLTW + 2, kZH = kLTH + 2;  // fp32 depth tile with a 1-pixel halo
 
 __device__ __forceinline__ double depth_of(float d, double fxb) {
   // NaN marks an invalid depth sample
@@ -68,18 +67,6 @@ __device__ __forceinline__ double edge_value(double c, double l, double r, doubl
 }
 
 __device__ __forceinline__ bool valid_z(double z) { return z == z; }
-
-// exact fp64 predicate at interior pixel (x, y) of frame f (row pitch W)
-__device__ __noinline__ bool exact_passable(const float* __restrict__ f, int64_t W, int64_t x,
-                                            int64_t y, double fxb, double t) {
-  const double c = depth_of(f[y * W + x], fxb);
-  const double l = depth_of(f[y * W + x - 1], fxb);
-  const double r = depth_of(f[y * W + x + 1], fxb);
-  const double u = depth_of(f[(y - 1) * W + x], fxb);
-  const double dn = depth_of(f[(y + 1) * W + x], fxb);
-  if (!(valid_z(c) && valid_z(l) && valid_z(r) && valid_z(u) && valid_z(dn))) return false;
-  return edge_value(c, l, r, u, dn) <= t;
-}
 
 // ---------------------------------------------------------------------------
 // standalone predicate (API sn_passable; exact fp64 per pixel, optional edges)
@@ -266,7 +253,7 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
   __syncthreads();
 }
 
-constexpr int kTilePx = kLTW * kLTH;  // 8192: tile pixel index fits 13 bits
+constexpr int kTilePx = kLTW * kLTH;  // 16384: tile pixel index fits 14 bits
 
 struct CclWorkspace {
   uint32_t* bits;   // [B][H][WW]
@@ -284,18 +271,19 @@ __device__ __forceinline__ int frame_index(int px, int x0, int y0, int W) {
 }
 
 // ---------------------------------------------------------------------------
-// 1. tile pass.  MODE 0: predicate from fp32 disparity; MODE 1: uint8
-// passable; MODE 2: the bit mask is the input (emitted by the fused pass)
+// 1. tile pass.  MODE 1: uint8 passable input; MODE 2: the bit mask is the
+// input (passable_bits_kernel).  Dynamic shared memory: the parent array
+// (kSlots int32) + the exported slot labels (kSlots uint16) = 48 KB.
+
+constexpr size_t kTileSmem = (size_t)kSlots * 4 + (size_t)kSlots * 2;
 
 template <int MODE>
 __global__ void __launch_bounds__(kLThreads)
-    ccl_tile_kernel(const float* __restrict__ disp, const uint8_t* __restrict__ pas_in,
-                    const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
-  // fp32 depth tile (MODE 0), then the parent array + the exported labels
-  __shared__ __align__(16) int32_t smem[MODE == 0 ? kZH * kZW : kSlots + kSlots / 2];
+    ccl_tile_kernel(const uint8_t* __restrict__ pas_in, const CclParams p, const CclWorkspace ws,
+                    int32_t* __restrict__ labels) {
+  extern __shared__ __align__(16) int32_t smem[];
   __shared__ uint32_t bits[kRowWords];
   __shared__ uint32_t flag[kTilePx / 32];
-  static_assert(kZH * kZW * 4 >= kSlots * 4 + kSlots * 2, "L + exported labels fit the z tile");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
   const int tx = blockIdx.x, ty = blockIdx.y;
@@ -304,33 +292,7 @@ __global__ void __launch_bounds__(kLThreads)
   const int64_t frow = (int64_t)blockIdx.z * H;
 
   for (int i = tid; i < kTilePx / 32; i += kLThreads) flag[i] = 0u;
-  if (MODE == 0) {
-    const float* f = disp + fbase;
-    float* zs = reinterpret_cast<float*>(smem);
-    for (int i = tid; i < kZH * kZW; i += kLThreads) {
-      const int iy = i / kZW, ix = i - iy * kZW;
-      const int gx = x0 - 1 + ix, gy = y0 - 1 + iy;
-      float z = __int_as_float(0x7fc00000);  // outside the frame: invalid sample
-      if ((unsigned)gx < (unsigned)W && (unsigned)gy < (unsigned)H)
-        z = p.exact_only ? __int_as_float(0x7f800000) : zfast(f[(int64_t)gy * W + gx], p.fxb_f);
-      zs[i] = z;
-    }
-    __syncthreads();
-    for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
-      const int r = rw >> 2, c = (rw & 3) * 32 + lane;
-      const int gx = x0 + c, gy = y0 + r;
-      bool pk = false;
-      if (gx < W && gy < H) {
-        const int zi = (r + 1) * kZW + c + 1;
-        const int dec = (int)zpred(zs[zi], zs[zi - 1], zs[zi + 1], zs[zi - kZW], zs[zi + kZW],
-                                   p.t_f);
-        if (dec == 2) pk = exact_passable(f, W, gx, gy, p.fxb, p.t);
-        else pk = dec == 1;
-      }
-      const uint32_t b = __ballot_sync(0xffffffffu, pk);
-      if (lane == 0) bits[rw] = b;
-    }
-  } else if (MODE == 1) {
+  if (MODE == 1) {
     for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
       const int r = rw >> 2, c = (rw & 3) * 32 + lane;
       const int gx = x0 + c, gy = y0 + r;
@@ -345,7 +307,7 @@ __global__ void __launch_bounds__(kLThreads)
     }
   }
   __syncthreads();
-  if (MODE != 2) {
+  if (MODE == 1) {
     for (int i = tid; i < kRowWords; i += kLThreads) {
       const int r = i >> 2, wc = tx * kLWords + (i & 3);
       if (y0 + r < H && wc < ws.WW) ws.bits[(frow + y0 + r) * ws.WW + wc] = bits[i];
@@ -816,14 +778,34 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
   q += align256((size_t)(tiles * kSlots) * 2);
   ws.flags = reinterpret_cast<uint32_t*>(q);
 
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(ccl_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kTileSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(ccl_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kTileSmem) != cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(ccl_tile_kernel)");
+    attr_set = true;
+  }
+  if (disp) {
+    // predicate from fp32 disparity: the streaming bit-mask kernel first
+    FixedParams fp{};
+    fp.B = p.B;
+    fp.H = p.H;
+    fp.W = p.W;
+    fp.fxb = p.fxb;
+    fp.fxb_f = (float)p.fxb;
+    fill_predicate(fp, p.fxb, p.t, ws.bits);
+    const int rc0 = run_passable_bits(ctx, disp, fp, ws.bits);
+    if (rc0) return rc0;
+    bits_in = ws.bits;
+  }
   if (bits_in) ws.bits = const_cast<uint32_t*>(bits_in);  // read-only in MODE 2
   dim3 grid((unsigned)ws.n_tx, (unsigned)ws.n_ty, (unsigned)p.B);
   if (bits_in)
-    ccl_tile_kernel<2><<<grid, kLThreads, 0, ctx.stream>>>(nullptr, nullptr, p, ws, labels);
-  else if (disp)
-    ccl_tile_kernel<0><<<grid, kLThreads, 0, ctx.stream>>>(disp, nullptr, p, ws, labels);
+    ccl_tile_kernel<2><<<grid, kLThreads, kTileSmem, ctx.stream>>>(nullptr, p, ws, labels);
   else
-    ccl_tile_kernel<1><<<grid, kLThreads, 0, ctx.stream>>>(nullptr, pas, p, ws, labels);
+    ccl_tile_kernel<1><<<grid, kLThreads, kTileSmem, ctx.stream>>>(pas, p, ws, labels);
   int rc = check_launch("ccl_tile_kernel");
   if (rc) return rc;
   const int64_t n_seam = ((int64_t)(ws.n_ty - 1) * p.W + (int64_t)(ws.n_tx - 1) * p.H) * p.B;
