@@ -451,7 +451,7 @@ __global__ void ccl_seam_kernel(const CclParams p, const CclWorkspace ws,
 
 __global__ void __launch_bounds__(kLThreads)
     ccl_resolve_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
-  __shared__ __align__(16) uint16_t lbl[kSlots];
+  __shared__ __align__(16) int32_t lab[kSlots];  // slot label, then slot FINAL label
   __shared__ uint32_t bits[kRowWords];
   __shared__ uint32_t flag[kTilePx / 32];
   __shared__ int32_t rank0[kTilePx / 32];  // flagged labels before word i
@@ -466,9 +466,15 @@ __global__ void __launch_bounds__(kLThreads)
   const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
   {
     const uint4* src = reinterpret_cast<const uint4*>(ws.lbl + tile * kSlots);
-    uint4* dst = reinterpret_cast<uint4*>(lbl);
+    int4* dst = reinterpret_cast<int4*>(lab);
 #pragma unroll
-    for (int i = 0; i < kSlots / 8 / kLThreads; ++i) dst[i * kLThreads + tid] = src[i * kLThreads + tid];
+    for (int i = 0; i < kSlots / 8 / kLThreads; ++i) {
+      const uint4 v = src[i * kLThreads + tid];
+      dst[2 * (i * kLThreads + tid)] =
+          make_int4(v.x & 0xffff, v.x >> 16, v.y & 0xffff, v.y >> 16);
+      dst[2 * (i * kLThreads + tid) + 1] =
+          make_int4(v.z & 0xffff, v.z >> 16, v.w & 0xffff, v.w >> 16);
+    }
     for (int i = tid; i < kRowWords; i += kLThreads) {
       const int r = i >> 2, wc = tx * kLWords + (i & 3);
       bits[i] = (y0 + r < H && wc < ws.WW)
@@ -512,21 +518,35 @@ __global__ void __launch_bounds__(kLThreads)
     }
   }
   __syncthreads();
+  // final label of every band-run slot, by the slot's owner thread (band, word)
+  {
+    const int kb = tid >> 2, w = tid & 3;
+    const int base = kb * kLTW + w * 32;
+    for (uint32_t m = run_starts(band_word(bits, kb, w)); m; m &= m - 1u) {
+      const int slot = base + __ffs(m) - 1;
+      const int v = lab[slot];
+      const uint32_t fwv = flag[v >> 5];
+      const uint32_t bit = 1u << (v & 31);
+      lab[slot] = (fwv & bit) ? fin[rank0[v >> 5] + __popc(fwv & (bit - 1u))]
+                              : frame_index(v, x0, y0, W);
+    }
+  }
+  __syncthreads();
+  // per pixel: band-run slot by bit ops -> final label; coalesced stores
   int32_t* out = labels + fbase;
   const bool full = x0 + kLTW <= W && y0 + kLTH <= H;
+  const uint32_t upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
   for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
     const int r = rw >> 2, w = rw & 3;
     const int gx = x0 + w * 32 + lane, gy = y0 + r;
     if (!full && (gx >= W || gy >= H)) continue;
     const uint32_t A = bits[rw];
-    int32_t lab = -1;
+    int32_t v = -1;
     if ((A >> lane) & 1u) {
-      const int v = lbl[pixel_slot(bits, r, w * 32 + lane)];
-      const uint32_t fwv = flag[v >> 5];
-      const uint32_t bit = 1u << (v & 31);
-      lab = (fwv & bit) ? fin[rank0[v >> 5] + __popc(fwv & (bit - 1u))] : frame_index(v, x0, y0, W);
+      const uint32_t st = run_starts(band_word(bits, r >> 1, w));
+      v = lab[(r >> 1) * kLTW + w * 32 + (31 - __clz(st & upto))];
     }
-    out[(int64_t)gy * W + gx] = lab;
+    out[gy * W + gx] = v;  // frame offsets fit int32 (host-checked)
   }
 }
 
