@@ -535,18 +535,37 @@ __global__ void __launch_bounds__(kLThreads)
   // per pixel: band-run slot by bit ops -> final label; coalesced stores
   int32_t* out = labels + fbase;
   const bool full = x0 + kLTW <= W && y0 + kLTH <= H;
-  const uint32_t upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
-  for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
-    const int r = rw >> 2, w = rw & 3;
-    const int gx = x0 + w * 32 + lane, gy = y0 + r;
-    if (!full && (gx >= W || gy >= H)) continue;
-    const uint32_t A = bits[rw];
-    int32_t v = -1;
-    if ((A >> lane) & 1u) {
+  if (full && (W & 3) == 0) {
+    // a warp writes one 128-pixel tile row per step, 4 pixels (16 B) per lane
+    const int w = lane >> 3, sub = (lane & 7) * 4;
+    for (int r = warp; r < kLTH; r += kLThreads / 32) {
+      const uint32_t A = bits[r * kLWords + w];
       const uint32_t st = run_starts(band_word(bits, r >> 1, w));
-      v = lab[(r >> 1) * kLTW + w * 32 + (31 - __clz(st & upto))];
+      const int base = (r >> 1) * kLTW + w * 32;
+      int v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int b = sub + j;
+        const uint32_t upto = (b == 31) ? 0xffffffffu : ((2u << b) - 1u);
+        v[j] = ((A >> b) & 1u) ? lab[base + (31 - __clz(st & upto))] : -1;
+      }
+      *reinterpret_cast<int4*>(out + (y0 + r) * W + x0 + w * 32 + sub) =
+          make_int4(v[0], v[1], v[2], v[3]);
     }
-    out[gy * W + gx] = v;  // frame offsets fit int32 (host-checked)
+  } else {
+    const uint32_t upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+    for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
+      const int r = rw >> 2, w = rw & 3;
+      const int gx = x0 + w * 32 + lane, gy = y0 + r;
+      if (gx >= W || gy >= H) continue;
+      const uint32_t A = bits[rw];
+      int32_t v = -1;
+      if ((A >> lane) & 1u) {
+        const uint32_t st = run_starts(band_word(bits, r >> 1, w));
+        v = lab[(r >> 1) * kLTW + w * 32 + (31 - __clz(st & upto))];
+      }
+      out[gy * W + gx] = v;  // frame offsets fit int32 (host-checked)
+    }
   }
 }
 
