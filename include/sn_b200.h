@@ -204,6 +204,19 @@ SN_API int sn_relabel(sn_plan_t* plan, int32_t* labels, int64_t n, int64_t index
                const int32_t* map_keys, const int32_t* map_vals, const int32_t* n_map,
                int32_t map_capacity, int32_t* scratch, void* stream);
 
+/* Oriented point cloud compaction (cli.py:118-123, the vertices
+ * formats.py:170-185 writes): the records of pixels whose normal is valid
+ * (mask != 0, as emitted by the fused pass), in raster order over the whole
+ * batch, packed into cloud [N][6] float32 -- the binary-PLY vertex body.
+ * frame_offsets (device, B + 1 int64): frame f's vertices are
+ * [offsets[f], offsets[f+1]); offsets[B] = N even when N > capacity (only
+ * the first capacity vertices are written).  Workspace:
+ * sn_cloud_workspace_bytes. */
+SN_API int sn_cloud_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes);
+SN_API int sn_compact_cloud(sn_plan_t* plan, const float* out6, const uint8_t* mask, int64_t B,
+                     int64_t H, int64_t W, float* cloud, int64_t capacity,
+                     int64_t* frame_offsets, void* workspace, size_t ws_bytes, void* stream);
+
 /* Test hook: the fixed pass forced onto the generic (non-TMA) kernel, used to
  * cross-check the TMA fast path on identical inputs. */
 SN_API int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,

@@ -62,6 +62,8 @@ SIGNATURES = {
     "sn_oriented_points_bits": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P,
                                 _P],
     "sn_passable_bits": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P],
+    "sn_cloud_workspace_bytes": [_I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
+    "sn_compact_cloud": [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_pipeline": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P],
     "sn_pipeline_ws": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P,
                        ctypes.c_size_t, _P],

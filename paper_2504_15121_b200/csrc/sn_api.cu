@@ -381,6 +381,28 @@ int sn_passable_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, i
   return run_passable_bits(make_ctx(plan, stream), disp, p, bits);
 }
 
+int sn_cloud_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
+  if (!bytes) return set_error(SN_EINVAL, "bytes out-pointer is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  *bytes = cloud_workspace_bytes(B, H, W);
+  return SN_OK;
+}
+
+int sn_compact_cloud(sn_plan_t* plan, const float* out6, const uint8_t* mask, int64_t B,
+                     int64_t H, int64_t W, float* cloud, int64_t capacity, int64_t* frame_offsets,
+                     void* workspace, size_t ws_bytes, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (capacity < 0) return set_error(SN_EINVAL, "negative capacity");
+  if (!frame_offsets || (B * H * W > 0 && (!out6 || !mask || (capacity > 0 && !cloud))))
+    return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_compact_cloud(make_ctx(plan, stream), out6, mask, B, H, W, cloud, capacity,
+                           frame_offsets, workspace, ws_bytes);
+}
+
 /* test hook: force the generic (non-TMA) kernel, to cross-check the fast path */
 int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                                const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,

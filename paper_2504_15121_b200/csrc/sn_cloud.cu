@@ -1,0 +1,179 @@
+// Oriented point cloud compaction for sm_100a.
+//
+// Reference: cli.py:118-123 keeps pixels with a valid normal and a finite
+// point (keep = normals.mask & isfinite(pts)) and writes them in raster order
+// as binary-PLY vertices (x, y, z, nx, ny, nz) float32 (formats.py:170-185).
+// A valid normal implies d finite and > 0, hence a finite reference point,
+// so keep = the normal mask the fused pass emits.  The dense [B][H][W][6]
+// record is already the vertex layout; compaction is a stable stream
+// compaction of 24-byte records over the whole batch in raster order:
+//   1. cloud_count_kernel    per 2048-pixel block: popcount of the mask
+//   2. cloud_scan_kernel     exclusive scan of the block counts (one CTA)
+//   3. cloud_scatter_kernel  warp ballots give each kept pixel its slot;
+//                            records are copied as 3 x 8-byte words
+// Frame f's vertices start at offsets[f] (= the scan at its first block);
+// offsets[B] is the total.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sn_internal.h"
+
+namespace sn {
+
+constexpr int kCloudBlock = 2048;  // pixels per count block (blocks tile each frame separately)
+constexpr int kCloudThreads = 256;
+
+// blocks never straddle frames: frame f owns blocks [f*bpf, (f+1)*bpf)
+__global__ void __launch_bounds__(kCloudThreads)
+    cloud_count_kernel(const uint8_t* __restrict__ mask, int64_t HW, int bpf, int64_t n_blocks,
+                       int64_t* __restrict__ counts) {
+  __shared__ int warp_cnt[kCloudThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
+    const int64_t f = blk / bpf;
+    const int64_t p0 = (blk - f * bpf) * kCloudBlock;
+    const uint8_t* m = mask + f * HW;
+    int c = 0;
+    for (int i = tid; i < kCloudBlock; i += kCloudThreads) {
+      const int64_t px = p0 + i;
+      c += (px < HW && m[px] != 0) ? 1 : 0;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+    if (lane == 0) warp_cnt[warp] = c;
+    __syncthreads();
+    if (tid == 0) {
+      int s = 0;
+      for (int w = 0; w < kCloudThreads / 32; ++w) s += warp_cnt[w];
+      counts[blk] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// in-place exclusive scan of counts[0 .. n) with one CTA; counts[n] = total
+__global__ void __launch_bounds__(1024) cloud_scan_kernel(int64_t* __restrict__ counts, int64_t n) {
+  __shared__ int64_t warp_sum[32];
+  __shared__ int64_t carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += 1024) {
+    const int64_t i = base + tid;
+    const int64_t v = i < n ? counts[i] : 0;
+    int64_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += u;
+    }
+    if (lane == 31) warp_sum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t ws = warp_sum[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, ws, d);
+        if (lane >= d) ws += u;
+      }
+      warp_sum[lane] = ws;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t before = carry + (warp > 0 ? warp_sum[warp - 1] : 0);
+    if (i < n) counts[i] = before + inc - v;
+    __syncthreads();
+    if (tid == 1023) carry = before + inc;
+    __syncthreads();
+  }
+  if (tid == 0) counts[n] = carry;
+}
+
+__global__ void __launch_bounds__(kCloudThreads)
+    cloud_scatter_kernel(const float* __restrict__ out6, const uint8_t* __restrict__ mask,
+                         int64_t HW, int bpf, int64_t n_blocks, const int64_t* __restrict__ starts,
+                         float* __restrict__ cloud, int64_t capacity) {
+  __shared__ int warp_off[kCloudThreads / 32 + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
+    const int64_t f = blk / bpf;
+    const int64_t p0 = (blk - f * bpf) * kCloudBlock;
+    const uint8_t* m = mask + f * HW;
+    int64_t next = starts[blk];
+    // the block's pixels in rounds of 256: each round keeps raster order
+    for (int r0 = 0; r0 < kCloudBlock; r0 += kCloudThreads) {
+      const int64_t px = p0 + r0 + tid;
+      const bool keep = px < HW && m[px] != 0;
+      const uint32_t b = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) warp_off[warp] = __popc(b);
+      __syncthreads();
+      if (tid == 0) {
+        int s = 0;
+        for (int w = 0; w < kCloudThreads / 32; ++w) {
+          const int c = warp_off[w];
+          warp_off[w] = s;
+          s += c;
+        }
+        warp_off[kCloudThreads / 32] = s;
+      }
+      __syncthreads();
+      if (keep) {
+        const int64_t slot = next + warp_off[warp] + __popc(b & ((1u << lane) - 1u));
+        if (slot < capacity) {
+          const float2* src = reinterpret_cast<const float2*>(out6 + (f * HW + px) * 6);
+          float2* dst = reinterpret_cast<float2*>(cloud + slot * 6);
+          dst[0] = src[0];
+          dst[1] = src[1];
+          dst[2] = src[2];
+        }
+      }
+      next += warp_off[kCloudThreads / 32];
+      __syncthreads();
+    }
+  }
+}
+
+size_t cloud_workspace_bytes(int64_t B, int64_t H, int64_t W) {
+  const int64_t bpf = (H * W + kCloudBlock - 1) / kCloudBlock;
+  return (size_t)(B * bpf + 1) * sizeof(int64_t);
+}
+
+int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
+                      int64_t H, int64_t W, float* cloud, int64_t capacity,
+                      int64_t* frame_offsets, void* workspace, size_t ws_bytes) {
+  const int64_t HW = H * W;
+  if (B * HW == 0) {
+    return cudaMemsetAsync(frame_offsets, 0, (size_t)(B + 1) * sizeof(int64_t), ctx.stream) ==
+                   cudaSuccess
+               ? SN_OK
+               : set_cuda_error("cudaMemsetAsync(frame offsets)");
+  }
+  if (!workspace || ws_bytes < cloud_workspace_bytes(B, H, W))
+    return set_error(SN_EINVAL, "compaction workspace too small");
+  const int64_t bpf64 = (HW + kCloudBlock - 1) / kCloudBlock;
+  if (bpf64 > 0x7fffffffLL) return set_error(SN_EINVAL, "frame too large");
+  const int bpf = (int)bpf64;
+  const int64_t n_blocks = B * bpf64;
+  int64_t* counts = static_cast<int64_t*>(workspace);
+  int64_t grid = n_blocks;
+  if (grid > (int64_t)ctx.num_sms * 16) grid = (int64_t)ctx.num_sms * 16;
+  cloud_count_kernel<<<(unsigned)grid, kCloudThreads, 0, ctx.stream>>>(mask, HW, bpf, n_blocks,
+                                                                      counts);
+  int rc = check_launch("cloud_count_kernel");
+  if (rc) return rc;
+  cloud_scan_kernel<<<1, 1024, 0, ctx.stream>>>(counts, n_blocks);
+  if ((rc = check_launch("cloud_scan_kernel"))) return rc;
+  cloud_scatter_kernel<<<(unsigned)grid, kCloudThreads, 0, ctx.stream>>>(
+      out6, mask, HW, bpf, n_blocks, counts, cloud, capacity);
+  if ((rc = check_launch("cloud_scatter_kernel"))) return rc;
+  // frame offsets: the scan at each frame's first block, and the total
+  if (cudaMemcpy2DAsync(frame_offsets, sizeof(int64_t), counts, (size_t)bpf * sizeof(int64_t),
+                        sizeof(int64_t), (size_t)B, cudaMemcpyDeviceToDevice,
+                        ctx.stream) != cudaSuccess ||
+      cudaMemcpyAsync(frame_offsets + B, counts + n_blocks, sizeof(int64_t),
+                      cudaMemcpyDeviceToDevice, ctx.stream) != cudaSuccess)
+    return set_cuda_error("frame offsets copy");
+  return SN_OK;
+}
+
+}  // namespace sn

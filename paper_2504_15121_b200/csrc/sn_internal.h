@@ -63,4 +63,9 @@ int run_relabel(const LaunchCtx& ctx, int32_t* labels, int64_t n, int64_t base,
                 const int32_t* keys, const int32_t* vals, const int32_t* n_map, int32_t cap,
                 int32_t* scratch);
 
+size_t cloud_workspace_bytes(int64_t B, int64_t H, int64_t W);
+int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
+                      int64_t H, int64_t W, float* cloud, int64_t capacity,
+                      int64_t* frame_offsets, void* workspace, size_t ws_bytes);
+
 }  // namespace sn

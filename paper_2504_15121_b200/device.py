@@ -183,6 +183,40 @@ def pipeline(disparity: torch.Tensor, rig, kernels, threshold: float, *, out=Non
     return out, labels
 
 
+def compact_cloud(records: torch.Tensor, mask: torch.Tensor):
+    """Stream-compact the dense ``[B, H, W, 6]`` records of pixels with a valid
+    normal (``mask`` uint8 ``[B, H, W]`` from ``oriented_points(..., mask=)``)
+    into ``[N, 6]`` float32 vertices in raster order -- the binary-PLY body
+    (cli.py:118-123, formats.py:170-185).  Returns (vertices, offsets): frame f
+    owns ``vertices[offsets[f]:offsets[f+1]]`` (offsets int64 ``[B+1]``, host)."""
+    if records.dim() == 3:
+        records = records.unsqueeze(0)
+    if records.dim() != 4 or records.shape[-1] != 6 or records.dtype != torch.float32:
+        raise ValueError("records must be float32 [B, H, W, 6]")
+    records = records.contiguous()
+    B, H, W, _ = records.shape
+    dev = records.device
+    mask = _check_out(mask, (B, H, W), torch.uint8, dev, "mask")
+    n = ctypes.c_size_t(0)
+    check(_native.load().sn_cloud_workspace_bytes(B, H, W, ctypes.byref(n)), "sn_cloud_workspace_bytes")
+    ws = torch.empty(max(1, n.value), dtype=torch.uint8, device=dev)
+    offsets = torch.empty(B + 1, dtype=torch.int64, device=dev)
+    lib = _native.load()
+
+    def run(cloud, cap):
+        rc = lib.sn_compact_cloud(_native.plan(dev.index), records.data_ptr(), mask.data_ptr(),
+                                  B, H, W, cloud.data_ptr() if cloud is not None else None, cap,
+                                  offsets.data_ptr(), ws.data_ptr(), n.value, _stream(dev))
+        check(rc, "compact_cloud")
+
+    run(None, 0)  # counts only: the total decides the allocation
+    total = int(offsets[B].item())
+    cloud = torch.empty((total, 6), dtype=torch.float32, device=dev)
+    if total:
+        run(cloud, total)
+    return cloud, offsets.cpu()
+
+
 def affine(disparity: torch.Tensor, kernels, *, a1=None, a2=None, mask=None):
     """convolve_affine on the device: (a1, a2, mask) fp64/fp64/uint8 ``[B, H, W]``."""
     d = _batched(disparity)

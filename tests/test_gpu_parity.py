@@ -314,3 +314,36 @@ def test_bits_filter_ties_and_ranges(cuda_dev):
     for t in (float(vals[len(vals) // 3]), float(vals[len(vals) // 2]), float(vals[-2]), 0.2):
         _, bits = device.oriented_points_bits(dt, sc.rig, 9, t)
         assert np.array_equal(_bits_to_bool(bits, 512)[0], orc.passable(d64, o, t)), t
+
+
+@pytest.mark.parametrize("shape", [(3, 256, 512), (2, 77, 130), (1, 1, 1), (4, 1024, 2048)])
+def test_compact_cloud(cuda_dev, shape):
+    """Device compaction == the reference's keep rule on the dense record
+    (keep = normal mask & finite points, raster order, cli.py:118-123), and the
+    PLY body is the compacted bytes."""
+    from paper_2504_15121_b200 import device, formats, scenes
+    B, H, W = shape
+    if H * W == 1:
+        d = np.full((B, 1, 1), 5.0, np.float32)
+        rig = scenes.street_scene(8, 8).rig
+    else:
+        sc = scenes.street_scene(W, H)
+        rig = sc.rig
+        clean = scenes.raycast(sc)[0]
+        d = np.stack([scenes.add_gaussian_noise(clean, 0.5, i) for i in range(B)]).astype(np.float32)
+        d[0, H // 3:H // 3 + 9, W // 4:W // 4 + 13] = np.nan
+    dt = torch.from_numpy(d).to(cuda_dev)
+    mask = torch.empty(d.shape, dtype=torch.uint8, device=cuda_dev)
+    rec = device.oriented_points(dt, rig, 9, mask=mask)
+    cloud, offsets = device.compact_cloud(rec, mask)
+    r = rec.cpu().numpy()
+    m = mask.cpu().numpy().astype(bool)
+    keep = m & np.isfinite(r[..., :3]).all(-1)
+    assert np.array_equal(keep, m)  # a valid normal implies a finite point
+    want = r[keep]
+    assert cloud.shape == want.shape
+    assert np.array_equal(cloud.cpu().numpy(), want)
+    counts = keep.reshape(B, -1).sum(1)
+    assert np.array_equal(offsets.numpy(), np.concatenate([[0], np.cumsum(counts)]))
+    ply = formats.ply_from_vertices(cloud.cpu().numpy())
+    assert ply.endswith(want.astype("<f4").tobytes())

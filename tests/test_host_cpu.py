@@ -128,3 +128,16 @@ def test_seam_merge_matches_full_frame_labels():
     lut = dict(zip(keys.tolist(), vals.tolist()))
     merged = np.concatenate([np.vectorize(lambda v: lut.get(v, v))(s) for s in strips])
     assert np.array_equal(merged, full)
+
+
+def test_ply_writer_matches_reference_bytes():
+    """formats.ply_from_vertices / write_ply_oriented == the reference writer
+    (golden bytes from formats.py:170-185), binary and ASCII, empty clouds."""
+    from paper_2504_15121_b200 import formats
+    z = np.load(Path(__file__).resolve().parent / "golden" / "ply_cases.npz")
+    pts, nrm = z["points"], z["normals"]
+    for binary, tag in ((True, "bin"), (False, "ascii")):
+        assert formats.write_ply_oriented(pts, nrm, binary) == z[f"ply_{tag}"].tobytes()
+        assert formats.ply_from_vertices(np.hstack([pts, nrm]), binary) == z[f"ply_{tag}"].tobytes()
+        assert formats.write_ply_oriented(np.zeros((0, 3)), np.zeros((0, 3)), binary) == \
+            z[f"empty_{tag}"].tobytes()
