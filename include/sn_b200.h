@@ -204,6 +204,21 @@ SN_API int sn_relabel(sn_plan_t* plan, int32_t* labels, int64_t n, int64_t index
                const int32_t* map_keys, const int32_t* map_vals, const int32_t* n_map,
                int32_t map_capacity, int32_t* scratch, void* stream);
 
+/* Adaptive star-fill normals (estimate_normals_adaptive, adaptive.py:177-268;
+ * StarConfig adaptive.py:32-57): the dense record of the fixed pass with
+ * normals fitted over edge-aware star supports.  The rays are the
+ * reference's ray_offsets(config) (adaptive.py:60-77), passed as n_rays
+ * lengths + the concatenated (vx, vy) int32 pairs; stop 0 = "st" (edge value
+ * valid and <= threshold), 1 = "cd" (covered depth range <= threshold * z_c,
+ * per ray or shared_range).  Masks bit-exact with the reference.  Workspace:
+ * sn_adaptive_workspace_bytes (fp64 depth map + bit mask). */
+SN_API int sn_adaptive_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes);
+SN_API int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
+                       int64_t W, const sn_rig_t* rig, int32_t n_rays, const int32_t* ray_len,
+                       const int32_t* ray_xy, int32_t stop, int32_t shared_range,
+                       double threshold, float* out6, uint8_t* mask, void* workspace,
+                       size_t ws_bytes, void* stream);
+
 /* Oriented point cloud compaction (cli.py:118-123, the vertices
  * formats.py:170-185 writes): the records of pixels whose normal is valid
  * (mask != 0, as emitted by the fused pass), in raster order over the whole

@@ -16,7 +16,10 @@ tensors, [B, H, W] in, [B, H, W, 6] fp32 out); multi-GPU sharding lives in
 
 from ._native import DegenerateSupportError, NativeLibraryError
 from .components import edge_map, label_components, oriented_point_cloud, passable_set
-from .estimators import AffineNormalEstimator, BaseNormalEstimator, as_rig, as_scalar_field
+from .adaptive import (StarConfig, estimate_affine_adaptive, estimate_normals_adaptive,
+                       ray_offsets, star_trace)
+from .estimators import (AdaptiveNormalEstimator, AffineNormalEstimator, BaseNormalEstimator,
+                         as_rig, as_scalar_field)
 from .fields import AffineField, NormalField, ScalarField
 from .geometry import StereoRig, pixel_grid, triangulate_grid
 from .kernels import (KernelSpec, PrecomputedKernels, build_kernels, convolve_affine,
@@ -25,7 +28,8 @@ from .kernels import (KernelSpec, PrecomputedKernels, build_kernels, convolve_af
 __version__ = "0.1.0"
 
 __all__ = [
-    "AffineField", "AffineNormalEstimator", "BaseNormalEstimator", "DegenerateSupportError",
+    "AdaptiveNormalEstimator", "AffineField", "AffineNormalEstimator", "StarConfig",
+    "estimate_affine_adaptive", "estimate_normals_adaptive", "ray_offsets", "star_trace", "BaseNormalEstimator", "DegenerateSupportError",
     "KernelSpec", "NativeLibraryError", "NormalField", "PrecomputedKernels", "ScalarField",
     "StereoRig", "as_rig", "as_scalar_field", "build_kernels", "convolve_affine", "edge_map",
     "estimate_affine_direct", "estimate_normals_fixed", "format_kernel_dump",

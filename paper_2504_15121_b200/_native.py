@@ -62,6 +62,9 @@ SIGNATURES = {
     "sn_oriented_points_bits": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P,
                                 _P],
     "sn_passable_bits": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P],
+    "sn_adaptive_workspace_bytes": [_I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
+    "sn_adaptive_points": [_P, _P, _I64, _I64, _I64, _RIGP, _I32, _P, _P, _I32, _I32, _D, _P, _P,
+                           _P, ctypes.c_size_t, _P],
     "sn_cloud_workspace_bytes": [_I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
     "sn_compact_cloud": [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_pipeline": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P],

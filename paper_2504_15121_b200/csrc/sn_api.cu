@@ -403,6 +403,76 @@ int sn_compact_cloud(sn_plan_t* plan, const float* out6, const uint8_t* mask, in
                            frame_offsets, workspace, ws_bytes);
 }
 
+int sn_adaptive_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
+  if (!bytes) return set_error(SN_EINVAL, "bytes out-pointer is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  *bytes = adaptive_workspace_bytes(B, H, W);
+  return SN_OK;
+}
+
+int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                       const sn_rig_t* rig, int32_t n_rays, const int32_t* ray_len,
+                       const int32_t* ray_xy, int32_t stop, int32_t shared_range,
+                       double threshold, float* out6, uint8_t* mask, void* workspace,
+                       size_t ws_bytes, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  // adaptive.py:49-57
+  if (stop != 0 && stop != 1) return set_error(SN_EINVAL, "stop must be 0 (st) or 1 (cd)");
+  if (!(threshold > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
+  if (n_rays < 3) return set_error(SN_EINVAL, "need at least 3 ray directions");
+  if (n_rays > kStarMaxRays) return set_error(SN_EINVAL, "at most %d directions", kStarMaxRays);
+  if (!ray_len || !ray_xy) return set_error(SN_EINVAL, "NULL ray table");
+  static thread_local StarTable tab;
+  tab.n_rays = n_rays;
+  tab.n_keys = 0;
+  int steps = 0;
+  std::unordered_map<int64_t, int> key_of;
+  for (int j = 0; j < n_rays; ++j) {
+    tab.ray_start[j] = steps;
+    if (ray_len[j] < 0) return set_error(SN_EINVAL, "negative ray length");
+    for (int i = 0; i < ray_len[j]; ++i, ++steps) {
+      if (steps >= kStarMaxSteps) return set_error(SN_EINVAL, "at most %d ray steps", kStarMaxSteps);
+      const int vx = ray_xy[2 * steps], vy = ray_xy[2 * steps + 1];
+      if (vx < -32767 || vx > 32767 || vy < -32767 || vy > 32767)
+        return set_error(SN_EINVAL, "ray offset out of range");
+      const int64_t kk = ((int64_t)vx << 32) ^ (uint32_t)vy;
+      auto it = key_of.find(kk);
+      int k;
+      if (it == key_of.end()) {
+        if (tab.n_keys >= kStarMaxKeys)
+          return set_error(SN_EINVAL, "at most %d distinct ray offsets", kStarMaxKeys);
+        k = tab.n_keys++;
+        key_of.emplace(kk, k);
+        tab.key_x[k] = (int16_t)vx;
+        tab.key_y[k] = (int16_t)vy;
+      } else {
+        k = it->second;
+      }
+      tab.step_key[steps] = (int16_t)k;
+    }
+  }
+  tab.ray_start[n_rays] = steps;
+  if (B * H * W == 0) return SN_OK;
+  if (!disp || !out6) return set_error(SN_EINVAL, "NULL buffer");
+  AdaptiveParams ap{};
+  ap.fp.B = B;
+  ap.fp.H = H;
+  ap.fp.W = W;
+  fill_rig(ap.fp, rig);
+  ap.threshold = threshold;
+  ap.baseline = rig->baseline;
+  ap.fxfx = rig->fx * rig->fx;
+  ap.nfxfy = -rig->fx * rig->fy;
+  ap.shared_range = shared_range != 0;
+  DeviceGuard g(plan->device);
+  return run_adaptive(make_ctx(plan, stream), disp, ap, tab, stop, out6, mask, workspace,
+                      ws_bytes);
+}
+
 /* test hook: force the generic (non-TMA) kernel, to cross-check the fast path */
 int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                                const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,

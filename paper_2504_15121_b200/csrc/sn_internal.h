@@ -63,6 +63,28 @@ int run_relabel(const LaunchCtx& ctx, int32_t* labels, int64_t n, int64_t base,
                 const int32_t* keys, const int32_t* vals, const int32_t* n_map, int32_t cap,
                 int32_t* scratch);
 
+// adaptive star-fill (sn_adaptive.cu)
+constexpr int kStarMaxRays = 64, kStarMaxSteps = 2048, kStarKeyWords = 16;
+constexpr int kStarMaxKeys = kStarKeyWords * 32;  // 512 distinct offsets
+struct StarTable {
+  int n_rays, n_keys;
+  int ray_start[kStarMaxRays + 1];  // steps of ray j: [ray_start[j], ray_start[j+1])
+  int16_t step_key[kStarMaxSteps];  // key of each step
+  int16_t key_x[kStarMaxKeys], key_y[kStarMaxKeys];  // keys in first-occurrence order
+};
+struct AdaptiveParams {
+  FixedParams fp;     // rig, shape, point constants (bits / bits_ww for ST)
+  double threshold;   // t (ST) or k (CD)
+  double baseline;
+  double fxfx;        // fx * fx (Python double, geometry.py:197)
+  double nfxfy;       // -fx * fy (geometry.py:199)
+  int shared_range;
+};
+size_t adaptive_workspace_bytes(int64_t B, int64_t H, int64_t W);
+int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& ap,
+                 const StarTable& tab, int stop, float* out6, uint8_t* mask, void* workspace,
+                 size_t ws_bytes);
+
 size_t cloud_workspace_bytes(int64_t B, int64_t H, int64_t W);
 int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
                       int64_t H, int64_t W, float* cloud, int64_t capacity,

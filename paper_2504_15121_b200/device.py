@@ -183,6 +183,38 @@ def pipeline(disparity: torch.Tensor, rig, kernels, threshold: float, *, out=Non
     return out, labels
 
 
+def adaptive_points(disparity: torch.Tensor, rig, config, *, out=None, mask=None,
+                    workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Adaptive star-fill pass (adaptive.py:177-268): ``[B, H, W, 6]`` fp32
+    records with normals over edge-aware star supports (``config`` a
+    ``StarConfig``); ``mask`` (uint8) optionally receives the validity."""
+    from .adaptive import ray_table
+    d = _fp32(_batched(disparity))
+    B, H, W = d.shape
+    dev = d.device
+    out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
+    if mask is not None:
+        mask = _check_out(mask, (B, H, W), torch.uint8, dev, "mask")
+    n = ctypes.c_size_t(0)
+    lib = _native.load()
+    check(lib.sn_adaptive_workspace_bytes(B, H, W, ctypes.byref(n)), "sn_adaptive_workspace_bytes")
+    if workspace is None:
+        workspace = torch.empty(max(1, n.value), dtype=torch.uint8, device=dev)
+    elif workspace.numel() * workspace.element_size() < n.value or workspace.device != dev:
+        raise ValueError(f"workspace must hold >= {n.value} bytes on {dev}")
+    lens, xy = ray_table(config)
+    rs = _native.rig_struct(rig)
+    rc = lib.sn_adaptive_points(_native.plan(dev.index), d.data_ptr(), B, H, W, ctypes.byref(rs),
+                                len(lens), lens.ctypes.data, xy.ctypes.data,
+                                0 if config.stop == "st" else 1, int(bool(config.shared_range)),
+                                float(config.threshold), out.data_ptr(),
+                                mask.data_ptr() if mask is not None else None,
+                                workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                _stream(dev))
+    check(rc, "adaptive_points")
+    return out
+
+
 def compact_cloud(records: torch.Tensor, mask: torch.Tensor):
     """Stream-compact the dense ``[B, H, W, 6]`` records of pixels with a valid
     normal (``mask`` uint8 ``[B, H, W]`` from ``oriented_points(..., mask=)``)

@@ -39,3 +39,16 @@ def cuda_dev():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="session")
+def adaptive_golden():
+    import json
+    z = np.load(GOLDEN / "adaptive_cases.npz", allow_pickle=False)
+    out = {}
+    for n, c in zip([str(v) for v in z["names"]], [str(v) for v in z["configs"]]):
+        pre = f"{n}__"
+        case = {k[len(pre):]: z[k] for k in z.files if k.startswith(pre)}
+        case["config"] = json.loads(c)
+        out[n] = case
+    return out

@@ -81,3 +81,20 @@ def test_label_components_kats():
     assert lab[1, 5] == 4
     assert (lab[~p] == -1).all()
     assert orc.label_components(p, index_offset=100)[1, 5] == 104
+
+
+ADAPTIVE = ["street_cd_d8_s10", "street_st_d8_s10", "street_cd_shared", "street_cd_holes",
+            "street_st_holes", "sphere_cd_d16_s5", "sphere_st_d3_s2", "sphere_cd_d5_s30",
+            "street_cd_s1", "tiny"]
+
+
+@pytest.mark.parametrize("name", ADAPTIVE)
+def test_oracle_adaptive_matches_reference(adaptive_golden, name):
+    """The oracle's star-fill restatement == reference estimate_normals_adaptive
+    (adaptive.py:177-268), bit for bit (same fp64 op order)."""
+    from oracle import stereonorm_oracle as orc
+    c = adaptive_golden[name]
+    fx, fy, u0, v0, b = (float(v) for v in c["rig"])
+    n, ok = orc.estimate_normals_adaptive(c["d"], orc.Rig(fx, fy, u0, v0, b), orc.Star(**c["config"]))
+    assert np.array_equal(ok, c["nmask"])
+    np.testing.assert_array_equal(n[ok], c["normals"][ok])
