@@ -219,6 +219,28 @@ SN_API int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int
                        double threshold, float* out6, uint8_t* mask, void* workspace,
                        size_t ws_bytes, void* stream);
 
+/* Accuracy evaluation on the device (evaluation.py:34-73): per frame, the
+ * unsigned angle map degrees(arccos(|n_est . n_gt|)) over jointly valid
+ * pixels (est normals: 3 floats at the start of each est_stride-float record,
+ * NaN = invalid -- est_stride 6 reads the dense oriented-point record; gt:
+ * [B][H][W][3] double + uint8 mask; extra_mask optional) and its statistics
+ * stats[B][6] = (avg, min, max, lower median, population std, count), NaN
+ * where a frame has no valid pixel.  err_out (optional) receives the map
+ * (NaN invalid).  Device pointers; workspace: sn_eval_workspace_bytes. */
+SN_API int sn_eval_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes);
+SN_API int sn_angular_error(sn_plan_t* plan, const float* est, int32_t est_stride,
+                     const double* gt, const uint8_t* gt_mask, const uint8_t* extra_mask,
+                     int64_t B, int64_t H, int64_t W, double* err_out, double* stats,
+                     void* workspace, size_t ws_bytes, void* stream);
+/* summarize (evaluation.py:58-73) of a given map: values [B][H][W] double,
+ * non-finite = invalid; same stats layout. */
+SN_API int sn_error_stats(sn_plan_t* plan, const double* values, int64_t B, int64_t H,
+                   int64_t W, double* stats, void* workspace, size_t ws_bytes, void* stream);
+SN_API int sn_angular_error_f64(sn_plan_t* plan, const double* est, int32_t est_stride,
+                         const double* gt, const uint8_t* gt_mask, const uint8_t* extra_mask,
+                         int64_t B, int64_t H, int64_t W, double* err_out, double* stats,
+                         void* workspace, size_t ws_bytes, void* stream);
+
 /* Oriented point cloud compaction (cli.py:118-123, the vertices
  * formats.py:170-185 writes): the records of pixels whose normal is valid
  * (mask != 0, as emitted by the fused pass), in raster order over the whole

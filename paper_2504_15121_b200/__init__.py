@@ -20,6 +20,7 @@ from .adaptive import (StarConfig, estimate_affine_adaptive, estimate_normals_ad
                        ray_offsets, star_trace)
 from .estimators import (AdaptiveNormalEstimator, AffineNormalEstimator, BaseNormalEstimator,
                          as_rig, as_scalar_field)
+from .evaluation import ErrorStats, angular_error_map, error_stats, summarize
 from .fields import AffineField, NormalField, ScalarField
 from .geometry import StereoRig, pixel_grid, triangulate_grid
 from .kernels import (KernelSpec, PrecomputedKernels, build_kernels, convolve_affine,
@@ -28,7 +29,7 @@ from .kernels import (KernelSpec, PrecomputedKernels, build_kernels, convolve_af
 __version__ = "0.1.0"
 
 __all__ = [
-    "AdaptiveNormalEstimator", "AffineField", "AffineNormalEstimator", "StarConfig",
+    "AdaptiveNormalEstimator", "ErrorStats", "angular_error_map", "error_stats", "summarize", "AffineField", "AffineNormalEstimator", "StarConfig",
     "estimate_affine_adaptive", "estimate_normals_adaptive", "ray_offsets", "star_trace", "BaseNormalEstimator", "DegenerateSupportError",
     "KernelSpec", "NativeLibraryError", "NormalField", "PrecomputedKernels", "ScalarField",
     "StereoRig", "as_rig", "as_scalar_field", "build_kernels", "convolve_affine", "edge_map",

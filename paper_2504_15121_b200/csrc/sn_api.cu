@@ -473,6 +473,56 @@ int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
                       ws_bytes);
 }
 
+int sn_eval_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
+  if (!bytes) return set_error(SN_EINVAL, "bytes out-pointer is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  *bytes = eval_workspace_bytes(B, H, W);
+  return SN_OK;
+}
+
+int sn_angular_error(sn_plan_t* plan, const float* est, int32_t est_stride, const double* gt,
+                     const uint8_t* gt_mask, const uint8_t* extra_mask, int64_t B, int64_t H,
+                     int64_t W, double* err_out, double* stats, void* workspace, size_t ws_bytes,
+                     void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (est_stride < 3) return set_error(SN_EINVAL, "est_stride must be >= 3");
+  if (H * W == 0) return set_error(SN_EINVAL, "cannot summarize an empty error map");
+  if (B > 0 && (!est || !gt || !gt_mask || !stats)) return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_eval(make_ctx(plan, stream), est, nullptr, est_stride, gt, gt_mask, extra_mask, B, H,
+                  W, err_out, stats, workspace, ws_bytes);
+}
+
+int sn_error_stats(sn_plan_t* plan, const double* values, int64_t B, int64_t H, int64_t W,
+                   double* stats, void* workspace, size_t ws_bytes, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (H * W == 0) return set_error(SN_EINVAL, "cannot summarize an empty error map");
+  if (B > 0 && (!values || !stats)) return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_eval(make_ctx(plan, stream), nullptr, nullptr, 3, nullptr, nullptr, nullptr, B, H, W,
+                  const_cast<double*>(values), stats, workspace, ws_bytes);
+}
+
+int sn_angular_error_f64(sn_plan_t* plan, const double* est, int32_t est_stride, const double* gt,
+                         const uint8_t* gt_mask, const uint8_t* extra_mask, int64_t B, int64_t H,
+                         int64_t W, double* err_out, double* stats, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (est_stride < 3) return set_error(SN_EINVAL, "est_stride must be >= 3");
+  if (H * W == 0) return set_error(SN_EINVAL, "cannot summarize an empty error map");
+  if (B > 0 && (!est || !gt || !gt_mask || !stats)) return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_eval(make_ctx(plan, stream), nullptr, est, est_stride, gt, gt_mask, extra_mask, B, H,
+                  W, err_out, stats, workspace, ws_bytes);
+}
+
 /* test hook: force the generic (non-TMA) kernel, to cross-check the fast path */
 int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                                const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,

@@ -85,6 +85,12 @@ int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& 
                  const StarTable& tab, int stop, float* out6, uint8_t* mask, void* workspace,
                  size_t ws_bytes);
 
+size_t eval_workspace_bytes(int64_t B, int64_t H, int64_t W);
+int run_eval(const LaunchCtx& ctx, const float* est, const double* est_d, int est_stride,
+             const double* gt,
+             const uint8_t* gt_mask, const uint8_t* extra, int64_t B, int64_t H, int64_t W,
+             double* err_out, double* stats, void* workspace, size_t ws_bytes);
+
 size_t cloud_workspace_bytes(int64_t B, int64_t H, int64_t W);
 int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
                       int64_t H, int64_t W, float* cloud, int64_t capacity,

@@ -215,6 +215,62 @@ def adaptive_points(disparity: torch.Tensor, rig, config, *, out=None, mask=None
     return out
 
 
+def angular_error(est: torch.Tensor, gt: torch.Tensor, gt_mask: torch.Tensor, *, mask=None,
+                  want_map: bool = True):
+    """Device accuracy evaluation (evaluation.py:34-73): ``est`` is either the
+    dense record ``[B, H, W, 6]`` (fp32) or normals ``[B, H, W, 3]`` (fp32 or
+    fp64, NaN = invalid); ``gt`` fp64 ``[B, H, W, 3]`` with ``gt_mask`` (bool /
+    uint8).  Returns (angle map fp64 ``[B, H, W]`` NaN-invalid or None,
+    stats fp64 ``[B, 6]`` = avg, min, max, lower median, population std, count)."""
+    if est.dim() == 3:
+        est, gt, gt_mask = est.unsqueeze(0), gt.unsqueeze(0), gt_mask.unsqueeze(0)
+        mask = mask.unsqueeze(0) if mask is not None else None
+    if est.dim() != 4 or est.shape[-1] not in (3, 6):
+        raise ValueError("est must be [B, H, W, 6] records or [B, H, W, 3] normals")
+    est = est.contiguous()
+    B, H, W, stride = est.shape
+    dev = est.device
+    if est.dtype == torch.float64 and stride != 3:
+        raise ValueError("fp64 est must be [B, H, W, 3] normals")
+    gt = _check_out(gt.contiguous(), (B, H, W, 3), torch.float64, dev, "gt")
+    gm = gt_mask.to(torch.uint8).contiguous()
+    em = mask.to(torch.uint8).contiguous() if mask is not None else None
+    n = ctypes.c_size_t(0)
+    lib = _native.load()
+    check(lib.sn_eval_workspace_bytes(B, H, W, ctypes.byref(n)), "sn_eval_workspace_bytes")
+    ws = torch.empty(max(1, n.value), dtype=torch.uint8, device=dev)
+    err = torch.empty((B, H, W), dtype=torch.float64, device=dev) if want_map else None
+    stats = torch.empty((B, 6), dtype=torch.float64, device=dev)
+    fn = lib.sn_angular_error_f64 if est.dtype == torch.float64 else lib.sn_angular_error
+    if est.dtype not in (torch.float32, torch.float64):
+        raise ValueError("est must be float32 or float64")
+    rc = fn(_native.plan(dev.index), est.data_ptr(), stride, gt.data_ptr(), gm.data_ptr(),
+            em.data_ptr() if em is not None else None, B, H, W,
+            err.data_ptr() if err is not None else None, stats.data_ptr(), ws.data_ptr(),
+            n.value, _stream(dev))
+    check(rc, "angular_error")
+    return err, stats
+
+
+def error_stats(values: torch.Tensor) -> torch.Tensor:
+    """summarize (evaluation.py:58-73) of fp64 maps ``[B, H, W]`` (non-finite =
+    invalid): ``[B, 6]`` = avg, min, max, lower median, population std, count."""
+    v = _batched(values, "values")
+    if v.dtype != torch.float64:
+        raise ValueError("values must be float64")
+    B, H, W = v.shape
+    dev = v.device
+    n = ctypes.c_size_t(0)
+    lib = _native.load()
+    check(lib.sn_eval_workspace_bytes(B, H, W, ctypes.byref(n)), "sn_eval_workspace_bytes")
+    ws = torch.empty(max(1, n.value), dtype=torch.uint8, device=dev)
+    stats = torch.empty((B, 6), dtype=torch.float64, device=dev)
+    rc = lib.sn_error_stats(_native.plan(dev.index), v.data_ptr(), B, H, W, stats.data_ptr(),
+                            ws.data_ptr(), n.value, _stream(dev))
+    check(rc, "error_stats")
+    return stats
+
+
 def compact_cloud(records: torch.Tensor, mask: torch.Tensor):
     """Stream-compact the dense ``[B, H, W, 6]`` records of pixels with a valid
     normal (``mask`` uint8 ``[B, H, W]`` from ``oriented_points(..., mask=)``)
