@@ -254,6 +254,37 @@ SN_API int sn_compact_cloud(sn_plan_t* plan, const float* out6, const uint8_t* m
                      int64_t H, int64_t W, float* cloud, int64_t capacity,
                      int64_t* frame_offsets, void* workspace, size_t ws_bytes, void* stream);
 
+/* Device input codecs (formats.py).  The container (PNG zlib stream, PFM
+ * header) is parsed on the host; these take the raw sample payload already
+ * in device memory.
+ *
+ * sn_dequant_png16: read_disparity_png16 (formats.py:133-150) per sample:
+ * d = (raw - 1.0) / scale in fp64, raw == invalid -> NaN (invalid = -1: no
+ * invalid value).  out_f64 gets the reference's value bit-exactly, out_f32
+ * that value rounded once; either may be NULL. */
+SN_API int sn_dequant_png16(sn_plan_t* plan, const uint16_t* raw, int64_t B, int64_t H, int64_t W,
+                     double scale, int32_t invalid, float* out_f32, double* out_f64,
+                     void* stream);
+
+/* sn_decode_pfm: the payload step of read_pfm / read_pfm_normals
+ * (formats.py:84-113): B payloads of H x W x channels 4-byte floats, bottom
+ * row first, big-endian when the header scale is positive -> out [B][H][W]
+ * (x channels) native fp32, top row first.  Non-finite samples stay as they
+ * are (they mark invalid pixels, fields.py ScalarField.from_array). */
+SN_API int sn_decode_pfm(sn_plan_t* plan, const void* payload, int64_t B, int64_t H, int64_t W,
+                  int32_t channels, int32_t big_endian, float* out, void* stream);
+
+/* sn_oriented_points with a 16-bit PNG disparity payload read directly by
+ * the fused pass (read_disparity_png16 + estimate_normals_fixed +
+ * triangulate_grid): 2 B/px in instead of 4.  Needs a centred square kernel
+ * (3..17), W % 8 == 0, 16-byte aligned buffers and 2^-100 <= |scale| <=
+ * 2^100; SN_EINVAL otherwise (dequantise with sn_dequant_png16 and use
+ * sn_oriented_points_f64). */
+SN_API int sn_oriented_points_png16(sn_plan_t* plan, const uint16_t* raw, int64_t B, int64_t H,
+                             int64_t W, double scale, int32_t invalid, const sn_rig_t* rig,
+                             const int32_t* offsets_xy, int32_t n_off, float* out6,
+                             uint8_t* mask, void* stream);
+
 /* Test hook: the fixed pass forced onto the generic (non-TMA) kernel, used to
  * cross-check the TMA fast path on identical inputs. */
 SN_API int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,

@@ -22,6 +22,8 @@ from .estimators import (AdaptiveNormalEstimator, AffineNormalEstimator, BaseNor
                          as_rig, as_scalar_field)
 from .evaluation import ErrorStats, angular_error_map, error_stats, summarize
 from .fields import AffineField, NormalField, ScalarField
+from .formats import (FormatError, read_disparity_png16, read_pfm, read_pfm_normals,
+                      write_disparity_png16, write_pfm, write_pfm_normals)
 from .geometry import StereoRig, pixel_grid, triangulate_grid
 from .kernels import (KernelSpec, PrecomputedKernels, build_kernels, convolve_affine,
                       estimate_affine_direct, estimate_normals_fixed, format_kernel_dump)
@@ -31,6 +33,8 @@ __version__ = "0.1.0"
 __all__ = [
     "AdaptiveNormalEstimator", "ErrorStats", "angular_error_map", "error_stats", "summarize", "AffineField", "AffineNormalEstimator", "StarConfig",
     "estimate_affine_adaptive", "estimate_normals_adaptive", "ray_offsets", "star_trace", "BaseNormalEstimator", "DegenerateSupportError",
+    "FormatError", "read_disparity_png16", "read_pfm", "read_pfm_normals",
+    "write_disparity_png16", "write_pfm", "write_pfm_normals",
     "KernelSpec", "NativeLibraryError", "NormalField", "PrecomputedKernels", "ScalarField",
     "StereoRig", "as_rig", "as_scalar_field", "build_kernels", "convolve_affine", "edge_map",
     "estimate_affine_direct", "estimate_normals_fixed", "format_kernel_dump",

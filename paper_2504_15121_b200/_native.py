@@ -70,6 +70,10 @@ SIGNATURES = {
     "sn_error_stats": [_P, _P, _I64, _I64, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_angular_error_f64": [_P, _P, _I32, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P,
                              ctypes.c_size_t, _P],
+    "sn_dequant_png16": [_P, _P, _I64, _I64, _I64, _D, _I32, _P, _P, _P],
+    "sn_decode_pfm": [_P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P],
+    "sn_oriented_points_png16": [_P, _P, _I64, _I64, _I64, _D, _I32, _RIGP, _P, _I32, _P, _P,
+                                 _P],
     "sn_cloud_workspace_bytes": [_I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
     "sn_compact_cloud": [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_pipeline": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P],

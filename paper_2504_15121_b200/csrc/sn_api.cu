@@ -381,6 +381,75 @@ int sn_passable_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, i
   return run_passable_bits(make_ctx(plan, stream), disp, p, bits);
 }
 
+static int check_png16(double scale, int32_t invalid) {
+  // nonzero values (raw - 1) / scale, |raw - 1| <= 65535, stay normal fp32
+  const double a = fabs(scale);
+  if (!(a >= 7.888609052210118e-31 && a <= 1.2676506002282294e30))  // 2^-100 .. 2^100
+    return set_error(SN_EINVAL, "PNG16 scale must be finite with 2^-100 <= |scale| <= 2^100");
+  if (invalid < -1 || invalid > 0xFFFF)
+    return set_error(SN_EINVAL, "invalid_value must be a 16-bit sample or -1 (none)");
+  return SN_OK;
+}
+
+int sn_oriented_points_png16(sn_plan_t* plan, const uint16_t* raw, int64_t B, int64_t H,
+                             int64_t W, double scale, int32_t invalid, const sn_rig_t* rig,
+                             const int32_t* offsets_xy, int32_t n_off, float* out6,
+                             uint8_t* mask, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  if ((rc = check_png16(scale, invalid))) return rc;
+  sn_moments_t m;
+  static thread_local OffsetTable tab;
+  if ((rc = prepare(offsets_xy, n_off, m, tab))) return rc;
+  if (B * H * W > 0 && (!raw || !out6)) return set_error(SN_EINVAL, "NULL buffer");
+  FixedParams p{};
+  p.B = B;
+  p.H = H;
+  p.W = W;
+  fill_rig(p, rig);
+  fill_moments(p, m);
+  p.png_scale = scale;
+  p.png_rcp = png16_rcp(scale);
+  p.png_rcp_f = (float)(1.0 / scale);
+  p.png_sign = scale > 0 ? 1 : -1;
+  p.png_invalid = invalid;
+  DeviceGuard g(plan->device);
+  return run_fixed_png16(make_ctx(plan, stream), raw, p, m, out6, mask);
+}
+
+int sn_dequant_png16(sn_plan_t* plan, const uint16_t* raw, int64_t B, int64_t H, int64_t W,
+                     double scale, int32_t invalid, float* out_f32, double* out_f64,
+                     void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (!(scale == scale) || scale == 0.0 || fabs(scale) > 1.7976931348623157e308)
+    return set_error(SN_EINVAL, "PNG16 scale must be finite and nonzero");
+  if (invalid < -1 || invalid > 0xFFFF)
+    return set_error(SN_EINVAL, "invalid_value must be a 16-bit sample or -1 (none)");
+  if (B * H * W > 0 && (!raw || (!out_f32 && !out_f64)))
+    return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_dequant_png16(make_ctx(plan, stream), raw, B * H * W, invalid, scale, out_f32,
+                           out_f64);
+}
+
+int sn_decode_pfm(sn_plan_t* plan, const void* payload, int64_t B, int64_t H, int64_t W,
+                  int32_t channels, int32_t big_endian, float* out, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (channels != 1 && channels != 3) return set_error(SN_EINVAL, "PFM has 1 or 3 channels");
+  if (B * H * W > 0 && (!payload || !out)) return set_error(SN_EINVAL, "NULL buffer");
+  if (reinterpret_cast<uintptr_t>(payload) % 4 || reinterpret_cast<uintptr_t>(out) % 4)
+    return set_error(SN_EINVAL, "PFM buffers must be 4-byte aligned");
+  DeviceGuard g(plan->device);
+  return run_decode_pfm(make_ctx(plan, stream), payload, B, H, W * channels, big_endian != 0,
+                        out);
+}
+
 int sn_cloud_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
   if (!bytes) return set_error(SN_EINVAL, "bytes out-pointer is NULL");
   int rc = check_shape(B, H, W);

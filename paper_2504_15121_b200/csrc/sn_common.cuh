@@ -33,6 +33,32 @@ struct FixedParams {
   int pred_exact;  // every predicate decision on the fp64 path (filter out of range)
   double t;        // ST threshold
   float t_f, fxb_pf;  // fp32 threshold / fx*b for the predicate filter
+  // 16-bit PNG disparity input (formats.py:133-150): d = (raw - 1) / scale,
+  // raw == invalid -> NaN
+  double png_scale, png_rcp;  // png_rcp = RN(1 / scale), 0 = divide
+  float png_rcp_f;            // (float)RN(1 / scale)
+  int png_invalid, png_sign;  // png_sign = sign(scale)
+};
+
+// (raw - 1) / scale correctly rounded (the reference's fp64 division,
+// formats.py:148).  With rcp = RN(1/scale): q = RN(a rcp) is within 1 ulp of
+// a/scale, r = a - q scale is exact (fma), and q + r rcp rounds to RN(a/scale)
+// (Markstein's theorem) as long as nothing over/underflows -- guaranteed for
+// |a| <= 65535 and 2^-100 <= |scale| <= 2^100 (the host passes rcp = 0
+// outside that range: plain division).  4 fp64 ops instead of a DDIV sequence.
+__device__ __forceinline__ double png16_value(uint32_t raw, int invalid, double scale,
+                                              double rcp) {
+  if ((int)raw == invalid) return __longlong_as_double(0x7ff8000000000000ll);
+  const double a = (double)raw - 1.0;
+  if (rcp == 0.0) return __ddiv_rn(a, scale);
+  const double q = __dmul_rn(a, rcp);
+  const double r = __fma_rn(-q, scale, a);
+  return __fma_rn(r, rcp, q);
+}
+
+// a 16-bit quantised disparity sample (the fused pass's third input type)
+struct Png16 {
+  uint16_t raw;
 };
 
 __device__ __forceinline__ float rcp_ftz(float x) {

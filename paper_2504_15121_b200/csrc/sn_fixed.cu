@@ -114,6 +114,65 @@ __device__ __forceinline__ bool small_t<float>(float v) {
   return (__float_as_uint(v) & 0x7fffffffu) <= kBigBits;
 }
 
+// disparity value of an input sample in fp64 (PNG16: the reference's
+// (raw - 1.0) / scale, formats.py:147-149, invalid raw -> NaN)
+template <typename T>
+__device__ __forceinline__ double dval(T x, const FixedParams&) {
+  return (double)x;
+}
+template <>
+__device__ __forceinline__ double dval<Png16>(Png16 x, const FixedParams& p) {
+  return png16_value(x.raw, p.png_invalid, p.png_scale, p.png_rcp);
+}
+
+// the value the sliding sums accumulate.  PNG16 sums the integers raw - 1
+// (exact, never "big") and scales U, V by 1/scale once per pixel: the sums of
+// d = (raw - 1) / scale then carry one rounding instead of one per sample
+template <typename T>
+__device__ __forceinline__ double sval(T x, const FixedParams& p) {
+  return dval(x, p);
+}
+template <>
+__device__ __forceinline__ double sval<Png16>(Png16 x, const FixedParams&) {
+  // raw - 1 exactly: (2^52 + raw) - (2^52 + 1), one DADD instead of a
+  // conversion.  Invalid samples keep their (finite, exact) value: pass V
+  // flags them from the integer, and only windows that hold one -- invalid
+  // anyway -- see it in their sums
+  return __dsub_rn(__hiloint2double(0x43300000, (int)x.raw), 4503599627370497.0);
+}
+
+// the fp32 epilogue's view of the centre sample: d rounded to fp32 and the
+// exact "valid and d > 0" test.  PNG16: (raw - 1) * RN32(1/scale) (within ~1
+// fp32 ulp of d; exact for power-of-two scales), and d > 0 decided on the
+// integer: raw != invalid and sign(raw - 1) == sign(scale)
+template <typename T>
+__device__ __forceinline__ float dflt(T x, const FixedParams& p) {
+  return (float)dval(x, p);
+}
+template <>
+__device__ __forceinline__ float dflt<Png16>(Png16 x, const FixedParams& p) {
+  // raw - 1 exactly: (2^23 + raw) - (2^23 + 1), an FADD instead of an I2F
+  const float a = __fsub_rn(__int_as_float(0x4b000000 | (int)x.raw), 8388609.0f);
+  const float v = __fmul_rn(a, p.png_rcp_f);
+  return (int)x.raw == p.png_invalid ? __int_as_float(0x7fc00000) : v;
+}
+template <typename T>
+__device__ __forceinline__ bool dpos(T x, const FixedParams& p) {
+  return dval(x, p) > 0.0;
+}
+template <>
+__device__ __forceinline__ bool dpos<Png16>(Png16 x, const FixedParams& p) {
+  // the caller's window test already excludes raw == invalid (the centre is
+  // in its own support): only the sign of (raw - 1) / scale is left
+  return ((int)x.raw - 1) * p.png_sign > 0;
+}
+
+// inputs whose records take the fp32 epilogue: fp32 disparities, and PNG16
+// ones (the host admits only scales that keep every nonzero value in the
+// fp32 normal range; d is rounded to fp32 once, ~6e-8 relative)
+template <typename T>
+constexpr bool kF32Epi = sizeof(T) <= 4;
+
 // normal from the exact sums, fp32 after one rounding of U and V: the
 // components are U fx, V fy and V dv + U du - alpha d, each bounded by ~|n|
 // (n . (du, dv, fx) = -alpha d fx for a camera-facing normal), so fp32 adds
@@ -254,7 +313,8 @@ __device__ __forceinline__ int tile_x0(int x0) {
 // idle lanes beyond NC.
 template <int R, typename T>
 __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int H, int W, int h,
-                                       int c, bool unit, double2* CR, uint32_t* fl) {
+                                       int c, bool unit, double2* CR, uint32_t* fl,
+                                       const FixedParams& p) {
   using Cfg = FastCfg<R, T>;
   constexpr int BW = Cfg::BW;
   // all operands live in shared memory: let the compiler emit LDS/STS
@@ -270,6 +330,7 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   const T* col = in + r0 * BW + c + sh;
   T raw[NV];
   bool all_small = true;  // every sample finite with |v| <= 2^40 (sliding sums exact)
+  uint32_t png_inv = 0;   // PNG16: bit i = sample i is the invalid value
   if (unit) {
     if constexpr (sizeof(T) == 4) {
       uint32_t mx = 0;
@@ -279,16 +340,22 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
         mx = max(mx, __float_as_uint(raw[i]) & 0x7fffffffu);
       }
       all_small = mx <= kBigBits;
+    } else if constexpr (sizeof(T) == 2) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        raw[i] = col[i * BW];
+        png_inv |= ((int)raw[i].raw == p.png_invalid ? 1u : 0u) << i;
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
         raw[i] = col[i * BW];
-        all_small &= small_t(raw[i]);
+        all_small &= fabs(sval(raw[i], p)) <= 1099511627776.0;  // 2^40, NaN fails
       }
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) raw[i] = (T)0;
+    for (int i = 0; i < NV; ++i) raw[i] = T{};
   }
   if (unit) {
     // rows of the unit inside the image
@@ -297,19 +364,19 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
     if ((unsigned)gx < (unsigned)W && hi > lo) inside = (uint32_t)(((1ull << (hi - lo)) - 1ull) << lo);
     double v[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = (double)raw[i];
+    for (int i = 0; i < NV; ++i) v[i] = sval(raw[i], p);
     constexpr uint32_t kAll = (NV >= 32) ? 0xffffffffu : ((1u << NV) - 1u);
-    uint32_t fin = kAll;
+    uint32_t fin = kAll & ~png_inv;
     bool big = false;
     if (!all_small) {
       // rare: non-finite (zeroed so the sliding sums stay finite) or huge samples
       fin = 0;
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
-        const bool f = finite_t(raw[i]);
+        const bool f = finite_d(v[i]);
         fin |= (f ? 1u : 0u) << i;
+        big |= f && !(fabs(v[i]) <= 1099511627776.0);
         if (!f) v[i] = 0.0;
-        big |= f && !small_t(raw[i]);
       }
     }
     const uint32_t invb = ~(fin & inside);
@@ -433,26 +500,35 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
       Vs[j] = V;
     }
   }
-  // depths zf = fxb * rcp(d) of the run's pixels (zc[1 .. kRun])
-  float zc[kRun + 2];
-  if constexpr (sizeof(T) == 4) {
+  if constexpr (sizeof(T) == 2) {  // PNG16: integer sums -> disparity sums
 #pragma unroll
-    for (int j = 1; j <= kRun; ++j) zc[j] = __fmul_rn(p.fxb_f, rcp_ftz((float)drow[j - 1]));
+    for (int j = 0; j < kRun; ++j) {
+      Us[j] *= p.png_rcp;
+      Vs[j] *= p.png_rcp;
+    }
+  }
+  // depths zf = fxb * rcp(d) of the run's pixels (zc[1 .. kRun])
+  float zc[kRun + 2], df[kRun];
+  if constexpr (kF32Epi<T>) {
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) {
+      df[j] = dflt(drow[j], p);
+      zc[j + 1] = __fmul_rn(p.fxb_f, rcp_ftz(df[j]));
+    }
   }
   float o[12];
 #pragma unroll
   for (int j = 0; j < kRun; j += 2) {
-    const T d0 = drow[j], d1 = drow[j + 1];
-    const bool ok0 = (((win >> j) & 1u) == 0u) && (d0 > (T)0);
-    const bool ok1 = (((win >> (j + 1)) & 1u) == 0u) && (d1 > (T)0);
+    const bool ok0 = (((win >> j) & 1u) == 0u) && dpos(drow[j], p);
+    const bool ok1 = (((win >> (j + 1)) & 1u) == 0u) && dpos(drow[j + 1], p);
     validbits |= ((ok0 ? 1u : 0u) | (ok1 ? 2u : 0u)) << j;
-    if constexpr (sizeof(T) == 4) {
-      records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], (float)d0, (float)d1,
+    if constexpr (kF32Epi<T>) {
+      records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], df[j], df[j + 1],
                    make_float2(zc[j + 1], zc[j + 2]), ok0, ok1, du_hi + (float)j, dv_f, p, o);
     } else {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const double dcv = (double)(e ? d1 : d0);
+        const double dcv = dval(drow[j + e], p);
         const double du = (double)(xb + j + e) - p.u0;
         float* r = o + 6 * e;
         point_from_disparity_f64(dcv, du, dv, p, r[0], r[1], r[2]);
@@ -476,8 +552,17 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   }
   if (mask_out != nullptr && yg < H) {
     uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
+    if (xb + kRun <= W && (reinterpret_cast<uintptr_t>(mrow) & 7u) == 0) {
+      // one 8-byte store: bit j -> byte j
+      const uint32_t lo = (validbits & 1u) | ((validbits & 2u) << 7) | ((validbits & 4u) << 14) |
+                          ((validbits & 8u) << 21);
+      const uint32_t hb = validbits >> 4;
+      const uint32_t hi = (hb & 1u) | ((hb & 2u) << 7) | ((hb & 4u) << 14) | ((hb & 8u) << 21);
+      *reinterpret_cast<uint2*>(mrow) = make_uint2(lo, hi);
+    } else {
 #pragma unroll 1
-    for (int j = 0; j < kRun && xb + j < W; ++j) mrow[j] = (uint8_t)((validbits >> j) & 1u);
+      for (int j = 0; j < kRun && xb + j < W; ++j) mrow[j] = (uint8_t)((validbits >> j) & 1u);
+    }
   }
 }
 
@@ -538,7 +623,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     const T* in = reinterpret_cast<const T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
     mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
-    pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl);
+    pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
     // staging of the previous item consumed by its TMA stores (issued by warp 8)
     if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait_read0();
     __syncthreads();
@@ -630,7 +715,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       mbar_wait(in_full + si, (uint32_t)(n / PC::kIn) & 1u);
       mbar_wait(cr_empty + ci, ((uint32_t)(n / PC::kCr) & 1u) ^ 1u);
       pass_v<R, float>(in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, H, W, h, c, unit,
-                       cr_slot(ci), fl_slot(ci));
+                       cr_slot(ci), fl_slot(ci), p);
       mbar_arrive(cr_full + ci);
     }
   } else if (tid < kPipeV + kPipeH) {
@@ -761,7 +846,9 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
   using Cfg = FastCfg<R, T>;
   CUtensorMap in_map, out_map;
   const CUtensorMapDataType dt =
-      sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+      sizeof(T) == 4   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+      : sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                       : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   {
     cuuint64_t dims[3] = {(cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.B};
     cuuint64_t strides[2] = {(cuuint64_t)(p.W * sizeof(T)), (cuuint64_t)(p.W * p.H * sizeof(T))};
@@ -886,6 +973,22 @@ int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const s
 template int run_fixed<float>(const LaunchCtx&, const float*, const FixedParams&,
                               const sn_moments_t&, const OffsetTable&, float*, uint8_t*, double*,
                               double*, bool, int);
+// 16-bit PNG input: the fast (square, aligned) kernel only
+int run_fixed_png16(const LaunchCtx& ctx, const uint16_t* raw, const FixedParams& p,
+                    const sn_moments_t& m, float* out6, uint8_t* mask) {
+  if (p.B * p.H * p.W == 0) return SN_OK;
+  const bool aligned = (reinterpret_cast<uintptr_t>(raw) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(out6) % 16 == 0) && (p.W % 8 == 0) &&
+                       p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
+  if (m.square_r < 1 || m.square_r > 8 || !aligned)
+    return set_error(SN_EINVAL,
+                     "16-bit input needs a centred square kernel (3..17), W % 8 == 0 and "
+                     "16-byte aligned buffers; dequantise with sn_dequant_png16 otherwise");
+  const int rc = dispatch_square<Png16>(m.square_r, ctx, reinterpret_cast<const Png16*>(raw), p,
+                                        out6, mask);
+  return rc >= 0 ? rc : set_error(SN_EINVAL, "batch too large");
+}
+
 template int run_fixed<double>(const LaunchCtx&, const double*, const FixedParams&,
                                const sn_moments_t&, const OffsetTable&, float*, uint8_t*, double*,
                                double*, bool, int);

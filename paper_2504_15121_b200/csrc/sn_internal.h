@@ -91,6 +91,19 @@ int run_eval(const LaunchCtx& ctx, const float* est, const double* est_d, int es
              const uint8_t* gt_mask, const uint8_t* extra, int64_t B, int64_t H, int64_t W,
              double* err_out, double* stats, void* workspace, size_t ws_bytes);
 
+// RN(1/scale) for png16_value's fast division, 0 (divide) outside
+// 2^-100 <= |scale| <= 2^100
+inline double png16_rcp(double scale) {
+  const double a = scale < 0 ? -scale : scale;
+  return (a >= 7.888609052210118e-31 && a <= 1.2676506002282294e30) ? 1.0 / scale : 0.0;
+}
+int run_fixed_png16(const LaunchCtx& ctx, const uint16_t* raw, const FixedParams& p,
+                    const sn_moments_t& m, float* out6, uint8_t* mask);
+int run_dequant_png16(const LaunchCtx& ctx, const uint16_t* raw, int64_t n, int invalid,
+                      double scale, float* out32, double* out64);
+int run_decode_pfm(const LaunchCtx& ctx, const void* payload, int64_t B, int64_t H, int64_t L,
+                   bool big_endian, float* out);
+
 size_t cloud_workspace_bytes(int64_t B, int64_t H, int64_t W);
 int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
                       int64_t H, int64_t W, float* cloud, int64_t capacity,

@@ -305,6 +305,88 @@ def compact_cloud(records: torch.Tensor, mask: torch.Tensor):
     return cloud, offsets.cpu()
 
 
+def _raw16(raw: torch.Tensor) -> torch.Tensor:
+    if raw.dtype not in (torch.uint16, torch.int16):
+        raise ValueError(f"PNG16 samples must be uint16 (or int16 bits), got {raw.dtype}")
+    if raw.dim() == 2:
+        raw = raw.unsqueeze(0)
+    if raw.dim() != 3:
+        raise ValueError("PNG16 samples must be [H, W] or [B, H, W]")
+    if not raw.is_cuda:
+        raise ValueError("PNG16 samples must be on a CUDA device")
+    return raw.contiguous()
+
+
+def _invalid16(invalid_value) -> int:
+    return -1 if invalid_value is None else int(invalid_value)
+
+
+def dequant_png16(raw: torch.Tensor, scale: float = 256.0, invalid_value: int | None = 0, *,
+                  dtype=torch.float64, out=None) -> torch.Tensor:
+    """read_disparity_png16's sample step (formats.py:133-150) on the device:
+    ``d = (raw - 1) / scale`` in fp64, ``raw == invalid_value`` -> NaN.
+    float64 output is the reference's value bit for bit, float32 that value
+    rounded once.  Returns ``[B, H, W]``."""
+    r = _raw16(raw)
+    B, H, W = r.shape
+    dev = r.device
+    if dtype not in (torch.float32, torch.float64):
+        raise ValueError("dtype must be float32 or float64")
+    out = _check_out(out, (B, H, W), dtype, dev, "out")
+    p32 = out.data_ptr() if dtype == torch.float32 else None
+    p64 = out.data_ptr() if dtype == torch.float64 else None
+    rc = _native.load().sn_dequant_png16(_native.plan(dev.index), r.data_ptr(), B, H, W,
+                                         float(scale), _invalid16(invalid_value), p32, p64,
+                                         _stream(dev))
+    check(rc, "dequant_png16")
+    return out
+
+
+def decode_pfm(payload: torch.Tensor, height: int, width: int, channels: int = 1,
+               big_endian: bool = False, *, out=None) -> torch.Tensor:
+    """The PFM payload step (formats.py:84-102) on the device: ``payload`` is
+    ``[B, H*W*C*4]`` (or flat) uint8 bytes of B images, bottom row first;
+    returns native float32 ``[B, H, W]`` (``[B, H, W, 3]`` for C = 3), top row
+    first."""
+    if payload.dtype != torch.uint8 or not payload.is_cuda:
+        raise ValueError("payload must be a CUDA uint8 tensor")
+    per = int(height) * int(width) * int(channels) * 4
+    flat = payload.contiguous().reshape(-1)
+    if per == 0 or flat.numel() % per:
+        raise ValueError(f"payload of {flat.numel()} bytes is not a whole number of "
+                         f"{height}x{width}x{channels} PFM images")
+    B = flat.numel() // per
+    dev = flat.device
+    shape = (B, height, width) + ((3,) if channels == 3 else ())
+    out = _check_out(out, shape, torch.float32, dev, "out")
+    rc = _native.load().sn_decode_pfm(_native.plan(dev.index), flat.data_ptr(), B, int(height),
+                                      int(width), int(channels), 1 if big_endian else 0,
+                                      out.data_ptr(), _stream(dev))
+    check(rc, "decode_pfm")
+    return out
+
+
+def oriented_points_png16(raw: torch.Tensor, rig, kernels=9, *, scale: float = 256.0,
+                          invalid_value: int | None = 0, out=None, mask=None) -> torch.Tensor:
+    """``oriented_points`` reading 16-bit PNG samples directly (2 B/px): the
+    fused pass dequantises on load exactly as read_disparity_png16 does.
+    Needs a centred square kernel, W % 8 == 0 and 2^-100 <= |scale| <= 2^100."""
+    r = _raw16(raw)
+    B, H, W = r.shape
+    dev = r.device
+    out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
+    if mask is not None:
+        mask = _check_out(mask, (B, H, W), torch.uint8, dev, "mask")
+    off = _offsets_of(kernels)
+    rs = _native.rig_struct(rig)
+    rc = _native.load().sn_oriented_points_png16(
+        _native.plan(dev.index), r.data_ptr(), B, H, W, float(scale), _invalid16(invalid_value),
+        ctypes.byref(rs), off.ctypes.data, len(off), out.data_ptr(),
+        mask.data_ptr() if mask is not None else None, _stream(dev))
+    check(rc, "oriented_points_png16")
+    return out
+
+
 def affine(disparity: torch.Tensor, kernels, *, a1=None, a2=None, mask=None):
     """convolve_affine on the device: (a1, a2, mask) fp64/fp64/uint8 ``[B, H, W]``."""
     d = _batched(disparity)

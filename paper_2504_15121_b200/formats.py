@@ -1,4 +1,14 @@
-"""Oriented PLY output of the dense cloud.
+"""Readers and writers either side of the hot path.
+
+Inputs (f3): PFM and 16-bit PNG disparity files.  The container is parsed on
+the host -- the PFM header (formats.py:55-81) here, the PNG zlib stream by
+PIL as in the reference (formats.py:133-150) -- and the per-sample work runs
+on the device (``device.decode_pfm`` / ``device.dequant_png16``) after one
+copy of the raw payload.  ``read_pfm`` / ``read_disparity_png16`` keep the
+reference's signatures, ScalarField results and FormatError behaviour; the
+``*_device`` variants return the CUDA tensor the fused pass consumes.
+
+Output (f2): oriented PLY.
 
 Byte-compatible with the reference writer ``write_ply_oriented``
 (formats.py:167-211): header ``ply`` / ``format binary_little_endian 1.0``
@@ -10,7 +20,172 @@ produces the binary body, so ``ply_from_vertices`` only prepends the header.
 
 from __future__ import annotations
 
+import io
+
 import numpy as np
+import torch
+
+from .fields import NormalField, ScalarField
+
+
+class FormatError(Exception):
+    """Malformed file content; ``offset`` is the parse position if known
+    (formats.py:40-47)."""
+
+    def __init__(self, message: str, offset: int | None = None):
+        if offset is not None:
+            message = f"{message} (at byte {offset})"
+        super().__init__(message)
+        self.offset = offset
+
+
+# --------------------------------------------------------------------------
+# PFM (formats.py:55-113)
+
+_WS = frozenset(b" \t\n\r\x0b\x0c")
+
+
+def _pfm_header(data: bytes):
+    """(magic, width, height, scale, payload offset): four whitespace-separated
+    tokens, exactly one whitespace byte before the payload (formats.py:55-81)."""
+    pos, n, tokens = 0, len(data), []
+    while len(tokens) < 4:
+        while pos < n and data[pos] in _WS:
+            pos += 1
+        start = pos
+        while pos < n and data[pos] not in _WS:
+            pos += 1
+        if pos == start:
+            raise FormatError("truncated PFM header", offset=pos)
+        tokens.append(data[start:pos])
+    if pos >= n or data[pos] not in _WS:
+        raise FormatError("missing whitespace after PFM scale", offset=pos)
+    pos += 1
+    magic = tokens[0]
+    if magic not in (b"Pf", b"PF"):
+        raise FormatError(f"bad PFM magic {magic!r}", offset=0)
+    try:
+        width, height = int(tokens[1]), int(tokens[2])
+        scale = float(tokens[3])
+    except ValueError as exc:
+        raise FormatError(f"bad PFM header field: {exc}") from None
+    if width <= 0 or height <= 0:
+        raise FormatError(f"bad PFM dimensions {width}x{height}")
+    if scale == 0.0:
+        raise FormatError("PFM scale must be nonzero")
+    return magic, width, height, scale, pos
+
+
+def read_pfm_device(data: bytes, magic: bytes = b"Pf", device=None) -> torch.Tensor:
+    """Decode a PFM on the device: float32 ``[H, W]`` (``[H, W, 3]`` for
+    ``PF``), top row first, NaN/inf samples kept (they mark invalid pixels)."""
+    magic_, width, height, scale, pos = _pfm_header(data)
+    if magic_ != magic:
+        kind = "grayscale 'Pf'" if magic == b"Pf" else "3-channel 'PF'"
+        raise FormatError(f"expected {kind} PFM, got {magic_.decode()!r}", offset=0)
+    ch = 3 if magic == b"PF" else 1
+    need = width * height * ch * 4
+    have = len(data) - pos
+    if have < need:
+        raise FormatError(f"truncated PFM payload: need {need} bytes, have {have}",
+                          offset=pos + have)
+    from . import device as _dev
+    from ._host import current_device
+    dev = torch.device(device) if device is not None else current_device()
+    host = torch.frombuffer(bytearray(data[pos:pos + need]), dtype=torch.uint8)
+    out = _dev.decode_pfm(host.to(dev), height, width, ch, big_endian=scale > 0)
+    return out[0]
+
+
+def read_pfm(data: bytes) -> ScalarField:
+    """Grayscale PFM to a scalar field; non-finite samples become invalid
+    (formats.py:105-108)."""
+    return ScalarField.from_array(read_pfm_device(data, b"Pf").double().cpu().numpy())
+
+
+def read_pfm_normals(data: bytes) -> NormalField:
+    """3-channel PFM to a normal field (formats.py:118-121)."""
+    return NormalField.from_array(read_pfm_device(data, b"PF").double().cpu().numpy())
+
+
+def write_pfm(field: ScalarField) -> bytes:
+    """Little-endian grayscale PFM, invalid pixels as NaN (formats.py:111-115)."""
+    header = f"Pf\n{field.width} {field.height}\n-1.0\n".encode("ascii")
+    return header + np.ascontiguousarray(field.values[::-1].astype("<f4")).tobytes()
+
+
+def write_pfm_normals(field: NormalField) -> bytes:
+    """3-channel little-endian PFM (formats.py:124-127)."""
+    header = f"PF\n{field.width} {field.height}\n-1.0\n".encode("ascii")
+    return header + np.ascontiguousarray(field.vectors[::-1].astype("<f4")).tobytes()
+
+
+# --------------------------------------------------------------------------
+# 16-bit disparity PNG (formats.py:130-162)
+
+def _png16_samples(data: bytes) -> np.ndarray:
+    """The PNG container (zlib + filters) decoded by PIL, as the reference
+    does; returns the raw 16-bit samples."""
+    from PIL import Image
+    try:
+        img = Image.open(io.BytesIO(data))
+        img.load()
+    except Exception as exc:
+        raise FormatError(f"not a decodable PNG: {exc}") from None
+    if img.format != "PNG":
+        raise FormatError(f"expected PNG, got {img.format}")
+    if img.mode not in ("I;16", "I"):
+        raise FormatError(f"expected 16-bit single-channel PNG, got mode {img.mode!r}")
+    raw = np.asarray(img)
+    if raw.ndim != 2 or raw.size == 0 or raw.min() < 0 or raw.max() > 0xFFFF:
+        raise FormatError("PNG samples out of 16-bit range")
+    return raw.astype(np.uint16)
+
+
+def read_disparity_png16_device(data: bytes, scale: float = 256.0, invalid_value: int = 0,
+                                dtype=torch.float32, device=None) -> torch.Tensor:
+    """Dequantised disparity ``[H, W]`` on the device (NaN where raw ==
+    invalid_value); float64 is the reference's value exactly."""
+    from . import device as _dev
+    from ._host import current_device
+    dev = torch.device(device) if device is not None else current_device()
+    raw = torch.from_numpy(_png16_samples(data)).to(dev)
+    inv = int(invalid_value)
+    return _dev.dequant_png16(raw, scale, inv if 0 <= inv <= 0xFFFF else None, dtype=dtype)[0]
+
+
+def read_png16_raw_device(data: bytes, device=None) -> torch.Tensor:
+    """The undecoded 16-bit samples on the device, for
+    ``device.oriented_points_png16`` (2 B/px into the fused pass)."""
+    from ._host import current_device
+    dev = torch.device(device) if device is not None else current_device()
+    return torch.from_numpy(_png16_samples(data)).to(dev)
+
+
+def read_disparity_png16(data: bytes, scale: float = 256.0,
+                         invalid_value: int = 0) -> ScalarField:
+    """Quantised disparity: d = (raw - 1) / scale, raw == invalid_value masked
+    (formats.py:133-150)."""
+    raw = _png16_samples(data)
+    mask = raw.astype(np.int64) != invalid_value
+    d = read_disparity_png16_device(data, scale, invalid_value, dtype=torch.float64)
+    return ScalarField(d.cpu().numpy(), mask)
+
+
+def write_disparity_png16(field: ScalarField, scale: float = 256.0,
+                          invalid_value: int = 0) -> bytes:
+    """Inverse of read_disparity_png16; valid raws clamp to [1, 65535]
+    (formats.py:153-162)."""
+    from PIL import Image
+    raw = np.clip(np.rint(field.values * float(scale) + 1.0), 1, 0xFFFF)
+    raw = np.where(field.mask, raw, float(invalid_value)).astype(np.uint16)
+    buf = io.BytesIO()
+    Image.fromarray(raw).save(buf, format="PNG")
+    return buf.getvalue()
+
+
+# --------------------------------------------------------------------------
+# PLY
 
 PLY_PROPS = ("x", "y", "z", "nx", "ny", "nz")
 

@@ -52,3 +52,16 @@ def adaptive_golden():
         case["config"] = json.loads(c)
         out[n] = case
     return out
+
+
+@pytest.fixture(scope="session")
+def codec_golden():
+    z = np.load(GOLDEN / "codec_cases.npz", allow_pickle=False)
+    out = {"pfm": {}, "png": {}, "fused": {}}
+    for kind in out:
+        for n in [str(v) for v in z[f"{kind}_names"]]:
+            pre = f"{kind}_{n}__"
+            out[kind][n] = {k[len(pre):]: z[k] for k in z.files if k.startswith(pre)}
+    out["pfmerr"] = [(bytes(z[f"pfmerr_{i}__bytes"]), str(m))
+                     for i, m in enumerate(z["pfmerr_msgs"])]
+    return out
