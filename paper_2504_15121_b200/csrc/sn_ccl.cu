@@ -272,10 +272,12 @@ __device__ __forceinline__ int frame_index(int px, int x0, int y0, int W) {
 
 // ---------------------------------------------------------------------------
 // 1. tile pass.  MODE 1: uint8 passable input; MODE 2: the bit mask is the
-// input (passable_bits_kernel).  Dynamic shared memory: the parent array
-// (kSlots int32) + the exported slot labels (kSlots uint16) = 48 KB.
+// input (passable_bits_kernel).  Dynamic shared memory: the parent array only
+// (kSlots int32 = 32 KB; 6 CTAs/SM) -- the slot labels go straight to the
+// workspace (measured: staging them in shared memory capped residency at 4
+// CTAs/SM).
 
-constexpr size_t kTileSmem = (size_t)kSlots * 4 + (size_t)kSlots * 2;
+constexpr size_t kTileSmem = (size_t)kSlots * 4;
 
 template <int MODE>
 __global__ void __launch_bounds__(kLThreads)
@@ -290,6 +292,7 @@ __global__ void __launch_bounds__(kLThreads)
   const int x0 = tx * kLTW, y0 = ty * kLTH;
   const int64_t fbase = (int64_t)blockIdx.z * p.H * p.W;
   const int64_t frow = (int64_t)blockIdx.z * H;
+  const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
 
   for (int i = tid; i < kTilePx / 32; i += kLThreads) flag[i] = 0u;
   if (MODE == 1) {
@@ -315,15 +318,16 @@ __global__ void __launch_bounds__(kLThreads)
   }
 
   int32_t* L = smem;
-  uint16_t* lbl = reinterpret_cast<uint16_t*>(smem + kSlots);
   band_union_find(L, bits, tid);
 
-  // export labels of the band-run slots; flag components touching the tile border
+  // export labels of the band-run slots (run-start entries of the workspace
+  // array; the others are never read); flag components touching the border
   {
     const int k = tid >> 2, w = tid & 3;
     const int base = k * kLTW + w * 32;
     const uint32_t A0 = bits[(2 * k) * kLWords + w], A1 = bits[(2 * k + 1) * kLWords + w];
     const uint32_t G = A0 | A1;
+    uint16_t* lbl = ws.lbl + tile * kSlots;
     for (uint32_t m = run_starts(G); m; m &= m - 1u) {
       const int s = __ffs(m) - 1;
       const int v = slot_label(L, base + s);
@@ -349,7 +353,7 @@ __global__ void __launch_bounds__(kLThreads)
         if (gx < W) {
           int32_t v = -1;
           if ((bits[r * kLWords + w] >> lane) & 1u)
-            v = frame_index(lbl[pixel_slot(bits, r, c)], x0, y0, W);
+            v = frame_index(slot_label(L, pixel_slot(bits, r, c)), x0, y0, W);
           dst[gx] = v;
         }
       }
@@ -362,12 +366,11 @@ __global__ void __launch_bounds__(kLThreads)
       if (y0 + r >= H) break;
       int32_t v = -1;
       if ((bits[r * kLWords + (c >> 5)] >> (c & 31)) & 1u)
-        v = frame_index(lbl[pixel_slot(bits, r, c)], x0, y0, W);
+        v = frame_index(slot_label(L, pixel_slot(bits, r, c)), x0, y0, W);
       dst[y0 + r] = v;
     }
   }
   // global union-find nodes: one per border-touching component, G[label] = label
-  const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
   {
     int32_t* G = labels + fbase;
     for (int i = tid; i < kTilePx / 32; i += kLThreads) {
@@ -378,13 +381,6 @@ __global__ void __launch_bounds__(kLThreads)
         G[g] = g;
       }
     }
-  }
-  // the slot labels for the resolve pass (run-start entries only are meaningful)
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(lbl);
-    uint4* dst = reinterpret_cast<uint4*>(ws.lbl + tile * kSlots);
-#pragma unroll
-    for (int i = 0; i < kSlots / 8 / kLThreads; ++i) dst[i * kLThreads + tid] = src[i * kLThreads + tid];
   }
 }
 
@@ -398,40 +394,35 @@ __global__ void __launch_bounds__(kLThreads)
 // A straight neighbour makes the diagonal links redundant (the diagonal
 // pixels are 8-adjacent to it along the seam row/column).
 
-__global__ void ccl_seam_kernel(const CclParams p, const CclWorkspace ws,
-                                int32_t* __restrict__ labels) {
+// One CTA per (seam line, 256-position chunk) and frame: the line decode is
+// block-uniform 32-bit arithmetic (a 64-bit division per position cost
+// more than the unions).
+constexpr int kSeamThreads = 256;
+
+__global__ void __launch_bounds__(kSeamThreads)
+    ccl_seam_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
   const int W = (int)p.W, H = (int)p.H;
-  const int64_t n_h = (int64_t)(ws.n_ty - 1) * W;  // horizontal seam positions per frame
-  const int64_t n_v = (int64_t)(ws.n_tx - 1) * H;
-  const int64_t per_frame = n_h + n_v;
-  const int64_t total = per_frame * p.B;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = idx / per_frame;
-    int64_t k = idx - f * per_frame;
+  const int chW = (W + kSeamThreads - 1) / kSeamThreads;
+  const int chH = (H + kSeamThreads - 1) / kSeamThreads;
+  const int nh = (ws.n_ty - 1) * chW;  // horizontal (line, chunk) pairs
+  const int b = blockIdx.x;
+  const bool horiz = b < nh;
+  const int bb = horiz ? b : b - nh;
+  const int ch = horiz ? chW : chH;
+  const int s = bb / ch;
+  const int i = (bb - s * ch) * kSeamThreads + threadIdx.x;
+  const int n = horiz ? W : H;
+  if (i >= n) return;
+  for (int64_t f = blockIdx.y; f < p.B; f += gridDim.y) {
     int32_t* G = labels + f * p.H * p.W;
-    const int32_t* a_row;
-    const int32_t* b_row;
-    int i, n;
-    if (k < n_h) {
-      const int s = (int)(k / W);
-      i = (int)(k - (int64_t)s * W);
-      n = W;
-      a_row = ws.bot + (f * ws.n_ty + s) * W;
-      b_row = ws.top + (f * ws.n_ty + s + 1) * W;
-    } else {
-      k -= n_h;
-      const int s = (int)(k / H);
-      i = (int)(k - (int64_t)s * H);
-      n = H;
-      a_row = ws.right + (f * ws.n_tx + s) * H;
-      b_row = ws.left + (f * ws.n_tx + s + 1) * H;
-    }
+    const int32_t* a_row = horiz ? ws.bot + (f * ws.n_ty + s) * W : ws.right + (f * ws.n_tx + s) * H;
+    const int32_t* b_row =
+        horiz ? ws.top + (f * ws.n_ty + s + 1) * W : ws.left + (f * ws.n_tx + s + 1) * H;
     const int32_t a = a_row[i];
     if (a < 0) continue;
-    const int32_t b = b_row[i];
-    if (b >= 0) {
-      if (a != b) uf_unite(G, a, b);
+    const int32_t c = b_row[i];
+    if (c >= 0) {
+      if (a != c) uf_unite(G, a, c);
     } else {
       if (i > 0) {
         const int32_t bl = b_row[i - 1];
@@ -847,9 +838,12 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
     ccl_tile_kernel<1><<<grid, kLThreads, kTileSmem, ctx.stream>>>(pas, p, ws, labels);
   int rc = check_launch("ccl_tile_kernel");
   if (rc) return rc;
-  const int64_t n_seam = ((int64_t)(ws.n_ty - 1) * p.W + (int64_t)(ws.n_tx - 1) * p.H) * p.B;
-  if (n_seam > 0) {
-    ccl_seam_kernel<<<grid_for(ctx, n_seam, 256), 256, 0, ctx.stream>>>(p, ws, labels);
+  const int64_t seam_blocks =
+      (int64_t)(ws.n_ty - 1) * ((p.W + kSeamThreads - 1) / kSeamThreads) +
+      (int64_t)(ws.n_tx - 1) * ((p.H + kSeamThreads - 1) / kSeamThreads);
+  if (seam_blocks > 0) {
+    dim3 sg((unsigned)seam_blocks, (unsigned)(p.B < 65535 ? p.B : 65535));
+    ccl_seam_kernel<<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
     if ((rc = check_launch("ccl_seam_kernel"))) return rc;
   }
   ccl_resolve_kernel<<<grid, kLThreads, 0, ctx.stream>>>(p, ws, labels);
