@@ -440,9 +440,14 @@ __global__ void __launch_bounds__(kSeamThreads)
 // 3. resolve: border-touching components through G (one walk each), then per
 // pixel: band-run slot (bit ops) -> tile label -> final label, coalesced stores
 
+__device__ __forceinline__ int lp(int slot) { return slot + (slot >> 5); }
+
 __global__ void __launch_bounds__(kLThreads)
     ccl_resolve_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
-  __shared__ __align__(16) int32_t lab[kSlots];  // slot label, then slot FINAL label
+  // slot label, then slot FINAL label; one pad word per 32 slots (lp) so the
+  // lanes of a warp looking up run starts at equal bit positions of different
+  // words hit different banks
+  __shared__ __align__(16) int32_t lab[kSlots + kSlots / 32];
   __shared__ uint32_t bits[kRowWords];
   __shared__ uint32_t flag[kTilePx / 32];
   __shared__ int32_t rank0[kTilePx / 32];  // flagged labels before word i
@@ -457,14 +462,19 @@ __global__ void __launch_bounds__(kLThreads)
   const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
   {
     const uint4* src = reinterpret_cast<const uint4*>(ws.lbl + tile * kSlots);
-    int4* dst = reinterpret_cast<int4*>(lab);
 #pragma unroll
     for (int i = 0; i < kSlots / 8 / kLThreads; ++i) {
-      const uint4 v = src[i * kLThreads + tid];
-      dst[2 * (i * kLThreads + tid)] =
-          make_int4(v.x & 0xffff, v.x >> 16, v.y & 0xffff, v.y >> 16);
-      dst[2 * (i * kLThreads + tid) + 1] =
-          make_int4(v.z & 0xffff, v.z >> 16, v.w & 0xffff, v.w >> 16);
+      const int j = i * kLThreads + tid;  // slots 8j .. 8j+7, one 32-slot group
+      const uint4 v = src[j];
+      int32_t* d = lab + lp(8 * j);
+      d[0] = v.x & 0xffff;
+      d[1] = v.x >> 16;
+      d[2] = v.y & 0xffff;
+      d[3] = v.y >> 16;
+      d[4] = v.z & 0xffff;
+      d[5] = v.z >> 16;
+      d[6] = v.w & 0xffff;
+      d[7] = v.w >> 16;
     }
     for (int i = tid; i < kRowWords; i += kLThreads) {
       const int r = i >> 2, wc = tx * kLWords + (i & 3);
@@ -514,7 +524,7 @@ __global__ void __launch_bounds__(kLThreads)
     const int kb = tid >> 2, w = tid & 3;
     const int base = kb * kLTW + w * 32;
     for (uint32_t m = run_starts(band_word(bits, kb, w)); m; m &= m - 1u) {
-      const int slot = base + __ffs(m) - 1;
+      const int slot = lp(base + __ffs(m) - 1);
       const int v = lab[slot];
       const uint32_t fwv = flag[v >> 5];
       const uint32_t bit = 1u << (v & 31);
@@ -532,7 +542,7 @@ __global__ void __launch_bounds__(kLThreads)
     for (int r = warp; r < kLTH; r += kLThreads / 32) {
       const uint32_t A = bits[r * kLWords + w];
       const uint32_t st = run_starts(band_word(bits, r >> 1, w));
-      const int base = (r >> 1) * kLTW + w * 32;
+      const int base = lp((r >> 1) * kLTW + w * 32);  // a 32-slot group: lp(base + b) = base + b
       int v[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -553,7 +563,7 @@ __global__ void __launch_bounds__(kLThreads)
       int32_t v = -1;
       if ((A >> lane) & 1u) {
         const uint32_t st = run_starts(band_word(bits, r >> 1, w));
-        v = lab[(r >> 1) * kLTW + w * 32 + (31 - __clz(st & upto))];
+        v = lab[lp((r >> 1) * kLTW + w * 32) + (31 - __clz(st & upto))];
       }
       out[gy * W + gx] = v;  // frame offsets fit int32 (host-checked)
     }
