@@ -100,41 +100,53 @@ __global__ void passable_kernel(const float* __restrict__ disp, const CclParams 
 // ---------------------------------------------------------------------------
 // union-find helpers (indices only ever point to smaller indices)
 
+// PAD: the tile's parent array keeps one pad word per 32 slots (tix), so the
+// lanes of a warp -- 8 bands x 4 words -- touching slots at the same bit
+// position of different words hit different banks; the global array G of
+// the seam pass is unpadded
+template <bool PAD>
+__device__ __forceinline__ int tix(int x) {
+  return PAD ? x + (x >> 5) : x;
+}
+
 // find with path halving: every write replaces a parent by an ancestor, so it
 // commutes with concurrent unions (which only atomicMin roots)
+template <bool PAD = false>
 __device__ __forceinline__ int uf_find(volatile int32_t* L, int x) {
   while (true) {
-    const int p = L[x];
+    const int p = L[tix<PAD>(x)];
     if (p == x) return x;
-    const int gp = L[p];
+    const int gp = L[tix<PAD>(p)];
     if (gp == p) return p;
-    L[x] = gp;
+    L[tix<PAD>(x)] = gp;
     x = gp;
   }
 }
 
 // read-only find
+template <bool PAD = false>
 __device__ __forceinline__ int uf_root(const volatile int32_t* L, int x) {
-  int p = L[x];
+  int p = L[tix<PAD>(x)];
   while (p != x) {
     x = p;
-    p = L[x];
+    p = L[tix<PAD>(x)];
   }
   return x;
 }
 
+template <bool PAD = false>
 __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
   volatile int32_t* V = L;
   while (true) {
-    a = uf_find(V, a);
-    b = uf_find(V, b);
+    a = uf_find<PAD>(V, a);
+    b = uf_find<PAD>(V, b);
     if (a == b) return;
     if (a > b) {
       const int t = a;
       a = b;
       b = t;
     }
-    const int old = atomicMin(&L[b], a);
+    const int old = atomicMin(&L[tix<PAD>(b)], a);
     if (old == b) return;
     b = old;
   }
@@ -181,8 +193,8 @@ __device__ __forceinline__ uint32_t run_mask(uint32_t G, int s) {
 }
 
 __device__ __forceinline__ int slot_label(const int32_t* L, int slot) {
-  const int v = L[slot];
-  return (v >= 0 ? L[v] : v) + kEnc;
+  const int v = L[tix<true>(slot)];
+  return (v >= 0 ? L[tix<true>(v)] : v) + kEnc;
 }
 
 // slot of the band run holding pixel (r, c) of the tile (the pixel must be set)
@@ -198,13 +210,13 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
   const uint32_t G = A0 | A1, stG = run_starts(G);
   for (uint32_t m = stG; m; m &= m - 1u) {
     const int n = base + __ffs(m) - 1;
-    L[n] = n;
+    L[tix<true>(n)] = n;
   }
   __syncthreads();
   // a band run crossing into this word from the left neighbour word
   if ((G & 1u) && w > 0) {
     const uint32_t Gl = band_word(bits, k, w - 1);
-    if (Gl >> 31) uf_unite(L, base, base - 32 + (31 - __clz(run_starts(Gl))));
+    if (Gl >> 31) uf_unite<true>(L, base, base - 32 + (31 - __clz(run_starts(Gl))));
   }
   // band k-1: only this band's first-row pixels touch it (its last row)
   if (k > 0) {
@@ -222,22 +234,22 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
       uint32_t o = (a | (a << 1) | (a >> 1)) & B;
       while (o) {
         const int p = __ffs(o) - 1;
-        uf_unite(L, n, bbase + start_of(stGb, p));
+        uf_unite<true>(L, n, bbase + start_of(stGb, p));
         const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
         const uint32_t zb = ~Gb & ~upto;  // zeros of band k-1 above p: end of that band run
         if (!zb) break;
         o &= ~((zb & (0u - zb)) - 1u);
       }
       if ((a & 1u) && (BL >> 31))
-        uf_unite(L, n, bbase - 32 + (31 - __clz(run_starts(bits[rb - kLWords - 1] | BL))));
-      if ((a >> 31) && (BR & 1u)) uf_unite(L, n, bbase + 32);
+        uf_unite<true>(L, n, bbase - 32 + (31 - __clz(run_starts(bits[rb - kLWords - 1] | BL))));
+      if ((a >> 31) && (BR & 1u)) uf_unite<true>(L, n, bbase + 32);
     }
   }
   __syncthreads();
   // every node -> its root (only root values are written in this phase)
   for (uint32_t m = stG; m; m &= m - 1u) {
     const int n = base + __ffs(m) - 1;
-    L[n] = uf_root(L, n);
+    L[tix<true>(n)] = uf_root<true>(L, n);
   }
   __syncthreads();
   // component label = smallest pixel index, reduced into the root's entry
@@ -247,8 +259,8 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
     const uint32_t a0 = A0 & run;
     const int mp = a0 ? (2 * k) * kLTW + w * 32 + __ffs(a0) - 1
                       : (2 * k + 1) * kLTW + w * 32 + __ffs(A1 & run) - 1;
-    const int pr = L[base + s];
-    atomicMin(&L[pr >= 0 ? pr : base + s], mp - kEnc);
+    const int pr = L[tix<true>(base + s)];
+    atomicMin(&L[tix<true>(pr >= 0 ? pr : base + s)], mp - kEnc);
   }
   __syncthreads();
 }
@@ -277,7 +289,7 @@ __device__ __forceinline__ int frame_index(int px, int x0, int y0, int W) {
 // workspace (measured: staging them in shared memory capped residency at 4
 // CTAs/SM).
 
-constexpr size_t kTileSmem = (size_t)kSlots * 4;
+constexpr size_t kTileSmem = (size_t)(kSlots + kSlots / 32) * 4;
 
 template <int MODE>
 __global__ void __launch_bounds__(kLThreads)
