@@ -73,3 +73,31 @@ def test_error_stats_random(cuda_dev, n):
         assert out[b, 3] == srt[(len(srt) - 1) // 2]
         assert out[b, 1] == srt[0] and out[b, 2] == srt[-1] and out[b, 5] == vals.size
         np.testing.assert_allclose([out[b, 0], out[b, 4]], [vals.mean(), vals.std()], rtol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["repeated", "all_equal", "narrow", "neg_zero"])
+def test_error_stats_crowded(cuda_dev, kind):
+    """Median prefixes holding more values than the candidate list (the
+    8-bit radix fallback) and ones just below it, batched with a normal frame."""
+    from paper_2504_15121_b200 import device
+    rng = np.random.default_rng(7)
+    n = 300007
+    v = rng.normal(5, 2, (2, 1, n))
+    if kind == "repeated":
+        v[0, 0, : 2 * n // 3] = 1.25
+    elif kind == "all_equal":
+        v[0, 0, :] = 3.0
+    elif kind == "narrow":  # ~all values share the top 24 key bits, distinct below
+        v[0, 0, :] = 1.0 + rng.random(n) * 2.0 ** -20
+    else:
+        v[0, 0, :] = rng.choice([-0.0, 0.0, 1e-300, -1e-300], n)
+    v[0, 0, ::11] = np.nan
+    out = device.error_stats(torch.from_numpy(v).to(cuda_dev)).cpu().numpy()
+    for b in range(2):
+        vals = v[b][np.isfinite(v[b])]
+        srt = np.sort(vals)
+        med = srt[(len(srt) - 1) // 2]
+        assert out[b, 3] == med or (med == 0 and out[b, 3] == 0), (kind, b, out[b, 3], med)
+        assert out[b, 1] == srt[0] and out[b, 2] == srt[-1] and out[b, 5] == vals.size
+        np.testing.assert_allclose([out[b, 0], out[b, 4]], [vals.mean(), vals.std()],
+                                   rtol=1e-12, atol=1e-300)
