@@ -30,80 +30,191 @@
 
 namespace sn {
 
+// depth map for the CD walks: RN32 of the reference's fp64 depth
+// z = fx*b/d (pred_depth: NaN unless d is finite and > 0).  Rounding is
+// monotonic, so running maxima / minima of these values are the roundings of
+// the fp64 ones -- the fp32 filter below relies on that.
 __global__ void depth_kernel(const float* __restrict__ disp, int64_t n, double fxb,
-                             double* __restrict__ z) {
+                             float* __restrict__ z) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    z[i] = pred_depth(disp[i], fxb);
+    z[i] = (float)pred_depth(disp[i], fxb);
 }
 
+// CD walk, exact: the reference's fp64 running range (adaptive.py:214-234)
+// over depths recomputed from the disparities, for the lanes the fp32 filter
+// cannot decide.  Sets this lane's bit in the warp's key masks.
+__device__ __noinline__ void cd_walk_exact(const float* __restrict__ fd, int x, int y, int W, int H,
+                                           double zc, const AdaptiveParams& ap,
+                                           const StarTable& tab, uint32_t* km, uint32_t bit) {
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  const double limit = __dmul_rn(ap.threshold, zc);
+  double rmax = zc, rmin = zc;
+  for (int j = 0; j < tab.n_rays; ++j) {
+    if (!ap.shared_range) rmax = rmin = zc;
+    for (int st = tab.ray_start[j]; st < tab.ray_start[j + 1]; ++st) {
+      const int k = tab.step_key[st];
+      const int sxy = tab.step_xy[st];
+      const int xx = x + (int)(int16_t)(sxy & 0xffff), yy = y + (sxy >> 16);
+      const bool inside = (unsigned)xx < (unsigned)W && (unsigned)yy < (unsigned)H;
+      // fmax/fmin ignore a NaN sample; while the ray is alive the shared-range
+      // update (adaptive.py:226-228) is the same as the per-ray one, and it
+      // still happens on the step that stops it
+      const double zs = inside ? pred_depth(fd[yy * W + xx], ap.fp.fxb) : qnan;
+      const double nmax = fmax(rmax, zs), nmin = fmin(rmin, zs);
+      const bool ok = (zs == zs) && __dsub_rn(nmax, nmin) <= limit;
+      rmax = nmax;
+      rmin = nmin;
+      if (!ok) break;
+      atomicOr(&km[k], bit);
+    }
+  }
+}
+
+constexpr int kAdaptiveThreads = 128;
+constexpr uint32_t kFull = 0xffffffffu;
+
+// One lane per pixel, a warp walks the rays in lockstep: the step (offset,
+// key) is warp-uniform, lanes whose ray has stopped idle until the whole warp
+// has stopped, and the support is recorded per key as a ballot of the lanes
+// that visited it (warp-private shared-memory masks) -- no per-lane member
+// bitmaps, no divergent table reads.
 template <int STOP>  // 0 = ST, 1 = CD
-__global__ void __launch_bounds__(128)
-    adaptive_kernel(const float* __restrict__ disp, const double* __restrict__ depth,
-                    const uint32_t* __restrict__ pbits, const AdaptiveParams ap,
+__global__ void __launch_bounds__(kAdaptiveThreads)
+    adaptive_kernel(const float* __restrict__ disp, const float* __restrict__ depth,
+                    const uint32_t* __restrict__ pbits, const __grid_constant__ AdaptiveParams ap,
                     const __grid_constant__ StarTable tab, float* __restrict__ out6,
                     uint8_t* __restrict__ mask) {
+  __shared__ uint32_t kmask[kAdaptiveThreads / 32][kStarMaxKeys];
   const FixedParams& p = ap.fp;
   const int W = (int)p.W, H = (int)p.H;
   const int64_t HW = p.H * p.W;
+  const int64_t n = p.B * HW;
+  const int lane = threadIdx.x & 31;
+  uint32_t* km = kmask[threadIdx.x >> 5];
+  const uint32_t lbit = 1u << lane;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < p.B * HW;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = idx / HW;
-    const int pix = (int)(idx - f * HW);
+  const float fnan = __int_as_float(0x7fc00000);
+  for (int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); wbase < n;
+       wbase += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = wbase + lane;
+    const bool have = idx < n;
+    const int64_t f = have ? idx / HW : 0;
+    const int pix = have ? (int)(idx - f * HW) : 0;
     const int y = pix / W, x = pix - y * W;
     const float* fd = disp + f * HW;
-    const double* fz = depth + f * HW;
-    const double zc = fz[pix];
+    const double zc = have ? pred_depth(fd[pix], p.fxb) : qnan;
     const bool center_ok = zc == zc;
-    uint32_t mem[kStarKeyWords];
-#pragma unroll
-    for (int i = 0; i < kStarKeyWords; ++i) mem[i] = 0u;
-    if (center_ok) {
-      const double limit = __dmul_rn(ap.threshold, zc);
-      double rmax = zc, rmin = zc;
+    for (int k = lane; k < tab.n_keys; k += 32) km[k] = 0u;
+    __syncwarp();
+    bool undecided = false;
+    if (STOP == 0) {
+      const uint32_t* fb = pbits + f * p.H * p.bits_ww;
       for (int j = 0; j < tab.n_rays; ++j) {
-        if (STOP == 1 && !ap.shared_range) rmax = rmin = zc;
+        bool alive = center_ok;
         for (int st = tab.ray_start[j]; st < tab.ray_start[j + 1]; ++st) {
+          if (!__any_sync(kFull, alive)) break;
           const int k = tab.step_key[st];
-          const int xx = x + tab.key_x[k], yy = y + tab.key_y[k];
+          const int sxy = tab.step_xy[st];
+          const int xx = x + (int)(int16_t)(sxy & 0xffff), yy = y + (sxy >> 16);
+          alive = alive && (unsigned)xx < (unsigned)W && (unsigned)yy < (unsigned)H &&
+                  ((fb[yy * p.bits_ww + (xx >> 5)] >> (xx & 31)) & 1u) != 0u;
+          const uint32_t b = __ballot_sync(kFull, alive);
+          if (lane == 0 && b) km[k] |= b;
+        }
+      }
+    } else {
+      // fp32 filter of the CD decisions: with z32 = RN32(z), the running
+      // extremes are RN32 of the fp64 ones, so |(max32 - min32) - (max - min)|
+      // <= 3 * 2^-24 max; a step is decided when the fp32 range clears the
+      // fp32 limit by the margin 2^-20 (max + limit) (which also covers the
+      // fp64 rounding of the reference's subtraction and of t * z_c); an
+      // undecided step, or a depth outside [2^-100, 2^100], sends the lane to
+      // the exact fp64 walk
+      const double limit = __dmul_rn(ap.threshold, zc);
+      const float lim32 = (float)limit, zc32 = (float)zc;
+      undecided = center_ok && !(zc32 >= 7.888609052210118e-31f && zc32 <= 1.2676506002282294e30f &&
+                                 lim32 >= 7.888609052210118e-31f && lim32 <= 1.2676506002282294e30f);
+      const float* fzp = depth + f * HW + pix;  // this lane's pixel
+      float rmax = zc32, rmin = zc32;
+      for (int j = 0; j < tab.n_rays; ++j) {
+        if (!ap.shared_range) rmax = rmin = zc32;
+        bool alive = center_ok && !undecided;
+        for (int st = tab.ray_start[j]; st < tab.ray_start[j + 1]; ++st) {
+          if (!__any_sync(kFull, alive)) break;
+          const int k = tab.step_key[st];
+          const int sxy = tab.step_xy[st];
+          const int xx = x + (int)(int16_t)(sxy & 0xffff), yy = y + (sxy >> 16);
           const bool inside = (unsigned)xx < (unsigned)W && (unsigned)yy < (unsigned)H;
-          bool ok;
-          if (STOP == 0) {
-            ok = inside &&
-                 ((pbits[(f * p.H + yy) * p.bits_ww + (xx >> 5)] >> (xx & 31)) & 1u) != 0u;
-          } else {
-            // fmax/fmin ignore a NaN sample; while the ray is alive the
-            // shared-range update (adaptive.py:226-228) is the same as the
-            // per-ray one, and it still happens on the step that stops it
-            const double zs = inside ? fz[yy * W + xx] : qnan;
-            const double nmax = fmax(rmax, zs), nmin = fmin(rmin, zs);
-            ok = (zs == zs) && __dsub_rn(nmax, nmin) <= limit;
+          const float zs = (alive && inside) ? fzp[tab.step_lin[st]] : fnan;
+          // NaN / outside: stop with the extremes unchanged; otherwise the
+          // extremes take the sample (also on the step that stops the ray)
+          const bool fin = zs == zs;
+          const float nmax = fmaxf(rmax, zs), nmin = fminf(rmin, zs);
+          const float range = nmax - nmin;
+          const float marg = (nmax + lim32) * 9.5367431640625e-07f;  // 2^-20
+          const bool inr = nmax <= 1.2676506002282294e30f && nmin >= 7.888609052210118e-31f;
+          const bool keep = range < lim32 - marg;
+          const bool over = range > lim32 + marg;
+          if (alive && fin) {
             rmax = nmax;
             rmin = nmin;
+            if (!inr || !(keep || over)) undecided = true;
           }
-          if (!ok) break;  // alive stays false for the rest of the ray
-          mem[k >> 5] |= 1u << (k & 31);
+          alive = alive && fin && inr && keep;
+          const uint32_t b = __ballot_sync(kFull, alive);
+          if (lane == 0 && b) km[k] |= b;
+        }
+        if (__all_sync(kFull, !center_ok || undecided)) break;
+      }
+      __syncwarp();
+      if (__any_sync(kFull, undecided)) {  // rare: exact walk for those lanes
+        if (undecided) {
+          for (int k = 0; k < tab.n_keys; ++k) atomicAnd(&km[k], ~lbit);
+          cd_walk_exact(fd, x, y, W, H, zc, ap, tab, km, lbit);
         }
       }
     }
-    // moments over the support in member order (adaptive.py:240-255)
-    double alpha = 0.0, beta = 0.0, gamma = 0.0, b1 = 0.0, b2 = 0.0;
+    __syncwarp();
+    // moments over the support in member order (adaptive.py:240-255): keys
+    // are numbered by first occurrence, so ascending key order IS member
+    // order.  alpha, beta, gamma are integer sums (exact, as the reference's
+    // fp64 sums are); v * (d_k - d_c) is exact for fp32 disparities, so one
+    // FMA per term rounds like the reference's multiply-then-add.
+    // 32-bit sums unless the table's sums could overflow them (tab.wide)
+    long long ia = 0, ib = 0, ig = 0;
+    int ja = 0, jb = 0, jg = 0;
+    double b1 = 0.0, b2 = 0.0;
     const double dc = (double)fd[pix];
-    if (center_ok) {
-      for (int w = 0; w < kStarKeyWords; ++w) {
-        for (uint32_t m = mem[w]; m; m &= m - 1u) {
-          const int k = w * 32 + __ffs(m) - 1;
-          const double vx = (double)tab.key_x[k], vy = (double)tab.key_y[k];
-          alpha = __dadd_rn(alpha, __dmul_rn(vx, vx));
-          beta = __dadd_rn(beta, __dmul_rn(vx, vy));
-          gamma = __dadd_rn(gamma, __dmul_rn(vy, vy));
-          const double dd = __dsub_rn((double)fd[(y + tab.key_y[k]) * W + x + tab.key_x[k]], dc);
-          b1 = __dadd_rn(b1, __dmul_rn(vx, dd));
-          b2 = __dadd_rn(b2, __dmul_rn(vy, dd));
+    const float* fdp = fd + pix;
+    for (int k = 0; k < tab.n_keys; ++k) {
+      const uint32_t mk = km[k];
+      if (mk == 0u) continue;  // warp-uniform
+      if (mk & lbit) {
+        const int kxy = tab.key_xy[k];
+        const int kx = (int)(int16_t)(kxy & 0xffff), ky = kxy >> 16;
+        if (tab.wide) {
+          ia += (long long)kx * kx;
+          ib += (long long)kx * ky;
+          ig += (long long)ky * ky;
+        } else {
+          ja += kx * kx;
+          jb += kx * ky;
+          jg += ky * ky;
         }
+        const double dd = __dsub_rn((double)fdp[tab.key_lin[k]], dc);
+        b1 = __fma_rn((double)kx, dd, b1);
+        b2 = __fma_rn((double)ky, dd, b2);
       }
     }
+    if (!tab.wide) {
+      ia = ja;
+      ib = jb;
+      ig = jg;
+    }
+    __syncwarp();  // the masks are cleared for the next pixels
+    if (!have) continue;
+    const double alpha = (double)ia, beta = (double)ib, gamma = (double)ig;
     const double det = __dsub_rn(__dmul_rn(alpha, gamma), __dmul_rn(beta, beta));
     bool ok = center_ok && det > 0.5;
     float n32[3] = {__int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
@@ -157,7 +268,7 @@ __global__ void __launch_bounds__(128)
 
 size_t adaptive_workspace_bytes(int64_t B, int64_t H, int64_t W) {
   const int64_t WW = (W + 31) / 32;
-  return (size_t)(B * H * W) * 8 + 256 + (size_t)(B * H * WW) * 4;
+  return (size_t)(B * H * W) * 4 + 256 + (size_t)(B * H * WW) * 4;
 }
 
 int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& ap,
@@ -169,14 +280,16 @@ int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& 
   if (p.H * p.W > 0x7fffffffLL) return set_error(SN_EINVAL, "frame too large");
   if (!workspace || ws_bytes < adaptive_workspace_bytes(p.B, p.H, p.W))
     return set_error(SN_EINVAL, "adaptive workspace too small");
-  double* depth = static_cast<double*>(workspace);
+  float* depth = static_cast<float*>(workspace);
   uint32_t* bits = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) +
-                                               ((size_t)n * 8 + 255) / 256 * 256);
-  int64_t g = (n + 255) / 256;
-  if (g > (int64_t)ctx.num_sms * 32) g = (int64_t)ctx.num_sms * 32;
-  depth_kernel<<<(unsigned)g, 256, 0, ctx.stream>>>(disp, n, p.fxb, depth);
-  int rc = check_launch("depth_kernel");
-  if (rc) return rc;
+                                               ((size_t)n * 4 + 255) / 256 * 256);
+  int rc = SN_OK;
+  if (stop == 1) {
+    int64_t g = (n + 255) / 256;
+    if (g > (int64_t)ctx.num_sms * 32) g = (int64_t)ctx.num_sms * 32;
+    depth_kernel<<<(unsigned)g, 256, 0, ctx.stream>>>(disp, n, p.fxb, depth);
+    if ((rc = check_launch("depth_kernel"))) return rc;
+  }
   AdaptiveParams a = ap;
   if (stop == 0) {
     FixedParams fp = p;
@@ -185,14 +298,14 @@ int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& 
     a.fp.bits = bits;
     a.fp.bits_ww = fp.bits_ww;
   }
-  int64_t ga = (n + 127) / 128;
+  int64_t ga = (n + kAdaptiveThreads - 1) / kAdaptiveThreads;
   if (ga > (int64_t)ctx.num_sms * 64) ga = (int64_t)ctx.num_sms * 64;
   if (stop == 0)
-    adaptive_kernel<0><<<(unsigned)ga, 128, 0, ctx.stream>>>(disp, depth, a.fp.bits, a, tab, out6,
-                                                             mask);
+    adaptive_kernel<0><<<(unsigned)ga, kAdaptiveThreads, 0, ctx.stream>>>(
+        disp, depth, a.fp.bits, a, tab, out6, mask);
   else
-    adaptive_kernel<1><<<(unsigned)ga, 128, 0, ctx.stream>>>(disp, depth, nullptr, a, tab, out6,
-                                                             mask);
+    adaptive_kernel<1><<<(unsigned)ga, kAdaptiveThreads, 0, ctx.stream>>>(
+        disp, depth, nullptr, a, tab, out6, mask);
   return check_launch("adaptive_kernel");
 }
 

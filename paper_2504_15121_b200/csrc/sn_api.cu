@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <numeric>
 #include <unordered_map>
@@ -516,15 +517,31 @@ int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
           return set_error(SN_EINVAL, "at most %d distinct ray offsets", kStarMaxKeys);
         k = tab.n_keys++;
         key_of.emplace(kk, k);
-        tab.key_x[k] = (int16_t)vx;
-        tab.key_y[k] = (int16_t)vy;
+        tab.key_xy[k] = (int32_t)(((uint32_t)(uint16_t)vx) | ((uint32_t)(uint16_t)vy << 16));
+        tab.key_lin[k] = (int32_t)((int64_t)vy * W + vx);
       } else {
         k = it->second;
       }
       tab.step_key[steps] = (int16_t)k;
+      tab.step_xy[steps] = tab.key_xy[k];
+      tab.step_lin[steps] = tab.key_lin[k];
     }
   }
   tab.ray_start[n_rays] = steps;
+  // y * W + x must fit int32 for every offset; moment sums (sum of x^2 etc.
+  // over all keys) pick 32- or 64-bit accumulation
+  {
+    int64_t sxx = 0, sxy = 0, syy = 0;
+    for (int k = 0; k < tab.n_keys; ++k) {
+      const int64_t vx = (int16_t)(tab.key_xy[k] & 0xffff), vy = (int16_t)(tab.key_xy[k] >> 16);
+      if (std::llabs(vy) * W + std::llabs(vx) > 0x7fffffffLL)
+        return set_error(SN_EINVAL, "ray offsets too large for the frame width");
+      sxx += vx * vx;
+      sxy += std::llabs(vx * vy);
+      syy += vy * vy;
+    }
+    tab.wide = (sxx > 0x7fffffffLL || sxy > 0x7fffffffLL || syy > 0x7fffffffLL) ? 1 : 0;
+  }
   if (B * H * W == 0) return SN_OK;
   if (!disp || !out6) return set_error(SN_EINVAL, "NULL buffer");
   AdaptiveParams ap{};

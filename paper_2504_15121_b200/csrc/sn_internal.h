@@ -68,9 +68,13 @@ constexpr int kStarMaxRays = 64, kStarMaxSteps = 2048, kStarKeyWords = 16;
 constexpr int kStarMaxKeys = kStarKeyWords * 32;  // 512 distinct offsets
 struct StarTable {
   int n_rays, n_keys;
+  int wide;                         // moment sums may exceed int32: 64-bit accumulation
   int ray_start[kStarMaxRays + 1];  // steps of ray j: [ray_start[j], ray_start[j+1])
   int16_t step_key[kStarMaxSteps];  // key of each step
-  int16_t key_x[kStarMaxKeys], key_y[kStarMaxKeys];  // keys in first-occurrence order
+  int32_t step_xy[kStarMaxSteps];   // offset of each step: x in the low, y in the high 16 bits
+  int32_t step_lin[kStarMaxSteps];  // y * W + x of each step
+  int32_t key_xy[kStarMaxKeys];     // keys in first-occurrence order (packed like step_xy)
+  int32_t key_lin[kStarMaxKeys];
 };
 struct AdaptiveParams {
   FixedParams fp;     // rig, shape, point constants (bits / bits_ww for ST)

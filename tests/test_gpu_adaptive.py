@@ -71,3 +71,27 @@ def test_adaptive_vs_oracle_street(cuda_dev, cfg):
     m = mask[0].cpu().numpy().astype(bool)
     assert np.array_equal(m, ok_ref)
     assert max_angle_deg(out[0].cpu().numpy()[m][:, 3:], n_ref[m]) < 1e-4
+
+
+@pytest.mark.parametrize("shared", [False, True])
+@pytest.mark.parametrize("t", [0.25, 0.5, 0.75])
+def test_adaptive_cd_exact_ties(cuda_dev, shared, t):
+    """Depths fx*b/d on a few exact values, so CD ranges hit t * z_c exactly:
+    the fp32 filter must hand every tie to the exact walk (masks and normals
+    vs the oracle's fp64 decisions)."""
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import StarConfig, StereoRig, device
+    rng = np.random.default_rng(int(t * 100) + shared)
+    d = rng.choice(np.array([1.0, 2.0, 4.0, 5.0, 8.0, 10.0], np.float32), (64, 72))
+    d[rng.random(d.shape) < 0.02] = np.nan
+    rig = StereoRig(100.0, 100.0, 35.5, 31.5, 1.0)
+    cfg = dict(stop="cd", threshold=t, shared_range=shared, max_steps=6, directions=8)
+    n_ref, ok_ref = orc.estimate_normals_adaptive(d.astype(np.float64),
+                                                  orc.Rig(100.0, 100.0, 35.5, 31.5, 1.0),
+                                                  orc.Star(**cfg))
+    mask = torch.empty((1,) + d.shape, dtype=torch.uint8, device=cuda_dev)
+    out = device.adaptive_points(torch.from_numpy(d).to(cuda_dev), rig, StarConfig(**cfg),
+                                 mask=mask)
+    m = mask[0].cpu().numpy().astype(bool)
+    assert np.array_equal(m, ok_ref)
+    assert max_angle_deg(out[0].cpu().numpy()[m][:, 3:], n_ref[m]) < 1e-4
