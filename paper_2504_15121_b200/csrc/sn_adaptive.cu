@@ -72,6 +72,13 @@ __device__ __noinline__ void cd_walk_exact(const float* __restrict__ fd, int x, 
 }
 
 constexpr int kAdaptiveThreads = 128;
+
+__host__ __device__ inline size_t star_smem_tables(int n_steps, int n_keys) {
+  return ((size_t)n_steps * 10 + (size_t)n_keys * 8 + 15) / 16 * 16;
+}
+static size_t star_smem(int n_steps, int n_keys) {
+  return star_smem_tables(n_steps, n_keys) + (size_t)(kAdaptiveThreads / 32) * n_keys * 4;
+}
 constexpr uint32_t kFull = 0xffffffffu;
 
 // One lane per pixel, a warp walks the rays in lockstep: the step (offset,
@@ -85,13 +92,33 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
                     const uint32_t* __restrict__ pbits, const __grid_constant__ AdaptiveParams ap,
                     const __grid_constant__ StarTable tab, float* __restrict__ out6,
                     uint8_t* __restrict__ mask) {
-  __shared__ uint32_t kmask[kAdaptiveThreads / 32][kStarMaxKeys];
+  // dynamic shared memory: the step / key tables (read warp-uniformly every
+  // step: shared-memory broadcasts instead of constant-cache misses once
+  // the tables outgrow it) and the warps' key masks
+  extern __shared__ __align__(16) uint8_t adyn[];
+  const int n_steps = tab.ray_start[tab.n_rays];
+  int32_t* s_xy = reinterpret_cast<int32_t*>(adyn);
+  int32_t* s_lin = s_xy + n_steps;
+  int32_t* k_xy = s_lin + n_steps;
+  int32_t* k_lin = k_xy + tab.n_keys;
+  int16_t* s_key = reinterpret_cast<int16_t*>(k_lin + tab.n_keys);
+  uint32_t* kmask = reinterpret_cast<uint32_t*>(adyn + star_smem_tables(n_steps, tab.n_keys));
+  for (int i = threadIdx.x; i < n_steps; i += blockDim.x) {
+    s_xy[i] = tab.step_xy[i];
+    s_lin[i] = tab.step_lin[i];
+    s_key[i] = tab.step_key[i];
+  }
+  for (int i = threadIdx.x; i < tab.n_keys; i += blockDim.x) {
+    k_xy[i] = tab.key_xy[i];
+    k_lin[i] = tab.key_lin[i];
+  }
+  __syncthreads();
   const FixedParams& p = ap.fp;
   const int W = (int)p.W, H = (int)p.H;
   const int64_t HW = p.H * p.W;
   const int64_t n = p.B * HW;
   const int lane = threadIdx.x & 31;
-  uint32_t* km = kmask[threadIdx.x >> 5];
+  uint32_t* km = kmask + (threadIdx.x >> 5) * tab.n_keys;
   const uint32_t lbit = 1u << lane;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   const float fnan = __int_as_float(0x7fc00000);
@@ -114,8 +141,8 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
         bool alive = center_ok;
         for (int st = tab.ray_start[j]; st < tab.ray_start[j + 1]; ++st) {
           if (!__any_sync(kFull, alive)) break;
-          const int k = tab.step_key[st];
-          const int sxy = tab.step_xy[st];
+          const int k = s_key[st];
+          const int sxy = s_xy[st];
           const int xx = x + (int)(int16_t)(sxy & 0xffff), yy = y + (sxy >> 16);
           alive = alive && (unsigned)xx < (unsigned)W && (unsigned)yy < (unsigned)H &&
                   ((fb[yy * p.bits_ww + (xx >> 5)] >> (xx & 31)) & 1u) != 0u;
@@ -142,11 +169,11 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
         bool alive = center_ok && !undecided;
         for (int st = tab.ray_start[j]; st < tab.ray_start[j + 1]; ++st) {
           if (!__any_sync(kFull, alive)) break;
-          const int k = tab.step_key[st];
-          const int sxy = tab.step_xy[st];
+          const int k = s_key[st];
+          const int sxy = s_xy[st];
           const int xx = x + (int)(int16_t)(sxy & 0xffff), yy = y + (sxy >> 16);
           const bool inside = (unsigned)xx < (unsigned)W && (unsigned)yy < (unsigned)H;
-          const float zs = (alive && inside) ? fzp[tab.step_lin[st]] : fnan;
+          const float zs = (alive && inside) ? fzp[s_lin[st]] : fnan;
           // NaN / outside: stop with the extremes unchanged; otherwise the
           // extremes take the sample (also on the step that stops the ray)
           const bool fin = zs == zs;
@@ -191,7 +218,7 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
       const uint32_t mk = km[k];
       if (mk == 0u) continue;  // warp-uniform
       if (mk & lbit) {
-        const int kxy = tab.key_xy[k];
+        const int kxy = k_xy[k];
         const int kx = (int)(int16_t)(kxy & 0xffff), ky = kxy >> 16;
         if (tab.wide) {
           ia += (long long)kx * kx;
@@ -202,7 +229,7 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
           jb += kx * ky;
           jg += ky * ky;
         }
-        const double dd = __dsub_rn((double)fdp[tab.key_lin[k]], dc);
+        const double dd = __dsub_rn((double)fdp[k_lin[k]], dc);
         b1 = __fma_rn((double)kx, dd, b1);
         b2 = __fma_rn((double)ky, dd, b2);
       }
@@ -300,11 +327,21 @@ int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& 
   }
   int64_t ga = (n + kAdaptiveThreads - 1) / kAdaptiveThreads;
   if (ga > (int64_t)ctx.num_sms * 64) ga = (int64_t)ctx.num_sms * 64;
+  const size_t sm = star_smem(tab.ray_start[tab.n_rays], tab.n_keys);
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(adaptive_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)star_smem(kStarMaxSteps, kStarMaxKeys)) != cudaSuccess ||
+        cudaFuncSetAttribute(adaptive_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)star_smem(kStarMaxSteps, kStarMaxKeys)) != cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(adaptive_kernel)");
+    attr_set = true;
+  }
   if (stop == 0)
-    adaptive_kernel<0><<<(unsigned)ga, kAdaptiveThreads, 0, ctx.stream>>>(
+    adaptive_kernel<0><<<(unsigned)ga, kAdaptiveThreads, sm, ctx.stream>>>(
         disp, depth, a.fp.bits, a, tab, out6, mask);
   else
-    adaptive_kernel<1><<<(unsigned)ga, kAdaptiveThreads, 0, ctx.stream>>>(
+    adaptive_kernel<1><<<(unsigned)ga, kAdaptiveThreads, sm, ctx.stream>>>(
         disp, depth, nullptr, a, tab, out6, mask);
   return check_launch("adaptive_kernel");
 }
