@@ -41,6 +41,10 @@
 
 namespace sn {
 
+#ifndef SN_EXP
+#define SN_EXP 0
+#endif
+
 constexpr int kTW = 128;           // output columns per item
 constexpr int kG = 16;             // output rows per item
 constexpr int kCP = kG + 1;        // pitch of the column-major C/Rr/Dc arrays (odd)
@@ -623,17 +627,20 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     const T* in = reinterpret_cast<const T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
     mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
-    pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
+    // SN_EXP (experiment builds only, tools/exp_fused.sh; 0 in the product):
+    // 1 no TMA stores, 2 no pass H, 3 no pass V, 4 neither pass
+    if (SN_EXP != 3 && SN_EXP != 4) pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
     // staging of the previous item consumed by its TMA stores (issued by warp 8)
     if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait_read0();
     __syncthreads();
 
-    if (tid < 256) pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
+    if (SN_EXP != 2 && SN_EXP != 4)
+      if (tid < 256) pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
     fence_proxy_async_smem();
     __syncthreads();
     // one TMA store per 128-B box column, one lane each, from a warp that is
     // idle in pass H -- warp 0 goes straight on to the next item
-    if (tid >= kStoreTid && tid < kStoreTid + kBoxes) {
+    if (SN_EXP != 1 && tid >= kStoreTid && tid < kStoreTid + kBoxes) {
       const int b = tid - kStoreTid;
       tma_store_3d(&out_map, smem + Cfg::STAGE + (size_t)b * kG * 128, x0 * 6 + b * kBoxF, y0, bz);
       bulk_commit();
