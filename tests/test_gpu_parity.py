@@ -347,3 +347,23 @@ def test_compact_cloud(cuda_dev, shape):
     assert np.array_equal(offsets.numpy(), np.concatenate([[0], np.cumsum(counts)]))
     ply = formats.ply_from_vertices(cloud.cpu().numpy())
     assert ply.endswith(want.astype("<f4").tobytes())
+
+
+def test_c_demo_runs(cuda_dev, tmp_path):
+    """The plain-C client (examples/sn_demo.c) runs the whole pipeline through
+    sn_pipeline_host: tilted-plane normals vs the closed form, masks and the
+    single-component labels."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    lib = root / "paper_2504_15121_b200" / "libsn_b200.so"
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc missing")
+    exe = tmp_path / "sn_demo"
+    subprocess.run(["gcc", "-O2", f"-I{root / 'include'}", str(root / "examples" / "sn_demo.c"),
+                    f"-L{lib.parent}", "-lsn_b200", f"-Wl,-rpath,{lib.parent}", "-lm", "-o",
+                    str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "mask errors 0" in r.stdout and "label errors 0" in r.stdout

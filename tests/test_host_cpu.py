@@ -141,3 +141,21 @@ def test_ply_writer_matches_reference_bytes():
         assert formats.ply_from_vertices(np.hstack([pts, nrm]), binary) == z[f"ply_{tag}"].tobytes()
         assert formats.write_ply_oriented(np.zeros((0, 3)), np.zeros((0, 3)), binary) == \
             z[f"empty_{tag}"].tobytes()
+
+
+def test_c_demo_builds_against_the_abi(tmp_path):
+    """examples/sn_demo.c is a plain-C client of include/sn_b200.h: it must
+    compile and link against the in-tree library (run on the GPU in
+    tests/test_gpu_parity.py::test_c_demo_runs)."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    lib = root / "paper_2504_15121_b200" / "libsn_b200.so"
+    if not lib.exists() or shutil.which("gcc") is None:
+        pytest.skip("library or gcc missing")
+    exe = tmp_path / "sn_demo"
+    subprocess.run(["gcc", "-O2", "-Wall", "-Werror", f"-I{root / 'include'}",
+                    str(root / "examples" / "sn_demo.c"), f"-L{lib.parent}", "-lsn_b200",
+                    f"-Wl,-rpath,{lib.parent}", "-lm", "-o", str(exe)], check=True)
+    assert exe.exists()
