@@ -64,3 +64,35 @@ def test_host_pipeline_matches_device(cuda_dev):
     dp, dl = device.pipeline(torch.from_numpy(frames).to(cuda_dev), sc.rig, 9, 0.2)
     assert np.array_equal(np.nan_to_num(pts, nan=7.0), np.nan_to_num(dp.cpu().numpy(), nan=7.0))
     assert np.array_equal(lab, dl.cpu().numpy())
+
+
+def test_c5_eight_strips(cuda_dev):
+    """C5: one 7680x4320 street frame split into 8 strips of
+    540 rows -- points and labels bit-identical to the whole frame, labels
+    equal to the oracle's, normals of an interior crop within 1e-4 deg of the
+    oracle's."""
+    from helpers import max_angle_deg
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import device, scenes
+    from paper_2504_15121_b200.parallel import StripPlan, local_strip_frame
+    sc = scenes.street_scene(7680, 4320)
+    d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.2, 0).astype(np.float32)
+    dt = torch.from_numpy(d).to(cuda_dev)
+    plan = StripPlan.for_kernel(4320, 7680, 8, 9)
+    assert [plan.owned(g) for g in range(8)] == [(540 * g, 540 * (g + 1)) for g in range(8)]
+    pts, lab = local_strip_frame(dt, plan, sc.rig, 9, 0.2)
+    whole = device.oriented_points(dt, sc.rig, 9)[0]
+    whole_lab = device.component_labels(dt, sc.rig, 0.2)[0]
+    assert _nan_eq(pts, whole)
+    assert torch.equal(lab, whole_lab)
+    r = sc.rig
+    orig = orc.Rig(r.fx, r.fy, r.u0, r.v0, r.baseline)
+    assert np.array_equal(whole_lab.cpu().numpy().astype(np.int64),
+                          orc.ccl_labels(d.astype(np.float64), orig, 0.2))
+    # normals: a crop across the strip seam at row 2160 (4-row halo for k = 9)
+    crop = d[2100:2220].astype(np.float64)
+    ref6, ok = orc.oriented_points(crop, orc.Rig(r.fx, r.fy, r.u0, r.v0 - 2100, r.baseline), 9)
+    got = whole[2104:2216].cpu().numpy()
+    okc = ok[4:-4]
+    assert np.array_equal(np.isfinite(got[..., 3:]).all(-1), okc)
+    assert max_angle_deg(got[okc][:, 3:], ref6[4:-4][okc][:, 3:]) < 1e-4
