@@ -143,7 +143,7 @@ def _oracle_record(d, sc_rig, k):
     return {"nmask": ok, "normals": rec[..., 3:], "points": rec[..., :3]}
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C1_noisy", "C3"])
+@pytest.mark.parametrize("cfg", ["C1", "C1_noisy", "C2", "C3"])
 def test_configs_vs_oracle(cuda_dev, cfg):
     from paper_2504_15121_b200 import device, scenes
     from paper_2504_15121_b200.geometry import StereoRig
@@ -153,6 +153,10 @@ def test_configs_vs_oracle(cuda_dev, cfg):
         disp, _ = scenes.plane_disparity(n, -5.0, rig, 640, 480)
         if cfg == "C1_noisy":
             disp = scenes.add_gaussian_noise(disp, 0.2, 7)
+    elif cfg == "C2":  # 2888x1920 curved surface (sphere.scn geometry, fx scaled), sigma 0.2
+        sc = scenes.sphere_scene(2888, 1920)
+        rig = sc.rig
+        disp = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.2, 7)
     else:
         sc = scenes.street_scene(2048, 1024)
         rig = sc.rig
