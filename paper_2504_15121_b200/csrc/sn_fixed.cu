@@ -467,6 +467,19 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
   const uint32_t gsw = (uint32_t)(g & 7);
   const uint32_t rowaddr = stage_base + (uint32_t)g * 128u;
+  // staging address of chunk c (0..11, 16 B) of this run: row chunk
+  // kk = 12q + c lives in box kk >> 3 at swizzled slot (kk & 7) ^ (g & 7).
+  // With 12q = 8(q + q/2) + P, P = 4(q & 1): kk & 7 = (c & 7) ^ P and
+  // kk >> 3 = q + q/2 + (c >> 3) + [P != 0 and c & 4], so with c known at
+  // compile time an address is one register pick, one XOR and one add
+  static_assert(kRun == 8, "staging address identity assumes 12 chunks per run");
+  const uint32_t stg_x = ((uint32_t)(4 * (q & 1)) ^ gsw) << 4;
+  const uint32_t stg_a0 = rowaddr + (uint32_t)(q + (q >> 1)) * (uint32_t)(kG * 128);
+  const uint32_t stg_a1 = stg_a0 + ((q & 1) ? (uint32_t)(kG * 128) : 0u);
+  auto stg_addr = [&](int c) {
+    return ((c & 4) ? stg_a1 : stg_a0) + (uint32_t)(c >> 3) * (uint32_t)(kG * 128) +
+           (((uint32_t)(c & 7) << 4) ^ stg_x);
+  };
   uint32_t validbits = 0;
 
   // sliding sums first (short dependent chain), then independent epilogues
@@ -543,16 +556,10 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
           r[3] = r[4] = r[5] = __int_as_float(0x7fc00000);
       }
     }
-    // pixels (j, j+1) = 12 floats = 3 chunks of the 128B-swizzled staging row
-    const int K = q * (kRun * 6 / 4) + (j >> 1) * 3;  // chunk index in the 768-float row
+    // pixels (j, j+1) = 12 floats = chunks c .. c+2 of the run (stg_addr)
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const int kk = K + t;
-      const uint32_t box = (uint32_t)(kk >> 3);
-      const uint32_t ch = (uint32_t)(kk & 7) ^ gsw;
-      st_shared_v4(rowaddr + box * (uint32_t)(kG * 128) + ch * 16u, o[4 * t], o[4 * t + 1],
-                   o[4 * t + 2], o[4 * t + 3]);
-    }
+    for (int t = 0; t < 3; ++t)
+      st_shared_v4(stg_addr((j >> 1) * 3 + t), o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
   }
   if (mask_out != nullptr && yg < H) {
     uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
