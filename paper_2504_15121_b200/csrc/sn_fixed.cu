@@ -240,6 +240,9 @@ __device__ __forceinline__ void records_pair(double U0, double V0, double U1, do
   // one Newton step: r *= 1.5 - 0.5 s r^2
   const float2 hs = __fmul2_rn(make_float2(-0.5f, -0.5f), __fmul2_rn(s, r));
   r = __fmul2_rn(r, __ffma2_rn(hs, r, make_float2(1.5f, 1.5f)));
+  // an invalid pixel's normal is NaN: one select on r instead of three on n
+  if (!ok0) r.x = __int_as_float(0x7fc00000);
+  if (!ok1) r.y = __int_as_float(0x7fc00000);
   const float2 nx = __fmul2_rn(ax, r), ny = __fmul2_rn(ay, r), nz = __fmul2_rn(az, r);
   o[3] = nx.x;
   o[4] = ny.x;
@@ -254,8 +257,6 @@ __device__ __forceinline__ void records_pair(double U0, double V0, double U1, do
   if (ok1 && !in1)
     normal_from_moments(U1, V1, p.alpha, (double)d1, (double)du.y, (double)dv, p.fx, p.fy, o[9],
                         o[10], o[11]);
-  if (!ok0) o[3] = o[4] = o[5] = __int_as_float(0x7fc00000);
-  if (!ok1) o[9] = o[10] = o[11] = __int_as_float(0x7fc00000);
 }
 
 // ---------------------------------------------------------------------------
