@@ -68,7 +68,9 @@ struct FastCfg {
   static constexpr size_t STAGE_BYTES = (size_t)kBoxes * kG * 128;
   static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
   static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;  // double2 (C, Rr) [NC][kCP]
-  static constexpr size_t FL_BYTES = align_up((size_t)NC * 4, 16);
+  // column flags (NC words) + 8-column block ORs of them (NB words)
+  static constexpr int NB = (NC + 7) / 8;
+  static constexpr size_t FL_BYTES = align_up((size_t)(NC + NB) * 4, 16);
   // single-CTA-pipeline layout (classic kernel: 1 stage, 2 inputs, 1 CR)
   static constexpr size_t STAGE = 0;
   static constexpr size_t IN0 = STAGE + STAGE_BYTES;
@@ -322,6 +324,7 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
                                        const FixedParams& p) {
   using Cfg = FastCfg<R, T>;
   constexpr int BW = Cfg::BW;
+  constexpr int NC = Cfg::NC;
   // all operands live in shared memory: let the compiler emit LDS/STS
   __builtin_assume(__isShared(in));
   __builtin_assume(__isShared(CR));
@@ -336,6 +339,7 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   T raw[NV];
   bool all_small = true;  // every sample finite with |v| <= 2^40 (sliding sums exact)
   uint32_t png_inv = 0;   // PNG16: bit i = sample i is the invalid value
+  uint32_t f16 = 0;       // this unit's column flags (0 for idle lanes)
   if (unit) {
     if constexpr (sizeof(T) == 4) {
       uint32_t mx = 0;
@@ -419,8 +423,16 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
     for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
     // flags of column c, half h: bits 0-7 = support of output row 8h+i holds
     // an invalid sample, bit 8 = the half's sums were computed directly
-    reinterpret_cast<uint16_t*>(fl + c)[h] = (uint16_t)((acc & 0xFFu) | (big ? 0x100u : 0u));
+    f16 = (acc & 0xFFu) | (big ? 0x100u : 0u);
+    reinterpret_cast<uint16_t*>(fl + c)[h] = (uint16_t)f16;
   }
+  // OR of the flags of the 8-column block of c (the warp's lanes are 32
+  // aligned columns of one half): pass H reads 2-3 block words per run
+  // instead of every column's flags
+  f16 |= __shfl_xor_sync(0xffffffffu, f16, 1);
+  f16 |= __shfl_xor_sync(0xffffffffu, f16, 2);
+  f16 |= __shfl_xor_sync(0xffffffffu, f16, 4);
+  if ((c & 7) == 0 && (c >> 3) < Cfg::NB) reinterpret_cast<uint16_t*>(fl + NC + (c >> 3))[h] = (uint16_t)f16;
 }
 
 // pass H + epilogue for lane hl (< 256) of one item
@@ -440,14 +452,16 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   const int q = hl >> 4;  // run of kRun output columns
   const int colbase = q * kRun;
   double cc[NH], rr[NH];
-  uint32_t any = 0;
 #pragma unroll
   for (int i = 0; i < NH; ++i) {
     const double2 v = CR[(colbase + i) * kCP + g];
     cc[i] = v.x;
     rr[i] = v.y;
-    any |= fl[colbase + i];
   }
+  // flags of the run's NH columns: the ORs of its 8-column blocks (pass V)
+  uint32_t any = 0;
+#pragma unroll
+  for (int b = 0; b < (NH + 7) / 8; ++b) any |= fl[Cfg::NC + (colbase >> 3) + b];
   const uint32_t hshift = (uint32_t)(g & 8) * 2;  // 0 or 16: the half of row g
   const bool big = ((any >> (hshift + 8)) & 1u) != 0u;
   uint32_t win = 0;  // bit j: support of output j holds an invalid sample
