@@ -167,6 +167,14 @@ __device__ __forceinline__ bool dpos(T x, const FixedParams& p) {
   return dval(x, p) > 0.0;
 }
 template <>
+__device__ __forceinline__ bool dpos<float>(float x, const FixedParams&) {
+  return x > 0.0f;  // = (double)x > 0, without the conversion
+}
+template <>
+__device__ __forceinline__ float dflt<float>(float x, const FixedParams&) {
+  return x;
+}
+template <>
 __device__ __forceinline__ bool dpos<Png16>(Png16 x, const FixedParams& p) {
   // the caller's window test already excludes raw == invalid (the centre is
   // in its own support): only the sign of (raw - 1) / scale is left
