@@ -1,0 +1,103 @@
+"""The C ABI's error contract and concurrency on the device:
+invalid arguments -> SN_EINVAL (ValueError), collinear patterns ->
+SN_EDEGENERATE (DegenerateSupportError), empty batches are no-ops, and calls
+from several host threads on their own streams / workspaces give the same
+results as sequential calls (the reference is safe to call concurrently,
+SPEC.md:97-98)."""
+
+import ctypes
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib_plan(dev):
+    from paper_2504_15121_b200 import _native
+    return _native.load(), _native.plan(dev.index)
+
+
+def test_abi_error_codes(cuda_dev):
+    from paper_2504_15121_b200 import _native, StereoRig
+    lib, plan = _lib_plan(cuda_dev)
+    d = torch.ones((1, 16, 32), device=cuda_dev)
+    out = torch.empty((1, 16, 32, 6), device=cuda_dev)
+    rs = _native.rig_struct(StereoRig(100.0, 100.0, 16.0, 8.0, 0.2))
+    sq = np.array([[dx, dy] for dy in (-1, 0, 1) for dx in (-1, 0, 1)], np.int32)
+    call = lambda *a: lib.sn_oriented_points(*a)  # noqa: E731
+    ok = call(plan, d.data_ptr(), 1, 16, 32, ctypes.byref(rs), sq.ctypes.data, 9, out.data_ptr(),
+              None, None)
+    assert ok == 0
+    # bad shapes / NULL buffers / NULL plan -> 1, with a message
+    assert call(plan, d.data_ptr(), -1, 16, 32, ctypes.byref(rs), sq.ctypes.data, 9,
+                out.data_ptr(), None, None) == 1
+    assert lib.sn_last_error()
+    assert call(plan, None, 1, 16, 32, ctypes.byref(rs), sq.ctypes.data, 9, out.data_ptr(),
+                None, None) == 1
+    assert call(None, d.data_ptr(), 1, 16, 32, ctypes.byref(rs), sq.ctypes.data, 9,
+                out.data_ptr(), None, None) == 1
+    bad = _native.rig_struct(StereoRig(100.0, 100.0, 16.0, 8.0, 0.2))
+    bad.fx = -1.0
+    assert call(plan, d.data_ptr(), 1, 16, 32, ctypes.byref(bad), sq.ctypes.data, 9,
+                out.data_ptr(), None, None) == 1
+    # collinear offsets: degenerate support (kernels.py:91-93) -> 2
+    line = np.array([[-1, 0], [0, 0], [1, 0]], np.int32)
+    assert call(plan, d.data_ptr(), 1, 16, 32, ctypes.byref(rs), line.ctypes.data, 3,
+                out.data_ptr(), None, None) == 2
+    # empty batch: nothing to do, NULL buffers allowed
+    assert call(plan, None, 0, 16, 32, ctypes.byref(rs), sq.ctypes.data, 9, None, None,
+                None) == 0
+    torch.cuda.synchronize()
+
+
+def test_python_errors_map_to_reference_exceptions(cuda_dev):
+    import paper_2504_15121_b200 as sn
+    from paper_2504_15121_b200 import device
+    d = torch.ones((8, 8), device=cuda_dev)
+    with pytest.raises(sn.DegenerateSupportError):
+        device.oriented_points(d, sn.StereoRig(10.0, 10.0, 4.0, 4.0, 0.1),
+                               sn.KernelSpec(np.array([[0, 0], [1, 1], [2, 2]])))
+    with pytest.raises(ValueError):
+        device.component_labels(d, sn.StereoRig(10.0, 10.0, 4.0, 4.0, 0.1), -1.0)
+    with pytest.raises(ValueError):
+        device.oriented_points(d.double().int(), sn.StereoRig(10.0, 10.0, 4.0, 4.0, 0.1), 3)
+
+
+def test_concurrent_host_threads(cuda_dev):
+    """4 host threads, each with its own stream and workspace, run the whole
+    pipeline on different batches at the same time; every result equals the
+    sequential one."""
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(512, 256)
+    clean = scenes.raycast(sc)[0]
+    batches = [torch.from_numpy(np.stack([scenes.add_gaussian_noise(clean, 0.3, 10 * i + j)
+                                          for j in range(3)]).astype(np.float32)).to(cuda_dev)
+               for i in range(4)]
+    ref = [device.pipeline(b, sc.rig, 9, 0.2) for b in batches]
+    torch.cuda.synchronize()
+    got = [None] * 4
+    errors = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream(cuda_dev)
+            with torch.cuda.stream(s):
+                ws = device.ccl_workspace(3, 256, 512, cuda_dev)
+                for _ in range(3):
+                    got[i] = device.pipeline(batches[i], sc.rig, 9, 0.2, workspace=ws)
+            s.synchronize()
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (p0, l0), (p1, l1) in zip(ref, got):
+        assert torch.equal(torch.nan_to_num(p0, 7.0), torch.nan_to_num(p1, 7.0))
+        assert torch.equal(l0, l1)
