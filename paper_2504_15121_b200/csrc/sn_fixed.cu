@@ -340,7 +340,6 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   constexpr int NWIN = 2 * R + 1;
   constexpr int HG = kG / 2;      // rows per pass-V unit
   constexpr int NV = HG + 2 * R;  // input rows read per pass-V unit
-  constexpr int kBlocks = kHalfUnits / 32;
   const int gx = x0 - R + c;
   const int r0 = h * HG;  // first input row of the unit (item-relative, incl. halo)
   const T* col = in + r0 * BW + c + sh;
@@ -620,7 +619,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
   const uint32_t stage_base = smem_u32(smem + Cfg::STAGE);
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int W = (int)p.W, H = (int)p.H;
 
   int item = blockIdx.x;
