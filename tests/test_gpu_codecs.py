@@ -114,21 +114,22 @@ def test_oriented_points_png16_golden(codec_golden, cuda_dev, name):
     assert np.array_equal(np.isnan(a), np.isnan(b))
 
 
-def test_oriented_points_png16_batched(cuda_dev):
-    """Batch of frames with invalid holes, vs the fp32 path on the decoded values
-    (power-of-two scale: dequantised values are exact in fp32)."""
+@pytest.mark.parametrize("B,H,W,k", [(3, 96, 136, 7), (2, 101, 72, 9), (1, 17, 8, 3),
+                                     (2, 64, 520, 17)])
+def test_oriented_points_png16_batched(cuda_dev, B, H, W, k):
+    """Batches with invalid holes and ragged tiles, vs the fp32 path on the
+    decoded values (power-of-two scale: dequantised values are exact in fp32)."""
     from paper_2504_15121_b200 import KernelSpec, StereoRig, device
-    rng = np.random.default_rng(5)
-    B, H, W = 3, 96, 136
+    rng = np.random.default_rng(5 + H)
     raw = rng.integers(2000, 9000, (B, H, W)).astype(np.uint16)
     raw[rng.random(raw.shape) < 0.01] = 0
     rig = StereoRig(200.0, 210.0, 70.0, 45.0, 0.3)
     r = torch.from_numpy(raw).to(cuda_dev)
     m1 = torch.empty((B, H, W), dtype=torch.uint8, device=cuda_dev)
     m2 = torch.empty_like(m1)
-    o1 = device.oriented_points_png16(r, rig, KernelSpec.square(7), scale=64.0, mask=m1)
+    o1 = device.oriented_points_png16(r, rig, KernelSpec.square(k), scale=64.0, mask=m1)
     d = device.dequant_png16(r, 64.0, 0, dtype=torch.float32)
-    o2 = device.oriented_points(d, rig, KernelSpec.square(7), mask=m2)
+    o2 = device.oriented_points(d, rig, KernelSpec.square(k), mask=m2)
     torch.cuda.synchronize()
     assert torch.equal(m1, m2)
     assert _bits_equal(o1.cpu().numpy(), o2.cpu().numpy())
