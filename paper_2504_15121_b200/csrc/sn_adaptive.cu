@@ -151,18 +151,26 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
         }
       }
     } else {
-      // fp32 filter of the CD decisions: with z32 = RN32(z), the running
-      // extremes are RN32 of the fp64 ones, so |(max32 - min32) - (max - min)|
-      // <= 3 * 2^-24 max; a step is decided when the fp32 range clears the
-      // fp32 limit by the margin 2^-20 (max + limit) (which also covers the
-      // fp64 rounding of the reference's subtraction and of t * z_c); an
-      // undecided step, or a depth outside [2^-100, 2^100], sends the lane to
-      // the exact fp64 walk
+      // fp32 filter of the CD decisions.  With z32 = RN32(z) (u = 2^-24),
+      // the running extremes are RN32 of the fp64 ones (rounding is
+      // monotonic), so the fp32 range r is within 3.02 u M of max - min, and
+      // the reference's RN64 subtraction and RN64(t z_c) add 2^-53 M and
+      // u L.  A keep decision (r < l - m0) implies M <= (z_c + L)(1 + 4u),
+      // so the per-pixel margin m0 = 2^-19 (z_c + 2 L) covers it with room to
+      // spare; a stop decision (r > l + m0) is safe for any M (large M only
+      // widens r - L).  Undecided steps, or depths outside [2^-100, 2^100],
+      // send the lane to the exact fp64 walk.
       const double limit = __dmul_rn(ap.threshold, zc);
       const float lim32 = (float)limit, zc32 = (float)zc;
       undecided = center_ok && !(zc32 >= 7.888609052210118e-31f && zc32 <= 1.2676506002282294e30f &&
                                  lim32 >= 7.888609052210118e-31f && lim32 <= 1.2676506002282294e30f);
+      const float m0 = (zc32 + 2.0f * lim32) * 1.9073486328125e-06f;  // 2^-19
+      const float lo = lim32 - m0, hi = lim32 + m0;
       const float* fzp = depth + f * HW + pix;  // this lane's pixel
+      // warps whose pixels all lie at least `reach` from the border skip the
+      // per-step bounds test
+      const bool interior = __all_sync(kFull, !have || (x >= tab.reach && x < W - tab.reach &&
+                                                        y >= tab.reach && y < H - tab.reach));
       float rmax = zc32, rmin = zc32;
       for (int j = 0; j < tab.n_rays; ++j) {
         if (!ap.shared_range) rmax = rmin = zc32;
@@ -170,25 +178,26 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
         for (int st = tab.ray_start[j]; st < tab.ray_start[j + 1]; ++st) {
           if (!__any_sync(kFull, alive)) break;
           const int k = s_key[st];
-          const int sxy = s_xy[st];
-          const int xx = x + (int)(int16_t)(sxy & 0xffff), yy = y + (sxy >> 16);
-          const bool inside = (unsigned)xx < (unsigned)W && (unsigned)yy < (unsigned)H;
+          bool inside = true;
+          if (!interior) {
+            const int sxy = s_xy[st];
+            const int xx = x + (int)(int16_t)(sxy & 0xffff), yy = y + (sxy >> 16);
+            inside = (unsigned)xx < (unsigned)W && (unsigned)yy < (unsigned)H;
+          }
           const float zs = (alive && inside) ? fzp[s_lin[st]] : fnan;
           // NaN / outside: stop with the extremes unchanged; otherwise the
           // extremes take the sample (also on the step that stops the ray)
           const bool fin = zs == zs;
+          const bool inr = zs >= 7.888609052210118e-31f && zs <= 1.2676506002282294e30f;
           const float nmax = fmaxf(rmax, zs), nmin = fminf(rmin, zs);
           const float range = nmax - nmin;
-          const float marg = (nmax + lim32) * 9.5367431640625e-07f;  // 2^-20
-          const bool inr = nmax <= 1.2676506002282294e30f && nmin >= 7.888609052210118e-31f;
-          const bool keep = range < lim32 - marg;
-          const bool over = range > lim32 + marg;
+          const bool keep = range < lo;
           if (alive && fin) {
             rmax = nmax;
             rmin = nmin;
-            if (!inr || !(keep || over)) undecided = true;
+            if (!inr || !(keep || range > hi)) undecided = true;
           }
-          alive = alive && fin && inr && keep;
+          alive = alive && inr && keep;
           const uint32_t b = __ballot_sync(kFull, alive);
           if (lane == 0 && b) km[k] |= b;
         }

@@ -532,8 +532,10 @@ int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
   // over all keys) pick 32- or 64-bit accumulation
   {
     int64_t sxx = 0, sxy = 0, syy = 0;
+    tab.reach = 0;
     for (int k = 0; k < tab.n_keys; ++k) {
       const int64_t vx = (int16_t)(tab.key_xy[k] & 0xffff), vy = (int16_t)(tab.key_xy[k] >> 16);
+      tab.reach = (int)std::max<int64_t>(tab.reach, std::max(std::llabs(vx), std::llabs(vy)));
       if (std::llabs(vy) * W + std::llabs(vx) > 0x7fffffffLL)
         return set_error(SN_EINVAL, "ray offsets too large for the frame width");
       sxx += vx * vx;

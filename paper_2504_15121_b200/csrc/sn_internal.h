@@ -69,6 +69,7 @@ constexpr int kStarMaxKeys = kStarKeyWords * 32;  // 512 distinct offsets
 struct StarTable {
   int n_rays, n_keys;
   int wide;                         // moment sums may exceed int32: 64-bit accumulation
+  int reach;                        // max |x|, |y| over the offsets
   int ray_start[kStarMaxRays + 1];  // steps of ray j: [ray_start[j], ray_start[j+1])
   int16_t step_key[kStarMaxSteps];  // key of each step
   int32_t step_xy[kStarMaxSteps];   // offset of each step: x in the low, y in the high 16 bits
