@@ -399,3 +399,18 @@ def test_c4_labels_vs_oracle(cuda_dev, t):
         assert np.array_equal(lab[i].astype(np.int64), ref)
         one = device.component_labels(dt[i], sc.rig, t)[0].cpu().numpy()
         assert np.array_equal(one, lab[i])
+
+
+@pytest.mark.parametrize("k", [11, 13, 17])
+def test_large_kernels_vs_oracle(cuda_dev, k):
+    """Square kernels beyond the golden set (R = 5, 6, 8: the largest fast-path
+    radius) on a noisy street crop with holes, against the oracle."""
+    from scipy import ndimage
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(512, 256)
+    d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.5, k)
+    d[ndimage.binary_dilation(np.random.default_rng(k).random(d.shape) < 0.001, iterations=2)] = np.nan
+    d = d.astype(np.float32)
+    mask = torch.empty((1,) + d.shape, dtype=torch.uint8, device=cuda_dev)
+    out = device.oriented_points(torch.from_numpy(d).to(cuda_dev), sc.rig, k, mask=mask)
+    _check_record(out[0].cpu().numpy(), mask[0].cpu().numpy(), _oracle_record(d, sc.rig, k))
