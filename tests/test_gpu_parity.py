@@ -401,10 +401,11 @@ def test_c4_labels_vs_oracle(cuda_dev, t):
         assert np.array_equal(one, lab[i])
 
 
-@pytest.mark.parametrize("k", [11, 13, 17])
+@pytest.mark.parametrize("k", [11, 13, 17, 21])
 def test_large_kernels_vs_oracle(cuda_dev, k):
     """Square kernels beyond the golden set (R = 5, 6, 8: the largest fast-path
-    radius) on a noisy street crop with holes, against the oracle."""
+    radius; 21 takes the generic kernel) on a noisy street crop with holes,
+    against the oracle."""
     from scipy import ndimage
     from paper_2504_15121_b200 import device, scenes
     sc = scenes.street_scene(512, 256)
