@@ -311,6 +311,40 @@ struct ItemDecoder {
   }
 };
 
+// the persistent loop's item coordinates, advanced by gridDim.x items per
+// step as a mixed-radix addition (one decode per CTA instead of one per item
+// and thread); the step's digits are each below their radix, so one carry
+// per digit at most
+struct ItemWalk {
+  int tx, ty, bz, dtx, dty, dbz, tiles_x, tiles_y;
+  __device__ ItemWalk(const ItemDecoder& dec, int item, int step)
+      : tiles_x(dec.tiles_x), tiles_y(dec.tiles_y) {
+    dec(item, tx, ty, bz);
+    dec(step, dtx, dty, dbz);
+    tx /= kTW;
+    ty /= kG;
+    dtx /= kTW;
+    dty /= kG;
+  }
+  __device__ void advance() {
+    tx += dtx;
+    int cy = 0;
+    if (tx >= tiles_x) {
+      tx -= tiles_x;
+      cy = 1;
+    }
+    ty += dty + cy;
+    int cz = 0;
+    if (ty >= tiles_y) {
+      ty -= tiles_y;
+      cz = 1;
+    }
+    bz += dbz + cz;
+  }
+  __device__ int x0() const { return tx * kTW; }
+  __device__ int y0() const { return ty * kG; }
+};
+
 // TMA tile origin: the halo origin with its innermost coordinate rounded
 // down to a 16-byte multiple (an unaligned innermost TMA coordinate raises
 // an illegal-instruction fault on this part -- measured with
@@ -625,12 +659,12 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   int item = blockIdx.x;
   if (item >= n_items) return;
   const ItemDecoder decode(tiles_x, tiles_y);
-  auto load_tile = [&](int it, int buf) {
-    int x0, y0, bz;
-    decode(it, x0, y0, bz);
+  ItemWalk cur(decode, item, (int)gridDim.x), nxt = cur;
+  nxt.advance();
+  auto load_tile = [&](const ItemWalk& w, int buf) {
     T* dst = reinterpret_cast<T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
     mbar_arrive_expect_tx(bar + buf, (uint32_t)Cfg::IN_BYTES);
-    tma_load_3d(dst, &in_map, bar + buf, tile_x0<R, AE>(x0), y0 - R, bz);
+    tma_load_3d(dst, &in_map, bar + buf, tile_x0<R, AE>(w.x0()), w.y0() - R, w.bz);
   };
 
   if (tid == 0) {
@@ -639,7 +673,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
     fence_mbar_init();
-    load_tile(item, 0);
+    load_tile(cur, 0);
   }
   __syncthreads();
 
@@ -647,11 +681,10 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   const int c = tid - h * kHalfUnits;
   const bool unit = c < NC;
 
-  for (int it = 0; item < n_items; ++it, item += gridDim.x) {
+  for (int it = 0; item < n_items; ++it, item += gridDim.x, cur = nxt, nxt.advance()) {
     const int buf = it & 1;
-    if (tid == 0 && item + (int)gridDim.x < n_items) load_tile(item + gridDim.x, buf ^ 1);
-    int x0, y0, bz;
-    decode(item, x0, y0, bz);
+    if (tid == 0 && item + (int)gridDim.x < n_items) load_tile(nxt, buf ^ 1);
+    const int x0 = cur.x0(), y0 = cur.y0(), bz = cur.bz;
     const int sh = (x0 - R) - tile_x0<R, AE>(x0);  // logical column c <-> smem column c + sh
     const T* in = reinterpret_cast<const T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
     mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
