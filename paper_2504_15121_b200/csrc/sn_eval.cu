@@ -68,6 +68,18 @@ __device__ __forceinline__ double key_value(uint64_t k) {
 
 __device__ __forceinline__ bool finite_v(double v) { return fabs(v) <= DBL_MAX; }
 
+// a / b correctly rounded from y = RN(1/b): q = RN(a y) is within an ulp of
+// a / b, r = a - q b is exact (FMA) and q + r y rounds to RN(a / b)
+// (Markstein).  Outside 2^-500 <= |b| <= 2^500 (or for non-finite or zero b)
+// the plain division is used, so no intermediate can overflow or underflow.
+__device__ __forceinline__ double div_rn_by(double a, double b, double y) {
+  const double ab = fabs(b);
+  if (!(ab >= 3.054936363499605e-151 && ab <= 3.273390607896142e150)) return a / b;
+  const double q = a * y;
+  const double r = fma(-q, b, a);
+  return fma(r, y, q);
+}
+
 // block-wide sum, valid in every thread (the same order in every thread)
 __device__ __forceinline__ double block_sum_all(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -133,8 +145,12 @@ __global__ void __launch_bounds__(kEvalThreads, 4)
         if (ok) {
           const double en = sqrt(ex * ex + ey * ey + ez * ez);
           const double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
-          const double dot = fabs((ex / en) * (g[0] / gn) + (ey / en) * (g[1] / gn) +
-                                  (ez / en) * (g[2] / gn));
+          // the reference's per-component divisions, correctly rounded: one
+          // reciprocal per vector + Markstein's correction (div_rn_by)
+          const double ye = __drcp_rn(en), yg = __drcp_rn(gn);
+          const double dot = fabs(div_rn_by(ex, en, ye) * div_rn_by(g[0], gn, yg) +
+                                  div_rn_by(ey, en, ye) * div_rn_by(g[1], gn, yg) +
+                                  div_rn_by(ez, en, ye) * div_rn_by(g[2], gn, yg));
           // numpy's clip keeps a NaN (zero-length vector) and arccos(NaN) is NaN
           if (dot == dot) v = acos(fmin(fmax(dot, 0.0), 1.0)) * (180.0 / 3.14159265358979323846);
           if (!finite_v(v)) v = qnan;
