@@ -105,6 +105,19 @@ __device__ __forceinline__ void hist_add(uint32_t* h, bool ok, uint32_t bin) {
   }
 }
 
+// the values k0 .. k0+7 of this thread in chunk ch (NaN past the frame),
+// loaded back to back: the loads are independent of the warp-synchronous
+// histogram / ballot work that follows, so all eight are in flight at once
+constexpr int kBatch = 8;
+__device__ __forceinline__ void load_batch(const double* __restrict__ fe, int64_t HW, int ch,
+                                           int k0, double (&v)[kBatch]) {
+#pragma unroll
+  for (int u = 0; u < kBatch; ++u) {
+    const int64_t i = (int64_t)ch * kEvalChunk + (k0 + u) * kEvalThreads + threadIdx.x;
+    v[u] = i < HW ? __ldcs(fe + i) : __longlong_as_double(0x7ff8000000000000ll);
+  }
+}
+
 __device__ __forceinline__ void flush_hist(const uint32_t* h, uint32_t* dst) {
   for (int i = threadIdx.x; i < kBins; i += kEvalThreads)
     if (h[i]) atomicAdd(&dst[i], h[i]);
@@ -331,20 +344,18 @@ __global__ void __launch_bounds__(kEvalThreads)
   const uint64_t d1 = prefix[f] >> 52;
   const int64_t base = (int64_t)f * HW;
   int any = 0;
-  const int64_t n_iter = (int64_t)((n_chunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * kVpt;
-#pragma unroll 8
-  for (int64_t it = 0; it < n_iter; ++it) {
-    const int ch = (int)blockIdx.x + (int)(it / kVpt) * (int)gridDim.x, k = (int)(it % kVpt);
-    const int64_t i = (int64_t)ch * kEvalChunk + k * kEvalThreads + tid;
-    bool take = false;
-    uint64_t key = 0;
-    if (i < HW) {
-      const double v = err[base + i];
-      key = order_key(v);
-      take = finite_v(v) && (key >> 52) == d1;
+  for (int ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    for (int k0 = 0; k0 < kVpt; k0 += kBatch) {
+      double v[kBatch];
+      load_batch(err + base, HW, ch, k0, v);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const uint64_t key = order_key(v[u]);
+        const bool take = finite_v(v[u]) && (key >> 52) == d1;
+        any |= take;
+        hist_add(h, take, (uint32_t)(key >> 40) & 0xfffu);
+      }
     }
-    any |= take;
-    hist_add(h, take, (uint32_t)(key >> 40) & 0xfffu);
   }
   if (__syncthreads_or(any)) flush_hist(h, hist2 + (int64_t)f * kBins);
 }
@@ -376,20 +387,14 @@ __global__ void __launch_bounds__(kEvalThreads)
   const uint64_t p24 = prefix[f] >> 40;
   const int64_t base = (int64_t)f * HW;
   uint64_t* cf = cand + (int64_t)f * cap;
-  const int64_t n_iter = (int64_t)((n_chunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * kVpt;
-#pragma unroll 8
-  for (int64_t it = 0; it < n_iter; ++it) {
-    const int ch = (int)blockIdx.x + (int)(it / kVpt) * (int)gridDim.x, k = (int)(it % kVpt);
-    const int64_t i = (int64_t)ch * kEvalChunk + k * kEvalThreads + tid;
-    bool take = false;
-    uint64_t key = 0;
-    if (i < HW) {
-      const double v = err[base + i];
-      if (finite_v(v)) {
-        key = order_key(v);
-        take = (key >> 40) == p24;
-      }
-    }
+  for (int ch = blockIdx.x; ch < n_chunks; ch += gridDim.x)
+    for (int k0 = 0; k0 < kVpt; k0 += kBatch) {
+      double v[kBatch];
+      load_batch(err + base, HW, ch, k0, v);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+    const uint64_t key = order_key(v[u]);
+    const bool take = finite_v(v[u]) && (key >> 40) == p24;
     const uint32_t b = __ballot_sync(0xffffffffu, take);
     if (b) {  // one atomic per warp
       const int leader = __ffs(b) - 1;
@@ -398,7 +403,8 @@ __global__ void __launch_bounds__(kEvalThreads)
       at = __shfl_sync(0xffffffffu, at, leader);
       if (take) cf[at + __popc(b & ((1u << lane) - 1u))] = key;
     }
-  }
+      }
+    }
 }
 
 // one CTA per frame: radix select of key bits 39..0 over the candidates
