@@ -142,14 +142,30 @@ __global__ void __launch_bounds__(kEvalThreads, 4)
   // a CTA takes chunks blockIdx.x, + gridDim.x, ... (one histogram flush)
   for (int ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
   double cnt = 0.0, sum = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+  auto accumulate = [&](double v) {
+    const bool ok = finite_v(v);
+    if (ok) {
+      cnt += 1.0;
+      sum += v;
+      mn = fmin(mn, v);
+      mx = fmax(mx, v);
+    }
+    hist_add(h, ok, (uint32_t)(order_key(v) >> 52));
+  };
+  if (SRC == 0) {  // the caller's map: batched streaming loads
+    for (int k0 = 0; k0 < kVpt; k0 += kBatch) {
+      double vb[kBatch];
+      load_batch(err + base, HW, ch, k0, vb);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) accumulate(vb[u]);
+    }
+  } else {
 #pragma unroll 4
   for (int k = 0; k < kVpt; ++k) {
     const int64_t i = (int64_t)ch * kEvalChunk + k * kEvalThreads + tid;
     double v = qnan;
     if (i < HW) {
-      if (SRC == 0) {
-        v = err[base + i];
-      } else {
+      {
         const TE* e = est + (base + i) * est_stride;
         const double* g = gt + (base + i) * 3;
         const double ex = e[0], ey = e[1], ez = e[2];
@@ -171,14 +187,8 @@ __global__ void __launch_bounds__(kEvalThreads, 4)
         err[base + i] = v;
       }
     }
-    const bool ok = finite_v(v);
-    if (ok) {
-      cnt += 1.0;
-      sum += v;
-      mn = fmin(mn, v);
-      mx = fmax(mx, v);
-    }
-    hist_add(h, ok, (uint32_t)(order_key(v) >> 52));
+    accumulate(v);
+  }
   }
   const double c = block_sum_all(cnt, red);
   const double s = block_sum_all(sum, red);
@@ -186,13 +196,12 @@ __global__ void __launch_bounds__(kEvalThreads, 4)
   // squared deviations from the chunk mean: the chunk's values again (this
   // CTA just wrote / read them: L2 hits)
   double dev = 0.0;
-#pragma unroll 8
-  for (int k = 0; k < kVpt; ++k) {
-    const int64_t i = (int64_t)ch * kEvalChunk + k * kEvalThreads + tid;
-    if (i < HW) {
-      const double v = err[base + i];
-      if (finite_v(v)) dev += (v - m) * (v - m);
-    }
+  for (int k0 = 0; k0 < kVpt; k0 += kBatch) {
+    double vb[kBatch];
+    load_batch(err + base, HW, ch, k0, vb);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (finite_v(vb[u])) dev += (vb[u] - m) * (vb[u] - m);
   }
   const double m2 = block_sum_all(dev, red);
 #pragma unroll
