@@ -285,6 +285,16 @@ SN_API int sn_oriented_points_png16(sn_plan_t* plan, const uint16_t* raw, int64_
                              const int32_t* offsets_xy, int32_t n_off, float* out6,
                              uint8_t* mask, void* stream);
 
+/* The two halves of sn_compact_cloud, for callers that size the output from
+ * the count: sn_cloud_count writes frame_offsets (device, B + 1; the total in
+ * offsets[B]) and leaves the block scan in the workspace; sn_cloud_scatter
+ * then writes the vertices, given the same mask and workspace. */
+SN_API int sn_cloud_count(sn_plan_t* plan, const uint8_t* mask, int64_t B, int64_t H, int64_t W,
+                   int64_t* frame_offsets, void* workspace, size_t ws_bytes, void* stream);
+SN_API int sn_cloud_scatter(sn_plan_t* plan, const float* out6, const uint8_t* mask, int64_t B,
+                     int64_t H, int64_t W, float* cloud, int64_t capacity, void* workspace,
+                     size_t ws_bytes, void* stream);
+
 /* Test hook: the fixed pass forced onto the generic (non-TMA) kernel, used to
  * cross-check the TMA fast path on identical inputs. */
 SN_API int sn_oriented_points_generic(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,

@@ -76,6 +76,8 @@ SIGNATURES = {
                                  _P],
     "sn_cloud_workspace_bytes": [_I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
     "sn_compact_cloud": [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P],
+    "sn_cloud_count": [_P, _P, _I64, _I64, _I64, _P, _P, ctypes.c_size_t, _P],
+    "sn_cloud_scatter": [_P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, ctypes.c_size_t, _P],
     "sn_pipeline": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P],
     "sn_pipeline_ws": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P,
                        ctypes.c_size_t, _P],

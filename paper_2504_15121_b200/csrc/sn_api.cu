@@ -473,6 +473,31 @@ int sn_compact_cloud(sn_plan_t* plan, const float* out6, const uint8_t* mask, in
                            frame_offsets, workspace, ws_bytes);
 }
 
+int sn_cloud_count(sn_plan_t* plan, const uint8_t* mask, int64_t B, int64_t H, int64_t W,
+                   int64_t* frame_offsets, void* workspace, size_t ws_bytes, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (!frame_offsets || (B * H * W > 0 && !mask)) return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_cloud_count(make_ctx(plan, stream), mask, B, H, W, frame_offsets, workspace,
+                         ws_bytes);
+}
+
+int sn_cloud_scatter(sn_plan_t* plan, const float* out6, const uint8_t* mask, int64_t B,
+                     int64_t H, int64_t W, float* cloud, int64_t capacity, void* workspace,
+                     size_t ws_bytes, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (capacity < 0) return set_error(SN_EINVAL, "negative capacity");
+  if (B * H * W > 0 && capacity > 0 && (!out6 || !mask || !cloud))
+    return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_cloud_scatter(make_ctx(plan, stream), out6, mask, B, H, W, cloud, capacity, workspace,
+                           ws_bytes);
+}
+
 int sn_adaptive_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
   if (!bytes) return set_error(SN_EINVAL, "bytes out-pointer is NULL");
   int rc = check_shape(B, H, W);

@@ -89,46 +89,52 @@ __global__ void __launch_bounds__(1024) cloud_scan_kernel(int64_t* __restrict__ 
   if (tid == 0) counts[n] = carry;
 }
 
+// each warp owns a contiguous 256-pixel segment of the 2048-pixel block: it
+// counts its segment (8 ballots), one block-wide exclusive scan of the 8
+// warp counts gives its start, then it scatters its segment alone (ballot +
+// popc per 32 pixels) -- one CTA barrier per block instead of two per 256
+// pixels
+constexpr int kSegPx = kCloudBlock / (kCloudThreads / 32);  // 256
+
 __global__ void __launch_bounds__(kCloudThreads)
     cloud_scatter_kernel(const float* __restrict__ out6, const uint8_t* __restrict__ mask,
                          int64_t HW, int bpf, int64_t n_blocks, const int64_t* __restrict__ starts,
                          float* __restrict__ cloud, int64_t capacity) {
-  __shared__ int warp_off[kCloudThreads / 32 + 1];
+  __shared__ int warp_cnt[kCloudThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
     const int64_t f = blk / bpf;
-    const int64_t p0 = (blk - f * bpf) * kCloudBlock;
+    const int64_t s0 = (blk - f * bpf) * kCloudBlock + warp * kSegPx;  // segment start in the frame
     const uint8_t* m = mask + f * HW;
+    uint32_t bal[kSegPx / 32];
+    int c = 0;
+#pragma unroll
+    for (int r = 0; r < kSegPx / 32; ++r) {
+      const int64_t px = s0 + r * 32 + lane;
+      bal[r] = __ballot_sync(0xffffffffu, px < HW && m[px] != 0);
+      c += __popc(bal[r]);
+    }
+    if (lane == 0) warp_cnt[warp] = c;
+    __syncthreads();
     int64_t next = starts[blk];
-    // the block's pixels in rounds of 256: each round keeps raster order
-    for (int r0 = 0; r0 < kCloudBlock; r0 += kCloudThreads) {
-      const int64_t px = p0 + r0 + tid;
-      const bool keep = px < HW && m[px] != 0;
-      const uint32_t b = __ballot_sync(0xffffffffu, keep);
-      if (lane == 0) warp_off[warp] = __popc(b);
-      __syncthreads();
-      if (tid == 0) {
-        int s = 0;
-        for (int w = 0; w < kCloudThreads / 32; ++w) {
-          const int c = warp_off[w];
-          warp_off[w] = s;
-          s += c;
-        }
-        warp_off[kCloudThreads / 32] = s;
-      }
-      __syncthreads();
-      if (keep) {
-        const int64_t slot = next + warp_off[warp] + __popc(b & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; ++w) next += warp_cnt[w];
+    __syncthreads();  // warp_cnt is rewritten by the next block
+#pragma unroll
+    for (int r = 0; r < kSegPx / 32; ++r) {
+      const uint32_t b = bal[r];
+      if ((b >> lane) & 1u) {
+        const int64_t px = s0 + r * 32 + lane;
+        const int64_t slot = next + __popc(b & ((1u << lane) - 1u));
         if (slot < capacity) {
           const float2* src = reinterpret_cast<const float2*>(out6 + (f * HW + px) * 6);
           float2* dst = reinterpret_cast<float2*>(cloud + slot * 6);
-          dst[0] = src[0];
-          dst[1] = src[1];
-          dst[2] = src[2];
+          const float2 a0 = src[0], a1 = src[1], a2 = src[2];
+          dst[0] = a0;
+          dst[1] = a1;
+          dst[2] = a2;
         }
       }
-      next += warp_off[kCloudThreads / 32];
-      __syncthreads();
+      next += __popc(b);
     }
   }
 }
@@ -138,9 +144,8 @@ size_t cloud_workspace_bytes(int64_t B, int64_t H, int64_t W) {
   return (size_t)(B * bpf + 1) * sizeof(int64_t);
 }
 
-int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
-                      int64_t H, int64_t W, float* cloud, int64_t capacity,
-                      int64_t* frame_offsets, void* workspace, size_t ws_bytes) {
+int run_cloud_count(const LaunchCtx& ctx, const uint8_t* mask, int64_t B, int64_t H, int64_t W,
+                    int64_t* frame_offsets, void* workspace, size_t ws_bytes) {
   const int64_t HW = H * W;
   if (B * HW == 0) {
     return cudaMemsetAsync(frame_offsets, 0, (size_t)(B + 1) * sizeof(int64_t), ctx.stream) ==
@@ -163,9 +168,6 @@ int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* ma
   if (rc) return rc;
   cloud_scan_kernel<<<1, 1024, 0, ctx.stream>>>(counts, n_blocks);
   if ((rc = check_launch("cloud_scan_kernel"))) return rc;
-  cloud_scatter_kernel<<<(unsigned)grid, kCloudThreads, 0, ctx.stream>>>(
-      out6, mask, HW, bpf, n_blocks, counts, cloud, capacity);
-  if ((rc = check_launch("cloud_scatter_kernel"))) return rc;
   // frame offsets: the scan at each frame's first block, and the total
   if (cudaMemcpy2DAsync(frame_offsets, sizeof(int64_t), counts, (size_t)bpf * sizeof(int64_t),
                         sizeof(int64_t), (size_t)B, cudaMemcpyDeviceToDevice,
@@ -174,6 +176,32 @@ int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* ma
                       cudaMemcpyDeviceToDevice, ctx.stream) != cudaSuccess)
     return set_cuda_error("frame offsets copy");
   return SN_OK;
+}
+
+int run_cloud_scatter(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
+                      int64_t H, int64_t W, float* cloud, int64_t capacity, void* workspace,
+                      size_t ws_bytes) {
+  const int64_t HW = H * W;
+  if (B * HW == 0 || capacity == 0) return SN_OK;
+  if (!workspace || ws_bytes < cloud_workspace_bytes(B, H, W))
+    return set_error(SN_EINVAL, "compaction workspace too small");
+  const int64_t bpf64 = (HW + kCloudBlock - 1) / kCloudBlock;
+  if (bpf64 > 0x7fffffffLL) return set_error(SN_EINVAL, "frame too large");
+  const int bpf = (int)bpf64;
+  const int64_t n_blocks = B * bpf64;
+  int64_t grid = n_blocks;
+  if (grid > (int64_t)ctx.num_sms * 16) grid = (int64_t)ctx.num_sms * 16;
+  cloud_scatter_kernel<<<(unsigned)grid, kCloudThreads, 0, ctx.stream>>>(
+      out6, mask, HW, bpf, n_blocks, static_cast<const int64_t*>(workspace), cloud, capacity);
+  return check_launch("cloud_scatter_kernel");
+}
+
+int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
+                      int64_t H, int64_t W, float* cloud, int64_t capacity,
+                      int64_t* frame_offsets, void* workspace, size_t ws_bytes) {
+  const int rc = run_cloud_count(ctx, mask, B, H, W, frame_offsets, workspace, ws_bytes);
+  if (rc) return rc;
+  return run_cloud_scatter(ctx, out6, mask, B, H, W, cloud, capacity, workspace, ws_bytes);
 }
 
 }  // namespace sn

@@ -110,6 +110,11 @@ int run_decode_pfm(const LaunchCtx& ctx, const void* payload, int64_t B, int64_t
                    bool big_endian, float* out);
 
 size_t cloud_workspace_bytes(int64_t B, int64_t H, int64_t W);
+int run_cloud_count(const LaunchCtx& ctx, const uint8_t* mask, int64_t B, int64_t H, int64_t W,
+                    int64_t* frame_offsets, void* workspace, size_t ws_bytes);
+int run_cloud_scatter(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
+                      int64_t H, int64_t W, float* cloud, int64_t capacity, void* workspace,
+                      size_t ws_bytes);
 int run_compact_cloud(const LaunchCtx& ctx, const float* out6, const uint8_t* mask, int64_t B,
                       int64_t H, int64_t W, float* cloud, int64_t capacity,
                       int64_t* frame_offsets, void* workspace, size_t ws_bytes);

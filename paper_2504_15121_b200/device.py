@@ -291,17 +291,16 @@ def compact_cloud(records: torch.Tensor, mask: torch.Tensor):
     offsets = torch.empty(B + 1, dtype=torch.int64, device=dev)
     lib = _native.load()
 
-    def run(cloud, cap):
-        rc = lib.sn_compact_cloud(_native.plan(dev.index), records.data_ptr(), mask.data_ptr(),
-                                  B, H, W, cloud.data_ptr() if cloud is not None else None, cap,
-                                  offsets.data_ptr(), ws.data_ptr(), n.value, _stream(dev))
-        check(rc, "compact_cloud")
-
-    run(None, 0)  # counts only: the total decides the allocation
+    plan = _native.plan(dev.index)
+    # count + scan, read the total back to size the output, then scatter
+    check(lib.sn_cloud_count(plan, mask.data_ptr(), B, H, W, offsets.data_ptr(), ws.data_ptr(),
+                             n.value, _stream(dev)), "compact_cloud")
     total = int(offsets[B].item())
     cloud = torch.empty((total, 6), dtype=torch.float32, device=dev)
     if total:
-        run(cloud, total)
+        check(lib.sn_cloud_scatter(plan, records.data_ptr(), mask.data_ptr(), B, H, W,
+                                   cloud.data_ptr(), total, ws.data_ptr(), n.value, _stream(dev)),
+              "compact_cloud")
     return cloud, offsets.cpu()
 
 
