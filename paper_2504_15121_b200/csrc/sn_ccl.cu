@@ -555,12 +555,16 @@ __global__ void __launch_bounds__(kLThreads)
       const uint32_t A = bits[r * kLWords + w];
       const uint32_t st = run_starts(band_word(bits, r >> 1, w));
       const int base = lp((r >> 1) * kLTW + w * 32);  // a 32-slot group: lp(base + b) = base + b
+      // run start of the lane's first pixel (the highest start <= sub), then
+      // carried along the 4 pixels: a pixel in the band run starts a new slot
+      // only where the band word has a run start
+      const uint32_t ab = A >> sub, sb = st >> sub;
+      int s = 31 - __clz(st & ((2u << sub) - 1u));  // sub <= 28
       int v[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int b = sub + j;
-        const uint32_t upto = (b == 31) ? 0xffffffffu : ((2u << b) - 1u);
-        v[j] = ((A >> b) & 1u) ? lab[base + (31 - __clz(st & upto))] : -1;
+        if (j > 0 && ((sb >> j) & 1u)) s = sub + j;
+        v[j] = ((ab >> j) & 1u) ? lab[base + s] : -1;
       }
       *reinterpret_cast<int4*>(out + (y0 + r) * W + x0 + w * 32 + sub) =
           make_int4(v[0], v[1], v[2], v[3]);
