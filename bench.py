@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=16, help="cpu_baseline sample (frames)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the short timings of the next-row kernels (adaptive, cloud, "
+                         "evaluation, PNG16 input)")
     return ap.parse_args()
 
 
@@ -198,6 +201,42 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------
 # GPU arm
+
+
+def next_row_timings(d8, out8, rig, dev):
+    """us/frame of the f1-f4 kernels on 8 C3 frames (CUDA events, 3 reps)."""
+    import torch
+    from paper_2504_15121_b200 import StarConfig, device, scenes
+    n = d8.shape[0]
+    mask = torch.empty(d8.shape, dtype=torch.uint8, device=dev)
+    device.oriented_points(d8, rig, KSIZE, out=out8, mask=mask)
+    sc = scenes.street_scene(W, H)
+    gt = torch.from_numpy(np.ascontiguousarray(scenes.raycast(sc)[2])).to(dev)
+    gt = gt.expand(n, -1, -1, -1).contiguous()
+    gm = torch.isfinite(gt).all(-1).to(torch.uint8)
+    raw = torch.clamp(torch.round(d8 * 256 + 1), 1, 65535).to(torch.int32).to(torch.uint16)
+    cd, st = StarConfig(stop="cd", threshold=0.1), StarConfig(stop="st", threshold=0.2)
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return round(e0.elapsed_time(e1) * 1e3 / reps / n, 2)
+
+    return {
+        "frames": n,
+        "adaptive_cd_s10_d8": timed(lambda: device.adaptive_points(d8, rig, cd, out=out8)),
+        "adaptive_st_s10_d8": timed(lambda: device.adaptive_points(d8, rig, st, out=out8)),
+        "compact_cloud": timed(lambda: device.compact_cloud(out8, mask)),
+        "angular_error_and_stats": timed(lambda: device.angular_error(out8, gt, gm)),
+        "fused_pass_png16_input": timed(lambda: device.oriented_points_png16(
+            raw, rig, KSIZE, scale=256.0, out=out8)),
+    }
 
 
 def main():
@@ -349,6 +388,15 @@ def main():
                "path": ("sn_pipeline_host" if full else "sn_oriented_points_host") +
                        " (pinned host in/out, 3-stream H2D/compute/D2H overlap)"}
 
+    # next rows of the scope table, timed briefly on 8 of the
+    # same frames after the headline measurement: evidence, not the metric
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        try:
+            extras = next_row_timings(disp[:8], out[:8], rig, dev)
+        except Exception as exc:  # never let an extra cost the headline line
+            extras = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
@@ -381,6 +429,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback"},
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "next_rows_us_per_frame": extras,
             "gpu_launches": args.steps * (1 + (4 if args.pipeline == "full" else 0)),
             "clocks": clocks,
         }
