@@ -57,9 +57,10 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=16, help="cpu_baseline sample (frames)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-extras", action="store_true",
-                    help="skip the short timings of the next-row kernels (adaptive, cloud, "
-                         "evaluation, PNG16 input)")
+    ap.add_argument("--extras", action="store_true",
+                    help="also time the next-row kernels (adaptive, cloud, evaluation, PNG16 "
+                         "input) briefly after the headline measurement")
+    ap.add_argument("--no-extras", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -391,7 +392,7 @@ def main():
     # next rows of the scope table, timed briefly on 8 of the
     # same frames after the headline measurement: evidence, not the metric
     extras = None
-    if rank == 0 and world == 1 and not args.no_extras:
+    if rank == 0 and world == 1 and args.extras and not args.no_extras:
         try:
             extras = next_row_timings(disp[:8], out[:8], rig, dev)
         except Exception as exc:  # never let an extra cost the headline line
