@@ -40,6 +40,8 @@
 #include <float.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "sn_internal.h"
 
 namespace sn {
@@ -809,11 +811,25 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
             const uint32_t* bits_in) {
   const int64_t n = p.B * p.H * p.W;
   if (n == 0) return SN_OK;
-  if (p.H * p.W > 0x7fffffffLL || p.B > 65535)
-    return set_error(SN_EINVAL, "frame too large for int32 labels");
+  if (p.H * p.W > 0x7fffffffLL) return set_error(SN_EINVAL, "frame too large for int32 labels");
   if (!workspace || ws_bytes < ccl_workspace_bytes(p.B, p.H, p.W))
     return set_error(SN_EINVAL, "labeller workspace too small (%zu < %zu bytes)", ws_bytes,
                      ccl_workspace_bytes(p.B, p.H, p.W));
+  constexpr int64_t kMaxFrames = 65535;  // grid.z
+  if (p.B > kMaxFrames) {
+    // frames are independent: consecutive launches of <= 65535 frames, each
+    // reusing the front of the workspace (stream order serialises them)
+    const int64_t HW = p.H * p.W, WW = (p.W + 31) / 32;
+    for (int64_t f0 = 0; f0 < p.B; f0 += kMaxFrames) {
+      CclParams q = p;
+      q.B = std::min<int64_t>(kMaxFrames, p.B - f0);
+      const int rc = run_ccl(ctx, disp ? disp + f0 * HW : nullptr, pas ? pas + f0 * HW : nullptr, q,
+                             index_base, labels + f0 * HW, workspace, ws_bytes,
+                             bits_in ? bits_in + f0 * p.H * WW : nullptr);
+      if (rc) return rc;
+    }
+    return SN_OK;
+  }
   CclWorkspace ws;
   ws.WW = (int)((p.W + 31) / 32);
   ws.n_tx = (int)((p.W + kLTW - 1) / kLTW);

@@ -520,7 +520,19 @@ int run_eval(const LaunchCtx& ctx, const float* est, const double* est_d, int es
   if (B == 0) return SN_OK;
   if (!workspace || ws_bytes < eval_workspace_bytes(B, H, W))
     return set_error(SN_EINVAL, "evaluation workspace too small");
-  if (B > 65535) return set_error(SN_EINVAL, "at most 65535 frames per call");
+  if (B > 65535) {  // grid.y: consecutive calls of <= 65535 frames reusing the workspace
+    for (int64_t f0 = 0; f0 < B; f0 += 65535) {
+      const int64_t b = B - f0 < 65535 ? B - f0 : 65535;
+      const int64_t o = f0 * HW;
+      const int rc = run_eval(ctx, est ? est + o * est_stride : nullptr,
+                              est_d ? est_d + o * est_stride : nullptr, est_stride,
+                              gt ? gt + o * 3 : nullptr, gt_mask ? gt_mask + o : nullptr,
+                              extra ? extra + o : nullptr, b, H, W, err_out ? err_out + o : nullptr,
+                              stats + f0 * 6, workspace, ws_bytes);
+      if (rc) return rc;
+    }
+    return SN_OK;
+  }
   const int64_t nch64 = (HW + kEvalChunk - 1) / kEvalChunk;
   if (nch64 > 0x7fffffffLL || nch64 == 0) return set_error(SN_EINVAL, "bad frame size");
   const int nch = (int)nch64;

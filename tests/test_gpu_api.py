@@ -133,3 +133,31 @@ def test_cuda_graph_capture(cuda_dev):
         torch.cuda.synchronize()
         assert torch.equal(torch.nan_to_num(out, 7.0), torch.nan_to_num(ref_out, 7.0))
         assert torch.equal(lab, ref_lab)
+
+
+def test_batch_beyond_int32_pixels(cuda_dev):
+    """A batch of more than 2^31 pixels (70,000 frames of 256x128: 9.2 GB in,
+    55 GB of records out) through one fused-pass call: 64-bit batch offsets
+    and 3D TMA coordinates past 2^16 frames -- the first, a middle and the
+    last frames equal the same frames processed alone."""
+    from paper_2504_15121_b200 import device, scenes
+    free, _ = torch.cuda.mem_get_info(cuda_dev)
+    B, H, W = 70000, 128, 256
+    if free < 70 * 2**30:
+        pytest.skip("needs ~70 GB of free device memory")
+    sc = scenes.street_scene(W, H)
+    base = torch.from_numpy(scenes.raycast(sc)[0].astype(np.float32)).to(cuda_dev)
+    d = base.expand(B, -1, -1).contiguous()
+    d[:, 10, :] += torch.arange(B, device=cuda_dev, dtype=torch.float32)[:, None] * 1e-3
+    out = device.oriented_points(d, sc.rig, 9)
+    for i in (0, 35001, B - 1):
+        one = device.oriented_points(d[i], sc.rig, 9)[0]
+        assert torch.equal(torch.nan_to_num(out[i], 7.0), torch.nan_to_num(one, 7.0)), i
+    del out
+    torch.cuda.empty_cache()
+    # labels: more frames than one launch's grid holds (65535), chunked inside
+    lab = device.component_labels(d, sc.rig, 0.2)
+    for i in (0, 65534, 65535, B - 1):
+        assert torch.equal(lab[i], device.component_labels(d[i], sc.rig, 0.2)[0]), i
+    del lab, d
+    torch.cuda.empty_cache()
