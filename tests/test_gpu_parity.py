@@ -415,3 +415,33 @@ def test_large_kernels_vs_oracle(cuda_dev, k):
     mask = torch.empty((1,) + d.shape, dtype=torch.uint8, device=cuda_dev)
     out = device.oriented_points(torch.from_numpy(d).to(cuda_dev), sc.rig, k, mask=mask)
     _check_record(out[0].cpu().numpy(), mask[0].cpu().numpy(), _oracle_record(d, sc.rig, k))
+
+
+def test_random_shapes_vs_oracle(cuda_dev):
+    """40 random frames: heights/widths 1..300 (fast path when W is a multiple of
+    4, the generic kernel otherwise), square kernels 3..17, NaN/inf/negative
+    samples, batches of 1-3 -- every record against the oracle."""
+    from paper_2504_15121_b200 import KernelSpec, StereoRig, device
+    rng = np.random.default_rng(2024)
+    for case in range(40):
+        H = int(rng.integers(1, 160))
+        W = int(rng.choice([rng.integers(1, 300), 8 * rng.integers(1, 38)]))
+        k = int(rng.choice([3, 5, 7, 9, 11, 13, 15, 17]))
+        B = int(rng.integers(1, 4))
+        rig = StereoRig(float(rng.uniform(50, 2000)), float(rng.uniform(50, 2000)),
+                        float(rng.uniform(0, W)), float(rng.uniform(0, H)),
+                        float(rng.uniform(0.05, 1.0)))
+        d = rng.uniform(1.0, 90.0, (B, H, W))
+        d += rng.normal(0, 0.3, d.shape)
+        bad = rng.random(d.shape)
+        d[bad < 0.01] = np.nan
+        d[(bad >= 0.01) & (bad < 0.012)] = -1.0
+        d[(bad >= 0.012) & (bad < 0.013)] = np.inf
+        d = d.astype(np.float32)
+        mask = torch.empty((B, H, W), dtype=torch.uint8, device=cuda_dev)
+        out = device.oriented_points(torch.from_numpy(d).to(cuda_dev), rig, KernelSpec.square(k),
+                                     mask=mask)
+        o = out.cpu().numpy()
+        m = mask.cpu().numpy()
+        for b in range(B):
+            _check_record(o[b], m[b], _oracle_record(d[b], rig, k))
