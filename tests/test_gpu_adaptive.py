@@ -95,3 +95,32 @@ def test_adaptive_cd_exact_ties(cuda_dev, shared, t):
     m = mask[0].cpu().numpy().astype(bool)
     assert np.array_equal(m, ok_ref)
     assert max_angle_deg(out[0].cpu().numpy()[m][:, 3:], n_ref[m]) < 1e-4
+
+
+def test_adaptive_random_configs_vs_oracle(cuda_dev):
+    """12 random small frames x star configurations (M = 3..16 directions,
+    s = 1..12 steps, ST / CD, shared range, thresholds), holes and border
+    pixels: masks bit-exact and normals within 1e-4 deg of the oracle."""
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import StarConfig, StereoRig, device
+    rng = np.random.default_rng(77)
+    for case in range(12):
+        H, W = int(rng.integers(8, 48)), int(rng.integers(8, 64))
+        v, u = np.mgrid[0:H, 0:W].astype(float)
+        d = 20.0 + 0.3 * u - 0.2 * v + rng.normal(0, 0.4, (H, W))
+        d[rng.random((H, W)) < 0.03] = np.nan
+        d = d.astype(np.float32)
+        stop = str(rng.choice(["st", "cd"]))
+        cfg = dict(stop=stop, threshold=float(rng.choice([0.05, 0.1, 0.3, 1.0])),
+                   max_steps=int(rng.integers(1, 13)), directions=int(rng.integers(3, 17)),
+                   shared_range=bool(rng.integers(0, 2)) if stop == "cd" else False)
+        rig = StereoRig(300.0, 310.0, W / 2.0, H / 2.0, 0.25)
+        n_ref, ok_ref = orc.estimate_normals_adaptive(d.astype(np.float64),
+                                                      orc.Rig(300.0, 310.0, W / 2.0, H / 2.0, 0.25),
+                                                      orc.Star(**cfg))
+        mask = torch.empty((1, H, W), dtype=torch.uint8, device=cuda_dev)
+        out = device.adaptive_points(torch.from_numpy(d).to(cuda_dev), rig, StarConfig(**cfg),
+                                     mask=mask)
+        m = mask[0].cpu().numpy().astype(bool)
+        assert np.array_equal(m, ok_ref), (case, cfg)
+        assert max_angle_deg(out[0].cpu().numpy()[m][:, 3:], n_ref[m]) < 1e-4, (case, cfg)
