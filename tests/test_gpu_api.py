@@ -161,3 +161,25 @@ def test_batch_beyond_int32_pixels(cuda_dev):
         assert torch.equal(lab[i], device.component_labels(d[i], sc.rig, 0.2)[0]), i
     del lab, d
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape", [(0, 16, 32), (2, 0, 32), (2, 16, 0)])
+def test_empty_inputs(cuda_dev, shape):
+    """Empty batches / frames through every device entry point: correctly
+    shaped empty results, no error, no launch on zero pixels."""
+    from paper_2504_15121_b200 import StarConfig, StereoRig, device
+    rig = StereoRig(100.0, 100.0, 8.0, 8.0, 0.2)
+    d = torch.empty(shape, device=cuda_dev)
+    B, H, W = shape
+    assert device.oriented_points(d, rig, 3).shape == (B, H, W, 6)
+    assert device.passable_bits(d, rig, 0.2).shape == (B, H, device.bit_words(W))
+    assert device.component_labels(d, rig, 0.2).shape == (B, H, W)
+    pts, lab = device.pipeline(d, rig, 3, 0.2)
+    assert pts.shape == (B, H, W, 6) and lab.shape == (B, H, W)
+    assert device.adaptive_points(d, rig, StarConfig(stop="cd", threshold=0.1)).shape == (B, H, W, 6)
+    m = torch.zeros(shape, dtype=torch.uint8, device=cuda_dev)
+    cloud, offs = device.compact_cloud(pts, m)
+    assert cloud.shape == (0, 6) and offs.shape == (B + 1,) and int(offs[-1]) == 0
+    raw = torch.from_numpy(np.zeros(shape, np.uint16)).to(cuda_dev)
+    assert device.dequant_png16(raw, 256.0, 0).shape == (B, H, W)
+    torch.cuda.synchronize()
