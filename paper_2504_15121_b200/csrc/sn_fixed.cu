@@ -383,13 +383,12 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   uint32_t f16 = 0;       // this unit's column flags (0 for idle lanes)
   if (unit) {
     if constexpr (sizeof(T) == 4) {
-      uint32_t mx = 0;
+      // |v| <= 2^40 for every sample (NaN fails): one predicated compare each
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
         raw[i] = col[i * BW];
-        mx = max(mx, __float_as_uint(raw[i]) & 0x7fffffffu);
+        all_small &= fabsf(raw[i]) <= 1099511627776.0f;
       }
-      all_small = mx <= kBigBits;
     } else if constexpr (sizeof(T) == 2) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
