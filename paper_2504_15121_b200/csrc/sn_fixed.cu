@@ -34,6 +34,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <algorithm>
+#include <mutex>
 #include <stdlib.h>
 
 #include "sn_common.cuh"
@@ -910,7 +913,7 @@ __global__ void __launch_bounds__(256)
 
 template <int R, typename T>
 static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams& p, float* out6,
-                         uint8_t* mask) {
+                         uint8_t* mask, int64_t in_pitch, int64_t out_pitch) {
   using Cfg = FastCfg<R, T>;
   CUtensorMap in_map, out_map;
   const CUtensorMapDataType dt =
@@ -919,7 +922,8 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
                        : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   {
     cuuint64_t dims[3] = {(cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.B};
-    cuuint64_t strides[2] = {(cuuint64_t)(p.W * sizeof(T)), (cuuint64_t)(p.W * p.H * sizeof(T))};
+    cuuint64_t strides[2] = {(cuuint64_t)(in_pitch * sizeof(T)),
+                             (cuuint64_t)(in_pitch * p.H * sizeof(T))};
     cuuint32_t box[3] = {(cuuint32_t)Cfg::BW, (cuuint32_t)Cfg::NR, 1};
     cuuint32_t es[3] = {1, 1, 1};
     if (encode_tiled(&in_map, dt, 3, (void*)disp, dims, strides, box, es,
@@ -928,7 +932,7 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
   }
   {
     cuuint64_t dims[3] = {(cuuint64_t)(p.W * 6), (cuuint64_t)p.H, (cuuint64_t)p.B};
-    cuuint64_t strides[2] = {(cuuint64_t)(p.W * 24), (cuuint64_t)(p.W * p.H * 24)};
+    cuuint64_t strides[2] = {(cuuint64_t)(out_pitch * 24), (cuuint64_t)(out_pitch * p.H * 24)};
     cuuint32_t box[3] = {(cuuint32_t)kBoxF, (cuuint32_t)kG, 1};
     cuuint32_t es[3] = {1, 1, 1};
     if (encode_tiled(&out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)out6, dims, strides, box,
@@ -983,18 +987,96 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
 
 template <typename T>
 static int dispatch_square(int R, const LaunchCtx& ctx, const T* disp, const FixedParams& p,
-                           float* out6, uint8_t* mask) {
+                           float* out6, uint8_t* mask, int64_t in_pitch = -1,
+                           int64_t out_pitch = -1) {
+  if (in_pitch < 0) in_pitch = p.W;
+  if (out_pitch < 0) out_pitch = p.W;
   switch (R) {
-    case 1: return launch_square<1, T>(ctx, disp, p, out6, mask);
-    case 2: return launch_square<2, T>(ctx, disp, p, out6, mask);
-    case 3: return launch_square<3, T>(ctx, disp, p, out6, mask);
-    case 4: return launch_square<4, T>(ctx, disp, p, out6, mask);
-    case 5: return launch_square<5, T>(ctx, disp, p, out6, mask);
-    case 6: return launch_square<6, T>(ctx, disp, p, out6, mask);
-    case 7: return launch_square<7, T>(ctx, disp, p, out6, mask);
-    case 8: return launch_square<8, T>(ctx, disp, p, out6, mask);
+    case 1: return launch_square<1, T>(ctx, disp, p, out6, mask, in_pitch, out_pitch);
+    case 2: return launch_square<2, T>(ctx, disp, p, out6, mask, in_pitch, out_pitch);
+    case 3: return launch_square<3, T>(ctx, disp, p, out6, mask, in_pitch, out_pitch);
+    case 4: return launch_square<4, T>(ctx, disp, p, out6, mask, in_pitch, out_pitch);
+    case 5: return launch_square<5, T>(ctx, disp, p, out6, mask, in_pitch, out_pitch);
+    case 6: return launch_square<6, T>(ctx, disp, p, out6, mask, in_pitch, out_pitch);
+    case 7: return launch_square<7, T>(ctx, disp, p, out6, mask, in_pitch, out_pitch);
+    case 8: return launch_square<8, T>(ctx, disp, p, out6, mask, in_pitch, out_pitch);
     default: return -1;
   }
+}
+
+// rows of `words` 4-byte words from src (pitch sp words) to dst (pitch dp
+// words): one thread per word, a 2D grid of (row chunk, word chunk)
+__global__ void __launch_bounds__(256)
+    pitch_copy_kernel(const uint32_t* __restrict__ src, int64_t sp, uint32_t* __restrict__ dst,
+                      int64_t dp, int64_t words, int64_t rows) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= words) return;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) dst[r * dp + w] = __ldcs(src + r * sp + w);
+}
+
+static int pitch_copy(const LaunchCtx& ctx, const void* src, int64_t sp_bytes, void* dst,
+                      int64_t dp_bytes, int64_t width_bytes, int64_t rows) {
+  const int64_t words = width_bytes / 4;
+  const unsigned gx = (unsigned)((words + 255) / 256);
+  int64_t gy = (int64_t)ctx.num_sms * 16 / std::max<int64_t>(1, (int64_t)gx);
+  gy = std::max<int64_t>(1, std::min<int64_t>(gy, std::min<int64_t>(rows, 65535)));
+  pitch_copy_kernel<<<dim3(gx, (unsigned)gy), 256, 0, ctx.stream>>>(
+      static_cast<const uint32_t*>(src), sp_bytes / 4, static_cast<uint32_t*>(dst), dp_bytes / 4,
+      words, rows);
+  return check_launch("pitch_copy_kernel");
+}
+
+// The fast kernel on widths (or pointers) TMA cannot address directly: the
+// disparities are copied into a row-pitched buffer (pitch rounded up to 16
+// bytes; +8 B/px of traffic), and for odd widths the records go through a
+// pitched buffer too (+48 B/px).  Stream-ordered allocations, so concurrent
+// calls on different streams do not share scratch.  Returns -1 to fall back
+// to the generic kernel if the scratch cannot be had.
+template <typename T>
+static int dispatch_square_staged(int R, const LaunchCtx& ctx, const T* disp, const FixedParams& p,
+                                  float* out6, uint8_t* mask) {
+  constexpr int64_t AE = 16 / (int64_t)sizeof(T);
+  const int64_t Wp = (p.W + AE - 1) / AE * AE;  // even (AE >= 2)
+  const bool out_direct = p.W % 2 == 0 && reinterpret_cast<uintptr_t>(out6) % 16 == 0;
+  // keep the stream-ordered pool's memory between calls (the default release
+  // threshold returns it to the driver at every synchronisation)
+  static std::mutex pool_mu;
+  static bool pool_kept[64] = {};
+  if (ctx.device >= 0 && ctx.device < 64) {
+    std::lock_guard<std::mutex> lock(pool_mu);
+    if (!pool_kept[ctx.device]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, ctx.device) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      pool_kept[ctx.device] = true;
+    }
+  }
+  T* in_tmp = nullptr;
+  float* out_tmp = nullptr;
+  const size_t in_bytes = (size_t)(p.B * p.H * Wp) * sizeof(T);
+  const size_t out_bytes = out_direct ? 0 : (size_t)(p.B * p.H * Wp) * 24;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&in_tmp), in_bytes, ctx.stream) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  if (!out_direct &&
+      cudaMallocAsync(reinterpret_cast<void**>(&out_tmp), out_bytes, ctx.stream) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeAsync(in_tmp, ctx.stream);
+    return -1;
+  }
+  int rc = pitch_copy(ctx, disp, p.W * (int64_t)sizeof(T), in_tmp, Wp * (int64_t)sizeof(T),
+                      p.W * (int64_t)sizeof(T), p.B * p.H);
+  if (rc == SN_OK)
+    rc = dispatch_square<T>(R, ctx, in_tmp, p, out_direct ? out6 : out_tmp, mask, Wp,
+                            out_direct ? p.W : Wp);
+  if (rc == SN_OK && !out_direct)
+    rc = pitch_copy(ctx, out_tmp, Wp * 24, out6, p.W * 24, p.W * 24, p.B * p.H);
+  cudaFreeAsync(in_tmp, ctx.stream);
+  if (out_tmp) cudaFreeAsync(out_tmp, ctx.stream);
+  return rc;
 }
 
 template <typename T>
@@ -1024,8 +1106,10 @@ int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const s
                        (reinterpret_cast<uintptr_t>(out6) % 16 == 0) &&
                        (p.W % (16 / (int64_t)sizeof(T)) == 0) && (p.W % 2 == 0) &&
                        p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
-  if (!affine && !force_generic && m.square_r >= 1 && m.square_r <= 8 && aligned) {
-    int rc = dispatch_square<T>(m.square_r, ctx, disp, p, out6, mask);
+  const bool sized = p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
+  if (!affine && !force_generic && m.square_r >= 1 && m.square_r <= 8 && sized) {
+    int rc = aligned ? dispatch_square<T>(m.square_r, ctx, disp, p, out6, mask)
+                     : dispatch_square_staged<T>(m.square_r, ctx, disp, p, out6, mask);
     if (rc == SN_OK && p.bits != nullptr) {
       if constexpr (sizeof(T) == 4) rc = run_passable_bits(ctx, disp, p, p.bits);
     }
