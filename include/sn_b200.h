@@ -276,10 +276,10 @@ SN_API int sn_decode_pfm(sn_plan_t* plan, const void* payload, int64_t B, int64_
 
 /* sn_oriented_points with a 16-bit PNG disparity payload read directly by
  * the fused pass (read_disparity_png16 + estimate_normals_fixed +
- * triangulate_grid): 2 B/px in instead of 4.  Needs a centred square kernel
- * (3..17), W % 8 == 0, 16-byte aligned buffers and 2^-100 <= |scale| <=
- * 2^100; SN_EINVAL otherwise (dequantise with sn_dequant_png16 and use
- * sn_oriented_points_f64). */
+ * triangulate_grid): 2 B/px in instead of 4 (widths that are not a multiple of 8
+ * go through a row-pitched copy).  Needs a centred square kernel (3..17) and
+ * 2^-100 <= |scale| <= 2^100; SN_EINVAL otherwise (dequantise with
+ * sn_dequant_png16 and use sn_oriented_points_f64). */
 SN_API int sn_oriented_points_png16(sn_plan_t* plan, const uint16_t* raw, int64_t B, int64_t H,
                              int64_t W, double scale, int32_t invalid, const sn_rig_t* rig,
                              const int32_t* offsets_xy, int32_t n_off, float* out6,

@@ -1006,23 +1006,31 @@ static int dispatch_square(int R, const LaunchCtx& ctx, const T* disp, const Fix
 
 // rows of `words` 4-byte words from src (pitch sp words) to dst (pitch dp
 // words): one thread per word, a 2D grid of (row chunk, word chunk)
+template <typename U>
 __global__ void __launch_bounds__(256)
-    pitch_copy_kernel(const uint32_t* __restrict__ src, int64_t sp, uint32_t* __restrict__ dst,
-                      int64_t dp, int64_t words, int64_t rows) {
+    pitch_copy_kernel(const U* __restrict__ src, int64_t sp, U* __restrict__ dst, int64_t dp,
+                      int64_t words, int64_t rows) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= words) return;
   for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) dst[r * dp + w] = __ldcs(src + r * sp + w);
 }
 
+// 4-byte words when every width and pitch allows it, else 2-byte ones
 static int pitch_copy(const LaunchCtx& ctx, const void* src, int64_t sp_bytes, void* dst,
                       int64_t dp_bytes, int64_t width_bytes, int64_t rows) {
-  const int64_t words = width_bytes / 4;
+  const int64_t ws = (width_bytes % 4 == 0 && sp_bytes % 4 == 0 && dp_bytes % 4 == 0) ? 4 : 2;
+  const int64_t words = width_bytes / ws;
   const unsigned gx = (unsigned)((words + 255) / 256);
   int64_t gy = (int64_t)ctx.num_sms * 16 / std::max<int64_t>(1, (int64_t)gx);
   gy = std::max<int64_t>(1, std::min<int64_t>(gy, std::min<int64_t>(rows, 65535)));
-  pitch_copy_kernel<<<dim3(gx, (unsigned)gy), 256, 0, ctx.stream>>>(
-      static_cast<const uint32_t*>(src), sp_bytes / 4, static_cast<uint32_t*>(dst), dp_bytes / 4,
-      words, rows);
+  if (ws == 4)
+    pitch_copy_kernel<uint32_t><<<dim3(gx, (unsigned)gy), 256, 0, ctx.stream>>>(
+        static_cast<const uint32_t*>(src), sp_bytes / 4, static_cast<uint32_t*>(dst),
+        dp_bytes / 4, words, rows);
+  else
+    pitch_copy_kernel<uint16_t><<<dim3(gx, (unsigned)gy), 256, 0, ctx.stream>>>(
+        static_cast<const uint16_t*>(src), sp_bytes / 2, static_cast<uint16_t*>(dst),
+        dp_bytes / 2, words, rows);
   return check_launch("pitch_copy_kernel");
 }
 
@@ -1129,16 +1137,17 @@ template int run_fixed<float>(const LaunchCtx&, const float*, const FixedParams&
 int run_fixed_png16(const LaunchCtx& ctx, const uint16_t* raw, const FixedParams& p,
                     const sn_moments_t& m, float* out6, uint8_t* mask) {
   if (p.B * p.H * p.W == 0) return SN_OK;
+  const bool sized = p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
   const bool aligned = (reinterpret_cast<uintptr_t>(raw) % 16 == 0) &&
-                       (reinterpret_cast<uintptr_t>(out6) % 16 == 0) && (p.W % 8 == 0) &&
-                       p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
-  if (m.square_r < 1 || m.square_r > 8 || !aligned)
+                       (reinterpret_cast<uintptr_t>(out6) % 16 == 0) && (p.W % 8 == 0);
+  if (m.square_r < 1 || m.square_r > 8 || !sized)
     return set_error(SN_EINVAL,
-                     "16-bit input needs a centred square kernel (3..17), W % 8 == 0 and "
-                     "16-byte aligned buffers; dequantise with sn_dequant_png16 otherwise");
-  const int rc = dispatch_square<Png16>(m.square_r, ctx, reinterpret_cast<const Png16*>(raw), p,
-                                        out6, mask);
-  return rc >= 0 ? rc : set_error(SN_EINVAL, "batch too large");
+                     "16-bit input needs a centred square kernel (3..17); dequantise with "
+                     "sn_dequant_png16 otherwise");
+  const Png16* in = reinterpret_cast<const Png16*>(raw);
+  const int rc = aligned ? dispatch_square<Png16>(m.square_r, ctx, in, p, out6, mask)
+                         : dispatch_square_staged<Png16>(m.square_r, ctx, in, p, out6, mask);
+  return rc >= 0 ? rc : set_error(SN_EINVAL, "batch too large or scratch unavailable");
 }
 
 template int run_fixed<double>(const LaunchCtx&, const double*, const FixedParams&,

@@ -369,7 +369,7 @@ def oriented_points_png16(raw: torch.Tensor, rig, kernels=9, *, scale: float = 2
                           invalid_value: int | None = 0, out=None, mask=None) -> torch.Tensor:
     """``oriented_points`` reading 16-bit PNG samples directly (2 B/px): the
     fused pass dequantises on load exactly as read_disparity_png16 does.
-    Needs a centred square kernel, W % 8 == 0 and 2^-100 <= |scale| <= 2^100."""
+    Needs a centred square kernel and 2^-100 <= |scale| <= 2^100."""
     r = _raw16(raw)
     B, H, W = r.shape
     dev = r.device

@@ -115,7 +115,7 @@ def test_oriented_points_png16_golden(codec_golden, cuda_dev, name):
 
 
 @pytest.mark.parametrize("B,H,W,k", [(3, 96, 136, 7), (2, 101, 72, 9), (1, 17, 8, 3),
-                                     (2, 64, 520, 17)])
+                                     (2, 64, 520, 17), (2, 40, 1242, 9), (1, 33, 37, 5)])
 def test_oriented_points_png16_batched(cuda_dev, B, H, W, k):
     """Batches with invalid holes and ragged tiles, vs the fp32 path on the
     decoded values (power-of-two scale: dequantised values are exact in fp32)."""
@@ -138,9 +138,9 @@ def test_oriented_points_png16_batched(cuda_dev, B, H, W, k):
 def test_png16_rejects(cuda_dev):
     from paper_2504_15121_b200 import KernelSpec, StereoRig, device
     rig = StereoRig(100.0, 100.0, 10.0, 10.0, 0.2)
-    r = torch.from_numpy(np.zeros((1, 16, 20), np.uint16)).to(cuda_dev)  # W % 8 != 0
-    with pytest.raises(ValueError, match="W % 8"):
-        device.oriented_points_png16(r, rig, KernelSpec.square(5))
+    with pytest.raises(ValueError, match="square kernel"):
+        r = torch.from_numpy(np.zeros((1, 16, 24), np.uint16)).to(cuda_dev)
+        device.oriented_points_png16(r, rig, KernelSpec(np.array([[0, 0], [1, 0], [0, 1]])))
     r = torch.from_numpy(np.zeros((1, 16, 24), np.uint16)).to(cuda_dev)
     with pytest.raises(ValueError, match="scale"):
         device.oriented_points_png16(r, rig, KernelSpec.square(5), scale=0.0)
