@@ -584,12 +584,10 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   }
   // depths zf = fxb * rcp(d) of the run's pixels (zc[1 .. kRun])
   float zc[kRun + 2], df[kRun];
-  if constexpr (kF32Epi<T>) {
 #pragma unroll
-    for (int j = 0; j < kRun; ++j) {
-      df[j] = dflt(drow[j], p);
-      zc[j + 1] = __fmul_rn(p.fxb_f, rcp_ftz(df[j]));
-    }
+  for (int j = 0; j < kRun; ++j) {
+    df[j] = dflt(drow[j], p);
+    zc[j + 1] = __fmul_rn(p.fxb_f, rcp_ftz(df[j]));
   }
   float o[12];
 #pragma unroll
@@ -597,7 +595,18 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
     const bool ok0 = (((win >> j) & 1u) == 0u) && dpos(drow[j], p);
     const bool ok1 = (((win >> (j + 1)) & 1u) == 0u) && dpos(drow[j + 1], p);
     validbits |= ((ok0 ? 1u : 0u) | (ok1 ? 2u : 0u)) << j;
-    if constexpr (kF32Epi<T>) {
+    // fp64 inputs take the fp32 epilogue too when both centre samples are
+    // invalid or within [2^-100, 2^100] (d rounded once to fp32: ~6e-8
+    // relative); others -- fp32-subnormal or huge disparities -- the fp64 one
+    bool f32_epi = kF32Epi<T>;
+    if constexpr (sizeof(T) == 8) {
+      auto safe = [](double d) {
+        return !(d > 0.0 && d <= 1.7976931348623157e308) ||
+               (d >= 7.888609052210118e-31 && d <= 1.2676506002282294e30);
+      };
+      f32_epi = safe((double)drow[j]) && safe((double)drow[j + 1]);
+    }
+    if (f32_epi) {
       records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], df[j], df[j + 1],
                    make_float2(zc[j + 1], zc[j + 2]), ok0, ok1, du_hi + (float)j, dv_f, p, o);
     } else {
