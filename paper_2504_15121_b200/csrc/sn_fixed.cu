@@ -58,6 +58,15 @@ constexpr int kFastThreads = 2 * kHalfUnits;  // 10 warps; pass H uses the first
 constexpr int kRun = 8;            // output columns per pass-H lane
 constexpr int kStoreTid = 8 * 32;  // warp 8 issues the output TMA stores
 constexpr uint32_t kBigBits = 0x53800000u;  // fp32 bit pattern of 2^40
+#ifndef SN_ROWBULK
+#define SN_ROWBULK 1
+#endif
+// row-major staging for the classic kernel: one output row of an item (128
+// records, 3072 B) per bulk copy; the 16-B pad makes the pitch 4 banks off,
+// so the 8 lanes (= 8 rows) of each quarter-warp phase of pass H's 16-byte
+// stores hit distinct banks
+constexpr int kRowPitch = kTW * 24 + 16;
+constexpr size_t kRowStageBytes = (size_t)kG * kRowPitch;
 
 __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -68,7 +77,7 @@ struct FastCfg {
   static constexpr int AE = 16 / (int)sizeof(T);
   // the box starts at (x0 - R) rounded down to 16 B, so it spans up to AE-1 extra columns
   static constexpr int BW = (NC + AE - 1 + AE - 1) / AE * AE;
-  static constexpr size_t STAGE_BYTES = (size_t)kBoxes * kG * 128;
+  static constexpr size_t STAGE_BYTES = SN_ROWBULK ? kRowStageBytes : (size_t)kBoxes * kG * 128;
   static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
   static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;  // double2 (C, Rr) [NC][kCP]
   // column flags (NC words) + 8-column block ORs of them (NB words)
@@ -81,7 +90,8 @@ struct FastCfg {
   static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);
   static constexpr size_t FL = align_up(CS + CS_BYTES, 16);
   static constexpr size_t BAR = align_up(FL + FL_BYTES, 16);
-  static constexpr size_t TOTAL = BAR + 16 + 1024;  // + slack for 1024-B alignment
+  // + slack for the base alignment (1024 B for the 128B-swizzled boxes)
+  static constexpr size_t TOTAL = BAR + 16 + (SN_ROWBULK ? 128 : 1024);
   static_assert(NC <= kHalfUnits, "pass V: one unit per thread");
   static_assert(NR <= 32, "row validity bits must fit 32 bits");
 };
@@ -93,7 +103,8 @@ struct PipeCfg {
   using C = FastCfg<R, float>;
   static constexpr int kIn = 3, kCr = 2, kSt = 2;
   static constexpr size_t STAGE = 0;
-  static constexpr size_t IN = STAGE + kSt * C::STAGE_BYTES;
+  static constexpr size_t SB = (size_t)kBoxes * kG * 128;  // swizzled boxes
+  static constexpr size_t IN = STAGE + kSt * SB;
   static constexpr size_t IN_STRIDE = align_up(C::IN_BYTES, 128);
   static constexpr size_t CS = IN + kIn * IN_STRIDE;
   static constexpr size_t CS_STRIDE = align_up(C::CS_BYTES, 128);
@@ -478,8 +489,9 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   if ((c & 7) == 0 && (c >> 3) < Cfg::NB) reinterpret_cast<uint16_t*>(fl + NC + (c >> 3))[h] = (uint16_t)f16;
 }
 
-// pass H + epilogue for lane hl (< 256) of one item
-template <int R, typename T>
+// pass H + epilogue for lane hl (< 256) of one item.  ROWS: row-major padded
+// staging (kRowPitch), else 24 128B-swizzled TMA boxes
+template <int R, typename T, bool ROWS = false>
 __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int y0, int bz, int H,
                                        int W, const double2* CR, const uint32_t* fl,
                                        uint32_t stage_base, const FixedParams& p,
@@ -534,7 +546,9 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   const uint32_t stg_x = ((uint32_t)(4 * (q & 1)) ^ gsw) << 4;
   const uint32_t stg_a0 = rowaddr + (uint32_t)(q + (q >> 1)) * (uint32_t)(kG * 128);
   const uint32_t stg_a1 = stg_a0 + ((q & 1) ? (uint32_t)(kG * 128) : 0u);
+  const uint32_t row_a = stage_base + (uint32_t)g * (uint32_t)kRowPitch + (uint32_t)q * 192u;
   auto stg_addr = [&](int c) {
+    if constexpr (ROWS) return row_a + (uint32_t)c * 16u;
     return ((c & 4) ? stg_a1 : stg_a0) + (uint32_t)(c >> 3) * (uint32_t)(kG * 128) +
            (((uint32_t)(c & 7) << 4) ^ stg_x);
   };
@@ -652,14 +666,17 @@ template <int R, typename T>
 __global__ void __launch_bounds__(kFastThreads, 2)
     fixed_square_kernel(const __grid_constant__ CUtensorMap in_map,
                         const __grid_constant__ CUtensorMap out_map, const FixedParams p,
-                        uint8_t* __restrict__ mask_out, const int n_items, const int tiles_x,
+                        uint8_t* __restrict__ mask_out, float* __restrict__ out6,
+                        const int64_t out_pitch, const int n_items, const int tiles_x,
                         const int tiles_y) {
   using Cfg = FastCfg<R, T>;
   constexpr int NC = Cfg::NC, AE = Cfg::AE;
+  constexpr int kStoreLanes = SN_ROWBULK ? kG : kBoxes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned base for the swizzled staging tile; offset arithmetic on the
   // __shared__ array keeps the shared address space (LDS/STS, not generic LD/ST)
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr uint32_t kAlign = SN_ROWBULK ? 128u : 1024u;
+  uint8_t* smem = smem_raw + ((kAlign - (smem_u32(smem_raw) & (kAlign - 1u))) & (kAlign - 1u));
   double2* CR = reinterpret_cast<double2*>(smem + Cfg::CS);
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
@@ -704,22 +721,35 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     // 1 no TMA stores, 2 no pass H, 3 no pass V, 4 neither pass
     if (SN_EXP != 3 && SN_EXP != 4) pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
     // staging of the previous item consumed by its TMA stores (issued by warp 8)
-    if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait_read0();
+    if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) bulk_wait_read0();
     __syncthreads();
 
     if (SN_EXP != 2 && SN_EXP != 4)
-      if (tid < 256) pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
+      if (tid < 256)
+        pass_h<R, T, SN_ROWBULK>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
     fence_proxy_async_smem();
     __syncthreads();
-    // one TMA store per 128-B box column, one lane each, from a warp that is
-    // idle in pass H -- warp 0 goes straight on to the next item
-    if (SN_EXP != 1 && tid >= kStoreTid && tid < kStoreTid + kBoxes) {
+    // output stores from a warp that is idle in pass H -- warp 0 goes
+    // straight on to the next item
+    if (SN_EXP != 1 && tid >= kStoreTid && tid < kStoreTid + kStoreLanes) {
       const int b = tid - kStoreTid;
-      tma_store_3d(&out_map, smem + Cfg::STAGE + (size_t)b * kG * 128, x0 * 6 + b * kBoxF, y0, bz);
+      if constexpr (SN_ROWBULK) {
+        // one contiguous bulk copy per output row (3072 B, less at the right
+        // edge).  The pitch is even, so rows start 16-B aligned and a row
+        // ends on a 16-B multiple; an odd width writes into a pitched buffer
+        // (dispatch_square_staged), whose pad column takes the extra record
+        if (y0 + b < H) {
+          const int n = min(kTW, (int)out_pitch - x0);
+          bulk_store_1d(out6 + (((int64_t)bz * H + y0 + b) * out_pitch + x0) * 6,
+                        smem + Cfg::STAGE + (size_t)b * kRowPitch, (uint32_t)n * 24u);
+        }
+      } else {
+        tma_store_3d(&out_map, smem + Cfg::STAGE + (size_t)b * kG * 128, x0 * 6 + b * kBoxF, y0, bz);
+      }
       bulk_commit();
     }
   }
-  if (tid >= kStoreTid && tid < kStoreTid + kBoxes) bulk_wait0();
+  if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) bulk_wait0();
 }
 
 // ---------------------------------------------------------------------------
@@ -759,7 +789,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
   auto in_tile = [&](int s) { return reinterpret_cast<float*>(smem + PC::IN + s * PC::IN_STRIDE); };
   auto cr_slot = [&](int s) { return reinterpret_cast<double2*>(smem + PC::CS + s * PC::CS_STRIDE); };
   auto fl_slot = [&](int s) { return reinterpret_cast<uint32_t*>(smem + PC::FL + s * Cfg::FL_BYTES); };
-  auto st_slot = [&](int s) { return smem + PC::STAGE + s * Cfg::STAGE_BYTES; };
+  auto st_slot = [&](int s) { return smem + PC::STAGE + s * PC::SB; };
 
   if (tid == 0) {
     tma_prefetch_desc(&in_map);
@@ -989,8 +1019,9 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * ctx.num_sms;
   if (grid > n_items) grid = n_items;
-  kern<<<(unsigned)grid, kFastThreads, Cfg::TOTAL, ctx.stream>>>(in_map, out_map, p, mask, n_items,
-                                                                 tiles_x, tiles_y);
+  kern<<<(unsigned)grid, kFastThreads, Cfg::TOTAL, ctx.stream>>>(in_map, out_map, p, mask, out6,
+                                                                 out_pitch, n_items, tiles_x,
+                                                                 tiles_y);
   return check_launch("fixed_square_kernel");
 }
 
