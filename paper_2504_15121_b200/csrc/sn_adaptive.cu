@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
       if (d32 > 0.0f && d32 < 1.175494351e-38f) {  // subnormal: rcp.approx flushes
         pz = (float)(p.fxb / (double)d32);
         px = du_f * pz * p.inv_fx_f;
-        py = dv_f * pz * p.inv_fy_f;
+        py = pz * (dv_f * p.inv_fy_f);
       }
     }
     float2* o = reinterpret_cast<float2*>(out6 + idx * 6);

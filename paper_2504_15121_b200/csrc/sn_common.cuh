@@ -304,7 +304,7 @@ __device__ __forceinline__ void point_from_disparity(float d, float du, float dv
   const float zz = ok ? fxb * r : __int_as_float(0x7fc00000);
   z = zz;
   x = du * zz * inv_fx;
-  y = dv * zz * inv_fy;
+  y = zz * (dv * inv_fy);  // = the fused pass (dv / fy hoisted per row)
 }
 
 // fp64-input variant (geometry.py:39-64 in double, then rounded to fp32).

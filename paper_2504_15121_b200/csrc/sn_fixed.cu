@@ -245,7 +245,9 @@ __device__ __forceinline__ void records_pair(double U0, double V0, double U1, do
   if (!pv0) zz.x = __int_as_float(0x7fc00000);
   if (!pv1) zz.y = __int_as_float(0x7fc00000);
   const float2 px = __fmul2_rn(__fmul2_rn(du, zz), make_float2(p.inv_fx_f, p.inv_fx_f));
-  const float2 py = __fmul2_rn(__fmul2_rn(make_float2(dv, dv), zz), make_float2(p.inv_fy_f, p.inv_fy_f));
+  // dv / fy is a per-row constant (hoisted out of the run): one product per pixel
+  const float dvy = dv * p.inv_fy_f;
+  const float2 py = __fmul2_rn(zz, make_float2(dvy, dvy));
   o[0] = px.x;
   o[1] = py.x;
   o[2] = zz.x;
@@ -260,10 +262,9 @@ __device__ __forceinline__ void records_pair(double U0, double V0, double U1, do
   const float2 az = __ffma2_rn(Vf, make_float2(dv, dv),
                                __ffma2_rn(Uf, du, __fmul2_rn(make_float2(nal, nal), dd)));
   const float2 s = __ffma2_rn(ax, ax, __ffma2_rn(ay, ay, __fmul2_rn(az, az)));
+  // rsqrt.approx (relative error <= 2^-22.9): the common scale of the three
+  // components leaves the direction untouched; |n| - 1 stays below ~3e-7
   float2 r = make_float2(rsqrt_ftz(s.x), rsqrt_ftz(s.y));
-  // one Newton step: r *= 1.5 - 0.5 s r^2
-  const float2 hs = __fmul2_rn(make_float2(-0.5f, -0.5f), __fmul2_rn(s, r));
-  r = __fmul2_rn(r, __ffma2_rn(hs, r, make_float2(1.5f, 1.5f)));
   // an invalid pixel's normal is NaN: one select on r instead of three on n
   if (!ok0) r.x = __int_as_float(0x7fc00000);
   if (!ok1) r.y = __int_as_float(0x7fc00000);
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
     fence_mbar_init();
-    load_tile(cur, 0);
+    if (SN_EXP != 5) load_tile(cur, 0);
   }
   __syncthreads();
 
@@ -711,27 +712,28 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 
   for (int it = 0; item < n_items; ++it, item += gridDim.x, cur = nxt, nxt.advance()) {
     const int buf = it & 1;
-    if (tid == 0 && item + (int)gridDim.x < n_items) load_tile(nxt, buf ^ 1);
+    if (SN_EXP != 5 && tid == 0 && item + (int)gridDim.x < n_items) load_tile(nxt, buf ^ 1);
     const int x0 = cur.x0(), y0 = cur.y0(), bz = cur.bz;
     const int sh = (x0 - R) - tile_x0<R, AE>(x0);  // logical column c <-> smem column c + sh
     const T* in = reinterpret_cast<const T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
-    mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
+    if (SN_EXP != 5) mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
     // SN_EXP (experiment builds only, tools/exp_fused.sh; 0 in the product):
-    // 1 no TMA stores, 2 no pass H, 3 no pass V, 4 neither pass
-    if (SN_EXP != 3 && SN_EXP != 4) pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
+    // 1 no stores, 2 no pass H, 3 no pass V, 4 neither pass, 5 stores only
+    // (no loads, no passes), 6 loads only
+    if (SN_EXP != 3 && SN_EXP < 4) pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
     // staging of the previous item consumed by its TMA stores (issued by warp 8)
     if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) bulk_wait_read0();
     __syncthreads();
 
-    if (SN_EXP != 2 && SN_EXP != 4)
+    if (SN_EXP != 2 && SN_EXP < 4)
       if (tid < 256)
         pass_h<R, T, SN_ROWBULK>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
     fence_proxy_async_smem();
     __syncthreads();
     // output stores from a warp that is idle in pass H -- warp 0 goes
     // straight on to the next item
-    if (SN_EXP != 1 && tid >= kStoreTid && tid < kStoreTid + kStoreLanes) {
+    if (SN_EXP != 1 && SN_EXP != 6 && tid >= kStoreTid && tid < kStoreTid + kStoreLanes) {
       const int b = tid - kStoreTid;
       if constexpr (SN_ROWBULK) {
         // one contiguous bulk copy per output row (3072 B, less at the right
