@@ -496,3 +496,43 @@ def test_unaligned_widths_take_the_fast_kernel(cuda_dev, W):
     for b in range(2):
         assert np.array_equal(np.isfinite(out[b]), np.isfinite(gen[b]))
         _check_record(out[b], m[b], _oracle_record(t[b].cpu().numpy(), sc.rig, 9))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,H", [(2, 1), (4, 3), (6, 17), (126, 15), (130, 16), (258, 33),
+                                 (299, 19), (301, 18), (302, 17), (1242, 20)])
+@pytest.mark.parametrize("dtype", ["f32", "f64", "png16"])
+def test_fused_stores_stay_inside_the_output(cuda_dev, W, H, dtype):
+    """The fused pass writes whole output rows with bulk copies (and, for odd
+    widths, through a pitched buffer): every record and mask byte is written,
+    and nothing outside the [B, H, W, 6] / [B, H, W] views -- guard words
+    around both stay intact (compute-sanitizer is not available on the GPU
+    pool, so the bounds are checked directly)."""
+    from paper_2504_15121_b200 import device, scenes
+    B, pad = 2, 1024  # floats / bytes of guard on each side (16-B aligned views)
+    sc = scenes.street_scene(max(W, 8), max(H, 8))
+    d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.3, W + H)[:H, :W]
+    d = np.ascontiguousarray(np.stack([d, d[::-1]]).astype(np.float32))
+    d[0, H // 2, W // 2] = np.nan
+    n = B * H * W * 6
+    canary = -1.2345e-30
+    flat = torch.full((n + 2 * pad,), canary, dtype=torch.float32, device=cuda_dev)
+    out = flat[pad:pad + n].view(B, H, W, 6)
+    mflat = torch.full((B * H * W + 2 * pad,), 0xA5, dtype=torch.uint8, device=cuda_dev)
+    mask = mflat[pad:pad + B * H * W].view(B, H, W)
+    t = torch.from_numpy(d).to(cuda_dev)
+    if dtype == "f32":
+        device.oriented_points(t, sc.rig, 9, out=out, mask=mask)
+    elif dtype == "f64":
+        device.oriented_points(t.double(), sc.rig, 9, out=out, mask=mask)
+    else:
+        raw = torch.from_numpy(np.clip(np.nan_to_num(d, nan=-1.0) * 256 + 1, 0, 65535)
+                               .astype(np.uint16).view(np.int16)).to(cuda_dev)
+        device.oriented_points_png16(raw, sc.rig, 9, out=out, mask=mask)
+    torch.cuda.synchronize()
+    f = flat.cpu().numpy()
+    assert np.all(f[:pad] == np.float32(canary)) and np.all(f[pad + n:] == np.float32(canary))
+    assert not np.any(f[pad:pad + n] == np.float32(canary)), "a record was not written"
+    m = mflat.cpu().numpy()
+    assert np.all(m[:pad] == 0xA5) and np.all(m[pad + B * H * W:] == 0xA5)
+    assert set(np.unique(m[pad:pad + B * H * W]).tolist()) <= {0, 1}

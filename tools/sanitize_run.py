@@ -27,5 +27,14 @@ local_strip_frame(dt[0].contiguous(), StripPlan.for_kernel(140, 300, 3, 9), r, 9
 device.compact_cloud(pts, mask)
 device.adaptive_points(dt, r, StarConfig(stop="cd", threshold=0.1))
 device.adaptive_points(dt, r, StarConfig(stop="st", threshold=0.5, shared_range=True))
+# widths TMA cannot address: pitched input (302), pitched input + output (301, 299)
+for w in (302, 301, 299):
+    dw = dt[:, :, :w].contiguous()
+    device.oriented_points(dw, r, 9, mask=torch.empty(dw.shape, dtype=torch.uint8, device="cuda"))
+    device.oriented_points(dw.double(), r, 5)
+    device.pipeline(dw, r, 9, 0.2)
+raw = torch.clamp(dt.nan_to_num(0.0) * 256 + 1, 0, 65535).to(torch.int32).to(torch.int16)
+device.oriented_points_png16(raw, r, 9)
+device.oriented_points_png16(raw[:, :, :301].contiguous(), r, 9)
 torch.cuda.synchronize()
 print("sanitize run ok")
