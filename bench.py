@@ -204,21 +204,31 @@ class ClockSampler:
 # GPU arm
 
 
-def next_row_timings(d8, out8, rig, dev):
-    """us/frame of the f1-f4 kernels on 8 C3 frames (CUDA events, 3 reps)."""
+def measured_hbm_peak() -> float:
+    """HBM GB/s: MEASURED_PEAKS.json (driver-written copy bandwidth), else the
+    profiling recipe's fallback."""
+    pk = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(pk.read_text()) if pk.exists() else {}
+    return float(peaks.get("hbm_gbs", 6650.0))
+
+
+def next_row_timings(dN, outN, rig, dev):
+    """us/frame of the f1-f4 kernels (CUDA events, 3 reps after one untimed
+    call): the adaptive walks on 8 C3 frames, the streaming rows (PNG16 fused
+    pass, cloud compaction, evaluation) on all of dN (64 frames: whole waves)."""
     import torch
     from paper_2504_15121_b200 import StarConfig, device, scenes
-    n = d8.shape[0]
-    mask = torch.empty(d8.shape, dtype=torch.uint8, device=dev)
-    device.oriented_points(d8, rig, KSIZE, out=out8, mask=mask)
+    n = dN.shape[0]
+    d8, out8 = dN[:8], outN[:8]
+    mask = torch.empty(dN.shape, dtype=torch.uint8, device=dev)
     sc = scenes.street_scene(W, H)
     gt = torch.from_numpy(np.ascontiguousarray(scenes.raycast(sc)[2])).to(dev)
     gt = gt.expand(n, -1, -1, -1).contiguous()
     gm = torch.isfinite(gt).all(-1).to(torch.uint8)
-    raw = torch.clamp(torch.round(d8 * 256 + 1), 1, 65535).to(torch.int32).to(torch.uint16)
+    raw = torch.clamp(torch.round(dN * 256 + 1), 1, 65535).to(torch.int32).to(torch.uint16)
     cd, st = StarConfig(stop="cd", threshold=0.1), StarConfig(stop="st", threshold=0.2)
 
-    def timed(fn, reps=3):
+    def timed(fn, frames, reps=3):
         fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -227,17 +237,58 @@ def next_row_timings(d8, out8, rig, dev):
             fn()
         e1.record()
         torch.cuda.synchronize()
-        return round(e0.elapsed_time(e1) * 1e3 / reps / n, 2)
+        return round(e0.elapsed_time(e1) * 1e3 / reps / frames, 2)
 
-    return {
-        "frames": n,
-        "adaptive_cd_s10_d8": timed(lambda: device.adaptive_points(d8, rig, cd, out=out8)),
-        "adaptive_st_s10_d8": timed(lambda: device.adaptive_points(d8, rig, st, out=out8)),
-        "compact_cloud": timed(lambda: device.compact_cloud(out8, mask)),
-        "angular_error_and_stats": timed(lambda: device.angular_error(out8, gt, gm)),
+    gpu = {
+        "frames_adaptive": 8,
+        "frames_streaming": n,
+        "adaptive_cd_s10_d8": timed(lambda: device.adaptive_points(d8, rig, cd, out=out8), 8),
+        "adaptive_st_s10_d8": timed(lambda: device.adaptive_points(d8, rig, st, out=out8), 8),
         "fused_pass_png16_input": timed(lambda: device.oriented_points_png16(
-            raw, rig, KSIZE, scale=256.0, out=out8)),
+            raw, rig, KSIZE, scale=256.0, out=outN), n),
     }
+    # the fixed-pass records + mask the cloud and the evaluation consume
+    device.oriented_points(dN, rig, KSIZE, out=outN, mask=mask)
+    gpu["compact_cloud"] = timed(lambda: device.compact_cloud(outN, mask), n)
+    gpu["angular_error_and_stats"] = timed(lambda: device.angular_error(outN, gt, gm), n)
+    # HBM rows: algorithmic bytes per frame / time vs the measured copy peak
+    keep = float(mask.float().mean())
+    peak = measured_hbm_peak()
+    roof = {}
+    for name, bpp in (("fused_pass_png16_input", 2 + 24), ("compact_cloud", 1 + 48 * keep)):
+        gbs = bpp * H * W / (gpu[name] * 1e-6) / 1e9
+        roof[name] = {"bytes_per_px": round(bpp, 3), "achieved_gbs": round(gbs, 1),
+                      "frac": round(gbs / peak, 4) if peak else None}
+    return gpu, roof, (dN[0].double().cpu().numpy(), gt[0].cpu().numpy(), gm[0].cpu().numpy())
+
+
+def next_row_cpu(d, gt_n, gt_m, rig):
+    """us/frame of the reference algorithms of the f1-f4 rows (the oracle port,
+    one C3 frame, numpy on the host; bench-only use of oracle/)."""
+    from oracle import stereonorm_oracle as orc
+    orig = orc.Rig(rig.fx, rig.fy, rig.u0, rig.v0, rig.baseline)
+
+    def t(fn):
+        t0 = time.perf_counter()
+        r = fn()
+        return round((time.perf_counter() - t0) * 1e6, 1), r
+
+    res = {"frames": 1, "cores": 1}
+    res["adaptive_cd_s10_d8"], _ = t(lambda: orc.estimate_normals_adaptive(
+        d, orig, orc.Star(stop="cd", threshold=0.1)))
+    res["adaptive_st_s10_d8"], _ = t(lambda: orc.estimate_normals_adaptive(
+        d, orig, orc.Star(stop="st", threshold=0.2)))
+    raw = np.clip(np.round(d * 256 + 1), 1, 65535).astype(np.int64)
+
+    def png_fused():
+        v, _ = orc.dequant_png16(raw, 256.0, 0)
+        return orc.oriented_points(v, orig, KSIZE, threads=1)
+
+    res["fused_pass_png16_input"], (p6, ok) = t(png_fused)
+    res["compact_cloud"], _ = t(lambda: orc.ply_keep(p6, ok))
+    res["angular_error_and_stats"], _ = t(
+        lambda: orc.summarize(*orc.angular_error_map(p6[..., 3:], ok, gt_n, gt_m)))
+    return res
 
 
 def main():
@@ -329,11 +380,8 @@ def main():
     value = world * px_step / 1e6 / (ms_per_step / 1e3)
 
     # roofline of the dominant kernel (fused pass): algorithmic bytes / its event time
-    peaks = {}
     pk = ROOT / "MEASURED_PEAKS.json"
-    if pk.exists():
-        peaks = json.loads(pk.read_text())
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak = measured_hbm_peak()
     fused_bytes = BYTES_PER_PX
     achieved = fused_bytes * px_step / (fused_avg / 1e3) / 1e9
     traffic = None
@@ -391,10 +439,12 @@ def main():
 
     # next rows of the scope table, timed briefly on 8 of the
     # same frames after the headline measurement: evidence, not the metric
-    extras = None
+    extras = extras_roof = extras_cpu = None
     if rank == 0 and world == 1 and args.extras and not args.no_extras:
         try:
-            extras = next_row_timings(disp[:8], out[:8], rig, dev)
+            extras, extras_roof, host = next_row_timings(disp[:64], out[:64], rig, dev)
+            if not args.no_cpu:
+                extras_cpu = next_row_cpu(*host, rig)
         except Exception as exc:  # never let an extra cost the headline line
             extras = {"error": f"{type(exc).__name__}: {exc}"}
 
@@ -431,6 +481,8 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "next_rows_us_per_frame": extras,
+            "next_rows_roofline": extras_roof,
+            "next_rows_cpu_us_per_frame": extras_cpu,
             "gpu_launches": args.steps * (1 + (4 if args.pipeline == "full" else 0)),
             "clocks": clocks,
         }

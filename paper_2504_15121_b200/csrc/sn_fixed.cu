@@ -70,6 +70,13 @@ constexpr size_t kRowStageBytes = (size_t)kG * kRowPitch;
 
 __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// accumulator of the sliding sums (see sval below): fp64, int32 for PNG16
+template <typename T> struct AccOf { using type = double; using pair = double2; };
+template <> struct AccOf<Png16> { using type = int; using pair = int2; };
+template <typename T> using Acc = typename AccOf<T>::type;
+template <typename T> using AccPair = typename AccOf<T>::pair;
+template <typename T> constexpr bool kIntAcc = sizeof(Acc<T>) == 4;
+
 template <int R, typename T>
 struct FastCfg {
   static constexpr int NC = kTW + 2 * R;  // C/Rr columns (output columns + halo)
@@ -79,7 +86,7 @@ struct FastCfg {
   static constexpr int BW = (NC + AE - 1 + AE - 1) / AE * AE;
   static constexpr size_t STAGE_BYTES = SN_ROWBULK ? kRowStageBytes : (size_t)kBoxes * kG * 128;
   static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
-  static constexpr size_t CS_BYTES = (size_t)NC * kCP * 16;  // double2 (C, Rr) [NC][kCP]
+  static constexpr size_t CS_BYTES = (size_t)NC * kCP * sizeof(AccPair<T>);  // (C, Rr) [NC][kCP]
   // column flags (NC words) + 8-column block ORs of them (NB words)
   static constexpr int NB = (NC + 7) / 8;
   static constexpr size_t FL_BYTES = align_up((size_t)(NC + NB) * 4, 16);
@@ -145,20 +152,32 @@ __device__ __forceinline__ double dval<Png16>(Png16 x, const FixedParams& p) {
   return png16_value(x.raw, p.png_invalid, p.png_scale, p.png_rcp);
 }
 
-// the value the sliding sums accumulate.  PNG16 sums the integers raw - 1
-// (exact, never "big") and scales U, V by 1/scale once per pixel: the sums of
-// d = (raw - 1) / scale then carry one rounding instead of one per sample
+// Accumulator of the sliding sums.  fp32/fp64 inputs: fp64, exact for the
+// window's dynamic range.  PNG16: the integers raw - 1 in
+// int32 -- |raw - 1| < 2^16, so C < 2^20, Rr < 2^23, U, V < 2^28 for R <= 8:
+// exact, on the full-rate integer pipe instead of the fp64 one, and 8-byte
+// (C, Rr) pairs in shared memory.  The 1/scale of d = (raw - 1)/scale is
+// never applied to the sums: the normal is homogeneous of degree 1 in
+// (U, V, d), so the integer sums with d_int = raw - 1 give the same direction
+// (times sign(scale)).
+// (AccOf: the accumulator types, defined above FastCfg)
+
+__device__ __forceinline__ double2 make_pair(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ int2 make_pair(int a, int b) { return make_int2(a, b); }
+// a + w * x: one FMA in fp64 (exact here), one IMAD in int32
+__device__ __forceinline__ double mac(double w, double x, double a) { return fma(w, x, a); }
+__device__ __forceinline__ int mac(int w, int x, int a) { return a + w * x; }
+
 template <typename T>
-__device__ __forceinline__ double sval(T x, const FixedParams& p) {
+__device__ __forceinline__ Acc<T> sval(T x, const FixedParams& p) {
   return dval(x, p);
 }
 template <>
-__device__ __forceinline__ double sval<Png16>(Png16 x, const FixedParams&) {
-  // raw - 1 exactly: (2^52 + raw) - (2^52 + 1), one DADD instead of a
-  // conversion.  Invalid samples keep their (finite, exact) value: pass V
-  // flags them from the integer, and only windows that hold one -- invalid
-  // anyway -- see it in their sums
-  return __dsub_rn(__hiloint2double(0x43300000, (int)x.raw), 4503599627370497.0);
+__device__ __forceinline__ int sval<Png16>(Png16 x, const FixedParams&) {
+  // Invalid samples keep their (finite, exact) value: pass V flags them from
+  // the integer, and only windows that hold one -- invalid anyway -- see it
+  // in their sums
+  return (int)x.raw - 1;
 }
 
 // the fp32 epilogue's view of the centre sample: d rounded to fp32 and the
@@ -193,6 +212,17 @@ __device__ __forceinline__ bool dpos<Png16>(Png16 x, const FixedParams& p) {
   // the caller's window test already excludes raw == invalid (the centre is
   // in its own support): only the sign of (raw - 1) / scale is left
   return ((int)x.raw - 1) * p.png_sign > 0;
+}
+
+// the centre value the normal's alpha*d term uses: d itself, or for PNG16
+// (integer sums) raw - 1 exactly
+template <typename T>
+__device__ __forceinline__ float dnorm(T, float d) {
+  return d;
+}
+template <>
+__device__ __forceinline__ float dnorm<Png16>(Png16 x, float) {
+  return __fsub_rn(__int_as_float(0x4b000000 | (int)x.raw), 8388609.0f);
 }
 
 // inputs whose records take the fp32 epilogue: fp32 disparities, and PNG16
@@ -230,13 +260,18 @@ __device__ __forceinline__ void normal_square(double U, double V, float alpha_f,
 // <= ~3 ulp), x = du z / fx, y = dv z / fy, NaN unless d is finite and > 0;
 // subnormal d takes an fp64 division (flush-to-zero would turn a finite z
 // into inf).  Normal: normal_square's formula for both pixels; a pixel whose
-// |n|^2 leaves fp32's comfortable range takes the fp64 path.
-__device__ __forceinline__ void records_pair(double U0, double V0, double U1, double V1, float d0,
-                                             float d1, float2 zz, bool ok0, bool ok1, float duh,
+// |n|^2 leaves fp32's comfortable range takes the fp64 path.  A = int: PNG16
+// sums of raw - 1 with dn = raw - 1 (the normal is homogeneous in (U, V, d):
+// same direction as with d = (raw - 1)/scale, up to sign(scale)); else
+// dn = d.
+template <typename A>
+__device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, float d1, float dn0,
+                                             float dn1, float2 zz, bool ok0, bool ok1, float duh,
                                              float dv, const FixedParams& p, float* o) {
+  constexpr bool kInt = sizeof(A) == 4;
   // points; zz = fxb_f * rcp(d) as computed by the caller (shared with the
   // passable predicate); duh = (x - u0_hi) exactly, du = duh - u0_lo
-  const float2 dd = make_float2(d0, d1);
+  const float2 dd = make_float2(dn0, dn1);
   const float2 du = make_float2(duh - p.u0_lo, (duh + 1.0f) - p.u0_lo);
   const bool pv0 = (d0 > 0.0f) && (d0 <= 3.402823466e38f);
   const bool pv1 = (d1 > 0.0f) && (d1 <= 3.402823466e38f);
@@ -265,6 +300,9 @@ __device__ __forceinline__ void records_pair(double U0, double V0, double U1, do
   // rsqrt.approx (relative error <= 2^-22.9): the common scale of the three
   // components leaves the direction untouched; |n| - 1 stays below ~3e-7
   float2 r = make_float2(rsqrt_ftz(s.x), rsqrt_ftz(s.y));
+  if constexpr (kInt) {
+    if (p.png_sign < 0) r = make_float2(-r.x, -r.y);
+  }
   // an invalid pixel's normal is NaN: one select on r instead of three on n
   if (!ok0) r.x = __int_as_float(0x7fc00000);
   if (!ok1) r.y = __int_as_float(0x7fc00000);
@@ -276,12 +314,17 @@ __device__ __forceinline__ void records_pair(double U0, double V0, double U1, do
   o[10] = ny.y;
   o[11] = nz.y;
   const bool in0 = s.x > 1e-30f && s.x < 1e30f, in1 = s.y > 1e-30f && s.y < 1e30f;
+  // the rare fp64 path works on the disparity sums: integer sums / scale
+  auto dsum = [&](A u) -> double {
+    if constexpr (kInt) return __ddiv_rn((double)u, p.png_scale);
+    else return u;
+  };
   if (ok0 && !in0)
-    normal_from_moments(U0, V0, p.alpha, (double)d0, (double)du.x, (double)dv, p.fx, p.fy, o[3],
-                        o[4], o[5]);
+    normal_from_moments(dsum(U0), dsum(V0), p.alpha, (double)d0, (double)du.x, (double)dv, p.fx,
+                        p.fy, o[3], o[4], o[5]);
   if (ok1 && !in1)
-    normal_from_moments(U1, V1, p.alpha, (double)d1, (double)du.y, (double)dv, p.fx, p.fy, o[9],
-                        o[10], o[11]);
+    normal_from_moments(dsum(U1), dsum(V1), p.alpha, (double)d1, (double)du.y, (double)dv, p.fx,
+                        p.fy, o[9], o[10], o[11]);
 }
 
 // ---------------------------------------------------------------------------
@@ -377,9 +420,10 @@ __device__ __forceinline__ int tile_x0(int x0) {
 // idle lanes beyond NC.
 template <int R, typename T>
 __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int H, int W, int h,
-                                       int c, bool unit, double2* CR, uint32_t* fl,
+                                       int c, bool unit, AccPair<T>* CR, uint32_t* fl,
                                        const FixedParams& p) {
   using Cfg = FastCfg<R, T>;
+  using A = Acc<T>;
   constexpr int BW = Cfg::BW;
   constexpr int NC = Cfg::NC;
   // all operands live in shared memory: let the compiler emit LDS/STS
@@ -426,13 +470,13 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
     const int lo = max(0, R - y0 - r0), hi = min(NV, H - y0 + R - r0);
     uint32_t inside = 0;
     if ((unsigned)gx < (unsigned)W && hi > lo) inside = (uint32_t)(((1ull << (hi - lo)) - 1ull) << lo);
-    double v[NV];
+    A v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = sval(raw[i], p);
     constexpr uint32_t kAll = (NV >= 32) ? 0xffffffffu : ((1u << NV) - 1u);
     uint32_t fin = kAll & ~png_inv;
     bool big = false;
-    if (!all_small) {
+    if constexpr (!kIntAcc<T>) if (!all_small) {
       // rare: non-finite (zeroed so the sliding sums stay finite) or huge samples
       fin = 0;
 #pragma unroll
@@ -444,33 +488,33 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
       }
     }
     const uint32_t invb = ~(fin & inside);
-    double2* cr = CR + c * kCP + r0;
+    AccPair<T>* cr = CR + c * kCP + r0;
     if (!big) {
-      double C = 0.0, Rr = 0.0;
+      A C = 0, Rr = 0;
 #pragma unroll
       for (int j = 0; j < NWIN; ++j) {
         C += v[j];
-        Rr = fma((double)(j - R), v[j], Rr);
+        Rr = mac((A)(j - R), v[j], Rr);
       }
-      cr[0] = make_double2(C, Rr);
+      cr[0] = make_pair(C, Rr);
 #pragma unroll
       for (int g = 1; g < HG; ++g) {
-        const double vin = v[g + 2 * R], vout = v[g - 1];
-        const double tin = fma((double)R, vout, (double)(R + 1) * vin);  // off the chain
+        const A vin = v[g + 2 * R], vout = v[g - 1];
+        const A tin = mac((A)R, vout, (A)(R + 1) * vin);  // off the chain
         C += vin - vout;
         Rr = (Rr - C) + tin;
-        cr[g] = make_double2(C, Rr);
+        cr[g] = make_pair(C, Rr);
       }
     } else {
 #pragma unroll
       for (int g = 0; g < HG; ++g) {
-        double C = 0.0, Rr = 0.0;
+        A C = 0, Rr = 0;
 #pragma unroll
         for (int j = 0; j < NWIN; ++j) {
           C += v[g + j];
-          Rr = fma((double)(j - R), v[g + j], Rr);
+          Rr = mac((A)(j - R), v[g + j], Rr);
         }
-        cr[g] = make_double2(C, Rr);
+        cr[g] = make_pair(C, Rr);
       }
     }
     uint32_t acc = 0;
@@ -494,10 +538,11 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
 // staging (kRowPitch), else 24 128B-swizzled TMA boxes
 template <int R, typename T, bool ROWS = false>
 __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int y0, int bz, int H,
-                                       int W, const double2* CR, const uint32_t* fl,
+                                       int W, const AccPair<T>* CR, const uint32_t* fl,
                                        uint32_t stage_base, const FixedParams& p,
                                        uint8_t* mask_out) {
   using Cfg = FastCfg<R, T>;
+  using A = Acc<T>;
   __builtin_assume(__isShared(in));
   __builtin_assume(__isShared(CR));
   __builtin_assume(__isShared(fl));
@@ -507,10 +552,10 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   const int g = hl & 15;
   const int q = hl >> 4;  // run of kRun output columns
   const int colbase = q * kRun;
-  double cc[NH], rr[NH];
+  A cc[NH], rr[NH];
 #pragma unroll
   for (int i = 0; i < NH; ++i) {
-    const double2 v = CR[(colbase + i) * kCP + g];
+    const AccPair<T> v = CR[(colbase + i) * kCP + g];
     cc[i] = v.x;
     rr[i] = v.y;
   }
@@ -556,21 +601,21 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   uint32_t validbits = 0;
 
   // sliding sums first (short dependent chain), then independent epilogues
-  double Us[kRun], Vs[kRun];
+  A Us[kRun], Vs[kRun];
   if (!big) {
-    double Bx = 0.0, U = 0.0, V = 0.0;
+    A Bx = 0, U = 0, V = 0;
 #pragma unroll
     for (int j = 0; j < NWIN; ++j) {
       Bx += cc[j];
-      U = fma((double)(j - R), cc[j], U);
+      U = mac((A)(j - R), cc[j], U);
       V += rr[j];
     }
     Us[0] = U;
     Vs[0] = V;
 #pragma unroll
     for (int j = 1; j < kRun; ++j) {
-      const double cin = cc[j + 2 * R], cout = cc[j - 1];
-      const double tin = fma((double)R, cout, (double)(R + 1) * cin);  // independent of the chain
+      const A cin = cc[j + 2 * R], cout = cc[j - 1];
+      const A tin = mac((A)R, cout, (A)(R + 1) * cin);  // independent of the chain
       Bx += cin - cout;
       U = (U - Bx) + tin;
       V += rr[j + 2 * R] - rr[j - 1];
@@ -580,21 +625,14 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   } else {
 #pragma unroll
     for (int j = 0; j < kRun; ++j) {
-      double U = 0.0, V = 0.0;
+      A U = 0, V = 0;
 #pragma unroll
       for (int i = 0; i < NWIN; ++i) {
-        U = fma((double)(i - R), cc[j + i], U);
+        U = mac((A)(i - R), cc[j + i], U);
         V += rr[j + i];
       }
       Us[j] = U;
       Vs[j] = V;
-    }
-  }
-  if constexpr (sizeof(T) == 2) {  // PNG16: integer sums -> disparity sums
-#pragma unroll
-    for (int j = 0; j < kRun; ++j) {
-      Us[j] *= p.png_rcp;
-      Vs[j] *= p.png_rcp;
     }
   }
   // depths zf = fxb * rcp(d) of the run's pixels (zc[1 .. kRun])
@@ -622,8 +660,9 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
       f32_epi = safe((double)drow[j]) && safe((double)drow[j + 1]);
     }
     if (f32_epi) {
-      records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], df[j], df[j + 1],
-                   make_float2(zc[j + 1], zc[j + 2]), ok0, ok1, du_hi + (float)j, dv_f, p, o);
+      records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], df[j], df[j + 1], dnorm(drow[j], df[j]),
+                   dnorm(drow[j + 1], df[j + 1]), make_float2(zc[j + 1], zc[j + 2]), ok0, ok1,
+                   du_hi + (float)j, dv_f, p, o);
     } else {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -678,7 +717,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   // __shared__ array keeps the shared address space (LDS/STS, not generic LD/ST)
   constexpr uint32_t kAlign = SN_ROWBULK ? 128u : 1024u;
   uint8_t* smem = smem_raw + ((kAlign - (smem_u32(smem_raw) & (kAlign - 1u))) & (kAlign - 1u));
-  double2* CR = reinterpret_cast<double2*>(smem + Cfg::CS);
+  AccPair<T>* CR = reinterpret_cast<AccPair<T>*>(smem + Cfg::CS);
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR);
   const uint32_t stage_base = smem_u32(smem + Cfg::STAGE);

@@ -5,6 +5,8 @@ make_golden.py); the oracle must reproduce them: masks/labels bit-exact,
 values to fp64 rounding.
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -98,3 +100,49 @@ def test_oracle_adaptive_matches_reference(adaptive_golden, name):
     n, ok = orc.estimate_normals_adaptive(c["d"], orc.Rig(fx, fy, u0, v0, b), orc.Star(**c["config"]))
     assert np.array_equal(ok, c["nmask"])
     np.testing.assert_array_equal(n[ok], c["normals"][ok])
+
+
+def test_oracle_evaluation_matches_reference():
+    """The oracle's angular_error_map + summarize == the reference's
+    (evaluation.py:34-73) on its own golden cases, bit for bit."""
+    from oracle import stereonorm_oracle as orc
+    z = np.load(Path(__file__).resolve().parent / "golden" / "eval_cases.npz")
+    for tag in z["names"]:
+        tag = str(tag)
+        err, ok = orc.angular_error_map(z[f"{tag}__est_n"], z[f"{tag}__est_m"], z["gt_n"], z["gt_m"],
+                                        z[f"{tag}__mask"])
+        ref = z[f"{tag}__err"]
+        assert np.array_equal(ok, np.isfinite(ref)), tag
+        np.testing.assert_array_equal(err[ok], ref[ok])
+        assert orc.summarize(err, ok) == tuple(
+            int(v) if i == 5 else float(v) for i, v in enumerate(z[f"{tag}__stats"])), tag
+    with pytest.raises(ValueError):
+        orc.summarize(np.zeros(3), np.zeros(3, bool))
+
+
+def test_oracle_codecs_match_reference():
+    """The oracle's PNG16 dequantisation and PFM payload decode == the
+    reference's read_disparity_png16 / read_pfm (formats.py:84-150) on its own
+    golden files, bit for bit."""
+    import io
+    from PIL import Image
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200.formats import _pfm_header
+    z = np.load(Path(__file__).resolve().parent / "golden" / "codec_cases.npz")
+    for tag in z["png_names"]:
+        tag = "png_" + str(tag)
+        raw = np.asarray(Image.open(io.BytesIO(z[f"{tag}__bytes"].tobytes())), dtype=np.int64)
+        assert np.array_equal(raw, z[f"{tag}__raw"]), tag
+        v, m = orc.dequant_png16(raw, float(z[f"{tag}__scale"]), int(z[f"{tag}__invalid"]))
+        assert np.array_equal(m, z[f"{tag}__mask"]), tag
+        np.testing.assert_array_equal(v[m], z[f"{tag}__values"][m])
+    for tag in z["pfm_names"]:
+        tag = "pfm_" + str(tag)
+        data = z[f"{tag}__bytes"].tobytes()
+        _, w, h, scale, pos = _pfm_header(data)  # the product's host-side header parser
+        ch = int(z[f"{tag}__channels"])
+        g = orc.decode_pfm_payload(data[pos:pos + w * h * ch * 4], h, w, ch, scale < 0)
+        # read_pfm / read_pfm_normals then mask non-finite samples (fields.py:37-46)
+        ok = np.isfinite(g) if ch == 1 else np.isfinite(g).all(-1)
+        assert np.array_equal(ok, z[f"{tag}__mask"]), tag
+        np.testing.assert_array_equal(g[ok], z[f"{tag}__values"][ok])
