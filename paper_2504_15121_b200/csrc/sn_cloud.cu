@@ -35,9 +35,16 @@ __global__ void __launch_bounds__(kCloudThreads)
     const int64_t p0 = (blk - f * bpf) * kCloudBlock;
     const uint8_t* m = mask + f * HW;
     int c = 0;
-    for (int i = tid; i < kCloudBlock; i += kCloudThreads) {
-      const int64_t px = p0 + i;
-      c += (px < HW && m[px] != 0) ? 1 : 0;
+    if (p0 + kCloudBlock <= HW && (reinterpret_cast<uintptr_t>(m + p0) & 7u) == 0) {
+      // 8 mask bytes per thread: nonzero bytes by a SIMD compare, then popc
+      static_assert(kCloudBlock == kCloudThreads * 8, "one uint2 per thread");
+      const uint2 w = reinterpret_cast<const uint2*>(m + p0)[tid];
+      c = (__popc(__vcmpne4(w.x, 0u)) + __popc(__vcmpne4(w.y, 0u))) >> 3;
+    } else {
+      for (int i = tid; i < kCloudBlock; i += kCloudThreads) {
+        const int64_t px = p0 + i;
+        c += (px < HW && m[px] != 0) ? 1 : 0;
+      }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
@@ -122,7 +129,17 @@ __global__ void __launch_bounds__(kCloudThreads)
 #pragma unroll
     for (int r = 0; r < kSegPx / 32; ++r) {
       const uint32_t b = bal[r];
-      if ((b >> lane) & 1u) {
+      if (b == 0xffffffffu && next + 32 <= capacity) {
+        // 32 kept pixels in a row: one contiguous 768-byte copy, lanes on
+        // consecutive 8-byte words (every access fully coalesced; records
+        // are 8-byte aligned at both ends)
+        const float2* src = reinterpret_cast<const float2*>(out6 + (f * HW + s0 + r * 32) * 6);
+        float2* dst = reinterpret_cast<float2*>(cloud + next * 6);
+        const float2 a0 = src[lane], a1 = src[lane + 32], a2 = src[lane + 64];
+        dst[lane] = a0;
+        dst[lane + 32] = a1;
+        dst[lane + 64] = a2;
+      } else if ((b >> lane) & 1u) {
         const int64_t px = s0 + r * 32 + lane;
         const int64_t slot = next + __popc(b & ((1u << lane) - 1u));
         if (slot < capacity) {

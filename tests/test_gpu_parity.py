@@ -536,3 +536,22 @@ def test_fused_stores_stay_inside_the_output(cuda_dev, W, H, dtype):
     m = mflat.cpu().numpy()
     assert np.all(m[:pad] == 0xA5) and np.all(m[pad + B * H * W:] == 0xA5)
     assert set(np.unique(m[pad:pad + B * H * W]).tolist()) <= {0, 1}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,p", [((3, 64, 96), 0.5), ((2, 37, 61), 0.97), ((2, 128, 256), 1.0),
+                                     ((1, 33, 65), 0.0)])
+def test_compact_cloud_any_mask(cuda_dev, shape, p):
+    """Compaction keeps the records whose mask byte is nonzero (any value, not
+    just 1), in raster order, for sparse, dense and full masks and frames whose
+    pixel count is not a multiple of the 8-byte mask reads."""
+    from paper_2504_15121_b200 import device
+    rng = np.random.default_rng(len(shape) + int(p * 100))
+    B, H, W = shape
+    rec = rng.standard_normal((B, H, W, 6)).astype(np.float32)
+    m = (rng.random((B, H, W)) < p).astype(np.uint8) * rng.choice([1, 7, 255], (B, H, W)).astype(np.uint8)
+    cloud, offsets = device.compact_cloud(torch.from_numpy(rec).to(cuda_dev),
+                                          torch.from_numpy(m).to(cuda_dev))
+    keep = m != 0
+    assert np.array_equal(cloud.cpu().numpy(), rec[keep])
+    assert np.array_equal(offsets.numpy(), np.concatenate([[0], np.cumsum(keep.reshape(B, -1).sum(1))]))
