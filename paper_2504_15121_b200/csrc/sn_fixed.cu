@@ -255,6 +255,17 @@ __device__ __forceinline__ void normal_square(double U, double V, float alpha_f,
   }
 }
 
+// rare paths of the epilogue, kept out of line so the hot loop stays small
+// (eight inlined copies of the fp64 normal and four of the fp64 division per
+// pass-H lane otherwise)
+__device__ __noinline__ float3 normal_rare(double U, double V, double alpha, double d, double du,
+                                           double dv, double fx, double fy) {
+  float3 n;
+  normal_from_moments(U, V, alpha, d, du, dv, fx, fy, n.x, n.y, n.z);
+  return n;
+}
+__device__ __noinline__ float depth_rare(double fxb, float d) { return (float)(fxb / (double)d); }
+
 // Oriented-point records of two neighbouring pixels (same row) with packed
 // f32x2 arithmetic (FFMA2/FMUL2 on sm_100a).  Point: z = fxb/d (rcp.approx,
 // <= ~3 ulp), x = du z / fx, y = dv z / fy, NaN unless d is finite and > 0;
@@ -275,8 +286,8 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
   const float2 du = make_float2(duh - p.u0_lo, (duh + 1.0f) - p.u0_lo);
   const bool pv0 = (d0 > 0.0f) && (d0 <= 3.402823466e38f);
   const bool pv1 = (d1 > 0.0f) && (d1 <= 3.402823466e38f);
-  if (pv0 && d0 < 1.175494351e-38f) zz.x = (float)(p.fxb / (double)d0);
-  if (pv1 && d1 < 1.175494351e-38f) zz.y = (float)(p.fxb / (double)d1);
+  if (pv0 && d0 < 1.175494351e-38f) zz.x = depth_rare(p.fxb, d0);
+  if (pv1 && d1 < 1.175494351e-38f) zz.y = depth_rare(p.fxb, d1);
   if (!pv0) zz.x = __int_as_float(0x7fc00000);
   if (!pv1) zz.y = __int_as_float(0x7fc00000);
   const float2 px = __fmul2_rn(__fmul2_rn(du, zz), make_float2(p.inv_fx_f, p.inv_fx_f));
@@ -319,12 +330,20 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
     if constexpr (kInt) return __ddiv_rn((double)u, p.png_scale);
     else return u;
   };
-  if (ok0 && !in0)
-    normal_from_moments(dsum(U0), dsum(V0), p.alpha, (double)d0, (double)du.x, (double)dv, p.fx,
-                        p.fy, o[3], o[4], o[5]);
-  if (ok1 && !in1)
-    normal_from_moments(dsum(U1), dsum(V1), p.alpha, (double)d1, (double)du.y, (double)dv, p.fx,
-                        p.fy, o[9], o[10], o[11]);
+  if (ok0 && !in0) {
+    const float3 n = normal_rare(dsum(U0), dsum(V0), p.alpha, (double)d0, (double)du.x,
+                                 (double)dv, p.fx, p.fy);
+    o[3] = n.x;
+    o[4] = n.y;
+    o[5] = n.z;
+  }
+  if (ok1 && !in1) {
+    const float3 n = normal_rare(dsum(U1), dsum(V1), p.alpha, (double)d1, (double)du.y,
+                                 (double)dv, p.fx, p.fy);
+    o[9] = n.x;
+    o[10] = n.y;
+    o[11] = n.z;
+  }
 }
 
 // ---------------------------------------------------------------------------
