@@ -525,13 +525,18 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
         cr[g] = make_pair(C, Rr);
       }
     } else {
-#pragma unroll
+      // rare (fp inputs, a sample above 2^40): direct sums per output row,
+      // re-read from the tile (non-finite samples as 0) in a rolled loop to
+      // keep the kernel's code small
+#pragma unroll 1
       for (int g = 0; g < HG; ++g) {
         A C = 0, Rr = 0;
 #pragma unroll
         for (int j = 0; j < NWIN; ++j) {
-          C += v[g + j];
-          Rr = mac((A)(j - R), v[g + j], Rr);
+          A x = sval(col[(g + j) * BW], p);
+          if constexpr (!kIntAcc<T>) x = finite_d(x) ? x : 0.0;
+          C += x;
+          Rr = mac((A)(j - R), x, Rr);
         }
         cr[g] = make_pair(C, Rr);
       }
@@ -689,10 +694,12 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
         const double du = (double)(xb + j + e) - p.u0;
         float* r = o + 6 * e;
         point_from_disparity_f64(dcv, du, dv, p, r[0], r[1], r[2]);
-        if (e ? ok1 : ok0)
-          normal_from_moments(Us[j + e], Vs[j + e], p.alpha, dcv, du, dv, p.fx, p.fy, r[3], r[4],
-                              r[5]);
-        else
+        if (e ? ok1 : ok0) {
+          const float3 n = normal_rare(Us[j + e], Vs[j + e], p.alpha, dcv, du, dv, p.fx, p.fy);
+          r[3] = n.x;
+          r[4] = n.y;
+          r[5] = n.z;
+        } else
           r[3] = r[4] = r[5] = __int_as_float(0x7fc00000);
       }
     }
