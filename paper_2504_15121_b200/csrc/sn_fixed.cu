@@ -26,10 +26,13 @@
 //
 // Data movement (B200): the input tile + halo is one 3D TMA load
 // (cp.async.bulk.tensor) per item, prefetched while the previous item's
-// pass H runs; the AoS-6 output tile is
-// staged in 128B-swizzled shared memory (conflict-free float4 writes from
-// lanes that own different rows) and leaves as 24 TMA stores per item, so
-// HBM sees full-line writes only.  Persistent grid, two CTAs per SM.
+// pass H runs; the AoS-6 output tile is staged in row-major shared memory
+// (pitch 3072 + 16 B: conflict-free float4 writes from lanes that own
+// different rows) and leaves as one contiguous 3 KB bulk copy
+// (cp.async.bulk) per output row, 16 per item, so HBM sees full-line writes
+// only.  Persistent grid, two CTAs per SM.  (The warp-specialised pipe
+// kernel keeps the earlier layout: 24 TMA tensor stores of 128B-swizzled
+// boxes.)
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -360,7 +363,8 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
 //           ballot per row.
 //   pass H  8 warps, lane <-> (output row, run of 8 columns): U, V as a
 //           sliding chain, closed-form normal + point (packed f32x2), 6 floats
-//           per pixel into the 128B-swizzled staging tile, TMA stores.
+//           per pixel into the staging tile, bulk row stores (the pipe
+//           kernel: 128B-swizzled boxes, TMA tensor stores).
 // Two kernels share the passes: fixed_square_kernel (2 CTAs/SM, passes
 // separated by CTA barriers, any R <= 8, fp32/fp64) and
 // fixed_square_pipe_kernel (1 CTA/SM, warp-specialised: pass V of item i+1,
@@ -739,8 +743,9 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   constexpr int NC = Cfg::NC, AE = Cfg::AE;
   constexpr int kStoreLanes = SN_ROWBULK ? kG : kBoxes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B aligned base for the swizzled staging tile; offset arithmetic on the
-  // __shared__ array keeps the shared address space (LDS/STS, not generic LD/ST)
+  // aligned base (128 B for the row staging, 1024 B for swizzled boxes); offset
+  // arithmetic on the __shared__ array keeps the shared address space (LDS/STS,
+  // not generic LD/ST)
   constexpr uint32_t kAlign = SN_ROWBULK ? 128u : 1024u;
   uint8_t* smem = smem_raw + ((kAlign - (smem_u32(smem_raw) & (kAlign - 1u))) & (kAlign - 1u));
   AccPair<T>* CR = reinterpret_cast<AccPair<T>*>(smem + Cfg::CS);
@@ -787,7 +792,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     // 1 no stores, 2 no pass H, 3 no pass V, 4 neither pass, 5 stores only
     // (no loads, no passes), 6 loads only
     if (SN_EXP != 3 && SN_EXP < 4) pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
-    // staging of the previous item consumed by its TMA stores (issued by warp 8)
+    // staging of the previous item read out by its bulk stores (issued by warp 8)
     if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) bulk_wait_read0();
     __syncthreads();
 
