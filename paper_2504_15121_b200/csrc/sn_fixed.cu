@@ -166,6 +166,14 @@ __device__ __forceinline__ double dval<Png16>(Png16 x, const FixedParams& p) {
 // (AccOf: the accumulator types, defined above FastCfg)
 
 __device__ __forceinline__ double2 make_pair(double a, double b) { return make_double2(a, b); }
+// pairwise (tree) sum of N values: every partial sum here is exact (see the
+// file header), so the association does not change the result -- only the
+// length of the dependent chain (log2 N instead of N)
+template <int N, typename A>
+__device__ __forceinline__ A tree_sum(const A* x) {
+  if constexpr (N == 1) return x[0];
+  else return tree_sum<N / 2>(x) + tree_sum<N - N / 2>(x + N / 2);
+}
 __device__ __forceinline__ int2 make_pair(int a, int b) { return make_int2(a, b); }
 // a + w * x: one FMA in fp64 (exact here), one IMAD in int32
 __device__ __forceinline__ double mac(double w, double x, double a) { return fma(w, x, a); }
@@ -513,12 +521,12 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
     const uint32_t invb = ~(fin & inside);
     AccPair<T>* cr = CR + c * kCP + r0;
     if (!big) {
-      A C = 0, Rr = 0;
+      // first window as trees (exact sums: any association gives the same)
+      A C = tree_sum<NWIN>(v);
+      A wd[R];
 #pragma unroll
-      for (int j = 0; j < NWIN; ++j) {
-        C += v[j];
-        Rr = mac((A)(j - R), v[j], Rr);
-      }
+      for (int k = 1; k <= R; ++k) wd[k - 1] = (A)k * (v[R + k] - v[R - k]);
+      A Rr = tree_sum<R>(wd);
       cr[0] = make_pair(C, Rr);
 #pragma unroll
       for (int g = 1; g < HG; ++g) {
@@ -631,13 +639,12 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   // sliding sums first (short dependent chain), then independent epilogues
   A Us[kRun], Vs[kRun];
   if (!big) {
-    A Bx = 0, U = 0, V = 0;
+    // first window as trees: U = sum_k k (c[R+k] - c[R-k])
+    A Bx = tree_sum<NWIN>(cc), V = tree_sum<NWIN>(rr);
+    A wd[R];
 #pragma unroll
-    for (int j = 0; j < NWIN; ++j) {
-      Bx += cc[j];
-      U = mac((A)(j - R), cc[j], U);
-      V += rr[j];
-    }
+    for (int k = 1; k <= R; ++k) wd[k - 1] = (A)k * (cc[R + k] - cc[R - k]);
+    A U = tree_sum<R>(wd);
     Us[0] = U;
     Vs[0] = V;
 #pragma unroll
