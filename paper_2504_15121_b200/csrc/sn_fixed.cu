@@ -295,12 +295,14 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
   // passable predicate); duh = (x - u0_hi) exactly, du = duh - u0_lo
   const float2 dd = make_float2(dn0, dn1);
   const float2 du = make_float2(duh - p.u0_lo, (duh + 1.0f) - p.u0_lo);
-  const bool pv0 = (d0 > 0.0f) && (d0 <= 3.402823466e38f);
-  const bool pv1 = (d1 > 0.0f) && (d1 <= 3.402823466e38f);
-  if (pv0 && d0 < 1.175494351e-38f) zz.x = depth_rare(p.fxb, d0);
-  if (pv1 && d1 < 1.175494351e-38f) zz.y = depth_rare(p.fxb, d1);
-  if (!pv0) zz.x = __int_as_float(0x7fc00000);
-  if (!pv1) zz.y = __int_as_float(0x7fc00000);
+  // zz is finite and > 0 exactly when d is a normal positive disparity whose
+  // reciprocal does not flush; anything else -- d invalid (NaN, <= 0, +inf:
+  // the point is NaN), subnormal, or so large or small that rcp or the
+  // product leaves the normal range -- takes the rare path
+  if (!(zz.x > 0.0f && zz.x < 3.402823466e38f))
+    zz.x = (d0 > 0.0f && d0 <= 3.402823466e38f) ? depth_rare(p.fxb, d0) : __int_as_float(0x7fc00000);
+  if (!(zz.y > 0.0f && zz.y < 3.402823466e38f))
+    zz.y = (d1 > 0.0f && d1 <= 3.402823466e38f) ? depth_rare(p.fxb, d1) : __int_as_float(0x7fc00000);
   const float2 px = __fmul2_rn(__fmul2_rn(du, zz), make_float2(p.inv_fx_f, p.inv_fx_f));
   // dv / fy is a per-row constant (hoisted out of the run): one product per pixel
   const float dvy = dv * p.inv_fy_f;
