@@ -337,6 +337,12 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
   o[9] = nx.y;
   o[10] = ny.y;
   o[11] = nz.y;
+  // both |n|^2 in fp32's comfortable range (NaN-propagating min/max: a NaN
+  // fails the test) -- else the per-pixel checks below
+  float smin, smax;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(smin) : "f"(s.x), "f"(s.y));
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(smax) : "f"(s.x), "f"(s.y));
+  if (smin > 1e-30f && smax < 1e30f) return;
   const bool in0 = s.x > 1e-30f && s.x < 1e30f, in1 = s.y > 1e-30f && s.y < 1e30f;
   // the rare fp64 path works on the disparity sums: integer sums / scale
   auto dsum = [&](A u) -> double {
