@@ -294,7 +294,8 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
   // points; zz = fxb_f * rcp(d) as computed by the caller (shared with the
   // passable predicate); duh = (x - u0_hi) exactly, du = duh - u0_lo
   const float2 dd = make_float2(dn0, dn1);
-  const float2 du = make_float2(duh - p.u0_lo, (duh + 1.0f) - p.u0_lo);
+  // (duh, duh + 1) exactly, then one packed subtraction: the same roundings
+  const float2 du = __fadd2_rn(make_float2(duh, duh + 1.0f), make_float2(-p.u0_lo, -p.u0_lo));
   // zz is finite and > 0 exactly when d is a normal positive disparity whose
   // reciprocal does not flush; anything else -- d invalid (NaN, <= 0, +inf:
   // the point is NaN), subnormal, or so large or small that rcp or the
@@ -642,7 +643,6 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
     return ((c & 4) ? stg_a1 : stg_a0) + (uint32_t)(c >> 3) * (uint32_t)(kG * 128) +
            (((uint32_t)(c & 7) << 4) ^ stg_x);
   };
-  uint32_t validbits = 0;
 
   // sliding sums first (short dependent chain), then independent epilogues
   A Us[kRun], Vs[kRun];
@@ -690,7 +690,6 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   for (int j = 0; j < kRun; j += 2) {
     const bool ok0 = (((win >> j) & 1u) == 0u) && dpos(drow[j], p);
     const bool ok1 = (((win >> (j + 1)) & 1u) == 0u) && dpos(drow[j + 1], p);
-    validbits |= ((ok0 ? 1u : 0u) | (ok1 ? 2u : 0u)) << j;
     // fp64 inputs take the fp32 epilogue too when both centre samples are
     // invalid or within [2^-100, 2^100] (d rounded once to fp32: ~6e-8
     // relative); others -- fp32-subnormal or huge disparities -- the fp64 one
@@ -728,6 +727,11 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
       st_shared_v4(stg_addr((j >> 1) * 3 + t), o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
   }
   if (mask_out != nullptr && yg < H) {
+    // the validity bits, recomputed here so the hot loop does not carry them
+    uint32_t validbits = 0;
+#pragma unroll
+    for (int j = 0; j < kRun; ++j)
+      validbits |= ((((win >> j) & 1u) == 0u && dpos(drow[j], p)) ? 1u : 0u) << j;
     uint8_t* mrow = mask_out + ((int64_t)bz * H + yg) * W + xb;
     if (xb + kRun <= W && (reinterpret_cast<uintptr_t>(mrow) & 7u) == 0) {
       // one 8-byte store: bit j -> byte j
