@@ -1,22 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the B200 hot path (BASELINE.json metric).
 
-Workload (default, N=1 and per rank for N>1): configuration C3 -- synthetic
+Headline workload (N=1, and per rank for N>1): configuration C3 -- synthetic
 2048x1024 street-scene disparities, 256 frames per GPU (weak scaling: each
-rank owns its own 256-frame shard, no data-path collective).  One step =
-the full north-star pipeline over the batch: fused fixed-kernel pass
-(k = 9 LSQ fit + closed-form normal + triangulation -> dense [B,H,W,6] fp32
-oriented points), the ST-passable bit mask (t = 0.2) and the 8-connected
-component labels from it.  Inputs are resident in HBM; they are 2.1 GB in / 12.9 GB out per
-step, far larger than the 126 MB L2, so no explicit flush is needed.
+rank owns its own 256-frame shard, no data-path collective).  One step = the
+full north-star pipeline over the batch: fused fixed-kernel pass (k = 9 LSQ
+fit + closed-form normal + triangulation -> dense [B,H,W,6] fp32 oriented
+points), the ST-passable bit mask (t = 0.2) and the 8-connected component
+labels from it.  Inputs are resident in HBM; 2.1 GB in / 12.9 GB out per
+step, far larger than the 126 MB L2, so no flush is needed between steps.
 
 Reported: value = whole-job Mpx/s (all ranks) from CUDA events on the launch
 stream, max over ranks; roofline of the dominant kernel (the fused pass) from
 its own CUDA-event time inside the timed region; e2e through the C-ABI
-host-buffer entry (pinned host in/out, copies inside the timed region);
-cpu_baseline = the oracle port (reference algorithm) on a bounded sample.
+host-buffer entry (pinned host in/out, copies inside the timed region) with
+its own PCIe roofline; cpu_baseline = the reference package itself
+(baseline/_ref, installed by tools/install_reference.sh) on a bounded sample,
+else the oracle port.  After the headline, the other named configs are
+measured briefly (`configs`): C2 (2888x1920 sphere, L2 flushed between
+repetitions), C4 (64 noisy frames with holes at t = 0.05 / 0.2 / 1.0) and C5
+(7680x4320 in one strip per rank: halo exchange, strip pass, NCCL seam
+all-gather and relabel inside the timed region).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+With --gpus N > 1 and no torchrun environment the script re-launches itself
+under torch.distributed.run with N ranks (one per GPU).
 """
 
 from __future__ import annotations
@@ -26,6 +35,7 @@ import ctypes
 import json
 import os
 import shutil
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,10 +47,13 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+REF_PATH = ROOT / "baseline" / "_ref"
 
 METRIC = "megapixels/sec (oriented points) at 2048×1024, 1/2/4/8 B200; % HBM roofline"
 H, W, FRAMES, KSIZE, T_ST = 1024, 2048, 256, 9, 0.2
 BYTES_PER_PX = 28  # algorithmic: 4 B fp32 disparity in + 24 B (x,y,z,nx,ny,nz) out
+WORKLOAD = "C3 2048x1024 street, fixed 9x9 pass + ST(t=0.2) component labels"
+IO = "fp32 disparity in, fp32 AoS-6 record out; exact fp64 sums, fp32 epilogue"
 
 
 def parse():
@@ -57,10 +70,13 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=16, help="cpu_baseline sample (frames)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2/C4/C5 legs")
     ap.add_argument("--extras", action="store_true",
                     help="also time the next-row kernels (adaptive, cloud, evaluation, PNG16 "
                          "input) briefly after the headline measurement")
     ap.add_argument("--no-extras", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="rank plumbing only (gloo on CPU, no GPU work): prints the ranks seen")
     return ap.parse_args()
 
 
@@ -71,6 +87,28 @@ def dist_env():
     return rank, world, local
 
 
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 without a torchrun environment: start N ranks on this node
+    (the driver's own launch line, 127.0.0.1 rendezvous)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def street_clean():
     from paper_2504_15121_b200 import scenes
     sc = scenes.street_scene(W, H)
@@ -79,28 +117,55 @@ def street_clean():
 
 
 # ---------------------------------------------------------------------------
-# CPU legs (oracle port of the reference algorithm; bench-only use)
+# CPU legs: the reference package itself (baseline/_ref) when installed, else
+# the oracle port of its algorithm -- bench-only use
+
+
+def reference_step_fn(rig, threads):
+    """(kind, fn(d) -> None) running the reference's hot path on one float64
+    frame: estimate_normals_fixed through its own bench closure
+    (bench.py:61-73 make_bench_callable 'affine-fixed', prebuilt kernels),
+    triangulate_grid, and the ST passable set depth_laplacian(depth_field)
+    <= t labelled 8-connected (scipy.ndimage.label + min-index relabel, as the
+    oracle: the reference has no labeller)."""
+    from oracle import stereonorm_oracle as orc
+    if (REF_PATH / "stereonorm").exists():
+        sys.path.insert(0, str(REF_PATH))
+        try:
+            import stereonorm as sn
+        finally:
+            sys.path.remove(str(REF_PATH))
+        rrig = sn.StereoRig(rig.fx, rig.fy, rig.u0, rig.v0, rig.baseline)
+
+        def fn(d):
+            field = sn.ScalarField.from_array(d)
+            sn.bench.make_bench_callable("affine-fixed", field, rrig, KSIZE, threads=threads)()
+            sn.triangulate_grid(field, rrig)
+            e = sn.depth_laplacian(sn.depth_field(field, rrig))
+            with np.errstate(invalid="ignore"):
+                orc.label_components(e.mask & (e.values <= T_ST))
+        return "reference", fn
+    orig = orc.Rig(rig.fx, rig.fy, rig.u0, rig.v0, rig.baseline)
+
+    def fn(d):
+        orc.oriented_points(d, orig, KSIZE, threads=threads)
+        orc.ccl_labels(d, orig, T_ST)
+    return "port", fn
 
 
 def cpu_sample(rig, clean, n_frames, threads):
-    """Time the reference algorithm (oracle port) over n_frames C3 frames with
-    the reference's own method (bench.py:38-52: 1 warm-up, perf_counter)."""
-    from oracle import stereonorm_oracle as orc
+    """Time the reference algorithm over n_frames C3 frames with the
+    reference's own method (bench.py:38-52: 1 warm-up, perf_counter)."""
     from paper_2504_15121_b200 import scenes
-    orig = orc.Rig(rig.fx, rig.fy, rig.u0, rig.v0, rig.baseline)
+    kind, fn = reference_step_fn(rig, threads)
     frames = [scenes.add_gaussian_noise(clean, 0.2, i).astype(np.float32).astype(np.float64)
               for i in range(n_frames + 1)]
-
-    def one(d):
-        orc.oriented_points(d, orig, KSIZE, threads=threads)
-        orc.ccl_labels(d, orig, T_ST)
-
-    one(frames[0])  # warm-up
+    fn(frames[0])  # warm-up
     t0 = time.perf_counter()
     for d in frames[1:]:
-        one(d)
+        fn(d)
     dt = time.perf_counter() - t0
-    return n_frames * H * W / 1e6 / dt, dt
+    return kind, n_frames * H * W / 1e6 / dt, dt
 
 
 def run_reference(args):
@@ -110,16 +175,14 @@ def run_reference(args):
     rig, clean = street_clean()
     threads = os.cpu_count() or 1
     per_step = 2  # bounded sample per step (frames)
-    from oracle import stereonorm_oracle as orc
     from paper_2504_15121_b200 import scenes
-    orig = orc.Rig(rig.fx, rig.fy, rig.u0, rig.v0, rig.baseline)
+    kind, fn = reference_step_fn(rig, threads)
     frames = [scenes.add_gaussian_noise(clean, 0.2, i).astype(np.float32).astype(np.float64)
               for i in range(per_step)]
 
     def step():
         for d in frames:
-            orc.oriented_points(d, orig, KSIZE, threads=threads)
-            orc.ccl_labels(d, orig, T_ST)
+            fn(d)
 
     for _ in range(args.warmup):
         step()
@@ -130,16 +193,20 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     sec = sum(times) / len(times)
     val = per_step * H * W / 1e6 / sec
+    what = ("the reference package (baseline/_ref stereonorm 0.1.0): estimate_normals_fixed "
+            "via its bench closure + triangulate_grid + depth_laplacian(depth_field) <= t, "
+            "scipy 8-connected labels" if kind == "reference" else
+            "oracle port of estimate_normals_fixed + triangulate_grid + ST labels")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "Mpx/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (C3 street scene, PCG64 noise sigma 0.2)",
-        "config": {"workload": "C3 2048x1024 street, k=9 fixed pass + ST(t=0.2) labels",
-                   "frames_per_step": per_step, "height": H, "width": W},
-        "cpu_baseline": {"value": val, "unit": "Mpx/s", "cores": threads, "kind": "port",
-                         "sample": f"{per_step} frames/step x {args.steps} steps, oracle port of "
-                                   "estimate_normals_fixed + triangulate_grid + labels"},
+        "data": "synthetic (C3 street scene, PCG64 noise sigma 0.2, fp32-representable values)",
+        "config": {"workload": WORKLOAD, "height": H, "width": W, "kernel": KSIZE},
+        "cpu_baseline": {"value": val, "unit": "Mpx/s", "cores": threads, "kind": kind,
+                         "cpu_model": cpu_model(),
+                         "sample": f"{per_step} C3 frames/step x {args.steps} steps, {what}, "
+                                   f"threads={threads}"},
         "e2e": {"value": val, "unit": "Mpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -212,6 +279,43 @@ def measured_hbm_peak() -> float:
     return float(peaks.get("hbm_gbs", 6650.0))
 
 
+def pcie_peaks(dev, nbytes=1 << 30):
+    """Pinned host<->device copy bandwidth (GB/s): one large cudaMemcpyAsync
+    per direction, best of 3, CUDA events -- the ceiling of the e2e leg."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    res = {}
+    for name, (dst, src) in (("h2d_gbs", (d, h)), ("d2h_gbs", (h, d))):
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        res[name] = round(best, 2)
+    # both directions at once (the e2e leg overlaps them on two streams)
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(s1):
+        d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(s2):
+        h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    res["duplex_gbs"] = round(2 * nbytes / (time.perf_counter() - t0) / 1e9, 2)
+    del h, d, h2, d2
+    return res
+
+
+def flush_l2(buf):
+    buf.add_(1)  # 256 MB read+write: evicts the 126 MB L2
+
+
 def next_row_timings(dN, outN, rig, dev):
     """us/frame of the f1-f4 kernels (CUDA events, 3 reps after one untimed
     call): the adaptive walks on 8 C3 frames, the streaming rows (PNG16 fused
@@ -246,6 +350,8 @@ def next_row_timings(dN, outN, rig, dev):
         "adaptive_st_s10_d8": timed(lambda: device.adaptive_points(d8, rig, st, out=out8), 8),
         "fused_pass_png16_input": timed(lambda: device.oriented_points_png16(
             raw, rig, KSIZE, scale=256.0, out=outN), n),
+        "fused_pass_fp64_input": timed(lambda: device.oriented_points(
+            dN.double(), rig, KSIZE, out=outN), n),
     }
     # the fixed-pass records + mask the cloud and the evaluation consume
     device.oriented_points(dN, rig, KSIZE, out=outN, mask=mask)
@@ -291,16 +397,151 @@ def next_row_cpu(d, gt_n, gt_m, rig):
     return res
 
 
+def other_configs(dev, rank, world, disp_buf, out_buf, lab_buf, ws, bits_buf):
+    """C2 / C4 / C5 (BASELINE.json configs 1, 3, 4), CUDA events on the launch
+    stream, a few repetitions each after one untimed call.  C4 reuses the C3
+    buffers (same frame shape); C2 flushes L2 between repetitions (its 155 MB
+    step is about the L2 size); C5 runs one strip per rank (world strips)."""
+    import torch
+    import torch.distributed as dist
+    from scipy import ndimage
+    from paper_2504_15121_b200 import device, scenes
+    from paper_2504_15121_b200.parallel import StripPlan, distributed_strip_frame, \
+        local_strip_frame
+    stream = torch.cuda.current_stream(dev)
+    res = {}
+
+    def ev_time(fn, reps, flush=None):
+        tot = 0.0
+        for _ in range(reps):
+            if flush is not None:
+                flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        return tot / reps
+
+    # C2: 2888x1920 sphere, one frame, full pipeline; L2 flushed before each rep
+    sp = scenes.sphere_scene(2888, 1920)
+    d2 = torch.from_numpy(scenes.add_gaussian_noise(scenes.raycast(sp)[0], 0.2, 7)
+                          .astype(np.float32)).to(dev)[None]
+    o2 = torch.empty((1, 1920, 2888, 6), dtype=torch.float32, device=dev)
+    l2 = torch.empty((1, 1920, 2888), dtype=torch.int32, device=dev)
+    ws2 = device.ccl_workspace(1, 1920, 2888, dev)
+    scratch = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    fn2 = lambda: device.pipeline(d2, sp.rig, KSIZE, T_ST, out=o2, labels=l2, workspace=ws2)  # noqa
+    fn2()
+    ms2 = ev_time(fn2, 10, lambda: flush_l2(scratch))
+    ms2p = ev_time(lambda: device.oriented_points(d2, sp.rig, KSIZE, out=o2), 10,
+                   lambda: flush_l2(scratch))
+    px2 = 2888 * 1920
+    res["C2"] = {"workload": "2888x1920 sphere (sigma 0.2), 1 frame, fixed 9x9 + ST(0.2) labels",
+                 "ms_per_frame": ms2, "value_mpx_s": px2 / 1e3 / ms2,
+                 "fused_pass_ms": ms2p,
+                 "fused_pass_frac_hbm": BYTES_PER_PX * px2 / (ms2p * 1e-3) / 1e9 /
+                 measured_hbm_peak(),
+                 "l2": "flushed (256 MB write) before each of 10 repetitions"}
+    del d2, o2, l2, ws2
+
+    # C4: 64 frames, sigma 1.0 + dilated holes (SURVEY.md §8(d)), t = 0.05/0.2/1.0
+    sc = scenes.street_scene(W, H)
+    clean = scenes.raycast(sc)[0]
+    n4 = min(64, disp_buf.shape[0])
+    d4 = disp_buf[:n4]
+    for i in range(n4):
+        d = scenes.add_gaussian_noise(clean, 1.0, 4000 + i)
+        holes = ndimage.binary_dilation(np.random.default_rng(1000 + i).random(d.shape) < 0.002,
+                                        iterations=3)
+        d4[i] = torch.from_numpy(np.where(holes, np.nan, d).astype(np.float32)).to(dev)
+    c4 = {"workload": f"C4 2048x1024 street sigma 1.0 + 4.9% dilated holes, {n4} frames"}
+    for t in (0.05, 0.2, 1.0):
+        fb = lambda: device.passable_bits(d4, sc.rig, t, bits=bits_buf[:n4])  # noqa: E731
+        fl = lambda: device.labels_from_bits(bits_buf[:n4], W, out=lab_buf[:n4],  # noqa: E731
+                                             workspace=ws)
+        fb(), fl()
+        ms_b = ev_time(fb, 3)
+        ms_l = ev_time(fl, 3)
+        ncomp = int(torch.unique(lab_buf[0]).numel() - 1)
+        c4[f"t={t}"] = {"bits_us_per_frame": ms_b * 1e3 / n4, "ccl_us_per_frame": ms_l * 1e3 / n4,
+                        "components_frame0": ncomp}
+    fp = lambda: device.pipeline(d4, sc.rig, KSIZE, T_ST, out=out_buf[:n4],  # noqa: E731
+                                 labels=lab_buf[:n4], workspace=ws)
+    fp()
+    ms4 = ev_time(fp, 3)
+    c4["pipeline_t0.2_us_per_frame"] = ms4 * 1e3 / n4
+    c4["value_mpx_s"] = n4 * H * W / 1e3 / ms4
+    res["C4"] = c4
+
+    # C5: 7680x4320, one strip per rank (world strips): halo exchange, strip
+    # pass, seam all-gather + relabel -- all inside the timed region
+    sc5 = scenes.street_scene(7680, 4320)
+    H5, W5 = 4320, 7680
+    plan = StripPlan.for_kernel(H5, W5, world, KSIZE)
+    r0, r1 = plan.owned(rank)
+    full = scenes.add_gaussian_noise(scenes.raycast(sc5)[0], 0.2, 0).astype(np.float32)
+    owned = torch.from_numpy(full[r0:r1]).to(dev)
+    if world > 1:
+        run5 = lambda: distributed_strip_frame(owned, plan, sc5.rig, KSIZE, T_ST)  # noqa: E731
+    else:
+        dfull = torch.from_numpy(full).to(dev)
+        run5 = lambda: local_strip_frame(dfull, StripPlan.for_kernel(H5, W5, 8, KSIZE),  # noqa
+                                         sc5.rig, KSIZE, T_ST)
+    run5()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms5 = ev_time(run5, 3)
+    if world > 1:
+        t5 = torch.tensor([ms5], dtype=torch.float64, device=dev)
+        dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+        ms5 = float(t5.item())
+    res["C5"] = {"workload": f"7680x4320 street, 1 frame, {max(world, 8) if world == 1 else world} "
+                             "strips (" + ("one per rank, NCCL halo P2P + seam all-gather"
+                                           if world > 1 else "8 strips in sequence on 1 GPU, "
+                                           "host seam merge") + ")",
+                 "ms_per_frame": ms5, "value_mpx_s": H5 * W5 / 1e3 / ms5, "ranks": world}
+    return res
+
+
+def dry_run(args):
+    """Rank plumbing without a GPU: gloo all-reduce of ones over the ranks."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.ones(1)
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": int(t.item()),
+                          "gpus_arg": args.gpus}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        if rank == 0:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.dry_run:
+        dry_run(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
     import torch
     import torch.distributed as dist
-    from paper_2504_15121_b200 import _native, device, scenes
+    from paper_2504_15121_b200 import _native, device
 
-    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -429,13 +670,25 @@ def main():
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         sec = float(e2e_s.item())
         px_e2e = Be * H * W
+        h2d_b = int(px_e2e * 4)
+        d2h_b = int(px_e2e * (24 + (4 if full else 0)))
+        pcie = pcie_peaks(dev)
+        # PCIe bound of one step: both directions run concurrently on the
+        # plan's copy streams, so the slower direction bounds the step
+        bound_s = max(h2d_b / (pcie["h2d_gbs"] * 1e9), d2h_b / (pcie["d2h_gbs"] * 1e9))
         e2e = {"value": world * px_e2e / 1e6 / sec, "unit": "Mpx/s",
                "frames_per_step_per_rank": Be,
-               "h2d_bytes_per_step": int(px_e2e * 4),
-               "d2h_bytes_per_step": int(px_e2e * (24 + (4 if full else 0))),
+               "frames_per_sec_per_gpu": Be / sec,
+               "h2d_bytes_per_step": h2d_b,
+               "d2h_bytes_per_step": d2h_b,
                "ms_per_step": sec * 1e3,
+               "pcie_gbs": pcie,
+               "bound_ms_per_step": bound_s * 1e3,
+               "frac": bound_s / sec,
+               "bound": "pcie (max of H2D bytes / pinned H2D peak, D2H bytes / pinned D2H peak)",
                "path": ("sn_pipeline_host" if full else "sn_oriented_points_host") +
                        " (pinned host in/out, 3-stream H2D/compute/D2H overlap)"}
+        del host_in, host_out, host_lab
 
     # next rows of the scope table, timed briefly on 8 of the
     # same frames after the headline measurement: evidence, not the metric
@@ -448,26 +701,38 @@ def main():
         except Exception as exc:  # never let an extra cost the headline line
             extras = {"error": f"{type(exc).__name__}: {exc}"}
 
+    configs = None
+    if not args.no_configs:
+        try:
+            configs = other_configs(dev, rank, world, disp, out, labels, ccl_ws, bits)
+        except Exception as exc:  # never let a side leg cost the headline line
+            configs = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        val, dt = cpu_sample(rig, clean, args.cpu_frames, threads)
-        cpu = {"value": val, "unit": "Mpx/s", "cores": threads, "kind": "port",
-               "sample": f"{args.cpu_frames} C3 frames ({dt:.1f} s wall), oracle port of "
-                         "estimate_normals_fixed + triangulate_grid + ST labels, "
-                         f"threads={threads}"}
+        kind, val, dt = cpu_sample(rig, clean, args.cpu_frames, threads)
+        _, val1, dt1 = cpu_sample(rig, clean, 2, 1)
+        cpu = {"value": val, "unit": "Mpx/s", "cores": threads, "kind": kind,
+               "cpu_model": cpu_model(),
+               "value_threads1": val1,
+               "sample": f"{args.cpu_frames} C3 frames ({dt:.1f} s wall) at threads={threads}; "
+                         f"2 frames ({dt1:.1f} s) at threads=1; " +
+                         ("the reference package itself (baseline/_ref stereonorm 0.1.0: "
+                          "estimate_normals_fixed + triangulate_grid + depth_laplacian "
+                          "predicate) + scipy 8-connected labels" if kind == "reference" else
+                          "oracle port of estimate_normals_fixed + triangulate_grid + ST labels")}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Mpx/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
             "data": "synthetic: raycast street scene (SURVEY.md C3) + device N(0,0.2) noise",
-            "config": {"workload": "C3 2048x1024 street, 256 frames/GPU, fixed 9x9 pass + "
-                                   "ST(t=0.2) component labels" if args.pipeline == "full" else
-                                   "C3 2048x1024 street, 256 frames/GPU, fixed 9x9 pass",
-                       "frames_per_gpu": B, "height": H, "width": W, "kernel": KSIZE,
-                       "io": "fp32 disparity in, fp32 AoS-6 record out, fp64 accumulation",
+            "config": {"workload": WORKLOAD if args.pipeline == "full" else
+                       "C3 2048x1024 street, fixed 9x9 pass",
+                       "height": H, "width": W, "kernel": KSIZE,
+                       "frames_per_gpu": B, "io": IO,
                        "parallelism": f"frame-batch dp{world}",
                        "l2": "inputs+outputs (15 GB/step) >> 126 MB L2, no flush needed"},
             "frames_per_sec_per_gpu": B / (ms_per_step / 1e3),
@@ -480,6 +745,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback"},
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "configs": configs,
             "next_rows_us_per_frame": extras,
             "next_rows_roofline": extras_roof,
             "next_rows_cpu_us_per_frame": extras_cpu,

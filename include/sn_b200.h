@@ -23,6 +23,12 @@
  *                             the ST-passable set, canonical min raster index
  *   sn_kernel_moments         build_kernels             kernels.py:78-103
  *
+ * Every entry point that reads disparities has an fp32 form and an _f64 form.
+ * The _f64 forms take the reference's own float64 values (ScalarField,
+ * fields.py:37-40) unrounded: masks, passable sets, labels and star-fill
+ * supports are then bit-exact with the reference on its inputs (no fp32 cast
+ * anywhere on the decision paths).
+ *
  * Layouts: disparity [B][H][W] row-major (fp32 or fp64, NaN/+-inf = invalid),
  * out6 [B][H][W][6] fp32 = (x, y, z, nx, ny, nz) -- the PLY vertex record
  * (formats.py:167-183) -- with NaN normals where the normal is invalid and
@@ -69,10 +75,13 @@ typedef struct sn_plan sn_plan_t;
 SN_API int sn_abi_version(void);
 SN_API const char* sn_last_error(void);
 
-/* A plan binds a device and owns the host-path workspace (pinned staging,
- * device buffers, copy/compute streams).  Device entry points only use it
- * for the device id and cached properties and are safe to call concurrently
- * on distinct streams. */
+/* A plan binds a device and owns the host-path workspace (copy/compute
+ * streams, double-buffered device chunks, and pinned host staging used when a
+ * caller's host buffers are pageable).  Device entry points only use the plan
+ * for the device id and cached properties (their scratch comes from the
+ * caller's workspace or from stream-ordered allocations on the caller's
+ * stream) and are safe to call concurrently on distinct streams; *_host
+ * calls on one plan are serialised by the plan's lock. */
 SN_API int sn_plan_create(int device, sn_plan_t** plan);
 SN_API int sn_plan_destroy(sn_plan_t* plan);
 
@@ -98,6 +107,10 @@ SN_API int sn_oriented_points_rows(sn_plan_t* plan, const float* disp, int64_t B
                             int64_t W, int64_t row0, const sn_rig_t* rig,
                             const int32_t* offsets_xy, int32_t n_off, float* out6,
                             uint8_t* mask, void* stream);
+SN_API int sn_oriented_points_rows_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                                int64_t W, int64_t row0, const sn_rig_t* rig,
+                                const int32_t* offsets_xy, int32_t n_off, float* out6,
+                                uint8_t* mask, void* stream);
 
 /* Same pass + the ST-passable bit mask (adaptive.py:80-97,130-132;
  * threshold t > 0; the fused pass and sn_passable_bits back to back on the
@@ -108,16 +121,25 @@ SN_API int sn_oriented_points_bits(sn_plan_t* plan, const float* disp, int64_t B
                             int64_t W, int64_t row0, const sn_rig_t* rig,
                             const int32_t* offsets_xy, int32_t n_off, double t, float* out6,
                             uint8_t* mask, uint32_t* bits, void* stream);
+SN_API int sn_oriented_points_bits_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                                int64_t W, int64_t row0, const sn_rig_t* rig,
+                                const int32_t* offsets_xy, int32_t n_off, double t, float* out6,
+                                uint8_t* mask, uint32_t* bits, void* stream);
 
 /* The ST-passable bit mask alone (layout of sn_oriented_points_bits), as one
  * streaming kernel over the disparity. */
 SN_API int sn_passable_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                      const sn_rig_t* rig, double t, uint32_t* bits, void* stream);
+SN_API int sn_passable_bits_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                         int64_t W, const sn_rig_t* rig, double t, uint32_t* bits,
+                         void* stream);
 
 /* The whole north-star pipeline in one call: fused fit + normal + point +
  * passable bits, then component labels from the bits (label semantics as
- * sn_ccl_labels with row_base 0).  Device pointers.  The _ws variant takes a
- * caller workspace of sn_ccl_workspace_bytes(B, H, W) bytes. */
+ * sn_ccl_labels with row_base 0).  Device pointers.  The _ws variants take a
+ * caller workspace of sn_ccl_workspace_bytes(B, H, W) bytes; the others take
+ * stream-ordered scratch from the library's private pool on `stream`, so
+ * concurrent calls on different streams never share it. */
 SN_API int sn_pipeline(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                 const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
                 float* out6, uint8_t* mask, int32_t* labels, void* stream);
@@ -125,19 +147,38 @@ SN_API int sn_pipeline_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t
                    const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
                    float* out6, uint8_t* mask, int32_t* labels, void* workspace,
                    size_t ws_bytes, void* stream);
+SN_API int sn_pipeline_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                    const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                    float* out6, uint8_t* mask, int32_t* labels, void* stream);
+SN_API int sn_pipeline_ws_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                       int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
+                       double t, float* out6, uint8_t* mask, int32_t* labels, void* workspace,
+                       size_t ws_bytes, void* stream);
 
-/* Same pass, host buffers: pinned staging + overlapped H2D / compute / D2H,
- * returns when out6 (and mask, if non-NULL) hold the result. */
+/* Same pass, host buffers: chunks of whole frames with H2D / compute / D2H
+ * overlapped on three streams; returns when out6 (and mask, if non-NULL)
+ * hold the result.  Page-locked buffers (cudaHostAlloc / cudaHostRegister /
+ * torch pin_memory) are copied directly; pageable ones are staged through
+ * the plan's pinned slots by multi-threaded host copies.  On an error every
+ * queued copy and kernel is drained before the call returns. */
 SN_API int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
                             int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
                             int32_t n_off, float* out6_host, uint8_t* mask_host);
+SN_API int sn_oriented_points_host_f64(sn_plan_t* plan, const double* disp_host, int64_t B,
+                                int64_t H, int64_t W, const sn_rig_t* rig,
+                                const int32_t* offsets_xy, int32_t n_off, float* out6_host,
+                                uint8_t* mask_host);
 
-/* The whole pipeline on host buffers (pinned for full overlap): points,
- * optional mask, and component labels, chunked with H2D / compute / D2H
- * overlapped; returns when every output is in host memory. */
+/* The whole pipeline on host buffers (staging as sn_oriented_points_host):
+ * points, optional mask, and component labels, chunked with H2D / compute /
+ * D2H overlapped; returns when every output is in host memory. */
 SN_API int sn_pipeline_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
                      int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
                      double t, float* out6_host, uint8_t* mask_host, int32_t* labels_host);
+SN_API int sn_pipeline_host_f64(sn_plan_t* plan, const double* disp_host, int64_t B, int64_t H,
+                         int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
+                         int32_t n_off, double t, float* out6_host, uint8_t* mask_host,
+                         int32_t* labels_host);
 
 /* convolve_affine (gradient convention a1 - 1 = dd/du, a2 = dd/dv); a1/a2 are
  * NaN where mask is 0.  Device pointers, fp64 outputs. */
@@ -154,6 +195,9 @@ SN_API int sn_affine_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t
 SN_API int sn_passable(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                 const sn_rig_t* rig, double t, uint8_t* passable, double* edges,
                 void* stream);
+SN_API int sn_passable_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                    const sn_rig_t* rig, double t, uint8_t* passable, double* edges,
+                    void* stream);
 
 /* 8-connected component labels of the passable set; label = smallest raster
  * index v*W + u + index_base in the component (per frame), -1 elsewhere.
@@ -162,21 +206,27 @@ SN_API int sn_passable(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
 SN_API int sn_ccl_labels(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                   const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
                   void* stream);
+SN_API int sn_ccl_labels_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                      const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                      void* stream);
 
 /* Label an already-computed passable grid (uint8) -- used by strip mode and
  * by tests of the labeller alone. */
 SN_API int sn_ccl_from_passable(sn_plan_t* plan, const uint8_t* passable, int64_t B, int64_t H,
                          int64_t W, int64_t row_base, int32_t* labels, void* stream);
 
-/* The labeller needs a device workspace (passable bit mask + tile seam rows,
- * ~H*W/8 + 8*(H*W/64 + H*W/128) bytes per frame).  The two entry points above
- * use one owned by the plan (grown on demand, so calls sharing a plan must
- * be stream-ordered); the *_ws variants take the caller's, so concurrent
- * streams each pass their own. */
+/* The labeller needs a device workspace (passable bit mask + tile seam rows
+ * + slot labels, sn_ccl_workspace_bytes).  The entry points above take
+ * stream-ordered scratch from the library's private pool on `stream`; the
+ * *_ws variants take the caller's, so concurrent streams each pass their
+ * own. */
 SN_API int sn_ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes);
 SN_API int sn_ccl_labels_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                      const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
                      void* workspace, size_t ws_bytes, void* stream);
+SN_API int sn_ccl_labels_ws_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                         int64_t W, const sn_rig_t* rig, double t, int64_t row_base,
+                         int32_t* labels, void* workspace, size_t ws_bytes, void* stream);
 /* Label from a passable bit mask (layout of sn_oriented_points_bits); the
  * workspace's own bit-mask region is unused. */
 SN_API int sn_ccl_from_bits_ws(sn_plan_t* plan, const uint32_t* bits, int64_t B, int64_t H,
@@ -185,6 +235,34 @@ SN_API int sn_ccl_from_bits_ws(sn_plan_t* plan, const uint32_t* bits, int64_t B,
 SN_API int sn_ccl_from_passable_ws(sn_plan_t* plan, const uint8_t* passable, int64_t B,
                             int64_t H, int64_t W, int64_t row_base, int32_t* labels,
                             void* workspace, size_t ws_bytes, void* stream);
+
+/* Element-wise geometry of the reference's public API, bit-exact fp64
+ * (device pointers, flat arrays of n elements):
+ *   sn_depth_map[_f64]     disparity_to_depth (geometry.py:39-45): z = (fx*b)/d,
+ *                          NaN unless d is finite and > 0 (inf kept).
+ *   sn_triangulate_f64     triangulate (geometry.py:57-64): x = ((u-u0)*z)/fx,
+ *                          y = ((v-v0)*z)/fy, z as above.
+ *   sn_triangulate_grid[_f64]  triangulate_grid (geometry.py:85-89): [B][H][W][3]
+ *                          fp64 points with u = column, v = row -- a points-only
+ *                          pass, no fit.
+ *   sn_depth_laplacian_f64 depth_laplacian (adaptive.py:80-97) of a depth field
+ *                          (values + uint8 mask): edges NaN and ok 0 outside the
+ *                          interior pixels whose five mask entries are set;
+ *                          either output may be NULL. */
+SN_API int sn_depth_map(sn_plan_t* plan, const float* disp, int64_t n, const sn_rig_t* rig,
+                 double* z, void* stream);
+SN_API int sn_depth_map_f64(sn_plan_t* plan, const double* disp, int64_t n, const sn_rig_t* rig,
+                     double* z, void* stream);
+SN_API int sn_triangulate_f64(sn_plan_t* plan, const double* u, const double* v, const double* d,
+                       int64_t n, const sn_rig_t* rig, double* x, double* y, double* z,
+                       void* stream);
+SN_API int sn_triangulate_grid(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
+                        int64_t W, const sn_rig_t* rig, double* xyz, void* stream);
+SN_API int sn_triangulate_grid_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                            int64_t W, const sn_rig_t* rig, double* xyz, void* stream);
+SN_API int sn_depth_laplacian_f64(sn_plan_t* plan, const double* depth, const uint8_t* mask,
+                           int64_t B, int64_t H, int64_t W, double* edges, uint8_t* ok,
+                           void* stream);
 
 /* Strip-seam merge.  HOST memory: `seams` holds, for each
  * of the n_strips strips in row order, its first and last owned label rows
@@ -218,6 +296,11 @@ SN_API int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int
                        const int32_t* ray_xy, int32_t stop, int32_t shared_range,
                        double threshold, float* out6, uint8_t* mask, void* workspace,
                        size_t ws_bytes, void* stream);
+SN_API int sn_adaptive_points_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                           int64_t W, const sn_rig_t* rig, int32_t n_rays,
+                           const int32_t* ray_len, const int32_t* ray_xy, int32_t stop,
+                           int32_t shared_range, double threshold, float* out6, uint8_t* mask,
+                           void* workspace, size_t ws_bytes, void* stream);
 
 /* Accuracy evaluation on the device (evaluation.py:34-73): per frame, the
  * unsigned angle map degrees(arccos(|n_est . n_gt|)) over jointly valid

@@ -16,15 +16,16 @@ tensors, [B, H, W] in, [B, H, W, 6] fp32 out); multi-GPU sharding lives in
 
 from ._native import DegenerateSupportError, NativeLibraryError
 from .components import edge_map, label_components, oriented_point_cloud, passable_set
-from .adaptive import (StarConfig, estimate_affine_adaptive, estimate_normals_adaptive,
-                       ray_offsets, star_trace)
+from .adaptive import (StarConfig, depth_laplacian, estimate_affine_adaptive,
+                       estimate_normals_adaptive, ray_offsets, star_trace)
 from .estimators import (AdaptiveNormalEstimator, AffineNormalEstimator, BaseNormalEstimator,
                          as_rig, as_scalar_field)
 from .evaluation import ErrorStats, angular_error_map, error_stats, summarize
 from .fields import AffineField, NormalField, ScalarField
 from .formats import (FormatError, read_disparity_png16, read_pfm, read_pfm_normals,
                       write_disparity_png16, write_pfm, write_pfm_normals)
-from .geometry import StereoRig, pixel_grid, triangulate_grid
+from .geometry import (StereoRig, depth_field, disparity_to_depth, pixel_grid, triangulate,
+                       triangulate_grid)
 from .kernels import (KernelSpec, PrecomputedKernels, build_kernels, convolve_affine,
                       estimate_affine_direct, estimate_normals_fixed, format_kernel_dump)
 
@@ -32,7 +33,9 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AdaptiveNormalEstimator", "ErrorStats", "angular_error_map", "error_stats", "summarize", "AffineField", "AffineNormalEstimator", "StarConfig",
-    "estimate_affine_adaptive", "estimate_normals_adaptive", "ray_offsets", "star_trace", "BaseNormalEstimator", "DegenerateSupportError",
+    "estimate_affine_adaptive", "estimate_normals_adaptive", "ray_offsets", "star_trace",
+    "depth_laplacian", "depth_field", "disparity_to_depth", "triangulate",
+    "BaseNormalEstimator", "DegenerateSupportError",
     "FormatError", "read_disparity_png16", "read_pfm", "read_pfm_normals",
     "write_disparity_png16", "write_pfm", "write_pfm_normals",
     "KernelSpec", "NativeLibraryError", "NormalField", "PrecomputedKernels", "ScalarField",

@@ -27,5 +27,10 @@ def to_device(values: np.ndarray, dtype=torch.float64) -> torch.Tensor:
     return torch.from_numpy(arr).to(device=current_device(), dtype=dtype, non_blocking=False)
 
 
+def stream_ptr(dev: torch.device):
+    import ctypes
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()

@@ -62,6 +62,19 @@ SIGNATURES = {
     "sn_oriented_points_bits": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P,
                                 _P],
     "sn_passable_bits": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P],
+    "sn_passable_bits_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P],
+    "sn_oriented_points_bits_f64": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P,
+                                    _P, _P],
+    "sn_oriented_points_rows_f64": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
+    "sn_adaptive_points_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _I32, _P, _P, _I32, _I32, _D, _P,
+                               _P, _P, ctypes.c_size_t, _P],
+    "sn_pipeline_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P],
+    "sn_pipeline_ws_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P, _P,
+                           ctypes.c_size_t, _P],
+    "sn_passable_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P, _P],
+    "sn_ccl_labels_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _I64, _P, _P],
+    "sn_ccl_labels_ws_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _I64, _P, _P, ctypes.c_size_t,
+                             _P],
     "sn_adaptive_workspace_bytes": [_I64, _I64, _I64, ctypes.POINTER(ctypes.c_size_t)],
     "sn_adaptive_points": [_P, _P, _I64, _I64, _I64, _RIGP, _I32, _P, _P, _I32, _I32, _D, _P, _P,
                            _P, ctypes.c_size_t, _P],
@@ -84,6 +97,8 @@ SIGNATURES = {
     "sn_ccl_from_bits_ws": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_oriented_points_host": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P],
     "sn_pipeline_host": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P],
+    "sn_pipeline_host_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P],
+    "sn_oriented_points_host_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P],
     "sn_affine": [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P, _P],
     "sn_affine_f64": [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P, _P],
     "sn_passable": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _P, _P, _P],
@@ -93,6 +108,12 @@ SIGNATURES = {
     "sn_ccl_labels_ws": [_P, _P, _I64, _I64, _I64, _RIGP, _D, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_ccl_from_passable_ws": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, ctypes.c_size_t, _P],
     "sn_seam_merge_host": [_P, _I32, _I64, _P, _P, _P],
+    "sn_depth_map": [_P, _P, _I64, _RIGP, _P, _P],
+    "sn_depth_map_f64": [_P, _P, _I64, _RIGP, _P, _P],
+    "sn_triangulate_f64": [_P, _P, _P, _P, _I64, _RIGP, _P, _P, _P, _P],
+    "sn_triangulate_grid": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _P],
+    "sn_triangulate_grid_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _P],
+    "sn_depth_laplacian_f64": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P],
     "sn_relabel": [_P, _P, _I64, _I64, _P, _P, _P, _I32, _P, _P],
 }
 _RESTYPES = {"sn_last_error": ctypes.c_char_p}

@@ -5,9 +5,12 @@ The ray table is computed here exactly as the reference does
 (``ray_offsets``, numpy ``rint`` of ``i * (cos, sin)``, adaptive.py:60-77) and
 handed to the sm_100a kernel (csrc/sn_adaptive.cu) through the C ABI, which
 walks the rays, builds the supports, sums the moments in the reference's
-member order in fp64 and evaluates the closed-form normal.  ``star_trace`` and
-``estimate_affine_adaptive`` are the reference's single-pixel diagnostics
-(host, scalar), as in the reference.
+member order in fp64 and evaluates the closed-form normal.  The disparities
+reach the kernel as the reference's own float64 values (no fp32 cast), so
+masks and supports are bit-exact with the reference on its inputs.
+``depth_laplacian`` (the ST edge measure) runs on the GPU too;
+``star_trace`` and ``estimate_affine_adaptive`` are the reference's
+single-pixel diagnostics, evaluated on the host ray by ray.
 """
 
 from __future__ import annotations
@@ -21,8 +24,8 @@ from .geometry import StereoRig
 
 _STOPS = ("st", "cd")
 
-__all__ = ["StarConfig", "ray_offsets", "estimate_normals_adaptive", "star_trace",
-           "estimate_affine_adaptive"]
+__all__ = ["StarConfig", "ray_offsets", "depth_laplacian", "estimate_normals_adaptive",
+           "star_trace", "estimate_affine_adaptive"]
 
 
 @dataclass(frozen=True)
@@ -73,73 +76,117 @@ def ray_table(config: StarConfig):
     return lens, xy
 
 
+def depth_laplacian(depth: ScalarField) -> ScalarField:
+    """5-point Laplacian magnitude of a depth field (adaptive.py:80-97), on the
+    GPU in fp64 with numpy's operation order: valid only at interior pixels
+    whose four neighbours are valid (mask), NaN elsewhere."""
+    import torch
+    from . import _native
+    from ._host import current_device, stream_ptr, to_device, to_host
+    z = to_device(depth.values)
+    m = to_device(np.ascontiguousarray(depth.mask, dtype=np.uint8), dtype=torch.uint8)
+    H, W = z.shape
+    e = torch.empty_like(z)
+    ok = torch.empty_like(m)
+    dev = current_device()
+    rc = _native.load().sn_depth_laplacian_f64(_native.plan(dev.index), z.data_ptr(),
+                                               m.data_ptr(), 1, H, W, e.data_ptr(), ok.data_ptr(),
+                                               stream_ptr(dev))
+    _native.check(rc, "depth_laplacian")
+    return ScalarField(to_host(e), to_host(ok).astype(bool))
+
+
 def estimate_normals_adaptive(disparity: ScalarField, rig: StereoRig, config: StarConfig,
                               threads: int | None = 1) -> NormalField:
     """Dense normals with star-shaped adaptive supports (adaptive.py:177-268),
-    computed on the GPU; masks bit-exact with the reference."""
+    computed on the GPU from the float64 disparities; masks bit-exact with
+    the reference."""
     import torch
     from . import device
     from ._host import resolve_threads, to_device, to_host
 
     resolve_threads(threads)
-    d = to_device(disparity.values, dtype=torch.float32)
+    d = to_device(disparity.values)
     mask = torch.empty((1,) + tuple(d.shape), dtype=torch.uint8, device=d.device)
     out = device.adaptive_points(d, rig, config, mask=mask)
     return NormalField(to_host(out[0, ..., 3:]).astype(np.float64), to_host(mask[0]).astype(bool))
 
 
+def _ray_reach(ray: np.ndarray, u: int, v: int, depth: ScalarField,
+               edges: ScalarField | None, config: StarConfig, zc: float, rng):
+    """Steps of one ray that the walk keeps (a prefix) and the running depth
+    range after it.  ``rng`` = (rmax, rmin) entering the ray."""
+    h, w = depth.shape
+    xx, yy = u + ray[:, 0], v + ray[:, 1]
+    inside = (xx >= 0) & (xx < w) & (yy >= 0) & (yy < h)
+    xi, yi = np.where(inside, xx, 0), np.where(inside, yy, 0)
+    # border and masked pixels stop the ray before any bookkeeping
+    hard = inside & depth.mask[yi, xi]
+    n_hard = len(ray) if hard.all() else int(np.argmin(hard))
+    rmax, rmin = rng
+    if config.stop == "st":
+        with np.errstate(invalid="ignore"):
+            ok = edges.mask[yi, xi] & ~(edges.values[yi, xi] > config.threshold)
+        ok = ok[:n_hard]
+        return (n_hard if ok.all() else int(np.argmin(ok))), rng
+    # cd: running extremes include the step that stops the ray
+    z = depth.values[yi[:n_hard], xi[:n_hard]]
+    hi = np.fmax.accumulate(np.concatenate(([rmax], z)))[1:]
+    lo = np.fmin.accumulate(np.concatenate(([rmin], z)))[1:]
+    bad = (hi - lo) > config.threshold * zc
+    n = int(np.argmax(bad)) if bad.any() else n_hard
+    last = min(n, n_hard - 1)
+    if last >= 0:
+        rmax, rmin = max(rmax, float(hi[last])), min(rmin, float(lo[last]))
+    return n, (rmax, rmin)
+
+
 def star_trace(center, depth: ScalarField, edges: ScalarField | None,
                config: StarConfig) -> np.ndarray:
-    """Offsets selected around one pixel (adaptive.py:100-143): the
-    reference's single-pixel diagnostic, scalar host code."""
+    """Offsets selected around one pixel, (0, 0) first and then each kept ray
+    step's offset at its first occurrence (adaptive.py:100-143).  Rays stop,
+    excluding the triggering pixel, at the border, at masked pixels, where the
+    edge measure is invalid or exceeds t (``st``) or once the covered depth
+    range exceeds t * z_c (``cd``; per ray, or shared by the pixel's rays)."""
     if config.stop == "st" and edges is None:
         raise ValueError("stop='st' requires an edge map")
     u, v = center
     h, w = depth.shape
-    selected = [(0, 0)]
     if not (0 <= v < h and 0 <= u < w) or not depth.mask[v, u]:
-        return np.asarray(selected, dtype=np.int64)
-    zc = depth.values[v, u]
-    seen = {(0, 0)}
-    rmax = rmin = zc
+        return np.zeros((1, 2), dtype=np.int64)
+    zc = float(depth.values[v, u])
+    kept = [np.zeros((1, 2), dtype=np.int64)]
+    rng = (zc, zc)
     for ray in ray_offsets(config):
         if config.stop == "cd" and not config.shared_range:
-            rmax = rmin = zc
-        for vx, vy in ray:
-            uu, vv = u + vx, v + vy
-            if not (0 <= uu < w and 0 <= vv < h) or not depth.mask[vv, uu]:
-                break
-            if config.stop == "st":
-                if not edges.mask[vv, uu] or edges.values[vv, uu] > config.threshold:
-                    break
-            else:
-                z = depth.values[vv, uu]
-                rmax, rmin = max(rmax, z), min(rmin, z)
-                if rmax - rmin > config.threshold * zc:
-                    break
-            key = (int(vx), int(vy))
-            if key not in seen:
-                seen.add(key)
-                selected.append(key)
-    return np.asarray(selected, dtype=np.int64)
+            rng = (zc, zc)
+        n, rng = _ray_reach(ray, u, v, depth, edges, config, zc, rng)
+        kept.append(ray[:n])
+    steps = np.concatenate(kept).astype(np.int64)
+    _, first = np.unique(steps, axis=0, return_index=True)
+    return steps[np.sort(first)]
 
 
 def estimate_affine_adaptive(disparity: ScalarField, depth: ScalarField,
                              edges: ScalarField | None, pixel, config: StarConfig):
-    """(a1, a2) over one pixel's star support (adaptive.py:146-174)."""
+    """(a1, a2) least-squares fit over one pixel's star support
+    (adaptive.py:146-174): offsets with an invalid disparity sample are left
+    out; (nan, nan) for an invalid centre or a rank-deficient support."""
     u, v = pixel
     h, w = disparity.shape
+    nan2 = (float("nan"), float("nan"))
     if not (0 <= v < h and 0 <= u < w) or not disparity.mask[v, u]:
-        return (float("nan"), float("nan"))
-    off = star_trace(pixel, depth, edges, config)
-    uu, vv = u + off[:, 0], v + off[:, 1]
-    ok = disparity.mask[vv, uu]
-    vxy = off[ok].astype(np.float64)
-    rhs = disparity.values[vv[ok], uu[ok]] - disparity.values[v, u]
-    alpha, beta, gamma = float(vxy[:, 0] @ vxy[:, 0]), float(vxy[:, 0] @ vxy[:, 1]), \
-        float(vxy[:, 1] @ vxy[:, 1])
-    det = alpha * gamma - beta * beta
+        return nan2
+    sup = star_trace(pixel, depth, edges, config)
+    sup = sup[disparity.mask[v + sup[:, 1], u + sup[:, 0]]]
+    # the moments as strided column dot products, the reference's own BLAS
+    # calls (a contiguous copy could take another summation order)
+    vxy = sup.astype(np.float64)
+    vx, vy = vxy[:, 0], vxy[:, 1]
+    dd = disparity.values[v + sup[:, 1], u + sup[:, 0]] - disparity.values[v, u]
+    al, be, ga = float(vx @ vx), float(vx @ vy), float(vy @ vy)
+    det = al * ga - be * be
     if det <= 0.5:
-        return (float("nan"), float("nan"))
-    b1, b2 = float(vxy[:, 0] @ rhs), float(vxy[:, 1] @ rhs)
-    return (1.0 + (gamma * b1 - beta * b2) / det, (-beta * b1 + alpha * b2) / det)
+        return nan2
+    b1, b2 = float(vx @ dd), float(vy @ dd)
+    return (1.0 + (ga * b1 - be * b2) / det, (-be * b1 + al * b2) / det)

@@ -34,7 +34,8 @@ namespace sn {
 // z = fx*b/d (pred_depth: NaN unless d is finite and > 0).  Rounding is
 // monotonic, so running maxima / minima of these values are the roundings of
 // the fp64 ones -- the fp32 filter below relies on that.
-__global__ void depth_kernel(const float* __restrict__ disp, int64_t n, double fxb,
+template <typename T>
+__global__ void depth_kernel(const T* __restrict__ disp, int64_t n, double fxb,
                              float* __restrict__ z) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -44,7 +45,8 @@ __global__ void depth_kernel(const float* __restrict__ disp, int64_t n, double f
 // CD walk, exact: the reference's fp64 running range (adaptive.py:214-234)
 // over depths recomputed from the disparities, for the lanes the fp32 filter
 // cannot decide.  Sets this lane's bit in the warp's key masks.
-__device__ __noinline__ void cd_walk_exact(const float* __restrict__ fd, int x, int y, int W, int H,
+template <typename T>
+__device__ __noinline__ void cd_walk_exact(const T* __restrict__ fd, int x, int y, int W, int H,
                                            double zc, const AdaptiveParams& ap,
                                            const StarTable& tab, uint32_t* km, uint32_t bit) {
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
@@ -86,9 +88,9 @@ constexpr uint32_t kFull = 0xffffffffu;
 // has stopped, and the support is recorded per key as a ballot of the lanes
 // that visited it (warp-private shared-memory masks) -- no per-lane member
 // bitmaps, no divergent table reads.
-template <int STOP>  // 0 = ST, 1 = CD
+template <int STOP, typename T>  // STOP 0 = ST, 1 = CD; T = fp32 / fp64 disparities
 __global__ void __launch_bounds__(kAdaptiveThreads)
-    adaptive_kernel(const float* __restrict__ disp, const float* __restrict__ depth,
+    adaptive_kernel(const T* __restrict__ disp, const float* __restrict__ depth,
                     const uint32_t* __restrict__ pbits, const __grid_constant__ AdaptiveParams ap,
                     const __grid_constant__ StarTable tab, float* __restrict__ out6,
                     uint8_t* __restrict__ mask) {
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
     const int64_t f = have ? idx / HW : 0;
     const int pix = have ? (int)(idx - f * HW) : 0;
     const int y = pix / W, x = pix - y * W;
-    const float* fd = disp + f * HW;
+    const T* fd = disp + f * HW;
     const double zc = have ? pred_depth(fd[pix], p.fxb) : qnan;
     const bool center_ok = zc == zc;
     for (int k = lane; k < tab.n_keys; k += 32) km[k] = 0u;
@@ -216,13 +218,14 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
     // are numbered by first occurrence, so ascending key order IS member
     // order.  alpha, beta, gamma are integer sums (exact, as the reference's
     // fp64 sums are); v * (d_k - d_c) is exact for fp32 disparities, so one
-    // FMA per term rounds like the reference's multiply-then-add.
+    // FMA per term rounds like the reference's multiply-then-add; fp64
+    // disparities round the product first (adaptive.py:251-252: b1 += vx * dd).
     // 32-bit sums unless the table's sums could overflow them (tab.wide)
     long long ia = 0, ib = 0, ig = 0;
     int ja = 0, jb = 0, jg = 0;
     double b1 = 0.0, b2 = 0.0;
     const double dc = (double)fd[pix];
-    const float* fdp = fd + pix;
+    const T* fdp = fd + pix;
     for (int k = 0; k < tab.n_keys; ++k) {
       const uint32_t mk = km[k];
       if (mk == 0u) continue;  // warp-uniform
@@ -239,8 +242,13 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
           jg += ky * ky;
         }
         const double dd = __dsub_rn((double)fdp[k_lin[k]], dc);
-        b1 = __fma_rn((double)kx, dd, b1);
-        b2 = __fma_rn((double)ky, dd, b2);
+        if constexpr (sizeof(T) == 4) {
+          b1 = __fma_rn((double)kx, dd, b1);
+          b2 = __fma_rn((double)ky, dd, b2);
+        } else {
+          b1 = __dadd_rn(b1, __dmul_rn((double)kx, dd));
+          b2 = __dadd_rn(b2, __dmul_rn((double)ky, dd));
+        }
       }
     }
     if (!tab.wide) {
@@ -281,9 +289,12 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
         n32[2] = (float)uz;
       }
     }
-    // point: the fused pass's formula (geometry.py:39-64, fp32)
+    // point: the fused pass's formula (geometry.py:39-64; fp32, or fp64 for
+    // fp64 disparities)
     float px, py, pz;
-    {
+    if constexpr (sizeof(T) == 8) {
+      point_from_disparity_f64(dc, (double)x - p.u0, (double)(y + p.row0) - p.v0, p, px, py, pz);
+    } else {
       const float d32 = fd[pix];
       const float du_f = ((float)x - p.u0_hi) - p.u0_lo;
       const float dv_f = ((float)(y + p.row0) - p.v0_hi) - p.v0_lo;
@@ -307,7 +318,8 @@ size_t adaptive_workspace_bytes(int64_t B, int64_t H, int64_t W) {
   return (size_t)(B * H * W) * 4 + 256 + (size_t)(B * H * WW) * 4;
 }
 
-int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& ap,
+template <typename T>
+int run_adaptive(const LaunchCtx& ctx, const T* disp, const AdaptiveParams& ap,
                  const StarTable& tab, int stop, float* out6, uint8_t* mask, void* workspace,
                  size_t ws_bytes) {
   const FixedParams& p = ap.fp;
@@ -323,36 +335,37 @@ int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& 
   if (stop == 1) {
     int64_t g = (n + 255) / 256;
     if (g > (int64_t)ctx.num_sms * 32) g = (int64_t)ctx.num_sms * 32;
-    depth_kernel<<<(unsigned)g, 256, 0, ctx.stream>>>(disp, n, p.fxb, depth);
+    depth_kernel<T><<<(unsigned)g, 256, 0, ctx.stream>>>(disp, n, p.fxb, depth);
     if ((rc = check_launch("depth_kernel"))) return rc;
   }
   AdaptiveParams a = ap;
   if (stop == 0) {
     FixedParams fp = p;
     fill_predicate(fp, p.fxb, ap.threshold, bits);
-    if ((rc = run_passable_bits(ctx, disp, fp, bits))) return rc;
+    if ((rc = run_passable_bits<T>(ctx, disp, fp, bits))) return rc;
     a.fp.bits = bits;
     a.fp.bits_ww = fp.bits_ww;
   }
   int64_t ga = (n + kAdaptiveThreads - 1) / kAdaptiveThreads;
   if (ga > (int64_t)ctx.num_sms * 64) ga = (int64_t)ctx.num_sms * 64;
   const size_t sm = star_smem(tab.ray_start[tab.n_rays], tab.n_keys);
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(adaptive_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)star_smem(kStarMaxSteps, kStarMaxKeys)) != cudaSuccess ||
-        cudaFuncSetAttribute(adaptive_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)star_smem(kStarMaxSteps, kStarMaxKeys)) != cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(adaptive_kernel)");
-    attr_set = true;
-  }
+  const int smax = (int)star_smem(kStarMaxSteps, kStarMaxKeys);
+  if ((rc = ensure_dyn_smem(reinterpret_cast<const void*>(adaptive_kernel<0, T>), smax, ctx.device,
+                            "adaptive_kernel<st>")) ||
+      (rc = ensure_dyn_smem(reinterpret_cast<const void*>(adaptive_kernel<1, T>), smax, ctx.device,
+                            "adaptive_kernel<cd>")))
+    return rc;
   if (stop == 0)
-    adaptive_kernel<0><<<(unsigned)ga, kAdaptiveThreads, sm, ctx.stream>>>(
+    adaptive_kernel<0, T><<<(unsigned)ga, kAdaptiveThreads, sm, ctx.stream>>>(
         disp, depth, a.fp.bits, a, tab, out6, mask);
   else
-    adaptive_kernel<1><<<(unsigned)ga, kAdaptiveThreads, sm, ctx.stream>>>(
+    adaptive_kernel<1, T><<<(unsigned)ga, kAdaptiveThreads, sm, ctx.stream>>>(
         disp, depth, nullptr, a, tab, out6, mask);
   return check_launch("adaptive_kernel");
 }
+template int run_adaptive<float>(const LaunchCtx&, const float*, const AdaptiveParams&,
+                                 const StarTable&, int, float*, uint8_t*, void*, size_t);
+template int run_adaptive<double>(const LaunchCtx&, const double*, const AdaptiveParams&,
+                                  const StarTable&, int, float*, uint8_t*, void*, size_t);
 
 }  // namespace sn

@@ -14,6 +14,8 @@
 #include <cstdlib>
 #include <mutex>
 #include <numeric>
+#include <set>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -41,6 +43,59 @@ int check_launch(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SN_ECUDA, "%s launch: %s", what, cudaGetErrorString(e));
   return SN_OK;
+}
+
+int ensure_dyn_smem(const void* func, int bytes, int device, const char* name) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;  // (kernel, device) pairs
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({func, device})) return SN_OK;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return set_error(SN_ECUDA, "cudaFuncSetAttribute(%s): %s", name,
+                     cudaGetErrorString(cudaGetLastError()));
+  done.insert({func, device});
+  return SN_OK;
+}
+
+// A private stream-ordered pool per device: its release threshold keeps the
+// memory between calls without touching the device's default pool (which
+// other cudaMallocAsync users in the process own).
+static cudaMemPool_t scratch_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[device] = pool;
+  }
+  return pools[device];
+}
+
+int scratch_alloc(const LaunchCtx& ctx, size_t bytes, void** ptr) {
+  *ptr = nullptr;
+  cudaMemPool_t pool = scratch_pool(ctx.device);
+  if (!pool) return set_error(SN_ECUDA, "cannot create the scratch memory pool");
+  if (cudaMallocFromPoolAsync(ptr, bytes ? bytes : 1, pool, ctx.stream) != cudaSuccess) {
+    *ptr = nullptr;
+    return set_cuda_error("cudaMallocFromPoolAsync(scratch)");
+  }
+  return SN_OK;
+}
+
+void scratch_free(const LaunchCtx& ctx, void* ptr) {
+  if (ptr) cudaFreeAsync(ptr, ctx.stream);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -85,19 +140,21 @@ using namespace sn;
 struct sn_plan {
   int device;
   int num_sms;
-  // host-path workspace
+  // host-path workspace (sn_*_host): three streams, double-buffered device
+  // staging, and pinned host staging used when the caller's buffers are
+  // pageable.  Guarded by mu: host-path calls on one plan run one at a time.
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr},
               ev_out[2] = {nullptr, nullptr};
-  float* d_in[2] = {nullptr, nullptr};
+  void* d_in[2] = {nullptr, nullptr};  // input chunk (fp32 or fp64)
   float* d_out[2] = {nullptr, nullptr};
   uint8_t* d_mask[2] = {nullptr, nullptr};
   int32_t* d_lab[2] = {nullptr, nullptr};
   void* d_ws[2] = {nullptr, nullptr};
-  size_t cap_px = 0, ws_cap = 0;
-  // labeller workspace for the entry points without an explicit one
-  void* ccl_ws = nullptr;
-  size_t ccl_ws_bytes = 0;
+  size_t cap_in = 0, cap_px = 0, ws_cap = 0;
+  void* h_in[2] = {nullptr, nullptr};  // pinned staging (pageable callers only)
+  void* h_out[2] = {nullptr, nullptr};
+  size_t h_in_cap = 0, h_out_cap = 0;
   std::mutex mu;
 };
 
@@ -275,6 +332,8 @@ int sn_plan_destroy(sn_plan_t* plan) {
   {
     DeviceGuard g(plan->device);
     for (int i = 0; i < 2; ++i) {
+      if (plan->h_in[i]) cudaFreeHost(plan->h_in[i]);
+      if (plan->h_out[i]) cudaFreeHost(plan->h_out[i]);
       if (plan->d_in[i]) cudaFree(plan->d_in[i]);
       if (plan->d_out[i]) cudaFree(plan->d_out[i]);
       if (plan->d_mask[i]) cudaFree(plan->d_mask[i]);
@@ -284,7 +343,6 @@ int sn_plan_destroy(sn_plan_t* plan) {
       if (plan->ev_done[i]) cudaEventDestroy(plan->ev_done[i]);
       if (plan->ev_out[i]) cudaEventDestroy(plan->ev_out[i]);
     }
-    if (plan->ccl_ws) cudaFree(plan->ccl_ws);
     if (plan->s_h2d) cudaStreamDestroy(plan->s_h2d);
     if (plan->s_comp) cudaStreamDestroy(plan->s_comp);
     if (plan->s_d2h) cudaStreamDestroy(plan->s_d2h);
@@ -363,8 +421,30 @@ int sn_oriented_points_bits(sn_plan_t* plan, const float* disp, int64_t B, int64
                                      stream, 0, row0, bits, t);
 }
 
-int sn_passable_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
-                     const sn_rig_t* rig, double t, uint32_t* bits, void* stream) {
+int sn_oriented_points_bits_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                                int64_t W, int64_t row0, const sn_rig_t* rig,
+                                const int32_t* offsets_xy, int32_t n_off, double t, float* out6,
+                                uint8_t* mask, uint32_t* bits, void* stream) {
+  if (B * H * W > 0 && !bits) return set_error(SN_EINVAL, "NULL bit-mask buffer");
+  return oriented_points_impl<double>(plan, disp, B, H, W, rig, offsets_xy, n_off, out6, mask,
+                                      stream, 0, row0, bits, t);
+}
+
+int sn_oriented_points_rows_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                                int64_t W, int64_t row0, const sn_rig_t* rig,
+                                const int32_t* offsets_xy, int32_t n_off, float* out6,
+                                uint8_t* mask, void* stream) {
+  return oriented_points_impl<double>(plan, disp, B, H, W, rig, offsets_xy, n_off, out6, mask,
+                                      stream, 0, row0);
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+int passable_bits_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                       const sn_rig_t* rig, double t, uint32_t* bits, void* stream) {
   if (!plan) return set_error(SN_EINVAL, "plan is NULL");
   int rc = check_shape(B, H, W);
   if (rc) return rc;
@@ -379,7 +459,21 @@ int sn_passable_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, i
   fill_rig(p, rig);
   fill_predicate(p, p.fxb, t, bits);
   DeviceGuard g(plan->device);
-  return run_passable_bits(make_ctx(plan, stream), disp, p, bits);
+  return run_passable_bits<T>(make_ctx(plan, stream), disp, p, bits);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_passable_bits(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                     const sn_rig_t* rig, double t, uint32_t* bits, void* stream) {
+  return passable_bits_impl<float>(plan, disp, B, H, W, rig, t, bits, stream);
+}
+
+int sn_passable_bits_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                         const sn_rig_t* rig, double t, uint32_t* bits, void* stream) {
+  return passable_bits_impl<double>(plan, disp, B, H, W, rig, t, bits, stream);
 }
 
 static int check_png16(double scale, int32_t invalid) {
@@ -506,11 +600,15 @@ int sn_adaptive_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) 
   return SN_OK;
 }
 
-int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
-                       const sn_rig_t* rig, int32_t n_rays, const int32_t* ray_len,
-                       const int32_t* ray_xy, int32_t stop, int32_t shared_range,
-                       double threshold, float* out6, uint8_t* mask, void* workspace,
-                       size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+int adaptive_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                  const sn_rig_t* rig, int32_t n_rays, const int32_t* ray_len,
+                  const int32_t* ray_xy, int32_t stop, int32_t shared_range, double threshold,
+                  float* out6, uint8_t* mask, void* workspace, size_t ws_bytes, void* stream) {
   if (!plan) return set_error(SN_EINVAL, "plan is NULL");
   int rc = check_shape(B, H, W);
   if (rc) return rc;
@@ -582,8 +680,30 @@ int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
   ap.nfxfy = -rig->fx * rig->fy;
   ap.shared_range = shared_range != 0;
   DeviceGuard g(plan->device);
-  return run_adaptive(make_ctx(plan, stream), disp, ap, tab, stop, out6, mask, workspace,
-                      ws_bytes);
+  return run_adaptive<T>(make_ctx(plan, stream), disp, ap, tab, stop, out6, mask, workspace,
+                         ws_bytes);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_adaptive_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                       const sn_rig_t* rig, int32_t n_rays, const int32_t* ray_len,
+                       const int32_t* ray_xy, int32_t stop, int32_t shared_range,
+                       double threshold, float* out6, uint8_t* mask, void* workspace,
+                       size_t ws_bytes, void* stream) {
+  return adaptive_impl<float>(plan, disp, B, H, W, rig, n_rays, ray_len, ray_xy, stop,
+                              shared_range, threshold, out6, mask, workspace, ws_bytes, stream);
+}
+
+int sn_adaptive_points_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                           const sn_rig_t* rig, int32_t n_rays, const int32_t* ray_len,
+                           const int32_t* ray_xy, int32_t stop, int32_t shared_range,
+                           double threshold, float* out6, uint8_t* mask, void* workspace,
+                           size_t ws_bytes, void* stream) {
+  return adaptive_impl<double>(plan, disp, B, H, W, rig, n_rays, ray_len, ray_xy, stop,
+                               shared_range, threshold, out6, mask, workspace, ws_bytes, stream);
 }
 
 int sn_eval_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
@@ -656,8 +776,13 @@ int sn_affine_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int
   return affine_impl<double>(plan, disp, B, H, W, offsets_xy, n_off, a1, a2, mask, stream);
 }
 
-int sn_passable(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
-                const sn_rig_t* rig, double t, uint8_t* passable, double* edges, void* stream) {
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+int passable_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                  const sn_rig_t* rig, double t, uint8_t* passable, double* edges, void* stream) {
   if (!plan) return set_error(SN_EINVAL, "plan is NULL");
   int rc = check_shape(B, H, W);
   if (rc) return rc;
@@ -666,7 +791,22 @@ int sn_passable(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_
   if (B * H * W > 0 && !disp) return set_error(SN_EINVAL, "NULL buffer");
   const CclParams p = make_ccl_params(B, H, W, rig->fx * rig->baseline, t);
   DeviceGuard g(plan->device);
-  return run_passable(make_ctx(plan, stream), disp, p, passable, edges);
+  return run_passable<T>(make_ctx(plan, stream), disp, p, passable, edges);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_passable(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                const sn_rig_t* rig, double t, uint8_t* passable, double* edges, void* stream) {
+  return passable_impl<float>(plan, disp, B, H, W, rig, t, passable, edges, stream);
+}
+
+int sn_passable_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                    const sn_rig_t* rig, double t, uint8_t* passable, double* edges,
+                    void* stream) {
+  return passable_impl<double>(plan, disp, B, H, W, rig, t, passable, edges, stream);
 }
 
 int sn_ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
@@ -676,6 +816,8 @@ int sn_ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, size_t* bytes) {
   *bytes = ccl_workspace_bytes(B, H, W);
   return SN_OK;
 }
+
+}  // extern "C"
 
 namespace {
 
@@ -690,47 +832,112 @@ int ccl_args(sn_plan_t* plan, int64_t B, int64_t H, int64_t W, int64_t row_base,
   return SN_OK;
 }
 
-// plan-owned workspace (grown on demand; stream-ordered use only)
-int plan_workspace(sn_plan_t* plan, int64_t B, int64_t H, int64_t W, void** ws, size_t* bytes) {
-  const size_t need = ccl_workspace_bytes(B, H, W);
-  if (plan->ccl_ws_bytes < need) {
-    if (plan->ccl_ws) cudaFree(plan->ccl_ws);  // synchronises the device: growth only
-    plan->ccl_ws = nullptr;
-    plan->ccl_ws_bytes = 0;
-    if (cudaMalloc(&plan->ccl_ws, need) != cudaSuccess)
-      return set_cuda_error("cudaMalloc(labeller workspace)");
-    plan->ccl_ws_bytes = need;
+// Entry points without a caller workspace take one from the device's private
+// stream-ordered pool on the caller's stream and free it there: concurrent
+// calls on different streams never share scratch, and the pool keeps the
+// memory between calls (no cudaMalloc in the steady state).
+struct StreamScratch {
+  LaunchCtx ctx;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int acquire(const LaunchCtx& c, size_t n) {
+    ctx = c;
+    bytes = n;
+    return scratch_alloc(c, n, &ptr);
   }
-  *ws = plan->ccl_ws;
-  *bytes = plan->ccl_ws_bytes;
-  return SN_OK;
-}
+  ~StreamScratch() {
+    if (ptr) scratch_free(ctx, ptr);
+  }
+};
 
-}  // namespace
-
-int sn_ccl_labels_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
-                     const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
-                     void* workspace, size_t ws_bytes, void* stream) {
+template <typename T>
+int ccl_labels_ws_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                       const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                       void* workspace, size_t ws_bytes, void* stream) {
   int rc = ccl_args(plan, B, H, W, row_base, disp, labels);
   if (rc) return rc;
   if ((rc = check_rig(rig))) return rc;
   if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
   const CclParams p = make_ccl_params(B, H, W, rig->fx * rig->baseline, t);
   DeviceGuard g(plan->device);
-  return run_ccl(make_ctx(plan, stream), disp, nullptr, p, row_base * W, labels, workspace,
-                 ws_bytes);
+  return run_ccl<T>(make_ctx(plan, stream), disp, nullptr, p, row_base * W, labels, workspace,
+                    ws_bytes);
+}
+
+template <typename T>
+int ccl_labels_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                    const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                    void* stream) {
+  int rc = ccl_args(plan, B, H, W, row_base, disp, labels);
+  if (rc) return rc;
+  if (B * H * W == 0) return ccl_labels_ws_impl<T>(plan, disp, B, H, W, rig, t, row_base, labels,
+                                                   nullptr, 0, stream);
+  DeviceGuard g(plan->device);
+  StreamScratch ws;
+  if ((rc = ws.acquire(make_ctx(plan, stream), ccl_workspace_bytes(B, H, W)))) return rc;
+  return ccl_labels_ws_impl<T>(plan, disp, B, H, W, rig, t, row_base, labels, ws.ptr, ws.bytes,
+                               stream);
+}
+
+template <typename T>
+int pipeline_ws_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                     const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                     float* out6, uint8_t* mask, int32_t* labels, void* workspace,
+                     size_t ws_bytes, void* stream) {
+  int rc = ccl_args(plan, B, H, W, 0, disp, labels);
+  if (rc) return rc;
+  if (B * H * W == 0) return SN_OK;
+  if (!workspace || ws_bytes < ccl_workspace_bytes(B, H, W))
+    return set_error(SN_EINVAL, "pipeline workspace too small");
+  // the bit mask lives at the head of the labeller workspace
+  uint32_t* bits = static_cast<uint32_t*>(workspace);
+  if ((rc = oriented_points_impl<T>(plan, disp, B, H, W, rig, offsets_xy, n_off, out6, mask,
+                                    stream, 0, 0, bits, t)))
+    return rc;
+  return sn_ccl_from_bits_ws(plan, bits, B, H, W, 0, labels, workspace, ws_bytes, stream);
+}
+
+template <typename T>
+int pipeline_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                  const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                  float* out6, uint8_t* mask, int32_t* labels, void* stream) {
+  int rc = ccl_args(plan, B, H, W, 0, disp, labels);
+  if (rc) return rc;
+  if (B * H * W == 0) return SN_OK;
+  DeviceGuard g(plan->device);
+  StreamScratch ws;
+  if ((rc = ws.acquire(make_ctx(plan, stream), ccl_workspace_bytes(B, H, W)))) return rc;
+  return pipeline_ws_impl<T>(plan, disp, B, H, W, rig, offsets_xy, n_off, t, out6, mask, labels,
+                             ws.ptr, ws.bytes, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_ccl_labels_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                     const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                     void* workspace, size_t ws_bytes, void* stream) {
+  return ccl_labels_ws_impl<float>(plan, disp, B, H, W, rig, t, row_base, labels, workspace,
+                                   ws_bytes, stream);
+}
+
+int sn_ccl_labels_ws_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                         const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  return ccl_labels_ws_impl<double>(plan, disp, B, H, W, rig, t, row_base, labels, workspace,
+                                    ws_bytes, stream);
 }
 
 int sn_ccl_labels(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                   const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels, void* stream) {
-  int rc = ccl_args(plan, B, H, W, row_base, disp, labels);
-  if (rc) return rc;
-  std::lock_guard<std::mutex> lock(plan->mu);
-  DeviceGuard g(plan->device);
-  void* ws = nullptr;
-  size_t bytes = 0;
-  if ((rc = plan_workspace(plan, B, H, W, &ws, &bytes))) return rc;
-  return sn_ccl_labels_ws(plan, disp, B, H, W, rig, t, row_base, labels, ws, bytes, stream);
+  return ccl_labels_impl<float>(plan, disp, B, H, W, rig, t, row_base, labels, stream);
+}
+
+int sn_ccl_labels_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                      const sn_rig_t* rig, double t, int64_t row_base, int32_t* labels,
+                      void* stream) {
+  return ccl_labels_impl<double>(plan, disp, B, H, W, rig, t, row_base, labels, stream);
 }
 
 int sn_ccl_from_passable_ws(sn_plan_t* plan, const uint8_t* passable, int64_t B, int64_t H,
@@ -740,20 +947,20 @@ int sn_ccl_from_passable_ws(sn_plan_t* plan, const uint8_t* passable, int64_t B,
   if (rc) return rc;
   const CclParams p = make_ccl_params(B, H, W, 0.0, 1.0);
   DeviceGuard g(plan->device);
-  return run_ccl(make_ctx(plan, stream), nullptr, passable, p, row_base * W, labels, workspace,
-                 ws_bytes);
+  return run_ccl<float>(make_ctx(plan, stream), nullptr, passable, p, row_base * W, labels,
+                        workspace, ws_bytes);
 }
 
 int sn_ccl_from_passable(sn_plan_t* plan, const uint8_t* passable, int64_t B, int64_t H, int64_t W,
                          int64_t row_base, int32_t* labels, void* stream) {
   int rc = ccl_args(plan, B, H, W, row_base, passable, labels);
   if (rc) return rc;
-  std::lock_guard<std::mutex> lock(plan->mu);
+  if (B * H * W == 0) return SN_OK;
   DeviceGuard g(plan->device);
-  void* ws = nullptr;
-  size_t bytes = 0;
-  if ((rc = plan_workspace(plan, B, H, W, &ws, &bytes))) return rc;
-  return sn_ccl_from_passable_ws(plan, passable, B, H, W, row_base, labels, ws, bytes, stream);
+  StreamScratch ws;
+  if ((rc = ws.acquire(make_ctx(plan, stream), ccl_workspace_bytes(B, H, W)))) return rc;
+  return sn_ccl_from_passable_ws(plan, passable, B, H, W, row_base, labels, ws.ptr, ws.bytes,
+                                 stream);
 }
 
 int sn_ccl_from_bits_ws(sn_plan_t* plan, const uint32_t* bits, int64_t B, int64_t H, int64_t W,
@@ -763,39 +970,120 @@ int sn_ccl_from_bits_ws(sn_plan_t* plan, const uint32_t* bits, int64_t B, int64_
   if (rc) return rc;
   const CclParams p = make_ccl_params(B, H, W, 0.0, 1.0);
   DeviceGuard g(plan->device);
-  return run_ccl(make_ctx(plan, stream), nullptr, nullptr, p, row_base * W, labels, workspace,
-                 ws_bytes, bits);
+  return run_ccl<float>(make_ctx(plan, stream), nullptr, nullptr, p, row_base * W, labels,
+                        workspace, ws_bytes, bits);
 }
 
 int sn_pipeline_ws(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                    const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
                    float* out6, uint8_t* mask, int32_t* labels, void* workspace, size_t ws_bytes,
                    void* stream) {
-  int rc = ccl_args(plan, B, H, W, 0, disp, labels);
-  if (rc) return rc;
-  if (B * H * W == 0) return SN_OK;
-  if (!workspace || ws_bytes < ccl_workspace_bytes(B, H, W))
-    return set_error(SN_EINVAL, "pipeline workspace too small");
-  // the bit mask lives at the head of the labeller workspace
-  uint32_t* bits = static_cast<uint32_t*>(workspace);
-  if ((rc = sn_oriented_points_bits(plan, disp, B, H, W, 0, rig, offsets_xy, n_off, t, out6, mask,
-                                    bits, stream)))
-    return rc;
-  return sn_ccl_from_bits_ws(plan, bits, B, H, W, 0, labels, workspace, ws_bytes, stream);
+  return pipeline_ws_impl<float>(plan, disp, B, H, W, rig, offsets_xy, n_off, t, out6, mask,
+                                 labels, workspace, ws_bytes, stream);
+}
+
+int sn_pipeline_ws_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                       const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                       float* out6, uint8_t* mask, int32_t* labels, void* workspace,
+                       size_t ws_bytes, void* stream) {
+  return pipeline_ws_impl<double>(plan, disp, B, H, W, rig, offsets_xy, n_off, t, out6, mask,
+                                  labels, workspace, ws_bytes, stream);
 }
 
 int sn_pipeline(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
                 const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
                 float* out6, uint8_t* mask, int32_t* labels, void* stream) {
-  int rc = ccl_args(plan, B, H, W, 0, disp, labels);
+  return pipeline_impl<float>(plan, disp, B, H, W, rig, offsets_xy, n_off, t, out6, mask, labels,
+                              stream);
+}
+
+int sn_pipeline_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                    const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
+                    float* out6, uint8_t* mask, int32_t* labels, void* stream) {
+  return pipeline_impl<double>(plan, disp, B, H, W, rig, offsets_xy, n_off, t, out6, mask, labels,
+                               stream);
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+int depth_map_impl(sn_plan_t* plan, const T* disp, int64_t n, const sn_rig_t* rig, double* z,
+                   void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  if (n < 0) return set_error(SN_EINVAL, "negative size");
+  int rc = check_rig(rig);
   if (rc) return rc;
-  std::lock_guard<std::mutex> lock(plan->mu);
+  if (n > 0 && (!disp || !z)) return set_error(SN_EINVAL, "NULL buffer");
   DeviceGuard g(plan->device);
-  void* ws = nullptr;
-  size_t bytes = 0;
-  if ((rc = plan_workspace(plan, B, H, W, &ws, &bytes))) return rc;
-  return sn_pipeline_ws(plan, disp, B, H, W, rig, offsets_xy, n_off, t, out6, mask, labels, ws,
-                        bytes, stream);
+  return run_depth_map<T>(make_ctx(plan, stream), disp, n, rig->fx * rig->baseline, z);
+}
+
+template <typename T>
+int triangulate_grid_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W,
+                          const sn_rig_t* rig, double* xyz, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if ((rc = check_rig(rig))) return rc;
+  if (B * H * W > 0 && (!disp || !xyz)) return set_error(SN_EINVAL, "NULL buffer");
+  FixedParams p{};
+  p.B = B;
+  p.H = H;
+  p.W = W;
+  fill_rig(p, rig);
+  DeviceGuard g(plan->device);
+  return run_triangulate_grid<T>(make_ctx(plan, stream), disp, p, xyz);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_depth_map(sn_plan_t* plan, const float* disp, int64_t n, const sn_rig_t* rig, double* z,
+                 void* stream) {
+  return depth_map_impl<float>(plan, disp, n, rig, z, stream);
+}
+
+int sn_depth_map_f64(sn_plan_t* plan, const double* disp, int64_t n, const sn_rig_t* rig,
+                     double* z, void* stream) {
+  return depth_map_impl<double>(plan, disp, n, rig, z, stream);
+}
+
+int sn_triangulate_f64(sn_plan_t* plan, const double* u, const double* v, const double* d,
+                       int64_t n, const sn_rig_t* rig, double* x, double* y, double* z,
+                       void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  if (n < 0) return set_error(SN_EINVAL, "negative size");
+  int rc = check_rig(rig);
+  if (rc) return rc;
+  if (n > 0 && (!u || !v || !d || !x || !y || !z)) return set_error(SN_EINVAL, "NULL buffer");
+  FixedParams p{};
+  fill_rig(p, rig);
+  DeviceGuard g(plan->device);
+  return run_triangulate(make_ctx(plan, stream), u, v, d, n, p, x, y, z);
+}
+
+int sn_triangulate_grid(sn_plan_t* plan, const float* disp, int64_t B, int64_t H, int64_t W,
+                        const sn_rig_t* rig, double* xyz, void* stream) {
+  return triangulate_grid_impl<float>(plan, disp, B, H, W, rig, xyz, stream);
+}
+
+int sn_triangulate_grid_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
+                            const sn_rig_t* rig, double* xyz, void* stream) {
+  return triangulate_grid_impl<double>(plan, disp, B, H, W, rig, xyz, stream);
+}
+
+int sn_depth_laplacian_f64(sn_plan_t* plan, const double* depth, const uint8_t* mask, int64_t B,
+                           int64_t H, int64_t W, double* edges, uint8_t* ok, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (B * H * W > 0 && (!depth || !mask || (!edges && !ok)))
+    return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_laplacian(make_ctx(plan, stream), depth, mask, B, H, W, edges, ok);
 }
 
 int sn_relabel(sn_plan_t* plan, int32_t* labels, int64_t n, int64_t index_base,
@@ -875,10 +1163,57 @@ int sn_seam_merge_host(const int32_t* seams, int32_t n_strips, int64_t W, int32_
 
 namespace {
 
+bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// host memcpy split over a few threads (a single core copies ~10 GB/s; the
+// pageable staging would otherwise run below the PCIe rate)
+void par_copy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kMinPart = 8u << 20;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t parts = std::min<size_t>(std::min<size_t>(hw, 8), std::max<size_t>(1, bytes / kMinPart));
+  if (parts <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t step = (bytes / parts + 63) / 64 * 64;
+  for (size_t off = 0; off < bytes; off += step) {
+    const size_t n = std::min(step, bytes - off);
+    th.emplace_back([=] { memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, n); });
+  }
+  for (auto& t : th) t.join();
+}
+
+int grow_pinned(void** buf, size_t& cap, size_t need) {
+  if (cap >= need) return SN_OK;
+  for (int i = 0; i < 2; ++i) {
+    if (buf[i]) cudaFreeHost(buf[i]);
+    buf[i] = nullptr;
+  }
+  cap = 0;
+  for (int i = 0; i < 2; ++i)
+    if (cudaHostAlloc(&buf[i], need, cudaHostAllocDefault) != cudaSuccess)
+      return set_cuda_error("cudaHostAlloc(host-path staging)");
+  cap = need;
+  return SN_OK;
+}
+
 // host-buffer pipeline: frames in chunks, H2D / compute / D2H overlapped on
-// three streams with double-buffered device staging; labels (and the
-// passable bits they need) only when labels_host is non-NULL
-int host_pipeline(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H, int64_t W,
+// three streams with double-buffered device staging; labels (and the passable
+// bits they need) only when labels_host is non-NULL.  Pinned (page-locked)
+// caller buffers are copied directly; pageable ones go through the plan's
+// pinned staging slots, filled / drained by multi-threaded host copies while
+// the device works on the other slot.
+template <typename T>
+int host_pipeline(sn_plan_t* plan, const T* disp_host, int64_t B, int64_t H, int64_t W,
                   const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
                   float* out6_host, uint8_t* mask_host, int32_t* labels_host) {
   if (!plan) return set_error(SN_EINVAL, "plan is NULL");
@@ -893,12 +1228,13 @@ int host_pipeline(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
   if (!disp_host || !out6_host) return set_error(SN_EINVAL, "NULL buffer");
   std::lock_guard<std::mutex> lock(plan->mu);
   DeviceGuard g(plan->device);
-  // chunk: ~16 Mpx per step (64 MB in, 384 MB out), whole frames
+  // chunk: ~16 Mpx per step (64-128 MB in, 384 MB out), whole frames
   int64_t chunk = std::max<int64_t>(1, (int64_t)(16 << 20) / std::max<int64_t>(frame_px, 1));
   chunk = std::min<int64_t>(chunk, B);
   const size_t need = (size_t)(chunk * frame_px);
   const size_t ws_need = labels_host ? ccl_workspace_bytes(chunk, H, W) : 0;
-  if (plan->cap_px < need || (labels_host && (!plan->d_lab[0] || plan->ws_cap < ws_need))) {
+  if (plan->cap_px < need || plan->cap_in < need * sizeof(T) ||
+      (labels_host && (!plan->d_lab[0] || plan->ws_cap < ws_need))) {
     for (int i = 0; i < 2; ++i) {
       cudaFree(plan->d_in[i]);
       cudaFree(plan->d_out[i]);
@@ -911,19 +1247,18 @@ int host_pipeline(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
       plan->d_lab[i] = nullptr;
       plan->d_ws[i] = nullptr;
     }
-    plan->cap_px = 0;
-    plan->ws_cap = 0;
-    const size_t cap = std::max(need, plan->cap_px);
+    plan->cap_px = plan->cap_in = plan->ws_cap = 0;
     for (int i = 0; i < 2; ++i) {
-      if (cudaMalloc(&plan->d_in[i], cap * sizeof(float)) != cudaSuccess ||
-          cudaMalloc(&plan->d_out[i], cap * 24) != cudaSuccess ||
-          cudaMalloc(&plan->d_mask[i], cap) != cudaSuccess)
+      if (cudaMalloc(&plan->d_in[i], need * sizeof(double)) != cudaSuccess ||
+          cudaMalloc(&plan->d_out[i], need * 24) != cudaSuccess ||
+          cudaMalloc(&plan->d_mask[i], need) != cudaSuccess)
         return set_cuda_error("cudaMalloc(host-path staging)");
-      if (labels_host && (cudaMalloc(&plan->d_lab[i], cap * 4) != cudaSuccess ||
+      if (labels_host && (cudaMalloc(&plan->d_lab[i], need * 4) != cudaSuccess ||
                           cudaMalloc(&plan->d_ws[i], ws_need) != cudaSuccess))
         return set_cuda_error("cudaMalloc(host-path labeller staging)");
     }
-    plan->cap_px = cap;
+    plan->cap_px = need;
+    plan->cap_in = need * sizeof(double);
     if (labels_host) plan->ws_cap = ws_need;
   }
   if (!plan->s_h2d) {
@@ -938,47 +1273,104 @@ int host_pipeline(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
         return set_cuda_error("cudaEventCreate");
     }
   }
+  // pageable buffers -> pinned staging slots; the output slot packs the
+  // records, then the mask, then the labels of one chunk
+  const bool pin_in = is_pinned(disp_host);
+  const bool pin_out = is_pinned(out6_host) && is_pinned(mask_host) && is_pinned(labels_host);
+  const size_t out_slot = need * 24 + (mask_host ? need : 0) + (labels_host ? need * 4 : 0);
+  if (!pin_in && (rc = grow_pinned(plan->h_in, plan->h_in_cap, need * sizeof(T)))) return rc;
+  if (!pin_out && (rc = grow_pinned(plan->h_out, plan->h_out_cap, out_slot))) return rc;
+
   const int64_t n_chunks = (B + chunk - 1) / chunk;
+  // every exit waits for the queued work (it may still read or write the
+  // caller's buffers or a staging slot)
+  auto drain_all = [&] {
+    cudaStreamSynchronize(plan->s_h2d);
+    cudaStreamSynchronize(plan->s_comp);
+    cudaStreamSynchronize(plan->s_d2h);
+  };
+  auto fail = [&](int code) {
+    drain_all();
+    cudaGetLastError();
+    return code;
+  };
+  // copy chunk c's outputs out of its pinned slot (pageable callers)
+  auto drain_out = [&](int64_t c) -> int {
+    const int s = (int)(c & 1);
+    const int64_t f0 = c * chunk, nf = std::min<int64_t>(chunk, B - f0);
+    const size_t px = (size_t)(nf * frame_px);
+    if (cudaEventSynchronize(plan->ev_out[s]) != cudaSuccess) return set_cuda_error("D2H wait");
+    const char* src = static_cast<const char*>(plan->h_out[s]);
+    par_copy(out6_host + f0 * frame_px * 6, src, px * 24);
+    src += need * 24;
+    if (mask_host) {
+      par_copy(mask_host + f0 * frame_px, src, px);
+      src += need;
+    }
+    if (labels_host) par_copy(labels_host + f0 * frame_px, src, px * 4);
+    return SN_OK;
+  };
   for (int64_t c = 0; c < n_chunks; ++c) {
     const int s = (int)(c & 1);
     const int64_t f0 = c * chunk;
     const int64_t nf = std::min<int64_t>(chunk, B - f0);
     const size_t px = (size_t)(nf * frame_px);
+    if (!pin_out && c >= 2 && (rc = drain_out(c - 2))) return fail(rc);
     // buffers of slot s are free once chunk c-2's compute (inputs) and D2H (outputs) are done
     if (c >= 2) {
       cudaStreamWaitEvent(plan->s_h2d, plan->ev_done[s], 0);
       cudaStreamWaitEvent(plan->s_comp, plan->ev_out[s], 0);
     }
-    if (cudaMemcpyAsync(plan->d_in[s], disp_host + f0 * frame_px, px * sizeof(float),
-                        cudaMemcpyHostToDevice, plan->s_h2d) != cudaSuccess)
-      return set_cuda_error("H2D copy");
+    const T* src = disp_host + f0 * frame_px;
+    if (!pin_in) {
+      // chunk c-2's H2D read this slot: its compute has started after it, so
+      // ev_in[s] (recorded after that copy) marks the slot free
+      if (c >= 2 && cudaEventSynchronize(plan->ev_in[s]) != cudaSuccess)
+        return fail(set_cuda_error("H2D wait"));
+      par_copy(plan->h_in[s], src, px * sizeof(T));
+      src = static_cast<const T*>(plan->h_in[s]);
+    }
+    if (cudaMemcpyAsync(plan->d_in[s], src, px * sizeof(T), cudaMemcpyHostToDevice,
+                        plan->s_h2d) != cudaSuccess)
+      return fail(set_cuda_error("H2D copy"));
     cudaEventRecord(plan->ev_in[s], plan->s_h2d);
     cudaStreamWaitEvent(plan->s_comp, plan->ev_in[s], 0);
     uint8_t* dmask = mask_host ? plan->d_mask[s] : nullptr;
+    const T* din = static_cast<const T*>(plan->d_in[s]);
     if (labels_host)
-      rc = sn_pipeline_ws(plan, plan->d_in[s], nf, H, W, rig, offsets_xy, n_off, t, plan->d_out[s],
-                          dmask, plan->d_lab[s], plan->d_ws[s], plan->ws_cap, plan->s_comp);
+      rc = pipeline_ws_impl<T>(plan, din, nf, H, W, rig, offsets_xy, n_off, t, plan->d_out[s],
+                               dmask, plan->d_lab[s], plan->d_ws[s], plan->ws_cap, plan->s_comp);
     else
-      rc = sn_oriented_points(plan, plan->d_in[s], nf, H, W, rig, offsets_xy, n_off,
-                              plan->d_out[s], dmask, plan->s_comp);
-    if (rc) return rc;
+      rc = oriented_points_impl<T>(plan, din, nf, H, W, rig, offsets_xy, n_off, plan->d_out[s],
+                                   dmask, plan->s_comp, 0);
+    if (rc) return fail(rc);
     cudaEventRecord(plan->ev_done[s], plan->s_comp);
     cudaStreamWaitEvent(plan->s_d2h, plan->ev_done[s], 0);
-    if (cudaMemcpyAsync(out6_host + f0 * frame_px * 6, plan->d_out[s], px * 24,
-                        cudaMemcpyDeviceToHost, plan->s_d2h) != cudaSuccess)
-      return set_cuda_error("D2H copy");
-    if (mask_host &&
-        cudaMemcpyAsync(mask_host + f0 * frame_px, plan->d_mask[s], px, cudaMemcpyDeviceToHost,
-                        plan->s_d2h) != cudaSuccess)
-      return set_cuda_error("D2H mask copy");
-    if (labels_host &&
-        cudaMemcpyAsync(labels_host + f0 * frame_px, plan->d_lab[s], px * 4,
-                        cudaMemcpyDeviceToHost, plan->s_d2h) != cudaSuccess)
-      return set_cuda_error("D2H label copy");
+    char* hout = pin_out ? nullptr : static_cast<char*>(plan->h_out[s]);
+    float* o6 = pin_out ? out6_host + f0 * frame_px * 6 : reinterpret_cast<float*>(hout);
+    if (cudaMemcpyAsync(o6, plan->d_out[s], px * 24, cudaMemcpyDeviceToHost, plan->s_d2h) !=
+        cudaSuccess)
+      return fail(set_cuda_error("D2H copy"));
+    if (mask_host) {
+      uint8_t* mo = pin_out ? mask_host + f0 * frame_px : reinterpret_cast<uint8_t*>(hout + need * 24);
+      if (cudaMemcpyAsync(mo, plan->d_mask[s], px, cudaMemcpyDeviceToHost, plan->s_d2h) !=
+          cudaSuccess)
+        return fail(set_cuda_error("D2H mask copy"));
+    }
+    if (labels_host) {
+      int32_t* lo = pin_out ? labels_host + f0 * frame_px
+                            : reinterpret_cast<int32_t*>(hout + need * 24 + (mask_host ? need : 0));
+      if (cudaMemcpyAsync(lo, plan->d_lab[s], px * 4, cudaMemcpyDeviceToHost, plan->s_d2h) !=
+          cudaSuccess)
+        return fail(set_cuda_error("D2H label copy"));
+    }
     cudaEventRecord(plan->ev_out[s], plan->s_d2h);
   }
-  if (cudaStreamSynchronize(plan->s_d2h) != cudaSuccess) return set_cuda_error("host-path sync");
-  if (cudaStreamSynchronize(plan->s_comp) != cudaSuccess) return set_cuda_error("host-path sync");
+  if (!pin_out)
+    for (int64_t c = std::max<int64_t>(0, n_chunks - 2); c < n_chunks; ++c)
+      if ((rc = drain_out(c))) return fail(rc);
+  if (cudaStreamSynchronize(plan->s_d2h) != cudaSuccess) return fail(set_cuda_error("host-path sync"));
+  if (cudaStreamSynchronize(plan->s_comp) != cudaSuccess) return fail(set_cuda_error("host-path sync"));
   return SN_OK;
 }
 
@@ -989,16 +1381,31 @@ extern "C" {
 int sn_oriented_points_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H,
                             int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
                             int32_t n_off, float* out6_host, uint8_t* mask_host) {
-  return host_pipeline(plan, disp_host, B, H, W, rig, offsets_xy, n_off, 0.0, out6_host,
-                       mask_host, nullptr);
+  return host_pipeline<float>(plan, disp_host, B, H, W, rig, offsets_xy, n_off, 0.0, out6_host,
+                              mask_host, nullptr);
+}
+
+int sn_oriented_points_host_f64(sn_plan_t* plan, const double* disp_host, int64_t B, int64_t H,
+                                int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
+                                int32_t n_off, float* out6_host, uint8_t* mask_host) {
+  return host_pipeline<double>(plan, disp_host, B, H, W, rig, offsets_xy, n_off, 0.0, out6_host,
+                               mask_host, nullptr);
 }
 
 int sn_pipeline_host(sn_plan_t* plan, const float* disp_host, int64_t B, int64_t H, int64_t W,
                      const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, double t,
                      float* out6_host, uint8_t* mask_host, int32_t* labels_host) {
   if (B * H * W > 0 && !labels_host) return set_error(SN_EINVAL, "NULL label buffer");
-  return host_pipeline(plan, disp_host, B, H, W, rig, offsets_xy, n_off, t, out6_host, mask_host,
-                       labels_host);
+  return host_pipeline<float>(plan, disp_host, B, H, W, rig, offsets_xy, n_off, t, out6_host,
+                              mask_host, labels_host);
+}
+
+int sn_pipeline_host_f64(sn_plan_t* plan, const double* disp_host, int64_t B, int64_t H,
+                         int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
+                         double t, float* out6_host, uint8_t* mask_host, int32_t* labels_host) {
+  if (B * H * W > 0 && !labels_host) return set_error(SN_EINVAL, "NULL label buffer");
+  return host_pipeline<double>(plan, disp_host, B, H, W, rig, offsets_xy, n_off, t, out6_host,
+                               mask_host, labels_host);
 }
 
 }  // extern "C"

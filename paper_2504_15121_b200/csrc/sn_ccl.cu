@@ -54,16 +54,6 @@ constexpr int kBands = kLTH / 2;      // 2-row bands per tile
 constexpr int kLThreads = kBands * kLWords;  // 256: one thread per (band, word)
 constexpr int kSlots = kBands * kLTW;  // node slots: band * 128 + column of a band-run start
 
-__device__ __forceinline__ double depth_of(float d, double fxb) {
-  // NaN marks an invalid depth sample
-  double z = __longlong_as_double(0x7ff8000000000000ll);
-  if (d > 0.0f && d <= FLT_MAX) {
-    const double q = __ddiv_rn(fxb, (double)d);
-    if (fabs(q) <= DBL_MAX) z = q;
-  }
-  return z;
-}
-
 __device__ __forceinline__ double edge_value(double c, double l, double r, double u, double dn) {
   return fabs(__dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(__dmul_rn(4.0, c), l), r), u), dn));
 }
@@ -73,22 +63,23 @@ __device__ __forceinline__ bool valid_z(double z) { return z == z; }
 // ---------------------------------------------------------------------------
 // standalone predicate (API sn_passable; exact fp64 per pixel, optional edges)
 
-__global__ void passable_kernel(const float* __restrict__ disp, const CclParams p,
+template <typename T>
+__global__ void passable_kernel(const T* __restrict__ disp, const CclParams p,
                                 uint8_t* __restrict__ pas, double* __restrict__ edges) {
   const int64_t total = p.B * p.H * p.W;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t x = idx % p.W;
     const int64_t y = (idx / p.W) % p.H;
-    const float* f = disp + (idx - y * p.W - x);
+    const T* f = disp + (idx - y * p.W - x);
     bool ok = false;
     double e = __longlong_as_double(0x7ff8000000000000ll);
     if (x >= 1 && x + 1 < p.W && y >= 1 && y + 1 < p.H) {
-      const double c = depth_of(f[y * p.W + x], p.fxb);
-      const double l = depth_of(f[y * p.W + x - 1], p.fxb);
-      const double r = depth_of(f[y * p.W + x + 1], p.fxb);
-      const double u = depth_of(f[(y - 1) * p.W + x], p.fxb);
-      const double dn = depth_of(f[(y + 1) * p.W + x], p.fxb);
+      const double c = pred_depth(f[y * p.W + x], p.fxb);
+      const double l = pred_depth(f[y * p.W + x - 1], p.fxb);
+      const double r = pred_depth(f[y * p.W + x + 1], p.fxb);
+      const double u = pred_depth(f[(y - 1) * p.W + x], p.fxb);
+      const double dn = pred_depth(f[(y + 1) * p.W + x], p.fxb);
       if (valid_z(c) && valid_z(l) && valid_z(r) && valid_z(u) && valid_z(dn)) {
         e = edge_value(c, l, r, u, dn);
         ok = true;
@@ -660,13 +651,18 @@ size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W) {
          align256((size_t)(tiles * kTilePx / 32) * 4);
 }
 
-int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, uint8_t* pas,
+template <typename T>
+int run_passable(const LaunchCtx& ctx, const T* disp, const CclParams& p, uint8_t* pas,
                  double* edges) {
   const int64_t n = p.B * p.H * p.W;
   if (n == 0) return SN_OK;
-  passable_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(disp, p, pas, edges);
+  passable_kernel<T><<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(disp, p, pas, edges);
   return check_launch("passable_kernel");
 }
+template int run_passable<float>(const LaunchCtx&, const float*, const CclParams&, uint8_t*,
+                                 double*);
+template int run_passable<double>(const LaunchCtx&, const double*, const CclParams&, uint8_t*,
+                                  double*);
 
 // ST-passable bit mask (adaptive.py:80-97,130-132) as a streaming kernel.
 // A warp owns 32 aligned columns x kPbRows rows of a frame, lane <-> column:
@@ -680,8 +676,9 @@ int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, ui
 // memory.
 constexpr int kPbRows = 16;
 
+template <typename T>
 __global__ void __launch_bounds__(256)
-    passable_bits_kernel(const float* __restrict__ disp, const FixedParams p,
+    passable_bits_kernel(const T* __restrict__ disp, const FixedParams p,
                          uint32_t* __restrict__ bits) {
   const int W = (int)p.W, H = (int)p.H, WW = p.bits_ww;
   const int lane = threadIdx.x & 31;
@@ -696,18 +693,19 @@ __global__ void __launch_bounds__(256)
     const unsigned f = rest / strips_y;
     const int y0 = (int)(rest - f * strips_y) * kPbRows;
     const int x = wc * 32 + lane;
-    const float* fr = disp + (int64_t)f * p.H * p.W;
+    const T* fr = disp + (int64_t)f * p.H * p.W;
     // depths of this column, rows y0-1 .. y0+kPbRows (NaN outside the frame)
     float z[kPbRows + 2];
     if (y0 >= 1 && y0 + kPbRows < H && wc * 32 + 32 <= W) {
-      const float* src = fr + (y0 - 1) * W + x;  // frame offsets fit int32 (host-checked)
+      const T* src = fr + (y0 - 1) * W + x;  // frame offsets fit int32 (host-checked)
 #pragma unroll
-      for (int k = 0; k < kPbRows + 2; ++k) z[k] = __fmul_rn(p.fxb_f, rcp_ftz(__ldg(src + k * W)));
+      for (int k = 0; k < kPbRows + 2; ++k)
+        z[k] = __fmul_rn(p.fxb_f, rcp_ftz(disp_f32(__ldg(src + k * W))));
     } else {
 #pragma unroll
       for (int k = 0; k < kPbRows + 2; ++k) {
         const int y = y0 - 1 + k;
-        const float d = (x < W && y >= 0 && y < H) ? __ldg(fr + y * W + x) : nanf_;
+        const float d = (x < W && y >= 0 && y < H) ? disp_f32(__ldg(fr + y * W + x)) : nanf_;
         z[k] = __fmul_rn(p.fxb_f, rcp_ftz(d));
       }
     }
@@ -718,8 +716,8 @@ __global__ void __launch_bounds__(256)
       const int y = y0 + lane;
       if (lane < kPbRows && y < H) {
         const int xl = wc * 32 - 1, xr = wc * 32 + 32;
-        if (xl >= 0) el = __fmul_rn(p.fxb_f, rcp_ftz(__ldg(fr + y * W + xl)));
-        if (xr < W) er = __fmul_rn(p.fxb_f, rcp_ftz(__ldg(fr + y * W + xr)));
+        if (xl >= 0) el = __fmul_rn(p.fxb_f, rcp_ftz(disp_f32(__ldg(fr + y * W + xl))));
+        if (xr < W) er = __fmul_rn(p.fxb_f, rcp_ftz(disp_f32(__ldg(fr + y * W + xr))));
       }
     }
     // interior pixels only (the reference has no padding): rows 1 .. H-2, cols 1 .. W-2
@@ -783,7 +781,7 @@ __global__ void __launch_bounds__(256)
         if (wu == 0u) continue;
         bool pk = false;
         if ((wu >> lane) & 1u) {
-          const float* c = fr + (y0 + k) * W + x;
+          const T* c = fr + (y0 + k) * W + x;
           pk = pred_exact_d(c[0], c[-1], c[1], c[-W], c[W], p.fxb, p.t) != 0u;
         }
         const uint32_t fix = __ballot_sync(0xffffffffu, pk);
@@ -794,7 +792,8 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-int run_passable_bits(const LaunchCtx& ctx, const float* disp, const FixedParams& p,
+template <typename T>
+int run_passable_bits(const LaunchCtx& ctx, const T* disp, const FixedParams& p,
                       uint32_t* bits) {
   const int64_t n = p.B * ((p.H + kPbRows - 1) / kPbRows) * p.bits_ww * 32;
   if (n == 0) return SN_OK;
@@ -802,11 +801,16 @@ int run_passable_bits(const LaunchCtx& ctx, const float* disp, const FixedParams
     return set_error(SN_EINVAL, "frame or batch too large for the passable-bit kernel");
   int64_t g = (n + 255) / 256;
   if (g > (int64_t)ctx.num_sms * 64) g = (int64_t)ctx.num_sms * 64;
-  passable_bits_kernel<<<(unsigned)g, 256, 0, ctx.stream>>>(disp, p, bits);
+  passable_bits_kernel<T><<<(unsigned)g, 256, 0, ctx.stream>>>(disp, p, bits);
   return check_launch("passable_bits_kernel");
 }
+template int run_passable_bits<float>(const LaunchCtx&, const float*, const FixedParams&,
+                                      uint32_t*);
+template int run_passable_bits<double>(const LaunchCtx&, const double*, const FixedParams&,
+                                       uint32_t*);
 
-int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const CclParams& p,
+template <typename T>
+int run_ccl(const LaunchCtx& ctx, const T* disp, const uint8_t* pas, const CclParams& p,
             int64_t index_base, int32_t* labels, void* workspace, size_t ws_bytes,
             const uint32_t* bits_in) {
   const int64_t n = p.B * p.H * p.W;
@@ -850,15 +854,12 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
   q += align256((size_t)(tiles * kSlots) * 2);
   ws.flags = reinterpret_cast<uint32_t*>(q);
 
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(ccl_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kTileSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(ccl_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kTileSmem) != cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(ccl_tile_kernel)");
-    attr_set = true;
-  }
+  int rc = ensure_dyn_smem(reinterpret_cast<const void*>(ccl_tile_kernel<1>), (int)kTileSmem,
+                           ctx.device, "ccl_tile_kernel<1>");
+  if (!rc)
+    rc = ensure_dyn_smem(reinterpret_cast<const void*>(ccl_tile_kernel<2>), (int)kTileSmem,
+                         ctx.device, "ccl_tile_kernel<2>");
+  if (rc) return rc;
   if (disp) {
     // predicate from fp32 disparity: the streaming bit-mask kernel first
     FixedParams fp{};
@@ -868,7 +869,7 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
     fp.fxb = p.fxb;
     fp.fxb_f = (float)p.fxb;
     fill_predicate(fp, p.fxb, p.t, ws.bits);
-    const int rc0 = run_passable_bits(ctx, disp, fp, ws.bits);
+    const int rc0 = run_passable_bits<T>(ctx, disp, fp, ws.bits);
     if (rc0) return rc0;
     bits_in = ws.bits;
   }
@@ -878,7 +879,7 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
     ccl_tile_kernel<2><<<grid, kLThreads, kTileSmem, ctx.stream>>>(nullptr, p, ws, labels);
   else
     ccl_tile_kernel<1><<<grid, kLThreads, kTileSmem, ctx.stream>>>(pas, p, ws, labels);
-  int rc = check_launch("ccl_tile_kernel");
+  rc = check_launch("ccl_tile_kernel");
   if (rc) return rc;
   const int64_t seam_blocks =
       (int64_t)(ws.n_ty - 1) * ((p.W + kSeamThreads - 1) / kSeamThreads) +
@@ -896,6 +897,10 @@ int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* pas, const C
   }
   return rc;
 }
+template int run_ccl<float>(const LaunchCtx&, const float*, const uint8_t*, const CclParams&,
+                            int64_t, int32_t*, void*, size_t, const uint32_t*);
+template int run_ccl<double>(const LaunchCtx&, const double*, const uint8_t*, const CclParams&,
+                             int64_t, int32_t*, void*, size_t, const uint32_t*);
 
 int run_relabel(const LaunchCtx& ctx, int32_t* labels, int64_t n, int64_t base,
                 const int32_t* keys, const int32_t* vals, const int32_t* n_map, int32_t cap,

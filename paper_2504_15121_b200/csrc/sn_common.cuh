@@ -104,73 +104,45 @@ static __device__ __noinline__ uint32_t pred_exact_d(float a, float b, float c, 
   return ev <= t ? 1u : 0u;
 }
 
-// fp32 filter on depths (z-form).  zf = fl(fxb_f * rcp.approx(d)) has
-// relative error <= 2^-24 (fxb_f) + 2^-23 (rcp.approx, 1 ulp) + 2^-24
+// fp64 disparities (the reference's own ScalarField values, fields.py:37-40):
+// the same predicate on the unrounded samples
+__device__ __forceinline__ double pred_depth(double d, double fxb) {
+  double z = __longlong_as_double(0x7ff8000000000000ll);
+  if (d > 0.0 && d <= 1.7976931348623157e308) {
+    const double q = __ddiv_rn(fxb, d);
+    if (fabs(q) <= 1.7976931348623157e308) z = q;
+  }
+  return z;
+}
+
+static __device__ __noinline__ uint32_t pred_exact_d(double a, double b, double c, double e,
+                                                     double f, double fxb, double t) {
+  const double zc = pred_depth(a, fxb), zl = pred_depth(b, fxb), zr = pred_depth(c, fxb),
+               zu = pred_depth(e, fxb), zd = pred_depth(f, fxb);
+  if (!(zc == zc && zl == zl && zr == zr && zu == zu && zd == zd)) return 0u;
+  const double ev =
+      fabs(__dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(__dmul_rn(4.0, zc), zl), zr), zu), zd));
+  return ev <= t ? 1u : 0u;
+}
+
+// fp32 view of a disparity sample for the predicate filters.  For fp64
+// samples the extra rounding adds 2^-24 to the depth's relative error (the
+// filter bound below grows from 2^-21 S to 0.5625 * 2^-20 S, still inside its
+// 2^-20 S margin); samples outside fp32's normal range become 0 or inf and
+// force the exact path.
+__device__ __forceinline__ float disp_f32(float d) { return d; }
+__device__ __forceinline__ float disp_f32(double d) { return __double2float_rn(d); }
+
+// fp32 filter on depths (passable_bits_kernel).  zf = fl(fxb_f * rcp.approx(d))
+// has relative error <= 2^-24 (fxb_f) + 2^-23 (rcp.approx, 1 ulp) + 2^-24
 // (product) = 2^-22 while zf stays a normal float.  With S = 4c + l + r + u + dn
 // (all depths > 0) the fp32 edge value is within 2^-22 S (inputs) + 4 * 2^-24 S
 // (four roundings of partial sums bounded by S) = 2^-21 S of the exact one, the
 // fp64 edge value within 2^-50 S, and t_f = fl(t) within 2^-24 t.  So when
 // |e32 - t_f| > 2^-20 S_f + 2^-21 t_f (twice the bound) both agree on e <= t;
 // otherwise the pixel takes pred_exact_d.  Invalid samples (non-finite or
-// <= 0) are NaN; samples whose zf would leave [1e-30, 1e30] are +inf and force
-// the exact path.  Valid for fx*b and t in [2^-40, 2^40] (host-checked).
-__device__ __forceinline__ float zfast(float d, float fxb_f) {
-  if (!(d > 0.0f && d <= 3.402823466e38f)) return __int_as_float(0x7fc00000);
-  float r;
-  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(d));
-  const float z = __fmul_rn(fxb_f, r);
-  return (z >= 1e-30f && z <= 1e30f) ? z : __int_as_float(0x7f800000);
-}
-
-// 0 = not passable, 1 = passable, 2 = undecided (exact path)
-__device__ __forceinline__ uint32_t zpred(float c, float l, float r, float u, float dn, float t_f) {
-  if (!(c == c && l == l && r == r && u == u && dn == dn)) return 0u;
-  const float c4 = __fmul_rn(4.0f, c);
-  const float S = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(c4, l), r), u), dn);
-  if (!(S <= 1e30f)) return 2u;  // an out-of-range sample
-  const float e = fabsf(__fsub_rn(__fsub_rn(__fsub_rn(__fsub_rn(c4, l), r), u), dn));
-  const float margin = __fadd_rn(__fmul_rn(S, 9.5367431640625e-07f /* 2^-20 */),
-                                 __fmul_rn(t_f, 4.76837158203125e-07f /* 2^-21 */));
-  const float gap = __fsub_rn(e, t_f);
-  return gap > margin ? 0u : (-gap > margin ? 1u : 2u);
-}
-
-// fp32 filter without divisions (used where depths are not at hand).  With
-// every d in [2^-8, 2^16] and K = fx*b:
-//   e = K |4/a - 1/b - 1/c - 1/e - 1/f| = K |N| / D,
-//   N = 4 bcef - a Q,  Q = ef (b + c) + bc (e + f),  D = a bcef > 0,
-// so e <= t  <=>  K |N| <= t D.  In fp32 (u = 2^-24) |N32 - N| <= 6u M with
-// M = 4 bcef + a Q, so |K32 |N32| - K |N|| <= 8u K M and |t32 D32 - t D| <=
-// 6u t D, while the fp64 evaluation of e is within 2^-50 K M / D of the real
-// value; so when |K32 |N32| - t32 D32| > 2^-20 (K32 M32 + t32 D32) -- twice the
-// bound -- the fp32 comparison equals the fp64 one.  The ranges keep every
-// product a normal float (K and t in [2^-40, 2^40], host-checked).
-// Returns 0 / 1 (decided) or 2 (out-of-range sample or inside the margin:
-// the caller evaluates pred_exact_d).
-__device__ __forceinline__ uint32_t pred_fast(float a, float b, float c, float e, float f,
-                                              const FixedParams& p) {
-  const uint32_t lo = 0x3b800000u, span = 0x47800000u - 0x3b800000u;  // [2^-8, 2^16)
-  const bool fast = ((__float_as_uint(a) - lo) < span) & ((__float_as_uint(b) - lo) < span) &
-                    ((__float_as_uint(c) - lo) < span) & ((__float_as_uint(e) - lo) < span) &
-                    ((__float_as_uint(f) - lo) < span);
-  if (!fast) return 2u;
-  const float bc = __fmul_rn(b, c), ef = __fmul_rn(e, f);
-  const float bcef = __fmul_rn(bc, ef);
-  const float Q = __fadd_rn(__fmul_rn(ef, __fadd_rn(b, c)), __fmul_rn(bc, __fadd_rn(e, f)));
-  const float m4 = __fmul_rn(4.0f, bcef), aQ = __fmul_rn(a, Q);
-  const float X = __fmul_rn(p.fxb_pf, fabsf(__fsub_rn(m4, aQ)));
-  const float Y = __fmul_rn(p.t_f, __fmul_rn(a, bcef));
-  const float margin =
-      __fmul_rn(__fadd_rn(__fmul_rn(p.fxb_pf, __fadd_rn(m4, aQ)), Y), 9.5367431640625e-07f);
-  const float gap = __fsub_rn(X, Y);
-  return gap > margin ? 0u : (-gap > margin ? 1u : 2u);
-}
-
-__device__ __forceinline__ uint32_t pred_bit(float a, float b, float c, float e, float f,
-                                             const FixedParams& p) {
-  const uint32_t r = p.pred_exact ? 2u : pred_fast(a, b, c, e, f, p);
-  return r != 2u ? r : pred_exact_d(a, b, c, e, f, p.fxb, p.t);
-}
+// <= 0) and depths outside [2^-100, 2^100] force the exact path.  Valid for
+// fx*b and t in [2^-40, 2^40] (host-checked, fill_predicate).
 
 // ---------------------------------------------------------------------------
 // PTX wrappers (sm_90+ async proxy; all used on sm_100a)

@@ -30,9 +30,7 @@
 // (pitch 3072 + 16 B: conflict-free float4 writes from lanes that own
 // different rows) and leaves as one contiguous 3 KB bulk copy
 // (cp.async.bulk) per output row, 16 per item, so HBM sees full-line writes
-// only.  Persistent grid, two CTAs per SM.  (The warp-specialised pipe
-// kernel keeps the earlier layout: 24 TMA tensor stores of 128B-swizzled
-// boxes.)
+// only.  Persistent grid, two CTAs per SM.
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -40,31 +38,21 @@
 
 #include <algorithm>
 #include <mutex>
-#include <stdlib.h>
 
 #include "sn_common.cuh"
 #include "sn_internal.h"
 
 namespace sn {
 
-#ifndef SN_EXP
-#define SN_EXP 0
-#endif
-
 constexpr int kTW = 128;           // output columns per item
 constexpr int kG = 16;             // output rows per item
 constexpr int kCP = kG + 1;        // pitch of the column-major C/Rr/Dc arrays (odd)
-constexpr int kBoxF = 32;          // floats per TMA store box row (128 B)
-constexpr int kBoxes = kTW * 6 / kBoxF;  // 24
 constexpr int kHalfUnits = 160;    // pass-V units per half: 5 warps, 32-column aligned
 constexpr int kFastThreads = 2 * kHalfUnits;  // 10 warps; pass H uses the first 8
 constexpr int kRun = 8;            // output columns per pass-H lane
-constexpr int kStoreTid = 8 * 32;  // warp 8 issues the output TMA stores
+constexpr int kStoreTid = 8 * 32;  // warp 8 issues the output bulk stores
 constexpr uint32_t kBigBits = 0x53800000u;  // fp32 bit pattern of 2^40
-#ifndef SN_ROWBULK
-#define SN_ROWBULK 1
-#endif
-// row-major staging for the classic kernel: one output row of an item (128
+// row-major staging: one output row of an item (128
 // records, 3072 B) per bulk copy; the 16-B pad makes the pitch 4 banks off,
 // so the 8 lanes (= 8 rows) of each quarter-warp phase of pass H's 16-byte
 // stores hit distinct banks
@@ -87,42 +75,23 @@ struct FastCfg {
   static constexpr int AE = 16 / (int)sizeof(T);
   // the box starts at (x0 - R) rounded down to 16 B, so it spans up to AE-1 extra columns
   static constexpr int BW = (NC + AE - 1 + AE - 1) / AE * AE;
-  static constexpr size_t STAGE_BYTES = SN_ROWBULK ? kRowStageBytes : (size_t)kBoxes * kG * 128;
+  static constexpr size_t STAGE_BYTES = kRowStageBytes;
   static constexpr size_t IN_BYTES = (size_t)NR * BW * sizeof(T);
   static constexpr size_t CS_BYTES = (size_t)NC * kCP * sizeof(AccPair<T>);  // (C, Rr) [NC][kCP]
   // column flags (NC words) + 8-column block ORs of them (NB words)
   static constexpr int NB = (NC + 7) / 8;
   static constexpr size_t FL_BYTES = align_up((size_t)(NC + NB) * 4, 16);
-  // single-CTA-pipeline layout (classic kernel: 1 stage, 2 inputs, 1 CR)
+  // shared-memory layout: 1 staging tile, 2 input tiles, 1 (C, Rr) array
   static constexpr size_t STAGE = 0;
   static constexpr size_t IN0 = STAGE + STAGE_BYTES;
   static constexpr size_t IN1 = align_up(IN0 + IN_BYTES, 128);
   static constexpr size_t CS = align_up(IN1 + IN_BYTES, 128);
   static constexpr size_t FL = align_up(CS + CS_BYTES, 16);
   static constexpr size_t BAR = align_up(FL + FL_BYTES, 16);
-  // + slack for the base alignment (1024 B for the 128B-swizzled boxes)
-  static constexpr size_t TOTAL = BAR + 16 + (SN_ROWBULK ? 128 : 1024);
+  // + slack for the 128-B base alignment
+  static constexpr size_t TOTAL = BAR + 16 + 128;
   static_assert(NC <= kHalfUnits, "pass V: one unit per thread");
   static_assert(NR <= 32, "row validity bits must fit 32 bits");
-};
-
-// warp-specialised pipeline layout: 2 staging tiles, 3 input tiles, 2 x (CR,
-// flags), 14 mbarriers
-template <int R>
-struct PipeCfg {
-  using C = FastCfg<R, float>;
-  static constexpr int kIn = 3, kCr = 2, kSt = 2;
-  static constexpr size_t STAGE = 0;
-  static constexpr size_t SB = (size_t)kBoxes * kG * 128;  // swizzled boxes
-  static constexpr size_t IN = STAGE + kSt * SB;
-  static constexpr size_t IN_STRIDE = align_up(C::IN_BYTES, 128);
-  static constexpr size_t CS = IN + kIn * IN_STRIDE;
-  static constexpr size_t CS_STRIDE = align_up(C::CS_BYTES, 128);
-  static constexpr size_t FL = CS + kCr * CS_STRIDE;
-  static constexpr size_t BAR = align_up(FL + kCr * C::FL_BYTES, 16);
-  static constexpr int kBars = kIn * 2 + kCr * 2 + kSt * 2;
-  static constexpr size_t TOTAL = BAR + kBars * 8 + 1024;
-  static constexpr bool fits = TOTAL <= 227 * 1024;
 };
 
 template <typename T>
@@ -380,13 +349,9 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
 //           ballot per row.
 //   pass H  8 warps, lane <-> (output row, run of 8 columns): U, V as a
 //           sliding chain, closed-form normal + point (packed f32x2), 6 floats
-//           per pixel into the staging tile, bulk row stores (the pipe
-//           kernel: 128B-swizzled boxes, TMA tensor stores).
-// Two kernels share the passes: fixed_square_kernel (2 CTAs/SM, passes
-// separated by CTA barriers, any R <= 8, fp32/fp64) and
-// fixed_square_pipe_kernel (1 CTA/SM, warp-specialised: pass V of item i+1,
-// pass H of item i and the TMA traffic of other items run concurrently,
-// synchronised by mbarriers; fp32, R <= 4).
+//           per pixel into the staging tile, bulk row stores.
+// fixed_square_kernel runs the passes (2 CTAs/SM, separated by CTA barriers,
+// any R <= 8, fp32/fp64/PNG16 input).
 
 struct ItemDecoder {
   int tiles_x, tiles_y;
@@ -579,9 +544,9 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   if ((c & 7) == 0 && (c >> 3) < Cfg::NB) reinterpret_cast<uint16_t*>(fl + NC + (c >> 3))[h] = (uint16_t)f16;
 }
 
-// pass H + epilogue for lane hl (< 256) of one item.  ROWS: row-major padded
-// staging (kRowPitch), else 24 128B-swizzled TMA boxes
-template <int R, typename T, bool ROWS = false>
+// pass H + epilogue for lane hl (< 256) of one item; records into the
+// row-major padded staging tile (kRowPitch)
+template <int R, typename T>
 __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int y0, int bz, int H,
                                        int W, const AccPair<T>* CR, const uint32_t* fl,
                                        uint32_t stage_base, const FixedParams& p,
@@ -626,23 +591,9 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   const float dv_f = ((float)yv - p.v0_hi) - p.v0_lo;
   const float du_hi = (float)xb - p.u0_hi;  // exact; + j stays exact
   const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
-  const uint32_t gsw = (uint32_t)(g & 7);
-  const uint32_t rowaddr = stage_base + (uint32_t)g * 128u;
-  // staging address of chunk c (0..11, 16 B) of this run: row chunk
-  // kk = 12q + c lives in box kk >> 3 at swizzled slot (kk & 7) ^ (g & 7).
-  // With 12q = 8(q + q/2) + P, P = 4(q & 1): kk & 7 = (c & 7) ^ P and
-  // kk >> 3 = q + q/2 + (c >> 3) + [P != 0 and c & 4], so with c known at
-  // compile time an address is one register pick, one XOR and one add
-  static_assert(kRun == 8, "staging address identity assumes 12 chunks per run");
-  const uint32_t stg_x = ((uint32_t)(4 * (q & 1)) ^ gsw) << 4;
-  const uint32_t stg_a0 = rowaddr + (uint32_t)(q + (q >> 1)) * (uint32_t)(kG * 128);
-  const uint32_t stg_a1 = stg_a0 + ((q & 1) ? (uint32_t)(kG * 128) : 0u);
+  // staging address of chunk c (0..11, 16 B) of this run: row g, 192 B per run
   const uint32_t row_a = stage_base + (uint32_t)g * (uint32_t)kRowPitch + (uint32_t)q * 192u;
-  auto stg_addr = [&](int c) {
-    if constexpr (ROWS) return row_a + (uint32_t)c * 16u;
-    return ((c & 4) ? stg_a1 : stg_a0) + (uint32_t)(c >> 3) * (uint32_t)(kG * 128) +
-           (((uint32_t)(c & 7) << 4) ^ stg_x);
-  };
+  auto stg_addr = [&](int c) { return row_a + (uint32_t)c * 16u; };
 
   // sliding sums first (short dependent chain), then independent epilogues
   A Us[kRun], Vs[kRun];
@@ -753,19 +704,17 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
 
 template <int R, typename T>
 __global__ void __launch_bounds__(kFastThreads, 2)
-    fixed_square_kernel(const __grid_constant__ CUtensorMap in_map,
-                        const __grid_constant__ CUtensorMap out_map, const FixedParams p,
+    fixed_square_kernel(const __grid_constant__ CUtensorMap in_map, const FixedParams p,
                         uint8_t* __restrict__ mask_out, float* __restrict__ out6,
                         const int64_t out_pitch, const int n_items, const int tiles_x,
                         const int tiles_y) {
   using Cfg = FastCfg<R, T>;
   constexpr int NC = Cfg::NC, AE = Cfg::AE;
-  constexpr int kStoreLanes = SN_ROWBULK ? kG : kBoxes;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // aligned base (128 B for the row staging, 1024 B for swizzled boxes); offset
-  // arithmetic on the __shared__ array keeps the shared address space (LDS/STS,
-  // not generic LD/ST)
-  constexpr uint32_t kAlign = SN_ROWBULK ? 128u : 1024u;
+  constexpr int kStoreLanes = kG;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // 128-B aligned base; offset arithmetic on the __shared__ array keeps the
+  // shared address space (LDS/STS, not generic LD/ST)
+  constexpr uint32_t kAlign = 128u;
   uint8_t* smem = smem_raw + ((kAlign - (smem_u32(smem_raw) & (kAlign - 1u))) & (kAlign - 1u));
   AccPair<T>* CR = reinterpret_cast<AccPair<T>*>(smem + Cfg::CS);
   uint32_t* fl = reinterpret_cast<uint32_t*>(smem + Cfg::FL);
@@ -787,11 +736,10 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 
   if (tid == 0) {
     tma_prefetch_desc(&in_map);
-    tma_prefetch_desc(&out_map);
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
     fence_mbar_init();
-    if (SN_EXP != 5) load_tile(cur, 0);
+    load_tile(cur, 0);
   }
   __syncthreads();
 
@@ -801,168 +749,37 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 
   for (int it = 0; item < n_items; ++it, item += gridDim.x, cur = nxt, nxt.advance()) {
     const int buf = it & 1;
-    if (SN_EXP != 5 && tid == 0 && item + (int)gridDim.x < n_items) load_tile(nxt, buf ^ 1);
+    if (tid == 0 && item + (int)gridDim.x < n_items) load_tile(nxt, buf ^ 1);
     const int x0 = cur.x0(), y0 = cur.y0(), bz = cur.bz;
     const int sh = (x0 - R) - tile_x0<R, AE>(x0);  // logical column c <-> smem column c + sh
     const T* in = reinterpret_cast<const T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
-    if (SN_EXP != 5) mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
+    mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
-    // SN_EXP (experiment builds only, tools/exp_fused.sh; 0 in the product):
-    // 1 no stores, 2 no pass H, 3 no pass V, 4 neither pass, 5 stores only
-    // (no loads, no passes), 6 loads only
-    if (SN_EXP != 3 && SN_EXP < 4) pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
+    pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
     // staging of the previous item read out by its bulk stores (issued by warp 8)
     if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) bulk_wait_read0();
     __syncthreads();
 
-    if (SN_EXP != 2 && SN_EXP < 4)
-      if (tid < 256)
-        pass_h<R, T, SN_ROWBULK>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
+    if (tid < 256) pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
     fence_proxy_async_smem();
     __syncthreads();
     // output stores from a warp that is idle in pass H -- warp 0 goes
     // straight on to the next item
-    if (SN_EXP != 1 && SN_EXP != 6 && tid >= kStoreTid && tid < kStoreTid + kStoreLanes) {
+    if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) {
       const int b = tid - kStoreTid;
-      if constexpr (SN_ROWBULK) {
-        // one contiguous bulk copy per output row (3072 B, less at the right
-        // edge).  The pitch is even, so rows start 16-B aligned and a row
-        // ends on a 16-B multiple; an odd width writes into a pitched buffer
-        // (dispatch_square_staged), whose pad column takes the extra record
-        if (y0 + b < H) {
-          const int n = min(kTW, (int)out_pitch - x0);
-          bulk_store_1d(out6 + (((int64_t)bz * H + y0 + b) * out_pitch + x0) * 6,
-                        smem + Cfg::STAGE + (size_t)b * kRowPitch, (uint32_t)n * 24u);
-        }
-      } else {
-        tma_store_3d(&out_map, smem + Cfg::STAGE + (size_t)b * kG * 128, x0 * 6 + b * kBoxF, y0, bz);
+      // one contiguous bulk copy per output row (3072 B, less at the right
+      // edge).  The pitch is even, so rows start 16-B aligned and a row
+      // ends on a 16-B multiple; an odd width writes into a pitched buffer
+      // (dispatch_square_staged), whose pad column takes the extra record
+      if (y0 + b < H) {
+        const int n = min(kTW, (int)out_pitch - x0);
+        bulk_store_1d(out6 + (((int64_t)bz * H + y0 + b) * out_pitch + x0) * 6,
+                      smem + Cfg::STAGE + (size_t)b * kRowPitch, (uint32_t)n * 24u);
       }
       bulk_commit();
     }
   }
   if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) bulk_wait0();
-}
-
-// ---------------------------------------------------------------------------
-// warp-specialised pipeline: 1 CTA/SM, 19 warps
-//   warps 0-9    pass V of item i (writes CR/flags/ballots slot i % 2)
-//   warps 10-17  pass H of item i-1 (reads them, writes staging slot (i-1) % 2)
-//   warp 18      TMA: input loads two items ahead, output stores of item i-2
-// mbarriers (use n of a slot has parity n & 1; a producer's first wait on an
-// "empty" barrier passes at once):
-//   in_full[3]  tx-count of the input load      in_empty[3]  256 pass-H threads
-//   cr_full[2]  320 pass-V threads              cr_empty[2]  256 pass-H threads
-//   st_full[2]  256 pass-H threads              st_empty[2]  1 (warp 18 after read-out)
-
-constexpr int kPipeV = 10 * 32, kPipeH = 8 * 32, kPipeThreads = kPipeV + kPipeH + 32;
-
-template <int R>
-__global__ void __launch_bounds__(kPipeThreads, 1)
-    fixed_square_pipe_kernel(const __grid_constant__ CUtensorMap in_map,
-                             const __grid_constant__ CUtensorMap out_map, const FixedParams p,
-                             uint8_t* __restrict__ mask_out, const int n_items, const int tiles_x,
-                             const int tiles_y) {
-  using Cfg = FastCfg<R, float>;
-  using PC = PipeCfg<R>;
-  constexpr int NC = Cfg::NC, AE = Cfg::AE;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + PC::BAR);
-  uint64_t* in_full = bar;
-  uint64_t* in_empty = bar + PC::kIn;
-  uint64_t* cr_full = bar + 2 * PC::kIn;
-  uint64_t* cr_empty = cr_full + PC::kCr;
-  uint64_t* st_full = cr_empty + PC::kCr;
-  uint64_t* st_empty = st_full + PC::kSt;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int W = (int)p.W, H = (int)p.H;
-  const ItemDecoder decode(tiles_x, tiles_y);
-  auto in_tile = [&](int s) { return reinterpret_cast<float*>(smem + PC::IN + s * PC::IN_STRIDE); };
-  auto cr_slot = [&](int s) { return reinterpret_cast<double2*>(smem + PC::CS + s * PC::CS_STRIDE); };
-  auto fl_slot = [&](int s) { return reinterpret_cast<uint32_t*>(smem + PC::FL + s * Cfg::FL_BYTES); };
-  auto st_slot = [&](int s) { return smem + PC::STAGE + s * PC::SB; };
-
-  if (tid == 0) {
-    tma_prefetch_desc(&in_map);
-    tma_prefetch_desc(&out_map);
-    for (int i = 0; i < PC::kIn; ++i) {
-      mbar_init(in_full + i, 1);
-      mbar_init(in_empty + i, kPipeH);
-    }
-    for (int i = 0; i < PC::kCr; ++i) {
-      mbar_init(cr_full + i, kPipeV);
-      mbar_init(cr_empty + i, kPipeH);
-    }
-    for (int i = 0; i < PC::kSt; ++i) {
-      mbar_init(st_full + i, kPipeH);
-      mbar_init(st_empty + i, 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  // this CTA's items: blockIdx.x + n * gridDim.x, n = 0 .. n_mine - 1
-  const int n_mine = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  auto item_of = [&](int n) { return (int)blockIdx.x + n * (int)gridDim.x; };
-
-  if (tid < kPipeV) {
-    // ---------------------------------------------------------- pass V
-    const int h = tid >= kHalfUnits ? 1 : 0;
-    const int c = tid - h * kHalfUnits;
-    const bool unit = c < NC;
-    for (int n = 0; n < n_mine; ++n) {
-      int x0, y0, bz;
-      decode(item_of(n), x0, y0, bz);
-      const int si = n % PC::kIn, ci = n % PC::kCr;
-      mbar_wait(in_full + si, (uint32_t)(n / PC::kIn) & 1u);
-      mbar_wait(cr_empty + ci, ((uint32_t)(n / PC::kCr) & 1u) ^ 1u);
-      pass_v<R, float>(in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, H, W, h, c, unit,
-                       cr_slot(ci), fl_slot(ci), p);
-      mbar_arrive(cr_full + ci);
-    }
-  } else if (tid < kPipeV + kPipeH) {
-    // ---------------------------------------------------------- pass H
-    const int hl = tid - kPipeV;
-    for (int n = 0; n < n_mine; ++n) {
-      int x0, y0, bz;
-      decode(item_of(n), x0, y0, bz);
-      const int si = n % PC::kIn, ci = n % PC::kCr, ss = n % PC::kSt;
-      mbar_wait(cr_full + ci, (uint32_t)(n / PC::kCr) & 1u);
-      mbar_wait(st_empty + ss, ((uint32_t)(n / PC::kSt) & 1u) ^ 1u);
-      pass_h<R, float>(hl, in_tile(si), (x0 - R) - tile_x0<R, AE>(x0), x0, y0, bz, H, W,
-                       cr_slot(ci), fl_slot(ci), smem_u32(st_slot(ss)), p, mask_out);
-      fence_proxy_async_smem();
-      mbar_arrive(st_full + ss);
-      mbar_arrive(cr_empty + ci);
-      mbar_arrive(in_empty + si);
-    }
-  } else {
-    // ---------------------------------------------------------- TMA warp
-    auto load = [&](int n) {
-      int x0, y0, bz;
-      decode(item_of(n), x0, y0, bz);
-      const int si = n % PC::kIn;
-      mbar_wait(in_empty + si, ((uint32_t)(n / PC::kIn) & 1u) ^ 1u);
-      mbar_arrive_expect_tx(in_full + si, (uint32_t)Cfg::IN_BYTES);
-      tma_load_3d(in_tile(si), &in_map, in_full + si, tile_x0<R, AE>(x0), y0 - R, bz);
-    };
-    if (lane == 0)
-      for (int n = 0; n < PC::kIn - 1 && n < n_mine; ++n) load(n);
-    for (int n = 0; n < n_mine; ++n) {
-      if (lane == 0 && n + PC::kIn - 1 < n_mine) load(n + PC::kIn - 1);
-      int x0, y0, bz;
-      decode(item_of(n), x0, y0, bz);
-      const int ss = n % PC::kSt;
-      mbar_wait(st_full + ss, (uint32_t)(n / PC::kSt) & 1u);
-      if (lane < kBoxes) {
-        tma_store_3d(&out_map, st_slot(ss) + (size_t)lane * kG * 128, x0 * 6 + lane * kBoxF, y0, bz);
-        bulk_commit();
-        bulk_wait_read0();
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(st_empty + ss);
-    }
-    if (lane < kBoxes) bulk_wait0();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1045,7 +862,7 @@ template <int R, typename T>
 static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams& p, float* out6,
                          uint8_t* mask, int64_t in_pitch, int64_t out_pitch) {
   using Cfg = FastCfg<R, T>;
-  CUtensorMap in_map, out_map;
+  CUtensorMap in_map;
   const CUtensorMapDataType dt =
       sizeof(T) == 4   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
       : sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
@@ -1060,49 +877,15 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != 0)
       return SN_ECUDA;
   }
-  {
-    cuuint64_t dims[3] = {(cuuint64_t)(p.W * 6), (cuuint64_t)p.H, (cuuint64_t)p.B};
-    cuuint64_t strides[2] = {(cuuint64_t)(out_pitch * 24), (cuuint64_t)(out_pitch * p.H * 24)};
-    cuuint32_t box[3] = {(cuuint32_t)kBoxF, (cuuint32_t)kG, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (encode_tiled(&out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)out6, dims, strides, box,
-                     es, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != 0)
-      return SN_ECUDA;
-  }
   const int tiles_x = (int)((p.W + kTW - 1) / kTW);
   const int tiles_y = (int)((p.H + kG - 1) / kG);
   const int64_t n_items64 = (int64_t)tiles_x * tiles_y * p.B;
   if (n_items64 >= 0x7fffffffLL) return -1;  // generic path handles absurd batches
   const int n_items = (int)n_items64;
-  if constexpr (sizeof(T) == 4 && R <= 4) {
-    // warp-specialised pipeline, opt-in (SN_FUSED_PIPE=1): measured 14.6 vs
-    // 13.8 us/frame for the classic kernel at C3 -- the passes are not
-    // barrier-bound but latency-bound at ~20 resident warps either way
-    static const bool pipe = getenv("SN_FUSED_PIPE") != nullptr;
-    if (pipe && PipeCfg<R>::fits) {
-      auto kern = fixed_square_pipe_kernel<R>;
-      static bool attr_set = false;
-      if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)PipeCfg<R>::TOTAL) != cudaSuccess)
-          return set_cuda_error("cudaFuncSetAttribute(fixed_square_pipe_kernel)");
-        attr_set = true;
-      }
-      int64_t grid = ctx.num_sms;
-      if (grid > n_items) grid = n_items;
-      kern<<<(unsigned)grid, kPipeThreads, PipeCfg<R>::TOTAL, ctx.stream>>>(
-          in_map, out_map, p, mask, n_items, tiles_x, tiles_y);
-      return check_launch("fixed_square_pipe_kernel");
-    }
-  }
   auto kern = fixed_square_kernel<R, T>;
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::TOTAL) !=
-        cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(fixed_square_kernel)");
-    attr_set = true;
-  }
+  if (ensure_dyn_smem(reinterpret_cast<const void*>(kern), (int)Cfg::TOTAL, ctx.device,
+                      "fixed_square_kernel"))
+    return SN_ECUDA;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFastThreads, Cfg::TOTAL) !=
       cudaSuccess)
@@ -1110,9 +893,8 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * ctx.num_sms;
   if (grid > n_items) grid = n_items;
-  kern<<<(unsigned)grid, kFastThreads, Cfg::TOTAL, ctx.stream>>>(in_map, out_map, p, mask, out6,
-                                                                 out_pitch, n_items, tiles_x,
-                                                                 tiles_y);
+  kern<<<(unsigned)grid, kFastThreads, Cfg::TOTAL, ctx.stream>>>(in_map, p, mask, out6, out_pitch,
+                                                                 n_items, tiles_x, tiles_y);
   return check_launch("fixed_square_kernel");
 }
 
@@ -1168,8 +950,9 @@ static int pitch_copy(const LaunchCtx& ctx, const void* src, int64_t sp_bytes, v
 // The fast kernel on widths (or pointers) TMA cannot address directly: the
 // disparities are copied into a row-pitched buffer (pitch rounded up to 16
 // bytes; +8 B/px of traffic), and for odd widths the records go through a
-// pitched buffer too (+48 B/px).  Stream-ordered allocations, so concurrent
-// calls on different streams do not share scratch.  Returns -1 to fall back
+// pitched buffer too (+48 B/px).  Stream-ordered allocations from the
+// library's private pool (scratch_alloc), so concurrent calls on different
+// streams do not share scratch.  Returns -1 to fall back
 // to the generic kernel if the scratch cannot be had.
 template <typename T>
 static int dispatch_square_staged(int R, const LaunchCtx& ctx, const T* disp, const FixedParams& p,
@@ -1177,33 +960,13 @@ static int dispatch_square_staged(int R, const LaunchCtx& ctx, const T* disp, co
   constexpr int64_t AE = 16 / (int64_t)sizeof(T);
   const int64_t Wp = (p.W + AE - 1) / AE * AE;  // even (AE >= 2)
   const bool out_direct = p.W % 2 == 0 && reinterpret_cast<uintptr_t>(out6) % 16 == 0;
-  // keep the stream-ordered pool's memory between calls (the default release
-  // threshold returns it to the driver at every synchronisation)
-  static std::mutex pool_mu;
-  static bool pool_kept[64] = {};
-  if (ctx.device >= 0 && ctx.device < 64) {
-    std::lock_guard<std::mutex> lock(pool_mu);
-    if (!pool_kept[ctx.device]) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, ctx.device) == cudaSuccess) {
-        uint64_t keep = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-      pool_kept[ctx.device] = true;
-    }
-  }
   T* in_tmp = nullptr;
   float* out_tmp = nullptr;
   const size_t in_bytes = (size_t)(p.B * p.H * Wp) * sizeof(T);
   const size_t out_bytes = out_direct ? 0 : (size_t)(p.B * p.H * Wp) * 24;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&in_tmp), in_bytes, ctx.stream) != cudaSuccess) {
-    cudaGetLastError();
-    return -1;
-  }
-  if (!out_direct &&
-      cudaMallocAsync(reinterpret_cast<void**>(&out_tmp), out_bytes, ctx.stream) != cudaSuccess) {
-    cudaGetLastError();
-    cudaFreeAsync(in_tmp, ctx.stream);
+  if (scratch_alloc(ctx, in_bytes, reinterpret_cast<void**>(&in_tmp)) != SN_OK) return -1;
+  if (!out_direct && scratch_alloc(ctx, out_bytes, reinterpret_cast<void**>(&out_tmp)) != SN_OK) {
+    scratch_free(ctx, in_tmp);
     return -1;
   }
   int rc = pitch_copy(ctx, disp, p.W * (int64_t)sizeof(T), in_tmp, Wp * (int64_t)sizeof(T),
@@ -1213,8 +976,8 @@ static int dispatch_square_staged(int R, const LaunchCtx& ctx, const T* disp, co
                             out_direct ? p.W : Wp);
   if (rc == SN_OK && !out_direct)
     rc = pitch_copy(ctx, out_tmp, Wp * 24, out6, p.W * 24, p.W * 24, p.B * p.H);
-  cudaFreeAsync(in_tmp, ctx.stream);
-  if (out_tmp) cudaFreeAsync(out_tmp, ctx.stream);
+  scratch_free(ctx, in_tmp);
+  if (out_tmp) scratch_free(ctx, out_tmp);
   return rc;
 }
 
@@ -1250,13 +1013,13 @@ int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const s
     int rc = aligned ? dispatch_square<T>(m.square_r, ctx, disp, p, out6, mask)
                      : dispatch_square_staged<T>(m.square_r, ctx, disp, p, out6, mask);
     if (rc == SN_OK && p.bits != nullptr) {
-      if constexpr (sizeof(T) == 4) rc = run_passable_bits(ctx, disp, p, p.bits);
+      if constexpr (sizeof(T) >= 4) rc = run_passable_bits<T>(ctx, disp, p, p.bits);
     }
     if (rc >= 0) return rc;
   }
   int rc = launch_generic<T>(ctx, disp, p, tab, out6, mask, a1, a2, affine);
   if (rc == SN_OK && !affine && p.bits != nullptr) {
-    if constexpr (sizeof(T) == 4) rc = run_passable_bits(ctx, disp, p, p.bits);
+    if constexpr (sizeof(T) >= 4) rc = run_passable_bits<T>(ctx, disp, p, p.bits);
   }
   return rc;
 }

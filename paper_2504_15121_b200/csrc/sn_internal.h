@@ -20,6 +20,12 @@ struct LaunchCtx {
 int set_error(int code, const char* fmt, ...);
 int set_cuda_error(const char* what);
 int check_launch(const char* what);
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device: set once per
+// (kernel, device) pair, under a lock (the caller has made `device` current)
+int ensure_dyn_smem(const void* func, int bytes, int device, const char* name);
+// stream-ordered scratch from the library's private per-device pool
+int scratch_alloc(const LaunchCtx& ctx, size_t bytes, void** ptr);
+void scratch_free(const LaunchCtx& ctx, void* ptr);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 int encode_tiled(CUtensorMap* map, CUtensorMapDataType dt, int rank, void* gaddr,
@@ -50,12 +56,16 @@ struct CclParams {
 CclParams make_ccl_params(int64_t B, int64_t H, int64_t W, double fxb, double t);
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W);
 
-int run_passable(const LaunchCtx& ctx, const float* disp, const CclParams& p, uint8_t* passable,
+// T = float or double disparities (explicit instantiations in sn_ccl.cu)
+template <typename T>
+int run_passable(const LaunchCtx& ctx, const T* disp, const CclParams& p, uint8_t* passable,
                  double* edges);
-int run_ccl(const LaunchCtx& ctx, const float* disp, const uint8_t* passable, const CclParams& p,
+template <typename T>
+int run_ccl(const LaunchCtx& ctx, const T* disp, const uint8_t* passable, const CclParams& p,
             int64_t index_base, int32_t* labels, void* workspace, size_t ws_bytes,
             const uint32_t* bits_in = nullptr);
-int run_passable_bits(const LaunchCtx& ctx, const float* disp, const FixedParams& p,
+template <typename T>
+int run_passable_bits(const LaunchCtx& ctx, const T* disp, const FixedParams& p,
                       uint32_t* bits);
 // host-side fill of the predicate fields of FixedParams
 void fill_predicate(FixedParams& p, double fxb, double t, uint32_t* bits);
@@ -86,7 +96,8 @@ struct AdaptiveParams {
   int shared_range;
 };
 size_t adaptive_workspace_bytes(int64_t B, int64_t H, int64_t W);
-int run_adaptive(const LaunchCtx& ctx, const float* disp, const AdaptiveParams& ap,
+template <typename T>
+int run_adaptive(const LaunchCtx& ctx, const T* disp, const AdaptiveParams& ap,
                  const StarTable& tab, int stop, float* out6, uint8_t* mask, void* workspace,
                  size_t ws_bytes);
 
@@ -108,6 +119,16 @@ int run_dequant_png16(const LaunchCtx& ctx, const uint16_t* raw, int64_t n, int 
                       double scale, float* out32, double* out64);
 int run_decode_pfm(const LaunchCtx& ctx, const void* payload, int64_t B, int64_t H, int64_t L,
                    bool big_endian, float* out);
+
+// element-wise geometry (sn_geometry.cu)
+template <typename T>
+int run_depth_map(const LaunchCtx& ctx, const T* disp, int64_t n, double fxb, double* z);
+int run_triangulate(const LaunchCtx& ctx, const double* u, const double* v, const double* d,
+                    int64_t n, const FixedParams& p, double* x, double* y, double* z);
+template <typename T>
+int run_triangulate_grid(const LaunchCtx& ctx, const T* disp, const FixedParams& p, double* xyz);
+int run_laplacian(const LaunchCtx& ctx, const double* z, const uint8_t* mask, int64_t B,
+                  int64_t H, int64_t W, double* e, uint8_t* ok);
 
 size_t cloud_workspace_bytes(int64_t B, int64_t H, int64_t W);
 int run_cloud_count(const LaunchCtx& ctx, const uint8_t* mask, int64_t B, int64_t H, int64_t W,

@@ -3,8 +3,9 @@
 Each function validates its tensors, takes the caller's current CUDA stream
 and calls the C ABI (include/sn_b200.h) asynchronously -- no host
 synchronisation, CUDA-graph capturable.  Shapes: disparity ``[B, H, W]`` (or
-``[H, W]``), fp32 (headline path) or fp64; outputs are allocated when not
-supplied.
+``[H, W]``), fp32 (headline path) or fp64 (the reference's own values: every
+entry point has an fp64 form, so decisions are made on the unrounded
+samples); outputs are allocated when not supplied.
 
 Reference functions these replace (pkg/src/stereonorm):
   oriented_points   estimate_normals_fixed kernels.py:237-261 +
@@ -46,6 +47,16 @@ def _batched(disp: torch.Tensor, name: str = "disparity") -> torch.Tensor:
     return disp.contiguous()
 
 
+def _disp_fn(d: torch.Tensor, name: str):
+    """The C-ABI function for ``d``'s dtype: ``name`` (fp32) or ``name_f64``."""
+    lib = _native.load()
+    if d.dtype == torch.float32:
+        return getattr(lib, name)
+    if d.dtype == torch.float64:
+        return getattr(lib, name + "_f64")
+    raise ValueError(f"disparity dtype must be float32 or float64, got {d.dtype}")
+
+
 def _stream(dev: torch.device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
@@ -68,7 +79,7 @@ def oriented_points(disparity: torch.Tensor, rig, kernels=9, *, out: torch.Tenso
     ``(x, y, z, nx, ny, nz)``; NaN normals where invalid, NaN points where
     the disparity is not finite and positive.  ``mask`` (uint8 ``[B, H, W]``)
     optionally receives the normal validity.  ``row0`` is the image row of
-    the first input row when the input is a strip of a taller image (fp32)."""
+    the first input row when the input is a strip of a taller image."""
     d = _batched(disparity)
     B, H, W = d.shape
     dev = d.device
@@ -88,11 +99,11 @@ def oriented_points(disparity: torch.Tensor, rig, kernels=9, *, out: torch.Tenso
     rs = _native.rig_struct(rig)
     mptr = mask.data_ptr() if mask is not None else None
     if row0:
-        if d.dtype != torch.float32 or generic:
-            raise ValueError("row0 is supported on the fp32 fast path only")
-        rc = lib.sn_oriented_points_rows(_native.plan(dev.index), d.data_ptr(), B, H, W, int(row0),
-                                         ctypes.byref(rs), off.ctypes.data, len(off),
-                                         out.data_ptr(), mptr, _stream(dev))
+        if generic:
+            raise ValueError("row0 is not supported by the generic test hook")
+        rc = _disp_fn(d, "sn_oriented_points_rows")(
+            _native.plan(dev.index), d.data_ptr(), B, H, W, int(row0), ctypes.byref(rs),
+            off.ctypes.data, len(off), out.data_ptr(), mptr, _stream(dev))
         check(rc, "oriented_points")
         return out
     rc = fn(_native.plan(dev.index), d.data_ptr(), B, H, W, ctypes.byref(rs), off.ctypes.data,
@@ -111,7 +122,7 @@ def oriented_points_bits(disparity: torch.Tensor, rig, kernels, threshold: float
     """Fused pass that also emits the ST-passable bit mask (same read of the
     disparity): returns (``[B, H, W, 6]`` fp32, ``[B, H, ceil(W/32)]`` int32
     bit words; bit ``u % 32`` of word ``u // 32`` = pixel ``u``)."""
-    d = _fp32(_batched(disparity))
+    d = _batched(disparity)
     B, H, W = d.shape
     dev = d.device
     out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
@@ -120,7 +131,7 @@ def oriented_points_bits(disparity: torch.Tensor, rig, kernels, threshold: float
     bits = _check_out(bits, (B, H, bit_words(W)), torch.int32, dev, "bits")
     off = _offsets_of(kernels)
     rs = _native.rig_struct(rig)
-    rc = _native.load().sn_oriented_points_bits(
+    rc = _disp_fn(d, "sn_oriented_points_bits")(
         _native.plan(dev.index), d.data_ptr(), B, H, W, int(row0), ctypes.byref(rs),
         off.ctypes.data, len(off), float(threshold), out.data_ptr(),
         mask.data_ptr() if mask is not None else None, bits.data_ptr(), _stream(dev))
@@ -130,12 +141,12 @@ def oriented_points_bits(disparity: torch.Tensor, rig, kernels, threshold: float
 
 def passable_bits(disparity: torch.Tensor, rig, threshold: float, *, bits=None) -> torch.Tensor:
     """ST-passable bit mask ``[B, H, ceil(W/32)]`` int32 (streaming kernel)."""
-    d = _fp32(_batched(disparity))
+    d = _batched(disparity)
     B, H, W = d.shape
     dev = d.device
     bits = _check_out(bits, (B, H, bit_words(W)), torch.int32, dev, "bits")
     rs = _native.rig_struct(rig)
-    rc = _native.load().sn_passable_bits(_native.plan(dev.index), d.data_ptr(), B, H, W,
+    rc = _disp_fn(d, "sn_passable_bits")(_native.plan(dev.index), d.data_ptr(), B, H, W,
                                          ctypes.byref(rs), float(threshold), bits.data_ptr(),
                                          _stream(dev))
     check(rc, "passable_bits")
@@ -165,7 +176,7 @@ def pipeline(disparity: torch.Tensor, rig, kernels, threshold: float, *, out=Non
     """The whole hot path in one call: fused fit + normal + point + passable
     bits, then component labels.  Returns (``[B, H, W, 6]`` fp32, ``[B, H, W]``
     int32 labels)."""
-    d = _fp32(_batched(disparity))
+    d = _batched(disparity)
     B, H, W = d.shape
     dev = d.device
     out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
@@ -175,7 +186,7 @@ def pipeline(disparity: torch.Tensor, rig, kernels, threshold: float, *, out=Non
     ws = _workspace(workspace, B, H, W, dev)
     off = _offsets_of(kernels)
     rs = _native.rig_struct(rig)
-    rc = _native.load().sn_pipeline_ws(
+    rc = _disp_fn(d, "sn_pipeline_ws")(
         _native.plan(dev.index), d.data_ptr(), B, H, W, ctypes.byref(rs), off.ctypes.data,
         len(off), float(threshold), out.data_ptr(), mask.data_ptr() if mask is not None else None,
         labels.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(), _stream(dev))
@@ -189,7 +200,7 @@ def adaptive_points(disparity: torch.Tensor, rig, config, *, out=None, mask=None
     records with normals over edge-aware star supports (``config`` a
     ``StarConfig``); ``mask`` (uint8) optionally receives the validity."""
     from .adaptive import ray_table
-    d = _fp32(_batched(disparity))
+    d = _batched(disparity)
     B, H, W = d.shape
     dev = d.device
     out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
@@ -204,7 +215,7 @@ def adaptive_points(disparity: torch.Tensor, rig, config, *, out=None, mask=None
         raise ValueError(f"workspace must hold >= {n.value} bytes on {dev}")
     lens, xy = ray_table(config)
     rs = _native.rig_struct(rig)
-    rc = lib.sn_adaptive_points(_native.plan(dev.index), d.data_ptr(), B, H, W, ctypes.byref(rs),
+    rc = _disp_fn(d, "sn_adaptive_points")(_native.plan(dev.index), d.data_ptr(), B, H, W, ctypes.byref(rs),
                                 len(lens), lens.ctypes.data, xy.ctypes.data,
                                 0 if config.stop == "st" else 1, int(bool(config.shared_range)),
                                 float(config.threshold), out.data_ptr(),
@@ -408,15 +419,9 @@ def affine(disparity: torch.Tensor, kernels, *, a1=None, a2=None, mask=None):
     return a1, a2, mask
 
 
-def _fp32(d: torch.Tensor) -> torch.Tensor:
-    if d.dtype != torch.float32:
-        raise ValueError(f"this entry point takes float32 disparities, got {d.dtype}")
-    return d
-
-
 def passable(disparity: torch.Tensor, rig, threshold: float, *, out=None, edges=None):
     """ST-passable set (uint8) and optionally the depth-Laplacian values."""
-    d = _fp32(_batched(disparity))
+    d = _batched(disparity)
     B, H, W = d.shape
     dev = d.device
     out = _check_out(out, (B, H, W), torch.uint8, dev, "out")
@@ -424,7 +429,7 @@ def passable(disparity: torch.Tensor, rig, threshold: float, *, out=None, edges=
     if want_edges:
         edges = _check_out(edges, (B, H, W), torch.float64, dev, "edges")
     rs = _native.rig_struct(rig)
-    rc = _native.load().sn_passable(_native.plan(dev.index), d.data_ptr(), B, H, W,
+    rc = _disp_fn(d, "sn_passable")(_native.plan(dev.index), d.data_ptr(), B, H, W,
                                     ctypes.byref(rs), float(threshold), out.data_ptr(),
                                     edges.data_ptr() if want_edges else None, _stream(dev))
     check(rc, "passable")
@@ -451,13 +456,13 @@ def component_labels(disparity: torch.Tensor, rig, threshold: float, *, out=None
     """8-connected labels of the ST-passable set: int32 ``[B, H, W]`` holding
     the smallest raster index ``v*W + u`` (+ ``row_base*W``) of each pixel's
     component, -1 where not passable."""
-    d = _fp32(_batched(disparity))
+    d = _batched(disparity)
     B, H, W = d.shape
     dev = d.device
     out = _check_out(out, (B, H, W), torch.int32, dev, "out")
     ws = _workspace(workspace, B, H, W, dev)
     rs = _native.rig_struct(rig)
-    rc = _native.load().sn_ccl_labels_ws(_native.plan(dev.index), d.data_ptr(), B, H, W,
+    rc = _disp_fn(d, "sn_ccl_labels_ws")(_native.plan(dev.index), d.data_ptr(), B, H, W,
                                          ctypes.byref(rs), float(threshold), int(row_base),
                                          out.data_ptr(), ws.data_ptr(),
                                          ws.numel() * ws.element_size(), _stream(dev))

@@ -447,37 +447,6 @@ def test_random_shapes_vs_oracle(cuda_dev):
             _check_record(o[b], m[b], _oracle_record(d[b], rig, k))
 
 
-def test_pipe_kernel_variant_matches(cuda_dev, tmp_path):
-    """The warp-specialised variant (opt-in, SN_FUSED_PIPE=1, read once per
-    process) gives the same records as the default kernel -- run in a child
-    process so the switch takes effect."""
-    import subprocess
-    import sys
-    from pathlib import Path
-    root = Path(__file__).resolve().parent.parent
-    code = f"""
-import sys, numpy as np, torch
-sys.path.insert(0, {str(root)!r})
-from paper_2504_15121_b200 import device, scenes
-sc = scenes.street_scene(512, 256)
-d = torch.from_numpy(scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.4, 3).astype(np.float32)).cuda()
-d = torch.stack([d, d.flip(1)])
-for k in (3, 9):
-    np.save({str(tmp_path)!r} + f'/o{{k}}.npy', device.oriented_points(d, sc.rig, k).cpu().numpy())
-"""
-    for tag, env in (("pipe", {"SN_FUSED_PIPE": "1"}), ("base", {})):
-        sub = tmp_path / tag
-        sub.mkdir()
-        r = subprocess.run([sys.executable, "-c", code.replace(str(tmp_path), str(sub))],
-                           env={**__import__("os").environ, **env}, capture_output=True, text=True,
-                           timeout=300)
-        assert r.returncode == 0, r.stderr[-2000:]
-    for k in (3, 9):
-        a = np.load(tmp_path / "pipe" / f"o{k}.npy")
-        b = np.load(tmp_path / "base" / f"o{k}.npy")
-        assert np.array_equal(np.nan_to_num(a, nan=7.0), np.nan_to_num(b, nan=7.0)), k
-
-
 @pytest.mark.parametrize("W", [1242, 1241, 130, 7])
 def test_unaligned_widths_take_the_fast_kernel(cuda_dev, W):
     """Widths TMA cannot address directly (W % 4 != 0, odd W) run the fast
