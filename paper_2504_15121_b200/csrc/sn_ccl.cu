@@ -665,143 +665,252 @@ template int run_passable<double>(const LaunchCtx&, const double*, const CclPara
                                   double*);
 
 // ST-passable bit mask (adaptive.py:80-97,130-132) as a streaming kernel.
-// A warp owns 32 aligned columns x kPbRows rows of a frame, lane <-> column:
-// depths zf = fxb * rcp(d) of rows -1 .. kPbRows in registers, left/right
-// neighbours by shuffle (the warp's edge columns come from two more strided
-// loads), one ballot per row = one bit-mask word.  The fp32 filter is the
-// z-form of sn_common.cuh (margin 2^-20 S + 2^-21 t, all five depths in
-// [2^-100, 2^100]); undecided pixels -- ties, out-of-range or invalid
-// samples -- take the exact fp64 path with the reference's op order.  Reads
-// 4 B/px (+ halo through L2), writes 1/8 B/px; full occupancy, no shared
-// memory.
-constexpr int kPbRows = 16;
+//
+// A warp owns 128 aligned columns x kPbRows rows of a frame; lane L owns the
+// 4 consecutive columns 4L .. 4L+3 (one 16-byte load per row for fp32).  The
+// rows stream through a 3-row register window of depths zf = fxb * rcp(d);
+// the left / right neighbours of a lane's first / last column come from the
+// neighbour lanes by shuffle (lanes 0 and 31 load the warp's outer columns),
+// and the arithmetic runs on pixel pairs with packed f32x2 ops.  Per pixel the
+// fp32 filter of sn_common.cuh decides passable (|e| < t - margin), not
+// passable (|e| > t + margin) or undecided, where margin = 2^-20 S + 2^-21 t.
+// Decisions need every depth of the 5-point stencil > 0: a row-lane whose
+// window holds a non-positive depth (negative, zero or +inf disparities) is
+// undecided as a whole; NaN samples propagate into e and leave the pixel
+// undecided; infinite depths make the margin infinite (undecided as well).
+// Undecided pixels -- ties, invalid or out-of-range samples -- take the exact
+// fp64 path with the reference's op order (pred_exact_d), so every decision
+// is the fp64 reference's.  The per-lane result is a nibble per row; an 8x8
+// nibble transpose across each 8-lane group (3 xor-shuffle stages) turns
+// them into the bit-mask words, one word per lane per 8 rows.  Reads 4 B/px
+// (+ halo rows through L2), writes 1/8 B/px.
+constexpr int kPbRows = 16;  // 32: spills at the 64-register cap (2.71 vs 2.44 us/frame)
+constexpr int kPbCols = 128;
 
-template <typename T>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ float4 pb_depth4(float4 d, float fxb) {
+  return make_float4(__fmul_rn(fxb, rcp_ftz(d.x)), __fmul_rn(fxb, rcp_ftz(d.y)),
+                     __fmul_rn(fxb, rcp_ftz(d.z)), __fmul_rn(fxb, rcp_ftz(d.w)));
+}
+
+__device__ __forceinline__ float pb_min4(float4 z) {
+  return fminf(fminf(z.x, z.y), fminf(z.z, z.w));
+}
+__device__ __forceinline__ float pb_max4(float4 z) {
+  return fmaxf(fmaxf(z.x, z.y), fmaxf(z.z, z.w));
+}
+
+// One row of a lane's 4 pixels: sets bit b + j of `yes` (passable) or `no`
+// (not passable) for every decided pixel j; `clean` = every non-NaN depth of
+// the stencils in (0, 2^100).  e = 4c - ((u + d) + (l + r)) has the four
+// roundings of the filter bound; lo / hi = t -/+ (2^-21 t + 2^-20 S).  In a
+// clean window a NaN e can only come from a NaN (invalid) sample, so the
+// unordered compare decides such pixels "not passable" at once.
+__device__ __forceinline__ void pb_row(float4 zu, float4 zc, float4 zd, float lft, float rgt,
+                                       bool clean, float2 qlo, float2 qhi, int b, uint32_t& yes,
+                                       uint32_t& no) {
+  // horizontal neighbour sums (scalar: the pairs would straddle registers)
+  const float2 hs01 = make_float2(__fadd_rn(lft, zc.y), __fadd_rn(zc.x, zc.z));
+  const float2 hs23 = make_float2(__fadd_rn(zc.y, zc.w), __fadd_rn(zc.z, rgt));
+  const float2 P01 = __fadd2_rn(__fadd2_rn(make_float2(zu.x, zu.y), make_float2(zd.x, zd.y)), hs01);
+  const float2 P23 = __fadd2_rn(__fadd2_rn(make_float2(zu.z, zu.w), make_float2(zd.z, zd.w)), hs23);
+  const float2 four = make_float2(4.0f, 4.0f);
+  const float2 e01 = __ffma2_rn(four, make_float2(zc.x, zc.y), make_float2(-P01.x, -P01.y));
+  const float2 e23 = __ffma2_rn(four, make_float2(zc.z, zc.w), make_float2(-P23.x, -P23.y));
+  const float2 S01 = __ffma2_rn(four, make_float2(zc.x, zc.y), P01);
+  const float2 S23 = __ffma2_rn(four, make_float2(zc.z, zc.w), P23);
+  const float2 km = make_float2(-9.5367431640625e-07f, -9.5367431640625e-07f);  // -2^-20
+  const float2 kp = make_float2(9.5367431640625e-07f, 9.5367431640625e-07f);
+  const float2 lo01 = __ffma2_rn(S01, km, qlo), lo23 = __ffma2_rn(S23, km, qlo);
+  const float2 hi01 = __ffma2_rn(S01, kp, qhi), hi23 = __ffma2_rn(S23, kp, qhi);
+  if (clean && fabsf(e01.x) < lo01.x) yes |= 1u << b;
+  if (clean && fabsf(e01.y) < lo01.y) yes |= 2u << b;
+  if (clean && fabsf(e23.x) < lo23.x) yes |= 4u << b;
+  if (clean && fabsf(e23.y) < lo23.y) yes |= 8u << b;
+  if (clean && !(fabsf(e01.x) <= hi01.x)) no |= 1u << b;
+  if (clean && !(fabsf(e01.y) <= hi01.y)) no |= 2u << b;
+  if (clean && !(fabsf(e23.x) <= hi23.x)) no |= 4u << b;
+  if (clean && !(fabsf(e23.y) <= hi23.y)) no |= 8u << b;
+}
+
+// A row's 4 raw samples as loaded (converted to fp32 only when used, so a
+// prefetched row does not wait for its load).  The caller clamps rows and
+// columns into the frame: samples of clamped (outside) rows and columns only
+// ever feed pixels that are not interior, whose bits are masked.
+template <typename T, bool VEC>
+struct PbRaw {
+  T v[4];
+  __device__ __forceinline__ void load(const T* row, int W) {
+    if constexpr (VEC && sizeof(T) == 4) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(row));
+      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+    } else if constexpr (VEC) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(row));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(row + 2));
+      v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = __ldg(row + min(j, W - 1));
+    }
+  }
+  __device__ __forceinline__ float4 depth(float fxb) const {
+    return pb_depth4(make_float4(disp_f32(v[0]), disp_f32(v[1]), disp_f32(v[2]), disp_f32(v[3])),
+                     fxb);
+  }
+};
+
+// The rows of one warp task; rows outside the frame are clamped into it.
+// Row r + 1 + PD is loaded while row r is evaluated (PD rows in flight).
+template <typename T, bool VEC>
+__device__ __forceinline__ void pb_task(const T* colp, const T* edgep, int y0, int H, int W, int xw,
+                                        int lane, float fxb, bool pe, float2 qlo, float2 qhi,
+                                        uint32_t* yes, uint32_t* no) {
+  constexpr int PD = 2;  // measured flat for 1..3 (ptxas schedules the loads itself)
+  auto rowoff = [&](int y) -> int {  // frame offsets fit int32 (host-checked)
+    return min(max(y, 0), H - 1) * W;
+  };
+  PbRaw<T, VEC> raw[PD];
+  T eraw[PD];
+#pragma unroll
+  for (int i = 0; i < PD; ++i) {
+    raw[i].load(colp + rowoff(y0 + 1 + i), xw);
+    eraw[i] = __ldg(edgep + rowoff(y0 + 1 + i));
+  }
+  PbRaw<T, VEC> r0;
+  r0.load(colp + rowoff(y0 - 1), xw);
+  float4 zu = r0.depth(fxb);
+  r0.load(colp + rowoff(y0), xw);
+  float4 zc = r0.depth(fxb);
+  float ec = __fmul_rn(fxb, rcp_ftz(disp_f32(__ldg(edgep + rowoff(y0)))));
+  float mu = pb_min4(zu), mc = pb_min4(zc), xu = pb_max4(zu), xcm = pb_max4(zc);
+#pragma unroll
+  for (int r = 0; r < kPbRows; ++r) {
+    const float4 zd = raw[r % PD].depth(fxb);
+    const float ed = __fmul_rn(fxb, rcp_ftz(disp_f32(eraw[r % PD])));
+    if (r + PD < kPbRows) {
+      const int off = rowoff(y0 + r + 1 + PD);
+      raw[r % PD].load(colp + off, xw);
+      eraw[r % PD] = __ldg(edgep + off);
+    }
+    const float md = pb_min4(zd), xd = pb_max4(zd);
+    float lft = __shfl_up_sync(0xffffffffu, zc.w, 1);
+    float rgt = __shfl_down_sync(0xffffffffu, zc.x, 1);
+    if (lane == 0) lft = ec;
+    if (lane == 31) rgt = ec;
+    // every non-NaN depth of the lane's stencils in (0, 2^100): NaN samples
+    // are skipped by min/max (a window of NaNs only is clean) and poison e
+    const float lo = fminf(fminf(fminf(mu, mc), fminf(md, lft)), rgt);
+    const float hi = fmaxf(fmaxf(fmaxf(xu, xcm), fmaxf(xd, lft)), rgt);
+    const bool clean = !pe && !(lo <= 0.0f) && !(hi >= 1.2676506002282294e30f);
+    pb_row(zu, zc, zd, lft, rgt, clean, qlo, qhi, 4 * (r & 7), yes[r >> 3], no[r >> 3]);
+    zu = zc;
+    zc = zd;
+    mu = mc;
+    mc = md;
+    xu = xcm;
+    xcm = xd;
+    ec = ed;
+  }
+}
+
+// One warp per block: the task loop and every shuffle are then in uniform
+// control flow (no divergence-safe shuffle sequences in the hot loop); 32
+// single-warp blocks per SM give the full 32 warps at 64 registers.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(32, 32)
     passable_bits_kernel(const T* __restrict__ disp, const FixedParams p,
                          uint32_t* __restrict__ bits) {
   const int W = (int)p.W, H = (int)p.H, WW = p.bits_ww;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x;
+  const unsigned tasks_x = (unsigned)((W + kPbCols - 1) / kPbCols);
   const unsigned strips_y = (unsigned)((H + kPbRows - 1) / kPbRows);
-  const unsigned n_tasks = (unsigned)p.B * strips_y * (unsigned)WW;  // < 2^31 (host-checked)
-  const float nanf_ = __int_as_float(0x7fc00000);
+  const unsigned n_tasks = (unsigned)p.B * strips_y * tasks_x;  // < 2^31 (host-checked)
   const float tm = __fmul_rn(p.t_f, 4.76837158203125e-07f /* 2^-21 */);
-  for (unsigned task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < n_tasks;
-       task += (gridDim.x * blockDim.x) >> 5) {
-    const unsigned rest = task / (unsigned)WW;
-    const int wc = (int)(task - rest * (unsigned)WW);
+  const float2 qlo = make_float2(__fsub_rn(p.t_f, tm), __fsub_rn(p.t_f, tm));
+  const float2 qhi = make_float2(__fadd_rn(p.t_f, tm), __fadd_rn(p.t_f, tm));
+  const bool pe = p.pred_exact != 0;
+  const int g8 = lane & 7;
+  for (unsigned task = blockIdx.x; task < n_tasks; task += gridDim.x) {
+    const unsigned rest = task / tasks_x;
+    const int tx = (int)(task - rest * tasks_x);
     const unsigned f = rest / strips_y;
     const int y0 = (int)(rest - f * strips_y) * kPbRows;
-    const int x = wc * 32 + lane;
+    const int x0 = tx * kPbCols, xl = x0 + 4 * lane;
     const T* fr = disp + (int64_t)f * p.H * p.W;
-    // depths of this column, rows y0-1 .. y0+kPbRows (NaN outside the frame)
-    float z[kPbRows + 2];
-    if (y0 >= 1 && y0 + kPbRows < H && wc * 32 + 32 <= W) {
-      const T* src = fr + (y0 - 1) * W + x;  // frame offsets fit int32 (host-checked)
+    // clamped load columns (see PbRaw): a lane past the right edge
+    // re-reads the last vector; the warp's outer columns (lane 0: left, lane
+    // 31: right; the other lanes' copy is unused) stay in the frame
+    const int xc = VEC ? min(xl, W - 4) : xl;
+    const int xe = min(max(lane == 0 ? x0 - 1 : x0 + kPbCols, 0), W - 1);
+    uint32_t yes[kPbRows / 8] = {}, no[kPbRows / 8] = {};
+    pb_task<T, VEC>(fr + xc, fr + xe, y0, H, W, VEC ? 4 : W - xc, lane, p.fxb_f, pe, qlo, qhi, yes,
+                    no);
+    // interior pixels only (the reference has no padding): columns 1 .. W-2
+    // (per lane, replicated over the rows' nibbles), rows 1 .. H-2
+    uint32_t cm = 0;
 #pragma unroll
-      for (int k = 0; k < kPbRows + 2; ++k)
-        z[k] = __fmul_rn(p.fxb_f, rcp_ftz(disp_f32(__ldg(src + k * W))));
-    } else {
+    for (int j = 0; j < 4; ++j) cm |= (xl + j >= 1 && xl + j + 1 < W) ? (0x11111111u << j) : 0u;
+    uint32_t und[kPbRows / 8], anyu = 0;
 #pragma unroll
-      for (int k = 0; k < kPbRows + 2; ++k) {
-        const int y = y0 - 1 + k;
-        const float d = (x < W && y >= 0 && y < H) ? disp_f32(__ldg(fr + y * W + x)) : nanf_;
-        z[k] = __fmul_rn(p.fxb_f, rcp_ftz(d));
-      }
+    for (int k = 0; k < kPbRows / 8; ++k) {
+      const int ya = y0 + 8 * k;  // rows ya .. ya+7 -> nibbles 0 .. 7
+      uint32_t rows = 0xffffffffu;
+      if (ya < 1) rows &= 0xfffffff0u;
+      if (ya + 8 > H - 1) rows &= (H - 1 - ya) <= 0 ? 0u : (0xffffffffu >> (4 * (8 - (H - 1 - ya))));
+      const uint32_t m = cm & rows;
+      yes[k] &= m;
+      und[k] = m & ~(yes[k] | no[k]);
+      anyu |= und[k];
     }
-    // the warp's edge columns: lane k < kPbRows holds row y0+k of column
-    // wc*32-1 (el) and of column wc*32+32 (er)
-    float el = nanf_, er = nanf_;
-    {
-      const int y = y0 + lane;
-      if (lane < kPbRows && y < H) {
-        const int xl = wc * 32 - 1, xr = wc * 32 + 32;
-        if (xl >= 0) el = __fmul_rn(p.fxb_f, rcp_ftz(disp_f32(__ldg(fr + y * W + xl))));
-        if (xr < W) er = __fmul_rn(p.fxb_f, rcp_ftz(disp_f32(__ldg(fr + y * W + xr))));
-      }
-    }
-    // interior pixels only (the reference has no padding): rows 1 .. H-2, cols 1 .. W-2
-    uint32_t rows_in = (kPbRows == 32) ? 0xffffffffu : ((1u << kPbRows) - 1u);
-    if (y0 == 0) rows_in &= ~1u;
-    if (H - 1 - y0 < kPbRows) rows_in &= (H - 1 - y0 > 0) ? ((1u << (H - 1 - y0)) - 1u) : 0u;
-    if (!(x >= 1 && x + 1 < W)) rows_in = 0;
-    const float2 tm2 = make_float2(tm, tm);
-    const float2 k20 = make_float2(9.5367431640625e-07f, 9.5367431640625e-07f);  // 2^-20
-    const float2 four = make_float2(4.0f, 4.0f);
-    const bool pe = p.pred_exact != 0;
-    // lane k < kPbRows ends up with the words of row y0 + k: passable (mine)
-    // and undecided by the filter (mund)
-    uint32_t mine = 0, mund = 0;
-    // rows in pairs, packed f32x2 (FADD2/FMUL2/FFMA2); one ballot per row
+    // rare exact decisions (fp64, reference op order)
+    if (__any_sync(0xffffffffu, anyu != 0u)) {
 #pragma unroll
-    for (int k = 0; k < kPbRows; k += 2) {
-      float2 L, R;
-      L.x = __shfl_up_sync(0xffffffffu, z[k + 1], 1);
-      L.y = __shfl_up_sync(0xffffffffu, z[k + 2], 1);
-      R.x = __shfl_down_sync(0xffffffffu, z[k + 1], 1);
-      R.y = __shfl_down_sync(0xffffffffu, z[k + 2], 1);
-      const float el0 = __shfl_sync(0xffffffffu, el, k), el1 = __shfl_sync(0xffffffffu, el, k + 1);
-      const float er0 = __shfl_sync(0xffffffffu, er, k), er1 = __shfl_sync(0xffffffffu, er, k + 1);
-      if (lane == 0) L = make_float2(el0, el1);
-      if (lane == 31) R = make_float2(er0, er1);
-      const float2 C = make_float2(z[k + 1], z[k + 2]);
-      const float2 U = make_float2(z[k], z[k + 1]), D = make_float2(z[k + 2], z[k + 3]);
-      const float2 c4 = __fmul2_rn(four, C);
-      const float2 ud = __fadd2_rn(U, D);
-      const float2 hs = __fadd2_rn(L, R);
-      const float2 S = __fadd2_rn(__fadd2_rn(c4, ud), hs);
-      // e = (4c - (u + d)) - (l + r): three roundings of partial sums <= S
-      const float2 e = __ffma2_rn(make_float2(-1.0f, -1.0f), hs,
-                                  __ffma2_rn(make_float2(-1.0f, -1.0f), ud, c4));
-      const float2 m = __ffma2_rn(S, k20, tm2);
-      const float a0 = __fsub_rn(fabsf(e.x), p.t_f), a1 = __fsub_rn(fabsf(e.y), p.t_f);  // e - t
-      const float mn0 = fminf(fminf(fminf(U.x, D.x), fminf(L.x, R.x)), C.x);
-      const float mn1 = fminf(fminf(fminf(U.y, D.y), fminf(L.y, R.y)), C.y);
-      const bool ok0 = !pe && (S.x <= 1.0141204801825835e31f) && (mn0 >= 7.888609052210118e-31f);
-      const bool ok1 = !pe && (S.y <= 1.0141204801825835e31f) && (mn1 >= 7.888609052210118e-31f);
-      const bool in0 = (rows_in >> k) & 1u, in1 = (rows_in >> (k + 1)) & 1u;
-      const uint32_t wp0 = __ballot_sync(0xffffffffu, in0 && ok0 && a0 < -m.x);
-      const uint32_t wp1 = __ballot_sync(0xffffffffu, in1 && ok1 && a1 < -m.y);
-      const uint32_t wu0 = __ballot_sync(0xffffffffu, in0 && !(ok0 && fabsf(a0) > m.x));
-      const uint32_t wu1 = __ballot_sync(0xffffffffu, in1 && !(ok1 && fabsf(a1) > m.y));
-      if (lane == k) {
-        mine = wp0;
-        mund = wu0;
-      }
-      if (lane == k + 1) {
-        mine = wp1;
-        mund = wu1;
-      }
-    }
-    // rare exact decisions (fp64, reference op order), after the row loop so
-    // a warp diverges only for the rows that need it
-    if (__any_sync(0xffffffffu, mund != 0u)) {
-      for (int k = 0; k < kPbRows; ++k) {
-        const uint32_t wu = __shfl_sync(0xffffffffu, mund, k);
-        if (wu == 0u) continue;
-        bool pk = false;
-        if ((wu >> lane) & 1u) {
-          const T* c = fr + (y0 + k) * W + x;
-          pk = pred_exact_d(c[0], c[-1], c[1], c[-W], c[W], p.fxb, p.t) != 0u;
+      for (int k = 0; k < kPbRows / 8; ++k) {
+        for (uint32_t m = und[k]; m; m &= m - 1u) {
+          const int b = __ffs(m) - 1;
+          const int y = y0 + 8 * k + (b >> 2), x = xl + (b & 3);
+          const T* c = fr + (int64_t)y * W + x;
+          if (pred_exact_d(c[0], c[-1], c[1], c[-W], c[W], p.fxb, p.t)) yes[k] |= 1u << b;
         }
-        const uint32_t fix = __ballot_sync(0xffffffffu, pk);
-        if (lane == k) mine |= fix;
       }
     }
-    if (lane < kPbRows && y0 + lane < H) bits[((int64_t)f * p.H + y0 + lane) * WW + wc] = mine;
+    // 8x8 nibble transpose inside each 8-lane group: lane 8g+i ends with the
+    // word of row 8k+i, columns x0 + 32g .. +31.  Stage s: the partner is
+    // lane ^ s; a lane keeps the nibbles whose row bit s equals its own lane
+    // bit s and takes the others from the partner, rotated into place (the
+    // rotation's wrapped-around bits land in the kept half and are masked).
+    const int gw = tx * (kPbCols / 32) + (lane >> 3);
+#pragma unroll
+    for (int k = 0; k < kPbRows / 8; ++k) {
+      uint32_t v = yes[k];
+#pragma unroll
+      for (int s = 4; s >= 1; s >>= 1) {
+        const uint32_t mc_ = s == 1 ? 0x0F0F0F0Fu : (s == 2 ? 0x00FF00FFu : 0x0000FFFFu);
+        const bool hi = (g8 & s) != 0;
+        const uint32_t keep = hi ? ~mc_ : mc_;
+        const uint32_t t = __shfl_xor_sync(0xffffffffu, v, s);
+        const uint32_t rot = __funnelshift_r(t, t, hi ? 4 * s : 32 - 4 * s);
+        v = (v & keep) | (rot & ~keep);
+      }
+      const int y = y0 + 8 * k + g8;
+      if (y < H && gw < WW) bits[((int64_t)f * p.H + y) * WW + gw] = v;
+    }
   }
 }
 
 template <typename T>
 int run_passable_bits(const LaunchCtx& ctx, const T* disp, const FixedParams& p,
                       uint32_t* bits) {
-  const int64_t n = p.B * ((p.H + kPbRows - 1) / kPbRows) * p.bits_ww * 32;
-  if (n == 0) return SN_OK;
-  if (p.H * p.W > 0x7fffffffLL || n / 32 > 0x7fffffffLL)
+  const int64_t tasks = p.B * ((p.H + kPbRows - 1) / kPbRows) * ((p.W + kPbCols - 1) / kPbCols);
+  if (tasks == 0) return SN_OK;
+  if (p.H * p.W > 0x7fffffffLL || tasks > 0x7fffffffLL)
     return set_error(SN_EINVAL, "frame or batch too large for the passable-bit kernel");
-  int64_t g = (n + 255) / 256;
-  if (g > (int64_t)ctx.num_sms * 64) g = (int64_t)ctx.num_sms * 64;
-  passable_bits_kernel<T><<<(unsigned)g, 256, 0, ctx.stream>>>(disp, p, bits);
+  const bool vec = p.W % 4 == 0 && reinterpret_cast<uintptr_t>(disp) % 16 == 0 && p.W >= 4;
+  int64_t g = tasks;
+  if (g > (int64_t)ctx.num_sms * 32) g = (int64_t)ctx.num_sms * 32;
+  if (vec)
+    passable_bits_kernel<T, true><<<(unsigned)g, 32, 0, ctx.stream>>>(disp, p, bits);
+  else
+    passable_bits_kernel<T, false><<<(unsigned)g, 32, 0, ctx.stream>>>(disp, p, bits);
   return check_launch("passable_bits_kernel");
 }
 template int run_passable_bits<float>(const LaunchCtx&, const float*, const FixedParams&,
