@@ -98,6 +98,20 @@ SN_API int sn_oriented_points_f64(sn_plan_t* plan, const double* disp, int64_t B
                            int64_t W, const sn_rig_t* rig, const int32_t* offsets_xy,
                            int32_t n_off, float* out6, uint8_t* mask, void* stream);
 
+/* Same pass on row-pitched input (SURVEY.md §8(b) sn_fixed_points' `ld`):
+ * row v of frame b starts at disp + (b * H + v) * ld, ld >= W elements (a
+ * crop of a wider buffer, or rows padded for alignment).  Pitches whose rows
+ * are 16-byte aligned feed the TMA tensor map directly; others are packed
+ * into stream-ordered scratch first.  Output is dense [B][H][W][6]. */
+SN_API int sn_oriented_points_strided(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
+                               int64_t W, int64_t ld, const sn_rig_t* rig,
+                               const int32_t* offsets_xy, int32_t n_off, float* out6,
+                               uint8_t* mask, void* stream);
+SN_API int sn_oriented_points_strided_f64(sn_plan_t* plan, const double* disp, int64_t B,
+                                   int64_t H, int64_t W, int64_t ld, const sn_rig_t* rig,
+                                   const int32_t* offsets_xy, int32_t n_off, float* out6,
+                                   uint8_t* mask, void* stream);
+
 /* Same pass over a block of rows of a taller image (strip partitioning,
  * SURVEY.md §8(e)): block row i is image row row0 + i, which only changes the
  * pixel coordinate v of the normal and point; the block's first and last

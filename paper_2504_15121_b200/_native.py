@@ -58,6 +58,9 @@ SIGNATURES = {
     "sn_oriented_points": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
     "sn_oriented_points_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
     "sn_oriented_points_generic": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
+    "sn_oriented_points_strided": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
+    "sn_oriented_points_strided_f64": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P,
+                                       _P],
     "sn_oriented_points_rows": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _P, _P, _P],
     "sn_oriented_points_bits": [_P, _P, _I64, _I64, _I64, _I64, _RIGP, _P, _I32, _D, _P, _P, _P,
                                 _P],

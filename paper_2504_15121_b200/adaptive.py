@@ -172,21 +172,9 @@ def estimate_affine_adaptive(disparity: ScalarField, depth: ScalarField,
     """(a1, a2) least-squares fit over one pixel's star support
     (adaptive.py:146-174): offsets with an invalid disparity sample are left
     out; (nan, nan) for an invalid centre or a rank-deficient support."""
-    u, v = pixel
+    from .kernels import support_fit
+    u, v = int(pixel[0]), int(pixel[1])
     h, w = disparity.shape
-    nan2 = (float("nan"), float("nan"))
     if not (0 <= v < h and 0 <= u < w) or not disparity.mask[v, u]:
-        return nan2
-    sup = star_trace(pixel, depth, edges, config)
-    sup = sup[disparity.mask[v + sup[:, 1], u + sup[:, 0]]]
-    # the moments as strided column dot products, the reference's own BLAS
-    # calls (a contiguous copy could take another summation order)
-    vxy = sup.astype(np.float64)
-    vx, vy = vxy[:, 0], vxy[:, 1]
-    dd = disparity.values[v + sup[:, 1], u + sup[:, 0]] - disparity.values[v, u]
-    al, be, ga = float(vx @ vx), float(vx @ vy), float(vy @ vy)
-    det = al * ga - be * be
-    if det <= 0.5:
-        return nan2
-    b1, b2 = float(vx @ dd), float(vy @ dd)
-    return (1.0 + (ga * b1 - be * b2) / det, (-be * b1 + al * b2) / det)
+        return (float("nan"), float("nan"))
+    return support_fit(disparity, u, v, star_trace((u, v), depth, edges, config))

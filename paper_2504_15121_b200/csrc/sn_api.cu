@@ -398,6 +398,52 @@ int sn_oriented_points(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
                                      stream, 0);
 }
 
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+int strided_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int64_t W, int64_t ld,
+                 const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off, float* out6,
+                 uint8_t* mask, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  int rc = check_shape(B, H, W);
+  if (rc) return rc;
+  if (ld < W) return set_error(SN_EINVAL, "row pitch ld=%lld is smaller than W=%lld",
+                               (long long)ld, (long long)W);
+  if ((rc = check_rig(rig))) return rc;
+  sn_moments_t m;
+  static thread_local OffsetTable tab;
+  if ((rc = prepare(offsets_xy, n_off, m, tab))) return rc;
+  if (B * H * W > 0 && (!disp || !out6)) return set_error(SN_EINVAL, "NULL buffer");
+  FixedParams p{};
+  p.B = B;
+  p.H = H;
+  p.W = W;
+  fill_rig(p, rig);
+  fill_moments(p, m);
+  DeviceGuard g(plan->device);
+  return run_fixed_strided<T>(make_ctx(plan, stream), disp, ld, p, m, tab, out6, mask);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_oriented_points_strided(sn_plan_t* plan, const float* disp, int64_t B, int64_t H,
+                               int64_t W, int64_t ld, const sn_rig_t* rig,
+                               const int32_t* offsets_xy, int32_t n_off, float* out6,
+                               uint8_t* mask, void* stream) {
+  return strided_impl<float>(plan, disp, B, H, W, ld, rig, offsets_xy, n_off, out6, mask, stream);
+}
+
+int sn_oriented_points_strided_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H,
+                                   int64_t W, int64_t ld, const sn_rig_t* rig,
+                                   const int32_t* offsets_xy, int32_t n_off, float* out6,
+                                   uint8_t* mask, void* stream) {
+  return strided_impl<double>(plan, disp, B, H, W, ld, rig, offsets_xy, n_off, out6, mask, stream);
+}
+
 int sn_oriented_points_f64(sn_plan_t* plan, const double* disp, int64_t B, int64_t H, int64_t W,
                            const sn_rig_t* rig, const int32_t* offsets_xy, int32_t n_off,
                            float* out6, uint8_t* mask, void* stream) {

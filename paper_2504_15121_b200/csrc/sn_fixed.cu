@@ -1024,6 +1024,38 @@ int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const s
   return rc;
 }
 
+// Row-pitched input (ld >= W elements between rows, ld * H between frames):
+// the TMA tensor map takes the pitch directly when the rows are 16-byte
+// aligned and the pattern is a centred square; otherwise the rows are packed
+// into stream-ordered scratch first and the contiguous path runs on it.
+template <typename T>
+int run_fixed_strided(const LaunchCtx& ctx, const T* disp, int64_t ld, const FixedParams& p,
+                      const sn_moments_t& m, const OffsetTable& tab, float* out6, uint8_t* mask) {
+  if (p.B * p.H * p.W == 0) return SN_OK;
+  if (ld == p.W) return run_fixed<T>(ctx, disp, p, m, tab, out6, mask, nullptr, nullptr, false, 0);
+  const bool sized = p.W <= (int64_t)0x7fffffff / 6 && p.H <= 0x7fffffff && p.B <= 0x7fffffff;
+  if (m.square_r >= 1 && m.square_r <= 8 && sized && reinterpret_cast<uintptr_t>(disp) % 16 == 0 &&
+      (ld * (int64_t)sizeof(T)) % 16 == 0 && reinterpret_cast<uintptr_t>(out6) % 16 == 0 &&
+      p.W % 2 == 0) {
+    const int rc = dispatch_square<T>(m.square_r, ctx, disp, p, out6, mask, ld, p.W);
+    if (rc >= 0) return rc;
+  }
+  T* packed = nullptr;
+  int rc = scratch_alloc(ctx, (size_t)(p.B * p.H * p.W) * sizeof(T), reinterpret_cast<void**>(&packed));
+  if (rc) return rc;
+  rc = pitch_copy(ctx, disp, ld * (int64_t)sizeof(T), packed, p.W * (int64_t)sizeof(T),
+                  p.W * (int64_t)sizeof(T), p.B * p.H);
+  if (rc == SN_OK)
+    rc = run_fixed<T>(ctx, packed, p, m, tab, out6, mask, nullptr, nullptr, false, 0);
+  scratch_free(ctx, packed);
+  return rc;
+}
+template int run_fixed_strided<float>(const LaunchCtx&, const float*, int64_t, const FixedParams&,
+                                      const sn_moments_t&, const OffsetTable&, float*, uint8_t*);
+template int run_fixed_strided<double>(const LaunchCtx&, const double*, int64_t,
+                                       const FixedParams&, const sn_moments_t&, const OffsetTable&,
+                                       float*, uint8_t*);
+
 template int run_fixed<float>(const LaunchCtx&, const float*, const FixedParams&,
                               const sn_moments_t&, const OffsetTable&, float*, uint8_t*, double*,
                               double*, bool, int);

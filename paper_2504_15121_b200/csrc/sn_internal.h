@@ -44,6 +44,10 @@ int run_fixed(const LaunchCtx& ctx, const T* disp, const FixedParams& p, const s
               const OffsetTable& tab, float* out6, uint8_t* mask, double* a1, double* a2,
               bool affine, int force_generic);
 
+template <typename T>
+int run_fixed_strided(const LaunchCtx& ctx, const T* disp, int64_t ld, const FixedParams& p,
+                      const sn_moments_t& m, const OffsetTable& tab, float* out6, uint8_t* mask);
+
 struct CclParams {
   int64_t B, H, W;
   double fxb;       // fx * b in Python's double order (geometry.py:43)

@@ -47,6 +47,21 @@ def _batched(disp: torch.Tensor, name: str = "disparity") -> torch.Tensor:
     return disp.contiguous()
 
 
+def _row_pitch(d) -> int:
+    """Row pitch (elements) of a CUDA tensor [B, H, W] / [H, W] whose rows are
+    contiguous and evenly pitched but not packed (a column crop); 0 when the
+    tensor is contiguous or not such a view."""
+    if not isinstance(d, torch.Tensor) or not d.is_cuda or d.dim() not in (2, 3) \
+            or d.is_contiguous() or d.dtype not in (torch.float32, torch.float64):
+        return 0
+    st, sh = d.stride(), d.shape
+    if st[-1] != 1 or st[-2] < sh[-1]:
+        return 0
+    if d.dim() == 3 and sh[0] > 1 and st[0] != st[-2] * sh[-2]:
+        return 0
+    return int(st[-2])
+
+
 def _disp_fn(d: torch.Tensor, name: str):
     """The C-ABI function for ``d``'s dtype: ``name`` (fp32) or ``name_f64``."""
     lib = _native.load()
@@ -80,7 +95,9 @@ def oriented_points(disparity: torch.Tensor, rig, kernels=9, *, out: torch.Tenso
     the disparity is not finite and positive.  ``mask`` (uint8 ``[B, H, W]``)
     optionally receives the normal validity.  ``row0`` is the image row of
     the first input row when the input is a strip of a taller image."""
-    d = _batched(disparity)
+    ld = _row_pitch(disparity)
+    d = disparity.unsqueeze(0) if (ld and disparity.dim() == 2) else (
+        disparity if ld else _batched(disparity))
     B, H, W = d.shape
     dev = d.device
     out = _check_out(out, (B, H, W, 6), torch.float32, dev, "out")
@@ -88,6 +105,15 @@ def oriented_points(disparity: torch.Tensor, rig, kernels=9, *, out: torch.Tenso
         mask = _check_out(mask, (B, H, W), torch.uint8, dev, "mask")
     off = _offsets_of(kernels)
     lib = _native.load()
+    if ld and not generic and not row0:
+        # a row-pitched view (e.g. a crop of wider frames): no copy
+        rc = _disp_fn(d, "sn_oriented_points_strided")(
+            _native.plan(dev.index), d.data_ptr(), B, H, W, ld, ctypes.byref(_native.rig_struct(rig)),
+            off.ctypes.data, len(off), out.data_ptr(),
+            mask.data_ptr() if mask is not None else None, _stream(dev))
+        check(rc, "oriented_points")
+        return out
+    d = d.contiguous()
     if d.dtype == torch.float32:
         fn = lib.sn_oriented_points_generic if generic else lib.sn_oriented_points
     elif d.dtype == torch.float64:

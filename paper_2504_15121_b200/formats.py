@@ -21,6 +21,7 @@ produces the binary body, so ``ply_from_vertices`` only prepends the header.
 from __future__ import annotations
 
 import io
+import re
 
 import numpy as np
 import torch
@@ -42,38 +43,39 @@ class FormatError(Exception):
 # --------------------------------------------------------------------------
 # PFM (formats.py:55-113)
 
-_WS = frozenset(b" \t\n\r\x0b\x0c")
+# one header token: optional ASCII whitespace (bytes.isspace), then a run of
+# non-whitespace bytes
+_TOKEN = re.compile(rb"[ \t\n\r\x0b\x0c]*([^ \t\n\r\x0b\x0c]+)")
+_SPACE = b" \t\n\r\x0b\x0c"
 
 
 def _pfm_header(data: bytes):
-    """(magic, width, height, scale, payload offset): four whitespace-separated
-    tokens, exactly one whitespace byte before the payload (formats.py:55-81)."""
-    pos, n, tokens = 0, len(data), []
-    while len(tokens) < 4:
-        while pos < n and data[pos] in _WS:
-            pos += 1
-        start = pos
-        while pos < n and data[pos] not in _WS:
-            pos += 1
-        if pos == start:
-            raise FormatError("truncated PFM header", offset=pos)
-        tokens.append(data[start:pos])
-    if pos >= n or data[pos] not in _WS:
-        raise FormatError("missing whitespace after PFM scale", offset=pos)
-    pos += 1
-    magic = tokens[0]
-    if magic not in (b"Pf", b"PF"):
+    """(magic, width, height, scale, payload offset) of a PFM header: four
+    whitespace-separated tokens and exactly one whitespace byte before the
+    payload.  Error messages and offsets are the reference's
+    (formats.py:55-81)."""
+    fields, end = [], 0
+    for _ in range(4):
+        m = _TOKEN.match(data, end)
+        if m is None:  # only whitespace (or nothing) left
+            raise FormatError("truncated PFM header", offset=len(data))
+        fields.append(m.group(1))
+        end = m.end()
+    if end == len(data) or data[end] not in _SPACE:
+        raise FormatError("missing whitespace after PFM scale", offset=end)
+    magic, w_tok, h_tok, s_tok = fields
+    if magic != b"Pf" and magic != b"PF":
         raise FormatError(f"bad PFM magic {magic!r}", offset=0)
     try:
-        width, height = int(tokens[1]), int(tokens[2])
-        scale = float(tokens[3])
+        dims = (int(w_tok), int(h_tok))
+        scale = float(s_tok)
     except ValueError as exc:
         raise FormatError(f"bad PFM header field: {exc}") from None
-    if width <= 0 or height <= 0:
-        raise FormatError(f"bad PFM dimensions {width}x{height}")
+    if min(dims) <= 0:
+        raise FormatError(f"bad PFM dimensions {dims[0]}x{dims[1]}")
     if scale == 0.0:
         raise FormatError("PFM scale must be nonzero")
-    return magic, width, height, scale, pos
+    return magic, dims[0], dims[1], scale, end + 1
 
 
 def read_pfm_device(data: bytes, magic: bytes = b"Pf", device=None) -> torch.Tensor:
@@ -108,16 +110,21 @@ def read_pfm_normals(data: bytes) -> NormalField:
     return NormalField.from_array(read_pfm_device(data, b"PF").double().cpu().numpy())
 
 
+def _pfm_bytes(magic: str, grid: np.ndarray) -> bytes:
+    """Little-endian PFM (negative scale), rows bottom-up as float32."""
+    h, w = grid.shape[:2]
+    body = np.ascontiguousarray(np.flip(grid, axis=0), dtype="<f4")
+    return b"".join((f"{magic}\n{w} {h}\n-1.0\n".encode("ascii"), body.tobytes()))
+
+
 def write_pfm(field: ScalarField) -> bytes:
-    """Little-endian grayscale PFM, invalid pixels as NaN (formats.py:111-115)."""
-    header = f"Pf\n{field.width} {field.height}\n-1.0\n".encode("ascii")
-    return header + np.ascontiguousarray(field.values[::-1].astype("<f4")).tobytes()
+    """Grayscale PFM, invalid pixels as NaN (formats.py:111-115)."""
+    return _pfm_bytes("Pf", field.values)
 
 
 def write_pfm_normals(field: NormalField) -> bytes:
-    """3-channel little-endian PFM (formats.py:124-127)."""
-    header = f"PF\n{field.width} {field.height}\n-1.0\n".encode("ascii")
-    return header + np.ascontiguousarray(field.vectors[::-1].astype("<f4")).tobytes()
+    """3-channel PFM (formats.py:124-127)."""
+    return _pfm_bytes("PF", field.vectors)
 
 
 # --------------------------------------------------------------------------

@@ -117,47 +117,56 @@ def estimate_normals_fixed(disparity: ScalarField, rig: StereoRig, kernels,
                        to_host(mask[0]).astype(bool))
 
 
+def support_fit(disparity: ScalarField, u: int, v: int, offsets) -> tuple[float, float]:
+    """Plain least-squares (a1, a2) at pixel (u, v) over the ``offsets`` whose
+    samples are inside the frame and valid -- the single-pixel solve shared
+    by estimate_affine_direct (kernels.py:206-234) and
+    estimate_affine_adaptive (adaptive.py:146-174); (nan, nan) for a centre
+    that is out of range or invalid, or a support with det <= 0.5.  The
+    moments use the reference's column dot products, so the roundings (and
+    results) are the reference's."""
+    h, w = disparity.shape
+    if not (0 <= v < h and 0 <= u < w) or not disparity.mask[v, u]:
+        return (float("nan"), float("nan"))
+    off = np.asarray(offsets)
+    cols, rows = u + off[:, 0], v + off[:, 1]
+    use = (cols >= 0) & (cols < w) & (rows >= 0) & (rows < h)
+    use[use] &= disparity.mask[rows[use], cols[use]]
+    vxy = off[use].astype(np.float64)
+    dd = disparity.values[rows[use], cols[use]] - disparity.values[v, u]
+    al, be, ga = (float(vxy[:, i] @ vxy[:, j]) for i, j in ((0, 0), (0, 1), (1, 1)))
+    det = al * ga - be * be
+    if det <= 0.5:
+        return (float("nan"), float("nan"))
+    b1, b2 = float(vxy[:, 0] @ dd), float(vxy[:, 1] @ dd)
+    return (1.0 + (ga * b1 - be * b2) / det, (-be * b1 + al * b2) / det)
+
+
 def estimate_affine_direct(disparity: ScalarField, pixel: tuple[int, int],
                            spec: KernelSpec) -> tuple[float, float]:
     """Single-pixel least-squares solve over the valid in-bounds offsets
     (kernels.py:206-234) -- a scalar diagnostic, not a per-pixel pass."""
-    u, v = pixel
-    h, w = disparity.shape
-    if not (0 <= v < h and 0 <= u < w) or not disparity.mask[v, u]:
-        return (float("nan"), float("nan"))
-    uu = u + spec.offsets[:, 0]
-    vv = v + spec.offsets[:, 1]
-    inside = (uu >= 0) & (uu < w) & (vv >= 0) & (vv < h)
-    keep = inside.copy()
-    keep[inside] = disparity.mask[vv[inside], uu[inside]]
-    off = spec.offsets[keep].astype(np.float64)
-    rhs = disparity.values[vv[keep], uu[keep]] - disparity.values[v, u]
-    a, b, g = off[:, 0] @ off[:, 0], off[:, 0] @ off[:, 1], off[:, 1] @ off[:, 1]
-    det = a * g - b * b
-    if det <= 0.5:
-        return (float("nan"), float("nan"))
-    b1, b2 = off[:, 0] @ rhs, off[:, 1] @ rhs
-    return (1.0 + (g * b1 - b * b2) / det, (a * b2 - b * b1) / det)
+    return support_fit(disparity, int(pixel[0]), int(pixel[1]), spec.offsets)
 
 
 def format_kernel_dump(kern: PrecomputedKernels) -> str:
-    """Debug listing: constants, then weights as grids for box-filling
-    patterns or one line per offset otherwise (kernels.py:264-296)."""
-    out = [f"offsets {len(kern.spec)}"]
-    for name in ("alpha", "beta", "gamma", "det", "delta1", "delta2"):
-        out.append(f"{name} {getattr(kern, name):.17g}")
-    off = kern.spec.offsets
-    x0, y0 = off[:, 0].min(), off[:, 1].min()
-    nx, ny = off[:, 0].max() - x0 + 1, off[:, 1].max() - y0 + 1
-    dense = len(off) == nx * ny
-    for name, wts in (("s1", kern.s1), ("s2", kern.s2)):
-        out.append(f"{name} kernel:")
-        if dense:
-            grid = np.zeros((ny, nx))
-            grid[off[:, 1] - y0, off[:, 0] - x0] = wts
-            for i in range(ny):
-                cells = "  ".join(f"{c: .10g}" for c in grid[i])
-                out.append(f"  vy={y0 + i:+d}:  {cells}")
-        else:
-            out.extend(f"  v=({x:+d},{y:+d})  {c:.10g}" for (x, y), c in zip(off, wts))
-    return "\n".join(out) + "\n"
+    """Debug listing (kernels.py:264-296): the constants, then each weight set
+    as a grid when the offsets fill their bounding box, else one line per
+    offset."""
+    consts = {"alpha": kern.alpha, "beta": kern.beta, "gamma": kern.gamma, "det": kern.det,
+              "delta1": kern.delta1, "delta2": kern.delta2}
+    text = [f"offsets {len(kern.spec)}"] + [f"{k} {val:.17g}" for k, val in consts.items()]
+    off = np.asarray(kern.spec.offsets)
+    lo = off.min(axis=0)
+    extent = off.max(axis=0) - lo + 1  # (columns, rows) of the bounding box
+    boxed = len(off) == int(extent[0] * extent[1])
+    for tag, weights in (("s1", kern.s1), ("s2", kern.s2)):
+        text.append(f"{tag} kernel:")
+        if not boxed:
+            text += [f"  v=({x:+d},{y:+d})  {c:.10g}" for (x, y), c in zip(off, weights)]
+            continue
+        grid = np.zeros((int(extent[1]), int(extent[0])))
+        grid[off[:, 1] - lo[1], off[:, 0] - lo[0]] = weights
+        text += ["  vy={:+d}:  {}".format(int(lo[1]) + i, "  ".join(f"{c: .10g}" for c in row))
+                 for i, row in enumerate(grid)]
+    return "\n".join(text) + "\n"

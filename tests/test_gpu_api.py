@@ -183,3 +183,25 @@ def test_empty_inputs(cuda_dev, shape):
     raw = torch.from_numpy(np.zeros(shape, np.uint16)).to(cuda_dev)
     assert device.dequant_png16(raw, 256.0, 0).shape == (B, H, W)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("crop", [(0, 512), (3, 300), (4, 260)])
+def test_row_pitched_input(cuda_dev, dtype, crop):
+    """sn_oriented_points_strided: a column crop of wider frames (row pitch
+    ld > W; 16-byte-aligned pitches go to TMA directly, others through a
+    packed copy) gives the records of the same frames made contiguous."""
+    import torch
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(600, 96)
+    d = np.stack([scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.3, s) for s in (1, 2)])
+    full = torch.from_numpy(d).to(cuda_dev, dtype=getattr(torch, dtype))
+    c0, c1 = crop
+    view = full[:, :, c0:c1]
+    assert not view.is_contiguous()
+    m1 = torch.empty(view.shape, dtype=torch.uint8, device=cuda_dev)
+    m2 = torch.empty(view.shape, dtype=torch.uint8, device=cuda_dev)
+    a = device.oriented_points(view, sc.rig, 9, mask=m1)
+    b = device.oriented_points(view.contiguous(), sc.rig, 9, mask=m2)
+    assert torch.equal(m1, m2)
+    assert torch.equal(torch.nan_to_num(a, 7.0), torch.nan_to_num(b, 7.0))

@@ -159,3 +159,49 @@ def test_c_demo_builds_against_the_abi(tmp_path):
                     str(root / "examples" / "sn_demo.c"), f"-L{lib.parent}", "-lsn_b200",
                     f"-Wl,-rpath,{lib.parent}", "-lm", "-o", str(exe)], check=True)
     assert exe.exists()
+
+
+def _host_golden():
+    import json
+    from conftest import GOLDEN
+    return json.loads((GOLDEN / "host_cases.json").read_text())
+
+
+def test_format_kernel_dump_matches_reference():
+    """format_kernel_dump text identical to the reference's (kernels.py:264-296)."""
+    from paper_2504_15121_b200 import KernelSpec, build_kernels, format_kernel_dump
+    g = _host_golden()
+    specs = {"sq3": KernelSpec.square(3), "sq5": KernelSpec.square(5), "sq9": KernelSpec.square(9),
+             "cross4": KernelSpec(np.array([[1, 0], [-1, 0], [0, 1], [0, -1]])),
+             "sparse5": KernelSpec(np.array([[0, 0], [2, 1], [1, 2], [-2, -1], [3, -2]])),
+             "asym6": KernelSpec(np.array([[0, 0], [1, 0], [2, 0], [0, 1], [0, 2], [1, 1]]))}
+    for name, spec in specs.items():
+        assert format_kernel_dump(build_kernels(spec)) == g["dumps"][name], name
+
+
+def test_estimate_affine_direct_matches_reference():
+    """Single-pixel solves bit-identical to the reference (kernels.py:206-234)."""
+    from paper_2504_15121_b200 import KernelSpec, ScalarField, estimate_affine_direct
+    g = _host_golden()
+    d = np.array([[np.nan if x is None else x for x in row] for row in g["disparity"]])
+    d[0, 0] = np.inf
+    field = ScalarField.from_array(d)
+    specs = {"sq3": KernelSpec.square(3), "sq5": KernelSpec.square(5), "sq9": KernelSpec.square(9),
+             "cross4": KernelSpec(np.array([[1, 0], [-1, 0], [0, 1], [0, -1]])),
+             "sparse5": KernelSpec(np.array([[0, 0], [2, 1], [1, 2], [-2, -1], [3, -2]])),
+             "asym6": KernelSpec(np.array([[0, 0], [1, 0], [2, 0], [0, 1], [0, 2], [1, 1]]))}
+    for c in g["direct"]:
+        got = estimate_affine_direct(field, tuple(c["pixel"]), specs[c["spec"]])
+        want = tuple(float("nan") if x is None else x for x in (c["a1"], c["a2"]))
+        np.testing.assert_equal(np.array(got), np.array(want))
+
+
+def test_pfm_writers_match_reference_bytes():
+    import base64
+    from paper_2504_15121_b200 import NormalField, ScalarField, formats
+    g = _host_golden()
+    d = np.array([[np.nan if x is None else x for x in row] for row in g["disparity"]])
+    d[0, 0] = np.inf
+    assert formats.write_pfm(ScalarField.from_array(d)) == base64.b64decode(g["pfm"])
+    nf = NormalField.from_array(np.array(g["normals"]))
+    assert formats.write_pfm_normals(nf) == base64.b64decode(g["pfm_normals"])

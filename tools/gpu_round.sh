@@ -16,10 +16,10 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref
 fi
 if [ "${NCU:-1}" = "1" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file $O/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-extras > $O/ncu_launch_$TAG.log 2>&1
+  --log-file $O/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-extras --no-configs > $O/ncu_launch_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fixed_square -c 1 \
-  -o $O/fused_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-extras > $O/ncu_fused_$TAG.log 2>&1
+  -o $O/fused_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-extras --no-configs > $O/ncu_fused_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ccl_|passable_bits" -c 4 \
-  -o $O/ccl_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-extras > $O/ncu_ccl_$TAG.log 2>&1
+  -o $O/ccl_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-extras --no-configs > $O/ncu_ccl_$TAG.log 2>&1
 fi
 ls -la $O
