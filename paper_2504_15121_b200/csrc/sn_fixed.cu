@@ -783,8 +783,52 @@ __global__ void __launch_bounds__(kFastThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
-// generic path: any offset pattern, any shape (thread per pixel, direct sums)
+// generic path: any offset pattern, any shape (direct sums U = sum vx d,
+// V = sum vy d in fp64, in the pattern's order)
 
+// the record / affine output of one pixel from its sums (shared by both
+// generic kernels)
+template <typename T, bool AFFINE>
+__device__ __forceinline__ void generic_out(int64_t idx, int64_t x, int64_t y, T dc, bool ok,
+                                            double U, double V, const FixedParams& p,
+                                            float* __restrict__ out6, uint8_t* __restrict__ mask,
+                                            double* __restrict__ a1, double* __restrict__ a2) {
+  const double dcd = (double)dc;
+  const double Up = U - p.sx * dcd;
+  const double Vp = V - p.sy * dcd;
+  const double P1 = p.gamma * Up - p.beta * Vp;  // det * dd/du
+  const double P2 = p.alpha * Vp - p.beta * Up;  // det * dd/dv
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  if (AFFINE) {
+    a1[idx] = ok ? 1.0 + P1 / p.det : qnan;
+    a2[idx] = ok ? P2 / p.det : qnan;
+    if (mask) mask[idx] = ok ? 1 : 0;
+  } else {
+    const bool valid = ok && (dc > (T)0);
+    float px, py, pz, nx, ny, nz;
+    if constexpr (sizeof(T) == 4) {
+      const float du_f = ((float)x - p.u0_hi) - p.u0_lo;
+      const float dv_f = ((float)(y + p.row0) - p.v0_hi) - p.v0_lo;
+      point_from_disparity((float)dc, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
+    } else {
+      point_from_disparity_f64(dcd, (double)x - p.u0, (double)(y + p.row0) - p.v0, p, px, py, pz);
+    }
+    if (valid) {
+      normal_from_moments(P1, P2, p.det, dcd, (double)x - p.u0, (double)(y + p.row0) - p.v0, p.fx,
+                          p.fy, nx, ny, nz);
+    } else {
+      nx = ny = nz = __int_as_float(0x7fc00000);
+    }
+    float* o6 = out6 + idx * 6;
+    reinterpret_cast<float2*>(o6)[0] = make_float2(px, py);
+    reinterpret_cast<float2*>(o6)[1] = make_float2(pz, nx);
+    reinterpret_cast<float2*>(o6)[2] = make_float2(ny, nz);
+    if (mask) mask[idx] = valid ? 1 : 0;
+  }
+}
+
+// thread per pixel, samples straight from global memory (patterns whose
+// bounding box does not fit the tiled kernel's shared memory)
 template <typename T, bool AFFINE>
 __global__ void __launch_bounds__(256)
     fixed_generic_kernel(const T* __restrict__ disp, const FixedParams p,
@@ -819,39 +863,90 @@ __global__ void __launch_bounds__(256)
       U = fma((double)o.x, (double)v, U);
       V = fma((double)o.y, (double)v, V);
     }
-    const double dcd = (double)dc;
-    const double Up = U - p.sx * dcd;
-    const double Vp = V - p.sy * dcd;
-    const double P1 = p.gamma * Up - p.beta * Vp;  // det * dd/du
-    const double P2 = p.alpha * Vp - p.beta * Up;  // det * dd/dv
-    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-    if (AFFINE) {
-      a1[idx] = ok ? 1.0 + P1 / p.det : qnan;
-      a2[idx] = ok ? P2 / p.det : qnan;
-      if (mask) mask[idx] = ok ? 1 : 0;
-    } else {
-      const bool valid = ok && (dc > (T)0);
-      float px, py, pz, nx, ny, nz;
-      if constexpr (sizeof(T) == 4) {
-        const float du_f = ((float)x - p.u0_hi) - p.u0_lo;
-        const float dv_f = ((float)(y + p.row0) - p.v0_hi) - p.v0_lo;
-        point_from_disparity((float)dc, du_f, dv_f, p.fxb_f, p.inv_fx_f, p.inv_fy_f, px, py, pz);
-      } else {
-        point_from_disparity_f64(dcd, (double)x - p.u0, (double)(y + p.row0) - p.v0, p, px, py,
-                                 pz);
-      }
-      if (valid) {
-        normal_from_moments(P1, P2, p.det, dcd, (double)x - p.u0, (double)(y + p.row0) - p.v0, p.fx, p.fy, nx,
-                            ny, nz);
-      } else {
-        nx = ny = nz = __int_as_float(0x7fc00000);
-      }
-      float* o6 = out6 + idx * 6;
-      reinterpret_cast<float2*>(o6)[0] = make_float2(px, py);
-      reinterpret_cast<float2*>(o6)[1] = make_float2(pz, nx);
-      reinterpret_cast<float2*>(o6)[2] = make_float2(ny, nz);
-      if (mask) mask[idx] = valid ? 1 : 0;
+    generic_out<T, AFFINE>(idx, x, y, dc, ok, U, V, p, out6, mask, a1, a2);
+  }
+}
+
+// Tiled generic kernel: one 32 x 16 block of a frame per CTA, the block plus
+// the pattern's bounding box staged in shared memory as fp64 (coalesced
+// loads, each sample read once from global memory), the pattern as (weights,
+// linear shared-memory offsets) in shared memory; a thread sums its two
+// pixels' supports from shared memory in the pattern's order.  A pixel is
+// valid iff its support box lies in the frame and every sample (and the
+// centre) is finite: for fp32 samples the fp64 sums carry any non-finite
+// sample (NaN, or inf times any weight) and never overflow, so finite sums
+// are the test; fp64 samples are tested one by one.
+constexpr int kGTW = 32, kGTH = 16;
+
+struct GenericGeom {
+  int minx, maxx, miny, maxy;  // pattern extents (validity)
+  int bx, by, bw, bh;          // staged box: origin offset (<= 0) and size, pattern + centre
+};
+
+// staged box rounded up to whole 16-byte units: the weight pairs follow it
+__host__ __device__ inline int generic_box(const GenericGeom& g) {
+  return ((kGTW + g.bw) * (kGTH + g.bh) + 1) & ~1;
+}
+__host__ __device__ inline size_t generic_smem(const GenericGeom& g, int n) {
+  return (size_t)generic_box(g) * 8 + (size_t)n * 20;
+}
+
+template <typename T, bool AFFINE>
+__global__ void __launch_bounds__(256)
+    fixed_generic_tiled_kernel(const T* __restrict__ disp, const FixedParams p,
+                               const __grid_constant__ OffsetTable tab, const GenericGeom g,
+                               float* __restrict__ out6, uint8_t* __restrict__ mask,
+                               double* __restrict__ a1, double* __restrict__ a2) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  const int SW = kGTW + g.bw, SH = kGTH + g.bh;  // staged box
+  double* tile = reinterpret_cast<double*>(gsm);
+  double2* wt = reinterpret_cast<double2*>(tile + generic_box(g));
+  int* lin = reinterpret_cast<int*>(wt + tab.n);
+  const int tid = threadIdx.x;
+  const int W = (int)p.W, H = (int)p.H;
+  const int tiles_x = (W + kGTW - 1) / kGTW, tiles_y = (H + kGTH - 1) / kGTH;
+  const int64_t bt = blockIdx.x;
+  const int tx = (int)(bt % tiles_x);
+  const int64_t rest = bt / tiles_x;
+  const int ty = (int)(rest % tiles_y);
+  const int64_t f = rest / tiles_y;
+  const int x0 = tx * kGTW, y0 = ty * kGTH;
+  const T* frame = disp + f * p.H * p.W;
+  for (int i = tid; i < tab.n; i += 256) {
+    const int2 o = tab.v[i];
+    wt[i] = make_double2((double)o.x, (double)o.y);
+    lin[i] = o.y * SW + o.x;
+  }
+  // the staged box, rows / columns clamped into the frame (samples of
+  // out-of-frame positions only ever feed invalid pixels)
+  for (int i = tid; i < SW * SH; i += 256) {
+    const int r = i / SW, c = i - r * SW;
+    const int yy = min(max(y0 + g.by + r, 0), H - 1), xx = min(max(x0 + g.bx + c, 0), W - 1);
+    tile[i] = (double)frame[(int64_t)yy * W + xx];
+  }
+  __syncthreads();
+  const int cx = tid & (kGTW - 1);
+#pragma unroll 1
+  for (int cy = tid / kGTW; cy < kGTH; cy += 256 / kGTW) {
+    const int x = x0 + cx, y = y0 + cy;
+    if (x >= W || y >= H) continue;
+    const double* c = tile + (cy - g.by) * SW + (cx - g.bx);  // the centre sample
+    const T dc = (T)c[0];
+    bool ok = finite_t(dc) && x + g.minx >= 0 && x + g.maxx < W && y + g.miny >= 0 &&
+              y + g.maxy < H;
+    double U = 0.0, V = 0.0;
+    bool fin = true;
+    for (int i = 0; i < tab.n; ++i) {
+      const double v = c[lin[i]];
+      const double2 w2 = wt[i];
+      if constexpr (sizeof(T) == 8) fin &= fabs(v) <= 1.7976931348623157e308;
+      U = fma(w2.x, v, U);
+      V = fma(w2.y, v, V);
     }
+    if constexpr (sizeof(T) == 8) ok = ok && fin;
+    else ok = ok && fabs(U) <= 1.7976931348623157e308 && fabs(V) <= 1.7976931348623157e308;
+    generic_out<T, AFFINE>(f * p.H * p.W + (int64_t)y * W + x, x, y, dc, ok, U, V, p, out6, mask,
+                           a1, a2);
   }
 }
 
@@ -987,6 +1082,32 @@ static int launch_generic(const LaunchCtx& ctx, const T* disp, const FixedParams
                           double* a2, bool affine) {
   const int64_t total = p.B * p.H * p.W;
   if (total == 0) return SN_OK;
+  // the tiled kernel when the staged box fits 96 KB of shared memory
+  GenericGeom g{0, 0, 0, 0, 0, 0, 0, 0};
+  if (tab.n > 0) {  // extents of the pattern itself (validity); the box also holds the centre
+    g.minx = g.maxx = tab.v[0].x;
+    g.miny = g.maxy = tab.v[0].y;
+    for (int i = 1; i < tab.n; ++i) {
+      g.minx = std::min(g.minx, tab.v[i].x);
+      g.maxx = std::max(g.maxx, tab.v[i].x);
+      g.miny = std::min(g.miny, tab.v[i].y);
+      g.maxy = std::max(g.maxy, tab.v[i].y);
+    }
+  }
+  g.bx = std::min(g.minx, 0);
+  g.by = std::min(g.miny, 0);
+  g.bw = std::max(g.maxx, 0) - g.bx;
+  g.bh = std::max(g.maxy, 0) - g.by;
+  const size_t sm = (g.bw < 4096 && g.bh < 4096) ? generic_smem(g, tab.n) : SIZE_MAX;
+  const int64_t tiles = p.B * ((p.H + kGTH - 1) / kGTH) * ((p.W + kGTW - 1) / kGTW);
+  if (sm <= 96 * 1024 && tiles < 0x7fffffffLL) {
+    auto kern = affine ? fixed_generic_tiled_kernel<T, true> : fixed_generic_tiled_kernel<T, false>;
+    if (ensure_dyn_smem(reinterpret_cast<const void*>(kern), 96 * 1024, ctx.device,
+                        "fixed_generic_tiled_kernel"))
+      return SN_ECUDA;
+    kern<<<(unsigned)tiles, 256, sm, ctx.stream>>>(disp, p, tab, g, out6, mask, a1, a2);
+    return check_launch("fixed_generic_tiled_kernel");
+  }
   int64_t grid = (total + 255) / 256;
   const int64_t cap = (int64_t)ctx.num_sms * 8;
   if (grid > cap) grid = cap;
