@@ -415,7 +415,10 @@ def other_configs(dev, rank, world, disp_buf, out_buf, lab_buf, ws, bits_buf):
     res = {}
 
     def ev_time(fn, reps, flush=None):
-        tot = 0.0
+        # every repetition (flush, events, launches) is enqueued before one
+        # synchronisation: the host runs ahead, so the events bracket device
+        # time only, not the host's per-call launch cost
+        evs = []
         for _ in range(reps):
             if flush is not None:
                 flush()
@@ -423,9 +426,9 @@ def other_configs(dev, rank, world, disp_buf, out_buf, lab_buf, ws, bits_buf):
             e0.record(stream)
             fn()
             e1.record(stream)
-            torch.cuda.synchronize()
-            tot += e0.elapsed_time(e1)
-        return tot / reps
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs) / reps
 
     # C2: 2888x1920 sphere, one frame, full pipeline; L2 flushed before each rep
     sp = scenes.sphere_scene(2888, 1920)

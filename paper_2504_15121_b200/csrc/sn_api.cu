@@ -14,7 +14,9 @@
 #include <cstdlib>
 #include <mutex>
 #include <numeric>
+#include <map>
 #include <set>
+#include <tuple>
 #include <thread>
 #include <unordered_map>
 #include <vector>
@@ -55,6 +57,23 @@ int ensure_dyn_smem(const void* func, int bytes, int device, const char* name) {
                      cudaGetErrorString(cudaGetLastError()));
   done.insert({func, device});
   return SN_OK;
+}
+
+int occupancy_per_sm(const void* func, int threads, size_t smem, int device) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(func, threads, smem, device);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  if (per_sm < 1) per_sm = 1;
+  cache.emplace(key, per_sm);
+  return per_sm;
 }
 
 // A private stream-ordered pool per device: its release threshold keeps the

@@ -981,11 +981,8 @@ static int launch_square(const LaunchCtx& ctx, const T* disp, const FixedParams&
   if (ensure_dyn_smem(reinterpret_cast<const void*>(kern), (int)Cfg::TOTAL, ctx.device,
                       "fixed_square_kernel"))
     return SN_ECUDA;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFastThreads, Cfg::TOTAL) !=
-      cudaSuccess)
-    return set_cuda_error("occupancy query");
-  if (per_sm < 1) per_sm = 1;
+  const int per_sm =
+      occupancy_per_sm(reinterpret_cast<const void*>(kern), kFastThreads, Cfg::TOTAL, ctx.device);
   int64_t grid = (int64_t)per_sm * ctx.num_sms;
   if (grid > n_items) grid = n_items;
   kern<<<(unsigned)grid, kFastThreads, Cfg::TOTAL, ctx.stream>>>(in_map, p, mask, out6, out_pitch,

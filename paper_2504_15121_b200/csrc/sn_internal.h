@@ -23,6 +23,8 @@ int check_launch(const char* what);
 // cudaFuncAttributeMaxDynamicSharedMemorySize is per device: set once per
 // (kernel, device) pair, under a lock (the caller has made `device` current)
 int ensure_dyn_smem(const void* func, int bytes, int device, const char* name);
+// resident blocks per SM of a kernel launch shape, queried once per device
+int occupancy_per_sm(const void* func, int threads, size_t smem, int device);
 // stream-ordered scratch from the library's private per-device pool
 int scratch_alloc(const LaunchCtx& ctx, size_t bytes, void** ptr);
 void scratch_free(const LaunchCtx& ctx, void* ptr);

@@ -18,6 +18,7 @@ Reference functions these replace (pkg/src/stereonorm):
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import numpy as np
 import torch
@@ -26,13 +27,22 @@ from . import _native
 from ._native import check
 
 
+@functools.lru_cache(maxsize=64)
+def _square_offsets(width: int) -> np.ndarray:
+    from .kernels import KernelSpec  # local: avoid import cycle
+    off = _native.offsets_array(KernelSpec.square(width).offsets)
+    off.setflags(write=False)
+    return off
+
+
 def _offsets_of(kernels) -> np.ndarray:
     from .kernels import PrecomputedKernels, KernelSpec  # local: avoid import cycle
     if isinstance(kernels, PrecomputedKernels):
         return _native.offsets_array(kernels.spec.offsets)
     if isinstance(kernels, KernelSpec):
         return _native.offsets_array(kernels.offsets)
-    return _native.offsets_array(KernelSpec.square(int(kernels)).offsets)
+    # an odd square width: the pattern is built (and validated) once per width
+    return _square_offsets(int(kernels))
 
 
 def _batched(disp: torch.Tensor, name: str = "disparity") -> torch.Tensor:
