@@ -57,7 +57,7 @@ extern "C" {
 #define SN_EDEGENERATE 2 /* collinear offset pattern    -> DegenerateSupportError */
 #define SN_ECUDA 3       /* CUDA / driver failure       -> RuntimeError           */
 
-#define SN_ABI_VERSION 1
+#define SN_ABI_VERSION 2
 
 typedef struct sn_rig {
   double fx, fy, u0, v0, baseline; /* geometry.py:22-36 (StereoRig) */

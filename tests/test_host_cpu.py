@@ -22,7 +22,7 @@ def test_library_exports_every_header_symbol():
     for n in names:
         assert hasattr(lib, n), n
         assert n in _native.SIGNATURES, f"{n} has no ctypes signature"
-    assert lib.sn_abi_version() == 1
+    assert lib.sn_abi_version() == 2
 
 
 def test_kernel_moments_match_build_kernels():
