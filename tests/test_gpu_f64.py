@@ -166,3 +166,70 @@ def test_fp32_inputs_unchanged(cuda_dev):
         assert torch.equal(device.passable_bits(d32, sc.rig, t), device.passable_bits(d64, sc.rig, t))
         assert torch.equal(device.component_labels(d32, sc.rig, t),
                            device.component_labels(d64, sc.rig, t))
+
+
+@pytest.mark.parametrize("pick", ["ties", "out_of_fp32_range", "tiny_shapes"])
+def test_f64_filter_edge_cases(cuda_dev, pick):
+    """fp64 inputs the fp32 filter cannot decide: thresholds equal to edge
+    values of float64 disparities that fp32 cannot represent, samples outside
+    fp32's range (1e-300, 1e300, fp64 subnormals, -0.0, +-inf), and frames
+    too small to hold an interior pixel -- bits, labels, pipeline and the
+    star-fill masks all equal the oracle's fp64 decisions."""
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import StarConfig, device, scenes
+    shapes = [(96, 200)] if pick != "tiny_shapes" else [(1, 1), (2, 2), (3, 3), (3, 40), (40, 3),
+                                                        (4, 5)]
+    for H, W in shapes:
+        sc = scenes.street_scene(max(W, 8), max(H, 8))
+        d = scenes.add_gaussian_noise(scenes.raycast(sc)[0], 0.7, 11)[:H, :W].copy()
+        rng = np.random.default_rng(H * 1000 + W)
+        if pick == "out_of_fp32_range":
+            sel = rng.random(d.shape)
+            d[sel < 0.02] = 1e-300
+            d[(sel >= 0.02) & (sel < 0.04)] = 1e300
+            d[(sel >= 0.04) & (sel < 0.05)] = 5e-324
+            d[(sel >= 0.05) & (sel < 0.06)] = -0.0
+            d[(sel >= 0.06) & (sel < 0.07)] = np.inf
+            d[(sel >= 0.07) & (sel < 0.08)] = -np.inf
+            d[(sel >= 0.08) & (sel < 0.09)] = np.nan
+            d[(sel >= 0.09) & (sel < 0.10)] = 3.0e-39  # fp32 subnormal range
+        o = orc.Rig(sc.rig.fx, sc.rig.fy, sc.rig.u0, sc.rig.v0, sc.rig.baseline)
+        e, em = orc.depth_laplacian(*orc.depth_field(d, o))
+        ts = [0.05, 0.2, 1.0]
+        if pick == "ties" and em.any():
+            vals = np.sort(e[em])
+            ts += [float(vals[len(vals) // 5]), float(vals[len(vals) // 2]), float(vals[-1])]
+        dt = torch.from_numpy(d).to(cuda_dev)
+        for t in ts:
+            want = orc.passable(d, o, t)
+            got = _bits_to_bool(device.passable_bits(dt, sc.rig, t), W)[0]
+            assert np.array_equal(got, want), (H, W, t)
+            lab = device.component_labels(dt, sc.rig, t)[0].cpu().numpy().astype(np.int64)
+            assert np.array_equal(lab, orc.ccl_labels(d, o, t)), (H, W, t)
+            if H * W >= 9:
+                _, lab2 = device.pipeline(dt, sc.rig, 3, t)
+                assert np.array_equal(lab2[0].cpu().numpy().astype(np.int64), lab), (H, W, t)
+        for cfg in (orc.Star(stop="st", threshold=0.5), orc.Star(stop="cd", threshold=0.1)):
+            n_ref, ok_ref = orc.estimate_normals_adaptive(d, o, cfg)
+            mask = torch.empty((1, H, W), dtype=torch.uint8, device=cuda_dev)
+            device.adaptive_points(dt, sc.rig, StarConfig(stop=cfg.stop, threshold=cfg.threshold),
+                                   mask=mask)
+            assert np.array_equal(mask[0].cpu().numpy().astype(bool), ok_ref), (H, W, cfg)
+
+
+@pytest.mark.parametrize("shape", [(0, 16, 32), (2, 0, 32), (2, 16, 0)])
+def test_empty_inputs_f64(cuda_dev, shape):
+    from paper_2504_15121_b200 import StarConfig, StereoRig, device
+    rig = StereoRig(100.0, 100.0, 8.0, 8.0, 0.2)
+    d = torch.empty(shape, dtype=torch.float64, device=cuda_dev)
+    B, H, W = shape
+    assert device.oriented_points(d, rig, 3).shape == (B, H, W, 6)
+    assert device.passable_bits(d, rig, 0.2).shape == (B, H, device.bit_words(W))
+    assert device.component_labels(d, rig, 0.2).shape == (B, H, W)
+    pts, lab = device.pipeline(d, rig, 3, 0.2)
+    assert pts.shape == (B, H, W, 6) and lab.shape == (B, H, W)
+    assert device.adaptive_points(d, rig, StarConfig(stop="st", threshold=0.1)).shape == (B, H, W, 6)
+    p8, e = device.passable(d, rig, 0.2, edges=torch.empty(shape, dtype=torch.float64,
+                                                             device=cuda_dev))
+    assert p8.shape == (B, H, W) and e.shape == (B, H, W)
+    torch.cuda.synchronize()
