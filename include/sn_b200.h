@@ -289,6 +289,18 @@ SN_API int sn_depth_laplacian_f64(sn_plan_t* plan, const double* depth, const ui
 SN_API int sn_seam_merge_host(const int32_t* seams, int32_t n_strips, int64_t W, int32_t* map_keys,
                        int32_t* map_vals, int32_t* n_map);
 
+/* The same merge on the device, with no host round trip (the multi-GPU strip
+ * path: the all-gathered rows stay in device memory).  seams: device
+ * [n_strips][2][W] int32; table: device int32[table_n] with table_n > every
+ * label value (the frame's pixel count); on return table[v] is the root of
+ * every label v on a seam, -1 elsewhere.  sn_relabel_table then maps a
+ * strip's labels in place: v -> table[v] where that is >= 0.  Deterministic
+ * (min-root links) and identical on every rank. */
+SN_API int sn_seam_merge(sn_plan_t* plan, const int32_t* seams, int32_t n_strips, int64_t W,
+                  int32_t* table, int64_t table_n, void* stream);
+SN_API int sn_relabel_table(sn_plan_t* plan, int32_t* labels, int64_t n, const int32_t* table,
+                     int64_t table_n, void* stream);
+
 /* Apply a (label -> root) map to a strip's label grid in place (device).
  * Labels of the strip are global raster indices in [index_base,
  * index_base + n); scratch is an int32 device buffer of n elements. */

@@ -118,6 +118,8 @@ SIGNATURES = {
     "sn_triangulate_grid_f64": [_P, _P, _I64, _I64, _I64, _RIGP, _P, _P],
     "sn_depth_laplacian_f64": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P],
     "sn_relabel": [_P, _P, _I64, _I64, _P, _P, _P, _I32, _P, _P],
+    "sn_seam_merge": [_P, _P, _I32, _I64, _P, _I64, _P],
+    "sn_relabel_table": [_P, _P, _I64, _P, _I64, _P],
 }
 _RESTYPES = {"sn_last_error": ctypes.c_char_p}
 

@@ -1163,6 +1163,25 @@ int sn_relabel(sn_plan_t* plan, int32_t* labels, int64_t n, int64_t index_base,
                      map_capacity, scratch);
 }
 
+int sn_seam_merge(sn_plan_t* plan, const int32_t* seams, int32_t n_strips, int64_t W,
+                  int32_t* table, int64_t table_n, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  if (n_strips < 0 || W < 0 || table_n < 0 || W > 0x7fffffffLL)
+    return set_error(SN_EINVAL, "bad seam-merge arguments");
+  if ((int64_t)n_strips * W > 0 && (!seams || !table)) return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_seam_merge(make_ctx(plan, stream), seams, n_strips, W, table, table_n);
+}
+
+int sn_relabel_table(sn_plan_t* plan, int32_t* labels, int64_t n, const int32_t* table,
+                     int64_t table_n, void* stream) {
+  if (!plan) return set_error(SN_EINVAL, "plan is NULL");
+  if (n < 0 || table_n < 0) return set_error(SN_EINVAL, "negative size");
+  if (n > 0 && (!labels || !table)) return set_error(SN_EINVAL, "NULL buffer");
+  DeviceGuard g(plan->device);
+  return run_relabel_table(make_ctx(plan, stream), labels, n, table, table_n);
+}
+
 // Strip-seam merge on gathered boundary rows (host memory; tiny: 2 rows per
 // strip).  Union-find over label values with min-root links, so the map is
 // independent of gather order and identical on every rank.

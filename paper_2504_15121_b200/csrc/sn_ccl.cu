@@ -1011,6 +1011,89 @@ template int run_ccl<float>(const LaunchCtx&, const float*, const uint8_t*, cons
 template int run_ccl<double>(const LaunchCtx&, const double*, const uint8_t*, const CclParams&,
                              int64_t, int32_t*, void*, size_t, const uint32_t*);
 
+// ---------------------------------------------------------------------------
+// strip seams on the device: the gathered first / last owned
+// label rows of every strip ([n_strips][2][W], global raster indices) are
+// merged with the labeller's own min-root union-find, on a table indexed by
+// label value (entries of labels that are not on a seam stay -1), then every
+// strip relabels its pixels through the table.  Deterministic: the roots are
+// the minimum labels, whatever the order of the unions -- every rank builds
+// the same table from the same gathered rows, with no host round trip.
+
+__global__ void seam_init_kernel(const int32_t* __restrict__ seams, int64_t n, int32_t* table) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = seams[i];
+    if (v >= 0) table[v] = v;
+  }
+}
+
+// position u of seam s: strip s's last row against strip s+1's first row,
+// 8-connected (the straight neighbour, else both diagonals)
+__global__ void seam_unite_kernel(const int32_t* __restrict__ seams, int n_strips, int W,
+                                  int32_t* table) {
+  const int64_t total = (int64_t)(n_strips - 1) * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(i / W), u = (int)(i - (int64_t)s * W);
+    const int32_t* a = seams + ((int64_t)s * 2 + 1) * W;   // last owned row of strip s
+    const int32_t* b = seams + ((int64_t)s + 1) * 2 * W;   // first owned row of strip s+1
+    const int32_t x = a[u];
+    if (x < 0) continue;
+    if (b[u] >= 0) {
+      if (b[u] != x) uf_unite(table, x, b[u]);
+    } else {
+      if (u > 0 && b[u - 1] >= 0 && b[u - 1] != x) uf_unite(table, x, b[u - 1]);
+      if (u + 1 < W && b[u + 1] >= 0 && b[u + 1] != x) uf_unite(table, x, b[u + 1]);
+    }
+  }
+}
+
+__global__ void seam_compress_kernel(const int32_t* __restrict__ seams, int64_t n, int32_t* table) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = seams[i];
+    if (v >= 0) table[v] = uf_root(table, v);
+  }
+}
+
+__global__ void relabel_table_kernel(int32_t* __restrict__ labels, int64_t n,
+                                     const int32_t* __restrict__ table, int64_t table_n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = labels[i];
+    if (v >= 0 && v < table_n) {
+      const int32_t r = __ldg(table + v);
+      if (r >= 0) labels[i] = r;
+    }
+  }
+}
+
+int run_seam_merge(const LaunchCtx& ctx, const int32_t* seams, int n_strips, int64_t W,
+                   int32_t* table, int64_t table_n) {
+  if (table_n > 0 && cudaMemsetAsync(table, 0xff, (size_t)table_n * 4, ctx.stream) != cudaSuccess)
+    return set_cuda_error("cudaMemsetAsync(seam table)");
+  const int64_t n = (int64_t)n_strips * 2 * W;
+  if (n == 0) return SN_OK;
+  seam_init_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(seams, n, table);
+  int rc = check_launch("seam_init_kernel");
+  if (rc) return rc;
+  if (n_strips > 1) {
+    seam_unite_kernel<<<grid_for(ctx, (int64_t)(n_strips - 1) * W, 256), 256, 0, ctx.stream>>>(
+        seams, n_strips, (int)W, table);
+    if ((rc = check_launch("seam_unite_kernel"))) return rc;
+  }
+  seam_compress_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(seams, n, table);
+  return check_launch("seam_compress_kernel");
+}
+
+int run_relabel_table(const LaunchCtx& ctx, int32_t* labels, int64_t n, const int32_t* table,
+                      int64_t table_n) {
+  if (n == 0) return SN_OK;
+  relabel_table_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx.stream>>>(labels, n, table, table_n);
+  return check_launch("relabel_table_kernel");
+}
+
 int run_relabel(const LaunchCtx& ctx, int32_t* labels, int64_t n, int64_t base,
                 const int32_t* keys, const int32_t* vals, const int32_t* n_map, int32_t cap,
                 int32_t* scratch) {

@@ -75,6 +75,10 @@ int run_passable_bits(const LaunchCtx& ctx, const T* disp, const FixedParams& p,
                       uint32_t* bits);
 // host-side fill of the predicate fields of FixedParams
 void fill_predicate(FixedParams& p, double fxb, double t, uint32_t* bits);
+int run_seam_merge(const LaunchCtx& ctx, const int32_t* seams, int n_strips, int64_t W,
+                   int32_t* table, int64_t table_n);
+int run_relabel_table(const LaunchCtx& ctx, int32_t* labels, int64_t n, const int32_t* table,
+                      int64_t table_n);
 int run_relabel(const LaunchCtx& ctx, int32_t* labels, int64_t n, int64_t base,
                 const int32_t* keys, const int32_t* vals, const int32_t* n_map, int32_t cap,
                 int32_t* scratch);

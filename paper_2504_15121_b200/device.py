@@ -556,3 +556,33 @@ def seam_merge(seams: np.ndarray):
                                            vals.ctypes.data, ctypes.byref(n))
     check(rc, "seam_merge")
     return keys[:n.value].copy(), vals[:n.value].copy()
+
+
+def seam_table(seams: torch.Tensor, table_n: int, *, table=None) -> torch.Tensor:
+    """Device seam merge (sn_seam_merge): ``seams`` int32 ``[n_strips, 2, W]``
+    on the device (the gathered first/last owned label rows); returns the
+    int32 table of ``table_n`` entries mapping every seam label to its root
+    (-1 elsewhere) -- identical on every rank, no host round trip."""
+    if not seams.is_cuda or seams.dtype != torch.int32 or seams.dim() != 3 or seams.shape[1] != 2:
+        raise ValueError("seams must be an int32 CUDA tensor [n_strips, 2, W]")
+    seams = seams.contiguous()
+    dev = seams.device
+    table = _check_out(table, (int(table_n),), torch.int32, dev, "table")
+    n_strips, _, W = seams.shape
+    rc = _native.load().sn_seam_merge(_native.plan(dev.index), seams.data_ptr(), n_strips, W,
+                                      table.data_ptr(), int(table_n), _stream(dev))
+    check(rc, "seam_table")
+    return table
+
+
+def relabel_table(labels: torch.Tensor, table: torch.Tensor) -> torch.Tensor:
+    """In place: every label v >= 0 with table[v] >= 0 becomes table[v]."""
+    if not labels.is_cuda or labels.dtype != torch.int32 or not labels.is_contiguous():
+        raise ValueError("labels must be a contiguous int32 CUDA tensor")
+    if table.dtype != torch.int32 or table.device != labels.device:
+        raise ValueError("table must be an int32 tensor on the labels' device")
+    dev = labels.device
+    rc = _native.load().sn_relabel_table(_native.plan(dev.index), labels.data_ptr(), labels.numel(),
+                                         table.data_ptr(), table.numel(), _stream(dev))
+    check(rc, "relabel_table")
+    return labels

@@ -17,9 +17,12 @@ and the same contract holds across GPU counts:
   rows; labels are computed on the owned rows (predicate on the extended
   block) with global raster indices, then merged across the seams:
   every rank contributes its first and last owned label rows to one
-  all-gather (2 x W int32 per rank), runs the same deterministic min-root
-  union-find (``sn_seam_merge_host``) and remaps its labels on the device
-  (``sn_relabel``).  That gather is the only collective of the path.
+  all-gather (2 x W int32 per rank, into device memory), runs the same
+  deterministic min-root union-find over them on its device
+  (``sn_seam_merge``: no host round trip) and remaps its labels there
+  (``sn_relabel_table``).  That gather is the only collective of the path.
+  (``sn_seam_merge_host`` is the same merge on the host, used by the CPU
+  tests.)
 """
 
 from __future__ import annotations
@@ -109,16 +112,26 @@ def exchange_halo(owned, plan: StripPlan, rank: int, group=None):
     return block
 
 
-def gather_seams(labels_owned, world: int, group=None) -> np.ndarray:
-    """All-gather every rank's first and last owned label rows: int32
-    ``[world, 2, W]`` on the host, identical on every rank."""
+def gather_seams_device(labels_owned, world: int, group=None):
+    """All-gather every rank's first and last owned label rows into one int32
+    ``[world, 2, W]`` tensor on this rank's device (NCCL over NVLink on a GPU
+    box), identical on every rank."""
     import torch
     import torch.distributed as dist
 
     edge = torch.stack([labels_owned[0], labels_owned[-1]]).to(torch.int32).contiguous()
-    parts = [torch.empty_like(edge) for _ in range(world)]
-    dist.all_gather(parts, edge, group=group)
-    return torch.stack(parts).cpu().numpy()
+    if not edge.is_cuda:  # gloo (the CPU tests): the list form
+        parts = [torch.empty_like(edge) for _ in range(world)]
+        dist.all_gather(parts, edge, group=group)
+        return torch.stack(parts)
+    out = torch.empty((world,) + tuple(edge.shape), dtype=torch.int32, device=edge.device)
+    dist.all_gather_into_tensor(out, edge, group=group)
+    return out
+
+
+def gather_seams(labels_owned, world: int, group=None) -> np.ndarray:
+    """The gathered seam rows on the host (int32 ``[world, 2, W]``)."""
+    return gather_seams_device(labels_owned, world, group).cpu().numpy()
 
 
 def seam_map(labels_owned, world: int, group=None) -> tuple[np.ndarray, np.ndarray]:
@@ -173,14 +186,22 @@ def distributed_strip_frame(owned, plan: StripPlan, rig, kernels=9, threshold: f
     for the owned rows -- bit-identical to the whole-frame result."""
     import torch.distributed as dist
 
+    from . import device
+
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     if world != plan.n_strips:
         raise ValueError("one strip per rank")
     block = exchange_halo(owned, plan, rank, group)
     pts, lab = strip_pass(block, plan, rank, rig, kernels, threshold)
-    keys, vals = seam_map(lab, world, group)
-    apply_seam_map(lab, plan, rank, keys, vals)
+    if lab.is_cuda:
+        # the merge on the device: all-gather, min-root union-find over the
+        # seams, relabel -- no host round trip
+        seams = gather_seams_device(lab, world, group)
+        device.relabel_table(lab, device.seam_table(seams, plan.height * plan.width))
+    else:  # CPU tensors (gloo tests): the host merge
+        keys, vals = seam_map(lab, world, group)
+        apply_seam_map(lab, plan, rank, keys, vals)
     return pts, lab
 
 
@@ -189,7 +210,6 @@ def local_strip_frame(disp, plan: StripPlan, rig, kernels=9, threshold: float = 
     waiting): exercises the strip path -- block slicing, per-strip passes,
     seam merge, relabel -- against the whole-frame result on a single GPU."""
     import torch
-    from .device import seam_merge
 
     if disp.dim() != 2:
         raise ValueError("disp must be one [H, W] frame")
@@ -199,8 +219,9 @@ def local_strip_frame(disp, plan: StripPlan, rig, kernels=9, threshold: float = 
         p_s, l_s = strip_pass(disp[b0:b1].contiguous(), plan, s, rig, kernels, threshold)
         pts.append(p_s)
         labs.append(l_s)
-    seams = np.stack([torch.stack([l[0], l[-1]]).cpu().numpy() for l in labs]).astype(np.int32)
-    keys, vals = seam_merge(seams)
-    for s, l in enumerate(labs):
-        apply_seam_map(l, plan, s, keys, vals)
+    from . import device
+    seams = torch.stack([torch.stack([lab[0], lab[-1]]) for lab in labs]).to(torch.int32)
+    table = device.seam_table(seams, plan.height * plan.width)
+    for lab in labs:
+        device.relabel_table(lab, table)
     return torch.cat(pts), torch.cat(labs)

@@ -96,3 +96,31 @@ def test_c5_eight_strips(cuda_dev):
     okc = ok[4:-4]
     assert np.array_equal(np.isfinite(got[..., 3:]).all(-1), okc)
     assert max_angle_deg(got[okc][:, 3:], ref6[4:-4][okc][:, 3:]) < 1e-4
+
+
+def test_device_seam_merge_matches_host(cuda_dev):
+    """sn_seam_merge (device, the multi-GPU strip path's merge) gives the
+    same roots as sn_seam_merge_host for every seam label, on random seam
+    rows with 8-connected contacts, including labels that chain across
+    several strips."""
+    from paper_2504_15121_b200 import device
+    rng = np.random.default_rng(3)
+    for n_strips, W in ((2, 64), (5, 300), (8, 7680)):
+        H = n_strips * 10
+        seams = np.full((n_strips, 2, W), -1, np.int32)
+        for s in range(n_strips):
+            for r in range(2):
+                row = s * 10 + (0 if r == 0 else 9)
+                on = rng.random(W) < 0.6
+                # labels: some raster index of a pixel at or before this row
+                seams[s, r][on] = rng.integers(0, row * W + 1, on.sum())
+        keys, vals = device.seam_merge(seams)
+        table = device.seam_table(torch.from_numpy(seams).to(cuda_dev), H * W).cpu().numpy()
+        want = {int(k): int(v) for k, v in zip(keys, vals)}
+        for v in np.unique(seams[seams >= 0]):
+            assert table[v] == want.get(int(v), int(v)), (n_strips, W, v)
+        lab = torch.from_numpy(seams.reshape(-1).copy()).to(cuda_dev)
+        device.relabel_table(lab, torch.from_numpy(table).to(cuda_dev))
+        got = lab.cpu().numpy()
+        ref = np.array([want.get(int(v), int(v)) if v >= 0 else -1 for v in seams.reshape(-1)])
+        assert np.array_equal(got, ref)
