@@ -1028,8 +1028,9 @@ __global__ void seam_init_kernel(const int32_t* __restrict__ seams, int64_t n, i
   }
 }
 
-// position u of seam s: strip s's last row against strip s+1's first row,
-// 8-connected (the straight neighbour, else both diagonals)
+// position u of seam s: strip s+1's first-row pixel u against strip s's
+// last-row pixels u-1, u, u+1 (8-connected; all three, as the host merge, so
+// the result does not rely on row neighbours sharing a label)
 __global__ void seam_unite_kernel(const int32_t* __restrict__ seams, int n_strips, int W,
                                   int32_t* table) {
   const int64_t total = (int64_t)(n_strips - 1) * W;
@@ -1038,13 +1039,13 @@ __global__ void seam_unite_kernel(const int32_t* __restrict__ seams, int n_strip
     const int s = (int)(i / W), u = (int)(i - (int64_t)s * W);
     const int32_t* a = seams + ((int64_t)s * 2 + 1) * W;   // last owned row of strip s
     const int32_t* b = seams + ((int64_t)s + 1) * 2 * W;   // first owned row of strip s+1
-    const int32_t x = a[u];
+    const int32_t x = b[u];
     if (x < 0) continue;
-    if (b[u] >= 0) {
-      if (b[u] != x) uf_unite(table, x, b[u]);
-    } else {
-      if (u > 0 && b[u - 1] >= 0 && b[u - 1] != x) uf_unite(table, x, b[u - 1]);
-      if (u + 1 < W && b[u + 1] >= 0 && b[u + 1] != x) uf_unite(table, x, b[u + 1]);
+    for (int du = -1; du <= 1; ++du) {
+      const int uu = u + du;
+      if (uu < 0 || uu >= W) continue;
+      const int32_t y = a[uu];
+      if (y >= 0 && y != x) uf_unite(table, x, y);
     }
   }
 }
