@@ -89,7 +89,7 @@ struct FastCfg {
   static constexpr size_t FL = align_up(CS + CS_BYTES, 16);
   static constexpr size_t BAR = align_up(FL + FL_BYTES, 16);
   // + slack for the 128-B base alignment
-  static constexpr size_t TOTAL = BAR + 16 + 128;
+  static constexpr size_t TOTAL = BAR + 24 + 128;  // 3 mbarriers
   static_assert(NC <= kHalfUnits, "pass V: one unit per thread");
   static_assert(NR <= 32, "row validity bits must fit 32 bits");
 };
@@ -550,7 +550,7 @@ template <int R, typename T>
 __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int y0, int bz, int H,
                                        int W, const AccPair<T>* CR, const uint32_t* fl,
                                        uint32_t stage_base, const FixedParams& p,
-                                       uint8_t* mask_out) {
+                                       uint8_t* mask_out, uint64_t* sfree, uint32_t sparity) {
   using Cfg = FastCfg<R, T>;
   using A = Acc<T>;
   __builtin_assume(__isShared(in));
@@ -636,6 +636,8 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
     df[j] = dflt(drow[j], p);
     zc[j + 1] = __fmul_rn(p.fxb_f, rcp_ftz(df[j]));
   }
+  // the staging tile is free once the previous item's bulk stores have read it
+  mbar_wait(sfree, sparity);
   float o[12];
 #pragma unroll
   for (int j = 0; j < kRun; j += 2) {
@@ -738,6 +740,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     tma_prefetch_desc(&in_map);
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
+    mbar_init(bar + 2, kStoreLanes);  // staging free (the store lanes' bulk reads done)
     fence_mbar_init();
     load_tile(cur, 0);
   }
@@ -756,11 +759,18 @@ __global__ void __launch_bounds__(kFastThreads, 2)
     mbar_wait(bar + buf, (uint32_t)(it >> 1) & 1u);
 
     pass_v<R, T>(in, sh, x0, y0, H, W, h, c, unit, CR, fl, p);
-    // staging of the previous item read out by its bulk stores (issued by warp 8)
-    if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) bulk_wait_read0();
     __syncthreads();
 
-    if (tid < 256) pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out);
+    if (tid < kStoreTid) {
+      pass_h<R, T>(tid, in, sh, x0, y0, bz, H, W, CR, fl, stage_base, p, mask_out, bar + 2,
+                   (uint32_t)it & 1u);
+    } else if (tid >= kStoreTid && tid < kStoreTid + kStoreLanes) {
+      // the store lanes (idle in pass H): the previous item's bulk stores have
+      // read the staging tile -> pass H may write it (waited for there, after
+      // its sliding sums, instead of before the barrier above)
+      bulk_wait_read0();
+      mbar_arrive(bar + 2);
+    }
     fence_proxy_async_smem();
     __syncthreads();
     // output stores from a warp that is idle in pass H -- warp 0 goes
