@@ -52,7 +52,12 @@ constexpr int kLWords = kLTW / 32;    // words per tile row
 constexpr int kRowWords = kLTH * kLWords;  // 512 row-words per tile
 constexpr int kBands = kLTH / 2;      // 2-row bands per tile
 constexpr int kLThreads = kBands * kLWords;  // 256: one thread per (band, word)
-constexpr int kSlots = kBands * kLTW;  // node slots: band * 128 + column of a band-run start
+// node slots: a word holds at most 16 band runs, so the slot of a band run is
+// band * 64 + word * 16 + (its rank among the word's runs) -- dense per word,
+// no block scan: the rank is a popcount of the word's run starts below it
+constexpr int kWordSlots = 16;
+constexpr int kBandSlots = kLWords * kWordSlots;  // 64
+constexpr int kSlots = kBands * kBandSlots;       // 4096
 
 __device__ __forceinline__ double edge_value(double c, double l, double r, double u, double dn) {
   return fabs(__dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(__dmul_rn(4.0, c), l), r), u), dn));
@@ -93,13 +98,13 @@ __global__ void passable_kernel(const T* __restrict__ disp, const CclParams p,
 // ---------------------------------------------------------------------------
 // union-find helpers (indices only ever point to smaller indices)
 
-// PAD: the tile's parent array keeps one pad word per 32 slots (tix), so the
-// lanes of a warp -- 8 bands x 4 words -- touching slots at the same bit
-// position of different words hit different banks; the global array G of
-// the seam pass is unpadded
+// PAD: the tile's parent array keeps one pad word per 16 slots (one word's
+// slots, tix), so the lanes of a warp -- 8 bands x 4 words -- touching slots
+// of equal rank in different words hit 32 different banks (4k + 17w mod 32);
+// the global array G of the seam pass is unpadded
 template <bool PAD>
 __device__ __forceinline__ int tix(int x) {
-  return PAD ? x + (x >> 5) : x;
+  return PAD ? x + (x >> 4) : x;
 }
 
 // find with path halving: every write replaces a parent by an ancestor, so it
@@ -147,11 +152,16 @@ __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
 
 __device__ __forceinline__ uint32_t run_starts(uint32_t A) { return A & ~(A << 1); }
 
-// start bit of the run (inside word A, starts st) that contains bit p
-__device__ __forceinline__ int start_of(uint32_t st, int p) {
-  const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
-  return 31 - __clz(st & upto);
+// bits 0 .. p of a word
+__device__ __forceinline__ uint32_t upto_bit(int p) {
+  return (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
 }
+
+// rank (among the word's band runs, starts st) of the run that contains bit p
+__device__ __forceinline__ int rank_at(uint32_t st, int p) { return __popc(st & upto_bit(p)) - 1; }
+
+// rank of the word's last run (the one holding bit 31 if it is set)
+__device__ __forceinline__ int last_rank(uint32_t st) { return __popc(st) - 1; }
 
 // ---------------------------------------------------------------------------
 // tile union-find over band runs
@@ -193,23 +203,21 @@ __device__ __forceinline__ int slot_label(const int32_t* L, int slot) {
 // slot of the band run holding pixel (r, c) of the tile (the pixel must be set)
 __device__ __forceinline__ int pixel_slot(const uint32_t* bits, int r, int c) {
   const int k = r >> 1, w = c >> 5;
-  return k * kLTW + w * 32 + start_of(run_starts(band_word(bits, k, w)), c & 31);
+  return k * kBandSlots + w * kWordSlots + rank_at(run_starts(band_word(bits, k, w)), c & 31);
 }
 
 __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits, int tid) {
   const int k = tid >> 2, w = tid & 3;
-  const int base = k * kLTW + w * 32;
+  const int base = k * kBandSlots + w * kWordSlots;
   const uint32_t A0 = bits[(2 * k) * kLWords + w], A1 = bits[(2 * k + 1) * kLWords + w];
   const uint32_t G = A0 | A1, stG = run_starts(G);
-  for (uint32_t m = stG; m; m &= m - 1u) {
-    const int n = base + __ffs(m) - 1;
-    L[tix<true>(n)] = n;
-  }
+  const int nr = __popc(stG);
+  for (int i = 0; i < nr; ++i) L[tix<true>(base + i)] = base + i;
   __syncthreads();
   // a band run crossing into this word from the left neighbour word
   if ((G & 1u) && w > 0) {
     const uint32_t Gl = band_word(bits, k, w - 1);
-    if (Gl >> 31) uf_unite<true>(L, base, base - 32 + (31 - __clz(run_starts(Gl))));
+    if (Gl >> 31) uf_unite<true>(L, base, base - kWordSlots + last_rank(run_starts(Gl)));
   }
   // band k-1: only this band's first-row pixels touch it (its last row)
   if (k > 0) {
@@ -218,42 +226,41 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
     const uint32_t stGb = run_starts(bits[rb - kLWords] | B);
     const uint32_t Gb = bits[rb - kLWords] | B;
     const uint32_t BL = w > 0 ? bits[rb - 1] : 0u, BR = w + 1 < kLWords ? bits[rb + 1] : 0u;
-    const int bbase = base - kLTW;
-    for (uint32_t m = stG; m; m &= m - 1u) {
+    const int bbase = base - kBandSlots;
+    int n = base;
+    for (uint32_t m = stG; m; m &= m - 1u, ++n) {
       const int s = __ffs(m) - 1;
       const uint32_t a = A0 & run_mask(G, s);
       if (!a) continue;
-      const int n = base + s;
       uint32_t o = (a | (a << 1) | (a >> 1)) & B;
       while (o) {
         const int p = __ffs(o) - 1;
-        uf_unite<true>(L, n, bbase + start_of(stGb, p));
-        const uint32_t upto = (p == 31) ? 0xffffffffu : ((2u << p) - 1u);
-        const uint32_t zb = ~Gb & ~upto;  // zeros of band k-1 above p: end of that band run
+        uf_unite<true>(L, n, bbase + rank_at(stGb, p));
+        const uint32_t zb = ~Gb & ~upto_bit(p);  // zeros of band k-1 above p: end of that band run
         if (!zb) break;
         o &= ~((zb & (0u - zb)) - 1u);
       }
       if ((a & 1u) && (BL >> 31))
-        uf_unite<true>(L, n, bbase - 32 + (31 - __clz(run_starts(bits[rb - kLWords - 1] | BL))));
-      if ((a >> 31) && (BR & 1u)) uf_unite<true>(L, n, bbase + 32);
+        uf_unite<true>(L, n, bbase - kWordSlots + last_rank(run_starts(bits[rb - kLWords - 1] | BL)));
+      if ((a >> 31) && (BR & 1u)) uf_unite<true>(L, n, bbase + kWordSlots);
     }
   }
   __syncthreads();
   // every node -> its root (only root values are written in this phase)
-  for (uint32_t m = stG; m; m &= m - 1u) {
-    const int n = base + __ffs(m) - 1;
-    L[tix<true>(n)] = uf_root<true>(L, n);
-  }
+  for (int i = 0; i < nr; ++i) L[tix<true>(base + i)] = uf_root<true>(L, base + i);
   __syncthreads();
   // component label = smallest pixel index, reduced into the root's entry
-  for (uint32_t m = stG; m; m &= m - 1u) {
-    const int s = __ffs(m) - 1;
-    const uint32_t run = run_mask(G, s);
-    const uint32_t a0 = A0 & run;
-    const int mp = a0 ? (2 * k) * kLTW + w * 32 + __ffs(a0) - 1
-                      : (2 * k + 1) * kLTW + w * 32 + __ffs(A1 & run) - 1;
-    const int pr = L[tix<true>(base + s)];
-    atomicMin(&L[tix<true>(pr >= 0 ? pr : base + s)], mp - kEnc);
+  {
+    int n = base;
+    for (uint32_t m = stG; m; m &= m - 1u, ++n) {
+      const int s = __ffs(m) - 1;
+      const uint32_t run = run_mask(G, s);
+      const uint32_t a0 = A0 & run;
+      const int mp = a0 ? (2 * k) * kLTW + w * 32 + __ffs(a0) - 1
+                        : (2 * k + 1) * kLTW + w * 32 + __ffs(A1 & run) - 1;
+      const int pr = L[tix<true>(n)];
+      atomicMin(&L[tix<true>(pr >= 0 ? pr : n)], mp - kEnc);
+    }
   }
   __syncthreads();
 }
@@ -278,11 +285,11 @@ __device__ __forceinline__ int frame_index(int px, int x0, int y0, int W) {
 // ---------------------------------------------------------------------------
 // 1. tile pass.  MODE 1: uint8 passable input; MODE 2: the bit mask is the
 // input (passable_bits_kernel).  Dynamic shared memory: the parent array only
-// (kSlots int32 = 32 KB; 6 CTAs/SM) -- the slot labels go straight to the
+// (kSlots int32 + pads = 17 KB; 8 CTAs/SM) -- the slot labels go straight to the
 // workspace (measured: staging them in shared memory capped residency at 4
 // CTAs/SM).
 
-constexpr size_t kTileSmem = (size_t)(kSlots + kSlots / 32) * 4;
+constexpr size_t kTileSmem = (size_t)(kSlots + kSlots / 16) * 4;
 
 template <int MODE>
 __global__ void __launch_bounds__(kLThreads)
@@ -329,14 +336,15 @@ __global__ void __launch_bounds__(kLThreads)
   // array; the others are never read); flag components touching the border
   {
     const int k = tid >> 2, w = tid & 3;
-    const int base = k * kLTW + w * 32;
+    const int base = k * kBandSlots + w * kWordSlots;
     const uint32_t A0 = bits[(2 * k) * kLWords + w], A1 = bits[(2 * k + 1) * kLWords + w];
     const uint32_t G = A0 | A1;
     uint16_t* lbl = ws.lbl + tile * kSlots;
-    for (uint32_t m = run_starts(G); m; m &= m - 1u) {
+    int n = base;
+    for (uint32_t m = run_starts(G); m; m &= m - 1u, ++n) {
       const int s = __ffs(m) - 1;
-      const int v = slot_label(L, base + s);
-      lbl[base + s] = (uint16_t)v;
+      const int v = slot_label(L, n);
+      lbl[n] = (uint16_t)v;
       const uint32_t run = run_mask(G, s);
       if ((k == 0 && (A0 & run)) || (k == kBands - 1 && (A1 & run)) || (w == 0 && (run & 1u)) ||
           (w == kLWords - 1 && (run >> 31)))
@@ -445,14 +453,14 @@ __global__ void __launch_bounds__(kSeamThreads)
 // 3. resolve: border-touching components through G (one walk each), then per
 // pixel: band-run slot (bit ops) -> tile label -> final label, coalesced stores
 
-__device__ __forceinline__ int lp(int slot) { return slot + (slot >> 5); }
+__device__ __forceinline__ int lp(int slot) { return slot + (slot >> 4); }
 
 __global__ void __launch_bounds__(kLThreads)
     ccl_resolve_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
-  // slot label, then slot FINAL label; one pad word per 32 slots (lp) so the
-  // lanes of a warp looking up run starts at equal bit positions of different
-  // words hit different banks
-  __shared__ __align__(16) int32_t lab[kSlots + kSlots / 32];
+  // slot label, then slot FINAL label; one pad word per word's 16 slots (lp)
+  // so the lanes of a warp looking up runs of equal rank in different words
+  // hit different banks
+  __shared__ __align__(16) int32_t lab[kSlots + kSlots / 16];
   __shared__ uint32_t bits[kRowWords];
   __shared__ uint32_t flag[kTilePx / 32];
   __shared__ int32_t rank0[kTilePx / 32];  // flagged labels before word i
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(kLThreads)
     const uint4* src = reinterpret_cast<const uint4*>(ws.lbl + tile * kSlots);
 #pragma unroll
     for (int i = 0; i < kSlots / 8 / kLThreads; ++i) {
-      const int j = i * kLThreads + tid;  // slots 8j .. 8j+7, one 32-slot group
+      const int j = i * kLThreads + tid;  // slots 8j .. 8j+7, one 16-slot group
       const uint4 v = src[j];
       int32_t* d = lab + lp(8 * j);
       d[0] = v.x & 0xffff;
@@ -527,9 +535,10 @@ __global__ void __launch_bounds__(kLThreads)
   // final label of every band-run slot, by the slot's owner thread (band, word)
   {
     const int kb = tid >> 2, w = tid & 3;
-    const int base = kb * kLTW + w * 32;
-    for (uint32_t m = run_starts(band_word(bits, kb, w)); m; m &= m - 1u) {
-      const int slot = lp(base + __ffs(m) - 1);
+    const int base = lp(kb * kBandSlots + w * kWordSlots);
+    const int nr = __popc(run_starts(band_word(bits, kb, w)));
+    for (int i = 0; i < nr; ++i) {
+      const int slot = base + i;
       const int v = lab[slot];
       const uint32_t fwv = flag[v >> 5];
       const uint32_t bit = 1u << (v & 31);
@@ -547,16 +556,16 @@ __global__ void __launch_bounds__(kLThreads)
     for (int r = warp; r < kLTH; r += kLThreads / 32) {
       const uint32_t A = bits[r * kLWords + w];
       const uint32_t st = run_starts(band_word(bits, r >> 1, w));
-      const int base = lp((r >> 1) * kLTW + w * 32);  // a 32-slot group: lp(base + b) = base + b
-      // run start of the lane's first pixel (the highest start <= sub), then
-      // carried along the 4 pixels: a pixel in the band run starts a new slot
-      // only where the band word has a run start
+      const int base = lp((r >> 1) * kBandSlots + w * kWordSlots);  // a 16-slot group
+      // rank of the run holding the lane's first pixel (starts <= sub, minus
+      // one), then carried along the 4 pixels: a pixel in the band run starts
+      // a new slot only where the band word has a run start
       const uint32_t ab = A >> sub, sb = st >> sub;
-      int s = 31 - __clz(st & ((2u << sub) - 1u));  // sub <= 28
+      int s = __popc(st & ((2u << sub) - 1u)) - 1;  // sub <= 28
       int v[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (j > 0 && ((sb >> j) & 1u)) s = sub + j;
+        if (j > 0 && ((sb >> j) & 1u)) ++s;
         v[j] = ((ab >> j) & 1u) ? lab[base + s] : -1;
       }
       *reinterpret_cast<int4*>(out + (y0 + r) * W + x0 + w * 32 + sub) =
@@ -572,7 +581,7 @@ __global__ void __launch_bounds__(kLThreads)
       int32_t v = -1;
       if ((A >> lane) & 1u) {
         const uint32_t st = run_starts(band_word(bits, r >> 1, w));
-        v = lab[lp((r >> 1) * kLTW + w * 32) + (31 - __clz(st & upto))];
+        v = lab[lp((r >> 1) * kBandSlots + w * kWordSlots) + __popc(st & upto) - 1];
       }
       out[gy * W + gx] = v;  // frame offsets fit int32 (host-checked)
     }

@@ -1,0 +1,11 @@
+#!/bin/bash
+# A/B of labeller variants in exp/*.so through tools/time_labels.py (C3)
+mkdir -p gpurun_out
+: > gpurun_out/ab_labels.log
+for so in exp/*.so; do
+  for rep in 1 2; do
+    echo "== $so" >> gpurun_out/ab_labels.log
+    SN_B200_LIB=$so timeout 300 python tools/time_labels.py ${B:-128} >> gpurun_out/ab_labels.log 2>&1
+  done
+done
+cat gpurun_out/ab_labels.log
