@@ -435,15 +435,19 @@ __global__ void __launch_bounds__(kSeamThreads)
     if (a < 0) continue;
     const int32_t c = b_row[i];
     if (c >= 0) {
-      if (a != c) uf_unite(G, a, c);
+      // a run crossing the seam gives the same (a, c) pair at consecutive
+      // positions: only its first position unites (the union is idempotent)
+      if (a != c && !(i > 0 && a_row[i - 1] == a && b_row[i - 1] == c)) uf_unite(G, a, c);
     } else {
+      // diagonals; skipped where the neighbour position pairs the same a
+      // with that pixel straight (it unites them itself)
       if (i > 0) {
         const int32_t bl = b_row[i - 1];
-        if (bl >= 0 && bl != a) uf_unite(G, a, bl);
+        if (bl >= 0 && bl != a && a_row[i - 1] != a) uf_unite(G, a, bl);
       }
       if (i + 1 < n) {
         const int32_t br = b_row[i + 1];
-        if (br >= 0 && br != a) uf_unite(G, a, br);
+        if (br >= 0 && br != a && a_row[i + 1] != a) uf_unite(G, a, br);
       }
     }
   }
