@@ -58,6 +58,7 @@ constexpr int kLThreads = kBands * kLWords;  // 256: one thread per (band, word)
 constexpr int kWordSlots = 16;
 constexpr int kBandSlots = kLWords * kWordSlots;  // 64
 constexpr int kSlots = kBands * kBandSlots;       // 4096
+static_assert(kLThreads * kWordSlots == kSlots, "slot export: one word's slots per thread");
 
 __device__ __forceinline__ double edge_value(double c, double l, double r, double u, double dn) {
   return fabs(__dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(__dmul_rn(4.0, c), l), r), u), dn));
@@ -332,19 +333,19 @@ __global__ void __launch_bounds__(kLThreads)
   int32_t* L = smem;
   band_union_find(L, bits, tid);
 
-  // export labels of the band-run slots (run-start entries of the workspace
-  // array; the others are never read); flag components touching the border
+  // every band run's entry becomes its component label, encoded as a root's
+  // (label - kEnc; race-free: roots keep their value, and a non-root entry is
+  // read by its owner only); flag components touching the tile border
   {
     const int k = tid >> 2, w = tid & 3;
     const int base = k * kBandSlots + w * kWordSlots;
     const uint32_t A0 = bits[(2 * k) * kLWords + w], A1 = bits[(2 * k + 1) * kLWords + w];
     const uint32_t G = A0 | A1;
-    uint16_t* lbl = ws.lbl + tile * kSlots;
     int n = base;
     for (uint32_t m = run_starts(G); m; m &= m - 1u, ++n) {
       const int s = __ffs(m) - 1;
       const int v = slot_label(L, n);
-      lbl[n] = (uint16_t)v;
+      L[tix<true>(n)] = v - kEnc;
       const uint32_t run = run_mask(G, s);
       if ((k == 0 && (A0 & run)) || (k == kBands - 1 && (A1 & run)) || (w == 0 && (run & 1u)) ||
           (w == kLWords - 1 && (run >> 31)))
@@ -352,6 +353,19 @@ __global__ void __launch_bounds__(kLThreads)
     }
   }
   __syncthreads();
+  // export the slot labels as 16-bit values, one word's 16 slots (32 B) per
+  // thread: coalesced full-sector stores (slots that hold no run carry stale
+  // values; the resolve pass reads run slots only)
+  {
+    const int* src = L + tix<true>(tid * kWordSlots);
+    uint32_t q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      q[i] = ((uint32_t)(src[2 * i] + kEnc) & 0xffffu) | ((uint32_t)(src[2 * i + 1] + kEnc) << 16);
+    uint4* dst = reinterpret_cast<uint4*>(ws.lbl + tile * kSlots + tid * kWordSlots);
+    dst[0] = make_uint4(q[0], q[1], q[2], q[3]);
+    dst[1] = make_uint4(q[4], q[5], q[6], q[7]);
+  }
 
   // seam rows / columns: frame index of each border pixel's component, -1 if not passable
   const int64_t seam_row = ((int64_t)blockIdx.z * ws.n_ty + ty) * W;
@@ -371,7 +385,7 @@ __global__ void __launch_bounds__(kLThreads)
         }
       }
     }
-  } else {
+  } else if (warp < 4) {
     // warp 2: first column, warp 3: last column; lanes <-> rows
     const int c = warp == 2 ? 0 : kLTW - 1;
     int32_t* dst = (warp == 2 ? ws.left : ws.right) + seam_col;
