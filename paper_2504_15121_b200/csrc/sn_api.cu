@@ -1365,7 +1365,19 @@ int host_pipeline(sn_plan_t* plan, const T* disp_host, int64_t B, int64_t H, int
   if (!pin_in && (rc = grow_pinned(plan->h_in, plan->h_in_cap, need * sizeof(T)))) return rc;
   if (!pin_out && (rc = grow_pinned(plan->h_out, plan->h_out_cap, out_slot))) return rc;
 
-  const int64_t n_chunks = (B + chunk - 1) / chunk;
+  // chunk c covers frames [cf0(c), cf0(c) + cnf(c)): a ramp of 1, 2, 4, ...
+  // frames up to `chunk`, so the first D2H starts after one frame's H2D and
+  // compute instead of a whole chunk's (the pipeline fill)
+  int ramp = 0;  // ramp chunks: sizes 1, 2, .., 2^(ramp-1), all < chunk
+  while (((int64_t)1 << ramp) < chunk) ++ramp;
+  auto cf0 = [&](int64_t c) -> int64_t {
+    return c <= ramp ? ((int64_t)1 << c) - 1 : (((int64_t)1 << ramp) - 1) + (c - ramp) * chunk;
+  };
+  auto cnf = [&](int64_t c) -> int64_t {
+    return std::min<int64_t>(c < ramp ? (int64_t)1 << c : chunk, B - cf0(c));
+  };
+  int64_t n_chunks = 0;
+  while (cf0(n_chunks) < B) ++n_chunks;
   // every exit waits for the queued work (it may still read or write the
   // caller's buffers or a staging slot)
   auto drain_all = [&] {
@@ -1381,7 +1393,7 @@ int host_pipeline(sn_plan_t* plan, const T* disp_host, int64_t B, int64_t H, int
   // copy chunk c's outputs out of its pinned slot (pageable callers)
   auto drain_out = [&](int64_t c) -> int {
     const int s = (int)(c & 1);
-    const int64_t f0 = c * chunk, nf = std::min<int64_t>(chunk, B - f0);
+    const int64_t f0 = cf0(c), nf = cnf(c);
     const size_t px = (size_t)(nf * frame_px);
     if (cudaEventSynchronize(plan->ev_out[s]) != cudaSuccess) return set_cuda_error("D2H wait");
     const char* src = static_cast<const char*>(plan->h_out[s]);
@@ -1396,8 +1408,8 @@ int host_pipeline(sn_plan_t* plan, const T* disp_host, int64_t B, int64_t H, int
   };
   for (int64_t c = 0; c < n_chunks; ++c) {
     const int s = (int)(c & 1);
-    const int64_t f0 = c * chunk;
-    const int64_t nf = std::min<int64_t>(chunk, B - f0);
+    const int64_t f0 = cf0(c);
+    const int64_t nf = cnf(c);
     const size_t px = (size_t)(nf * frame_px);
     if (!pin_out && c >= 2 && (rc = drain_out(c - 2))) return fail(rc);
     // buffers of slot s are free once chunk c-2's compute (inputs) and D2H (outputs) are done
