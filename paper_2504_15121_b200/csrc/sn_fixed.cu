@@ -260,19 +260,12 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
                                              float dn1, float2 zz, bool ok0, bool ok1, float duh,
                                              float dv, const FixedParams& p, float* o) {
   constexpr bool kInt = sizeof(A) == 4;
-  // points; zz = fxb_f * rcp(d) as computed by the caller (shared with the
-  // passable predicate); duh = (x - u0_hi) exactly, du = duh - u0_lo
+  // points; zz = the depths as fixed by the caller (pass_h: fxb_f * rcp(d),
+  // or NaN / an fp64 division where that leaves (0, FLT_MAX)); duh = (x -
+  // u0_hi) exactly, du = duh - u0_lo
   const float2 dd = make_float2(dn0, dn1);
   // (duh, duh + 1) exactly, then one packed subtraction: the same roundings
   const float2 du = __fadd2_rn(make_float2(duh, duh + 1.0f), make_float2(-p.u0_lo, -p.u0_lo));
-  // zz is finite and > 0 exactly when d is a normal positive disparity whose
-  // reciprocal does not flush; anything else -- d invalid (NaN, <= 0, +inf:
-  // the point is NaN), subnormal, or so large or small that rcp or the
-  // product leaves the normal range -- takes the rare path
-  if (!(zz.x > 0.0f && zz.x < 3.402823466e38f))
-    zz.x = (d0 > 0.0f && d0 <= 3.402823466e38f) ? depth_rare(p.fxb, d0) : __int_as_float(0x7fc00000);
-  if (!(zz.y > 0.0f && zz.y < 3.402823466e38f))
-    zz.y = (d1 > 0.0f && d1 <= 3.402823466e38f) ? depth_rare(p.fxb, d1) : __int_as_float(0x7fc00000);
   const float2 px = __fmul2_rn(__fmul2_rn(du, zz), make_float2(p.inv_fx_f, p.inv_fx_f));
   // dv / fy is a per-row constant (hoisted out of the run): one product per pixel
   const float dvy = dv * p.inv_fy_f;
@@ -466,9 +459,6 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
         all_small &= fabs(sval(raw[i], p)) <= 1099511627776.0;  // 2^40, NaN fails
       }
     }
-  } else {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) raw[i] = T{};
   }
   if (unit) {
     // rows of the unit inside the image
@@ -635,6 +625,26 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   for (int j = 0; j < kRun; ++j) {
     df[j] = dflt(drow[j], p);
     zc[j + 1] = __fmul_rn(p.fxb_f, rcp_ftz(df[j]));
+  }
+  // zf is finite and > 0 exactly when d is a normal positive disparity whose
+  // reciprocal does not flush; anything else -- d invalid (NaN, <= 0, +inf:
+  // the point is NaN), subnormal, or so large or small that rcp or the
+  // product leaves the normal range -- is fixed here, once for the run
+  // (NaN-propagating min / max: one test for its 8 depths)
+  {
+    float lo = zc[1], hi = zc[1];
+#pragma unroll
+    for (int j = 2; j <= kRun; ++j) {
+      asm("min.NaN.f32 %0, %0, %1;" : "+f"(lo) : "f"(zc[j]));
+      asm("max.NaN.f32 %0, %0, %1;" : "+f"(hi) : "f"(zc[j]));
+    }
+    if (!(lo > 0.0f && hi < 3.402823466e38f)) {
+#pragma unroll
+      for (int j = 0; j < kRun; ++j)
+        if (!(zc[j + 1] > 0.0f && zc[j + 1] < 3.402823466e38f))
+          zc[j + 1] = (df[j] > 0.0f && df[j] <= 3.402823466e38f) ? depth_rare(p.fxb, df[j])
+                                                                : __int_as_float(0x7fc00000);
+    }
   }
   // the staging tile is free once the previous item's bulk stores have read it
   mbar_wait(sfree, sparity);
