@@ -99,53 +99,97 @@ __global__ void passable_kernel(const T* __restrict__ disp, const CclParams p,
 // ---------------------------------------------------------------------------
 // union-find helpers (indices only ever point to smaller indices)
 
-// PAD: the tile's parent array keeps one pad word per 16 slots (one word's
-// slots, tix), so the lanes of a warp -- 8 bands x 4 words -- touching slots
-// of equal rank in different words hit 32 different banks (4k + 17w mod 32);
-// the global array G of the seam pass is unpadded
-template <bool PAD>
-__device__ __forceinline__ int tix(int x) {
-  return PAD ? x + (x >> 4) : x;
-}
-
 // find with path halving: every write replaces a parent by an ancestor, so it
-// commutes with concurrent unions (which only atomicMin roots)
-template <bool PAD = false>
+// commutes with concurrent unions (which only atomicMin roots).  The global
+// array G of the seam pass: node = label = frame index.
 __device__ __forceinline__ int uf_find(volatile int32_t* L, int x) {
   while (true) {
-    const int p = L[tix<PAD>(x)];
+    const int p = L[x];
     if (p == x) return x;
-    const int gp = L[tix<PAD>(p)];
+    const int gp = L[p];
     if (gp == p) return p;
-    L[tix<PAD>(x)] = gp;
+    L[x] = gp;
     x = gp;
   }
 }
 
 // read-only find
-template <bool PAD = false>
 __device__ __forceinline__ int uf_root(const volatile int32_t* L, int x) {
-  int p = L[tix<PAD>(x)];
+  int p = L[x];
   while (p != x) {
     x = p;
-    p = L[tix<PAD>(x)];
+    p = L[x];
   }
   return x;
 }
 
-template <bool PAD = false>
 __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
   volatile int32_t* V = L;
   while (true) {
-    a = uf_find<PAD>(V, a);
-    b = uf_find<PAD>(V, b);
+    a = uf_find(V, a);
+    b = uf_find(V, b);
     if (a == b) return;
     if (a > b) {
       const int t = a;
       a = b;
       b = t;
     }
-    const int old = atomicMin(&L[tix<PAD>(b)], a);
+    const int old = atomicMin(&L[b], a);
+    if (old == b) return;
+    b = old;
+  }
+}
+
+// The tile's parent array (shared memory) holds BYTE OFFSETS of padded slot
+// entries: slot s lives at soff(s) = 4 (s + s/16), one pad word per word's
+// 16 slots, so the lanes of a warp -- 8 bands x 4 words -- touching slots of
+// equal rank in different words hit 32 different banks (4k + 17w mod 32).
+// Offsets grow with the slot, so min-offset roots are min-slot roots; a
+// parent value is directly the address of its entry (no index arithmetic in
+// the find loops).  Roots' entries later hold label - kEnc (< 0).
+__device__ __forceinline__ int soff(int s) { return (s + (s >> 4)) << 2; }
+__device__ __forceinline__ int ld_o(const volatile int32_t* L, int off) {
+  return *reinterpret_cast<const volatile int32_t*>(reinterpret_cast<const volatile char*>(L) + off);
+}
+__device__ __forceinline__ void st_o(volatile int32_t* L, int off, int v) {
+  *reinterpret_cast<volatile int32_t*>(reinterpret_cast<volatile char*>(L) + off) = v;
+}
+__device__ __forceinline__ int* at_o(int32_t* L, int off) {
+  return reinterpret_cast<int*>(reinterpret_cast<char*>(L) + off);
+}
+
+__device__ __forceinline__ int uf_find_o(volatile int32_t* L, int x) {
+  while (true) {
+    const int p = ld_o(L, x);
+    if (p == x) return x;
+    const int gp = ld_o(L, p);
+    if (gp == p) return p;
+    st_o(L, x, gp);
+    x = gp;
+  }
+}
+
+__device__ __forceinline__ int uf_root_o(const volatile int32_t* L, int x) {
+  int p = ld_o(L, x);
+  while (p != x) {
+    x = p;
+    p = ld_o(L, x);
+  }
+  return x;
+}
+
+__device__ __forceinline__ void uf_unite_o(int32_t* L, int a, int b) {
+  volatile int32_t* V = L;
+  while (true) {
+    a = uf_find_o(V, a);
+    b = uf_find_o(V, b);
+    if (a == b) return;
+    if (a > b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicMin(at_o(L, b), a);
     if (old == b) return;
     b = old;
   }
@@ -196,29 +240,34 @@ __device__ __forceinline__ uint32_t run_mask(uint32_t G, int s) {
   return zer ? ((zer & (0u - zer)) - 1u) & hi : hi;
 }
 
-__device__ __forceinline__ int slot_label(const int32_t* L, int slot) {
-  const int v = L[tix<true>(slot)];
-  return (v >= 0 ? L[tix<true>(v)] : v) + kEnc;
+// component label of the slot at byte offset `off`
+__device__ __forceinline__ int slot_label(const int32_t* L, int off) {
+  const int v = ld_o(L, off);
+  return (v >= 0 ? ld_o(L, v) : v) + kEnc;
 }
 
-// slot of the band run holding pixel (r, c) of the tile (the pixel must be set)
+// offset of the band run holding pixel (r, c) of the tile (the pixel must be set)
 __device__ __forceinline__ int pixel_slot(const uint32_t* bits, int r, int c) {
   const int k = r >> 1, w = c >> 5;
-  return k * kBandSlots + w * kWordSlots + rank_at(run_starts(band_word(bits, k, w)), c & 31);
+  return soff(k * kBandSlots + w * kWordSlots) +
+         4 * rank_at(run_starts(band_word(bits, k, w)), c & 31);
 }
 
 __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits, int tid) {
   const int k = tid >> 2, w = tid & 3;
-  const int base = k * kBandSlots + w * kWordSlots;
+  // byte offset of this word's first slot; the word's slots follow at +4,
+  // the left word's at -68, the band above's at -272 (one band = 68 words)
+  const int base = soff(k * kBandSlots + w * kWordSlots);
+  constexpr int kWordOff = (kWordSlots + 1) * 4, kBandOff = kLWords * kWordOff;
   const uint32_t A0 = bits[(2 * k) * kLWords + w], A1 = bits[(2 * k + 1) * kLWords + w];
   const uint32_t G = A0 | A1, stG = run_starts(G);
   const int nr = __popc(stG);
-  for (int i = 0; i < nr; ++i) L[tix<true>(base + i)] = base + i;
+  for (int i = 0; i < nr; ++i) st_o(L, base + 4 * i, base + 4 * i);
   __syncthreads();
   // a band run crossing into this word from the left neighbour word
   if ((G & 1u) && w > 0) {
     const uint32_t Gl = band_word(bits, k, w - 1);
-    if (Gl >> 31) uf_unite<true>(L, base, base - kWordSlots + last_rank(run_starts(Gl)));
+    if (Gl >> 31) uf_unite_o(L, base, base - kWordOff + 4 * last_rank(run_starts(Gl)));
   }
   // band k-1: only this band's first-row pixels touch it (its last row)
   if (k > 0) {
@@ -227,40 +276,40 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
     const uint32_t stGb = run_starts(bits[rb - kLWords] | B);
     const uint32_t Gb = bits[rb - kLWords] | B;
     const uint32_t BL = w > 0 ? bits[rb - 1] : 0u, BR = w + 1 < kLWords ? bits[rb + 1] : 0u;
-    const int bbase = base - kBandSlots;
+    const int bbase = base - kBandOff;
     int n = base;
-    for (uint32_t m = stG; m; m &= m - 1u, ++n) {
+    for (uint32_t m = stG; m; m &= m - 1u, n += 4) {
       const int s = __ffs(m) - 1;
       const uint32_t a = A0 & run_mask(G, s);
       if (!a) continue;
       uint32_t o = (a | (a << 1) | (a >> 1)) & B;
       while (o) {
         const int p = __ffs(o) - 1;
-        uf_unite<true>(L, n, bbase + rank_at(stGb, p));
+        uf_unite_o(L, n, bbase + 4 * rank_at(stGb, p));
         const uint32_t zb = ~Gb & ~upto_bit(p);  // zeros of band k-1 above p: end of that band run
         if (!zb) break;
         o &= ~((zb & (0u - zb)) - 1u);
       }
       if ((a & 1u) && (BL >> 31))
-        uf_unite<true>(L, n, bbase - kWordSlots + last_rank(run_starts(bits[rb - kLWords - 1] | BL)));
-      if ((a >> 31) && (BR & 1u)) uf_unite<true>(L, n, bbase + kWordSlots);
+        uf_unite_o(L, n, bbase - kWordOff + 4 * last_rank(run_starts(bits[rb - kLWords - 1] | BL)));
+      if ((a >> 31) && (BR & 1u)) uf_unite_o(L, n, bbase + kWordOff);
     }
   }
   __syncthreads();
   // every node -> its root (only root values are written in this phase)
-  for (int i = 0; i < nr; ++i) L[tix<true>(base + i)] = uf_root<true>(L, base + i);
+  for (int i = 0; i < nr; ++i) st_o(L, base + 4 * i, uf_root_o(L, base + 4 * i));
   __syncthreads();
   // component label = smallest pixel index, reduced into the root's entry
   {
     int n = base;
-    for (uint32_t m = stG; m; m &= m - 1u, ++n) {
+    for (uint32_t m = stG; m; m &= m - 1u, n += 4) {
       const int s = __ffs(m) - 1;
       const uint32_t run = run_mask(G, s);
       const uint32_t a0 = A0 & run;
       const int mp = a0 ? (2 * k) * kLTW + w * 32 + __ffs(a0) - 1
                         : (2 * k + 1) * kLTW + w * 32 + __ffs(A1 & run) - 1;
-      const int pr = L[tix<true>(n)];
-      atomicMin(&L[tix<true>(pr >= 0 ? pr : n)], mp - kEnc);
+      const int pr = ld_o(L, n);
+      atomicMin(at_o(L, pr >= 0 ? pr : n), mp - kEnc);
     }
   }
   __syncthreads();
@@ -338,14 +387,13 @@ __global__ void __launch_bounds__(kLThreads)
   // read by its owner only); flag components touching the tile border
   {
     const int k = tid >> 2, w = tid & 3;
-    const int base = k * kBandSlots + w * kWordSlots;
     const uint32_t A0 = bits[(2 * k) * kLWords + w], A1 = bits[(2 * k + 1) * kLWords + w];
     const uint32_t G = A0 | A1;
-    int n = base;
-    for (uint32_t m = run_starts(G); m; m &= m - 1u, ++n) {
+    int n = soff(k * kBandSlots + w * kWordSlots);
+    for (uint32_t m = run_starts(G); m; m &= m - 1u, n += 4) {
       const int s = __ffs(m) - 1;
       const int v = slot_label(L, n);
-      L[tix<true>(n)] = v - kEnc;
+      st_o(L, n, v - kEnc);
       const uint32_t run = run_mask(G, s);
       if ((k == 0 && (A0 & run)) || (k == kBands - 1 && (A1 & run)) || (w == 0 && (run & 1u)) ||
           (w == kLWords - 1 && (run >> 31)))
@@ -357,7 +405,7 @@ __global__ void __launch_bounds__(kLThreads)
   // thread: coalesced full-sector stores (slots that hold no run carry stale
   // values; the resolve pass reads run slots only)
   {
-    const int* src = L + tix<true>(tid * kWordSlots);
+    const int* src = L + (soff(tid * kWordSlots) >> 2);
     uint32_t q[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
