@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(kLThreads)
 // block-uniform 32-bit arithmetic (a 64-bit division per position cost
 // more than the unions).
 constexpr int kSeamThreads = 256;
+constexpr int kSeamFrames = 4;
 
 __global__ void __launch_bounds__(kSeamThreads)
     ccl_seam_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
@@ -488,14 +489,30 @@ __global__ void __launch_bounds__(kSeamThreads)
   const int i = (bb - s * ch) * kSeamThreads + threadIdx.x;
   const int n = horiz ? W : H;
   if (i >= n) return;
-  for (int64_t f = blockIdx.y; f < p.B; f += gridDim.y) {
+  // kSeamFrames frames per thread, their seam loads issued together
+  for (int64_t f0 = (int64_t)blockIdx.y * kSeamFrames; f0 < p.B;
+       f0 += (int64_t)gridDim.y * kSeamFrames) {
+    int32_t av[kSeamFrames], cv[kSeamFrames];
+#pragma unroll
+    for (int k = 0; k < kSeamFrames; ++k) {
+      const int64_t f = f0 + k;
+      av[k] = cv[k] = -1;
+      if (f < p.B) {
+        av[k] = horiz ? ws.bot[(f * ws.n_ty + s) * W + i] : ws.right[(f * ws.n_tx + s) * H + i];
+        cv[k] = horiz ? ws.top[(f * ws.n_ty + s + 1) * W + i]
+                      : ws.left[(f * ws.n_tx + s + 1) * H + i];
+      }
+    }
+#pragma unroll 1
+    for (int k = 0; k < kSeamFrames; ++k) {
+    const int64_t f = f0 + k;
+    const int32_t a = av[k];
+    if (a < 0) continue;
     int32_t* G = labels + f * p.H * p.W;
     const int32_t* a_row = horiz ? ws.bot + (f * ws.n_ty + s) * W : ws.right + (f * ws.n_tx + s) * H;
     const int32_t* b_row =
         horiz ? ws.top + (f * ws.n_ty + s + 1) * W : ws.left + (f * ws.n_tx + s + 1) * H;
-    const int32_t a = a_row[i];
-    if (a < 0) continue;
-    const int32_t c = b_row[i];
+    const int32_t c = cv[k];
     if (c >= 0) {
       // a run crossing the seam gives the same (a, c) pair at consecutive
       // positions: only its first position unites (the union is idempotent)
@@ -511,6 +528,7 @@ __global__ void __launch_bounds__(kSeamThreads)
         const int32_t br = b_row[i + 1];
         if (br >= 0 && br != a && a_row[i + 1] != a) uf_unite(G, a, br);
       }
+    }
     }
   }
 }
@@ -1069,7 +1087,8 @@ int run_ccl(const LaunchCtx& ctx, const T* disp, const uint8_t* pas, const CclPa
       (int64_t)(ws.n_ty - 1) * ((p.W + kSeamThreads - 1) / kSeamThreads) +
       (int64_t)(ws.n_tx - 1) * ((p.H + kSeamThreads - 1) / kSeamThreads);
   if (seam_blocks > 0) {
-    dim3 sg((unsigned)seam_blocks, (unsigned)(p.B < 65535 ? p.B : 65535));
+    const int64_t gy = (p.B + kSeamFrames - 1) / kSeamFrames;
+    dim3 sg((unsigned)seam_blocks, (unsigned)(gy < 65535 ? gy : 65535));
     ccl_seam_kernel<<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
     if ((rc = check_launch("ccl_seam_kernel"))) return rc;
   }
