@@ -169,15 +169,6 @@ __device__ __forceinline__ int uf_find_o(volatile int32_t* L, int x) {
   }
 }
 
-__device__ __forceinline__ int uf_root_o(const volatile int32_t* L, int x) {
-  int p = ld_o(L, x);
-  while (p != x) {
-    x = p;
-    p = ld_o(L, x);
-  }
-  return x;
-}
-
 __device__ __forceinline__ void uf_unite_o(int32_t* L, int a, int b) {
   volatile int32_t* V = L;
   while (true) {
@@ -296,10 +287,10 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
     }
   }
   __syncthreads();
-  // every node -> its root (only root values are written in this phase)
-  for (int i = 0; i < nr; ++i) st_o(L, base + 4 * i, uf_root_o(L, base + 4 * i));
-  __syncthreads();
-  // component label = smallest pixel index, reduced into the root's entry
+  // component label = smallest pixel index, reduced into the root's entry;
+  // each node is pointed at its root on the way (roots may already hold a
+  // label -- a negative value -- from another run's reduction: the walk
+  // stops at a self-pointer or a negative entry)
   {
     int n = base;
     for (uint32_t m = stG; m; m &= m - 1u, n += 4) {
@@ -308,8 +299,10 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
       const uint32_t a0 = A0 & run;
       const int mp = a0 ? (2 * k) * kLTW + w * 32 + __ffs(a0) - 1
                         : (2 * k + 1) * kLTW + w * 32 + __ffs(A1 & run) - 1;
-      const int pr = ld_o(L, n);
-      atomicMin(at_o(L, pr >= 0 ? pr : n), mp - kEnc);
+      int x = n;
+      for (int q = ld_o(L, x); q >= 0 && q != x; q = ld_o(L, x)) x = q;
+      if (x != n) st_o(L, n, x);
+      atomicMin(at_o(L, x), mp - kEnc);
     }
   }
   __syncthreads();
