@@ -14,26 +14,26 @@
 // Labelling (no reference function): 8-connected
 // components of the passable set, canonical label = smallest raster index in
 // the component.  The passable set is a BIT mask (one uint32 word per 32
-// pixels of a row) and the union-find runs over word-runs (maximal runs of
-// set bits inside one word), not pixels: ~4x fewer nodes and unions than a
-// pixel union-find on street scenes.  Every link goes from the larger node
-// to the smaller (atomicMin), so a root is always its component's minimum
-// and the result is independent of scheduling.  Three launches per batch:
+// pixels of a row) and the union-find runs over band runs (maximal runs of
+// set bits of two OR-ed rows inside one word), not pixels.  Every link goes
+// from the larger node to the smaller (atomicMin), so a root is always its
+// component's minimum and the result is independent of scheduling.  Three
+// launches per batch:
 //
 //   1. ccl_tile_kernel   128x128 tile per CTA, 256 threads = (2-row band,
 //      word); bits from passable_bits_kernel (or a uint8 grid), band-run
-//      union-find in shared memory, tile-border labels -> compact
-//      seam rows / columns, global node init G[root] = root for
-//      border-touching roots, and the tile's parent array (2-byte node ids,
-//      roots at run starts) + border-root flags for pass 3.
+//      union-find in shared memory, tile-border labels -> compact seam rows
+//      / columns, global node init G[root] = root for border-touching roots,
+//      the slot labels (16-bit tile pixel index per band-run slot) and the
+//      border-root flags for pass 3.
 //   2. ccl_seam_kernel   unions across tile seams in global memory (G is the
 //      label array itself; only border-touching roots are ever nodes).
 //   3. ccl_resolve_kernel  walks G once per border-touching root, then maps
-//      each pixel to its run start (bit ops), the run to its root (the tile's
-//      parent array) and the root to its label, with coalesced stores.
+//      each pixel to its band run (bit ops), the run to its tile label (the
+//      slot labels) and that to its final label, with coalesced stores.
 //
-// HBM traffic per pixel from the fused pass's bit mask: 1/8 B bits in, 2 B
-// local roots out and back, 4 B labels out (+ the sparse seam/root traffic),
+// HBM traffic per pixel from the bit mask: 1/8 B bits in (twice), 1/2 B slot
+// labels out and back, 4 B labels out (+ the sparse seam / root traffic),
 // against the 4 B/px floor of writing the labels.
 
 #include <cuda_runtime.h>
