@@ -29,8 +29,10 @@
 // pass H runs; the AoS-6 output tile is staged in row-major shared memory
 // (pitch 3072 + 16 B: conflict-free float4 writes from lanes that own
 // different rows) and leaves as one contiguous 3 KB bulk copy
-// (cp.async.bulk) per output row, 16 per item, so HBM sees full-line writes
-// only.  Persistent grid, two CTAs per SM.
+// (cp.async.bulk, L2 evict_first) per output row, 16 per item, so HBM sees
+// full-line writes only; the store lanes hand the staging tile back through
+// an mbarrier that pass H waits on only after its sliding sums.  Persistent
+// grid, two CTAs per SM.
 
 #include <cuda.h>
 #include <cuda_runtime.h>
