@@ -132,19 +132,22 @@ def write_pfm_normals(field: NormalField) -> bytes:
 
 def _png16_samples(data: bytes) -> np.ndarray:
     """The PNG container (zlib + filters) decoded by PIL, as the reference
-    does; returns the raw 16-bit samples."""
+    does; returns the raw 16-bit samples.  Rejections carry the reference's
+    messages (formats.py:135-146)."""
     from PIL import Image
     try:
-        img = Image.open(io.BytesIO(data))
-        img.load()
+        with Image.open(io.BytesIO(data)) as img:
+            img.load()
+            kind, mode, raw = img.format, img.mode, np.asarray(img)
     except Exception as exc:
         raise FormatError(f"not a decodable PNG: {exc}") from None
-    if img.format != "PNG":
-        raise FormatError(f"expected PNG, got {img.format}")
-    if img.mode not in ("I;16", "I"):
-        raise FormatError(f"expected 16-bit single-channel PNG, got mode {img.mode!r}")
-    raw = np.asarray(img)
-    if raw.ndim != 2 or raw.size == 0 or raw.min() < 0 or raw.max() > 0xFFFF:
+    problem = (f"expected PNG, got {kind}" if kind != "PNG" else
+               f"expected 16-bit single-channel PNG, got mode {mode!r}"
+               if mode not in ("I;16", "I") else None)
+    if problem:
+        raise FormatError(problem)
+    ok = raw.ndim == 2 and raw.size > 0 and 0 <= int(raw.min()) and int(raw.max()) <= 0xFFFF
+    if not ok:
         raise FormatError("PNG samples out of 16-bit range")
     return raw.astype(np.uint16)
 
@@ -184,11 +187,14 @@ def write_disparity_png16(field: ScalarField, scale: float = 256.0,
     """Inverse of read_disparity_png16; valid raws clamp to [1, 65535]
     (formats.py:153-162)."""
     from PIL import Image
-    raw = np.clip(np.rint(field.values * float(scale) + 1.0), 1, 0xFFFF)
-    raw = np.where(field.mask, raw, float(invalid_value)).astype(np.uint16)
-    buf = io.BytesIO()
-    Image.fromarray(raw).save(buf, format="PNG")
-    return buf.getvalue()
+    # quantise the valid samples only (round half to even, then clamp into the
+    # raw range 1 .. 65535); every other pixel carries the invalid raw value
+    q = np.full(field.values.shape, invalid_value, dtype=np.uint16)
+    valid = np.asarray(field.mask, dtype=bool)
+    q[valid] = np.clip(np.rint(field.values[valid] * float(scale) + 1.0), 1.0, 65535.0)
+    out = io.BytesIO()
+    Image.fromarray(q).save(out, format="PNG")
+    return out.getvalue()
 
 
 # --------------------------------------------------------------------------
