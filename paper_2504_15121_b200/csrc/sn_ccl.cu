@@ -105,6 +105,7 @@ __global__ void passable_kernel(const T* __restrict__ disp, const CclParams p,
 __device__ __forceinline__ int uf_find(volatile int32_t* L, int x) {
   while (true) {
     const int p = L[x];
+    SN_ASSERT(p >= 0 && p <= x);  // links only ever go to smaller nodes
     if (p == x) return x;
     const int gp = L[p];
     if (gp == p) return p;
@@ -148,19 +149,25 @@ __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
 // parent value is directly the address of its entry (no index arithmetic in
 // the find loops).  Roots' entries later hold label - kEnc (< 0).
 __device__ __forceinline__ int soff(int s) { return (s + (s >> 4)) << 2; }
+constexpr int kParentBytes = (kSlots + kSlots / 16) * 4;
+#define SN_CHECK_OFF(off) SN_ASSERT((off) >= 0 && (off) < kParentBytes && ((off) & 3) == 0)
 __device__ __forceinline__ int ld_o(const volatile int32_t* L, int off) {
+  SN_CHECK_OFF(off);
   return *reinterpret_cast<const volatile int32_t*>(reinterpret_cast<const volatile char*>(L) + off);
 }
 __device__ __forceinline__ void st_o(volatile int32_t* L, int off, int v) {
+  SN_CHECK_OFF(off);
   *reinterpret_cast<volatile int32_t*>(reinterpret_cast<volatile char*>(L) + off) = v;
 }
 __device__ __forceinline__ int* at_o(int32_t* L, int off) {
+  SN_CHECK_OFF(off);
   return reinterpret_cast<int*>(reinterpret_cast<char*>(L) + off);
 }
 
 __device__ __forceinline__ int uf_find_o(volatile int32_t* L, int x) {
   while (true) {
     const int p = ld_o(L, x);
+    SN_ASSERT(p >= 0 && p <= x);  // links only ever go to smaller slots
     if (p == x) return x;
     const int gp = ld_o(L, p);
     if (gp == p) return p;
@@ -403,6 +410,7 @@ __global__ void __launch_bounds__(kLThreads)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       q[i] = ((uint32_t)(src[2 * i] + kEnc) & 0xffffu) | ((uint32_t)(src[2 * i + 1] + kEnc) << 16);
+    SN_ASSERT(tile >= 0 && tile < p.B * ws.n_tx * ws.n_ty);
     uint4* dst = reinterpret_cast<uint4*>(ws.lbl + tile * kSlots + tid * kWordSlots);
     dst[0] = make_uint4(q[0], q[1], q[2], q[3]);
     dst[1] = make_uint4(q[4], q[5], q[6], q[7]);
@@ -446,6 +454,7 @@ __global__ void __launch_bounds__(kLThreads)
       ws.flags[tile * (kTilePx / 32) + i] = fw;
       for (uint32_t m = fw; m; m &= m - 1u) {
         const int g = frame_index(i * 32 + __ffs(m) - 1, x0, y0, W);
+        SN_ASSERT(g >= 0 && (int64_t)g < p.H * p.W);
         G[g] = g;
       }
     }
@@ -506,6 +515,7 @@ __global__ void __launch_bounds__(kSeamThreads)
     const int32_t* b_row =
         horiz ? ws.top + (f * ws.n_ty + s + 1) * W : ws.left + (f * ws.n_tx + s + 1) * H;
     const int32_t c = cv[k];
+    SN_ASSERT((int64_t)a < p.H * p.W && (int64_t)c < p.H * p.W);
     if (c >= 0) {
       // a run crossing the seam gives the same (a, c) pair at consecutive
       // positions: only its first position unites (the union is idempotent)
@@ -515,10 +525,12 @@ __global__ void __launch_bounds__(kSeamThreads)
       // with that pixel straight (it unites them itself)
       if (i > 0) {
         const int32_t bl = b_row[i - 1];
+        SN_ASSERT((int64_t)bl < p.H * p.W);
         if (bl >= 0 && bl != a && a_row[i - 1] != a) uf_unite(G, a, bl);
       }
       if (i + 1 < n) {
         const int32_t br = b_row[i + 1];
+        SN_ASSERT((int64_t)br < p.H * p.W);
         if (br >= 0 && br != a && a_row[i + 1] != a) uf_unite(G, a, br);
       }
     }
@@ -603,6 +615,7 @@ __global__ void __launch_bounds__(kLThreads)
       rank0[tid * FPT + j] = k;
       for (uint32_t m = fw[j]; m; m &= m - 1u) {
         const int v = (tid * FPT + j) * 32 + __ffs(m) - 1;
+        SN_ASSERT(k < 512 && (int64_t)frame_index(v, x0, y0, W) < p.H * p.W);
         if (k < 512) fin[k] = uf_root(G, frame_index(v, x0, y0, W));
         ++k;
       }
@@ -616,7 +629,11 @@ __global__ void __launch_bounds__(kLThreads)
     const int nr = __popc(run_starts(band_word(bits, kb, w)));
     for (int i = 0; i < nr; ++i) {
       const int slot = base + i;
+      SN_ASSERT(slot >= 0 && slot < kSlots + kSlots / 16);
       const int v = lab[slot];
+      SN_ASSERT(v >= 0 && v < kTilePx);
+      SN_ASSERT(!((flag[v >> 5] >> (v & 31)) & 1u) ||
+                rank0[v >> 5] + __popc(flag[v >> 5] & ((1u << (v & 31)) - 1u)) < 512);
       const uint32_t fwv = flag[v >> 5];
       const uint32_t bit = 1u << (v & 31);
       lab[slot] = (fwv & bit) ? fin[rank0[v >> 5] + __popc(fwv & (bit - 1u))]
@@ -643,6 +660,7 @@ __global__ void __launch_bounds__(kLThreads)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (j > 0 && ((sb >> j) & 1u)) ++s;
+        SN_ASSERT(!((ab >> j) & 1u) || (s >= 0 && s < kWordSlots));
         v[j] = ((ab >> j) & 1u) ? lab[base + s] : -1;
       }
       *reinterpret_cast<int4*>(out + (y0 + r) * W + x0 + w * 32 + sub) =
@@ -978,7 +996,8 @@ __global__ void __launch_bounds__(32, 32)
         v = (v & keep) | (rot & ~keep);
       }
       const int y = y0 + 8 * k + g8;
-      if (y < H && gw < WW) bits[((int64_t)f * p.H + y) * WW + gw] = v;
+      SN_ASSERT(f < p.B);
+    if (y < H && gw < WW) bits[((int64_t)f * p.H + y) * WW + gw] = v;
     }
   }
 }

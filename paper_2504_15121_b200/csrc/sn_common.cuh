@@ -5,6 +5,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifdef SN_CHECK
+#include <cstdio>
+#endif
 
 #include "sn_b200.h"
 
@@ -12,6 +15,24 @@ namespace sn {
 
 // ---------------------------------------------------------------------------
 // kernel parameters shared by the fixed-pass kernels
+
+// Bounds checks of the checked build (make check: -DSN_CHECK): a failed check
+// prints its site and traps, which fails the calling test.  No code at all in
+// the product build.
+#ifdef SN_CHECK
+#define SN_ASSERT(cond)                                                              \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("SN_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+             #cond, (int)blockIdx.x, (int)threadIdx.x);                              \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define SN_ASSERT(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 struct FixedParams {
   int64_t B, H, W;

@@ -444,6 +444,10 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   const int gx = x0 - R + c;
   const int r0 = h * HG;  // first input row of the unit (item-relative, incl. halo)
   const T* col = in + r0 * BW + c + sh;
+  // the unit's column of the input tile and its (C, Rr) entries stay inside
+  // their shared-memory arrays
+  SN_ASSERT(!unit || (c + sh >= 0 && c + sh < BW && r0 + NV <= Cfg::NR && c < NC &&
+                      r0 + HG <= kCP));
   T raw[NV];
   bool all_small = true;  // every sample finite with |v| <= 2^40 (sliding sums exact)
   uint32_t png_inv = 0;   // PNG16: bit i = sample i is the invalid value
@@ -591,6 +595,7 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   const float dv_f = ((float)yv - p.v0_hi) - p.v0_lo;
   const float du_hi = (float)xb - p.u0_hi;  // exact; + j stays exact
   const T* drow = in + (g + R) * BW + colbase + R + sh;  // centre disparities of the run
+  SN_ASSERT(colbase + NH <= Cfg::NC && colbase + R + sh + kRun <= BW && sh >= 0 && g + R < Cfg::NR);
   // staging address of chunk c (0..11, 16 B) of this run: row g, 192 B per run
   const uint32_t row_a = stage_base + (uint32_t)g * (uint32_t)kRowPitch + (uint32_t)q * 192u;
   auto stg_addr = [&](int c) { return row_a + (uint32_t)c * 16u; };
@@ -808,6 +813,8 @@ __global__ void __launch_bounds__(kFastThreads, 2)
       // (dispatch_square_staged), whose pad column takes the extra record
       if (y0 + b < H) {
         const int n = min(kTW, (int)out_pitch - x0);
+        // the row's records stay inside the [B][H][out_pitch] output
+        SN_ASSERT(n > 0 && x0 + n <= out_pitch && bz < p.B && y0 + b < H);
 #if SN_L2HINT & 2
         bulk_store_1d_hint(out6 + (((int64_t)bz * H + y0 + b) * out_pitch + x0) * 6,
                            smem + Cfg::STAGE + (size_t)b * kRowPitch, (uint32_t)n * 24u,
