@@ -150,6 +150,7 @@ __device__ __forceinline__ void uf_unite(int32_t* L, int a, int b) {
 // the find loops).  Roots' entries later hold label - kEnc (< 0).
 __device__ __forceinline__ int soff(int s) { return (s + (s >> 4)) << 2; }
 constexpr int kParentBytes = (kSlots + kSlots / 16) * 4;
+static_assert(kParentBytes < 65536, "queued pairs pack two offsets into 16 bits each");
 #define SN_CHECK_OFF(off) SN_ASSERT((off) >= 0 && (off) < kParentBytes && ((off) & 3) == 0)
 __device__ __forceinline__ int ld_o(const volatile int32_t* L, int off) {
   SN_CHECK_OFF(off);
@@ -251,7 +252,36 @@ __device__ __forceinline__ int pixel_slot(const uint32_t* bits, int r, int c) {
          4 * rank_at(run_starts(band_word(bits, k, w)), c & 31);
 }
 
-__device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits, int tid) {
+constexpr int kUnionQueue = 160;  // pairs per warp queue (8 CTAs/SM: <= 27.5 KB each)
+
+// One union of the tile pass.  A lane's first pair is united in place; the
+// later ones go to the warp's queue while it has room (warp-aggregated: the
+// active lanes take consecutive slots, one shared-memory atomic per call
+// site), else in place too.  The queue is united by all 32 lanes after the
+// pair walk: the per-lane pair counts differ a lot within a warp (a lane
+// with many runs or overlaps kept the others idle), the queue spreads them.
+__device__ __forceinline__ void unite_or_queue(int32_t* L, uint32_t* uq, int* uq_n, int a, int b,
+                                               int& done) {
+  if (done++ == 0) {
+    uf_unite_o(L, a, b);
+    return;
+  }
+  const uint32_t act = __activemask();
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(act) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(uq_n, __popc(act));
+  base = __shfl_sync(act, base, leader);
+  const int slot = base + __popc(act & ((1u << lane) - 1u));
+  if (slot < kUnionQueue) {
+    uq[slot] = ((uint32_t)a << 16) | (uint32_t)b;  // offsets < 2^16
+    return;
+  }
+  uf_unite_o(L, a, b);
+}
+
+__device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits, int tid,
+                                                uint32_t* uq, int* uq_n) {
   const int k = tid >> 2, w = tid & 3;
   // byte offset of this word's first slot; the word's slots follow at +4,
   // the left word's at -68, the band above's at -272 (one band = 68 words)
@@ -261,11 +291,13 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
   const uint32_t G = A0 | A1, stG = run_starts(G);
   const int nr = __popc(stG);
   for (int i = 0; i < nr; ++i) st_o(L, base + 4 * i, base + 4 * i);
+  if ((tid & 31) == 0) *uq_n = 0;
+  int npairs = 0;  // this lane's pairs so far
   __syncthreads();
   // a band run crossing into this word from the left neighbour word
   if ((G & 1u) && w > 0) {
     const uint32_t Gl = band_word(bits, k, w - 1);
-    if (Gl >> 31) uf_unite_o(L, base, base - kWordOff + 4 * last_rank(run_starts(Gl)));
+    if (Gl >> 31) unite_or_queue(L, uq, uq_n, base, base - kWordOff + 4 * last_rank(run_starts(Gl)), npairs);
   }
   // band k-1: only this band's first-row pixels touch it (its last row)
   if (k > 0) {
@@ -283,14 +315,26 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
       uint32_t o = (a | (a << 1) | (a >> 1)) & B;
       while (o) {
         const int p = __ffs(o) - 1;
-        uf_unite_o(L, n, bbase + 4 * rank_at(stGb, p));
+        unite_or_queue(L, uq, uq_n, n, bbase + 4 * rank_at(stGb, p), npairs);
         const uint32_t zb = ~Gb & ~upto_bit(p);  // zeros of band k-1 above p: end of that band run
         if (!zb) break;
         o &= ~((zb & (0u - zb)) - 1u);
       }
       if ((a & 1u) && (BL >> 31))
-        uf_unite_o(L, n, bbase - kWordOff + 4 * last_rank(run_starts(bits[rb - kLWords - 1] | BL)));
-      if ((a >> 31) && (BR & 1u)) uf_unite_o(L, n, bbase + kWordOff);
+        unite_or_queue(L, uq, uq_n, n,
+                       bbase - kWordOff + 4 * last_rank(run_starts(bits[rb - kLWords - 1] | BL)),
+                       npairs);
+      if ((a >> 31) && (BR & 1u)) unite_or_queue(L, uq, uq_n, n, bbase + kWordOff, npairs);
+    }
+  }
+  // the queued pairs, one per lane (any union order gives the same min-slot
+  // roots)
+  __syncwarp();
+  {
+    const int cnt = min(*reinterpret_cast<volatile int*>(uq_n), kUnionQueue);
+    for (int i = tid & 31; i < cnt; i += 32) {
+      const uint32_t e = uq[i];
+      uf_unite_o(L, (int)(e >> 16), (int)(e & 0xffffu));
     }
   }
   __syncthreads();
@@ -342,7 +386,7 @@ __device__ __forceinline__ int frame_index(int px, int x0, int y0, int W) {
 constexpr size_t kTileSmem = (size_t)(kSlots + kSlots / 16) * 4;
 
 template <int MODE>
-__global__ void __launch_bounds__(kLThreads)
+__global__ void __launch_bounds__(kLThreads, 8)
     ccl_tile_kernel(const uint8_t* __restrict__ pas_in, const CclParams p, const CclWorkspace ws,
                     int32_t* __restrict__ labels) {
   extern __shared__ __align__(16) int32_t smem[];
@@ -380,7 +424,9 @@ __global__ void __launch_bounds__(kLThreads)
   }
 
   int32_t* L = smem;
-  band_union_find(L, bits, tid);
+  __shared__ uint32_t union_q[kLThreads / 32][kUnionQueue];
+  __shared__ int union_n[kLThreads / 32];
+  band_union_find(L, bits, tid, union_q[warp], &union_n[warp]);
 
   // every band run's entry becomes its component label, encoded as a root's
   // (label - kEnc; race-free: roots keep their value, and a non-root entry is
