@@ -252,7 +252,12 @@ __device__ __forceinline__ int pixel_slot(const uint32_t* bits, int r, int c) {
          4 * rank_at(run_starts(band_word(bits, k, w)), c & 31);
 }
 
-constexpr int kUnionQueue = 160;  // pairs per warp queue (8 CTAs/SM: <= 27.5 KB each)
+// pairs per warp queue: the 8 queues (7 KB) share their shared memory with the
+// tile's border flags (2 KB), which are only used after the unions -- 8 CTAs
+// per SM need <= 27.5 KB each (160 / 192 / 224 pairs measured alike: the
+// queues rarely fill)
+constexpr int kUnionQueue = 224;
+constexpr int kScratchWords = (kLThreads / 32) * kUnionQueue;
 
 // One union of the tile pass.  A lane's first pair is united in place; the
 // later ones go to the warp's queue while it has room (warp-aggregated: the
@@ -281,7 +286,7 @@ __device__ __forceinline__ void unite_or_queue(int32_t* L, uint32_t* uq, int* uq
 }
 
 __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits, int tid,
-                                                uint32_t* uq, int* uq_n) {
+                                                uint32_t* uq, int* uq_n, uint32_t* flag) {
   const int k = tid >> 2, w = tid & 3;
   // byte offset of this word's first slot; the word's slots follow at +4,
   // the left word's at -68, the band above's at -272 (one band = 68 words)
@@ -356,6 +361,8 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
       atomicMin(at_o(L, x), mp - kEnc);
     }
   }
+  // the union queues are spent: their memory becomes the border flags
+  for (int i = tid; i < kLTW * kLTH / 32; i += kLThreads) flag[i] = 0u;
   __syncthreads();
 }
 
@@ -391,7 +398,9 @@ __global__ void __launch_bounds__(kLThreads, 8)
                     int32_t* __restrict__ labels) {
   extern __shared__ __align__(16) int32_t smem[];
   __shared__ uint32_t bits[kRowWords];
-  __shared__ uint32_t flag[kTilePx / 32];
+  static_assert(kScratchWords >= kTilePx / 32, "the border flags live in the union queues");
+  __shared__ uint32_t scratch[kScratchWords];
+  uint32_t* flag = scratch;  // after the unions
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int W = (int)p.W, H = (int)p.H;
   const int tx = blockIdx.x, ty = blockIdx.y;
@@ -400,7 +409,6 @@ __global__ void __launch_bounds__(kLThreads, 8)
   const int64_t frow = (int64_t)blockIdx.z * H;
   const int64_t tile = ((int64_t)blockIdx.z * ws.n_ty + ty) * ws.n_tx + tx;
 
-  for (int i = tid; i < kTilePx / 32; i += kLThreads) flag[i] = 0u;
   if (MODE == 1) {
     for (int rw = warp; rw < kRowWords; rw += kLThreads / 32) {
       const int r = rw >> 2, c = (rw & 3) * 32 + lane;
@@ -424,9 +432,8 @@ __global__ void __launch_bounds__(kLThreads, 8)
   }
 
   int32_t* L = smem;
-  __shared__ uint32_t union_q[kLThreads / 32][kUnionQueue];
   __shared__ int union_n[kLThreads / 32];
-  band_union_find(L, bits, tid, union_q[warp], &union_n[warp]);
+  band_union_find(L, bits, tid, scratch + warp * kUnionQueue, &union_n[warp], flag);
 
   // every band run's entry becomes its component label, encoded as a root's
   // (label - kEnc; race-free: roots keep their value, and a non-root entry is
