@@ -661,18 +661,27 @@ __global__ void __launch_bounds__(kLThreads)
   // walk G once per flagged component.  Nodes are only ever tile-component
   // labels, and a concurrent resolve of another tile overwrites such a node
   // with its final label -- an ancestor -- so the read-only walk is valid.
+  // The components' frame indices first (each thread its flag words), then
+  // the walks spread over the block, one component per thread: a thread's
+  // flag words can hold many components, and every walk is a chain of
+  // dependent L2 loads
+  int n_flagged = 0;
+  for (int i = 0; i < kLThreads / 32; ++i) n_flagged += warp_sum[i];
+  n_flagged = min(n_flagged, 512);
+#pragma unroll
+  for (int j = 0; j < FPT; ++j) {
+    rank0[tid * FPT + j] = k;
+    for (uint32_t m = fw[j]; m; m &= m - 1u) {
+      const int v = (tid * FPT + j) * 32 + __ffs(m) - 1;
+      SN_ASSERT(k < 512 && (int64_t)frame_index(v, x0, y0, W) < p.H * p.W);
+      if (k < 512) fin[k] = frame_index(v, x0, y0, W);
+      ++k;
+    }
+  }
+  __syncthreads();
   {
     const volatile int32_t* G = labels + fbase;
-#pragma unroll
-    for (int j = 0; j < FPT; ++j) {
-      rank0[tid * FPT + j] = k;
-      for (uint32_t m = fw[j]; m; m &= m - 1u) {
-        const int v = (tid * FPT + j) * 32 + __ffs(m) - 1;
-        SN_ASSERT(k < 512 && (int64_t)frame_index(v, x0, y0, W) < p.H * p.W);
-        if (k < 512) fin[k] = uf_root(G, frame_index(v, x0, y0, W));
-        ++k;
-      }
-    }
+    for (int i = tid; i < n_flagged; i += kLThreads) fin[i] = uf_root(G, fin[i]);
   }
   __syncthreads();
   // final label of every band-run slot, by the slot's owner thread (band, word)
