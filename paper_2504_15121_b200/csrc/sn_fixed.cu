@@ -265,10 +265,17 @@ __device__ __noinline__ float depth_rare(double fxb, float d) { return (float)(f
 // sums of raw - 1 with dn = raw - 1 (the normal is homogeneous in (U, V, d):
 // same direction as with d = (raw - 1)/scale, up to sign(scale)); else
 // dn = d.
-template <typename A>
+//
+// NANOK (fp32 input): the validity test folds into the arithmetic -- the
+// fixed depth zz is NaN exactly when d is not a positive value, so r + (zz -
+// zz) is r or NaN; pixels whose window holds an invalid sample or whose depth
+// overflowed to inf (rare2, bit e for pixel e; usually 0) take the explicit
+// test.  Otherwise ok0 / ok1 are the pixels' validity.
+template <typename A, bool NANOK = false>
 __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, float d1, float dn0,
                                              float dn1, float2 zz, bool ok0, bool ok1, float duh,
-                                             float dv, const FixedParams& p, float* o) {
+                                             float dv, const FixedParams& p, float* o,
+                                             uint32_t wb2 = 0u, uint32_t rare2 = 0u) {
   constexpr bool kInt = sizeof(A) == 4;
   // points; zz = the depths as fixed by the caller (pass_h: fxb_f * rcp(d),
   // or NaN / an fp64 division where that leaves (0, FLT_MAX)); duh = (x -
@@ -301,8 +308,19 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
     if (p.png_sign < 0) r = make_float2(-r.x, -r.y);
   }
   // an invalid pixel's normal is NaN: one select on r instead of three on n
-  if (!ok0) r.x = __int_as_float(0x7fc00000);
-  if (!ok1) r.y = __int_as_float(0x7fc00000);
+  if constexpr (NANOK) {
+    const float2 r_in = r;
+    r = __fadd2_rn(r, __fadd2_rn(zz, make_float2(-zz.x, -zz.y)));
+    ok0 = !(wb2 & 1u) && d0 > 0.0f;  // = dpos, used by the rare paths below only
+    ok1 = !(wb2 & 2u) && d1 > 0.0f;
+    if (rare2) {
+      r.x = ok0 ? r_in.x : __int_as_float(0x7fc00000);
+      r.y = ok1 ? r_in.y : __int_as_float(0x7fc00000);
+    }
+  } else {
+    if (!ok0) r.x = __int_as_float(0x7fc00000);
+    if (!ok1) r.y = __int_as_float(0x7fc00000);
+  }
   const float2 nx = __fmul2_rn(ax, r), ny = __fmul2_rn(ay, r), nz = __fmul2_rn(az, r);
   o[3] = nx.x;
   o[4] = ny.x;
@@ -636,6 +654,7 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   }
   // depths zf = fxb * rcp(d) of the run's pixels (zc[1 .. kRun])
   float zc[kRun + 2], df[kRun];
+  uint32_t zinf = 0;  // bit j: pixel j's depth overflowed fp32 (fp64 division > FLT_MAX)
 #pragma unroll
   for (int j = 0; j < kRun; ++j) {
     df[j] = dflt(drow[j], p);
@@ -656,9 +675,11 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
     if (!(lo > 0.0f && hi < 3.402823466e38f)) {
 #pragma unroll
       for (int j = 0; j < kRun; ++j)
-        if (!(zc[j + 1] > 0.0f && zc[j + 1] < 3.402823466e38f))
+        if (!(zc[j + 1] > 0.0f && zc[j + 1] < 3.402823466e38f)) {
           zc[j + 1] = (df[j] > 0.0f && df[j] <= 3.402823466e38f) ? depth_rare(p.fxb, df[j])
                                                                 : __int_as_float(0x7fc00000);
+          if (zc[j + 1] == __int_as_float(0x7f800000)) zinf |= 1u << j;  // z beyond fp32
+        }
     }
   }
   // the staging tile is free once the previous item's bulk stores have read it
@@ -679,7 +700,13 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
       };
       f32_epi = safe((double)drow[j]) && safe((double)drow[j + 1]);
     }
-    if (f32_epi) {
+    if constexpr (sizeof(T) == 4 && !kIntAcc<T>) {
+      // fp32 input: validity from the fixed depths and the support bits
+      records_pair<A, true>(Us[j], Vs[j], Us[j + 1], Vs[j + 1], df[j], df[j + 1], df[j],
+                            df[j + 1], make_float2(zc[j + 1], zc[j + 2]), false, false,
+                            du_hi + (float)j, dv_f, p, o, (win >> j) & 3u,
+                            ((win | zinf) >> j) & 3u);
+    } else if (f32_epi) {
       records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], df[j], df[j + 1], dnorm(drow[j], df[j]),
                    dnorm(drow[j + 1], df[j + 1]), make_float2(zc[j + 1], zc[j + 2]), ok0, ok1,
                    du_hi + (float)j, dv_f, p, o);
