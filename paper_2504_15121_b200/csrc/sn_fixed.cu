@@ -472,12 +472,16 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
   uint32_t f16 = 0;       // this unit's column flags (0 for idle lanes)
   if (unit) {
     if constexpr (sizeof(T) == 4) {
-      // |v| <= 2^40 for every sample (NaN fails): one predicated compare each
+      // |v| <= 2^40 for every sample (NaN fails): a chain of three-input
+      // NaN-propagating maxima of |v|, one compare
 #pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        raw[i] = col[i * BW];
-        all_small &= fabsf(raw[i]) <= 1099511627776.0f;
-      }
+      for (int i = 0; i < NV; ++i) raw[i] = col[i * BW];
+      float m = fabsf(raw[0]);
+      int i = 1;
+#pragma unroll
+      for (; i + 1 < NV; i += 2) m = max3_nan(m, fabsf(raw[i]), fabsf(raw[i + 1]));
+      if (i < NV) m = max3_nan(m, fabsf(raw[i]), fabsf(raw[i]));
+      all_small = m <= 1099511627776.0f;
     } else if constexpr (sizeof(T) == 2) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
@@ -667,11 +671,14 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   // (NaN-propagating min / max: one test for its 8 depths)
   {
     float lo = zc[1], hi = zc[1];
+    static_assert(kRun % 2 == 0, "depth test: pairs after the first");
 #pragma unroll
-    for (int j = 2; j <= kRun; ++j) {
-      asm("min.NaN.f32 %0, %0, %1;" : "+f"(lo) : "f"(zc[j]));
-      asm("max.NaN.f32 %0, %0, %1;" : "+f"(hi) : "f"(zc[j]));
+    for (int j = 2; j + 1 <= kRun; j += 2) {
+      lo = min3_nan(lo, zc[j], zc[j + 1]);
+      hi = max3_nan(hi, zc[j], zc[j + 1]);
     }
+    lo = min3_nan(lo, zc[kRun], zc[kRun]);
+    hi = max3_nan(hi, zc[kRun], zc[kRun]);
     if (!(lo > 0.0f && hi < 3.402823466e38f)) {
 #pragma unroll
       for (int j = 0; j < kRun; ++j)
