@@ -436,6 +436,24 @@ struct ItemWalk {
 // samples outside the image are masked by coordinate in pass V, which
 // reproduces the no-padding border rule kernels.py:166-176 (and arrive as
 // zeros, i.e. invalid depths, for the passable predicate).
+// OR of x >> j for j in [0, N): bit i = any of bits i .. i+N-1.  Doubling
+// spans up to the largest power of two P <= N, then the remaining N - P
+// (2 log N shift-ors instead of N)
+__host__ __device__ constexpr int pow2_floor(int n) { return n >= 2 ? 2 * pow2_floor(n / 2) : 1; }
+template <int N>
+__device__ __forceinline__ uint32_t window_or(uint32_t x) {
+  if constexpr (N <= 1) {
+    return x;
+  } else {
+    constexpr int P = pow2_floor(N);
+    uint32_t a = x;
+#pragma unroll
+    for (int span = 1; span < P; span *= 2) a |= a >> span;
+    if constexpr (P < N) a |= window_or<N - P>(x >> P);
+    return a;
+  }
+}
+
 template <int R, int AE>
 __device__ __forceinline__ int tile_x0(int x0) {
   return (x0 - R) & ~(AE - 1);
@@ -553,9 +571,7 @@ __device__ __forceinline__ void pass_v(const T* in, int sh, int x0, int y0, int 
         cr[g] = make_pair(C, Rr);
       }
     }
-    uint32_t acc = 0;
-#pragma unroll
-    for (int j = 0; j < NWIN; ++j) acc |= invb >> j;
+    const uint32_t acc = window_or<NWIN>(invb);
     // flags of column c, half h: bits 0-7 = support of output row 8h+i holds
     // an invalid sample, bit 8 = the half's sums were computed directly
     f16 = (acc & 0xFFu) | (big ? 0x100u : 0u);
@@ -606,8 +622,7 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
     uint32_t colinv = 0;
 #pragma unroll
     for (int i = 0; i < NH; ++i) colinv |= ((fl[colbase + i] >> (hshift + (g & 7))) & 1u) << i;
-#pragma unroll
-    for (int j = 0; j < NWIN; ++j) win |= colinv >> j;
+    win = window_or<NWIN>(colinv);
   }
 
   const int yg = y0 + g;
