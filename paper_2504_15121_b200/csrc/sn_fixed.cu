@@ -46,14 +46,6 @@
 
 namespace sn {
 
-// L2 policies of the fused pass (bit 0: evict_last on the input tiles, bit 1:
-// evict_first on the output rows).  Default 2: the 24 B/px of records stream
-// through L2 without pushing out the input rows that the vertically adjacent
-// item reads again as its halo -- DRAM reads 1.08x -> 1.00x of the 4 B/px
-// (64 C3 frames), time unchanged
-#ifndef SN_L2HINT
-#define SN_L2HINT 2
-#endif
 constexpr int kTW = 128;           // output columns per item
 constexpr int kG = 16;             // output rows per item
 constexpr int kCP = kG + 1;        // pitch of the column-major C/Rr/Dc arrays (odd)
@@ -807,12 +799,7 @@ __global__ void __launch_bounds__(kFastThreads, 2)
   auto load_tile = [&](const ItemWalk& w, int buf) {
     T* dst = reinterpret_cast<T*>(smem + (buf ? Cfg::IN1 : Cfg::IN0));
     mbar_arrive_expect_tx(bar + buf, (uint32_t)Cfg::IN_BYTES);
-#if SN_L2HINT & 1
-    tma_load_3d_hint(dst, &in_map, bar + buf, tile_x0<R, AE>(w.x0()), w.y0() - R, w.bz,
-                     policy_evict_last());
-#else
     tma_load_3d(dst, &in_map, bar + buf, tile_x0<R, AE>(w.x0()), w.y0() - R, w.bz);
-#endif
   };
 
   if (tid == 0) {
@@ -864,14 +851,12 @@ __global__ void __launch_bounds__(kFastThreads, 2)
         const int n = min(kTW, (int)out_pitch - x0);
         // the row's records stay inside the [B][H][out_pitch] output
         SN_ASSERT(n > 0 && x0 + n <= out_pitch && bz < p.B && y0 + b < H);
-#if SN_L2HINT & 2
+        // L2 evict_first: the 24 B/px of records stream through L2 without
+        // pushing out the input rows the vertically adjacent item reads as
+        // its halo (DRAM reads 1.08x -> 1.00x of the 4 B/px, DESIGN 4.1)
         bulk_store_1d_hint(out6 + (((int64_t)bz * H + y0 + b) * out_pitch + x0) * 6,
                            smem + Cfg::STAGE + (size_t)b * kRowPitch, (uint32_t)n * 24u,
                            policy_evict_first());
-#else
-        bulk_store_1d(out6 + (((int64_t)bz * H + y0 + b) * out_pitch + x0) * 6,
-                      smem + Cfg::STAGE + (size_t)b * kRowPitch, (uint32_t)n * 24u);
-#endif
       }
       bulk_commit();
     }

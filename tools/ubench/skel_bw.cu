@@ -21,6 +21,13 @@
 
 using namespace sn;
 
+// plain (no cache hint) bulk row copy shared -> global
+__device__ __forceinline__ void bulk_store_1d(void* gdst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
 #define CK(x)                                                                 \
   do {                                                                        \
     cudaError_t e = (x);                                                      \
