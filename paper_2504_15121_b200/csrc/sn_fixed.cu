@@ -267,7 +267,8 @@ template <typename A, bool NANOK = false>
 __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, float d1, float dn0,
                                              float dn1, float2 zz, bool ok0, bool ok1, float duh,
                                              float dv, const FixedParams& p, float* o,
-                                             uint32_t wb2 = 0u, uint32_t rare2 = 0u) {
+                                             uint32_t wb2 = 0u, uint32_t rare2 = 0u,
+                                             float2* s_out = nullptr) {
   constexpr bool kInt = sizeof(A) == 4;
   // points; zz = the depths as fixed by the caller (pass_h: fxb_f * rcp(d),
   // or NaN / an fp64 division where that leaves (0, FLT_MAX)); duh = (x -
@@ -320,6 +321,10 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
   o[9] = nx.y;
   o[10] = ny.y;
   o[11] = nz.y;
+  if (s_out != nullptr) {  // the caller tests the range once for its whole run
+    *s_out = s;
+    return;
+  }
   // both |n|^2 in fp32's comfortable range (NaN-propagating min/max: a NaN
   // fails the test) -- else the per-pixel checks below
   float smin, smax;
@@ -699,6 +704,7 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
   // the staging tile is free once the previous item's bulk stores have read it
   mbar_wait(sfree, sparity);
   float o[12];
+  float2 srun[kRun / 2];  // fp32 input: |n|^2 of the run's pixels
 #pragma unroll
   for (int j = 0; j < kRun; j += 2) {
     const bool ok0 = (((win >> j) & 1u) == 0u) && dpos(drow[j], p);
@@ -719,7 +725,7 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
       records_pair<A, true>(Us[j], Vs[j], Us[j + 1], Vs[j + 1], df[j], df[j + 1], df[j],
                             df[j + 1], make_float2(zc[j + 1], zc[j + 2]), false, false,
                             du_hi + (float)j, dv_f, p, o, (win >> j) & 3u,
-                            ((win | zinf) >> j) & 3u);
+                            ((win | zinf) >> j) & 3u, &srun[j >> 1]);
     } else if (f32_epi) {
       records_pair(Us[j], Vs[j], Us[j + 1], Vs[j + 1], df[j], df[j + 1], dnorm(drow[j], df[j]),
                    dnorm(drow[j + 1], df[j + 1]), make_float2(zc[j + 1], zc[j + 2]), ok0, ok1,
@@ -744,6 +750,33 @@ __device__ __forceinline__ void pass_h(int hl, const T* in, int sh, int x0, int 
 #pragma unroll
     for (int t = 0; t < 3; ++t)
       st_shared_v4(stg_addr((j >> 1) * 3 + t), o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
+  }
+  if constexpr (sizeof(T) == 4 && !kIntAcc<T>) {
+    // |n|^2 of the whole run in fp32's comfortable range (NaN-skipping: a NaN
+    // comes from an invalid sample, whose normal is NaN anyway) -- else the
+    // fp64 normal of every valid pixel out of range, over its staged record
+    float smin = srun[0].x, smax = srun[0].x;
+#pragma unroll
+    for (int k = 0; k < kRun / 2; ++k) {
+      smin = fminf(fminf(smin, srun[k].x), srun[k].y);
+      smax = fmaxf(fmaxf(smax, srun[k].x), srun[k].y);
+    }
+    if (!(smin > 1e-30f && smax < 1e30f)) {
+#pragma unroll
+      for (int k = 0; k < kRun; ++k) {
+        const float sk = (k & 1) ? srun[k >> 1].y : srun[k >> 1].x;
+        const bool ok = !((win >> k) & 1u) && df[k] > 0.0f;
+        if (ok && !(sk > 1e-30f && sk < 1e30f)) {
+          const float du = __fsub_rn(du_hi + (float)k, p.u0_lo);
+          const float3 n = normal_rare(Us[k], Vs[k], p.alpha, (double)df[k], (double)du,
+                                       (double)dv_f, p.fx, p.fy);
+          const uint32_t a = row_a + (uint32_t)k * 24u + 12u;
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(n.x) : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 4u), "f"(n.y) : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 8u), "f"(n.z) : "memory");
+        }
+      }
+    }
   }
   if (mask_out != nullptr && yg < H) {
     // the validity bits, recomputed here so the hot loop does not carry them
