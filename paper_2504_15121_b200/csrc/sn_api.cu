@@ -219,6 +219,8 @@ void fill_rig(FixedParams& p, const sn_rig_t* rig) {
   p.fxb = rig->fx * rig->baseline;  // geometry.py:43 evaluates fx * b first
   p.fxb_f = (float)p.fxb;
   p.inv_fx_f = (float)(1.0 / rig->fx);
+  p.nfx_f = -(float)rig->fx;
+  p.nfy_f = -(float)rig->fy;
   p.inv_fy_f = (float)(1.0 / rig->fy);
   p.u0_hi = (float)rig->u0;
   p.u0_lo = (float)(rig->u0 - (double)p.u0_hi);
@@ -253,6 +255,7 @@ int prepare(const int32_t* offsets_xy, int32_t n_off, sn_moments_t& m, OffsetTab
 
 void fill_moments(FixedParams& p, const sn_moments_t& m) {
   p.alpha = (double)m.alpha;
+  p.nal_f = -(float)p.alpha;
   p.beta = (double)m.beta;
   p.gamma = (double)m.gamma;
   p.det = (double)m.det;

@@ -41,6 +41,7 @@ struct FixedParams {
   double fxb;      // fx * b (Python double product, geometry.py:43)
   float fxb_f;     // fp32(fx * b)       point path
   float inv_fx_f;  // fp32(1 / fx)
+  float nfx_f, nfy_f, nal_f;  // -fp32(fx), -fp32(fy), -fp32(alpha): the fp32 normal's factors
   float inv_fy_f;  // fp32(1 / fy)
   float u0_hi, u0_lo, v0_hi, v0_lo;  // two-float split of u0, v0
   // integer moments of the offset pattern (exact in double)

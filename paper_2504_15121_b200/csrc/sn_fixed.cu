@@ -288,7 +288,7 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
   o[8] = zz.y;
   // normals
   const float2 Uf = make_float2((float)U0, (float)U1), Vf = make_float2((float)V0, (float)V1);
-  const float nfx = -(float)p.fx, nfy = -(float)p.fy, nal = -(float)p.alpha;
+  const float nfx = p.nfx_f, nfy = p.nfy_f, nal = p.nal_f;
   const float2 ax = __fmul2_rn(Uf, make_float2(nfx, nfx));
   const float2 ay = __fmul2_rn(Vf, make_float2(nfy, nfy));
   const float2 az = __ffma2_rn(Vf, make_float2(dv, dv),
@@ -304,11 +304,14 @@ __device__ __forceinline__ void records_pair(A U0, A V0, A U1, A V1, float d0, f
   if constexpr (NANOK) {
     const float2 r_in = r;
     r = __fadd2_rn(r, __fadd2_rn(zz, make_float2(-zz.x, -zz.y)));
-    ok0 = !(wb2 & 1u) && d0 > 0.0f;  // = dpos, used by the rare paths below only
-    ok1 = !(wb2 & 2u) && d1 > 0.0f;
-    if (rare2) {
+    if (rare2) {  // ok = dpos and support clear
+      ok0 = !(wb2 & 1u) && d0 > 0.0f;
+      ok1 = !(wb2 & 2u) && d1 > 0.0f;
       r.x = ok0 ? r_in.x : __int_as_float(0x7fc00000);
       r.y = ok1 ? r_in.y : __int_as_float(0x7fc00000);
+    } else if (s_out == nullptr) {
+      ok0 = !(wb2 & 1u) && d0 > 0.0f;
+      ok1 = !(wb2 & 2u) && d1 > 0.0f;
     }
   } else {
     if (!ok0) r.x = __int_as_float(0x7fc00000);
