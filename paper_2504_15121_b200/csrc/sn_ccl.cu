@@ -358,7 +358,9 @@ __device__ __forceinline__ void band_union_find(int32_t* L, const uint32_t* bits
       int x = n;
       for (int q = ld_o(L, x); q >= 0 && q != x; q = ld_o(L, x)) x = q;
       if (x != n) st_o(L, n, x);
-      atomicMin(at_o(L, x), mp - kEnc);
+      // the component's smallest pixel lies in its first band -- the root's
+      // band (slots are band-major): only runs of that band reduce
+      if (x >= k * kBandOff) atomicMin(at_o(L, x), mp - kEnc);
     }
   }
   // the union queues are spent: their memory becomes the border flags
