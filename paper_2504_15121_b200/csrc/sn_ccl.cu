@@ -526,12 +526,14 @@ __global__ void __launch_bounds__(kLThreads, 8)
 // A straight neighbour makes the diagonal links redundant (the diagonal
 // pixels are 8-adjacent to it along the seam row/column).
 
-// One CTA per (seam line, 256-position chunk) and frame: the line decode is
-// block-uniform 32-bit arithmetic (a 64-bit division per position cost
-// more than the unions).
+// One CTA per (seam line, 256-position chunk) and F frames: the line decode
+// is block-uniform 32-bit arithmetic (a 64-bit division per position cost
+// more than the unions).  F = 4 frames per thread (their seam loads issued
+// together) from 256-frame launches, fewer below: 64 x F frames keep the grid
+// large enough to hide the unions' latency (measured, DESIGN 4.3)
 constexpr int kSeamThreads = 256;
-constexpr int kSeamFrames = 4;
 
+template <int kSeamFrames>
 __global__ void __launch_bounds__(kSeamThreads)
     ccl_seam_kernel(const CclParams p, const CclWorkspace ws, int32_t* __restrict__ labels) {
   const int W = (int)p.W, H = (int)p.H;
@@ -1163,9 +1165,15 @@ int run_ccl(const LaunchCtx& ctx, const T* disp, const uint8_t* pas, const CclPa
       (int64_t)(ws.n_ty - 1) * ((p.W + kSeamThreads - 1) / kSeamThreads) +
       (int64_t)(ws.n_tx - 1) * ((p.H + kSeamThreads - 1) / kSeamThreads);
   if (seam_blocks > 0) {
-    const int64_t gy = (p.B + kSeamFrames - 1) / kSeamFrames;
+    const int F = p.B >= 256 ? 4 : p.B >= 128 ? 2 : 1;
+    const int64_t gy = (p.B + F - 1) / F;
     dim3 sg((unsigned)seam_blocks, (unsigned)(gy < 65535 ? gy : 65535));
-    ccl_seam_kernel<<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
+    if (F == 4)
+      ccl_seam_kernel<4><<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
+    else if (F == 2)
+      ccl_seam_kernel<2><<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
+    else
+      ccl_seam_kernel<1><<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
     if ((rc = check_launch("ccl_seam_kernel"))) return rc;
   }
   ccl_resolve_kernel<<<grid, kLThreads, 0, ctx.stream>>>(p, ws, labels);

@@ -221,6 +221,26 @@ def test_labeller_random_grids(cuda_dev, shape, density):
         assert np.array_equal(lab[i].astype(np.int64), label_components(p[i]))
 
 
+@pytest.mark.parametrize("B", [127, 128, 255, 256, 261])
+def test_labeller_batch_sizes(cuda_dev, B):
+    """Every seam-kernel variant (1 / 2 / 4 frames per thread, chosen by the
+    batch size, ragged last group included): the batch's labels equal the
+    frames' own labels computed one by one, and a sample of frames equals the
+    oracle."""
+    from oracle.stereonorm_oracle import label_components
+    from paper_2504_15121_b200 import device
+    rng = np.random.default_rng(B)
+    p = rng.random((B, 140, 270)) < 0.6
+    pd = torch.from_numpy(p).to(cuda_dev)
+    lab = device.labels_from_passable(pd).cpu().numpy()
+    for i in (0, 1, B // 2, B - 2, B - 1):
+        one = device.labels_from_passable(pd[i:i + 1]).cpu().numpy()[0]
+        assert np.array_equal(lab[i], one), i
+        assert np.array_equal(lab[i].astype(np.int64), label_components(p[i])), i
+    for i in range(0, B, 17):
+        assert np.array_equal(lab[i].astype(np.int64), label_components(p[i])), i
+
+
 @pytest.mark.parametrize("pick", ["exact_tie", "exact_only_rig", "tiny_and_huge"])
 def test_labels_filter_edge_cases(cuda_dev, pick):
     """The fp32 predicate filter must defer to the exact fp64 decision:
