@@ -420,10 +420,17 @@ __global__ void __launch_bounds__(kLThreads, 8)
       if (lane == 0) bits[rw] = b;
     }
   } else {
-    for (int i = tid; i < kRowWords; i += kLThreads) {
+    // both loads in flight before the stores (a rolled load -> store loop
+    // waits one round trip per iteration)
+    uint32_t bw[kRowWords / kLThreads];
+#pragma unroll
+    for (int k = 0; k < kRowWords / kLThreads; ++k) {
+      const int i = k * kLThreads + tid;
       const int r = i >> 2, wc = tx * kLWords + (i & 3);
-      bits[i] = (y0 + r < H && wc < ws.WW) ? ws.bits[(frow + y0 + r) * ws.WW + wc] : 0u;
+      bw[k] = (y0 + r < H && wc < ws.WW) ? __ldg(ws.bits + (frow + y0 + r) * ws.WW + wc) : 0u;
     }
+#pragma unroll
+    for (int k = 0; k < kRowWords / kLThreads; ++k) bits[k * kLThreads + tid] = bw[k];
   }
   __syncthreads();
   if (MODE == 1) {
