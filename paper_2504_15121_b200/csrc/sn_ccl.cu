@@ -554,50 +554,50 @@ __global__ void __launch_bounds__(kSeamThreads)
   const int s = bb / ch;
   const int i = (bb - s * ch) * kSeamThreads + threadIdx.x;
   const int n = horiz ? W : H;
-  if (i >= n) return;
-  // kSeamFrames frames per thread, their seam loads issued together
+  const int lane = threadIdx.x & 31;
+  // kSeamFrames frames per thread, their seam loads issued together.  The
+  // neighbour positions' values (dedupe and diagonals) come from the
+  // neighbour lanes by shuffle -- positions are consecutive across a warp --
+  // and lanes 0 / 31 load theirs with the batch (so the warp stays whole for
+  // the shuffles: positions past the line's end carry -1)
   for (int64_t f0 = (int64_t)blockIdx.y * kSeamFrames; f0 < p.B;
        f0 += (int64_t)gridDim.y * kSeamFrames) {
-    int32_t av[kSeamFrames], cv[kSeamFrames];
+    int32_t av[kSeamFrames], cv[kSeamFrames], ae[kSeamFrames], ce[kSeamFrames];
+    const int ie = lane == 0 ? i - 1 : i + 1;  // edge lanes' outside neighbour
 #pragma unroll
     for (int k = 0; k < kSeamFrames; ++k) {
       const int64_t f = f0 + k;
-      av[k] = cv[k] = -1;
-      if (f < p.B) {
-        av[k] = horiz ? ws.bot[(f * ws.n_ty + s) * W + i] : ws.right[(f * ws.n_tx + s) * H + i];
-        cv[k] = horiz ? ws.top[(f * ws.n_ty + s + 1) * W + i]
-                      : ws.left[(f * ws.n_tx + s + 1) * H + i];
-      }
+      const int32_t* a_row = horiz ? ws.bot + (f * ws.n_ty + s) * W : ws.right + (f * ws.n_tx + s) * H;
+      const int32_t* b_row =
+          horiz ? ws.top + (f * ws.n_ty + s + 1) * W : ws.left + (f * ws.n_tx + s + 1) * H;
+      const bool fin = f < p.B;
+      av[k] = fin && i < n ? a_row[i] : -1;
+      cv[k] = fin && i < n ? b_row[i] : -1;
+      const bool edge = fin && (lane == 0 || lane == 31) && ie >= 0 && ie < n;
+      ae[k] = edge ? a_row[ie] : -1;
+      ce[k] = edge ? b_row[ie] : -1;
     }
 #pragma unroll 1
     for (int k = 0; k < kSeamFrames; ++k) {
-    const int64_t f = f0 + k;
-    const int32_t a = av[k];
-    if (a < 0) continue;
-    int32_t* G = labels + f * p.H * p.W;
-    const int32_t* a_row = horiz ? ws.bot + (f * ws.n_ty + s) * W : ws.right + (f * ws.n_tx + s) * H;
-    const int32_t* b_row =
-        horiz ? ws.top + (f * ws.n_ty + s + 1) * W : ws.left + (f * ws.n_tx + s + 1) * H;
-    const int32_t c = cv[k];
-    SN_ASSERT((int64_t)a < p.H * p.W && (int64_t)c < p.H * p.W);
-    if (c >= 0) {
-      // a run crossing the seam gives the same (a, c) pair at consecutive
-      // positions: only its first position unites (the union is idempotent)
-      if (a != c && !(i > 0 && a_row[i - 1] == a && b_row[i - 1] == c)) uf_unite(G, a, c);
-    } else {
-      // diagonals; skipped where the neighbour position pairs the same a
-      // with that pixel straight (it unites them itself)
-      if (i > 0) {
-        const int32_t bl = b_row[i - 1];
-        SN_ASSERT((int64_t)bl < p.H * p.W);
-        if (bl >= 0 && bl != a && a_row[i - 1] != a) uf_unite(G, a, bl);
+      const int32_t a = av[k], c = cv[k];
+      int32_t al = __shfl_up_sync(0xffffffffu, a, 1), cl = __shfl_up_sync(0xffffffffu, c, 1);
+      int32_t ar = __shfl_down_sync(0xffffffffu, a, 1), cr = __shfl_down_sync(0xffffffffu, c, 1);
+      if (lane == 0) al = ae[k], cl = ce[k];
+      if (lane == 31) ar = ae[k], cr = ce[k];
+      if (a < 0) continue;
+      int32_t* G = labels + (f0 + k) * p.H * p.W;
+      SN_ASSERT((int64_t)a < p.H * p.W && (int64_t)c < p.H * p.W);
+      SN_ASSERT((int64_t)cl < p.H * p.W && (int64_t)cr < p.H * p.W);
+      if (c >= 0) {
+        // a run crossing the seam gives the same (a, c) pair at consecutive
+        // positions: only its first position unites (the union is idempotent)
+        if (a != c && !(al == a && cl == c)) uf_unite(G, a, c);
+      } else {
+        // diagonals; skipped where the neighbour position pairs the same a
+        // with that pixel straight (it unites them itself)
+        if (cl >= 0 && cl != a && al != a) uf_unite(G, a, cl);
+        if (cr >= 0 && cr != a && ar != a) uf_unite(G, a, cr);
       }
-      if (i + 1 < n) {
-        const int32_t br = b_row[i + 1];
-        SN_ASSERT((int64_t)br < p.H * p.W);
-        if (br >= 0 && br != a && a_row[i + 1] != a) uf_unite(G, a, br);
-      }
-    }
     }
   }
 }
