@@ -322,6 +322,67 @@ def pcie_peaks(dev, nbytes=1 << 30):
     return res
 
 
+def copy_schedule_ms(dev, B, H, W, full):
+    """The host pipeline's copies alone: sn_pipeline_host's chunks (1, 2, 4, ..
+    frames up to ~16 Mpx, sn_api.cu host_pipeline) and its event graph over
+    three streams (H2D of chunk c after chunk c-2's "compute", "compute" after
+    its H2D and chunk c-2's D2H, D2H after the "compute"), with no kernels: what
+    the PCIe link alone allows in that schedule (both directions share the
+    full-duplex link).  Best of 3, wall clock around synchronised steps."""
+    import torch
+    px = H * W
+    chunk = min(B, max(1, (16 << 20) // px))
+    sizes, f = [], 0
+    while f < B:
+        n = min(B - f, chunk if (1 << len(sizes)) >= chunk else 1 << len(sizes))
+        sizes.append(n)
+        f += n
+    n_in, n_out = chunk * px * 4, chunk * px * (28 if full else 24)
+    h_in = torch.empty(B * px * 4, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(B * px * (28 if full else 24), dtype=torch.uint8).pin_memory()
+    d_in = [torch.empty(n_in, dtype=torch.uint8, device=dev) for _ in range(2)]
+    d_out = [torch.empty(n_out, dtype=torch.uint8, device=dev) for _ in range(2)]
+    s_h, s_c, s_d = (torch.cuda.Stream(dev) for _ in range(3))
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+
+    def step():
+        f0 = 0
+        for c, n in enumerate(sizes):
+            k = c & 1
+            if c >= 2:
+                s_h.wait_event(ev_done[k])
+                s_c.wait_event(ev_out[k])
+            bi, bo = n * px * 4, n * px * (28 if full else 24)
+            with torch.cuda.stream(s_h):
+                d_in[k][:bi].copy_(h_in[f0 * px * 4:f0 * px * 4 + bi], non_blocking=True)
+            ev_in[k].record(s_h)
+            s_c.wait_event(ev_in[k])
+            ev_done[k].record(s_c)
+            s_d.wait_event(ev_done[k])
+            o = f0 * px * (28 if full else 24)
+            with torch.cuda.stream(s_d):
+                if full:  # records, then labels: two copies as in the pipeline
+                    r = n * px * 24
+                    h_out[o:o + r].copy_(d_out[k][:r], non_blocking=True)
+                    h_out[o + r:o + bo].copy_(d_out[k][r:bo], non_blocking=True)
+                else:
+                    h_out[o:o + bo].copy_(d_out[k][:bo], non_blocking=True)
+            ev_out[k].record(s_d)
+            f0 += n
+
+    best = 1e9
+    for _ in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    del h_in, h_out, d_in, d_out
+    return best * 1e3
+
+
 def flush_l2(buf, sink):
     # read 256 MB (clean lines: evicts the 126 MB L2 without leaving dirty
     # lines for the timed kernel to write back)
@@ -709,6 +770,9 @@ def main():
         # PCIe bound of one step: both directions run concurrently on the
         # plan's copy streams, so the slower direction bounds the step
         bound_s = max(h2d_b / (pcie["h2d_gbs"] * 1e9), d2h_b / (pcie["d2h_gbs"] * 1e9))
+        # the same chunks' copies with no compute (the duplex link gives a
+        # concurrent D2H less than its solo peak): what the schedule allows
+        copies_ms = copy_schedule_ms(dev, Be, H, W, full)
         e2e = {"value": world * px_e2e / 1e6 / sec, "unit": "Mpx/s",
                "frames_per_step_per_rank": Be,
                "frames_per_sec_per_gpu": Be / sec,
@@ -718,6 +782,8 @@ def main():
                "pcie_gbs": pcie,
                "bound_ms_per_step": bound_s * 1e3,
                "frac": bound_s / sec,
+               "copies_only_ms_per_step": copies_ms,
+               "frac_vs_copies_only": copies_ms / (sec * 1e3),
                "bound": "pcie (max of H2D bytes / pinned H2D peak, D2H bytes / pinned D2H peak)",
                "path": ("sn_pipeline_host" if full else "sn_oriented_points_host") +
                        " (pinned host in/out, 3-stream H2D/compute/D2H overlap)"}
