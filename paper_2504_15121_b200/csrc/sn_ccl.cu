@@ -736,8 +736,8 @@ __global__ void __launch_bounds__(kLThreads)
         SN_ASSERT(!((ab >> j) & 1u) || (s >= 0 && s < kWordSlots));
         v[j] = ((ab >> j) & 1u) ? lab[base + s] : -1;
       }
-      *reinterpret_cast<int4*>(out + (y0 + r) * W + x0 + w * 32 + sub) =
-          make_int4(v[0], v[1], v[2], v[3]);
+      __stcs(reinterpret_cast<int4*>(out + (y0 + r) * W + x0 + w * 32 + sub),
+             make_int4(v[0], v[1], v[2], v[3]));
     }
   } else {
     const uint32_t upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
