@@ -481,31 +481,25 @@ __global__ void __launch_bounds__(kLThreads, 8)
   // seam rows / columns: frame index of each border pixel's component, -1 if not passable
   const int64_t seam_row = ((int64_t)blockIdx.z * ws.n_ty + ty) * W;
   const int64_t seam_col = ((int64_t)blockIdx.z * ws.n_tx + tx) * H;
-  if (warp < 2) {
-    const int r = warp == 0 ? 0 : kLTH - 1;
-    int32_t* dst = (warp == 0 ? ws.top : ws.bot) + seam_row;
-    if (y0 + r < H) {
+  // the 4 x 128 border positions over the whole block, two per thread: warps
+  // 0-3 take 32-position pieces of the first row, then of the first column,
+  // warps 4-7 of the last row, then of the last column (line warp-uniform,
+  // coalesced stores)
+  static_assert(kLTW == 128 && kLTH == 128 && kLThreads == 256, "border split");
 #pragma unroll
-      for (int w = 0; w < kLWords; ++w) {
-        const int c = w * 32 + lane, gx = x0 + c;
-        if (gx < W) {
-          int32_t v = -1;
-          if ((bits[r * kLWords + w] >> lane) & 1u)
-            v = frame_index(slot_label(L, pixel_slot(bits, r, c)), x0, y0, W);
-          dst[gx] = v;
-        }
-      }
-    }
-  } else if (warp < 4) {
-    // warp 2: first column, warp 3: last column; lanes <-> rows
-    const int c = warp == 2 ? 0 : kLTW - 1;
-    int32_t* dst = (warp == 2 ? ws.left : ws.right) + seam_col;
-    for (int r = lane; r < kLTH; r += 32) {
-      if (y0 + r >= H) break;
+  for (int j = 0; j < 2; ++j) {
+    const int q = j * kLThreads + tid;
+    const int line = q >> 7, t = q & 127;  // 0 top, 1 bottom, 2 left, 3 right
+    const bool row = line < 2;
+    const int r = row ? (line == 0 ? 0 : kLTH - 1) : t;
+    const int c = row ? t : (line == 2 ? 0 : kLTW - 1);
+    if (y0 + r < H && (!row || x0 + c < W)) {
       int32_t v = -1;
       if ((bits[r * kLWords + (c >> 5)] >> (c & 31)) & 1u)
         v = frame_index(slot_label(L, pixel_slot(bits, r, c)), x0, y0, W);
-      dst[y0 + r] = v;
+      int32_t* dst = row ? (line == 0 ? ws.top : ws.bot) + seam_row + x0 + c
+                         : (line == 2 ? ws.left : ws.right) + seam_col + y0 + r;
+      *dst = v;
     }
   }
   // global union-find nodes: one per border-touching component, G[label] = label
