@@ -989,7 +989,7 @@ __device__ __forceinline__ void pb_task(const T* colp, const T* edgep, int y0, i
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(32, 32)
     passable_bits_kernel(const T* __restrict__ disp, const FixedParams p,
-                         uint32_t* __restrict__ bits) {
+                         uint32_t* __restrict__ bits, unsigned* __restrict__ next_task) {
   const int W = (int)p.W, H = (int)p.H, WW = p.bits_ww;
   const int lane = threadIdx.x;
   const unsigned tasks_x = (unsigned)((W + kPbCols - 1) / kPbCols);
@@ -1000,7 +1000,11 @@ __global__ void __launch_bounds__(32, 32)
   const float2 qhi = make_float2(__fadd_rn(p.t_f, tm), __fadd_rn(p.t_f, tm));
   const bool pe = p.pred_exact != 0;
   const int g8 = lane & 7;
-  for (unsigned task = blockIdx.x; task < n_tasks; task += gridDim.x) {
+  // tasks handed out dynamically (their cost varies: exact-path pixels): the
+  // first by block index, then from a counter whose next value is fetched
+  // while the current task runs
+  unsigned nraw = lane == 0 ? atomicAdd(next_task, 1u) : 0u;
+  for (unsigned task = blockIdx.x; task < n_tasks;) {
     const unsigned rest = task / tasks_x;
     const int tx = (int)(task - rest * tasks_x);
     const unsigned f = rest / strips_y;
@@ -1066,6 +1070,8 @@ __global__ void __launch_bounds__(32, 32)
       SN_ASSERT(f < p.B);
     if (y < H && gw < WW) bits[((int64_t)f * p.H + y) * WW + gw] = v;
     }
+    task = gridDim.x + __shfl_sync(0xffffffffu, nraw, 0);
+    if (task < n_tasks && lane == 0) nraw = atomicAdd(next_task, 1u);
   }
 }
 
@@ -1079,11 +1085,22 @@ int run_passable_bits(const LaunchCtx& ctx, const T* disp, const FixedParams& p,
   const bool vec = p.W % 4 == 0 && reinterpret_cast<uintptr_t>(disp) % 16 == 0 && p.W >= 4;
   int64_t g = tasks;
   if (g > (int64_t)ctx.num_sms * 32) g = (int64_t)ctx.num_sms * 32;
+  // the task counter: stream-ordered scratch (concurrent calls on other
+  // streams get their own)
+  unsigned* next_task = nullptr;
+  int rc = scratch_alloc(ctx, sizeof(unsigned), reinterpret_cast<void**>(&next_task));
+  if (rc) return rc;
+  if (cudaMemsetAsync(next_task, 0, sizeof(unsigned), ctx.stream) != cudaSuccess) {
+    scratch_free(ctx, next_task);
+    return set_cuda_error("cudaMemsetAsync(task counter)");
+  }
   if (vec)
-    passable_bits_kernel<T, true><<<(unsigned)g, 32, 0, ctx.stream>>>(disp, p, bits);
+    passable_bits_kernel<T, true><<<(unsigned)g, 32, 0, ctx.stream>>>(disp, p, bits, next_task);
   else
-    passable_bits_kernel<T, false><<<(unsigned)g, 32, 0, ctx.stream>>>(disp, p, bits);
-  return check_launch("passable_bits_kernel");
+    passable_bits_kernel<T, false><<<(unsigned)g, 32, 0, ctx.stream>>>(disp, p, bits, next_task);
+  rc = check_launch("passable_bits_kernel");
+  scratch_free(ctx, next_task);
+  return rc;
 }
 template int run_passable_bits<float>(const LaunchCtx&, const float*, const FixedParams&,
                                       uint32_t*);
