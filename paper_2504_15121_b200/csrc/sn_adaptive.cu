@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
     adaptive_kernel(const T* __restrict__ disp, const float* __restrict__ depth,
                     const uint32_t* __restrict__ pbits, const __grid_constant__ AdaptiveParams ap,
                     const __grid_constant__ StarTable tab, float* __restrict__ out6,
-                    uint8_t* __restrict__ mask) {
+                    uint8_t* __restrict__ mask, unsigned* __restrict__ next_span) {
   // dynamic shared memory: the step / key tables (read warp-uniformly every
   // step: shared-memory broadcasts instead of constant-cache misses once
   // the tables outgrow it) and the warps' key masks
@@ -124,8 +124,16 @@ __global__ void __launch_bounds__(kAdaptiveThreads)
   const uint32_t lbit = 1u << lane;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   const float fnan = __int_as_float(0x7fc00000);
-  for (int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); wbase < n;
-       wbase += (int64_t)gridDim.x * blockDim.x) {
+  // 32-pixel spans handed out dynamically (a span's walks vary a lot in
+  // length): a warp's first span by its global warp index, the next ones
+  // from a counter, the next value fetched while the current span runs
+  const int64_t n_spans = (n + 31) / 32;
+  const int64_t n_static = (int64_t)gridDim.x * blockDim.x / 32;
+  unsigned nraw = lane == 0 ? atomicAdd(next_span, 1u) : 0u;
+  for (int64_t span = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / 32; span < n_spans;
+       span = n_static + __shfl_sync(0xffffffffu, nraw, 0),
+               nraw = (lane == 0 && span < n_spans) ? atomicAdd(next_span, 1u) : nraw) {
+    const int64_t wbase = span * 32;
     const int64_t idx = wbase + lane;
     const bool have = idx < n;
     const int64_t f = have ? idx / HW : 0;
@@ -355,13 +363,23 @@ int run_adaptive(const LaunchCtx& ctx, const T* disp, const AdaptiveParams& ap,
       (rc = ensure_dyn_smem(reinterpret_cast<const void*>(adaptive_kernel<1, T>), smax, ctx.device,
                             "adaptive_kernel<cd>")))
     return rc;
+  // the span counter: stream-ordered scratch (concurrent calls on other
+  // streams get their own)
+  unsigned* next_span = nullptr;
+  if ((rc = scratch_alloc(ctx, sizeof(unsigned), reinterpret_cast<void**>(&next_span)))) return rc;
+  if (cudaMemsetAsync(next_span, 0, sizeof(unsigned), ctx.stream) != cudaSuccess) {
+    scratch_free(ctx, next_span);
+    return set_cuda_error("cudaMemsetAsync(span counter)");
+  }
   if (stop == 0)
     adaptive_kernel<0, T><<<(unsigned)ga, kAdaptiveThreads, sm, ctx.stream>>>(
-        disp, depth, a.fp.bits, a, tab, out6, mask);
+        disp, depth, a.fp.bits, a, tab, out6, mask, next_span);
   else
     adaptive_kernel<1, T><<<(unsigned)ga, kAdaptiveThreads, sm, ctx.stream>>>(
-        disp, depth, nullptr, a, tab, out6, mask);
-  return check_launch("adaptive_kernel");
+        disp, depth, nullptr, a, tab, out6, mask, next_span);
+  rc = check_launch("adaptive_kernel");
+  scratch_free(ctx, next_span);
+  return rc;
 }
 template int run_adaptive<float>(const LaunchCtx&, const float*, const AdaptiveParams&,
                                  const StarTable&, int, float*, uint8_t*, void*, size_t);
