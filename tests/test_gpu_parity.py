@@ -340,6 +340,25 @@ def test_bits_filter_ties_and_ranges(cuda_dev):
         assert np.array_equal(_bits_to_bool(bits, 512)[0], orc.passable(d64, o, t)), t
 
 
+def test_bits_dynamic_tasks_cover_the_batch(cuda_dev):
+    """More bit-mask tasks than resident warps (the counter hands out all but
+    the first wave): every frame's bits equal the exact fp64 predicate's and
+    the frame computed alone."""
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(512, 256)
+    base = scenes.raycast(sc)[0]
+    B = 80  # 80 x 16 strips x 4 column tasks = 5120 tasks > 148 x 32 warps
+    d = np.stack([scenes.add_gaussian_noise(base, 0.3, 100 + i) for i in range(B)]).astype(np.float32)
+    dt = torch.from_numpy(d).to(cuda_dev)
+    bits = device.passable_bits(dt, sc.rig, 0.2)
+    ref = device.passable(dt, sc.rig, 0.2).cpu().numpy().astype(bool)
+    got = _bits_to_bool(bits, 512)
+    assert np.array_equal(got, ref)
+    for i in (0, B // 2, B - 1):
+        one = _bits_to_bool(device.passable_bits(dt[i:i + 1], sc.rig, 0.2), 512)[0]
+        assert np.array_equal(one, got[i]), i
+
+
 @pytest.mark.parametrize("shape", [(3, 256, 512), (2, 77, 130), (1, 1, 1), (4, 1024, 2048)])
 def test_compact_cloud(cuda_dev, shape):
     """Device compaction == the reference's keep rule on the dense record
