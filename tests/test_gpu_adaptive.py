@@ -124,3 +124,23 @@ def test_adaptive_random_configs_vs_oracle(cuda_dev):
         m = mask[0].cpu().numpy().astype(bool)
         assert np.array_equal(m, ok_ref), (case, cfg)
         assert max_angle_deg(out[0].cpu().numpy()[m][:, 3:], n_ref[m]) < 1e-4, (case, cfg)
+
+
+@pytest.mark.parametrize("stop", ["st", "cd"])
+def test_adaptive_dynamic_spans_match_single_frames(cuda_dev, stop):
+    """A batch with more 32-pixel spans than resident warps (the counter hands
+    out the rest) gives every frame the records and mask of the frame run
+    alone (which the static first wave covers)."""
+    from paper_2504_15121_b200 import StarConfig, device, scenes
+    sc = scenes.street_scene(2048, 1024)
+    base = scenes.raycast(sc)[0]
+    d = np.stack([scenes.add_gaussian_noise(base, 0.2, 40 + i) for i in range(3)]).astype(np.float32)
+    dt = torch.from_numpy(d).to(cuda_dev)
+    cfg = StarConfig(stop=stop, threshold=0.2 if stop == "st" else 0.1)
+    m = torch.empty(dt.shape, dtype=torch.uint8, device=cuda_dev)
+    rec = device.adaptive_points(dt, sc.rig, cfg, mask=m)
+    for i in range(3):
+        mi = torch.empty((1,) + dt.shape[1:], dtype=torch.uint8, device=cuda_dev)
+        ri = device.adaptive_points(dt[i:i + 1], sc.rig, cfg, mask=mi)
+        assert torch.equal(mi[0], m[i]), i
+        assert torch.equal(ri[0].view(torch.int32), rec[i].view(torch.int32)), i
