@@ -656,19 +656,18 @@ def main():
     bits = torch.empty((B, H, device.bit_words(W)), dtype=torch.int32, device=dev)
 
     def step(ev=None):
-        # = device.pipeline(...): fused pass, passable bits, labels -- split so
-        # each kernel's own time is bracketed by events on the launch stream
+        # the fused pass, then the labels from the disparities (predicate bit
+        # mask + labeller; from 128 frames on the library runs the two half
+        # batches on two streams, joined back into this one) -- split so the
+        # fused kernel's own time is bracketed by events on the launch stream
         if ev is not None:
             ev[0].record(stream)
         device.oriented_points(disp, rig, KSIZE, out=out)
         if ev is not None:
             ev[1].record(stream)
-        if args.pipeline == "full":
-            device.passable_bits(disp, rig, T_ST, bits=bits)
-        if ev is not None:
             ev[2].record(stream)
         if args.pipeline == "full":
-            device.labels_from_bits(bits, W, out=labels, workspace=ccl_ws)
+            device.component_labels(disp, rig, T_ST, out=labels, workspace=ccl_ws)
         if ev is not None:
             ev[3].record(stream)
 
@@ -836,8 +835,8 @@ def main():
                               "parallelism": f"frame-batch dp{world}",
                               "l2": "inputs+outputs (15 GB/step) >> 126 MB L2, no flush needed"},
             "frames_per_sec_per_gpu": B / (ms_per_step / 1e3),
-            "stages_ms_per_frame": {"fused_pass": fused_avg / B, "passable_bits": bits_avg / B,
-                                    "ccl": ccl_avg / B},
+            "stages_ms_per_frame": {"fused_pass": fused_avg / B,
+                                    "labels_incl_passable_bits": ccl_avg / B},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "fixed_square_kernel<4,float>",
@@ -849,7 +848,9 @@ def main():
             "next_rows_us_per_frame": extras,
             "next_rows_roofline": extras_roof,
             "next_rows_cpu_us_per_frame": extras_cpu,
-            "gpu_launches": args.steps * (1 + (4 if args.pipeline == "full" else 0)),
+            # fused pass + (bits, tile, seam, resolve) per half batch: two
+            # halves from 128 frames on (sn_ccl_labels_ws)
+            "gpu_launches": args.steps * (1 + ((8 if B >= 128 else 4) if args.pipeline == "full" else 0)),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -81,7 +81,11 @@ SN_API const char* sn_last_error(void);
  * for the device id and cached properties (their scratch comes from the
  * caller's workspace or from stream-ordered allocations on the caller's
  * stream) and are safe to call concurrently on distinct streams; *_host
- * calls on one plan are serialised by the plan's lock. */
+ * calls on one plan are serialised by the plan's lock.  sn_ccl_labels[_ws]
+ * [_f64] with B >= 128 frames also use the plan's second stream: the two half
+ * batches run on the caller's stream and that one (forked from and joined
+ * back into the caller's stream with events; concurrent calls on one plan
+ * queue their second halves behind each other there). */
 SN_API int sn_plan_create(int device, sn_plan_t** plan);
 SN_API int sn_plan_destroy(sn_plan_t* plan);
 
@@ -230,7 +234,8 @@ SN_API int sn_ccl_from_passable(sn_plan_t* plan, const uint8_t* passable, int64_
                          int64_t W, int64_t row_base, int32_t* labels, void* stream);
 
 /* The labeller needs a device workspace (passable bit mask + tile seam rows
- * + slot labels, sn_ccl_workspace_bytes).  The entry points above take
+ * + slot labels, sn_ccl_workspace_bytes; from 128 frames on it has room for
+ * the two half-batch workspaces sn_ccl_labels_ws uses).  The entry points above take
  * stream-ordered scratch from the library's private pool on `stream`; the
  * *_ws variants take the caller's, so concurrent streams each pass their
  * own. */

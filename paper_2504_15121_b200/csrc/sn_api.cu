@@ -175,6 +175,11 @@ struct sn_plan {
   void* h_out[2] = {nullptr, nullptr};
   size_t h_in_cap = 0, h_out_cap = 0;
   std::mutex mu;
+  // second stream for the labeller's half batches (ccl_labels_ws_impl);
+  // its own lock, held while the halves are enqueued
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::mutex aux_mu;
 };
 
 namespace {
@@ -368,6 +373,9 @@ int sn_plan_destroy(sn_plan_t* plan) {
     if (plan->s_h2d) cudaStreamDestroy(plan->s_h2d);
     if (plan->s_comp) cudaStreamDestroy(plan->s_comp);
     if (plan->s_d2h) cudaStreamDestroy(plan->s_d2h);
+    if (plan->s_aux) cudaStreamDestroy(plan->s_aux);
+    if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
+    if (plan->ev_join) cudaEventDestroy(plan->ev_join);
   }
   delete plan;
   return SN_OK;
@@ -928,8 +936,40 @@ int ccl_labels_ws_impl(sn_plan_t* plan, const T* disp, int64_t B, int64_t H, int
   if (!(t > 0.0)) return set_error(SN_EINVAL, "threshold must be positive");
   const CclParams p = make_ccl_params(B, H, W, rig->fx * rig->baseline, t);
   DeviceGuard g(plan->device);
-  return run_ccl<T>(make_ctx(plan, stream), disp, nullptr, p, row_base * W, labels, workspace,
-                    ws_bytes);
+  const LaunchCtx ctx = make_ctx(plan, stream);
+  const int64_t B0 = B / 2, B1 = B - B0;
+  const size_t w0 = ccl_workspace_bytes_one(B0, H, W);
+  if (B < kCclSplitFrames || !workspace || ws_bytes < ccl_workspace_bytes(B, H, W))
+    return run_ccl<T>(ctx, disp, nullptr, p, row_base * W, labels, workspace, ws_bytes);
+  // two half batches on two streams (the caller's and the plan's second):
+  // one half's issue-bound tile pass runs beside the other's memory-bound
+  // predicate and resolve kernels, and each launch's tail is filled
+  // (DESIGN 4.3).  Each half has its own workspace; the caller's stream
+  // waits for both.
+  std::lock_guard<std::mutex> lock(plan->aux_mu);
+  if (!plan->s_aux) {
+    if (cudaStreamCreateWithFlags(&plan->s_aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&plan->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&plan->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return set_cuda_error("cudaStreamCreate(labeller halves)");
+  }
+  if (cudaEventRecord(plan->ev_fork, ctx.stream) != cudaSuccess ||
+      cudaStreamWaitEvent(plan->s_aux, plan->ev_fork, 0) != cudaSuccess)
+    return set_cuda_error("labeller fork");
+  LaunchCtx aux = ctx;
+  aux.stream = plan->s_aux;
+  const CclParams p0 = make_ccl_params(B0, H, W, rig->fx * rig->baseline, t);
+  const CclParams p1 = make_ccl_params(B1, H, W, rig->fx * rig->baseline, t);
+  const int64_t off = B0 * H * W;
+  rc = run_ccl<T>(ctx, disp, nullptr, p0, row_base * W, labels, workspace, w0);
+  const int rc1 = run_ccl<T>(aux, disp + off, nullptr, p1, row_base * W, labels + off,
+                             static_cast<uint8_t*>(workspace) + w0, ws_bytes - w0);
+  // the join is recorded whatever happened, so the caller's stream never
+  // runs ahead of work still queued on the second stream
+  if (cudaEventRecord(plan->ev_join, plan->s_aux) != cudaSuccess ||
+      cudaStreamWaitEvent(ctx.stream, plan->ev_join, 0) != cudaSuccess)
+    return set_cuda_error("labeller join");
+  return rc ? rc : rc1;
 }
 
 template <typename T>

@@ -814,6 +814,13 @@ CclParams make_ccl_params(int64_t B, int64_t H, int64_t W, double fxb, double t)
 static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W) {
+  const size_t one = ccl_workspace_bytes_one(B, H, W);
+  if (B < kCclSplitFrames) return one;
+  const size_t halves = ccl_workspace_bytes_one(B / 2, H, W) + ccl_workspace_bytes_one(B - B / 2, H, W);
+  return one > halves ? one : halves;
+}
+
+size_t ccl_workspace_bytes_one(int64_t B, int64_t H, int64_t W) {
   const int64_t WW = (W + 31) / 32;
   const int64_t n_tx = (W + kLTW - 1) / kLTW, n_ty = (H + kLTH - 1) / kLTH;
   const int64_t tiles = B * n_tx * n_ty;
@@ -1114,9 +1121,9 @@ int run_ccl(const LaunchCtx& ctx, const T* disp, const uint8_t* pas, const CclPa
   const int64_t n = p.B * p.H * p.W;
   if (n == 0) return SN_OK;
   if (p.H * p.W > 0x7fffffffLL) return set_error(SN_EINVAL, "frame too large for int32 labels");
-  if (!workspace || ws_bytes < ccl_workspace_bytes(p.B, p.H, p.W))
+  if (!workspace || ws_bytes < ccl_workspace_bytes_one(p.B, p.H, p.W))
     return set_error(SN_EINVAL, "labeller workspace too small (%zu < %zu bytes)", ws_bytes,
-                     ccl_workspace_bytes(p.B, p.H, p.W));
+                     ccl_workspace_bytes_one(p.B, p.H, p.W));
   constexpr int64_t kMaxFrames = 65535;  // grid.z
   if (p.B > kMaxFrames) {
     // frames are independent: consecutive launches of <= 65535 frames, each

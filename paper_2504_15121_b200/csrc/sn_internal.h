@@ -60,7 +60,12 @@ struct CclParams {
 };
 
 CclParams make_ccl_params(int64_t B, int64_t H, int64_t W, double fxb, double t);
+// labeller workspace of B frames; from kCclSplitFrames frames on it also holds
+// two half-batch workspaces (labels from disparities run the halves on two
+// streams, sn_api.cu ccl_labels_ws_impl)
+constexpr int64_t kCclSplitFrames = 128;
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W);
+size_t ccl_workspace_bytes_one(int64_t B, int64_t H, int64_t W);  // one batch, no split
 
 // T = float or double disparities (explicit instantiations in sn_ccl.cu)
 template <typename T>

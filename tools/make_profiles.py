@@ -119,12 +119,15 @@ def main():
         }
     ccl = full_summary(tag, "ccl", "ccl_|passable_bits")
     if ccl:
-        summ["ccl"] = {}
+        # from 128 frames on the labels run as two half batches (sn_ccl_labels_ws):
+        # each predicate / labeller launch covers half the frames
+        lf = frames // 2 if frames >= 128 else frames
+        summ["ccl"] = {"frames_per_launch": lf}
         for d in ccl:
             name = d.get("Kernel Name", ("?", ""))[0][:60]
-            summ["ccl"][name] = {"us_per_frame_under_ncu": num(d, "gpu__time_duration.sum") * 1e6 / frames,
+            summ["ccl"][name] = {"us_per_frame_under_ncu": num(d, "gpu__time_duration.sum") * 1e6 / lf,
                                  "dram_bytes_per_px": (num(d, "dram__bytes_read.sum") +
-                                                       num(d, "dram__bytes_write.sum")) / (frames * 2048 * 1024)}
+                                                       num(d, "dram__bytes_write.sum")) / (lf * 2048 * 1024)}
     if launches:
         summ["launch_list_mean_us"] = launches
     (PROF / "ncu_summary.json").write_text(json.dumps(summ, indent=1) + "\n")
