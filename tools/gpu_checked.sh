@@ -4,7 +4,7 @@
 # union-find link monotonicity, trap on failure) -- the memory-safety evidence
 # in place of compute-sanitizer, which the pool does not run.
 mkdir -p gpurun_out
-[ -f paper_2504_15121_b200/libsn_b200_check.so ] || make -C paper_2504_15121_b200/csrc check -j8 > /dev/null
+make -C paper_2504_15121_b200/csrc check -j8 > /dev/null  # incremental: rebuilt when a source changed
 export SN_B200_LIB=$PWD/paper_2504_15121_b200/libsn_b200_check.so
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/checked_pytest.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/checked_pytest.log
