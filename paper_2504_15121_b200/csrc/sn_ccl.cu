@@ -1190,7 +1190,7 @@ int run_ccl(const LaunchCtx& ctx, const T* disp, const uint8_t* pas, const CclPa
       (int64_t)(ws.n_ty - 1) * ((p.W + kSeamThreads - 1) / kSeamThreads) +
       (int64_t)(ws.n_tx - 1) * ((p.H + kSeamThreads - 1) / kSeamThreads);
   if (seam_blocks > 0) {
-    const int F = p.B >= 256 ? 4 : p.B >= 128 ? 2 : 1;
+    const int F = p.B >= 128 ? 4 : 1;
     const int64_t gy = (p.B + F - 1) / F;
     dim3 sg((unsigned)seam_blocks, (unsigned)(gy < 65535 ? gy : 65535));
     if (F == 4)
