@@ -530,8 +530,8 @@ __global__ void __launch_bounds__(kLThreads, 8)
 // One CTA per (seam line, 256-position chunk) and F frames: the line decode
 // is block-uniform 32-bit arithmetic (a 64-bit division per position cost
 // more than the unions).  F = 4 frames per thread (their seam loads issued
-// together) from 256-frame launches, fewer below: 64 x F frames keep the grid
-// large enough to hide the unions' latency (measured, DESIGN 4.3)
+// together) from 128-frame launches, 1 below: smaller batches need the wider
+// grid to hide the unions' latency (measured, DESIGN 4.3)
 constexpr int kSeamThreads = 256;
 
 template <int kSeamFrames>
@@ -1195,8 +1195,6 @@ int run_ccl(const LaunchCtx& ctx, const T* disp, const uint8_t* pas, const CclPa
     dim3 sg((unsigned)seam_blocks, (unsigned)(gy < 65535 ? gy : 65535));
     if (F == 4)
       ccl_seam_kernel<4><<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
-    else if (F == 2)
-      ccl_seam_kernel<2><<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
     else
       ccl_seam_kernel<1><<<sg, kSeamThreads, 0, ctx.stream>>>(p, ws, labels);
     if ((rc = check_launch("ccl_seam_kernel"))) return rc;

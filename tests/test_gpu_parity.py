@@ -223,8 +223,8 @@ def test_labeller_random_grids(cuda_dev, shape, density):
 
 @pytest.mark.parametrize("B", [127, 128, 255, 256, 261])
 def test_labeller_batch_sizes(cuda_dev, B):
-    """Every seam-kernel variant (1 / 2 / 4 frames per thread, chosen by the
-    batch size, ragged last group included): the batch's labels equal the
+    """Both seam-kernel variants (1 / 4 frames per thread, chosen by the batch
+    size, ragged last group included) and the two-stream half batches: the batch's labels equal the
     frames' own labels computed one by one, and a sample of frames equals the
     oracle."""
     from oracle.stereonorm_oracle import label_components
