@@ -224,7 +224,7 @@ def test_labeller_random_grids(cuda_dev, shape, density):
 @pytest.mark.parametrize("B", [127, 128, 255, 256, 261])
 def test_labeller_batch_sizes(cuda_dev, B):
     """Both seam-kernel variants (1 / 4 frames per thread, chosen by the batch
-    size, ragged last group included) and the two-stream half batches: the batch's labels equal the
+    size, ragged last group included): the batch's labels equal the
     frames' own labels computed one by one, and a sample of frames equals the
     oracle."""
     from oracle.stereonorm_oracle import label_components
@@ -239,6 +239,27 @@ def test_labeller_batch_sizes(cuda_dev, B):
         assert np.array_equal(lab[i].astype(np.int64), label_components(p[i])), i
     for i in range(0, B, 17):
         assert np.array_equal(lab[i].astype(np.int64), label_components(p[i])), i
+
+
+@pytest.mark.parametrize("B", [128, 131])
+def test_labels_half_batches_on_two_streams(cuda_dev, B):
+    """Labels from disparities at >= 128 frames run as two half batches on two
+    streams (sn_ccl_labels_ws): every frame equals the frame labelled alone,
+    and sampled frames equal the oracle."""
+    from oracle import stereonorm_oracle as orc
+    from paper_2504_15121_b200 import device, scenes
+    sc = scenes.street_scene(512, 256)
+    base = scenes.raycast(sc)[0]
+    d = np.stack([scenes.add_gaussian_noise(base, 0.3, 500 + i) for i in range(B)]).astype(np.float32)
+    dt = torch.from_numpy(d).to(cuda_dev)
+    lab = device.component_labels(dt, sc.rig, 0.2).cpu().numpy()
+    o = orc.Rig(sc.rig.fx, sc.rig.fy, sc.rig.u0, sc.rig.v0, sc.rig.baseline)
+    for i in (0, B // 2 - 1, B // 2, B - 1):
+        one = device.component_labels(dt[i:i + 1], sc.rig, 0.2)[0].cpu().numpy()
+        assert np.array_equal(lab[i], one), i
+    for i in (0, B // 2, B - 1):
+        ref = orc.ccl_labels(d[i].astype(np.float64), o, 0.2)
+        assert np.array_equal(lab[i].astype(np.int64), ref), i
 
 
 @pytest.mark.parametrize("pick", ["exact_tie", "exact_only_rig", "tiny_and_huge"])
