@@ -59,6 +59,35 @@ def test_scratch_entry_points_on_concurrent_streams(cuda_dev):
         assert torch.equal(torch.nan_to_num(pts, 7.0), torch.nan_to_num(want_p, 7.0))
 
 
+def test_half_batches_on_concurrent_streams(cuda_dev):
+    """From 128 frames on, sn_ccl_labels runs its second half on the plan's
+    second stream: two caller streams on one plan (their second halves queue
+    on that stream) must both get the one-stream answer."""
+    from paper_2504_15121_b200 import _native, device
+    d, rig = _frames(4, w=256, h=128)
+    d = np.concatenate([d] * 33)[:130]  # 130 frames -> halves of 65
+    dt = torch.from_numpy(np.ascontiguousarray(d)).to(cuda_dev)
+    want = torch.stack([device.component_labels(dt[i:i + 1], rig, 0.2)[0] for i in range(4)])
+    lib = _native.load()
+    plan = _native.plan(cuda_dev.index)
+    rs = _native.rig_struct(rig)
+    streams = [torch.cuda.Stream(cuda_dev) for _ in range(2)]
+    outs = []
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for s in streams:
+            lab = torch.empty(dt.shape, dtype=torch.int32, device=cuda_dev)
+            with torch.cuda.stream(s):
+                B, H, W = dt.shape
+                _native.check(lib.sn_ccl_labels(plan, dt.data_ptr(), B, H, W, ctypes.byref(rs), 0.2,
+                                                0, lab.data_ptr(), ctypes.c_void_p(s.cuda_stream)))
+            outs.append(lab)
+    torch.cuda.synchronize()
+    for lab in outs:
+        for i in range(dt.shape[0]):
+            assert torch.equal(lab[i], want[i % 4]), i
+
+
 def test_labeller_repeat_determinism(cuda_dev):
     """The union-find's atomics race by design; its answer may not depend on
     scheduling.  50 runs of C4-style frames, each against the first."""
