@@ -527,12 +527,12 @@ __global__ void __launch_bounds__(kLThreads, 8)
 // A straight neighbour makes the diagonal links redundant (the diagonal
 // pixels are 8-adjacent to it along the seam row/column).
 
-// One CTA per (seam line, 256-position chunk) and F frames: the line decode
+// One CTA per (seam line, 128-position chunk) and F frames: the line decode
 // is block-uniform 32-bit arithmetic (a 64-bit division per position cost
 // more than the unions).  F = 4 frames per thread (their seam loads issued
 // together) from 128-frame launches, 1 below: smaller batches need the wider
 // grid to hide the unions' latency (measured, DESIGN 4.3)
-constexpr int kSeamThreads = 256;
+constexpr int kSeamThreads = 128;
 
 template <int kSeamFrames>
 __global__ void __launch_bounds__(kSeamThreads)
