@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--frames", type=int, default=FRAMES, help="frames per GPU")
     ap.add_argument("--pipeline", choices=["full", "points"], default="full")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=7)
     ap.add_argument("--e2e-frames", type=int, default=64,
                     help="frames per rank in the e2e leg (pinned host buffers ~70 MB/frame)")
     ap.add_argument("--cpu-frames", type=int, default=16, help="cpu_baseline sample (frames)")
@@ -751,11 +751,14 @@ def main():
         host_step()
         if world > 1:
             dist.barrier()
-        t0 = time.perf_counter()
+        # each step timed on the host clock around the blocking call; the
+        # median step (the shared host's PCIe rate drifts from run to run)
+        step_s = []
         for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
             host_step()
-        e2e_s = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64,
-                             device=dev)
+            step_s.append(time.perf_counter() - t0)
+        e2e_s = torch.tensor([statistics.median(step_s)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         sec = float(e2e_s.item())
@@ -778,6 +781,8 @@ def main():
                "h2d_bytes_per_step": h2d_b,
                "d2h_bytes_per_step": d2h_b,
                "ms_per_step": sec * 1e3,
+               "ms_per_step_each": [round(x * 1e3, 2) for x in step_s],
+               "statistic": f"median of {args.e2e_steps} steps",
                "pcie_gbs": pcie,
                "bound_ms_per_step": bound_s * 1e3,
                "frac": bound_s / sec,
